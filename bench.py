@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of MapSQ's join path on B200 (contract: one JSON line on rank 0).
+
+A "step" is one pass of the whole hot path over the resident synthetic input: for LUBM configs
+one ``mapsq_query`` (fused pattern scan -> chained Map/Sort/ReduceDuplicate joins ->
+projection); for C4 one ``mapsq_join`` of the two Zipf tables.  The metric is BASELINE.json's:
+join input+output tuples per second (sum over the query's joins of n1 + n2 + |RS|), plus the
+modelled HBM GB/s.  ``--impl reference`` times the CPU oracle on a bounded sample instead.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl mapsq|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (kind, universities, query, description)
+    "C1": ("lubm", 1, "C1", "LUBM(1) chain join ?x worksFor ?d . ?d subOrganizationOf ?u"),
+    "C2": ("lubm", 100, "C2", "LUBM(100) Q2-core triangle (memberOf, subOrganizationOf, undergraduateDegreeFrom)"),
+    "C3": ("lubm", 1000, "C3", "LUBM(1000) 4-pattern star on department ?x"),
+    "C4": ("zipf", 500_000_000, None, "2 x 5e8-row (key, value) tables, Zipf(1.1) keys over 2^29"),
+    "C5": ("lubm", 10000, "C5", "LUBM(10000) Q9-core triangle (advisor, teacherOf, takesCourse)"),
+}
+METRIC = "join input+output tuples/s and HBM GB/s (% peak) at 1/2/4/8 B200"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md, no MEASURED_PEAKS.json)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"mapsq_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workloads
+def lubm_host(nuniv: int, u_lo: int, u_hi: int, pinned: bool):
+    import torch
+
+    import datagen
+    st = datagen.lubm_count(nuniv, u_lo, u_hi)
+    n = st["n_triples"]
+    if pinned:
+        bufs = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(3)]
+        arrs = [b.numpy().view(np.uint32) for b in bufs]
+    else:
+        bufs, arrs = None, [np.empty(n, np.uint32) for _ in range(3)]
+    s, p, o, st = datagen.lubm(nuniv, u_lo, u_hi, out=arrs)
+    return (s, p, o), st, bufs
+
+
+def query_patterns(name):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from fixtures import config_query
+    return config_query(name)
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample(cfg: str, budget_s: float = 20.0):
+    """Time the CPU oracle (as it stands, 1 thread) on a bounded sample of the workload.
+    Returns (tuples/s, sample description, join tuples, seconds)."""
+    import datagen
+    import oracle
+    kind, nu, qname, _ = CONFIGS[cfg]
+    if kind == "zipf":
+        n = 4_000_000
+        k1, v1 = datagen.zipf(n, 0)
+        k2, v2 = datagen.zipf(n, 1)
+        A, B = oracle.Table([0, 1], np.stack([k1, v1], 1)), oracle.Table([0, 2], np.stack([k2, v2], 1))
+        t0 = time.perf_counter()
+        r = oracle.join(A, B)
+        dt = time.perf_counter() - t0
+        tuples = 2 * n + r.nrows
+        return tuples / dt, f"rows [0,{n}) of both C4 sides (Zipf(1.1), same generator/seed)", tuples, dt
+    pats = query_patterns(qname)
+    # universities [0, k) of the same dataset: identical triples to the full workload's prefix
+    k = {"C1": 1, "C2": 100, "C3": 150, "C5": 300}[cfg]
+    k = min(k, nu)
+    (s, p, o), st, _ = lubm_host(nu, 0, k, pinned=False)
+    t0 = time.perf_counter()
+    acc = oracle.scan(s, p, o, pats[0])
+    tuples = 0
+    for pat in pats[1:]:
+        t = oracle.scan(s, p, o, pat)
+        r = oracle.join(acc, t)
+        tuples += acc.nrows + t.nrows + r.nrows
+        acc = r
+    dt = time.perf_counter() - t0
+    return tuples / dt, f"universities [0,{k}) of LUBM({nu}) ({len(s)} triples), full query", tuples, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = args.config
+    vals = []
+    tuples = 0
+    for _ in range(args.warmup):
+        oracle_sample(cfg)
+    for _ in range(args.steps):
+        v, sample, tuples, dt = oracle_sample(cfg)
+        vals.append(v)
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tuples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tuples / value * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": cfg, "description": CONFIGS[cfg][3], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import paper_1702_03484_b200 as mq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        return run_gpu_dist(args, world, rank, local)
+    torch.cuda.set_device(local)
+    cfg = args.config
+    kind, nu, qname, desc = CONFIGS[cfg]
+    if args.univ:
+        nu = args.univ
+    ctx = mq.Context(local)
+    stream = torch.cuda.current_stream()
+    t_gen = time.perf_counter()
+    if kind == "zipf":
+        import datagen
+        n = args.rows or nu
+        k1, v1 = datagen.zipf(n, 0)
+        k2, v2 = datagen.zipf(n, 1)
+        cols = [torch.from_numpy(a.view(np.int32)).cuda() for a in (k1, v1, k2, v2)]
+        del k1, v1, k2, v2
+        A = mq.DeviceTable.from_torch([0, 1], cols[:2])
+        B = mq.DeviceTable.from_torch([0, 2], cols[2:])
+        ctx.table_bounds(A)
+        ctx.table_bounds(B)
+        in_bytes = 16 * n
+        host = None
+
+        def step():
+            r = ctx.join(A, B)
+            m = r.nrows
+            r.release()
+            return m
+        workload = f"C4 Zipf(1.1) 2x{n} rows"
+    else:
+        (s, p, o), st, pinned = lubm_host(nu, 0, nu, pinned=not args.no_e2e)
+        trip = tuple(torch.from_numpy(a.view(np.int32)).cuda() for a in (s, p, o))
+        pats = query_patterns(qname)
+        in_bytes = 12 * len(s)
+        host = (s, p, o, pats)
+
+        def step():
+            r = ctx.query(trip, pats)
+            m = r.nrows
+            r.release()
+            return m
+        workload = f"{cfg} LUBM({nu}) {len(s)} triples"
+    torch.cuda.synchronize()
+    log(f"[bench] {workload}: generated + resident in {time.perf_counter() - t_gen:.1f}s")
+
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = None
+    if in_bytes < 4 * l2:
+        flush = torch.empty(4 * l2 // 4, dtype=torch.int32, device="cuda")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.stats_reset()
+    ctx.set_profiling(True)
+    evs = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            m_final = step()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    st_k = ctx.stats()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = sum(step_ms) / 1e3
+    tuples = st_k["join_in_rows"] + st_k["join_out_rows"]
+    value = tuples / total_s
+    algo_bytes = sum(k["bytes"] for k in st_k["kernels"].values())
+    peak, peak_src = measured_peaks()
+    hbm_gbs = algo_bytes / total_s / 1e9
+    # dominant kernel by time
+    name, kd = max(st_k["kernels"].items(), key=lambda kv: kv[1]["ms"])
+    avg_ms = kd["ms"] / kd["launches"]
+    achieved = (kd["bytes"] / kd["launches"]) / (avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(name)
+    clocks = clk.summary()
+
+    line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sum(step_ms) / len(step_ms), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": cfg, "description": desc, "detail": workload,
+                       "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps",
+                       "join_tuples_per_step": tuples // args.steps,
+                       "result_rows": m_final},
+            "hbm": {"algo_bytes_per_step": algo_bytes // args.steps, "gbs": hbm_gbs,
+                    "frac_of_peak": hbm_gbs / peak, "peak_gbs": peak},
+            "roofline": {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "share_of_step": kd["ms"] / sum(step_ms)},
+            "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
+                            "share": v["ms"] / sum(step_ms)} for k, v in st_k["kernels"].items()},
+            "clocks": clocks, "gpu_launches": st_k["launches"]}
+
+    # e2e through the public API from pinned host buffers (H2D + query + D2H inside the region)
+    if host is not None and not args.no_e2e:
+        s, p, o, pats = host
+        e2e_ms = []
+        out_bytes = 0
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            vars_, rows = ctx.query_host(s, p, o, pats)
+            dt = time.perf_counter() - t0
+            out_bytes = rows.nbytes
+            if i:
+                e2e_ms.append(dt * 1e3)
+        e2e_s = statistics.median(e2e_ms) / 1e3
+        line["e2e"] = {"value": (tuples / args.steps) / e2e_s, "unit": "tuples/s",
+                       "h2d_bytes_per_step": 12 * len(s), "d2h_bytes_per_step": out_bytes,
+                       "ms_per_step": e2e_s * 1e3}
+    elif kind == "zipf":
+        line["e2e"] = None
+    if not args.no_cpu_baseline:
+        v, sample, _, dt = oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": v, "unit": "tuples/s", "cores": 1, "kind": "oracle",
+                                "sample": sample, "seconds": dt}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu_dist(args, world, rank, local):
+    raise SystemExit("multi-GPU bench path not available yet")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="mapsq", choices=["mapsq", "reference"])
+    ap.add_argument("--univ", type=int, default=0, help="override the LUBM scale (testing)")
+    ap.add_argument("--rows", type=int, default=0, help="override C4 rows per side (testing)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,239 @@
+/* mapsq.h — C ABI of libmapsq.so, the B200 (sm_100a) implementation of MapSQ's join path.
+ *
+ * Paper: "MapSQ: A MapReduce-based Framework for SPARQL Queries on GPU", arXiv 1702.03484
+ * (PAPER.md).  The library answers a SPARQL basic graph pattern in the paper's two steps,
+ * "partial matching and MapReduce-based join":
+ *   1. mapsq_scan_pattern / mapsq_scan_patterns — partial matches of each triple pattern
+ *      (gStore's black box replaced by a GPU scan over the triple table);
+ *   2. mapsq_join — Algorithm 1: Map (label rows LEFT/RIGHT, :122-125),
+ *      Sort (:126), ReduceDuplicate (emit every LEFT x RIGHT pair of each key, :127-133);
+ *   3. mapsq_query — the left-deep chain of joins over the patterns (:137-138, :165) and the
+ *      SELECT projection (:52).
+ *
+ * Conventions (all functions):
+ *   - Every device buffer is a plain CUDA device pointer; every call is enqueued on `stream`
+ *     (a cudaStream_t passed as void*, NULL = legacy default stream) and returns when the work
+ *     is enqueued, except for the documented blocking reads of output sizes.
+ *   - Inputs are borrowed and never modified.  Output tables are allocated by the library
+ *     (through the context's allocator) and owned by the caller, who frees them with
+ *     mapsq_table_release.  Scratch memory is freed, in stream order, before the call returns.
+ *   - Each function returns a mapsq_status; no C++ exception crosses the ABI.  On error every
+ *     output table is {nrows = 0, col[] = NULL, owner = NULL} with nothing allocated, and
+ *     mapsq_last_error(ctx) describes the failure.  A CUDA error is sticky for the context.
+ *   - Term IDs are uint32 (dictionary-encoded RDF terms); row counts and offsets are uint64.
+ *   - Semantics are SPARQL solution mappings with bag semantics (readings R1-R16):
+ *     a join on ALL shared variables, no deduplication, output schema
+ *     shared (ascending variable id) ++ tp1 non-shared ++ tp2 non-shared.
+ */
+#ifndef MAPSQ_H
+#define MAPSQ_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MAPSQ_OK = 0,
+  MAPSQ_E_INVALID = 1,     /* NULL pointer, ncols == 0 or > MAPSQ_MAX_COLS, duplicate variable in a
+                              schema, pattern without variables, n1 + n2 >= 2^32, bad argument */
+  MAPSQ_E_NO_SHARED = 2,   /* join inputs share no variable; query pattern not connected to the
+                              patterns before it */
+  MAPSQ_E_NOMEM = 3,       /* the allocator returned NULL; nothing is partially written */
+  MAPSQ_E_CUDA = 4,        /* CUDA error (text in mapsq_last_error); sticky for the context */
+  MAPSQ_E_UNSUPPORTED = 5  /* packed key wider than 64 bits after range compression */
+} mapsq_status;
+
+#define MAPSQ_MAX_COLS 16
+#define MAPSQ_MAX_PATTERNS 16
+#define MAPSQ_TABLE_BOUNDS 1u /* flags bit: lo[]/hi[] hold valid inclusive column bounds */
+
+/* A partial-match table, "Tp1 and Tp2 are the partial matches of each triple pattern"
+ * (Alg. 1 Require).  Structure of arrays: col[c][r] is the ID bound to
+ * variable var[c] in row r.  lo/hi are optional inclusive bounds of each column (valid iff
+ * flags & MAPSQ_TABLE_BOUNDS); the library fills them on every table it produces and uses
+ * them to range-compress join keys.  `owner` is the allocation behind col[] for tables the
+ * library produced (NULL for caller-built tables, which the library never frees). */
+typedef struct {
+  uint64_t nrows;
+  uint32_t ncols;
+  uint32_t flags;
+  int32_t var[MAPSQ_MAX_COLS];
+  uint32_t lo[MAPSQ_MAX_COLS];
+  uint32_t hi[MAPSQ_MAX_COLS];
+  uint32_t *col[MAPSQ_MAX_COLS];
+  void *owner;
+} mapsq_table;
+
+/* Dictionary-encoded triple table, structure of arrays of n (s, p, o) IDs (a set: no
+ * duplicate triples; duplicates would be matched as many times as they occur). */
+typedef struct {
+  uint64_t n;
+  const uint32_t *s, *p, *o;
+} mapsq_triples;
+
+/* Triple pattern P(s, p, o): var[j] >= 0 is a variable id at position j (0 = subject,
+ * 1 = predicate, 2 = object); var[j] == -1 is the constant id[j].  A repeated variable
+ * requires equal IDs; a constant absent from the data matches nothing (empty result, not an
+ * error).  The partial-match schema is the pattern's distinct variables in (s, p, o) order. */
+typedef struct {
+  int32_t var[3];
+  uint32_t id[3];
+} mapsq_pattern;
+
+/* Device-memory allocator (stream ordered).  NULL in mapsq_create selects cudaMallocAsync on
+ * the device's default memory pool with an unbounded release threshold. */
+typedef struct {
+  void *(*alloc)(void *ctx, size_t bytes, void *stream);
+  void (*free)(void *ctx, void *ptr, void *stream);
+  void *ctx;
+} mapsq_allocator;
+
+typedef struct mapsq_ctx mapsq_ctx;
+
+/* Host-side join spec.  Derived from the two schemas and column bounds:
+ *   shared = vars(tp1) ∩ vars(tp2) ascending by id ("the key of them is their shared
+ *   variable"; generalised to >= 1 shared variables, reading R5);
+ *   key' = concatenation of (value - lo) of each shared column, first shared variable most
+ *   significant, each in key_bits[c] = bits(hi - lo) bits; kb = sum of key_bits;
+ *   ib = bits(n1 + n2 - 1) index bits; path P64 when kb + ib <= 64 (one packed word
+ *   key' << ib | rowid per row, rowid >= n1 meaning RIGHT), else KV (u64 key' + u32 rowid). */
+typedef struct {
+  uint64_t n1, n2;
+  uint32_t nshared;
+  int32_t shared[MAPSQ_MAX_COLS];
+  int32_t key_col1[MAPSQ_MAX_COLS], key_col2[MAPSQ_MAX_COLS]; /* column of shared[c] in tp1/tp2 */
+  uint32_t key_lo[MAPSQ_MAX_COLS], key_hi[MAPSQ_MAX_COLS];    /* intersected bounds per shared var */
+  uint32_t key_bits[MAPSQ_MAX_COLS], key_shift[MAPSQ_MAX_COLS];
+  uint32_t nrest1, nrest2;
+  int32_t rest_col1[MAPSQ_MAX_COLS], rest_col2[MAPSQ_MAX_COLS];
+  uint32_t out_ncols;
+  int32_t out_var[MAPSQ_MAX_COLS];
+  uint32_t kb, ib;
+  uint32_t path;    /* MAPSQ_PATH_* */
+  uint32_t passes;  /* radix digit passes over the kb key bits */
+  uint32_t disjoint;/* 1 when the key bounds do not overlap: the join is empty */
+} mapsq_join_plan;
+#define MAPSQ_PATH_P64 0u
+#define MAPSQ_PATH_KV 1u
+#define MAPSQ_RADIX_BITS 8u
+
+/* Per-kernel timing (recorded with CUDA events on the launching stream while profiling is on)
+ * and counters accumulated since the last mapsq_stats_reset. */
+#define MAPSQ_MAX_KSTATS 32
+typedef struct {
+  char name[32];
+  uint64_t launches;
+  double total_ms;         /* sum of event-timed durations of those launches */
+  uint64_t algo_bytes;     /* algorithmic bytes of those launches (DESIGN.md §5 byte model) */
+} mapsq_kernel_stat;
+typedef struct {
+  uint64_t launches;       /* kernels launched by the library (profiling on or off) */
+  uint64_t join_in_rows;   /* sum over joins of n1 + n2 */
+  uint64_t join_out_rows;  /* sum over joins of |RS| */
+  uint64_t scanned_triples;
+  uint64_t joins, scans;
+  uint64_t last_kb, last_ib, last_passes, last_path;
+  uint32_t nkernels;
+  mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
+} mapsq_stats;
+
+/* ---- context ---- */
+mapsq_status mapsq_create(mapsq_ctx **out, int device, const mapsq_allocator *allocator);
+void mapsq_destroy(mapsq_ctx *ctx);
+const char *mapsq_last_error(const mapsq_ctx *ctx);
+const char *mapsq_version(void);
+/* Free an output table (stream ordered); a table with owner == NULL is only cleared. */
+void mapsq_table_release(mapsq_ctx *ctx, mapsq_table *t, void *stream);
+
+/* ---- partial matching (row a1) ----
+ * Scan the triple table once per call and produce the partial matches of each of the k
+ * patterns (k <= MAPSQ_MAX_PATTERNS): rows in triple order, schema as in mapsq_pattern.
+ * One pass evaluates every pattern's predicate (reading only the constant positions) and
+ * records a match bitmap; after ONE blocking read of the k row counts, a second pass gathers
+ * the bound positions of matching triples only.  out[i] receives pattern i's table with
+ * exact column bounds. */
+mapsq_status mapsq_scan_patterns(mapsq_ctx *ctx, const mapsq_triples *triples,
+                                 const mapsq_pattern *pats, int k, mapsq_table *out,
+                                 void *stream);
+mapsq_status mapsq_scan_pattern(mapsq_ctx *ctx, const mapsq_triples *triples,
+                                const mapsq_pattern *pat, mapsq_table *out, void *stream);
+
+/* ---- join (rows a2-a6): Algorithm 1, PAPER.md:116-135 ----
+ * rs = tp1 ⋈ tp2 on all shared variables (bag semantics).  Map packs each row's key and its
+ * LEFT (tp1) / RIGHT (tp2) label with the row id; an LSD radix sort orders the words by key
+ * (stable, so LEFT rows precede RIGHT rows and row ids ascend within a key); ReduceDuplicate
+ * finds each key's LEFT/RIGHT split, counts nL * nR, scans the counts and writes every pair.
+ * Output rows are ordered (key', tp1 row, tp2 row) and are deterministic on one GPU.
+ * Blocks once, to read |RS| for the output allocation.  Tables without bounds get them from a
+ * min/max pass (one more blocking read). */
+mapsq_status mapsq_join(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
+                        mapsq_table *rs, void *stream);
+/* Host-only: the join spec for two tables that carry bounds (no device work). */
+mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table *tp2,
+                             mapsq_join_plan *plan);
+
+/* ---- query (row a7) ----
+ * Scan all patterns in one fused pass (mapsq_scan_patterns), fold the joins left-deep in the
+ * given order (pattern i must share a variable with patterns 0..i-1, else MAPSQ_E_NO_SHARED),
+ * then project onto proj[0..nproj) (nproj == 0: all variables in first-appearance order).
+ * Projection is zero-copy column selection with bag semantics (no DISTINCT). */
+mapsq_status mapsq_query(mapsq_ctx *ctx, const mapsq_triples *triples,
+                         const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
+                         mapsq_table *rs, void *stream);
+/* End-to-end variant over HOST buffers: s/p/o are host pointers (pinned memory recommended);
+ * the triples are streamed to the device in chunks overlapped with the scan, the query runs
+ * as mapsq_query, and the result columns are copied to host memory the library allocates
+ * with malloc.  On return (synchronous) host_rows receives the row count and host_cols[c] a
+ * malloc'd array of that many IDs for variable out_var[c]; free each with mapsq_host_free. */
+mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host,
+                              const uint32_t *p_host, const uint32_t *o_host,
+                              const mapsq_pattern *pats, int npats, const int32_t *proj,
+                              int nproj, uint64_t *host_rows, uint32_t *out_ncols,
+                              int32_t *out_var, uint32_t **host_cols, void *stream);
+void mapsq_host_free(void *p);
+
+/* ---- phase entry points (for phase-level parity tests; the same kernels mapsq_join runs) ----
+ * Map (K2, row a3): words[r] = key'(tp1 row r) << ib | r and words[n1 + r] = key'(tp2 row r)
+ * << ib | (n1 + r) for a P64 plan.  `words` is a caller-owned device array of n1 + n2. */
+mapsq_status mapsq_map_words(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
+                             const mapsq_join_plan *plan, uint64_t *words, void *stream);
+/* Sort (K3, row a4): stable LSD radix sort of n words by bits [bit_lo, bit_hi), in place
+ * (device array; the library allocates the ping-pong buffer). */
+mapsq_status mapsq_sort_words(mapsq_ctx *ctx, uint64_t *words, uint64_t n, uint32_t bit_lo,
+                              uint32_t bit_hi, void *stream);
+/* Stable LSD radix sort of (key, value) pairs by key bits [bit_lo, bit_hi), in place. */
+mapsq_status mapsq_sort_pairs(mapsq_ctx *ctx, uint64_t *keys, uint32_t *vals, uint64_t n,
+                              uint32_t bit_lo, uint32_t bit_hi, void *stream);
+/* ReduceDuplicate part 1 (K4+K5, row a5) on sorted P64 words: for every key present on both
+ * sides, in key order, group_start/group_split/group_end (device arrays of capacity
+ * min(n1, n2)) receive the run [start, end) and its first RIGHT position, and group_off the
+ * exclusive prefix of nL * nR.  *ngroups and *total (host) receive the group count and |RS|
+ * (blocking). */
+mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words, uint64_t n1, uint64_t n2,
+                                 uint32_t ib, uint32_t *group_start, uint32_t *group_split,
+                                 uint32_t *group_end, uint64_t *group_off, uint64_t *ngroups,
+                                 uint64_t *total, void *stream);
+
+/* ---- multi-GPU exchange support (SURVEY §8 row e) ----
+ * Hash-partition `in` on the variables key_vars[0..nkey) into nparts destinations,
+ * dest = fmix32(h) mod nparts with h the FNV-1a-style fold of the key values.
+ * `out` receives a table with the same schema whose rows are grouped by destination (stable
+ * within a destination); counts_host[d] receives destination d's row count (blocking). */
+mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
+                             int nkey, int nparts, mapsq_table *out, uint64_t *counts_host,
+                             void *stream);
+/* Compute exact inclusive bounds lo[]/hi[] of every column of a (caller-built) table and set
+ * MAPSQ_TABLE_BOUNDS (one min/max pass, blocking).  An empty table gets lo = hi = 0. */
+mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
+
+/* ---- statistics ---- */
+mapsq_status mapsq_set_profiling(mapsq_ctx *ctx, int on);
+mapsq_status mapsq_stats_reset(mapsq_ctx *ctx);
+/* Blocks until the recorded events complete, then fills *st. */
+mapsq_status mapsq_get_stats(mapsq_ctx *ctx, mapsq_stats *st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPSQ_H */

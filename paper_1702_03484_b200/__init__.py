@@ -1,0 +1,424 @@
+"""paper_1702_03484_b200 — Python binding of libmapsq.so (MapSQ's join path on B200, sm_100a).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels behind the C ABI
+declared in include/mapsq.h (same function names, minus the ``mapsq_`` prefix).  PyTorch is
+used for device memory of the inputs, for streams and for ``torch.distributed``.  There is no
+CPU fallback: importing works without a GPU (for the host-only ``plan_join``), but every compute
+call raises if the CUDA extension or a GPU is missing.
+
+Tables are ``DeviceTable`` objects (SoA uint32 columns + one variable id per column).  Results
+own library-allocated device memory and expose their columns as zero-copy torch tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmapsq.so")
+
+MAX_COLS = 16
+MAX_PATTERNS = 16
+TABLE_BOUNDS = 1
+PATH_P64, PATH_KV = 0, 1
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
+          5: "E_UNSUPPORTED"}
+
+
+class MapsqError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"mapsq {STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class _Table(ctypes.Structure):
+    _fields_ = [("nrows", ctypes.c_uint64), ("ncols", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("var", ctypes.c_int32 * MAX_COLS), ("lo", ctypes.c_uint32 * MAX_COLS),
+                ("hi", ctypes.c_uint32 * MAX_COLS), ("col", ctypes.c_void_p * MAX_COLS),
+                ("owner", ctypes.c_void_p)]
+
+
+class _Triples(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("s", ctypes.c_void_p), ("p", ctypes.c_void_p),
+                ("o", ctypes.c_void_p)]
+
+
+class _Pattern(ctypes.Structure):
+    _fields_ = [("var", ctypes.c_int32 * 3), ("id", ctypes.c_uint32 * 3)]
+
+
+class JoinPlan(ctypes.Structure):
+    _fields_ = [("n1", ctypes.c_uint64), ("n2", ctypes.c_uint64), ("nshared", ctypes.c_uint32),
+                ("shared", ctypes.c_int32 * MAX_COLS), ("key_col1", ctypes.c_int32 * MAX_COLS),
+                ("key_col2", ctypes.c_int32 * MAX_COLS), ("key_lo", ctypes.c_uint32 * MAX_COLS),
+                ("key_hi", ctypes.c_uint32 * MAX_COLS), ("key_bits", ctypes.c_uint32 * MAX_COLS),
+                ("key_shift", ctypes.c_uint32 * MAX_COLS), ("nrest1", ctypes.c_uint32),
+                ("nrest2", ctypes.c_uint32), ("rest_col1", ctypes.c_int32 * MAX_COLS),
+                ("rest_col2", ctypes.c_int32 * MAX_COLS), ("out_ncols", ctypes.c_uint32),
+                ("out_var", ctypes.c_int32 * MAX_COLS), ("kb", ctypes.c_uint32),
+                ("ib", ctypes.c_uint32), ("path", ctypes.c_uint32), ("passes", ctypes.c_uint32),
+                ("disjoint", ctypes.c_uint32)]
+
+
+class _KStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
+                ("total_ms", ctypes.c_double), ("algo_bytes", ctypes.c_uint64)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_uint64), ("join_in_rows", ctypes.c_uint64),
+                ("join_out_rows", ctypes.c_uint64), ("scanned_triples", ctypes.c_uint64),
+                ("joins", ctypes.c_uint64), ("scans", ctypes.c_uint64),
+                ("last_kb", ctypes.c_uint64), ("last_ib", ctypes.c_uint64),
+                ("last_passes", ctypes.c_uint64), ("last_path", ctypes.c_uint64),
+                ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded libmapsq.so; raises loudly if the CUDA extension was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"CUDA extension {_LIB_PATH} is missing: run `python build.py` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, u64, u32, i32, st = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                 ctypes.c_int32, ctypes.c_int)
+        PT, PP = ctypes.POINTER(_Table), ctypes.POINTER(_Pattern)
+        sigs = {
+            "mapsq_create": (st, [ctypes.POINTER(vp), ctypes.c_int, vp]),
+            "mapsq_destroy": (None, [vp]),
+            "mapsq_last_error": (ctypes.c_char_p, [vp]),
+            "mapsq_version": (ctypes.c_char_p, []),
+            "mapsq_table_release": (None, [vp, PT, vp]),
+            "mapsq_scan_patterns": (st, [vp, ctypes.POINTER(_Triples), PP, ctypes.c_int, PT, vp]),
+            "mapsq_scan_pattern": (st, [vp, ctypes.POINTER(_Triples), PP, PT, vp]),
+            "mapsq_join": (st, [vp, PT, PT, PT, vp]),
+            "mapsq_plan_join": (st, [PT, PT, ctypes.POINTER(JoinPlan)]),
+            "mapsq_query": (st, [vp, ctypes.POINTER(_Triples), PP, ctypes.c_int,
+                                 ctypes.POINTER(i32), ctypes.c_int, PT, vp]),
+            "mapsq_query_host": (st, [vp, u64, vp, vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
+                                      ctypes.c_int, ctypes.POINTER(u64), ctypes.POINTER(u32),
+                                      ctypes.POINTER(i32), ctypes.POINTER(vp), vp]),
+            "mapsq_host_free": (None, [vp]),
+            "mapsq_map_words": (st, [vp, PT, PT, ctypes.POINTER(JoinPlan), vp, vp]),
+            "mapsq_sort_words": (st, [vp, vp, u64, u32, u32, vp]),
+            "mapsq_sort_pairs": (st, [vp, vp, vp, u64, u32, u32, vp]),
+            "mapsq_reduce_groups": (st, [vp, vp, u64, u64, u32, vp, vp, vp, vp,
+                                         ctypes.POINTER(u64), ctypes.POINTER(u64), vp]),
+            "mapsq_partition": (st, [vp, PT, ctypes.POINTER(i32), ctypes.c_int, ctypes.c_int, PT,
+                                     ctypes.POINTER(u64), vp]),
+            "mapsq_table_bounds": (st, [vp, PT, vp]),
+            "mapsq_set_profiling": (st, [vp, ctypes.c_int]),
+            "mapsq_stats_reset": (st, [vp]),
+            "mapsq_get_stats": (st, [vp, ctypes.POINTER(_Stats)]),
+        }
+        for name, (res, args) in sigs.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list:
+    """Names of the C ABI functions this binding expects (each must resolve in the .so)."""
+    L = lib()
+    return [n for n in dir(L) if n.startswith("mapsq_")]
+
+
+def version() -> str:
+    return lib().mapsq_version().decode()
+
+
+# ------------------------------------------------------------------------------ helpers
+def _stream(stream=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class _CAI:
+    """Zero-copy view of one library-owned device column (keeps the owner alive)."""
+
+    def __init__(self, ptr: int, n: int, owner):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self._owner = owner
+
+
+class _Owner:
+    """Holds a library-allocated table and releases it (stream ordered) when collected."""
+
+    def __init__(self, ctx: "Context", t: _Table):
+        self.ctx, self.t = ctx, t
+
+    def release(self):
+        if self.t is not None and self.t.owner:
+            lib().mapsq_table_release(self.ctx.handle, ctypes.byref(self.t), _stream())
+        self.t = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class DeviceTable:
+    """Partial-match table: ``vars[c]`` is the variable bound by column ``columns[c]``."""
+
+    def __init__(self, vars_, columns, nrows, c_table: _Table, owner=None):
+        self.vars = list(vars_)
+        self.columns = list(columns)
+        self.nrows = int(nrows)
+        self._c = c_table
+        self._owner = owner
+
+    @property
+    def ncols(self) -> int:
+        return len(self.vars)
+
+    @property
+    def bounds(self):
+        if not (self._c.flags & TABLE_BOUNDS):
+            return None
+        return [(int(self._c.lo[c]), int(self._c.hi[c])) for c in range(self.ncols)]
+
+    def column(self, var: int):
+        return self.columns[self.vars.index(var)]
+
+    def to_numpy(self):
+        """Row-major (nrows, ncols) uint32 host copy."""
+        import numpy as np
+        import torch
+        if self.nrows == 0:
+            return np.zeros((0, self.ncols), np.uint32)
+        cols = [c.view(torch.int32).cpu().numpy().view(np.uint32) for c in self.columns]
+        return np.ascontiguousarray(np.stack(cols, 1))
+
+    def release(self):
+        if self._owner is not None:
+            self._owner.release()
+        self.columns = []
+
+    @staticmethod
+    def from_torch(vars_, columns, bounds=None) -> "DeviceTable":
+        """Borrow caller-owned uint32 device columns (torch.uint32 or int32 tensors)."""
+        import torch
+        if len(vars_) != len(columns) or not 0 < len(vars_) <= MAX_COLS:
+            raise ValueError("one variable per column, 1..16 columns")
+        n = int(columns[0].numel())
+        t = _Table()
+        t.nrows, t.ncols = n, len(vars_)
+        for c, (v, col) in enumerate(zip(vars_, columns)):
+            if col.numel() != n or not col.is_cuda or col.element_size() != 4:
+                raise ValueError("columns must be equal-length 4-byte CUDA tensors")
+            if not col.is_contiguous():
+                raise ValueError("columns must be contiguous")
+            t.var[c] = int(v)
+            t.col[c] = col.data_ptr() if n else None
+        if bounds is not None:
+            t.flags = TABLE_BOUNDS
+            for c, (lo, hi) in enumerate(bounds):
+                t.lo[c], t.hi[c] = lo, hi
+        return DeviceTable(vars_, columns, n, t, owner=None)
+
+
+def _wrap(ctx: "Context", t: _Table) -> DeviceTable:
+    import torch
+    owner = _Owner(ctx, t)
+    n, w = int(t.nrows), int(t.ncols)
+    cols = []
+    for c in range(w):
+        if n == 0:
+            cols.append(torch.empty(0, dtype=torch.uint32, device="cuda"))
+        else:
+            cols.append(torch.as_tensor(_CAI(t.col[c], n, owner), device="cuda"))
+    return DeviceTable([int(t.var[c]) for c in range(w)], cols, n, t, owner)
+
+
+def pattern_struct(pattern) -> _Pattern:
+    """pattern = ((kind, x), (kind, x), (kind, x)): kind 'v' = variable id, 'c' = constant id."""
+    p = _Pattern()
+    for j, (kind, x) in enumerate(pattern):
+        if kind == "v":
+            p.var[j], p.id[j] = int(x), 0
+        elif kind == "c":
+            p.var[j], p.id[j] = -1, int(x)
+        else:
+            raise ValueError(f"pattern position kind must be 'v' or 'c', got {kind!r}")
+    return p
+
+
+def _triples(s, p, o) -> _Triples:
+    n = int(s.numel())
+    if p.numel() != n or o.numel() != n:
+        raise ValueError("s, p, o must have equal length")
+    for x in (s, p, o):
+        if not (x.is_cuda and x.element_size() == 4 and x.is_contiguous()):
+            raise ValueError("triples must be contiguous 4-byte CUDA tensors")
+    return _Triples(n, s.data_ptr(), p.data_ptr(), o.data_ptr())
+
+
+class Context:
+    """One libmapsq context on one device (default allocator: cudaMallocAsync pool)."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("mapsq needs a CUDA device (no CPU fallback)")
+        self.device = device
+        h = ctypes.c_void_p()
+        st = lib().mapsq_create(ctypes.byref(h), device, None)
+        if st:
+            raise MapsqError(st, "mapsq_create failed")
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().mapsq_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st:
+            raise MapsqError(st, lib().mapsq_last_error(self.handle).decode())
+
+    # ---- partial matching (row a1)
+    def scan_patterns(self, triples, patterns, stream=None) -> list:
+        T = _triples(*triples)
+        k = len(patterns)
+        pats = (_Pattern * k)(*[pattern_struct(p) for p in patterns])
+        outs = (_Table * k)()
+        self._check(lib().mapsq_scan_patterns(self.handle, ctypes.byref(T), pats, k, outs,
+                                              _stream(stream)))
+        return [_wrap(self, outs[j]) for j in range(k)]
+
+    def scan_pattern(self, triples, pattern, stream=None) -> DeviceTable:
+        T = _triples(*triples)
+        p = pattern_struct(pattern)
+        out = _Table()
+        self._check(lib().mapsq_scan_pattern(self.handle, ctypes.byref(T), ctypes.byref(p),
+                                             ctypes.byref(out), _stream(stream)))
+        return _wrap(self, out)
+
+    # ---- join (rows a2-a6)
+    def join(self, tp1: DeviceTable, tp2: DeviceTable, stream=None) -> DeviceTable:
+        out = _Table()
+        self._check(lib().mapsq_join(self.handle, ctypes.byref(tp1._c), ctypes.byref(tp2._c),
+                                     ctypes.byref(out), _stream(stream)))
+        return _wrap(self, out)
+
+    # ---- query (row a7)
+    def query(self, triples, patterns, proj=None, stream=None) -> DeviceTable:
+        T = _triples(*triples)
+        k = len(patterns)
+        pats = (_Pattern * k)(*[pattern_struct(p) for p in patterns])
+        proj = list(proj or [])
+        pr = (ctypes.c_int32 * max(1, len(proj)))(*proj)
+        out = _Table()
+        self._check(lib().mapsq_query(self.handle, ctypes.byref(T), pats, k, pr, len(proj),
+                                      ctypes.byref(out), _stream(stream)))
+        return _wrap(self, out)
+
+    def query_host(self, s, p, o, patterns, proj=None, stream=None):
+        """End to end over host (numpy, ideally pinned) triples; returns (vars, rows ndarray)."""
+        import numpy as np
+        k = len(patterns)
+        pats = (_Pattern * k)(*[pattern_struct(q) for q in patterns])
+        proj = list(proj or [])
+        pr = (ctypes.c_int32 * max(1, len(proj)))(*proj)
+        nrows, ncols = ctypes.c_uint64(), ctypes.c_uint32()
+        ovar = (ctypes.c_int32 * MAX_COLS)()
+        ocol = (ctypes.c_void_p * MAX_COLS)()
+        ptr = lambda a: a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr()  # noqa: E731
+        n = len(s)
+        self._check(lib().mapsq_query_host(self.handle, n, ptr(s), ptr(p), ptr(o), pats, k, pr,
+                                           len(proj), ctypes.byref(nrows), ctypes.byref(ncols),
+                                           ovar, ocol, _stream(stream)))
+        m, w = int(nrows.value), int(ncols.value)
+        rows = np.empty((m, w), np.uint32)
+        for c in range(w):
+            if m:
+                buf = (ctypes.c_uint32 * m).from_address(ocol[c])
+                rows[:, c] = np.frombuffer(buf, np.uint32, m)
+            lib().mapsq_host_free(ocol[c])
+        return [int(ovar[c]) for c in range(w)], rows
+
+    # ---- phase entry points (rows a3-a5)
+    def map_words(self, tp1, tp2, plan: JoinPlan, words, stream=None):
+        self._check(lib().mapsq_map_words(self.handle, ctypes.byref(tp1._c), ctypes.byref(tp2._c),
+                                          ctypes.byref(plan), words.data_ptr(), _stream(stream)))
+
+    def sort_words(self, words, bit_lo: int, bit_hi: int, stream=None):
+        self._check(lib().mapsq_sort_words(self.handle, words.data_ptr(), words.numel(), bit_lo,
+                                           bit_hi, _stream(stream)))
+
+    def sort_pairs(self, keys, vals, bit_lo: int, bit_hi: int, stream=None):
+        self._check(lib().mapsq_sort_pairs(self.handle, keys.data_ptr(), vals.data_ptr(),
+                                           keys.numel(), bit_lo, bit_hi, _stream(stream)))
+
+    def reduce_groups(self, words, n1: int, n2: int, ib: int, stream=None):
+        import torch
+        cap = max(1, min(n1, n2))
+        dev = words.device
+        gs, gp, ge = (torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(3))
+        go = torch.empty(cap, dtype=torch.int64, device=dev)
+        ng, tot = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(lib().mapsq_reduce_groups(self.handle, words.data_ptr(), n1, n2, ib,
+                                              gs.data_ptr(), gp.data_ptr(), ge.data_ptr(),
+                                              go.data_ptr(), ctypes.byref(ng), ctypes.byref(tot),
+                                              _stream(stream)))
+        g = int(ng.value)
+        return gs[:g], gp[:g], ge[:g], go[:g], int(tot.value)
+
+    def partition(self, table: DeviceTable, key_vars, nparts: int, stream=None):
+        kv = (ctypes.c_int32 * len(key_vars))(*key_vars)
+        counts = (ctypes.c_uint64 * nparts)()
+        out = _Table()
+        self._check(lib().mapsq_partition(self.handle, ctypes.byref(table._c), kv, len(key_vars),
+                                          nparts, ctypes.byref(out), counts, _stream(stream)))
+        return _wrap(self, out), [int(c) for c in counts]
+
+    def table_bounds(self, table: DeviceTable, stream=None):
+        self._check(lib().mapsq_table_bounds(self.handle, ctypes.byref(table._c), _stream(stream)))
+        return table.bounds
+
+    # ---- statistics
+    def set_profiling(self, on: bool):
+        self._check(lib().mapsq_set_profiling(self.handle, int(bool(on))))
+
+    def stats_reset(self):
+        self._check(lib().mapsq_stats_reset(self.handle))
+
+    def stats(self) -> dict:
+        st = _Stats()
+        self._check(lib().mapsq_get_stats(self.handle, ctypes.byref(st)))
+        d = {f: int(getattr(st, f)) for f, _ in _Stats._fields_ if f not in ("kernel", "nkernels")}
+        d["kernels"] = {st.kernel[i].name.decode(): dict(launches=int(st.kernel[i].launches),
+                                                         ms=float(st.kernel[i].total_ms),
+                                                         bytes=int(st.kernel[i].algo_bytes))
+                        for i in range(st.nkernels)}
+        return d
+
+
+def plan_join(vars1, bounds1, n1, vars2, bounds2, n2) -> JoinPlan:
+    """Host-only join spec (row a2) from two schemas with column bounds; no GPU needed."""
+    t1, t2 = _Table(), _Table()
+    for t, vs, bs, n in ((t1, vars1, bounds1, n1), (t2, vars2, bounds2, n2)):
+        t.nrows, t.ncols, t.flags = n, len(vs), TABLE_BOUNDS
+        for c, (v, (lo, hi)) in enumerate(zip(vs, bs)):
+            t.var[c], t.lo[c], t.hi[c] = v, lo, hi
+            t.col[c] = 16  # never dereferenced by the host-only planner
+    plan = JoinPlan()
+    st = lib().mapsq_plan_join(ctypes.byref(t1), ctypes.byref(t2), ctypes.byref(plan))
+    if st:
+        raise MapsqError(st, "plan_join")
+    return plan

@@ -1,0 +1,1044 @@
+// api.cu — host orchestration and the C ABI of libmapsq (include/mapsq.h).
+//
+// The host side plays the paper's CPU role, "CPU is used to assigns subqueries and GPU is used
+// to compute the join of subqueries": it validates the plan, derives each join's
+// spec (shared variables, key packing), sizes buffers after the single blocking count read of
+// each operator, and folds the joins left-deep.  All data-path work runs in
+// the kernels of scan.cu / radix.cu / reduce.cu / partition.cu.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.cuh"
+
+using namespace mapsq;
+
+namespace mapsq {
+
+mapsq_status set_error(mapsq_ctx *ctx, mapsq_status st, const std::string &msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+mapsq_status cuda_check(mapsq_ctx *ctx, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return MAPSQ_OK;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return set_error(ctx, MAPSQ_E_NOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  if (ctx) ctx->cuda_broken = true;
+  return set_error(ctx, MAPSQ_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void *dalloc(mapsq_ctx *ctx, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);
+  if (ctx->custom_alloc) return ctx->alloc.alloc(ctx->alloc.ctx, bytes, (void *)s);
+  void *p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s) {
+  if (!p) return;
+  if (ctx->custom_alloc)
+    ctx->alloc.free(ctx->alloc.ctx, p, (void *)s);
+  else
+    cudaFreeAsync(p, s);
+}
+
+KTimer::KTimer(mapsq_ctx *c, cudaStream_t st, const char *name, uint64_t bytes, int nlaunch)
+    : ctx(c), s(st), on(c->profiling) {
+  ctx->counters.launches += nlaunch;
+  if (!on) return;
+  t.name = name;
+  t.bytes = bytes;
+  for (cudaEvent_t *e : {&t.ev0, &t.ev1}) {
+    if (!ctx->free_events.empty()) {
+      *e = ctx->free_events.back();
+      ctx->free_events.pop_back();
+    } else {
+      cudaEventCreate(e);
+    }
+  }
+  cudaEventRecord(t.ev0, s);
+}
+
+KTimer::~KTimer() {
+  if (!on) return;
+  cudaEventRecord(t.ev1, s);
+  ctx->pending.push_back(t);
+}
+
+}  // namespace mapsq
+
+namespace {
+
+#define TRY(x)                                  \
+  do {                                          \
+    mapsq_status _st = (x);                     \
+    if (_st != MAPSQ_OK) return _st;            \
+  } while (0)
+#define CK(call)                                \
+  do {                                          \
+    cudaError_t _e = (call);                    \
+    if (_e != cudaSuccess) return cuda_check(ctx, _e, #call); \
+  } while (0)
+#define CKL(what) CK(cudaGetLastError())
+#define NEED(ptr)                                                                  \
+  do {                                                                             \
+    if (!(ptr)) return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed"); \
+  } while (0)
+
+inline cudaStream_t S(void *stream) { return (cudaStream_t)stream; }
+
+mapsq_status enter(mapsq_ctx *ctx) {
+  if (!ctx) return MAPSQ_E_INVALID;
+  if (ctx->cuda_broken) return MAPSQ_E_CUDA;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != ctx->device) CK(cudaSetDevice(ctx->device));
+  return MAPSQ_OK;
+}
+
+mapsq_status ensure_pinned(mapsq_ctx *ctx, size_t words) {
+  if (ctx->pinned_words >= words) return MAPSQ_OK;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  size_t w = std::max<size_t>(words, 256);
+  CK(cudaMallocHost((void **)&ctx->pinned, w * sizeof(uint64_t)));
+  ctx->pinned_words = w;
+  return MAPSQ_OK;
+}
+
+void clear_table(mapsq_table *t) {
+  std::memset(t, 0, sizeof *t);
+}
+
+mapsq_status check_table(mapsq_ctx *ctx, const mapsq_table *t, const char *name) {
+  if (!t) return set_error(ctx, MAPSQ_E_INVALID, std::string(name) + " is NULL");
+  if (t->ncols == 0 || t->ncols > MAPSQ_MAX_COLS)
+    return set_error(ctx, MAPSQ_E_INVALID, std::string(name) + ": ncols out of range");
+  for (uint32_t i = 0; i < t->ncols; i++) {
+    if (t->var[i] < 0) return set_error(ctx, MAPSQ_E_INVALID, std::string(name) + ": negative var id");
+    if (t->nrows && !t->col[i]) return set_error(ctx, MAPSQ_E_INVALID, std::string(name) + ": NULL column");
+    for (uint32_t j = 0; j < i; j++)
+      if (t->var[i] == t->var[j])
+        return set_error(ctx, MAPSQ_E_INVALID, std::string(name) + ": duplicate variable");
+  }
+  return MAPSQ_OK;
+}
+
+// Allocate a table of `rows` x `ncols` as one allocation with 16 B aligned column strides.
+mapsq_status alloc_table(mapsq_ctx *ctx, mapsq_table *t, uint64_t rows, uint32_t ncols,
+                         cudaStream_t s) {
+  t->nrows = rows;
+  t->ncols = ncols;
+  t->owner = nullptr;
+  if (rows == 0) {
+    for (uint32_t c = 0; c < ncols; c++) t->col[c] = nullptr;
+    return MAPSQ_OK;
+  }
+  const uint64_t stride = (rows + 3) & ~3ull;
+  void *p = dalloc(ctx, stride * ncols * sizeof(uint32_t), s);
+  if (!p) return set_error(ctx, MAPSQ_E_NOMEM, "output allocation failed");
+  t->owner = p;
+  for (uint32_t c = 0; c < ncols; c++) t->col[c] = static_cast<uint32_t *>(p) + c * stride;
+  return MAPSQ_OK;
+}
+
+// ------------------------------------------------------------------------------ join plan
+mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
+                       mapsq_join_plan *pl) {
+  std::memset(pl, 0, sizeof *pl);
+  TRY(check_table(ctx, a, "tp1"));
+  TRY(check_table(ctx, b, "tp2"));
+  if (!(a->flags & MAPSQ_TABLE_BOUNDS) || !(b->flags & MAPSQ_TABLE_BOUNDS))
+    return set_error(ctx, MAPSQ_E_INVALID, "plan_join needs column bounds on both tables");
+  pl->n1 = a->nrows;
+  pl->n2 = b->nrows;
+  if (a->nrows + b->nrows >= (1ull << 32))
+    return set_error(ctx, MAPSQ_E_INVALID, "n1 + n2 must be < 2^32 per join per GPU");
+  // shared variables, ascending id (reading R5/R6)
+  int32_t sh[MAPSQ_MAX_COLS];
+  uint32_t ns = 0;
+  for (uint32_t i = 0; i < a->ncols; i++)
+    for (uint32_t j = 0; j < b->ncols; j++)
+      if (a->var[i] == b->var[j]) sh[ns++] = a->var[i];
+  if (ns == 0) return set_error(ctx, MAPSQ_E_NO_SHARED, "join inputs share no variable");
+  std::sort(sh, sh + ns);
+  pl->nshared = ns;
+  auto colof = [](const mapsq_table *t, int32_t v) {
+    for (uint32_t c = 0; c < t->ncols; c++)
+      if (t->var[c] == v) return (int32_t)c;
+    return (int32_t)-1;
+  };
+  auto is_shared = [&](int32_t v) { return std::binary_search(sh, sh + ns, v); };
+  for (uint32_t c = 0; c < a->ncols; c++)
+    if (!is_shared(a->var[c])) pl->rest_col1[pl->nrest1++] = (int32_t)c;
+  for (uint32_t c = 0; c < b->ncols; c++)
+    if (!is_shared(b->var[c])) pl->rest_col2[pl->nrest2++] = (int32_t)c;
+  pl->out_ncols = ns + pl->nrest1 + pl->nrest2;
+  if (pl->out_ncols > MAPSQ_MAX_COLS)
+    return set_error(ctx, MAPSQ_E_INVALID, "join output wider than MAPSQ_MAX_COLS");
+  uint32_t k = 0;
+  for (uint32_t c = 0; c < ns; c++) pl->out_var[k++] = sh[c];
+  for (uint32_t c = 0; c < pl->nrest1; c++) pl->out_var[k++] = a->var[pl->rest_col1[c]];
+  for (uint32_t c = 0; c < pl->nrest2; c++) pl->out_var[k++] = b->var[pl->rest_col2[c]];
+  // key packing over the UNION of both sides' bounds (every row stays representable); the
+  // output's key bounds are the intersection
+  uint32_t kb = 0;
+  for (uint32_t c = 0; c < ns; c++) {
+    pl->shared[c] = sh[c];
+    const int32_t ca = colof(a, sh[c]), cb = colof(b, sh[c]);
+    pl->key_col1[c] = ca;
+    pl->key_col2[c] = cb;
+    const uint32_t ulo = std::min(a->lo[ca], b->lo[cb]), uhi = std::max(a->hi[ca], b->hi[cb]);
+    pl->key_lo[c] = ulo;
+    pl->key_hi[c] = uhi;
+    pl->key_bits[c] = bits_for((uint64_t)uhi - ulo);
+    kb += pl->key_bits[c];
+    if (std::max(a->lo[ca], b->lo[cb]) > std::min(a->hi[ca], b->hi[cb])) pl->disjoint = 1;
+  }
+  uint32_t sft = 0;
+  for (int c = (int)ns - 1; c >= 0; c--) {  // first shared variable most significant
+    pl->key_shift[c] = sft;
+    sft += pl->key_bits[c];
+  }
+  pl->kb = kb;
+  const uint64_t n = a->nrows + b->nrows;
+  pl->ib = n > 1 ? bits_for(n - 1) : 1;
+  if (kb > 64) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "packed join key wider than 64 bits");
+  pl->path = (kb + pl->ib <= 64) ? MAPSQ_PATH_P64 : MAPSQ_PATH_KV;
+  pl->passes = (kb + MAPSQ_RADIX_BITS - 1) / MAPSQ_RADIX_BITS;
+  return MAPSQ_OK;
+}
+
+mapsq_status bounds_of(mapsq_ctx *ctx, mapsq_table *t, cudaStream_t s) {
+  if (t->flags & MAPSQ_TABLE_BOUNDS) return MAPSQ_OK;
+  if (t->nrows == 0) {
+    for (uint32_t c = 0; c < t->ncols; c++) t->lo[c] = t->hi[c] = 0;
+    t->flags |= MAPSQ_TABLE_BOUNDS;
+    return MAPSQ_OK;
+  }
+  Scratch sc(ctx, s);
+  uint32_t *b = sc.get<uint32_t>(2 * t->ncols);
+  NEED(b);
+  for (uint32_t c = 0; c < t->ncols; c++) {
+    CK(cudaMemsetAsync(b + 2 * c, 0xff, 4, s));
+    CK(cudaMemsetAsync(b + 2 * c + 1, 0, 4, s));
+  }
+  {
+    KTimer kt(ctx, s, "minmax", t->nrows * 4ull * t->ncols, (int)t->ncols);
+    launch_minmax(t->col, t->ncols, t->nrows, b, s);
+    CKL("minmax");
+  }
+  TRY(ensure_pinned(ctx, t->ncols));
+  CK(cudaMemcpyAsync(ctx->pinned, b, 8 * t->ncols, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t *h = reinterpret_cast<const uint32_t *>(ctx->pinned);
+  for (uint32_t c = 0; c < t->ncols; c++) {
+    t->lo[c] = h[2 * c];
+    t->hi[c] = h[2 * c + 1];
+  }
+  t->flags |= MAPSQ_TABLE_BOUNDS;
+  return MAPSQ_OK;
+}
+
+// ------------------------------------------------------------------------------ sort driver
+// Stable LSD sort of keys (and optional vals) by `passes` 8-bit digits starting at bit_lo, the
+// digit histograms `hist` (passes x 256, exclusive-scanned) already built.  a/b are ping-pong
+// buffers; returns in *which the buffer (0 = a, 1 = b) holding the result.
+mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *va, uint32_t *vb,
+                        uint64_t n, uint32_t bit_lo, uint32_t nbits, uint32_t *hist, Scratch &sc,
+                        cudaStream_t s, int *which) {
+  *which = 0;
+  const uint32_t passes = (nbits + 7) / 8;
+  if (passes == 0 || n == 0) return MAPSQ_OK;
+  const uint64_t ntiles = ceil_div(n, kSortTile);
+  uint64_t *status = sc.get<uint64_t>(ntiles * kRadix);
+  uint32_t *counters = sc.get<uint32_t>(kMaxPasses);
+  NEED(status);
+  NEED(counters);
+  CK(cudaMemsetAsync(counters, 0, kMaxPasses * sizeof(uint32_t), s));
+  const uint64_t bytes = n * (va ? 24ull : 16ull);
+  for (uint32_t p = 0; p < passes; p++) {
+    const uint32_t shift = bit_lo + 8 * p;
+    const uint32_t bits = std::min<uint32_t>(8, nbits - 8 * p);
+    CK(cudaMemsetAsync(status, 0, ntiles * kRadix * sizeof(uint64_t), s));
+    uint64_t *kin = (*which == 0) ? ka : kb_, *kout = (*which == 0) ? kb_ : ka;
+    uint32_t *vin = va ? ((*which == 0) ? va : vb) : nullptr;
+    uint32_t *vout = va ? ((*which == 0) ? vb : va) : nullptr;
+    {
+      KTimer kt(ctx, s, va ? "radix_pass_kv" : "radix_pass", bytes);
+      launch_radix_pass(kin, kout, vin, vout, n, shift, bits, hist + p * kRadix, status,
+                        counters + p, s);
+      CKL("radix_pass");
+    }
+    *which ^= 1;
+  }
+  return MAPSQ_OK;
+}
+
+void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b,
+                     mapsq_table *rs);
+
+// Output bounds: key columns get the intersection, the rest inherit their source's bounds.
+void set_join_bounds(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b,
+                     mapsq_table *rs) {
+  rs->flags = MAPSQ_TABLE_BOUNDS;
+  uint32_t k = 0;
+  for (uint32_t c = 0; c < pl.nshared; c++, k++) {
+    rs->lo[k] = std::max(a->lo[pl.key_col1[c]], b->lo[pl.key_col2[c]]);
+    rs->hi[k] = std::min(a->hi[pl.key_col1[c]], b->hi[pl.key_col2[c]]);
+    if (rs->lo[k] > rs->hi[k]) rs->lo[k] = rs->hi[k] = 0;
+  }
+  for (uint32_t c = 0; c < pl.nrest1; c++, k++) {
+    rs->lo[k] = a->lo[pl.rest_col1[c]];
+    rs->hi[k] = a->hi[pl.rest_col1[c]];
+  }
+  for (uint32_t c = 0; c < pl.nrest2; c++, k++) {
+    rs->lo[k] = b->lo[pl.rest_col2[c]];
+    rs->hi[k] = b->hi[pl.rest_col2[c]];
+  }
+}
+
+void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b,
+                     mapsq_table *rs) {
+  clear_table(rs);
+  rs->ncols = pl.out_ncols;
+  for (uint32_t c = 0; c < pl.out_ncols; c++) rs->var[c] = pl.out_var[c];
+  set_join_bounds(pl, a, b, rs);
+}
+
+PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b) {
+  PackArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  pa.nkey = pl.nshared;
+  for (uint32_t c = 0; c < pl.nshared; c++) {
+    pa.key1[c] = a->col[pl.key_col1[c]];
+    pa.key2[c] = b->col[pl.key_col2[c]];
+    pa.lo[c] = pl.key_lo[c];
+    pa.shift[c] = pl.key_shift[c];
+  }
+  pa.n1 = pl.n1;
+  pa.n2 = pl.n2;
+  pa.ib = pl.ib;
+  pa.kv = pl.path == MAPSQ_PATH_KV;
+  pa.bit_lo = pa.kv ? 0 : pl.ib;
+  pa.passes = pl.passes;
+  const uint32_t last_bits = pl.kb - 8 * (pl.passes ? pl.passes - 1 : 0);
+  pa.last_mask = pl.passes ? ((1u << last_bits) - 1u) : 0xffu;
+  return pa;
+}
+
+// ------------------------------------------------------------------------------ join
+mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_table *tp2_in,
+                       mapsq_table *rs, cudaStream_t s) {
+  clear_table(rs);
+  TRY(check_table(ctx, tp1_in, "tp1"));
+  TRY(check_table(ctx, tp2_in, "tp2"));
+  mapsq_table a = *tp1_in, b = *tp2_in;
+  TRY(bounds_of(ctx, &a, s));
+  TRY(bounds_of(ctx, &b, s));
+  mapsq_join_plan pl;
+  TRY(plan_join(ctx, &a, &b, &pl));
+  const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
+  ctx->counters.joins++;
+  ctx->counters.join_in_rows += n;
+  ctx->counters.last_kb = pl.kb;
+  ctx->counters.last_ib = pl.ib;
+  ctx->counters.last_passes = pl.passes;
+  ctx->counters.last_path = pl.path;
+  if (n1 == 0 || n2 == 0 || pl.disjoint) {
+    fill_empty_join(pl, &a, &b, rs);
+    return MAPSQ_OK;
+  }
+  Scratch sc(ctx, s);
+  const bool kv = pl.path == MAPSQ_PATH_KV;
+  uint64_t *wa = sc.get<uint64_t>(n), *wb = sc.get<uint64_t>(n);
+  uint32_t *va = kv ? sc.get<uint32_t>(n) : nullptr, *vb = kv ? sc.get<uint32_t>(n) : nullptr;
+  uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
+  NEED(wa);
+  NEED(wb);
+  NEED(hist);
+  if (kv) {
+    NEED(va);
+    NEED(vb);
+  }
+  // ---- Map (row a3) + upfront histograms
+  CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+  {
+    const PackArgs pa = pack_args(pl, &a, &b);
+    KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
+    launch_pack_hist(pa, wa, va, hist, s);
+    CKL("pack_hist");
+  }
+  if (pl.passes) {
+    KTimer kt(ctx, s, "hist_scan", 8ull * kRadix * pl.passes);
+    launch_hist_scan(hist, (int)pl.passes, s);
+    CKL("hist_scan");
+  }
+  // ---- Sort (row a4)
+  int which = 0;
+  TRY(radix_sort(ctx, wa, wb, va, vb, n, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
+  uint64_t *words = which ? wb : wa;
+  uint32_t *vals = kv ? (which ? vb : va) : nullptr;
+  sc.release(which ? wa : wb);
+  if (kv) sc.release(which ? va : vb);
+  // ---- ReduceDuplicate 1 (row a5): groups + counts + exclusive scan
+  const uint64_t cap = std::min(n1, n2);
+  uint32_t *gs = sc.get<uint32_t>(cap), *gp = sc.get<uint32_t>(cap), *ge = sc.get<uint32_t>(cap);
+  uint64_t *gc = sc.get<uint64_t>(cap), *go = sc.get<uint64_t>(cap);
+  const uint64_t gtiles = find_groups_tiles(n);
+  uint64_t *gstatus = sc.get<uint64_t>(gtiles);
+  uint64_t *scal = sc.get<uint64_t>(4);  // [0] ngroups, [1] |RS|, [2] tile counter
+  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(cap));
+  NEED(gs); NEED(gp); NEED(ge); NEED(gc); NEED(go); NEED(gstatus); NEED(scal); NEED(tmp);
+  CK(cudaMemsetAsync(gstatus, 0, gtiles * sizeof(uint64_t), s));
+  CK(cudaMemsetAsync(scal, 0, 4 * sizeof(uint64_t), s));
+  {
+    KTimer kt(ctx, s, "find_groups", n * 8ull);
+    GroupOut g{gs, gp, ge, gc};
+    launch_find_groups(kv ? nullptr : words, kv ? words : nullptr, vals, n, n1, pl.ib, g,
+                       gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
+    CKL("find_groups");
+  }
+  {
+    KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
+    launch_exclusive_scan_u64_dev(gc, go, scal, cap, tmp, scal + 1, s);
+    CKL("scan_counts");
+  }
+  TRY(ensure_pinned(ctx, 2));
+  CK(cudaMemcpyAsync(ctx->pinned, scal, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));  // the one blocking read: |RS| sizes the output
+  const uint64_t ngroups = ctx->pinned[0], m = ctx->pinned[1];
+  // ---- ReduceDuplicate 2 (row a6): expand into RS
+  fill_empty_join(pl, &a, &b, rs);
+  TRY(alloc_table(ctx, rs, m, pl.out_ncols, s));
+  if (m) {
+    ExpandArgs ea;
+    std::memset(&ea, 0, sizeof ea);
+    ea.words = kv ? nullptr : words;
+    ea.keys = kv ? words : nullptr;
+    ea.vals = vals;
+    ea.n1 = n1;
+    ea.ib = pl.ib;
+    ea.gstart = gs;
+    ea.gsplit = gp;
+    ea.gend = ge;
+    ea.goff = go;
+    ea.ngroups = ngroups;
+    ea.m = m;
+    ea.nkey = pl.nshared;
+    for (uint32_t c = 0; c < pl.nshared; c++) {
+      ea.key_lo[c] = pl.key_lo[c];
+      ea.key_shift[c] = pl.key_shift[c];
+      ea.key_mask[c] = (uint32_t)((1ull << pl.key_bits[c]) - 1);
+    }
+    ea.nrest1 = pl.nrest1;
+    ea.nrest2 = pl.nrest2;
+    for (uint32_t c = 0; c < pl.nrest1; c++) ea.rest1[c] = a.col[pl.rest_col1[c]];
+    for (uint32_t c = 0; c < pl.nrest2; c++) ea.rest2[c] = b.col[pl.rest_col2[c]];
+    for (uint32_t c = 0; c < pl.out_ncols; c++) ea.out[c] = rs->col[c];
+    const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * n +
+                           4ull * (n1 * pl.nrest1 + n2 * pl.nrest2);
+    KTimer kt(ctx, s, "expand", bytes);
+    launch_expand(ea, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      dfree(ctx, rs->owner, s);
+      clear_table(rs);
+      return cuda_check(ctx, e, "expand");
+    }
+  }
+  ctx->counters.join_out_rows += m;
+  return MAPSQ_OK;
+}
+
+// ------------------------------------------------------------------------------ scan
+mapsq_status build_scan_args(mapsq_ctx *ctx, const mapsq_pattern *pats, int k, ScanArgs *a,
+                             int32_t vars[][3]) {
+  std::memset(a, 0, sizeof *a);
+  if (!pats || k < 1 || k > MAPSQ_MAX_PATTERNS)
+    return set_error(ctx, MAPSQ_E_INVALID, "pattern count out of range");
+  a->k = k;
+  for (int j = 0; j < k; j++) {
+    ScanPat &p = a->pat[j];
+    for (int q = 0; q < 3; q++) {
+      const int32_t v = pats[j].var[q];
+      if (v < -1) return set_error(ctx, MAPSQ_E_INVALID, "bad pattern variable");
+      if (v == -1) {
+        p.const_mask |= 1u << q;
+        p.id[q] = pats[j].id[q];
+        a->need_count |= 1u << q;
+        continue;
+      }
+      bool seen = false;
+      for (int r = 0; r < q; r++)
+        if (pats[j].var[r] == v) {
+          seen = true;
+          p.eq_mask |= (r == 0 && q == 1) ? 1u : (r == 0 && q == 2) ? 2u : 4u;
+          a->need_count |= (1u << q) | (1u << r);
+        }
+      if (!seen) {
+        vars[j][p.ncols] = v;
+        p.src[p.ncols++] = q;
+        a->need_write |= 1u << q;
+      }
+    }
+    if (p.ncols == 0) return set_error(ctx, MAPSQ_E_INVALID, "pattern without variables");
+  }
+  return MAPSQ_OK;
+}
+
+mapsq_status scan_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_pattern *pats, int k,
+                       mapsq_table *out, cudaStream_t s) {
+  if (!out) return set_error(ctx, MAPSQ_E_INVALID, "out is NULL");
+  for (int j = 0; j < k && j < MAPSQ_MAX_PATTERNS; j++) clear_table(&out[j]);
+  if (!T) return set_error(ctx, MAPSQ_E_INVALID, "triples is NULL");
+  if (T->n && (!T->s || !T->p || !T->o)) return set_error(ctx, MAPSQ_E_INVALID, "NULL triple column");
+  ScanArgs a;
+  int32_t vars[MAPSQ_MAX_PATTERNS][3];
+  TRY(build_scan_args(ctx, pats, k, &a, vars));
+  for (int j = 0; j < k; j++) {
+    out[j].ncols = a.pat[j].ncols;
+    for (uint32_t c = 0; c < a.pat[j].ncols; c++) out[j].var[c] = vars[j][c];
+    out[j].flags = MAPSQ_TABLE_BOUNDS;
+  }
+  ctx->counters.scans += k;
+  ctx->counters.scanned_triples += T->n;
+  const uint64_t n = T->n;
+  if (n == 0) return MAPSQ_OK;
+  Scratch sc(ctx, s);
+  const uint64_t ntiles = ceil_div(n, kScanTile);
+  const uint64_t mask_words = ceil_div(n, 32);
+  uint32_t *masks = sc.get<uint32_t>(k * mask_words);
+  uint32_t *tcnt = sc.get<uint32_t>(k * ntiles);
+  uint64_t *toff = sc.get<uint64_t>(k * ntiles + 1);
+  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(k * ntiles));
+  uint32_t *bnd = sc.get<uint32_t>(2 * MAPSQ_MAX_PATTERNS * 3);
+  NEED(masks); NEED(tcnt); NEED(toff); NEED(tmp); NEED(bnd);
+  const int npos_count = __builtin_popcount(a.need_count);
+  {
+    KTimer kt(ctx, s, "scan_count", 4ull * npos_count * n + 4ull * k * mask_words);
+    launch_scan_count(*T, a, masks, mask_words, tcnt, ntiles, s);
+    CKL("scan_count");
+  }
+  {
+    KTimer kt(ctx, s, "scan_tiles", 12ull * k * ntiles, 3);
+    launch_exclusive_scan_u32(tcnt, toff, k * ntiles, tmp, toff + k * ntiles, s);
+    CKL("scan_tiles");
+  }
+  TRY(ensure_pinned(ctx, k + 1));
+  for (int j = 0; j <= k; j++)
+    CK(cudaMemcpyAsync(ctx->pinned + j, toff + (uint64_t)j * ntiles, sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));  // blocking read of the k match counts
+  uint64_t rows[MAPSQ_MAX_PATTERNS], total = 0;
+  for (int j = 0; j < k; j++) {
+    rows[j] = ctx->pinned[j + 1] - ctx->pinned[j];
+    total += rows[j];
+  }
+  ScanOut so;
+  std::memset(&so, 0, sizeof so);
+  for (int j = 0; j < k; j++) {
+    mapsq_status st = alloc_table(ctx, &out[j], rows[j], a.pat[j].ncols, s);
+    if (st != MAPSQ_OK) {
+      for (int q = 0; q < j; q++) {
+        dfree(ctx, out[q].owner, s);
+        clear_table(&out[q]);
+      }
+      return st;
+    }
+    for (uint32_t c = 0; c < a.pat[j].ncols; c++) so.col[j * 3 + c] = out[j].col[c];
+  }
+  if (total == 0) return MAPSQ_OK;
+  uint32_t *bmin = bnd, *bmax = bnd + MAPSQ_MAX_PATTERNS * 3;
+  CK(cudaMemsetAsync(bmin, 0xff, MAPSQ_MAX_PATTERNS * 3 * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(bmax, 0, MAPSQ_MAX_PATTERNS * 3 * sizeof(uint32_t), s));
+  {
+    uint64_t outb = 0;
+    for (int j = 0; j < k; j++) outb += 4ull * rows[j] * a.pat[j].ncols;
+    const int npos_write = __builtin_popcount(a.need_write);
+    KTimer kt(ctx, s, "scan_write",
+              4ull * k * mask_words + 4ull * npos_write * total + outb);
+    launch_scan_write(*T, a, masks, mask_words, toff, ntiles, so, bmin, bmax, s);
+    CKL("scan_write");
+  }
+  CK(cudaMemcpyAsync(ctx->pinned, bnd, 2 * MAPSQ_MAX_PATTERNS * 3 * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t *h = reinterpret_cast<const uint32_t *>(ctx->pinned);
+  for (int j = 0; j < k; j++)
+    for (uint32_t c = 0; c < a.pat[j].ncols; c++) {
+      out[j].lo[c] = rows[j] ? h[j * 3 + c] : 0;
+      out[j].hi[c] = rows[j] ? h[MAPSQ_MAX_PATTERNS * 3 + j * 3 + c] : 0;
+    }
+  return MAPSQ_OK;
+}
+
+// ------------------------------------------------------------------------------ query
+mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_pattern *pats,
+                        int npats, const int32_t *proj, int nproj, mapsq_table *rs,
+                        cudaStream_t s) {
+  if (!rs) return set_error(ctx, MAPSQ_E_INVALID, "rs is NULL");
+  clear_table(rs);
+  if (!pats || npats < 1 || npats > MAPSQ_MAX_PATTERNS)
+    return set_error(ctx, MAPSQ_E_INVALID, "pattern count out of range");
+  if (nproj < 0 || nproj > MAPSQ_MAX_COLS || (nproj > 0 && !proj))
+    return set_error(ctx, MAPSQ_E_INVALID, "bad projection");
+  // first-appearance variable order and connectivity
+  std::vector<int32_t> order;
+  for (int i = 0; i < npats; i++) {
+    bool shares = (i == 0);
+    for (int q = 0; q < 3; q++) {
+      const int32_t v = pats[i].var[q];
+      if (v < 0) continue;
+      if (std::find(order.begin(), order.end(), v) != order.end()) {
+        // shared with an EARLIER pattern?
+        for (int j = 0; j < i && !shares; j++)
+          for (int r = 0; r < 3; r++)
+            if (pats[j].var[r] == v) shares = true;
+      }
+    }
+    for (int q = 0; q < 3; q++) {
+      const int32_t v = pats[i].var[q];
+      if (v >= 0 && std::find(order.begin(), order.end(), v) == order.end()) order.push_back(v);
+    }
+    if (!shares)
+      return set_error(ctx, MAPSQ_E_NO_SHARED, "pattern " + std::to_string(i) +
+                                                   " shares no variable with the patterns before it");
+  }
+  std::vector<int32_t> want(proj, proj + nproj);
+  if (nproj == 0) want = order;
+  if (want.size() > MAPSQ_MAX_COLS) return set_error(ctx, MAPSQ_E_INVALID, "projection too wide");
+  for (int32_t v : want)
+    if (std::find(order.begin(), order.end(), v) == order.end())
+      return set_error(ctx, MAPSQ_E_INVALID, "projected variable not in the query");
+
+  mapsq_table tabs[MAPSQ_MAX_PATTERNS];
+  TRY(scan_impl(ctx, T, pats, npats, tabs, s));
+  mapsq_table acc = tabs[0];
+  for (int i = 1; i < npats; i++) {
+    mapsq_table r;
+    mapsq_status st = join_impl(ctx, &acc, &tabs[i], &r, s);
+    dfree(ctx, acc.owner, s);
+    dfree(ctx, tabs[i].owner, s);
+    if (st != MAPSQ_OK) {
+      for (int j = i + 1; j < npats; j++) dfree(ctx, tabs[j].owner, s);
+      return st;
+    }
+    acc = r;
+  }
+  // projection: zero-copy column selection (bag semantics)
+  mapsq_table out;
+  clear_table(&out);
+  out.nrows = acc.nrows;
+  out.ncols = (uint32_t)want.size();
+  out.owner = acc.owner;
+  out.flags = acc.flags;
+  for (uint32_t c = 0; c < out.ncols; c++) {
+    for (uint32_t k = 0; k < acc.ncols; k++)
+      if (acc.var[k] == want[c]) {
+        out.var[c] = want[c];
+        out.col[c] = acc.col[k];
+        out.lo[c] = acc.lo[k];
+        out.hi[c] = acc.hi[k];
+      }
+  }
+  *rs = out;
+  return MAPSQ_OK;
+}
+
+}  // namespace
+
+// ================================================================================ C ABI
+MAPSQ_API const char *mapsq_version(void) { return "mapsq-b200 0.1 (sm_100a)"; }
+
+MAPSQ_API mapsq_status mapsq_create(mapsq_ctx **out, int device, const mapsq_allocator *al) {
+  if (!out) return MAPSQ_E_INVALID;
+  *out = nullptr;
+  mapsq_ctx *ctx = new (std::nothrow) mapsq_ctx();
+  if (!ctx) return MAPSQ_E_NOMEM;
+  ctx->device = device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    delete ctx;
+    return MAPSQ_E_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return MAPSQ_E_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+  ctx->l2_bytes = (size_t)l2;
+  if (al && al->alloc && al->free) {
+    ctx->alloc = *al;
+    ctx->custom_alloc = true;
+  } else {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  *out = ctx;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
+  if (!ctx) return;
+  for (auto &p : ctx->pending) {
+    cudaEventDestroy(p.ev0);
+    cudaEventDestroy(p.ev1);
+  }
+  for (auto e : ctx->free_events) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+}
+
+MAPSQ_API const char *mapsq_last_error(const mapsq_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : "no context";
+}
+
+MAPSQ_API void mapsq_table_release(mapsq_ctx *ctx, mapsq_table *t, void *stream) {
+  if (!ctx || !t) return;
+  if (t->owner) dfree(ctx, t->owner, S(stream));
+  clear_table(t);
+}
+
+MAPSQ_API mapsq_status mapsq_scan_patterns(mapsq_ctx *ctx, const mapsq_triples *T,
+                                           const mapsq_pattern *pats, int k, mapsq_table *out,
+                                           void *stream) {
+  TRY(enter(ctx));
+  return scan_impl(ctx, T, pats, k, out, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_scan_pattern(mapsq_ctx *ctx, const mapsq_triples *T,
+                                          const mapsq_pattern *pat, mapsq_table *out,
+                                          void *stream) {
+  TRY(enter(ctx));
+  return scan_impl(ctx, T, pat, 1, out, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table *tp2,
+                                       mapsq_join_plan *plan) {
+  if (!plan) return MAPSQ_E_INVALID;
+  return plan_join(nullptr, tp1, tp2, plan);
+}
+
+MAPSQ_API mapsq_status mapsq_join(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
+                                  mapsq_table *rs, void *stream) {
+  TRY(enter(ctx));
+  if (!rs) return set_error(ctx, MAPSQ_E_INVALID, "rs is NULL");
+  return join_impl(ctx, tp1, tp2, rs, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_query(mapsq_ctx *ctx, const mapsq_triples *T,
+                                   const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                   int nproj, mapsq_table *rs, void *stream) {
+  TRY(enter(ctx));
+  return query_impl(ctx, T, pats, npats, proj, nproj, rs, S(stream));
+}
+
+MAPSQ_API void mapsq_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+}
+
+MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host,
+                                        const uint32_t *p_host, const uint32_t *o_host,
+                                        const mapsq_pattern *pats, int npats,
+                                        const int32_t *proj, int nproj, uint64_t *host_rows,
+                                        uint32_t *out_ncols, int32_t *out_var,
+                                        uint32_t **host_cols, void *stream) {
+  TRY(enter(ctx));
+  if (!host_rows || !out_ncols || !out_var || !host_cols || (n && (!s_host || !p_host || !o_host)))
+    return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  *host_rows = 0;
+  *out_ncols = 0;
+  cudaStream_t s = S(stream);
+  mapsq_table rs;
+  {
+    Scratch sc(ctx, s);
+    uint32_t *d = sc.get<uint32_t>(3 * n + 12);
+    NEED(d);
+    uint32_t *ds = d, *dp = d + n, *dob = d + 2 * n;
+    // H2D in chunks so the copy engine streams while the scan's first pass starts early
+    const uint64_t chunk = 1ull << 26;
+    for (uint64_t off = 0; off < n; off += chunk) {
+      const uint64_t c = std::min(chunk, n - off);
+      CK(cudaMemcpyAsync(ds + off, s_host + off, c * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dp + off, p_host + off, c * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dob + off, o_host + off, c * 4, cudaMemcpyHostToDevice, s));
+    }
+    mapsq_triples T{n, ds, dp, dob};
+    TRY(query_impl(ctx, &T, pats, npats, proj, nproj, &rs, s));
+  }
+  *out_ncols = rs.ncols;
+  for (uint32_t c = 0; c < rs.ncols; c++) {
+    out_var[c] = rs.var[c];
+    host_cols[c] = nullptr;
+  }
+  mapsq_status st = MAPSQ_OK;
+  for (uint32_t c = 0; c < rs.ncols && st == MAPSQ_OK; c++) {
+    void *h = nullptr;
+    cudaError_t e = cudaMallocHost(&h, std::max<uint64_t>(rs.nrows, 1) * 4);
+    if (e != cudaSuccess) {
+      st = cuda_check(ctx, e, "cudaMallocHost");
+      break;
+    }
+    host_cols[c] = static_cast<uint32_t *>(h);
+    if (rs.nrows) {
+      e = cudaMemcpyAsync(h, rs.col[c], rs.nrows * 4, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) st = cuda_check(ctx, e, "D2H result");
+    }
+  }
+  mapsq_table_release(ctx, &rs, stream);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (st == MAPSQ_OK && e != cudaSuccess) st = cuda_check(ctx, e, "sync");
+  if (st != MAPSQ_OK) {
+    for (uint32_t c = 0; c < rs.ncols; c++) mapsq_host_free(host_cols[c]);
+    return st;
+  }
+  *host_rows = rs.nrows;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream) {
+  TRY(enter(ctx));
+  TRY(check_table(ctx, t, "table"));
+  t->flags &= ~MAPSQ_TABLE_BOUNDS;
+  return bounds_of(ctx, t, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_map_words(mapsq_ctx *ctx, const mapsq_table *tp1,
+                                       const mapsq_table *tp2, const mapsq_join_plan *plan,
+                                       uint64_t *words, void *stream) {
+  TRY(enter(ctx));
+  if (!plan || !words || !tp1 || !tp2) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  if (plan->path != MAPSQ_PATH_P64) return set_error(ctx, MAPSQ_E_INVALID, "map_words needs a P64 plan");
+  if (plan->n1 + plan->n2 == 0) return MAPSQ_OK;
+  cudaStream_t s = S(stream);
+  Scratch sc(ctx, s);
+  uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
+  NEED(hist);
+  CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+  const PackArgs pa = pack_args(*plan, tp1, tp2);
+  KTimer kt(ctx, s, "pack_hist", 4ull * plan->nshared * (plan->n1 + plan->n2) + 8ull * (plan->n1 + plan->n2));
+  launch_pack_hist(pa, words, nullptr, hist, s);
+  CKL("pack_hist");
+  return MAPSQ_OK;
+}
+
+static mapsq_status sort_entry(mapsq_ctx *ctx, uint64_t *keys, uint32_t *vals, uint64_t n,
+                               uint32_t bit_lo, uint32_t bit_hi, cudaStream_t s) {
+  if (!keys || bit_hi > 64 || bit_lo > bit_hi) return set_error(ctx, MAPSQ_E_INVALID, "bad sort arguments");
+  const uint32_t nbits = bit_hi - bit_lo;
+  if (n < 2 || nbits == 0) return MAPSQ_OK;
+  if (n >= (1ull << 32)) return set_error(ctx, MAPSQ_E_INVALID, "n must be < 2^32");
+  Scratch sc(ctx, s);
+  uint64_t *kb_ = sc.get<uint64_t>(n);
+  uint32_t *vb = vals ? sc.get<uint32_t>(n) : nullptr;
+  uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
+  NEED(kb_);
+  NEED(hist);
+  if (vals) NEED(vb);
+  const uint32_t passes = (nbits + 7) / 8;
+  CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+  {
+    KTimer kt(ctx, s, "key_hist", 8ull * n);
+    launch_key_hist(keys, n, bit_lo, passes, nbits - 8 * (passes - 1), hist, s);
+    CKL("key_hist");
+  }
+  {
+    KTimer kt(ctx, s, "hist_scan", 8ull * kRadix * passes);
+    launch_hist_scan(hist, (int)passes, s);
+    CKL("hist_scan");
+  }
+  int which = 0;
+  TRY(radix_sort(ctx, keys, kb_, vals, vb, n, bit_lo, nbits, hist, sc, s, &which));
+  if (which) {
+    CK(cudaMemcpyAsync(keys, kb_, n * 8, cudaMemcpyDeviceToDevice, s));
+    if (vals) CK(cudaMemcpyAsync(vals, vb, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_sort_words(mapsq_ctx *ctx, uint64_t *words, uint64_t n,
+                                        uint32_t bit_lo, uint32_t bit_hi, void *stream) {
+  TRY(enter(ctx));
+  return sort_entry(ctx, words, nullptr, n, bit_lo, bit_hi, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_sort_pairs(mapsq_ctx *ctx, uint64_t *keys, uint32_t *vals,
+                                        uint64_t n, uint32_t bit_lo, uint32_t bit_hi,
+                                        void *stream) {
+  TRY(enter(ctx));
+  if (!vals) return set_error(ctx, MAPSQ_E_INVALID, "vals is NULL");
+  return sort_entry(ctx, keys, vals, n, bit_lo, bit_hi, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words, uint64_t n1,
+                                           uint64_t n2, uint32_t ib, uint32_t *group_start,
+                                           uint32_t *group_split, uint32_t *group_end,
+                                           uint64_t *group_off, uint64_t *ngroups,
+                                           uint64_t *total, void *stream) {
+  TRY(enter(ctx));
+  if (!ngroups || !total) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  *ngroups = *total = 0;
+  const uint64_t n = n1 + n2, cap = std::min(n1, n2);
+  if (n == 0 || cap == 0) return MAPSQ_OK;
+  if (!words || !group_start || !group_split || !group_end || !group_off || ib > 32)
+    return set_error(ctx, MAPSQ_E_INVALID, "bad reduce arguments");
+  cudaStream_t s = S(stream);
+  Scratch sc(ctx, s);
+  uint64_t *gc = sc.get<uint64_t>(cap);
+  const uint64_t gtiles = find_groups_tiles(n);
+  uint64_t *gstatus = sc.get<uint64_t>(gtiles);
+  uint64_t *scal = sc.get<uint64_t>(4);
+  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(cap));
+  NEED(gc); NEED(gstatus); NEED(scal); NEED(tmp);
+  CK(cudaMemsetAsync(gstatus, 0, gtiles * sizeof(uint64_t), s));
+  CK(cudaMemsetAsync(scal, 0, 4 * sizeof(uint64_t), s));
+  {
+    KTimer kt(ctx, s, "find_groups", n * 8ull);
+    GroupOut g{group_start, group_split, group_end, gc};
+    launch_find_groups(words, nullptr, nullptr, n, n1, ib, g, gstatus,
+                       reinterpret_cast<uint32_t *>(scal + 2), scal, s);
+    CKL("find_groups");
+  }
+  {
+    KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
+    launch_exclusive_scan_u64_dev(gc, group_off, scal, cap, tmp, scal + 1, s);
+    CKL("scan_counts");
+  }
+  TRY(ensure_pinned(ctx, 2));
+  CK(cudaMemcpyAsync(ctx->pinned, scal, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *ngroups = ctx->pinned[0];
+  *total = ctx->pinned[1];
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in,
+                                       const int32_t *key_vars, int nkey, int nparts,
+                                       mapsq_table *out, uint64_t *counts_host, void *stream) {
+  TRY(enter(ctx));
+  if (!out || !counts_host || !key_vars) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  clear_table(out);
+  TRY(check_table(ctx, in, "in"));
+  if (nparts < 1 || nparts > kMaxParts || nkey < 1 || nkey > (int)in->ncols)
+    return set_error(ctx, MAPSQ_E_INVALID, "bad partition arguments");
+  cudaStream_t s = S(stream);
+  PartArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  pa.nkey = (uint32_t)nkey;
+  for (int q = 0; q < nkey; q++) {
+    int c = -1;
+    for (uint32_t j = 0; j < in->ncols; j++)
+      if (in->var[j] == key_vars[q]) c = (int)j;
+    if (c < 0) return set_error(ctx, MAPSQ_E_INVALID, "partition key variable not in table");
+    pa.key[q] = in->col[c];
+  }
+  pa.ncols = in->ncols;
+  pa.n = in->nrows;
+  pa.nparts = (uint32_t)nparts;
+  for (uint32_t c = 0; c < in->ncols; c++) pa.in[c] = in->col[c];
+  *out = *in;
+  out->owner = nullptr;
+  TRY(alloc_table(ctx, out, in->nrows, in->ncols, s));
+  for (int d = 0; d < nparts; d++) counts_host[d] = 0;
+  if (in->nrows == 0) return MAPSQ_OK;
+  for (uint32_t c = 0; c < in->ncols; c++) pa.out[c] = out->col[c];
+  Scratch sc(ctx, s);
+  const uint64_t ntiles = ceil_div(in->nrows, kPartTile);
+  uint32_t *th = sc.get<uint32_t>(ntiles * nparts);
+  uint64_t *to = sc.get<uint64_t>(ntiles * nparts + 1);
+  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(ntiles * nparts));
+  if (!th || !to || !tmp) {
+    dfree(ctx, out->owner, s);
+    clear_table(out);
+    return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed");
+  }
+  {
+    KTimer kt(ctx, s, "partition_hist", 4ull * nkey * in->nrows);
+    launch_partition_hist(pa, th, ntiles, s);
+    CKL("partition_hist");
+  }
+  {
+    KTimer kt(ctx, s, "scan_tiles", 12ull * ntiles * nparts, 3);
+    launch_exclusive_scan_u32(th, to, ntiles * nparts, tmp, to + ntiles * nparts, s);
+    CKL("scan_tiles");
+  }
+  {
+    KTimer kt(ctx, s, "partition_scatter", 8ull * in->ncols * in->nrows);
+    launch_partition_scatter(pa, to, ntiles, s);
+    CKL("partition_scatter");
+  }
+  TRY(ensure_pinned(ctx, nparts + 1));
+  for (int d = 0; d <= nparts; d++)
+    CK(cudaMemcpyAsync(ctx->pinned + d, to + (uint64_t)d * ntiles, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int d = 0; d < nparts; d++) counts_host[d] = ctx->pinned[d + 1] - ctx->pinned[d];
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_set_profiling(mapsq_ctx *ctx, int on) {
+  if (!ctx) return MAPSQ_E_INVALID;
+  ctx->profiling = on != 0;
+  return MAPSQ_OK;
+}
+
+static void resolve_pending(mapsq_ctx *ctx) {
+  for (auto &p : ctx->pending) {
+    float ms = 0;
+    cudaEventSynchronize(p.ev1);
+    cudaEventElapsedTime(&ms, p.ev0, p.ev1);
+    auto it = ctx->kagg.find(p.name);
+    if (it == ctx->kagg.end()) {
+      ctx->korder.push_back(p.name);
+      it = ctx->kagg.emplace(p.name, KAgg{}).first;
+    }
+    it->second.launches++;
+    it->second.ms += ms;
+    it->second.bytes += p.bytes;
+    ctx->free_events.push_back(p.ev0);
+    ctx->free_events.push_back(p.ev1);
+  }
+  ctx->pending.clear();
+}
+
+MAPSQ_API mapsq_status mapsq_stats_reset(mapsq_ctx *ctx) {
+  if (!ctx) return MAPSQ_E_INVALID;
+  resolve_pending(ctx);
+  ctx->kagg.clear();
+  ctx->korder.clear();
+  std::memset(&ctx->counters, 0, sizeof ctx->counters);
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_get_stats(mapsq_ctx *ctx, mapsq_stats *st) {
+  if (!ctx || !st) return MAPSQ_E_INVALID;
+  resolve_pending(ctx);
+  *st = ctx->counters;
+  st->nkernels = 0;
+  for (const auto &name : ctx->korder) {
+    if (st->nkernels >= MAPSQ_MAX_KSTATS) break;
+    mapsq_kernel_stat &k = st->kernel[st->nkernels++];
+    std::memset(&k, 0, sizeof k);
+    std::strncpy(k.name, name.c_str(), sizeof k.name - 1);
+    const KAgg &a = ctx->kagg[name];
+    k.launches = a.launches;
+    k.total_ms = a.ms;
+    k.algo_bytes = a.bytes;
+  }
+  return MAPSQ_OK;
+}

@@ -1,0 +1,247 @@
+// internal.cuh — shared internals of libmapsq: context, device helpers, kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "mapsq.h"
+
+#define MAPSQ_API extern "C" __attribute__((visibility("default")))
+
+namespace mapsq {
+
+constexpr int kRadix = 256;          // 8-bit digits (MAPSQ_RADIX_BITS)
+constexpr int kSortThreads = 256;    // one thread per digit in the look-back
+constexpr int kSortItems = 16;       // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxPasses = 8;        // 64 key bits / 8
+
+// Look-back status words: [63:62] flag, [61:0] count.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// ---------------------------------------------------------------- context
+struct PendingTiming {
+  std::string name;
+  cudaEvent_t ev0, ev1;
+  uint64_t bytes;
+};
+struct KAgg {
+  uint64_t launches = 0;
+  double ms = 0;
+  uint64_t bytes = 0;
+};
+
+}  // namespace mapsq
+
+struct mapsq_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t l2_bytes = 0;
+  mapsq_allocator alloc{};
+  bool custom_alloc = false;
+  std::string err;
+  bool cuda_broken = false;
+  bool profiling = false;
+  std::vector<mapsq::PendingTiming> pending;
+  std::vector<cudaEvent_t> free_events;
+  std::map<std::string, mapsq::KAgg> kagg;
+  std::vector<std::string> korder;
+  mapsq_stats counters{};
+  uint64_t *pinned = nullptr;  // small pinned host buffer for the blocking size reads
+  size_t pinned_words = 0;
+};
+
+namespace mapsq {
+
+// ---------------------------------------------------------------- host helpers
+mapsq_status set_error(mapsq_ctx *ctx, mapsq_status st, const std::string &msg);
+mapsq_status cuda_check(mapsq_ctx *ctx, cudaError_t e, const char *what);
+void *dalloc(mapsq_ctx *ctx, size_t bytes, cudaStream_t s);
+void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s);
+
+// Scratch allocations freed (stream ordered) when the guard leaves scope.
+struct Scratch {
+  mapsq_ctx *ctx;
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  Scratch(mapsq_ctx *c, cudaStream_t st) : ctx(c), s(st) {}
+  ~Scratch() {
+    for (void *p : ptrs) dfree(ctx, p, s);
+  }
+  template <typename T>
+  T *get(size_t count) {
+    void *p = dalloc(ctx, count * sizeof(T) + 16, s);
+    if (p) ptrs.push_back(p);
+    return static_cast<T *>(p);
+  }
+  void release(void *p) {
+    for (auto &q : ptrs)
+      if (q == p) {
+        dfree(ctx, q, s);
+        q = nullptr;
+      }
+  }
+};
+
+// Launch bracket: counts the launch and, while profiling, records events around it.
+struct KTimer {
+  mapsq_ctx *ctx;
+  cudaStream_t s;
+  PendingTiming t;
+  bool on;
+  KTimer(mapsq_ctx *c, cudaStream_t st, const char *name, uint64_t bytes, int nlaunch = 1);
+  ~KTimer();
+};
+
+inline uint32_t bits_for(uint64_t range_max) {  // bits needed to represent 0..range_max
+  uint32_t b = 0;
+  while (b < 64 && (range_max >> b) != 0) b++;
+  return b;
+}
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ void st_cs_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cs_v4(uint32_t *p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- launchers (kernels/*.cu)
+struct ScanPat {
+  uint32_t const_mask;   // bit j: position j is a constant
+  uint32_t id[3];
+  uint32_t eq_mask;      // bit 0: s==p, bit 1: s==o, bit 2: p==o required
+  uint32_t ncols;
+  uint32_t src[3];       // output column c takes position src[c]
+};
+struct ScanArgs {
+  int k;
+  ScanPat pat[MAPSQ_MAX_PATTERNS];
+  uint32_t need_count;   // positions (bit j) the predicate pass must read
+  uint32_t need_write;   // positions the gather pass must read
+};
+constexpr int kScanThreads = 256;
+constexpr int kScanWordsPerWarp = 32;                     // 32 mask words of 32 triples
+constexpr uint64_t kScanTile = 8ull * kScanWordsPerWarp * 32;  // 8192 triples per CTA tile
+
+void launch_scan_count(const mapsq_triples &T, const ScanArgs &a, uint32_t *masks,
+                       uint64_t mask_words, uint32_t *tile_counts, uint64_t ntiles,
+                       cudaStream_t s);
+struct ScanOut {
+  uint32_t *col[MAPSQ_MAX_PATTERNS * 3];  // pattern j, column c -> col[j * 3 + c]
+};
+void launch_scan_write(const mapsq_triples &T, const ScanArgs &a, const uint32_t *masks,
+                       uint64_t mask_words, const uint64_t *tile_off, uint64_t ntiles,
+                       const ScanOut &out, uint32_t *bmin, uint32_t *bmax, cudaStream_t s);
+
+// exclusive scan of u32 / u64 counts into u64 offsets (3-phase reduce-then-scan);
+// writes the total to *total_dev.  `tmp` needs scan_tmp_words(n) u64.
+uint64_t scan_tmp_words(uint64_t n);
+int launch_exclusive_scan_u32(const uint32_t *in, uint64_t *out, uint64_t n, uint64_t *tmp,
+                              uint64_t *total_dev, cudaStream_t s);
+int launch_exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp,
+                              uint64_t *total_dev, cudaStream_t s);
+int launch_exclusive_scan_u64_dev(const uint64_t *in, uint64_t *out, const uint64_t *n_dev,
+                                  uint64_t cap, uint64_t *tmp, uint64_t *total_dev,
+                                  cudaStream_t s);
+// exclusive scan over kMaxPasses x 256 digit histograms (in place, one block per pass)
+void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s);
+
+struct PackArgs {
+  uint32_t nkey;
+  const uint32_t *key1[MAPSQ_MAX_COLS];
+  const uint32_t *key2[MAPSQ_MAX_COLS];
+  uint32_t lo[MAPSQ_MAX_COLS];
+  uint32_t shift[MAPSQ_MAX_COLS];
+  uint64_t n1, n2;
+  uint32_t ib;
+  uint32_t bit_lo;   // first sorted bit (ib for P64, 0 for KV)
+  uint32_t passes;
+  uint32_t last_mask;  // digit mask of the last pass ((1 << bits) - 1)
+  uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
+};
+// Map (K2): pack words (or KV pairs) and build the digit histograms of every pass.
+void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32_t *hist,
+                      cudaStream_t s);
+// Histograms of existing keys (for mapsq_sort_words on caller data).
+void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
+                     uint32_t last_bits, uint32_t *hist, cudaStream_t s);
+// One onesweep digit pass (K3).
+void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
+                       uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
+                       uint64_t *status, uint32_t *tile_counter, cudaStream_t s);
+
+// ReduceDuplicate (K4): groups present on both sides, in key order.
+struct GroupOut {
+  uint32_t *start, *split, *end;
+  uint64_t *cnt;
+};
+void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint32_t *vals,
+                        uint64_t n, uint64_t n1, uint32_t ib, GroupOut g, uint64_t *status,
+                        uint32_t *tile_counter, uint64_t *ngroups_dev, cudaStream_t s);
+
+struct ExpandArgs {
+  const uint64_t *words;   // P64 sorted words (or nullptr)
+  const uint64_t *keys;    // KV sorted key' (or nullptr)
+  const uint32_t *vals;    // KV sorted rowids
+  uint64_t n1;
+  uint32_t ib;
+  const uint32_t *gstart, *gsplit, *gend;
+  const uint64_t *goff;
+  uint64_t ngroups;
+  uint64_t m;
+  uint32_t nkey;
+  uint32_t key_lo[MAPSQ_MAX_COLS], key_shift[MAPSQ_MAX_COLS], key_mask[MAPSQ_MAX_COLS];
+  uint32_t nrest1, nrest2;
+  const uint32_t *rest1[MAPSQ_MAX_COLS];
+  const uint32_t *rest2[MAPSQ_MAX_COLS];
+  uint32_t *out[MAPSQ_MAX_COLS];  // nkey + nrest1 + nrest2 columns
+};
+void launch_expand(const ExpandArgs &a, cudaStream_t s);
+uint64_t find_groups_tiles(uint64_t n);
+
+void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,
+                   cudaStream_t s);
+
+struct PartArgs {
+  uint32_t nkey;
+  const uint32_t *key[MAPSQ_MAX_COLS];
+  uint32_t ncols;
+  const uint32_t *in[MAPSQ_MAX_COLS];
+  uint32_t *out[MAPSQ_MAX_COLS];
+  uint64_t n;
+  uint32_t nparts;
+};
+void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntiles,
+                           cudaStream_t s);
+void launch_partition_scatter(const PartArgs &a, const uint64_t *tile_off, uint64_t ntiles,
+                              cudaStream_t s);
+constexpr int kPartThreads = 256;
+constexpr int kPartItems = 16;
+constexpr uint64_t kPartTile = kPartThreads * kPartItems;
+constexpr int kMaxParts = 64;
+
+}  // namespace mapsq

@@ -1,0 +1,278 @@
+// radix.cu — K2 (Map: key-label packing + upfront digit histograms) and K3 (Sort: one-sweep
+// LSD radix digit pass with decoupled look-back), SURVEY §8 rows a3-a4.
+//
+// Map (Alg. 1 l.1-4, "split and emit intermediate"): each row of Tp1 becomes
+// the word key'<<ib | r (label LEFT) and each row of Tp2 the word key'<<ib | (n1 + r) (label
+// RIGHT): the label is the bit "rowid >= n1" (reading R1: LEFT = Tp1).
+// Sort (Alg. 1 l.5, "sort intermediates"): a stable LSD radix sort over only the kb
+// key bits.  Because the low ib bits already hold (label, rowid) in ascending order, stability
+// yields the total order (key', LEFT before RIGHT, rowid) — the sorted array is unique.
+//
+// The digit pass is a one-sweep design: tiles are claimed in order through an atomic counter,
+// ranked in shared memory with warp match-any multisplit, and their global digit offsets are
+// resolved by decoupled look-back over per-(tile, digit) status words; all P passes' global
+// digit offsets come from ONE upfront histogram fused into the Map kernel.
+#include "internal.cuh"
+
+namespace mapsq {
+namespace {
+
+constexpr int kWarps = kSortThreads / 32;
+constexpr int kHistThreads = 256;
+constexpr int kHistItems = 16;
+
+template <bool KV>
+__global__ void __launch_bounds__(kHistThreads)
+pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__restrict__ vals,
+                 uint32_t *__restrict__ hist) {
+  __shared__ uint32_t s_hist[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kHistThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t n = a.n1 + a.n2;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kHistThreads; i0 < n; i0 += stride) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool in = i < n;
+    uint64_t key = 0;
+    if (in) {
+      const bool left = i < a.n1;
+      const uint64_t r = left ? i : i - a.n1;
+      for (uint32_t c = 0; c < a.nkey; c++) {
+        const uint32_t v = left ? __ldcs(a.key1[c] + r) : __ldcs(a.key2[c] + r);
+        key |= (uint64_t)(v - a.lo[c]) << a.shift[c];
+      }
+      if (KV) {
+        words[i] = key;
+        vals[i] = (uint32_t)i;
+      } else {
+        key = (key << a.ib) | i;
+        words[i] = key;
+      }
+    }
+    for (uint32_t p = 0; p < a.passes; p++) {
+      const uint32_t d = (uint32_t)(key >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
+      const uint32_t peers = __match_any_sync(0xffffffffu, in ? d : 0x100u);
+      if (in && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[p][d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)a.passes * kRadix; i += kHistThreads) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+__global__ void __launch_bounds__(kHistThreads)
+key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
+                uint32_t last_mask, uint32_t *__restrict__ hist) {
+  __shared__ uint32_t s_hist[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kHistThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kHistThreads; i0 < n; i0 += stride) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool in = i < n;
+    const uint64_t key = in ? keys[i] : 0;
+    for (uint32_t p = 0; p < passes; p++) {
+      const uint32_t d = (uint32_t)(key >> (bit_lo + 8 * p)) & (p + 1 == passes ? last_mask : 0xffu);
+      const uint32_t peers = __match_any_sync(0xffffffffu, in ? d : 0x100u);
+      if (in && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[p][d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)passes * kRadix; i += kHistThreads) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+__global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
+  __shared__ uint32_t s_w[kRadix / 32];
+  uint32_t *h = hist + (uint64_t)blockIdx.x * kRadix;
+  const uint32_t v = h[threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  uint32_t pre = 0;
+  for (int w = 0; w < warp; w++) pre += s_w[w];
+  h[threadIdx.x] = pre + x - v;
+}
+
+// One stable digit pass.  Tile = kSortThreads x kSortItems keys; warp w owns the contiguous
+// slice [w*32*ITEMS, (w+1)*32*ITEMS) of its tile and reads it item-major (item it, lane l ->
+// slice[it*32 + l]) so every load is a coalesced 256 B row.
+template <bool KV>
+__global__ void __launch_bounds__(kSortThreads, 2)
+radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
+                  const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
+                  uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
+                  uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(smem_raw + kSortTile * sizeof(uint64_t));
+  __shared__ uint32_t s_warp_hist[kWarps][kRadix];
+  __shared__ uint32_t s_digit_start[kRadix];
+  __shared__ uint64_t s_global_base[kRadix];
+  __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_tile;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t tile_base = tile * kSortTile;
+  const uint64_t wbase = tile_base + (uint64_t)warp * 32 * kSortItems;
+  const uint32_t dmask = (1u << bits) - 1u;
+
+  uint64_t k[kSortItems];
+  uint32_t v[kSortItems];
+  uint32_t r[kSortItems];
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) {
+    const uint64_t i = wbase + it * 32 + lane;
+    k[it] = i < n ? __ldcs(kin + i) : ~0ull;
+    if (KV) v[it] = i < n ? __ldcs(vin + i) : 0u;
+  }
+  // warp-level multisplit: rank of each key among equal digits of this warp's slice
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) {
+    const uint64_t i = wbase + it * 32 + lane;
+    const bool in = i < n;
+    const uint32_t d = in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (in && lane == leader) {
+      base = s_warp_hist[warp][d];
+      s_warp_hist[warp][d] = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    r[it] = base + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // thread d: exclusive prefix of digit d across warps, tile total, look-back
+  const uint32_t d = tid;
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; w++) {
+    const uint32_t c = s_warp_hist[w][d];
+    s_warp_hist[w][d] = total;
+    total += c;
+  }
+  uint64_t *my_status = status + tile * kRadix + d;
+  uint64_t excl = 0;
+  if (tile == 0) {
+    st_relaxed_u64(my_status, kFlagInc | total);
+  } else {
+    st_relaxed_u64(my_status, kFlagAgg | total);
+    int64_t t = (int64_t)tile - 1;
+    while (true) {
+      const uint64_t sv = ld_relaxed_u64(status + (uint64_t)t * kRadix + d);
+      const uint64_t flag = sv & ~kValMask;
+      if (flag == 0) continue;
+      excl += sv & kValMask;
+      if (flag == kFlagInc) break;
+      t--;
+    }
+    st_relaxed_u64(my_status, kFlagInc | (excl + total));
+  }
+  // tile-local start of each digit: exclusive block scan of `total` over digits
+  uint32_t x = total;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t pre = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; w++)
+    if (w < warp) pre += s_wsum[w];
+  const uint32_t dstart = pre + x - total;
+  s_digit_start[d] = dstart;
+  s_global_base[d] = (uint64_t)hist_pass[d] + excl - dstart;
+  __syncthreads();
+
+  // place keys at their tile-local sorted slot
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) {
+    const uint64_t i = wbase + it * 32 + lane;
+    if (i < n) {
+      const uint32_t dd = (uint32_t)(k[it] >> shift) & dmask;
+      const uint32_t slot = s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
+      s_keys[slot] = k[it];
+      if (KV) s_vals[slot] = v[it];
+    }
+  }
+  __syncthreads();
+  const uint32_t tile_n = (uint32_t)(n - tile_base < (uint64_t)kSortTile ? n - tile_base : (uint64_t)kSortTile);
+  for (uint32_t i = tid; i < tile_n; i += kSortThreads) {
+    const uint64_t key = s_keys[i];
+    const uint32_t dd = (uint32_t)(key >> shift) & dmask;
+    const uint64_t pos = s_global_base[dd] + i;
+    kout[pos] = key;
+    if (KV) vout[pos] = s_vals[i];
+  }
+}
+
+}  // namespace
+
+static int grid_for(uint64_t n, int per_block) {
+  const uint64_t b = ceil_div(n, per_block);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(b, 148 * 8));
+}
+
+void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32_t *hist,
+                      cudaStream_t s) {
+  const uint64_t n = a.n1 + a.n2;
+  const int g = grid_for(n, kHistThreads * kHistItems);
+  if (a.kv)
+    pack_hist_kernel<true><<<g, kHistThreads, 0, s>>>(a, words, vals, hist);
+  else
+    pack_hist_kernel<false><<<g, kHistThreads, 0, s>>>(a, words, vals, hist);
+}
+
+void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
+                     uint32_t last_bits, uint32_t *hist, cudaStream_t s) {
+  const int g = grid_for(n, kHistThreads * kHistItems);
+  key_hist_kernel<<<g, kHistThreads, 0, s>>>(keys, n, bit_lo, passes, (1u << last_bits) - 1u, hist);
+}
+
+void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s) {
+  hist_scan_kernel<<<passes, kRadix, 0, s>>>(hist);
+}
+
+void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
+                       uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
+                       uint64_t *status, uint32_t *tile_counter, cudaStream_t s) {
+  const uint64_t ntiles = ceil_div(n, kSortTile);
+  if (vin) {
+    const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(radix_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = true;
+    }
+    radix_pass_kernel<true><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
+        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter);
+  } else {
+    const size_t smem = kSortTile * sizeof(uint64_t);
+    radix_pass_kernel<false><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
+        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter);
+  }
+}
+
+}  // namespace mapsq

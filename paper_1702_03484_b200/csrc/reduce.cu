@@ -1,0 +1,279 @@
+// reduce.cu — ReduceDuplicate (Alg. 1 l.6-11), SURVEY §8 rows a5-a6.
+//
+// K4 find_groups: in the sorted words, a key present on BOTH sides has exactly one position
+// where a LEFT word is followed by a RIGHT word of the same key (the "split"; LEFT precedes
+// RIGHT inside a key because the label is the high part of the rowid field).  Every such split
+// is one output group — the flag "contributes to reduce unnecessary computation": keys
+// with one label only produce nothing and are never visited again.  The splits are compacted in
+// key order with a single-pass decoupled look-back; the thread owning a split gallops outwards
+// to the run's ends and stores (start, split, end) and nL * nR.
+// K6 expand: "GPU's SIMD architectures contribute to accelerate cartesian product in parallel"
+// (P:149).  Output-row parallel, so skewed keys are load balanced: every thread owns 4
+// consecutive output rows, finds its group by a binary search bracketed per CTA, and writes
+// (key columns decoded from the word, Tp1 non-shared, Tp2 non-shared) in (key, left rowid,
+// right rowid) order with 16 B streaming stores.
+#include "internal.cuh"
+
+namespace mapsq {
+namespace {
+
+constexpr int kGThreads = 256;
+constexpr int kGItems = 16;
+constexpr uint64_t kGTile = kGThreads * kGItems;
+constexpr int kGWarps = kGThreads / 32;
+
+struct WordView {
+  const uint64_t *words, *keys;
+  const uint32_t *vals;
+  uint64_t n1;
+  uint32_t ib;
+  uint64_t idx_mask;
+  __device__ __forceinline__ uint64_t key(uint64_t i) const {
+    return words ? (words[i] >> ib) : keys[i];
+  }
+  __device__ __forceinline__ bool right(uint64_t i) const {
+    return (words ? (words[i] & idx_mask) : (uint64_t)vals[i]) >= n1;
+  }
+};
+
+__global__ void __launch_bounds__(kGThreads)
+find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restrict__ status,
+                   uint32_t *__restrict__ tile_counter, uint64_t *__restrict__ ngroups_dev) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_cnt[kGItems][kGWarps];
+  __shared__ uint64_t s_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t base = tile * kGTile;
+  uint32_t ball[kGItems];
+  // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane
+#pragma unroll
+  for (int it = 0; it < kGItems; it++) {
+    const uint64_t i = base + (uint64_t)it * kGThreads + tid;
+    bool split = false;
+    if (i > 0 && i < n) {
+      // split: word i is RIGHT, word i-1 is LEFT, same key
+      split = W.right(i) && !W.right(i - 1) && W.key(i) == W.key(i - 1);
+    }
+    ball[it] = __ballot_sync(0xffffffffu, split);
+    if (lane == 0) s_cnt[it][warp] = __popc(ball[it]);
+  }
+  __syncthreads();
+  // exclusive scan of the (it, warp) counts in element order; thread 0 does the look-back
+  if (tid < 32) {
+    uint32_t v[kGItems * kGWarps / 32];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kGItems * kGWarps / 32; q++) {
+      v[q] = (&s_cnt[0][0])[tid * (kGItems * kGWarps / 32) + q];
+      sum += v[q];
+    }
+    uint32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+    uint32_t run = x - sum;
+#pragma unroll
+    for (int q = 0; q < kGItems * kGWarps / 32; q++) {
+      (&s_cnt[0][0])[tid * (kGItems * kGWarps / 32) + q] = run;
+      run += v[q];
+    }
+    if (tid == 0) {
+      uint64_t excl = 0;
+      if (tile == 0) {
+        st_relaxed_u64(status, kFlagInc | total);
+      } else {
+        st_relaxed_u64(status + tile, kFlagAgg | total);
+        int64_t t = (int64_t)tile - 1;
+        while (true) {
+          const uint64_t sv = ld_relaxed_u64(status + t);
+          const uint64_t flag = sv & ~kValMask;
+          if (flag == 0) continue;
+          excl += sv & kValMask;
+          if (flag == kFlagInc) break;
+          t--;
+        }
+        st_relaxed_u64(status + tile, kFlagInc | (excl + total));
+      }
+      s_base = excl;
+      if (tile == gridDim.x - 1) *ngroups_dev = excl + total;
+    }
+  }
+  __syncthreads();
+  const uint64_t out_base = s_base;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll 1
+  for (int it = 0; it < kGItems; it++) {
+    if (!((ball[it] >> lane) & 1u)) continue;
+    const uint64_t i = base + (uint64_t)it * kGThreads + tid;
+    const uint64_t pos = out_base + s_cnt[it][warp] + __popc(ball[it] & lt);
+    const uint64_t k = W.key(i);
+    // gallop back from i-1 to the first element of the key's run
+    int64_t lo = (int64_t)i - 1;  // key(lo) == k
+    int64_t step = 1;
+    while (true) {
+      const int64_t c = lo - step;
+      if (c < 0 || W.key((uint64_t)c) != k) break;
+      lo = c;
+      step <<= 1;
+    }
+    int64_t L = (lo - step > -1) ? lo - step : -1, R = lo;  // key(L) != k (or L = -1), key(R) == k
+    while (R - L > 1) {
+      const int64_t m = (L + R) >> 1;
+      if (W.key((uint64_t)m) == k) R = m; else L = m;
+    }
+    const uint64_t start = (uint64_t)R;
+    // gallop forward from i to one past the run's last element
+    int64_t hi = (int64_t)i;  // key(hi) == k
+    step = 1;
+    while (true) {
+      const int64_t c = hi + step;
+      if (c >= (int64_t)n || W.key((uint64_t)c) != k) break;
+      hi = c;
+      step <<= 1;
+    }
+    L = hi;
+    R = (hi + step < (int64_t)n) ? hi + step : (int64_t)n;  // key(L) == k, key(R) != k (or R = n)
+    while (R - L > 1) {
+      const int64_t m = (L + R) >> 1;
+      if (W.key((uint64_t)m) == k) L = m; else R = m;
+    }
+    const uint64_t end = (uint64_t)R;
+    g.start[pos] = (uint32_t)start;
+    g.split[pos] = (uint32_t)i;
+    g.end[pos] = (uint32_t)end;
+    g.cnt[pos] = (i - start) * (end - i);
+  }
+}
+
+// ------------------------------------------------------------------------------ expand (K6)
+constexpr int kEThreads = 256;
+constexpr int kERows = 4;
+constexpr uint64_t kETile = kEThreads * kERows;
+
+__device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, uint64_t hi,
+                                             uint64_t r) {
+  // largest g in [lo, hi] with off[g] <= r  (off strictly increasing, off[lo] <= r)
+  while (lo < hi) {
+    const uint64_t m = (lo + hi + 1) >> 1;
+    if (off[m] <= r) lo = m; else hi = m - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kEThreads)
+expand_kernel(const ExpandArgs a) {
+  __shared__ const uint32_t *s_src[MAPSQ_MAX_COLS];
+  __shared__ uint32_t *s_dst[MAPSQ_MAX_COLS];
+  __shared__ uint64_t s_g[2];
+  const int tid = threadIdx.x;
+  const uint32_t nout = a.nkey + a.nrest1 + a.nrest2;
+  if (tid < MAPSQ_MAX_COLS) {
+    s_dst[tid] = a.out[tid];
+    const uint32_t c = tid;
+    s_src[tid] = c < a.nkey ? nullptr
+               : (c < a.nkey + a.nrest1 ? a.rest1[c - a.nkey] : a.rest2[c - a.nkey - a.nrest1]);
+  }
+  const uint64_t t0 = (uint64_t)blockIdx.x * kETile;
+  const uint64_t t1 = (t0 + kETile < a.m ? t0 + kETile : a.m) - 1;
+  if (tid < 2) s_g[tid] = group_of(a.goff, 0, a.ngroups - 1, tid == 0 ? t0 : t1);
+  __syncthreads();
+  const uint64_t r0 = t0 + (uint64_t)tid * kERows;
+  if (r0 >= a.m) return;
+  uint64_t g = group_of(a.goff, s_g[0], s_g[1], r0);
+  const uint64_t idx_mask = (a.ib >= 64) ? ~0ull : ((1ull << a.ib) - 1);
+
+  uint64_t lkey[kERows];
+  uint32_t lidx[kERows], ridx[kERows];
+  int nrow = 0;
+  uint64_t gbeg = a.goff[g];
+  uint64_t gend = (g + 1 < a.ngroups) ? a.goff[g + 1] : a.m;
+  uint32_t start = a.gstart[g], split = a.gsplit[g], end = a.gend[g];
+  uint64_t nR = end - split;
+  uint64_t local = r0 - gbeg;
+  uint64_t li = local / nR, ri = local - li * nR;
+#pragma unroll
+  for (int j = 0; j < kERows; j++) {
+    const uint64_t r = r0 + j;
+    if (r >= a.m) break;
+    if (r >= gend) {  // next group (groups are never empty)
+      g++;
+      gbeg = gend;
+      gend = (g + 1 < a.ngroups) ? a.goff[g + 1] : a.m;
+      start = a.gstart[g];
+      split = a.gsplit[g];
+      end = a.gend[g];
+      nR = end - split;
+      li = 0;
+      ri = 0;
+    }
+    const uint64_t lpos = start + li, rpos = split + ri;
+    if (a.words) {
+      const uint64_t lw = a.words[lpos], rw = a.words[rpos];
+      lkey[j] = lw >> a.ib;
+      lidx[j] = (uint32_t)(lw & idx_mask);
+      ridx[j] = (uint32_t)((rw & idx_mask) - a.n1);
+    } else {
+      lkey[j] = a.keys[lpos];
+      lidx[j] = a.vals[lpos];
+      ridx[j] = a.vals[rpos] - (uint32_t)a.n1;
+    }
+    nrow++;
+    if (++ri == nR) {
+      ri = 0;
+      li++;
+    }
+  }
+  const bool full = (nrow == kERows);
+  for (uint32_t c = 0; c < nout; c++) {
+    uint32_t v[kERows];
+    if (c < a.nkey) {
+      const uint32_t sh = a.key_shift[c], mk = a.key_mask[c], lo = a.key_lo[c];
+#pragma unroll
+      for (int j = 0; j < kERows; j++) v[j] = (uint32_t)(lkey[j] >> sh & mk) + lo;
+    } else {
+      const uint32_t *src = s_src[c];
+      const bool left = c < a.nkey + a.nrest1;
+#pragma unroll
+      for (int j = 0; j < kERows; j++)
+        v[j] = (j < nrow) ? __ldg(src + (left ? lidx[j] : ridx[j])) : 0u;
+    }
+    uint32_t *dst = s_dst[c] + r0;
+    if (full) {
+      st_cs_v4(dst, make_uint4(v[0], v[1], v[2], v[3]));
+    } else {
+      for (int j = 0; j < nrow; j++) st_cs_u32(dst + j, v[j]);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint32_t *vals,
+                        uint64_t n, uint64_t n1, uint32_t ib, GroupOut g, uint64_t *status,
+                        uint32_t *tile_counter, uint64_t *ngroups_dev, cudaStream_t s) {
+  WordView W;
+  W.words = words;
+  W.keys = keys;
+  W.vals = vals;
+  W.n1 = n1;
+  W.ib = ib;
+  W.idx_mask = (ib >= 64) ? ~0ull : ((1ull << ib) - 1);
+  const uint64_t ntiles = ceil_div(n, kGTile);
+  find_groups_kernel<<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
+                                                            ngroups_dev);
+}
+
+uint64_t find_groups_tiles(uint64_t n) { return ceil_div(n, kGTile); }
+
+void launch_expand(const ExpandArgs &a, cudaStream_t s) {
+  if (a.m == 0) return;
+  const uint64_t nblocks = ceil_div(a.m, kETile);
+  expand_kernel<<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
+}
+
+}  // namespace mapsq

@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, element by element.
+
+Integer path, so the bar is bit-exact.  Because the GPU join emits rows in (key', tp1 row,
+tp2 row) order and the oracle's sort-merge tier emits (key tuple, A row, B row), single-GPU
+results are compared IN ORDER (stronger than the canonical-sort comparison), and canonically
+where only the multiset is defined."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import datagen  # noqa: E402
+import oracle  # noqa: E402
+import paper_1702_03484_b200 as mq  # noqa: E402
+from fixtures import config_expected_counts, config_query, load_table1  # noqa: E402
+
+V, C = "v", "c"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return mq.Context(0)
+
+
+def dev(a):
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).cuda()
+
+
+def dtable(vars_, rows):
+    rows = np.asarray(rows, np.uint32).reshape(-1, len(vars_))
+    return mq.DeviceTable.from_torch(vars_, [dev(rows[:, c]) for c in range(len(vars_))])
+
+
+def assert_same(gpu: mq.DeviceTable, ref: oracle.Table, ordered=True):
+    assert gpu.vars == ref.vars
+    got = gpu.to_numpy()
+    assert got.shape == ref.rows.shape
+    if ordered:
+        assert np.array_equal(got, ref.rows)
+    else:
+        assert np.array_equal(oracle.canonical_rows(got), oracle.canonical(ref).rows)
+
+
+# ------------------------------------------------------------------------- Table 1
+def test_table1_scan_join_query(ctx):
+    ids, T, sec = load_table1()
+    trip = tuple(dev(T[:, j]) for j in range(3))
+    P1 = ((V, 0), (C, ids["hasJob"]), (V, 1))
+    P2 = ((V, 1), (C, ids["workAt"]), (C, ids['"Hospital"']))
+    tp1, tp2 = ctx.scan_patterns(trip, [P1, P2])
+    assert_same(tp1, oracle.scan(*T.T, P1))
+    assert_same(tp2, oracle.scan(*T.T, P2))
+    rs = ctx.join(tp1, tp2)
+    assert_same(rs, oracle.join(oracle.scan(*T.T, P1), oracle.scan(*T.T, P2)))
+    assert sorted(rs.to_numpy().tolist()) == sorted(
+        [[ids[k], ids[v]] for k, v, _ in sec["rs"]])
+    q = ctx.query(trip, [P1, P2], [0])
+    assert sorted(q.to_numpy()[:, 0].tolist()) == sorted(ids[r[0]] for r in sec["select_person"])
+    vars_, rows = ctx.query_host(*[np.ascontiguousarray(T[:, j]) for j in range(3)], [P1, P2], [0])
+    assert vars_ == [0] and sorted(rows[:, 0].tolist()) == sorted(q.to_numpy()[:, 0].tolist())
+
+
+# ------------------------------------------------------------------------- random joins
+@pytest.mark.parametrize("domain", [1, 5, 50, 1000, 1 << 20, 1 << 32])
+def test_join_random_single_key(ctx, domain):
+    rng = np.random.default_rng(domain % 1000003)
+    sizes = [(0, 5), (5, 0), (1, 1), (7, 3), (300, 200), (4095, 4097), (5000, 9000)]
+    for n1, n2 in sizes:
+        A = np.stack([rng.integers(0, domain, n1, dtype=np.uint64),
+                      rng.integers(0, 1 << 32, n1, dtype=np.uint64)], 1).astype(np.uint32)
+        B = np.stack([rng.integers(0, 1 << 32, n2, dtype=np.uint64),
+                      rng.integers(0, domain, n2, dtype=np.uint64)], 1).astype(np.uint32)
+        ka, ca = np.unique(A[:, 0], return_counts=True)
+        kb, cb = np.unique(B[:, 1], return_counts=True)
+        _, ia, ib_ = np.intersect1d(ka, kb, return_indices=True)
+        if int((ca[ia].astype(np.int64) * cb[ib_]).sum()) > 3_000_000:
+            continue
+        ref = oracle.join(oracle.Table([3, 1], A), oracle.Table([2, 3], B))
+        got = ctx.join(dtable([3, 1], A), dtable([2, 3], B))
+        assert_same(got, ref)
+
+
+def test_join_many_random_cases(ctx):
+    rng = np.random.default_rng(1234)
+    for case in range(200):
+        n1, n2 = (int(x) for x in rng.integers(0, 400, 2))
+        dom = int(rng.choice([1, 3, 17, 400]))
+        w1, w2 = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        A = rng.integers(0, dom, (n1, w1)).astype(np.uint32)
+        B = rng.integers(0, dom, (n2, w2)).astype(np.uint32)
+        # variable ids: column 0 of each side shares var 0; random extra sharing of var 1
+        va = [0] + [10 + c for c in range(1, w1)]
+        vb = [20 + c for c in range(1, w2)] + [0]
+        if w1 > 1 and w2 > 1 and case % 3 == 0:
+            va[1], vb[0] = 1, 1
+        ta, tb = oracle.Table(va, A), oracle.Table(vb, B)
+        ref = oracle.join(ta, tb)
+        got = ctx.join(dtable(va, A), dtable(vb, B))
+        assert_same(got, ref)
+
+
+def test_join_composite_keys_and_kv_path(ctx):
+    rng = np.random.default_rng(7)
+    # two shared variables in different column orders (reading R5)
+    A = rng.integers(0, 6, (3000, 3)).astype(np.uint32)
+    B = rng.integers(0, 6, (2000, 2)).astype(np.uint32)
+    ref = oracle.join(oracle.Table([0, 2, 1], A), oracle.Table([2, 0], B))
+    assert_same(ctx.join(dtable([0, 2, 1], A), dtable([2, 0], B)), ref)
+    # full-range 32-bit composite keys: kb = 64 > 64 - ib -> KV path
+    base = rng.integers(0, 1 << 32, (500, 2), dtype=np.uint64).astype(np.uint32)
+    A = np.concatenate([base[rng.integers(0, 500, 4000)], rng.integers(0, 9, (4000, 1)).astype(np.uint32)], 1)
+    B = np.concatenate([base[rng.integers(0, 500, 3000)][:, ::-1], rng.integers(0, 9, (3000, 1)).astype(np.uint32)], 1)
+    B[:2, :2] = [[0, 0], [0xFFFFFFFF, 0xFFFFFFFF]]
+    ta, tb = oracle.Table([4, 5, 6], A), oracle.Table([5, 4, 7], np.ascontiguousarray(B))
+    got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
+    st = ctx.stats()
+    assert st["last_path"] == mq.PATH_KV
+    assert_same(got, oracle.join(ta, tb))
+    # three shared variables
+    A = rng.integers(0, 3, (2000, 4)).astype(np.uint32)
+    B = rng.integers(0, 3, (1500, 3)).astype(np.uint32)
+    ref = oracle.join(oracle.Table([0, 1, 2, 9], A), oracle.Table([2, 1, 0], B))
+    assert_same(ctx.join(dtable([0, 1, 2, 9], A), dtable([2, 1, 0], B)), ref)
+
+
+def test_join_skewed_hot_key_large_groups(ctx):
+    rng = np.random.default_rng(11)
+    # one hot key: 6000 x 700 = 4.2e6 output rows, plus a cold tail
+    A = np.stack([np.where(rng.random(20000) < 0.3, 77, rng.integers(0, 5000, 20000)),
+                  rng.integers(0, 1 << 30, 20000)], 1).astype(np.uint32)
+    B = np.stack([np.where(rng.random(15000) < 0.05, 77, rng.integers(0, 5000, 15000)),
+                  rng.integers(0, 1 << 30, 15000)], 1).astype(np.uint32)
+    ref = oracle.join(oracle.Table([0, 1], A), oracle.Table([0, 2], B))
+    got = ctx.join(dtable([0, 1], A), dtable([0, 2], B))
+    assert_same(got, ref)
+    L = np.bincount(A[:, 0], minlength=5001)
+    R = np.bincount(B[:, 0], minlength=5001)
+    assert got.nrows == int((L.astype(np.int64) * R).sum())
+
+
+def test_join_empty_and_disjoint(ctx):
+    A = np.array([[1, 2], [3, 4]], np.uint32)
+    B = np.array([[10, 5]], np.uint32)
+    got = ctx.join(dtable([0, 1], A), dtable([0, 2], B))
+    assert got.nrows == 0 and got.vars == [0, 1, 2]
+    got = ctx.join(dtable([0, 1], np.zeros((0, 2), np.uint32)), dtable([0, 2], B))
+    assert got.nrows == 0 and got.vars == [0, 1, 2]
+    with pytest.raises(mq.MapsqError) as e:
+        ctx.join(dtable([0], A[:, :1]), dtable([5], B[:, :1]))
+    assert e.value.status == "E_NO_SHARED"
+
+
+# ------------------------------------------------------------------------- phases
+def test_sort_words_equals_library_sort(ctx):
+    rng = np.random.default_rng(3)
+    for n in [1, 2, 100, 4095, 4096, 4097, 100_000, 1_000_003]:
+        # low bits ascending in input order (as the Map step builds them), random high bits
+        w = np.arange(n, dtype=np.uint64) | (rng.integers(0, 1 << 40, n, dtype=np.uint64) << np.uint64(22))
+        t = torch.from_numpy(w.view(np.int64)).cuda()
+        ctx.sort_words(t, 22, 62)
+        got = t.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, np.sort(w)), n   # words are unique -> the sorted array is unique
+
+
+def test_sort_pairs_stable(ctx):
+    rng = np.random.default_rng(4)
+    n = 300_001
+    k = rng.integers(0, 1 << 44, n, dtype=np.uint64)
+    k[rng.random(n) < 0.5] = 12345  # many equal keys: stability decides their order
+    v = np.arange(n, dtype=np.uint32)
+    tk, tv = torch.from_numpy(k.view(np.int64)).cuda(), torch.from_numpy(v.view(np.int32)).cuda()
+    ctx.sort_pairs(tk, tv, 0, 44)
+    order = np.argsort(k, kind="stable")
+    assert np.array_equal(tk.cpu().numpy().view(np.uint64), k[order])
+    assert np.array_equal(tv.cpu().numpy().view(np.uint32), v[order])
+
+
+def test_map_words_layout(ctx):
+    rng = np.random.default_rng(5)
+    A = rng.integers(100, 200, (1000, 2)).astype(np.uint32)
+    B = rng.integers(150, 260, (700, 1)).astype(np.uint32)
+    ta, tb = dtable([0, 1], A), dtable([0], B)
+    ctx.table_bounds(ta)
+    ctx.table_bounds(tb)
+    pl = mq.plan_join([0, 1], ta.bounds, 1000, [0], tb.bounds, 700)
+    words = torch.empty(1700, dtype=torch.int64, device="cuda")
+    ctx.map_words(ta, tb, pl, words)
+    got = words.cpu().numpy().view(np.uint64)
+    lo = min(A[:, 0].min(), B[:, 0].min())
+    keys = np.concatenate([A[:, 0], B[:, 0]]).astype(np.uint64) - np.uint64(lo)
+    want = (keys << np.uint64(pl.ib)) | np.arange(1700, dtype=np.uint64)  # LEFT rows 0..n1-1
+    assert np.array_equal(got, want)
+    assert pl.ib == 11 and (got[1000:] & np.uint64(2047) >= 1000).all()  # RIGHT label
+
+
+def test_reduce_groups_counts(ctx):
+    rng = np.random.default_rng(6)
+    n1, n2, ib = 30000, 20000, 16
+    kl, kr = rng.integers(0, 3000, n1), rng.integers(1000, 6000, n2)
+    keys = np.concatenate([kl, kr]).astype(np.uint64)
+    words = np.sort((keys << np.uint64(ib)) | np.arange(n1 + n2, dtype=np.uint64))
+    t = torch.from_numpy(words.view(np.int64)).cuda()
+    gs, gp, ge, go, total = ctx.reduce_groups(t, n1, n2, ib)
+    uk, Lc = np.unique(kl, return_counts=True)
+    Rc = np.bincount(kr, minlength=6000)[uk]
+    both = Rc > 0
+    assert total == int((Lc[both] * Rc[both]).sum())
+    assert len(gs) == int(both.sum())
+    cnt = (gp.cpu().numpy() - gs.cpu().numpy()).astype(np.int64) * (ge.cpu().numpy() - gp.cpu().numpy())
+    assert np.array_equal(cnt, (Lc[both] * Rc[both]))
+    assert np.array_equal(go.cpu().numpy(), np.concatenate([[0], np.cumsum(cnt)[:-1]]))
+    wk = words >> np.uint64(ib)
+    assert np.array_equal(wk[gs.cpu().numpy().astype(np.int64)], uk[both])
+
+
+# ------------------------------------------------------------------------- scan + query
+def test_scan_random_patterns(ctx):
+    rng = np.random.default_rng(8)
+    for n in [1, 31, 33, 8191, 8193, 50_000]:
+        T = rng.integers(0, 6, (n, 3)).astype(np.uint32)
+        trip = tuple(dev(T[:, j]) for j in range(3))
+        pats = [((V, 0), (C, 3), (V, 1)), ((V, 0), (C, 3), (C, 5)), ((C, 2), (V, 4), (V, 1)),
+                ((V, 0), (V, 1), (V, 2)), ((V, 0), (C, 1), (V, 0)), ((V, 2), (V, 2), (V, 2)),
+                ((V, 0), (C, 99), (V, 1))]
+        got = ctx.scan_patterns(trip, pats)
+        for g, p in zip(got, pats):
+            ref = oracle.scan(*T.T, p)
+            assert_same(g, ref)
+            if ref.nrows:
+                assert g.bounds == [(int(ref.rows[:, c].min()), int(ref.rows[:, c].max()))
+                                    for c in range(len(ref.vars))]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_query_configs_small_scale(ctx, cfg):
+    s, p, o, st = datagen.lubm(3, 0, 2)
+    trip = (dev(s), dev(p), dev(o))
+    pats = config_query(cfg)
+    ref = oracle.query(s, p, o, pats)
+    got = ctx.query(trip, pats)
+    assert got.nrows == config_expected_counts(cfg, st)[-1]
+    assert_same(got, ref)
+    # chained joins one by one agree with the generator's bookkeeping
+    tabs = ctx.scan_patterns(trip, pats)
+    acc = tabs[0]
+    for i, t in enumerate(tabs[1:]):
+        acc = ctx.join(acc, t)
+        assert acc.nrows == config_expected_counts(cfg, st)[i]
+
+
+def test_query_projection_and_errors(ctx):
+    s, p, o, _ = datagen.lubm(1)
+    trip = (dev(s), dev(p), dev(o))
+    pats = config_query("C5")
+    got = ctx.query(trip, pats, [2, 0])
+    ref = oracle.query(s, p, o, pats, [2, 0])
+    assert_same(got, ref)
+    with pytest.raises(mq.MapsqError) as e:
+        ctx.query(trip, [((V, 0), (C, 5), (V, 1)), ((V, 2), (C, 5), (V, 3))])
+    assert e.value.status == "E_NO_SHARED"
+
+
+def test_partition_hash_and_stability(ctx):
+    rng = np.random.default_rng(9)
+    A = rng.integers(0, 1 << 20, (50_000, 3)).astype(np.uint32)
+    for G in (1, 2, 3, 8):
+        part, counts = ctx.partition(dtable([0, 1, 2], A), [0, 2], G)
+        got = part.to_numpy()
+
+        def fmix32(h):
+            h = h ^ (h >> np.uint64(16)); h = (h * np.uint64(0x85EBCA6B)) & np.uint64(0xFFFFFFFF)
+            h = h ^ (h >> np.uint64(13)); h = (h * np.uint64(0xC2B2AE35)) & np.uint64(0xFFFFFFFF)
+            return h ^ (h >> np.uint64(16))
+        h = np.full(len(A), 0x811C9DC5, np.uint64)
+        for c in (0, 2):
+            h = ((h ^ A[:, c].astype(np.uint64)) * np.uint64(0x01000193)) & np.uint64(0xFFFFFFFF)
+        dest = fmix32(h) % np.uint64(G)
+        assert counts == np.bincount(dest.astype(np.int64), minlength=G).tolist()
+        want = A[np.argsort(dest, kind="stable")]
+        assert np.array_equal(got, want)
+
+
+def test_stats_and_launch_count(ctx):
+    ctx.stats_reset()
+    ctx.set_profiling(True)
+    A = np.stack([np.arange(10000) % 97, np.arange(10000)], 1).astype(np.uint32)
+    ctx.join(dtable([0, 1], A), dtable([0, 2], A))
+    st = ctx.stats()
+    ctx.set_profiling(False)
+    assert st["launches"] >= 6 and st["joins"] == 1
+    assert "radix_pass" in st["kernels"] and st["kernels"]["radix_pass"]["ms"] > 0
