@@ -181,17 +181,18 @@ mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table *tp2,
 mapsq_status mapsq_query(mapsq_ctx *ctx, const mapsq_triples *triples,
                          const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
                          mapsq_table *rs, void *stream);
-/* End-to-end variant over HOST buffers: s/p/o are host pointers (pinned memory recommended);
- * the triples are streamed to the device in chunks overlapped with the scan, the query runs
- * as mapsq_query, and the result columns are copied to host memory the library allocates
- * with malloc.  On return (synchronous) host_rows receives the row count and host_cols[c] a
- * malloc'd array of that many IDs for variable out_var[c]; free each with mapsq_host_free. */
+/* End-to-end variant over HOST buffers: s/p/o are host pointers (pinned memory recommended)
+ * holding n triples.  The triples are copied to the device, the query runs as mapsq_query, and
+ * the result columns are copied back into a pinned result arena owned by the context.  On
+ * return (synchronous) *host_rows is the row count, *out_ncols the width, out_var[c] the
+ * variable of column c and host_cols[c] a pointer to that column's *host_rows IDs inside the
+ * arena.  The arena (and every host_cols pointer) stays valid until the next
+ * mapsq_query_host on this context or mapsq_destroy; the caller never frees it. */
 mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host,
                               const uint32_t *p_host, const uint32_t *o_host,
                               const mapsq_pattern *pats, int npats, const int32_t *proj,
                               int nproj, uint64_t *host_rows, uint32_t *out_ncols,
                               int32_t *out_var, uint32_t **host_cols, void *stream);
-void mapsq_host_free(void *p);
 
 /* ---- phase entry points (for phase-level parity tests; the same kernels mapsq_join runs) ----
  * Map (K2, row a3): words[r] = key'(tp1 row r) << ib | r and words[n1 + r] = key'(tp2 row r)

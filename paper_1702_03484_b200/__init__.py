@@ -104,7 +104,6 @@ def lib():
             "mapsq_query_host": (st, [vp, u64, vp, vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
                                       ctypes.c_int, ctypes.POINTER(u64), ctypes.POINTER(u32),
                                       ctypes.POINTER(i32), ctypes.POINTER(vp), vp]),
-            "mapsq_host_free": (None, [vp]),
             "mapsq_map_words": (st, [vp, PT, PT, ctypes.POINTER(JoinPlan), vp, vp]),
             "mapsq_sort_words": (st, [vp, vp, u64, u32, u32, vp]),
             "mapsq_sort_pairs": (st, [vp, vp, vp, u64, u32, u32, vp]),
@@ -328,8 +327,10 @@ class Context:
                                       ctypes.byref(out), _stream(stream)))
         return _wrap(self, out)
 
-    def query_host(self, s, p, o, patterns, proj=None, stream=None):
-        """End to end over host (numpy, ideally pinned) triples; returns (vars, rows ndarray)."""
+    def query_host(self, s, p, o, patterns, proj=None, stream=None, copy=False):
+        """End to end over host (numpy, ideally pinned) triples: returns (vars, rows) where rows
+        is an (nrows, ncols) view of the context's pinned result arena (valid until the next
+        query_host on this context) or, with copy=True, an independent array."""
         import numpy as np
         k = len(patterns)
         pats = (_Pattern * k)(*[pattern_struct(q) for q in patterns])
@@ -344,13 +345,14 @@ class Context:
                                            len(proj), ctypes.byref(nrows), ctypes.byref(ncols),
                                            ovar, ocol, _stream(stream)))
         m, w = int(nrows.value), int(ncols.value)
-        rows = np.empty((m, w), np.uint32)
-        for c in range(w):
-            if m:
-                buf = (ctypes.c_uint32 * m).from_address(ocol[c])
-                rows[:, c] = np.frombuffer(buf, np.uint32, m)
-            lib().mapsq_host_free(ocol[c])
-        return [int(ovar[c]) for c in range(w)], rows
+        vars_ = [int(ovar[c]) for c in range(w)]
+        if m == 0 or w == 0:
+            return vars_, np.zeros((m, w), np.uint32)
+        # columns are consecutive in the arena: one (w, m) block -> transpose view (m, w)
+        buf = (ctypes.c_uint32 * (m * w)).from_address(ocol[0])
+        cols = np.frombuffer(buf, np.uint32, m * w).reshape(w, m)
+        rows = cols.T
+        return vars_, (np.ascontiguousarray(rows) if copy else rows)
 
     # ---- phase entry points (rows a3-a5)
     def map_words(self, tp1, tp2, plan: JoinPlan, words, stream=None):

@@ -702,6 +702,7 @@ MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
   }
   for (auto e : ctx->free_events) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
   delete ctx;
 }
 
@@ -749,10 +750,6 @@ MAPSQ_API mapsq_status mapsq_query(mapsq_ctx *ctx, const mapsq_triples *T,
   return query_impl(ctx, T, pats, npats, proj, nproj, rs, S(stream));
 }
 
-MAPSQ_API void mapsq_host_free(void *p) {
-  if (p) cudaFreeHost(p);
-}
-
 MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host,
                                         const uint32_t *p_host, const uint32_t *o_host,
                                         const mapsq_pattern *pats, int npats,
@@ -771,7 +768,7 @@ MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32
     uint32_t *d = sc.get<uint32_t>(3 * n + 12);
     NEED(d);
     uint32_t *ds = d, *dp = d + n, *dob = d + 2 * n;
-    // H2D in chunks so the copy engine streams while the scan's first pass starts early
+    // H2D in chunks (one copy engine stream); the scan starts once the table is resident
     const uint64_t chunk = 1ull << 26;
     for (uint64_t off = 0; off < n; off += chunk) {
       const uint64_t c = std::min(chunk, n - off);
@@ -782,33 +779,38 @@ MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32
     mapsq_triples T{n, ds, dp, dob};
     TRY(query_impl(ctx, &T, pats, npats, proj, nproj, &rs, s));
   }
-  *out_ncols = rs.ncols;
-  for (uint32_t c = 0; c < rs.ncols; c++) {
-    out_var[c] = rs.var[c];
-    host_cols[c] = nullptr;
-  }
-  mapsq_status st = MAPSQ_OK;
-  for (uint32_t c = 0; c < rs.ncols && st == MAPSQ_OK; c++) {
-    void *h = nullptr;
-    cudaError_t e = cudaMallocHost(&h, std::max<uint64_t>(rs.nrows, 1) * 4);
+  const uint64_t m = rs.nrows;
+  const uint32_t w = rs.ncols;
+  const size_t need = std::max<size_t>(16, (size_t)m * w * sizeof(uint32_t));
+  if (need > ctx->host_arena_bytes) {
+    if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+    ctx->host_arena = nullptr;
+    ctx->host_arena_bytes = 0;
+    const size_t bytes = std::max(need, ctx->host_arena_bytes * 2);
+    cudaError_t e = cudaMallocHost(&ctx->host_arena, bytes);
     if (e != cudaSuccess) {
-      st = cuda_check(ctx, e, "cudaMallocHost");
-      break;
+      ctx->host_arena = nullptr;
+      mapsq_table_release(ctx, &rs, stream);
+      return cuda_check(ctx, e, "cudaMallocHost(result arena)");
     }
-    host_cols[c] = static_cast<uint32_t *>(h);
-    if (rs.nrows) {
-      e = cudaMemcpyAsync(h, rs.col[c], rs.nrows * 4, cudaMemcpyDeviceToHost, s);
+    ctx->host_arena_bytes = bytes;
+  }
+  uint32_t *arena = static_cast<uint32_t *>(ctx->host_arena);
+  mapsq_status st = MAPSQ_OK;
+  for (uint32_t c = 0; c < w; c++) {
+    out_var[c] = rs.var[c];
+    host_cols[c] = arena + (size_t)c * m;
+    if (m && st == MAPSQ_OK) {
+      cudaError_t e = cudaMemcpyAsync(host_cols[c], rs.col[c], m * 4, cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) st = cuda_check(ctx, e, "D2H result");
     }
   }
   mapsq_table_release(ctx, &rs, stream);
   cudaError_t e = cudaStreamSynchronize(s);
   if (st == MAPSQ_OK && e != cudaSuccess) st = cuda_check(ctx, e, "sync");
-  if (st != MAPSQ_OK) {
-    for (uint32_t c = 0; c < rs.ncols; c++) mapsq_host_free(host_cols[c]);
-    return st;
-  }
-  *host_rows = rs.nrows;
+  if (st != MAPSQ_OK) return st;
+  *out_ncols = w;
+  *host_rows = m;
   return MAPSQ_OK;
 }
 

@@ -55,6 +55,8 @@ struct mapsq_ctx {
   mapsq_stats counters{};
   uint64_t *pinned = nullptr;  // small pinned host buffer for the blocking size reads
   size_t pinned_words = 0;
+  void *host_arena = nullptr;  // pinned result arena of mapsq_query_host (reused across calls)
+  size_t host_arena_bytes = 0;
 };
 
 namespace mapsq {

@@ -19,46 +19,62 @@ namespace {
 
 constexpr int kWarps = kSortThreads / 32;
 constexpr int kHistThreads = 256;
-constexpr int kHistItems = 16;
+constexpr int kHistItems = 8;
+
+// Histogram counters: one private copy per warp pair (4 copies per CTA) so that equal digits
+// (skewed keys) contend on fewer lanes; plain shared atomics, one per pass per element.
+constexpr int kHistCopies = 4;
 
 template <bool KV>
 __global__ void __launch_bounds__(kHistThreads)
 pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__restrict__ vals,
                  uint32_t *__restrict__ hist) {
-  __shared__ uint32_t s_hist[kMaxPasses][kRadix];
-  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kHistThreads) (&s_hist[0][0])[i] = 0;
+  __shared__ uint32_t s_hist[kHistCopies][kMaxPasses * kRadix];
+  for (int i = threadIdx.x; i < kHistCopies * kMaxPasses * kRadix; i += kHistThreads)
+    (&s_hist[0][0])[i] = 0;
   __syncthreads();
+  uint32_t *h = s_hist[(threadIdx.x >> 5) % kHistCopies];
   const uint64_t n = a.n1 + a.n2;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * kHistThreads; i0 < n; i0 += stride) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool in = i < n;
-    uint64_t key = 0;
-    if (in) {
-      const bool left = i < a.n1;
-      const uint64_t r = left ? i : i - a.n1;
-      for (uint32_t c = 0; c < a.nkey; c++) {
-        const uint32_t v = left ? __ldcs(a.key1[c] + r) : __ldcs(a.key2[c] + r);
-        key |= (uint64_t)(v - a.lo[c]) << a.shift[c];
+  const uint64_t chunk = (uint64_t)kHistThreads * kHistItems;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    uint64_t key[kHistItems];
+#pragma unroll
+    for (int it = 0; it < kHistItems; it++) {
+      const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
+      uint64_t kk = 0;
+      if (i < n) {
+        const bool left = i < a.n1;
+        const uint64_t r = left ? i : i - a.n1;
+        for (uint32_t c = 0; c < a.nkey; c++) {
+          const uint32_t v = left ? __ldcs(a.key1[c] + r) : __ldcs(a.key2[c] + r);
+          kk |= (uint64_t)(v - a.lo[c]) << a.shift[c];
+        }
       }
-      if (KV) {
-        words[i] = key;
-        vals[i] = (uint32_t)i;
-      } else {
-        key = (key << a.ib) | i;
-        words[i] = key;
-      }
+      key[it] = kk;
     }
-    for (uint32_t p = 0; p < a.passes; p++) {
-      const uint32_t d = (uint32_t)(key >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
-      const uint32_t peers = __match_any_sync(0xffffffffu, in ? d : 0x100u);
-      if (in && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[p][d], __popc(peers));
+#pragma unroll
+    for (int it = 0; it < kHistItems; it++) {
+      const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
+      if (i >= n) continue;
+      uint64_t kk = key[it];
+      if (KV) {
+        __stcs(words + i, kk);
+        __stcs(vals + i, (uint32_t)i);
+      } else {
+        kk = (kk << a.ib) | i;
+        __stcs(words + i, kk);
+      }
+      for (uint32_t p = 0; p < a.passes; p++) {
+        const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
+        atomicAdd(h + p * kRadix + d, 1u);
+      }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (int)a.passes * kRadix; i += kHistThreads) {
-    const uint32_t c = (&s_hist[0][0])[i];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kHistCopies; q++) c += s_hist[q][i];
     if (c) atomicAdd(hist + i, c);
   }
 }
@@ -66,24 +82,24 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
 __global__ void __launch_bounds__(kHistThreads)
 key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
                 uint32_t last_mask, uint32_t *__restrict__ hist) {
-  __shared__ uint32_t s_hist[kMaxPasses][kRadix];
-  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kHistThreads) (&s_hist[0][0])[i] = 0;
+  __shared__ uint32_t s_hist[kHistCopies][kMaxPasses * kRadix];
+  for (int i = threadIdx.x; i < kHistCopies * kMaxPasses * kRadix; i += kHistThreads)
+    (&s_hist[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t lane = threadIdx.x & 31;
+  uint32_t *h = s_hist[(threadIdx.x >> 5) % kHistCopies];
   const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * kHistThreads; i0 < n; i0 += stride) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool in = i < n;
-    const uint64_t key = in ? keys[i] : 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * kHistThreads + threadIdx.x; i < n; i += stride) {
+    const uint64_t key = __ldcs(keys + i);
     for (uint32_t p = 0; p < passes; p++) {
       const uint32_t d = (uint32_t)(key >> (bit_lo + 8 * p)) & (p + 1 == passes ? last_mask : 0xffu);
-      const uint32_t peers = __match_any_sync(0xffffffffu, in ? d : 0x100u);
-      if (in && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[p][d], __popc(peers));
+      atomicAdd(h + p * kRadix + d, 1u);
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (int)passes * kRadix; i += kHistThreads) {
-    const uint32_t c = (&s_hist[0][0])[i];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kHistCopies; q++) c += s_hist[q][i];
     if (c) atomicAdd(hist + i, c);
   }
 }

@@ -28,20 +28,24 @@ __device__ __forceinline__ bool pat_match(const ScanPat &p, uint32_t s, uint32_t
   return ok;
 }
 
+// Patterns are evaluated in a runtime loop over descriptors staged in shared memory (no unroll
+// over MAPSQ_MAX_PATTERNS: that blew the instruction cache).
 __global__ void __launch_bounds__(kScanThreads)
 scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
                   const uint32_t *__restrict__ O, uint64_t n, const ScanArgs a,
                   uint32_t *__restrict__ masks, uint64_t mask_words,
                   uint32_t *__restrict__ tile_counts, uint64_t ntiles) {
+  __shared__ ScanPat s_pat[MAPSQ_MAX_PATTERNS];
+  __shared__ uint32_t s_mw[kWarps][MAPSQ_MAX_PATTERNS][kScanWordsPerWarp];
   __shared__ uint32_t s_cnt[kWarps][MAPSQ_MAX_PATTERNS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
+  if (threadIdx.x < (unsigned)k) s_pat[threadIdx.x] = a.pat[threadIdx.x];
+  __syncthreads();
   const uint64_t tile = blockIdx.x;
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
-  uint32_t mword[MAPSQ_MAX_PATTERNS];
-#pragma unroll
-  for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) mword[j] = 0;
   const bool ns = a.need_count & 1, np = a.need_count & 2, no = a.need_count & 4;
-#pragma unroll 4
+#pragma unroll 1
   for (int w = 0; w < kScanWordsPerWarp; w += 8) {
     uint32_t vs[8], vp[8], vo[8];
 #pragma unroll
@@ -54,29 +58,24 @@ scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
     }
 #pragma unroll
     for (int u = 0; u < 8; u++) {
-      const uint64_t i = (word0 + w + u) * 32 + lane;
-      const bool in = i < n;
-#pragma unroll
-      for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) {
-        if (j < a.k) {
-          const uint32_t m = __ballot_sync(0xffffffffu, in && pat_match(a.pat[j], vs[u], vp[u], vo[u]));
-          if (lane == w + u) mword[j] = m;
-        }
+      const bool in = (word0 + w + u) * 32 + lane < n;
+#pragma unroll 1
+      for (int j = 0; j < k; j++) {
+        const uint32_t m = __ballot_sync(0xffffffffu, in && pat_match(s_pat[j], vs[u], vp[u], vo[u]));
+        if (lane == 0) s_mw[warp][j][w + u] = m;
       }
     }
   }
-  // lane l now holds match word (word0 + l) of every pattern
+  __syncwarp();
   const uint64_t my_word = word0 + lane;
-#pragma unroll
-  for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) {
-    if (j < a.k) {
-      if (my_word < mask_words) masks[(uint64_t)j * mask_words + my_word] = mword[j];
-      const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(mword[j]));
-      if (lane == 0) s_cnt[warp][j] = c;
-    }
+  for (int j = 0; j < k; j++) {
+    const uint32_t m = s_mw[warp][j][lane];
+    if (my_word < mask_words) masks[(uint64_t)j * mask_words + my_word] = m;
+    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(m));
+    if (lane == 0) s_cnt[warp][j] = c;
   }
   __syncthreads();
-  if (threadIdx.x < (unsigned)a.k) {
+  if (threadIdx.x < (unsigned)k) {
     uint32_t t = 0;
     for (int w = 0; w < kWarps; w++) t += s_cnt[w][threadIdx.x];
     tile_counts[(uint64_t)threadIdx.x * ntiles + tile] = t;
@@ -89,52 +88,47 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
                   const uint32_t *__restrict__ masks, uint64_t mask_words,
                   const uint64_t *__restrict__ tile_off, uint64_t ntiles, const ScanOut out,
                   uint32_t *__restrict__ bmin, uint32_t *__restrict__ bmax) {
+  __shared__ ScanPat s_pat[MAPSQ_MAX_PATTERNS];
+  __shared__ uint32_t s_mw[kWarps][MAPSQ_MAX_PATTERNS][kScanWordsPerWarp];
   __shared__ uint32_t s_wcnt[kWarps][MAPSQ_MAX_PATTERNS];
+  __shared__ uint64_t s_cur[kWarps][MAPSQ_MAX_PATTERNS];
   __shared__ uint32_t s_min[kWarps][MAPSQ_MAX_PATTERNS * 3], s_max[kWarps][MAPSQ_MAX_PATTERNS * 3];
   __shared__ uint32_t *s_out[MAPSQ_MAX_PATTERNS * 3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
   const uint64_t tile = blockIdx.x;
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
   const uint64_t my_word = word0 + lane;
   if (threadIdx.x < MAPSQ_MAX_PATTERNS * 3) s_out[threadIdx.x] = out.col[threadIdx.x];
+  if (threadIdx.x < (unsigned)k) s_pat[threadIdx.x] = a.pat[threadIdx.x];
   for (int j = lane; j < MAPSQ_MAX_PATTERNS * 3; j += 32) {
     s_min[warp][j] = 0xffffffffu;
     s_max[warp][j] = 0u;
   }
-  // this lane's match word of every pattern, and the warp's count
-  uint32_t mword[MAPSQ_MAX_PATTERNS];
-#pragma unroll
-  for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) {
-    mword[j] = 0;
-    if (j < a.k) {
-      mword[j] = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
-      const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(mword[j]));
-      if (lane == 0) s_wcnt[warp][j] = c;
-    }
+  uint32_t any_mine = 0;  // OR over patterns of this lane's word
+  for (int j = 0; j < k; j++) {
+    const uint32_t m = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
+    s_mw[warp][j][lane] = m;
+    any_mine |= m;
+    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(m));
+    if (lane == 0) s_wcnt[warp][j] = c;
   }
   __syncthreads();
-  // output cursor of this warp for each pattern (tile offset + earlier warps of the tile)
-  uint64_t cur[MAPSQ_MAX_PATTERNS];
-#pragma unroll
-  for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) {
-    cur[j] = 0;
-    if (j < a.k) {
-      // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
-      uint64_t c = tile_off[(uint64_t)j * ntiles + tile] - tile_off[(uint64_t)j * ntiles];
-      for (int w = 0; w < warp; w++) c += s_wcnt[w][j];
-      cur[j] = c;
-    }
+  if (lane < k) {
+    // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
+    uint64_t c = tile_off[(uint64_t)lane * ntiles + tile] - tile_off[(uint64_t)lane * ntiles];
+    for (int w = 0; w < warp; w++) c += s_wcnt[w][lane];
+    s_cur[warp][lane] = c;
   }
+  __syncwarp();
   const bool ws = a.need_write & 1, wp = a.need_write & 2, wo = a.need_write & 4;
   const uint32_t lt = lanemask_lt();
+#pragma unroll 1
   for (int w = 0; w < kScanWordsPerWarp; w += 8) {
     uint32_t vs[8], vp[8], vo[8], any[8];
 #pragma unroll
     for (int u = 0; u < 8; u++) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++)
-        if (j < a.k) m |= __shfl_sync(0xffffffffu, mword[j], w + u);
+      const uint32_t m = __shfl_sync(0xffffffffu, any_mine, w + u);
       any[u] = m;
       const uint64_t i = (word0 + w + u) * 32 + lane;
       const bool hit = (m >> lane) & 1u;
@@ -145,16 +139,16 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
 #pragma unroll
     for (int u = 0; u < 8; u++) {
       if (any[u] == 0) continue;  // warp-uniform
-#pragma unroll
-      for (int j = 0; j < MAPSQ_MAX_PATTERNS; j++) {
-        if (j >= a.k) continue;
-        const uint32_t m = __shfl_sync(0xffffffffu, mword[j], w + u);
+#pragma unroll 1
+      for (int j = 0; j < k; j++) {
+        const uint32_t m = s_mw[warp][j][w + u];
         if (m == 0) continue;
         const bool hit = (m >> lane) & 1u;
-        const uint64_t pos = cur[j] + __popc(m & lt);
-        const ScanPat &pt = a.pat[j];
-        for (uint32_t c = 0; c < pt.ncols; c++) {
-          const uint32_t src = pt.src[c];
+        const uint64_t base = s_cur[warp][j];
+        const uint64_t pos = base + __popc(m & lt);
+        const uint32_t nc = s_pat[j].ncols;
+        for (uint32_t c = 0; c < nc; c++) {
+          const uint32_t src = s_pat[j].src[c];
           const uint32_t v = src == 0 ? vs[u] : (src == 1 ? vp[u] : vo[u]);
           if (hit) st_cs_u32(s_out[j * 3 + c] + pos, v);
           const uint32_t mn = __reduce_min_sync(0xffffffffu, hit ? v : 0xffffffffu);
@@ -164,14 +158,16 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
             s_max[warp][j * 3 + c] = max(s_max[warp][j * 3 + c], mx);
           }
         }
-        cur[j] += __popc(m);
+        __syncwarp();
+        if (lane == 0) s_cur[warp][j] = base + __popc(m);
+        __syncwarp();
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x < (unsigned)a.k * 3) {
+  if (threadIdx.x < (unsigned)k * 3) {
     const int j = threadIdx.x / 3, c = threadIdx.x % 3;
-    if ((uint32_t)c < a.pat[j].ncols) {
+    if ((uint32_t)c < s_pat[j].ncols) {
       uint32_t mn = 0xffffffffu, mx = 0;
       for (int w = 0; w < kWarps; w++) {
         mn = min(mn, s_min[w][threadIdx.x]);
