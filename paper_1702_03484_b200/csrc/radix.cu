@@ -21,21 +21,36 @@ constexpr int kWarps = kSortThreads / 32;
 constexpr int kHistThreads = 256;
 constexpr int kHistItems = 8;
 
-// Histogram counters: one private copy per warp pair (4 copies per CTA) so that equal digits
-// (skewed keys) contend on fewer lanes; plain shared atomics, one per pass per element.
-constexpr int kHistCopies = 4;
+// Upfront histograms of every pass (onesweep).  Each warp owns a private row per pass; equal
+// digits inside a warp are found with one ballot per digit bit and counted by a single leader
+// lane, so no shared-memory atomics are issued (they bounded the first version of this kernel).
+__device__ __forceinline__ void warp_count_digit(uint32_t *row, uint32_t d, bool in,
+                                                 uint32_t bits, uint32_t lane) {
+  uint32_t peers = __ballot_sync(0xffffffffu, in);
+#pragma unroll
+  for (int b = 0; b < 8; b++) {
+    if ((uint32_t)b < bits) {
+      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+  }
+  if (in && lane == 31u - __clz(peers)) row[d] += __popc(peers);
+  __syncwarp();
+}
 
 template <bool KV>
 __global__ void __launch_bounds__(kHistThreads)
 pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__restrict__ vals,
                  uint32_t *__restrict__ hist) {
-  __shared__ uint32_t s_hist[kHistCopies][kMaxPasses * kRadix];
-  for (int i = threadIdx.x; i < kHistCopies * kMaxPasses * kRadix; i += kHistThreads)
-    (&s_hist[0][0])[i] = 0;
+  extern __shared__ uint32_t s_whist[];  // [warps][passes][256]
+  const int nw = kHistThreads / 32;
+  for (int i = threadIdx.x; i < nw * (int)a.passes * kRadix; i += kHistThreads) s_whist[i] = 0;
   __syncthreads();
-  uint32_t *h = s_hist[(threadIdx.x >> 5) % kHistCopies];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t *my = s_whist + warp * a.passes * kRadix;
   const uint64_t n = a.n1 + a.n2;
   const uint64_t chunk = (uint64_t)kHistThreads * kHistItems;
+  const uint32_t last_bits = 32 - __clz(a.last_mask);
   for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
     uint64_t key[kHistItems];
 #pragma unroll
@@ -55,29 +70,29 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
 #pragma unroll
     for (int it = 0; it < kHistItems; it++) {
       const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
-      if (i >= n) continue;
+      const bool in = i < n;
       uint64_t kk = key[it];
-      if (KV) {
+      if (!KV) kk = (kk << a.ib) | i;
+      if (in) {
         __stcs(words + i, kk);
-        __stcs(vals + i, (uint32_t)i);
-      } else {
-        kk = (kk << a.ib) | i;
-        __stcs(words + i, kk);
+        if (KV) __stcs(vals + i, (uint32_t)i);
       }
       for (uint32_t p = 0; p < a.passes; p++) {
-        const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
-        atomicAdd(h + p * kRadix + d, 1u);
+        const bool last = p + 1 == a.passes;
+        const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (last ? a.last_mask : 0xffu);
+        warp_count_digit(my + p * kRadix, d, in, last ? last_bits : 8u, lane);
       }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (int)a.passes * kRadix; i += kHistThreads) {
     uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < kHistCopies; q++) c += s_hist[q][i];
+    for (int w = 0; w < nw; w++) c += s_whist[w * a.passes * kRadix + i];
     if (c) atomicAdd(hist + i, c);
   }
 }
+
+constexpr int kHistCopies = 4;
 
 __global__ void __launch_bounds__(kHistThreads)
 key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
@@ -125,7 +140,7 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
 // slice [w*32*ITEMS, (w+1)*32*ITEMS) of its tile and reads it item-major (item it, lane l ->
 // slice[it*32 + l]) so every load is a coalesced 256 B row.
 template <bool KV>
-__global__ void __launch_bounds__(kSortThreads, 2)
+__global__ void __launch_bounds__(kSortThreads, 3)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
                   uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
@@ -157,15 +172,24 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     k[it] = i < n ? __ldcs(kin + i) : ~0ull;
     if (KV) v[it] = i < n ? __ldcs(vin + i) : 0u;
   }
-  // warp-level multisplit: rank of each key among equal digits of this warp's slice
+  // warp-level multisplit: rank of each key among equal digits of this warp's slice.  Peers
+  // with the same digit are found with one ballot per digit bit (MATCH.ANY's latency dominated
+  // the first version of this kernel).
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < kSortItems; it++) {
     const uint64_t i = wbase + it * 32 + lane;
     const bool in = i < n;
-    const uint32_t d = in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(peers) - 1;
+    const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
+    uint32_t peers = __ballot_sync(0xffffffffu, in);
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+      if ((uint32_t)b < bits) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+      }
+    }
+    const int leader = 31 - __clz(peers);
     uint32_t base = 0;
     if (in && lane == leader) {
       base = s_warp_hist[warp][d];
@@ -196,7 +220,10 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     while (true) {
       const uint64_t sv = ld_relaxed_u64(status + (uint64_t)t * kRadix + d);
       const uint64_t flag = sv & ~kValMask;
-      if (flag == 0) continue;
+      if (flag == 0) {
+        __nanosleep(64);
+        continue;
+      }
       excl += sv & kValMask;
       if (flag == kFlagInc) break;
       t--;
@@ -254,10 +281,17 @@ void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32
                       cudaStream_t s) {
   const uint64_t n = a.n1 + a.n2;
   const int g = grid_for(n, kHistThreads * kHistItems);
+  const size_t smem = (kHistThreads / 32) * std::max<uint32_t>(a.passes, 1) * kRadix * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaFuncSetAttribute(pack_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    attr = true;
+  }
   if (a.kv)
-    pack_hist_kernel<true><<<g, kHistThreads, 0, s>>>(a, words, vals, hist);
+    pack_hist_kernel<true><<<g, kHistThreads, smem, s>>>(a, words, vals, hist);
   else
-    pack_hist_kernel<false><<<g, kHistThreads, 0, s>>>(a, words, vals, hist);
+    pack_hist_kernel<false><<<g, kHistThreads, smem, s>>>(a, words, vals, hist);
 }
 
 void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t passes,

@@ -34,6 +34,16 @@ struct WordView {
   __device__ __forceinline__ bool right(uint64_t i) const {
     return (words ? (words[i] & idx_mask) : (uint64_t)vals[i]) >= n1;
   }
+  __device__ __forceinline__ void load(uint64_t i, uint64_t *k, bool *r) const {
+    if (words) {
+      const uint64_t w = __ldcs(words + i);
+      *k = w >> ib;
+      *r = (w & idx_mask) >= n1;
+    } else {
+      *k = __ldcs(keys + i);
+      *r = __ldcs(vals + i) >= n1;
+    }
+  }
 };
 
 __global__ void __launch_bounds__(kGThreads)
@@ -48,15 +58,23 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   const uint64_t tile = s_tile;
   const uint64_t base = tile * kGTile;
   uint32_t ball[kGItems];
-  // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane
+  // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane.  Each
+  // element is loaded once; its predecessor comes from the neighbouring lane (lane 0 loads it).
 #pragma unroll
   for (int it = 0; it < kGItems; it++) {
     const uint64_t i = base + (uint64_t)it * kGThreads + tid;
-    bool split = false;
-    if (i > 0 && i < n) {
-      // split: word i is RIGHT, word i-1 is LEFT, same key
-      split = W.right(i) && !W.right(i - 1) && W.key(i) == W.key(i - 1);
+    uint64_t k = ~0ull;
+    bool r = false;
+    if (i < n) W.load(i, &k, &r);
+    uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    bool rp = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) {
+      kp = ~0ull;
+      rp = true;
+      if (i > 0 && i < n) W.load(i - 1, &kp, &rp);
     }
+    // split: word i is RIGHT, word i-1 is LEFT, same key
+    const bool split = i > 0 && i < n && r && !rp && k == kp;
     ball[it] = __ballot_sync(0xffffffffu, split);
     if (lane == 0) s_cnt[it][warp] = __popc(ball[it]);
   }
