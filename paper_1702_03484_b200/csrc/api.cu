@@ -50,6 +50,53 @@ void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s) {
     cudaFreeAsync(p, s);
 }
 
+Scratch::Scratch(mapsq_ctx *c, cudaStream_t st) : ctx(c), s(st), mark(c->arena_used) {
+  if (ctx->arena_depth++ == 0) {
+    ctx->arena_demand = 0;
+    if (ctx->arena && ctx->arena_stream != s && ctx->arena_ev)
+      cudaStreamWaitEvent(s, ctx->arena_ev, 0);  // previous user of the arena on another stream
+    if (!ctx->custom_alloc && ctx->arena_hw > ctx->arena_cap) {
+      if (ctx->arena) cudaFreeAsync(ctx->arena, s);
+      ctx->arena = nullptr;
+      ctx->arena_cap = 0;
+      const size_t want = (ctx->arena_hw + ctx->arena_hw / 8 + 4095) & ~size_t(4095);
+      void *p = nullptr;
+      if (cudaMallocAsync(&p, want, s) == cudaSuccess) {
+        ctx->arena = static_cast<char *>(p);
+        ctx->arena_cap = want;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    ctx->arena_used = 0;
+    mark = 0;
+  }
+}
+
+Scratch::~Scratch() {
+  for (void *p : ptrs) dfree(ctx, p, s);
+  ctx->arena_used = mark;
+  if (--ctx->arena_depth == 0) {
+    ctx->arena_hw = std::max(ctx->arena_hw, ctx->arena_demand);
+    if (!ctx->arena_ev) cudaEventCreateWithFlags(&ctx->arena_ev, cudaEventDisableTiming);
+    cudaEventRecord(ctx->arena_ev, s);
+    ctx->arena_stream = s;
+  }
+}
+
+void *Scratch::raw(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  ctx->arena_demand += bytes;
+  if (ctx->arena && ctx->arena_used + bytes <= ctx->arena_cap) {
+    void *p = ctx->arena + ctx->arena_used;
+    ctx->arena_used += bytes;
+    return p;
+  }
+  void *p = dalloc(ctx, bytes, s);
+  if (p) ptrs.push_back(p);
+  return p;
+}
+
 KTimer::KTimer(mapsq_ctx *c, cudaStream_t st, const char *name, uint64_t bytes, int nlaunch)
     : ctx(c), s(st), on(c->profiling) {
   ctx->counters.launches += nlaunch;
@@ -703,6 +750,8 @@ MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
   for (auto e : ctx->free_events) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->arena_ev) cudaEventDestroy(ctx->arena_ev);
   delete ctx;
 }
 

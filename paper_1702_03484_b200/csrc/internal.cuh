@@ -57,6 +57,12 @@ struct mapsq_ctx {
   size_t pinned_words = 0;
   void *host_arena = nullptr;  // pinned result arena of mapsq_query_host (reused across calls)
   size_t host_arena_bytes = 0;
+  // device scratch arena: grow-only bump allocator reused by every operation (stream ordered)
+  char *arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0, arena_demand = 0, arena_hw = 0;
+  int arena_depth = 0;
+  cudaStream_t arena_stream = nullptr;
+  cudaEvent_t arena_ev = nullptr;
 };
 
 namespace mapsq {
@@ -67,22 +73,23 @@ mapsq_status cuda_check(mapsq_ctx *ctx, cudaError_t e, const char *what);
 void *dalloc(mapsq_ctx *ctx, size_t bytes, cudaStream_t s);
 void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s);
 
-// Scratch allocations freed (stream ordered) when the guard leaves scope.
+// Scratch allocations of one operation.  They come from the context's grow-only arena (bump
+// pointer, reset when the guard leaves scope); what does not fit is taken from the allocator and
+// freed (stream ordered) on exit, and the arena grows to the observed high-water mark before the
+// next operation, so steady-state operations never touch the allocator for scratch.
 struct Scratch {
   mapsq_ctx *ctx;
   cudaStream_t s;
+  size_t mark;
   std::vector<void *> ptrs;
-  Scratch(mapsq_ctx *c, cudaStream_t st) : ctx(c), s(st) {}
-  ~Scratch() {
-    for (void *p : ptrs) dfree(ctx, p, s);
-  }
+  Scratch(mapsq_ctx *c, cudaStream_t st);
+  ~Scratch();
+  void *raw(size_t bytes);
   template <typename T>
   T *get(size_t count) {
-    void *p = dalloc(ctx, count * sizeof(T) + 16, s);
-    if (p) ptrs.push_back(p);
-    return static_cast<T *>(p);
+    return static_cast<T *>(raw(count * sizeof(T) + 16));
   }
-  void release(void *p) {
+  void release(void *p) {  // only allocator-backed blocks are returned early
     for (auto &q : ptrs)
       if (q == p) {
         dfree(ctx, q, s);
@@ -129,6 +136,40 @@ __device__ __forceinline__ void st_cs_v4(uint32_t *p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// Decoupled look-back over one count per tile, run by ALL 32 lanes of one warp: lane l inspects
+// tile (t0 - l), so 32 predecessors are examined per round trip instead of one.  Publishes
+// AGG(agg) then INC(excl + agg) for `tile` and returns the exclusive prefix (all lanes).
+// Counts are < 2^32 (n < 2^32 per join), so 32-bit warp reductions suffice.
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t *status, uint64_t tile, uint32_t agg) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_u64(status, kFlagInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | agg);
+  uint64_t excl = 0;
+  int64_t t0 = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = t0 - (int64_t)lane;
+    const uint64_t v = t >= 0 ? ld_relaxed_u64(status + t) : kFlagInc;  // virtual INC(0)
+    const uint64_t flag = v & ~kValMask;
+    const uint32_t inc = __ballot_sync(0xffffffffu, flag == kFlagInc);
+    const uint32_t zero = __ballot_sync(0xffffffffu, flag == 0);
+    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+    const uint32_t need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+    if (zero & need) {
+      __nanosleep(32);
+      continue;
+    }
+    const uint32_t val = ((int)lane <= first_inc) ? (uint32_t)(v & kValMask) : 0u;
+    excl += __reduce_add_sync(0xffffffffu, val);
+    if (first_inc < 32) break;
+    t0 -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | (excl + agg));
+  return excl;
 }
 
 // ---------------------------------------------------------------- launchers (kernels/*.cu)

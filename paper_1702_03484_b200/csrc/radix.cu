@@ -21,36 +21,21 @@ constexpr int kWarps = kSortThreads / 32;
 constexpr int kHistThreads = 256;
 constexpr int kHistItems = 8;
 
-// Upfront histograms of every pass (onesweep).  Each warp owns a private row per pass; equal
-// digits inside a warp are found with one ballot per digit bit and counted by a single leader
-// lane, so no shared-memory atomics are issued (they bounded the first version of this kernel).
-__device__ __forceinline__ void warp_count_digit(uint32_t *row, uint32_t d, bool in,
-                                                 uint32_t bits, uint32_t lane) {
-  uint32_t peers = __ballot_sync(0xffffffffu, in);
-#pragma unroll
-  for (int b = 0; b < 8; b++) {
-    if ((uint32_t)b < bits) {
-      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bb : ~bb;
-    }
-  }
-  if (in && lane == 31u - __clz(peers)) row[d] += __popc(peers);
-  __syncwarp();
-}
+constexpr int kHistCopies = 4;
 
+// Upfront histograms of every pass (onesweep), one shared atomic per pass per element into one
+// of kHistCopies private copies (warps w and w+4 share a copy).
 template <bool KV>
 __global__ void __launch_bounds__(kHistThreads)
 pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__restrict__ vals,
                  uint32_t *__restrict__ hist) {
-  extern __shared__ uint32_t s_whist[];  // [warps][passes][256]
-  const int nw = kHistThreads / 32;
-  for (int i = threadIdx.x; i < nw * (int)a.passes * kRadix; i += kHistThreads) s_whist[i] = 0;
+  extern __shared__ uint32_t s_hcopy[];  // [kHistCopies][passes * 256]
+  const uint32_t plen = a.passes * kRadix;
+  for (uint32_t i = threadIdx.x; i < kHistCopies * plen; i += kHistThreads) s_hcopy[i] = 0;
   __syncthreads();
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t *my = s_whist + warp * a.passes * kRadix;
+  uint32_t *h = s_hcopy + ((threadIdx.x >> 5) % kHistCopies) * plen;
   const uint64_t n = a.n1 + a.n2;
   const uint64_t chunk = (uint64_t)kHistThreads * kHistItems;
-  const uint32_t last_bits = 32 - __clz(a.last_mask);
   for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
     uint64_t key[kHistItems];
 #pragma unroll
@@ -70,29 +55,29 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
 #pragma unroll
     for (int it = 0; it < kHistItems; it++) {
       const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
-      const bool in = i < n;
+      if (i >= n) continue;
       uint64_t kk = key[it];
-      if (!KV) kk = (kk << a.ib) | i;
-      if (in) {
+      if (KV) {
         __stcs(words + i, kk);
-        if (KV) __stcs(vals + i, (uint32_t)i);
+        __stcs(vals + i, (uint32_t)i);
+      } else {
+        kk = (kk << a.ib) | i;
+        __stcs(words + i, kk);
       }
       for (uint32_t p = 0; p < a.passes; p++) {
-        const bool last = p + 1 == a.passes;
-        const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (last ? a.last_mask : 0xffu);
-        warp_count_digit(my + p * kRadix, d, in, last ? last_bits : 8u, lane);
+        const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
+        atomicAdd(h + p * kRadix + d, 1u);
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)a.passes * kRadix; i += kHistThreads) {
+  for (uint32_t i = threadIdx.x; i < plen; i += kHistThreads) {
     uint32_t c = 0;
-    for (int w = 0; w < nw; w++) c += s_whist[w * a.passes * kRadix + i];
+#pragma unroll
+    for (int q = 0; q < kHistCopies; q++) c += s_hcopy[q * plen + i];
     if (c) atomicAdd(hist + i, c);
   }
 }
-
-constexpr int kHistCopies = 4;
 
 __global__ void __launch_bounds__(kHistThreads)
 key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
@@ -281,7 +266,7 @@ void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32
                       cudaStream_t s) {
   const uint64_t n = a.n1 + a.n2;
   const int g = grid_for(n, kHistThreads * kHistItems);
-  const size_t smem = (kHistThreads / 32) * std::max<uint32_t>(a.passes, 1) * kRadix * sizeof(uint32_t);
+  const size_t smem = kHistCopies * std::max<uint32_t>(a.passes, 1) * kRadix * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(pack_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);

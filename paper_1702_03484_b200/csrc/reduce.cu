@@ -57,7 +57,7 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t base = tile * kGTile;
-  uint32_t ball[kGItems];
+  __shared__ uint32_t s_ball[kGItems][kGWarps];
   // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane.  Each
   // element is loaded once; its predecessor comes from the neighbouring lane (lane 0 loads it).
 #pragma unroll
@@ -75,11 +75,14 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
     }
     // split: word i is RIGHT, word i-1 is LEFT, same key
     const bool split = i > 0 && i < n && r && !rp && k == kp;
-    ball[it] = __ballot_sync(0xffffffffu, split);
-    if (lane == 0) s_cnt[it][warp] = __popc(ball[it]);
+    const uint32_t bl = __ballot_sync(0xffffffffu, split);
+    if (lane == 0) {
+      s_ball[it][warp] = bl;
+      s_cnt[it][warp] = __popc(bl);
+    }
   }
   __syncthreads();
-  // exclusive scan of the (it, warp) counts in element order; thread 0 does the look-back
+  // exclusive scan of the (it, warp) counts in element order; warp 0 also does the look-back
   if (tid < 32) {
     uint32_t v[kGItems * kGWarps / 32];
     uint32_t sum = 0;
@@ -100,23 +103,8 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
       (&s_cnt[0][0])[tid * (kGItems * kGWarps / 32) + q] = run;
       run += v[q];
     }
+    const uint64_t excl = warp_lookback(status, tile, total);
     if (tid == 0) {
-      uint64_t excl = 0;
-      if (tile == 0) {
-        st_relaxed_u64(status, kFlagInc | total);
-      } else {
-        st_relaxed_u64(status + tile, kFlagAgg | total);
-        int64_t t = (int64_t)tile - 1;
-        while (true) {
-          const uint64_t sv = ld_relaxed_u64(status + t);
-          const uint64_t flag = sv & ~kValMask;
-          if (flag == 0) continue;
-          excl += sv & kValMask;
-          if (flag == kFlagInc) break;
-          t--;
-        }
-        st_relaxed_u64(status + tile, kFlagInc | (excl + total));
-      }
       s_base = excl;
       if (tile == gridDim.x - 1) *ngroups_dev = excl + total;
     }
@@ -126,9 +114,10 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   const uint32_t lt = lanemask_lt();
 #pragma unroll 1
   for (int it = 0; it < kGItems; it++) {
-    if (!((ball[it] >> lane) & 1u)) continue;
+    const uint32_t bl = s_ball[it][warp];
+    if (!((bl >> lane) & 1u)) continue;
     const uint64_t i = base + (uint64_t)it * kGThreads + tid;
-    const uint64_t pos = out_base + s_cnt[it][warp] + __popc(ball[it] & lt);
+    const uint64_t pos = out_base + s_cnt[it][warp] + __popc(bl & lt);
     const uint64_t k = W.key(i);
     // gallop back from i-1 to the first element of the key's run
     int64_t lo = (int64_t)i - 1;  // key(lo) == k
