@@ -18,6 +18,7 @@ namespace mapsq {
 namespace {
 
 constexpr int kWarps = kSortThreads / 32;
+constexpr int kLookWin = 8;
 constexpr int kHistThreads = 256;
 constexpr int kHistItems = 8;
 
@@ -201,17 +202,31 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     st_relaxed_u64(my_status, kFlagInc | total);
   } else {
     st_relaxed_u64(my_status, kFlagAgg | total);
-    int64_t t = (int64_t)tile - 1;
+    // Windowed look-back: kLookWin predecessors are read at once (independent loads), so the
+    // walk to the nearest inclusive prefix costs one L2 round trip per kLookWin tiles instead of
+    // one per tile (the serial walk bounded the first version of this kernel).
+    int64_t t0 = (int64_t)tile - 1;
     while (true) {
-      const uint64_t sv = ld_relaxed_u64(status + (uint64_t)t * kRadix + d);
-      const uint64_t flag = sv & ~kValMask;
-      if (flag == 0) {
-        __nanosleep(64);
-        continue;
+      uint64_t v[kLookWin];
+#pragma unroll
+      for (int w = 0; w < kLookWin; w++) {
+        const int64_t t = t0 - w;
+        v[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
       }
-      excl += sv & kValMask;
-      if (flag == kFlagInc) break;
-      t--;
+      int consumed = 0;
+      bool done = false;
+#pragma unroll
+      for (int w = 0; w < kLookWin; w++) {
+        if (consumed != w || done) continue;
+        const uint64_t flag = v[w] & ~kValMask;
+        if (flag == 0) continue;  // not published yet: stop consuming here
+        excl += v[w] & kValMask;
+        consumed = w + 1;
+        if (flag == kFlagInc) done = true;
+      }
+      if (done) break;
+      t0 -= consumed;
+      if (consumed < kLookWin) __nanosleep(32);
     }
     st_relaxed_u64(my_status, kFlagInc | (excl + total));
   }

@@ -18,7 +18,7 @@ namespace mapsq {
 namespace {
 
 constexpr int kGThreads = 256;
-constexpr int kGItems = 16;
+constexpr int kGItems = 64;
 constexpr uint64_t kGTile = kGThreads * kGItems;
 constexpr int kGWarps = kGThreads / 32;
 

@@ -33,3 +33,14 @@ for rep in range(3):
     ctx.sort_words(words, pl.ib, pl.ib + pl.kb); torch.cuda.synchronize(); t2 = time.perf_counter()
     g = ctx.reduce_groups(words, n, n, pl.ib); torch.cuda.synchronize(); t3 = time.perf_counter()
     print(f"map {1e3*(t1-t0):.2f} sort {1e3*(t2-t1):.2f} reduce {1e3*(t3-t2):.2f} ms")
+# reference point only (never on the product path): CUB radix sort via torch.sort, 64-bit keys
+x = torch.randint(0, 1 << 62, (2 * n,), device='cuda')
+for rep in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    y = torch.sort(x).values; torch.cuda.synchronize(); t1 = time.perf_counter()
+    print(f"torch.sort int64 2n={2*n}: {1e3*(t1-t0):.2f} ms (8 passes)")
+x32 = torch.randint(0, 1 << 30, (2 * n,), device='cuda', dtype=torch.int32)
+for rep in range(2):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    y = torch.sort(x32).values; torch.cuda.synchronize(); t1 = time.perf_counter()
+    print(f"torch.sort int32 2n={2*n}: {1e3*(t1-t0):.2f} ms (4 passes)")
