@@ -158,32 +158,30 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     k[it] = i < n ? __ldcs(kin + i) : ~0ull;
     if (KV) v[it] = i < n ? __ldcs(vin + i) : 0u;
   }
-  // warp-level multisplit: rank of each key among equal digits of this warp's slice.  Peers
-  // with the same digit are found with one ballot per digit bit (MATCH.ANY's latency dominated
-  // the first version of this kernel).
+  // warp-level multisplit: rank of each key among equal digits of this warp's slice.  All
+  // match-any operations are issued first (independent, so their latency overlaps); the
+  // sequential per-warp counters are updated afterwards by one leader lane per digit group.
   const uint32_t lt = lanemask_lt();
+  uint32_t peers[kSortItems];
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) {
+    const uint64_t i = wbase + it * 32 + lane;
+    const uint32_t d = i < n ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u;
+    peers[it] = __match_any_sync(0xffffffffu, d);
+  }
 #pragma unroll
   for (int it = 0; it < kSortItems; it++) {
     const uint64_t i = wbase + it * 32 + lane;
     const bool in = i < n;
     const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
-    uint32_t peers = __ballot_sync(0xffffffffu, in);
-#pragma unroll
-    for (int b = 0; b < 8; b++) {
-      if ((uint32_t)b < bits) {
-        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bb : ~bb;
-      }
-    }
-    const int leader = 31 - __clz(peers);
+    const int leader = 31 - __clz(peers[it]);
     uint32_t base = 0;
     if (in && lane == leader) {
       base = s_warp_hist[warp][d];
-      s_warp_hist[warp][d] = base + __popc(peers);
+      s_warp_hist[warp][d] = base + __popc(peers[it]);
     }
     base = __shfl_sync(0xffffffffu, base, leader);
-    r[it] = base + __popc(peers & lt);
-    __syncwarp();
+    r[it] = base + __popc(peers[it] & lt);
   }
   __syncthreads();
 
