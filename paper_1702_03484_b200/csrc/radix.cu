@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
 
 // One stable digit pass.  Tile = kSortThreads x kSortItems keys; warp w owns the contiguous
 // slice [w*32*ITEMS, (w+1)*32*ITEMS) of its tile and reads it item-major (item it, lane l ->
-// slice[it*32 + l]) so every load is a coalesced 256 B row.
+// slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
+// full tiles skip every bounds check (the first version spent most of its issue slots on 64-bit
+// index arithmetic).
 template <bool KV>
 __global__ void __launch_bounds__(kSortThreads, 3)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
@@ -140,48 +142,55 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   __shared__ uint32_t s_wsum[kWarps];
   __shared__ uint32_t s_tile;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0;
+#pragma unroll
+  for (int q = 0; q < kWarps; q++) s_warp_hist[q][tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t tile_base = tile * kSortTile;
-  const uint64_t wbase = tile_base + (uint64_t)warp * 32 * kSortItems;
+  const uint64_t rem = n - tile_base;
+  const uint32_t tile_n = rem < (uint64_t)kSortTile ? (uint32_t)rem : (uint32_t)kSortTile;
+  const uint32_t wslice = warp * 32 * kSortItems;
   const uint32_t dmask = (1u << bits) - 1u;
+  const uint64_t *src = kin + tile_base + wslice + lane;
 
   uint64_t k[kSortItems];
-  uint32_t v[kSortItems];
+  uint32_t v[KV ? kSortItems : 1];
   uint32_t r[kSortItems];
-#pragma unroll
-  for (int it = 0; it < kSortItems; it++) {
-    const uint64_t i = wbase + it * 32 + lane;
-    k[it] = i < n ? __ldcs(kin + i) : ~0ull;
-    if (KV) v[it] = i < n ? __ldcs(vin + i) : 0u;
-  }
-  // warp-level multisplit: rank of each key among equal digits of this warp's slice.  All
-  // match-any operations are issued first (independent, so their latency overlaps); the
-  // sequential per-warp counters are updated afterwards by one leader lane per digit group.
-  const uint32_t lt = lanemask_lt();
   uint32_t peers[kSortItems];
+  if (tile_n == (uint32_t)kSortTile) {
 #pragma unroll
-  for (int it = 0; it < kSortItems; it++) {
-    const uint64_t i = wbase + it * 32 + lane;
-    const uint32_t d = i < n ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u;
-    peers[it] = __match_any_sync(0xffffffffu, d);
+    for (int it = 0; it < kSortItems; it++) k[it] = __ldcs(src + it * 32);
+    if (KV) {
+#pragma unroll
+      for (int it = 0; it < kSortItems; it++) v[KV ? it : 0] = __ldcs(vin + tile_base + wslice + lane + it * 32);
+    }
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++)
+      peers[it] = __match_any_sync(0xffffffffu, (uint32_t)(k[it] >> shift) & dmask);
+  } else {
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++) {
+      const bool in = wslice + it * 32 + lane < tile_n;
+      k[it] = in ? __ldcs(src + it * 32) : 0ull;
+      if (KV) v[KV ? it : 0] = in ? __ldcs(vin + tile_base + wslice + lane + it * 32) : 0u;
+      peers[it] = __match_any_sync(0xffffffffu, in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u);
+    }
   }
+  // warp-level multisplit: one leader lane per digit group bumps the warp's counter
+  const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < kSortItems; it++) {
-    const uint64_t i = wbase + it * 32 + lane;
-    const bool in = i < n;
     const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
-    const int leader = 31 - __clz(peers[it]);
+    const uint32_t leader = 31 - __clz(peers[it]);
+    const bool in = wslice + it * 32 + lane < tile_n;
     uint32_t base = 0;
     if (in && lane == leader) {
       base = s_warp_hist[warp][d];
       s_warp_hist[warp][d] = base + __popc(peers[it]);
     }
-    base = __shfl_sync(0xffffffffu, base, leader);
-    r[it] = base + __popc(peers[it] & lt);
+    r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[it] & lt);
   }
   __syncthreads();
 
@@ -200,25 +209,23 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     st_relaxed_u64(my_status, kFlagInc | total);
   } else {
     st_relaxed_u64(my_status, kFlagAgg | total);
-    // Windowed look-back: kLookWin predecessors are read at once (independent loads), so the
-    // walk to the nearest inclusive prefix costs one L2 round trip per kLookWin tiles instead of
-    // one per tile (the serial walk bounded the first version of this kernel).
+    // Windowed look-back: kLookWin predecessors are read at once (independent loads).
     int64_t t0 = (int64_t)tile - 1;
     while (true) {
-      uint64_t v[kLookWin];
+      uint64_t sv[kLookWin];
 #pragma unroll
       for (int w = 0; w < kLookWin; w++) {
         const int64_t t = t0 - w;
-        v[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
+        sv[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
       }
       int consumed = 0;
       bool done = false;
 #pragma unroll
       for (int w = 0; w < kLookWin; w++) {
         if (consumed != w || done) continue;
-        const uint64_t flag = v[w] & ~kValMask;
+        const uint64_t flag = sv[w] & ~kValMask;
         if (flag == 0) continue;  // not published yet: stop consuming here
-        excl += v[w] & kValMask;
+        excl += sv[w] & kValMask;
         consumed = w + 1;
         if (flag == kFlagInc) done = true;
       }
@@ -233,14 +240,14 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    if (lane >= (uint32_t)o) x += y;
   }
   if (lane == 31) s_wsum[warp] = x;
   __syncthreads();
   uint32_t pre = 0;
 #pragma unroll
   for (int w = 0; w < kWarps; w++)
-    if (w < warp) pre += s_wsum[w];
+    if ((uint32_t)w < warp) pre += s_wsum[w];
   const uint32_t dstart = pre + x - total;
   s_digit_start[d] = dstart;
   s_global_base[d] = (uint64_t)hist_pass[d] + excl - dstart;
@@ -249,22 +256,22 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   // place keys at their tile-local sorted slot
 #pragma unroll
   for (int it = 0; it < kSortItems; it++) {
-    const uint64_t i = wbase + it * 32 + lane;
-    if (i < n) {
+    if (wslice + it * 32 + lane < tile_n) {
       const uint32_t dd = (uint32_t)(k[it] >> shift) & dmask;
       const uint32_t slot = s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
       s_keys[slot] = k[it];
-      if (KV) s_vals[slot] = v[it];
+      if (KV) s_vals[slot] = v[KV ? it : 0];
     }
   }
   __syncthreads();
-  const uint32_t tile_n = (uint32_t)(n - tile_base < (uint64_t)kSortTile ? n - tile_base : (uint64_t)kSortTile);
+  // coalesced write-out: consecutive slots of one digit go to consecutive global positions
+#pragma unroll 4
   for (uint32_t i = tid; i < tile_n; i += kSortThreads) {
     const uint64_t key = s_keys[i];
     const uint32_t dd = (uint32_t)(key >> shift) & dmask;
     const uint64_t pos = s_global_base[dd] + i;
-    kout[pos] = key;
-    if (KV) vout[pos] = s_vals[i];
+    __stcs(kout + pos, key);
+    if (KV) __stcs(vout + pos, s_vals[i]);
   }
 }
 
