@@ -1,0 +1,250 @@
+// radix_ablate.cu — developer micro-benchmark (not product code): times the one-sweep digit
+// pass of paper_1702_03484_b200/csrc/radix.cu against ablated variants to locate its limiter.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include tools/radix_ablate.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1702_03484_b200/csrc/radix.cu"
+
+using namespace mapsq;
+
+// MODE bit 1: skip look-back (excl = 0); bit 2: skip ranking (identity slot); bit 4: plain
+// copy of the tile (no digit scatter); bit 8: no write-out at all.
+template <int MODE>
+__global__ void __launch_bounds__(kSortThreads, 3)
+ablate_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout, uint64_t n,
+              uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
+              uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
+  __shared__ uint32_t s_warp_hist[8][kRadix];
+  __shared__ uint32_t s_digit_start[kRadix];
+  __shared__ uint64_t s_global_base[kRadix];
+  __shared__ uint32_t s_wsum[8];
+  __shared__ uint32_t s_tile;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+#pragma unroll
+  for (int q = 0; q < 8; q++) s_warp_hist[q][tid] = 0;
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t tile_base = tile * kSortTile;
+  const uint32_t wslice = warp * 32 * kSortItems;
+  const uint32_t dmask = (1u << bits) - 1u;
+  const uint64_t *src = kin + tile_base + wslice + lane;
+  uint64_t k[kSortItems];
+  uint32_t r[kSortItems], peers[kSortItems];
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) k[it] = __ldcs(src + it * 32);
+  if (MODE & 4) {
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++) __stcs(kout + tile_base + wslice + lane + it * 32, k[it]);
+    return;
+  }
+  const uint32_t lt = lanemask_lt();
+  if (!(MODE & 2)) {
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++)
+      peers[it] = __match_any_sync(0xffffffffu, (uint32_t)(k[it] >> shift) & dmask);
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++) {
+      const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
+      const uint32_t leader = 31 - __clz(peers[it]);
+      uint32_t base = 0;
+      if (lane == leader) {
+        base = s_warp_hist[warp][d];
+        s_warp_hist[warp][d] = base + __popc(peers[it]);
+      }
+      r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[it] & lt);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < kSortItems; it++) {
+      r[it] = it * 32 + lane;
+      if (lane == 0) atomicAdd(&s_warp_hist[warp][(uint32_t)(k[it] >> shift) & dmask], 0u);
+    }
+  }
+  __syncthreads();
+  const uint32_t d = tid;
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < 8; w++) {
+    const uint32_t c = s_warp_hist[w][d];
+    s_warp_hist[w][d] = total;
+    total += c;
+  }
+  uint64_t excl = 0;
+  if (!(MODE & 1)) {
+    uint64_t *my_status = status + tile * kRadix + d;
+    if (tile == 0) {
+      st_relaxed_u64(my_status, kFlagInc | total);
+    } else {
+      st_relaxed_u64(my_status, kFlagAgg | total);
+      int64_t t0 = (int64_t)tile - 1;
+      while (true) {
+        uint64_t sv[8];
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+          const int64_t t = t0 - w;
+          sv[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
+        }
+        int consumed = 0;
+        bool done = false;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+          if (consumed != w || done) continue;
+          const uint64_t flag = sv[w] & ~kValMask;
+          if (flag == 0) continue;
+          excl += sv[w] & kValMask;
+          consumed = w + 1;
+          if (flag == kFlagInc) done = true;
+        }
+        if (done) break;
+        t0 -= consumed;
+        if (consumed < 8) __nanosleep(32);
+      }
+      st_relaxed_u64(my_status, kFlagInc | (excl + total));
+    }
+  } else {
+    excl = (tile * kSortTile) / kRadix;  // plausible spread, results are garbage
+  }
+  uint32_t x = total;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t pre = 0;
+#pragma unroll
+  for (int w = 0; w < 8; w++)
+    if ((uint32_t)w < warp) pre += s_wsum[w];
+  const uint32_t dstart = pre + x - total;
+  s_digit_start[d] = dstart;
+  s_global_base[d] = (uint64_t)hist_pass[d] + excl - dstart;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortItems; it++) {
+    const uint32_t dd = (uint32_t)(k[it] >> shift) & dmask;
+    const uint32_t slot = (MODE & 2) ? r[it] + wslice : s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
+    s_keys[slot & (kSortTile - 1)] = k[it];
+  }
+  __syncthreads();
+  if (MODE & 8) {
+    if (s_keys[tid] == 12345) kout[0] = 1;
+    return;
+  }
+#pragma unroll 4
+  for (uint32_t i = tid; i < kSortTile; i += kSortThreads) {
+    const uint64_t key = s_keys[i];
+    const uint32_t dd = (uint32_t)(key >> shift) & dmask;
+    const uint64_t pos = (s_global_base[dd] + i) % n;
+    __stcs(kout + pos, key);
+  }
+}
+
+template <int MODE>
+float run(const uint64_t *kin, uint64_t *kout, uint64_t n, uint32_t *hist, uint64_t *status,
+          uint32_t *ctr) {
+  const uint64_t ntiles = n / kSortTile;
+  const size_t smem = kSortTile * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int rep = 0; rep < 5; rep++) {
+    cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
+    cudaMemsetAsync(ctr, 0, 4);
+    cudaEventRecord(a);
+    ablate_kernel<MODE><<<(unsigned)ntiles, kSortThreads, smem>>>(kin, kout, n, 8, 8, hist, status, ctr);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int MODE>
+void report(const char *name, const uint64_t *kin, uint64_t *kout, uint64_t n, uint32_t *hist,
+            uint64_t *status, uint32_t *ctr) {
+  float ms = run<MODE>(kin, kout, n, hist, status, ctr);
+  printf("%-28s %8.3f ms  %7.1f GB/s (16 B/key)\n", name, ms, 16.0 * n / ms / 1e6);
+}
+
+int main(int argc, char **argv) {
+  const uint64_t n = (argc > 1 ? strtoull(argv[1], 0, 10) : 200000000ull) / kSortTile * kSortTile;
+  std::vector<uint64_t> h(n);
+  uint64_t x = 88172645463325252ull;
+  for (uint64_t i = 0; i < n; i++) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    h[i] = (x & ~0xffffffffull) | i;  // random high bits, index low bits
+  }
+  uint64_t *kin, *kout, *status;
+  uint32_t *hist, *ctr;
+  cudaMalloc(&kin, n * 8);
+  cudaMalloc(&kout, n * 8);
+  cudaMalloc(&status, (n / kSortTile) * kRadix * 8);
+  cudaMalloc(&hist, 8 * kRadix * 4);
+  cudaMalloc(&ctr, 4);
+  cudaMemcpy(kin, h.data(), n * 8, cudaMemcpyHostToDevice);
+  // exact digit offsets of bits [8,16) for the real pass
+  std::vector<uint32_t> hh(kRadix, 0);
+  for (uint64_t i = 0; i < n; i++) hh[(h[i] >> 8) & 255]++;
+  uint32_t run_ = 0;
+  for (int d = 0; d < kRadix; d++) { uint32_t c = hh[d]; hh[d] = run_; run_ += c; }
+  cudaMemcpy(hist, hh.data(), kRadix * 4, cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(ablate_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortTile * 8);
+  report<0>("full pass", kin, kout, n, hist, status, ctr);
+  report<1>("no look-back", kin, kout, n, hist, status, ctr);
+  report<2>("no ranking", kin, kout, n, hist, status, ctr);
+  report<3>("no ranking, no look-back", kin, kout, n, hist, status, ctr);
+  report<4>("tile copy (same shape)", kin, kout, n, hist, status, ctr);
+  report<8>("no write-out", kin, kout, n, hist, status, ctr);
+  report<9>("no write-out, no look-back", kin, kout, n, hist, status, ctr);
+  // the library's real pass for comparison
+  {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e9;
+    for (int rep = 0; rep < 5; rep++) {
+      cudaMemsetAsync(status, 0, (n / kSortTile) * kRadix * 8);
+      cudaMemsetAsync(ctr, 0, 4);
+      cudaEventRecord(a);
+      launch_radix_pass(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, 0);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = ms < best ? ms : best;
+    }
+    printf("%-28s %8.3f ms  %7.1f GB/s\n", "library radix_pass", best, 16.0 * n / best / 1e6);
+    std::vector<uint64_t> o(n);
+    cudaMemcpy(o.data(), kout, n * 8, cudaMemcpyDeviceToHost);
+    bool ok = true;
+    for (uint64_t i = 1; i < n && ok; i++) ok = ((o[i - 1] >> 8) & 255) <= ((o[i] >> 8) & 255);
+    printf("library pass digit order ok: %d  err=%s\n", (int)ok, cudaGetErrorString(cudaGetLastError()));
+  }
+  // plain copy reference
+  {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e9;
+    for (int rep = 0; rep < 5; rep++) {
+      cudaEventRecord(a);
+      cudaMemcpyAsync(kout, kin, n * 8, cudaMemcpyDeviceToDevice);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = ms < best ? ms : best;
+    }
+    printf("%-28s %8.3f ms  %7.1f GB/s\n", "cudaMemcpy D2D", best, 16.0 * n / best / 1e6);
+  }
+  return 0;
+}
