@@ -275,171 +275,6 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   }
 }
 
-// Persistent one-sweep digit pass (P64 words).  Each CTA loops over tiles claimed in order from
-// the atomic counter; while it ranks / looks back / scatters tile t, the TMA engine already
-// streams the NEXT claimed tile into the other shared-memory buffer (cp.async.bulk + mbarrier),
-// so DRAM reads stay in flight through the rank and look-back phases that idled the
-// one-tile-per-CTA version.  Claiming in order keeps the look-back deadlock free: the smallest
-// unfinished claimed tile only waits on finished tiles.
-constexpr int kTmaCtasPerSm = 2;
-constexpr size_t kTmaSmem = 3ull * kSortTile * sizeof(uint64_t);
-
-__global__ void __launch_bounds__(kSortThreads, kTmaCtasPerSm)
-radix_pass_tma_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout, uint64_t n,
-                      uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
-                      uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t *s_out = reinterpret_cast<uint64_t *>(smem_raw + 2 * kSortTile * sizeof(uint64_t));
-  __shared__ __align__(8) uint64_t s_bar[2];
-  __shared__ uint32_t s_warp_hist[kWarps][kRadix];
-  __shared__ uint32_t s_digit_start[kRadix];
-  __shared__ uint64_t s_global_base[kRadix];
-  __shared__ uint32_t s_wsum[kWarps];
-  __shared__ uint32_t s_tile[2];
-
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t ntiles = ceil_div(n, kSortTile);
-  const uint32_t dmask = (1u << bits) - 1u;
-  const uint32_t wslice = warp * 32 * kSortItems;
-  const uint32_t lt = lanemask_lt();
-
-  auto issue = [&](uint32_t t, int buf) {  // tid 0 only
-    const uint64_t base = (uint64_t)t * kSortTile;
-    const uint64_t rem = n - base;
-    const uint32_t cnt = rem < (uint64_t)kSortTile ? (uint32_t)rem : (uint32_t)kSortTile;
-    const uint32_t bulk = cnt & ~1u;  // 16 B granularity
-    uint64_t *dst = reinterpret_cast<uint64_t *>(smem_raw + (size_t)buf * kSortTile * sizeof(uint64_t));
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&s_bar[buf], bulk * 8u);
-    if (bulk) bulk_g2s(dst, kin + base, bulk * 8u, &s_bar[buf]);
-  };
-
-  if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    fence_mbar_init();
-    const uint32_t t = atomicAdd(tile_counter, 1u);
-    s_tile[0] = t;
-    if (t < ntiles) issue(t, 0);
-  }
-  __syncthreads();
-  uint32_t phase0 = 0, phase1 = 0;
-  for (int b = 0;; b ^= 1) {
-    const uint32_t tile = s_tile[b];
-    if (tile >= ntiles) break;
-    uint64_t *s_in = reinterpret_cast<uint64_t *>(smem_raw + (size_t)b * kSortTile * sizeof(uint64_t));
-    if (tid == 0) {  // claim + prefetch the next tile into the other buffer
-      const uint32_t t2 = atomicAdd(tile_counter, 1u);
-      s_tile[b ^ 1] = t2;
-      if (t2 < ntiles) issue(t2, b ^ 1);
-    }
-#pragma unroll
-    for (int q = 0; q < kWarps; q++) s_warp_hist[q][tid] = 0;
-    const uint64_t tile_base = (uint64_t)tile * kSortTile;
-    const uint64_t rem = n - tile_base;
-    const uint32_t tile_n = rem < (uint64_t)kSortTile ? (uint32_t)rem : (uint32_t)kSortTile;
-    if (b == 0) { mbar_wait(&s_bar[0], phase0); phase0 ^= 1; }
-    else { mbar_wait(&s_bar[1], phase1); phase1 ^= 1; }
-    if (tid == 0 && (tile_n & 1u)) s_in[tile_n - 1] = kin[tile_base + tile_n - 1];
-    __syncthreads();
-
-    uint64_t k[kSortItems];
-    uint32_t r[kSortItems], peers[kSortItems];
-    const bool full = tile_n == (uint32_t)kSortTile;
-#pragma unroll
-    for (int it = 0; it < kSortItems; it++) {
-      const uint32_t loc = wslice + it * 32 + lane;
-      const bool in = full || loc < tile_n;
-      k[it] = s_in[loc];
-      peers[it] = __match_any_sync(0xffffffffu, in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u);
-    }
-#pragma unroll
-    for (int it = 0; it < kSortItems; it++) {
-      const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
-      const uint32_t leader = 31 - __clz(peers[it]);
-      const bool in = full || wslice + it * 32 + lane < tile_n;
-      uint32_t base = 0;
-      if (in && lane == leader) {
-        base = s_warp_hist[warp][d];
-        s_warp_hist[warp][d] = base + __popc(peers[it]);
-      }
-      r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[it] & lt);
-    }
-    __syncthreads();
-
-    const uint32_t d = tid;
-    uint32_t total = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; w++) {
-      const uint32_t c = s_warp_hist[w][d];
-      s_warp_hist[w][d] = total;
-      total += c;
-    }
-    uint64_t *my_status = status + (uint64_t)tile * kRadix + d;
-    uint64_t excl = 0;
-    if (tile == 0) {
-      st_relaxed_u64(my_status, kFlagInc | total);
-    } else {
-      st_relaxed_u64(my_status, kFlagAgg | total);
-      int64_t t0 = (int64_t)tile - 1;
-      while (true) {
-        uint64_t sv[kLookWin];
-#pragma unroll
-        for (int w = 0; w < kLookWin; w++) {
-          const int64_t t = t0 - w;
-          sv[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
-        }
-        int consumed = 0;
-        bool done = false;
-#pragma unroll
-        for (int w = 0; w < kLookWin; w++) {
-          if (consumed != w || done) continue;
-          const uint64_t flag = sv[w] & ~kValMask;
-          if (flag == 0) continue;
-          excl += sv[w] & kValMask;
-          consumed = w + 1;
-          if (flag == kFlagInc) done = true;
-        }
-        if (done) break;
-        t0 -= consumed;
-        if (consumed < kLookWin) __nanosleep(32);
-      }
-      st_relaxed_u64(my_status, kFlagInc | (excl + total));
-    }
-    uint32_t x = total;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= (uint32_t)o) x += y;
-    }
-    if (lane == 31) s_wsum[warp] = x;
-    __syncthreads();
-    uint32_t pre = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; w++)
-      if ((uint32_t)w < warp) pre += s_wsum[w];
-    const uint32_t dstart = pre + x - total;
-    s_digit_start[d] = dstart;
-    s_global_base[d] = (uint64_t)hist_pass[d] + excl - dstart;
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < kSortItems; it++) {
-      if (full || wslice + it * 32 + lane < tile_n) {
-        const uint32_t dd = (uint32_t)(k[it] >> shift) & dmask;
-        s_out[s_digit_start[dd] + s_warp_hist[warp][dd] + r[it]] = k[it];
-      }
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (uint32_t i = tid; i < tile_n; i += kSortThreads) {
-      const uint64_t key = s_out[i];
-      const uint32_t dd = (uint32_t)(key >> shift) & dmask;
-      __stcs(kout + s_global_base[dd] + i, key);
-    }
-    __syncthreads();  // s_out, histograms and s_in[b] are reused by the next iterations
-  }
-}
-
 }  // namespace
 
 static int grid_for(uint64_t n, int per_block) {
@@ -478,23 +313,6 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, cudaStream_t s) {
   const uint64_t ntiles = ceil_div(n, kSortTile);
-  if (!vin && ((uintptr_t)kin & 15) == 0) {
-    static int grid = 0;
-    if (!grid) {
-      cudaFuncSetAttribute(radix_pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kTmaSmem);
-      int dev = 0, sms = 148, occ = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, radix_pass_tma_kernel, kSortThreads,
-                                                    kTmaSmem);
-      grid = sms * std::max(occ, 1);
-    }
-    const unsigned g = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)grid);
-    radix_pass_tma_kernel<<<g, kSortThreads, kTmaSmem, s>>>(kin, kout, n, shift, bits, hist_pass,
-                                                           status, tile_counter);
-    return;
-  }
   if (vin) {
     const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
     static bool attr = false;
