@@ -17,163 +17,158 @@ namespace {
 
 constexpr int kWarps = kScanThreads / 32;
 
-__device__ __forceinline__ bool pat_match(const ScanPat &p, uint32_t s, uint32_t pp, uint32_t o) {
-  bool ok = true;
-  if (p.const_mask & 1) ok &= (s == p.id[0]);
-  if (p.const_mask & 2) ok &= (pp == p.id[1]);
-  if (p.const_mask & 4) ok &= (o == p.id[2]);
-  if (p.eq_mask & 1) ok &= (s == pp);
-  if (p.eq_mask & 2) ok &= (s == o);
-  if (p.eq_mask & 4) ok &= (pp == o);
+// A pattern's constant tests as masked XORs: match <=> ((s^cs)&ms | (p^cp)&mp | (o^co)&mo) == 0,
+// plus the rare repeated-variable equalities.
+struct PatTest {
+  uint32_t cs, cp, co, ms, mp, mo, eq;
+};
+__device__ __forceinline__ PatTest pat_test(const ScanPat &p) {
+  PatTest t;
+  t.ms = (p.const_mask & 1) ? ~0u : 0u;
+  t.mp = (p.const_mask & 2) ? ~0u : 0u;
+  t.mo = (p.const_mask & 4) ? ~0u : 0u;
+  t.cs = p.id[0] & t.ms;
+  t.cp = p.id[1] & t.mp;
+  t.co = p.id[2] & t.mo;
+  t.eq = p.eq_mask;
+  return t;
+}
+__device__ __forceinline__ bool pat_eval(const PatTest &t, uint32_t s, uint32_t p, uint32_t o) {
+  bool ok = (((s ^ t.cs) & t.ms) | ((p ^ t.cp) & t.mp) | ((o ^ t.co) & t.mo)) == 0u;
+  if (t.eq) {  // warp-uniform
+    if (t.eq & 1) ok &= (s == p);
+    if (t.eq & 2) ok &= (s == o);
+    if (t.eq & 4) ok &= (p == o);
+  }
   return ok;
 }
 
-// Patterns are evaluated in a runtime loop over descriptors staged in shared memory (no unroll
-// over MAPSQ_MAX_PATTERNS: that blew the instruction cache).
+// Pass 1 (predicate).  Warp w of tile T owns 32 match words (1024 triples); lane l reads triple
+// (word0 + w') * 32 + l of every word w' (coalesced 128 B rows) into registers once, then every
+// pattern is evaluated over the 32 register-resident rows with its constants hoisted.
+template <int NEED>
 __global__ void __launch_bounds__(kScanThreads)
 scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
                   const uint32_t *__restrict__ O, uint64_t n, const ScanArgs a,
                   uint32_t *__restrict__ masks, uint64_t mask_words,
                   uint32_t *__restrict__ tile_counts, uint64_t ntiles) {
-  __shared__ ScanPat s_pat[MAPSQ_MAX_PATTERNS];
-  __shared__ uint32_t s_mw[kWarps][MAPSQ_MAX_PATTERNS][kScanWordsPerWarp];
   __shared__ uint32_t s_cnt[kWarps][MAPSQ_MAX_PATTERNS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = a.k;
-  if (threadIdx.x < (unsigned)k) s_pat[threadIdx.x] = a.pat[threadIdx.x];
-  __syncthreads();
   const uint64_t tile = blockIdx.x;
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
-  const bool ns = a.need_count & 1, np = a.need_count & 2, no = a.need_count & 4;
-#pragma unroll 1
-  for (int w = 0; w < kScanWordsPerWarp; w += 8) {
-    uint32_t vs[8], vp[8], vo[8];
+  const uint64_t base = word0 * 32 + lane;
+  const bool full = (word0 + kScanWordsPerWarp) * 32 <= n;
+  uint32_t vs[kScanWordsPerWarp], vp[kScanWordsPerWarp], vo[kScanWordsPerWarp];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint64_t i = (word0 + w + u) * 32 + lane;
-      const bool in = i < n;
-      vs[u] = (ns && in) ? __ldcs(S + i) : 0u;
-      vp[u] = (np && in) ? __ldcs(P + i) : 0u;
-      vo[u] = (no && in) ? __ldcs(O + i) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const bool in = (word0 + w + u) * 32 + lane < n;
-#pragma unroll 1
-      for (int j = 0; j < k; j++) {
-        const uint32_t m = __ballot_sync(0xffffffffu, in && pat_match(s_pat[j], vs[u], vp[u], vo[u]));
-        if (lane == 0) s_mw[warp][j][w + u] = m;
-      }
-    }
+  for (int w = 0; w < kScanWordsPerWarp; w++) {
+    const uint64_t i = base + (uint64_t)w * 32;
+    const bool in = full || i < n;
+    vs[w] = ((NEED & 1) && in) ? __ldcs(S + i) : 0u;
+    vp[w] = ((NEED & 2) && in) ? __ldcs(P + i) : 0u;
+    vo[w] = ((NEED & 4) && in) ? __ldcs(O + i) : 0u;
   }
-  __syncwarp();
   const uint64_t my_word = word0 + lane;
-  for (int j = 0; j < k; j++) {
-    const uint32_t m = s_mw[warp][j][lane];
-    if (my_word < mask_words) masks[(uint64_t)j * mask_words + my_word] = m;
-    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(m));
+  for (int j = 0; j < a.k; j++) {
+    const PatTest t = pat_test(a.pat[j]);
+    uint32_t mine = 0;
+#pragma unroll
+    for (int w = 0; w < kScanWordsPerWarp; w++) {
+      const bool in = full || base + (uint64_t)w * 32 < n;
+      const uint32_t m = __ballot_sync(0xffffffffu, in && pat_eval(t, vs[w], vp[w], vo[w]));
+      mine = (lane == w) ? m : mine;
+    }
+    if (my_word < mask_words) masks[(uint64_t)j * mask_words + my_word] = mine;
+    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(mine));
     if (lane == 0) s_cnt[warp][j] = c;
   }
   __syncthreads();
-  if (threadIdx.x < (unsigned)k) {
+  if (threadIdx.x < (unsigned)a.k) {
     uint32_t t = 0;
     for (int w = 0; w < kWarps; w++) t += s_cnt[w][threadIdx.x];
     tile_counts[(uint64_t)threadIdx.x * ntiles + tile] = t;
   }
 }
 
+// Pass 2 (gather), pattern-outer: for pattern j the warp walks its 32 words with the output
+// cursor and the column bounds in registers, loading s/p/o only for matching lanes.
 __global__ void __launch_bounds__(kScanThreads)
 scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
                   const uint32_t *__restrict__ O, uint64_t n, const ScanArgs a,
                   const uint32_t *__restrict__ masks, uint64_t mask_words,
                   const uint64_t *__restrict__ tile_off, uint64_t ntiles, const ScanOut out,
                   uint32_t *__restrict__ bmin, uint32_t *__restrict__ bmax) {
-  __shared__ ScanPat s_pat[MAPSQ_MAX_PATTERNS];
-  __shared__ uint32_t s_mw[kWarps][MAPSQ_MAX_PATTERNS][kScanWordsPerWarp];
   __shared__ uint32_t s_wcnt[kWarps][MAPSQ_MAX_PATTERNS];
-  __shared__ uint64_t s_cur[kWarps][MAPSQ_MAX_PATTERNS];
   __shared__ uint32_t s_min[kWarps][MAPSQ_MAX_PATTERNS * 3], s_max[kWarps][MAPSQ_MAX_PATTERNS * 3];
-  __shared__ uint32_t *s_out[MAPSQ_MAX_PATTERNS * 3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.k;
   const uint64_t tile = blockIdx.x;
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
   const uint64_t my_word = word0 + lane;
-  if (threadIdx.x < MAPSQ_MAX_PATTERNS * 3) s_out[threadIdx.x] = out.col[threadIdx.x];
-  if (threadIdx.x < (unsigned)k) s_pat[threadIdx.x] = a.pat[threadIdx.x];
-  for (int j = lane; j < MAPSQ_MAX_PATTERNS * 3; j += 32) {
-    s_min[warp][j] = 0xffffffffu;
-    s_max[warp][j] = 0u;
-  }
-  uint32_t any_mine = 0;  // OR over patterns of this lane's word
+  const uint64_t base = word0 * 32 + lane;
   for (int j = 0; j < k; j++) {
     const uint32_t m = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
-    s_mw[warp][j][lane] = m;
-    any_mine |= m;
     const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(m));
     if (lane == 0) s_wcnt[warp][j] = c;
   }
   __syncthreads();
-  if (lane < k) {
-    // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
-    uint64_t c = tile_off[(uint64_t)lane * ntiles + tile] - tile_off[(uint64_t)lane * ntiles];
-    for (int w = 0; w < warp; w++) c += s_wcnt[w][lane];
-    s_cur[warp][lane] = c;
-  }
-  __syncwarp();
-  const bool ws = a.need_write & 1, wp = a.need_write & 2, wo = a.need_write & 4;
   const uint32_t lt = lanemask_lt();
-#pragma unroll 1
-  for (int w = 0; w < kScanWordsPerWarp; w += 8) {
-    uint32_t vs[8], vp[8], vo[8], any[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t m = __shfl_sync(0xffffffffu, any_mine, w + u);
-      any[u] = m;
-      const uint64_t i = (word0 + w + u) * 32 + lane;
-      const bool hit = (m >> lane) & 1u;
-      vs[u] = (ws && hit) ? __ldcs(S + i) : 0u;
-      vp[u] = (wp && hit) ? __ldcs(P + i) : 0u;
-      vo[u] = (wo && hit) ? __ldcs(O + i) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      if (any[u] == 0) continue;  // warp-uniform
-#pragma unroll 1
-      for (int j = 0; j < k; j++) {
-        const uint32_t m = s_mw[warp][j][w + u];
-        if (m == 0) continue;
-        const bool hit = (m >> lane) & 1u;
-        const uint64_t base = s_cur[warp][j];
-        const uint64_t pos = base + __popc(m & lt);
-        const uint32_t nc = s_pat[j].ncols;
-        for (uint32_t c = 0; c < nc; c++) {
-          const uint32_t src = s_pat[j].src[c];
-          const uint32_t v = src == 0 ? vs[u] : (src == 1 ? vp[u] : vo[u]);
-          if (hit) st_cs_u32(s_out[j * 3 + c] + pos, v);
-          const uint32_t mn = __reduce_min_sync(0xffffffffu, hit ? v : 0xffffffffu);
-          const uint32_t mx = __reduce_max_sync(0xffffffffu, hit ? v : 0u);
-          if (lane == 0) {
-            s_min[warp][j * 3 + c] = min(s_min[warp][j * 3 + c], mn);
-            s_max[warp][j * 3 + c] = max(s_max[warp][j * 3 + c], mx);
+  for (int j = 0; j < k; j++) {
+    const uint32_t mine = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
+    // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
+    uint64_t cur = tile_off[(uint64_t)j * ntiles + tile] - tile_off[(uint64_t)j * ntiles];
+    for (int w = 0; w < warp; w++) cur += s_wcnt[w][j];
+    const ScanPat &pt = a.pat[j];
+    const uint32_t nc = pt.ncols, src0 = pt.src[0], src1 = pt.src[1], src2 = pt.src[2];
+    uint32_t *o0 = out.col[j * 3], *o1 = out.col[j * 3 + 1], *o2 = out.col[j * 3 + 2];
+    uint32_t mn0 = ~0u, mn1 = ~0u, mn2 = ~0u, mx0 = 0, mx1 = 0, mx2 = 0;
+#pragma unroll 4
+    for (int w = 0; w < kScanWordsPerWarp; w++) {
+      const uint32_t m = __shfl_sync(0xffffffffu, mine, w);
+      if (m == 0) continue;  // warp-uniform
+      if ((m >> lane) & 1u) {
+        const uint64_t i = base + (uint64_t)w * 32;
+        const uint64_t pos = cur + __popc(m & lt);
+        const uint32_t v0 = src0 == 0 ? __ldcs(S + i) : (src0 == 1 ? __ldcs(P + i) : __ldcs(O + i));
+        st_cs_u32(o0 + pos, v0);
+        mn0 = min(mn0, v0);
+        mx0 = max(mx0, v0);
+        if (nc > 1) {
+          const uint32_t v1 = src1 == 0 ? __ldcs(S + i) : (src1 == 1 ? __ldcs(P + i) : __ldcs(O + i));
+          st_cs_u32(o1 + pos, v1);
+          mn1 = min(mn1, v1);
+          mx1 = max(mx1, v1);
+          if (nc > 2) {
+            const uint32_t v2 = src2 == 0 ? __ldcs(S + i) : (src2 == 1 ? __ldcs(P + i) : __ldcs(O + i));
+            st_cs_u32(o2 + pos, v2);
+            mn2 = min(mn2, v2);
+            mx2 = max(mx2, v2);
           }
         }
-        __syncwarp();
-        if (lane == 0) s_cur[warp][j] = base + __popc(m);
-        __syncwarp();
       }
+      cur += __popc(m);
+    }
+    mn0 = __reduce_min_sync(0xffffffffu, mn0);
+    mx0 = __reduce_max_sync(0xffffffffu, mx0);
+    mn1 = __reduce_min_sync(0xffffffffu, mn1);
+    mx1 = __reduce_max_sync(0xffffffffu, mx1);
+    mn2 = __reduce_min_sync(0xffffffffu, mn2);
+    mx2 = __reduce_max_sync(0xffffffffu, mx2);
+    if (lane == 0) {
+      s_min[warp][j * 3] = mn0; s_max[warp][j * 3] = mx0;
+      s_min[warp][j * 3 + 1] = mn1; s_max[warp][j * 3 + 1] = mx1;
+      s_min[warp][j * 3 + 2] = mn2; s_max[warp][j * 3 + 2] = mx2;
     }
   }
   __syncthreads();
   if (threadIdx.x < (unsigned)k * 3) {
     const int j = threadIdx.x / 3, c = threadIdx.x % 3;
-    if ((uint32_t)c < s_pat[j].ncols) {
+    if ((uint32_t)c < a.pat[j].ncols) {
       uint32_t mn = 0xffffffffu, mx = 0;
       for (int w = 0; w < kWarps; w++) {
         mn = min(mn, s_min[w][threadIdx.x]);
         mx = max(mx, s_max[w][threadIdx.x]);
       }
-      if (mn != 0xffffffffu || mx != 0) {
+      if (mn <= mx) {  // at least one match in this tile
         atomicMin(bmin + threadIdx.x, mn);
         atomicMax(bmax + threadIdx.x, mx);
       }
@@ -306,8 +301,19 @@ minmax_kernel(const uint32_t *__restrict__ col, uint64_t n, uint32_t *__restrict
 void launch_scan_count(const mapsq_triples &T, const ScanArgs &a, uint32_t *masks,
                        uint64_t mask_words, uint32_t *tile_counts, uint64_t ntiles,
                        cudaStream_t s) {
-  scan_count_kernel<<<(unsigned)ntiles, kScanThreads, 0, s>>>(T.s, T.p, T.o, T.n, a, masks,
-                                                              mask_words, tile_counts, ntiles);
+#define MAPSQ_SCAN_COUNT(NEED)                                                              \
+  scan_count_kernel<NEED><<<(unsigned)ntiles, kScanThreads, 0, s>>>(T.s, T.p, T.o, T.n, a, masks, \
+                                                                   mask_words, tile_counts, ntiles)
+  switch (a.need_count & 7) {
+    case 1: MAPSQ_SCAN_COUNT(1); break;
+    case 2: MAPSQ_SCAN_COUNT(2); break;
+    case 3: MAPSQ_SCAN_COUNT(3); break;
+    case 4: MAPSQ_SCAN_COUNT(4); break;
+    case 5: MAPSQ_SCAN_COUNT(5); break;
+    case 6: MAPSQ_SCAN_COUNT(6); break;
+    default: MAPSQ_SCAN_COUNT(7); break;
+  }
+#undef MAPSQ_SCAN_COUNT
 }
 
 void launch_scan_write(const mapsq_triples &T, const ScanArgs &a, const uint32_t *masks,
