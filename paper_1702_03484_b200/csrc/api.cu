@@ -521,6 +521,8 @@ mapsq_status build_scan_args(mapsq_ctx *ctx, const mapsq_pattern *pats, int k, S
       if (v == -1) {
         p.const_mask |= 1u << q;
         p.id[q] = pats[j].id[q];
+        p.c[q] = pats[j].id[q];
+        p.m[q] = ~0u;
         a->need_count |= 1u << q;
         continue;
       }

@@ -214,6 +214,8 @@ struct ScanPat {
   uint32_t eq_mask;      // bit 0: s==p, bit 1: s==o, bit 2: p==o required
   uint32_t ncols;
   uint32_t src[3];       // output column c takes position src[c]
+  // the constant tests as masked XORs: match <=> ((s^c[0])&m[0] | (p^c[1])&m[1] | (o^c[2])&m[2]) == 0
+  uint32_t c[3], m[3];
 };
 struct ScanArgs {
   int k;

@@ -17,35 +17,20 @@ namespace {
 
 constexpr int kWarps = kScanThreads / 32;
 
-// A pattern's constant tests as masked XORs: match <=> ((s^cs)&ms | (p^cp)&mp | (o^co)&mo) == 0,
-// plus the rare repeated-variable equalities.
-struct PatTest {
-  uint32_t cs, cp, co, ms, mp, mo, eq;
-};
-__device__ __forceinline__ PatTest pat_test(const ScanPat &p) {
-  PatTest t;
-  t.ms = (p.const_mask & 1) ? ~0u : 0u;
-  t.mp = (p.const_mask & 2) ? ~0u : 0u;
-  t.mo = (p.const_mask & 4) ? ~0u : 0u;
-  t.cs = p.id[0] & t.ms;
-  t.cp = p.id[1] & t.mp;
-  t.co = p.id[2] & t.mo;
-  t.eq = p.eq_mask;
-  return t;
-}
-__device__ __forceinline__ bool pat_eval(const PatTest &t, uint32_t s, uint32_t p, uint32_t o) {
-  bool ok = (((s ^ t.cs) & t.ms) | ((p ^ t.cp) & t.mp) | ((o ^ t.co) & t.mo)) == 0u;
-  if (t.eq) {  // warp-uniform
-    if (t.eq & 1) ok &= (s == p);
-    if (t.eq & 2) ok &= (s == o);
-    if (t.eq & 4) ok &= (p == o);
-  }
-  return ok;
-}
-
 // Pass 1 (predicate).  Warp w of tile T owns 32 match words (1024 triples); lane l reads triple
 // (word0 + w') * 32 + l of every word w' (coalesced 128 B rows) into registers once, then every
-// pattern is evaluated over the 32 register-resident rows with its constants hoisted.
+// pattern is evaluated over the 32 register-resident rows with its constants hoisted: one
+// masked-XOR test (precomputed on the host), one ballot and one select per word and pattern.
+template <int NEED>
+__device__ __forceinline__ bool const_test(const uint32_t c[3], const uint32_t m[3], uint32_t s,
+                                           uint32_t p, uint32_t o) {
+  uint32_t x = 0;
+  if (NEED & 1) x |= (s ^ c[0]) & m[0];
+  if (NEED & 2) x |= (p ^ c[1]) & m[1];
+  if (NEED & 4) x |= (o ^ c[2]) & m[2];
+  return x == 0;
+}
+
 template <int NEED>
 __global__ void __launch_bounds__(kScanThreads)
 scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
@@ -58,28 +43,62 @@ scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
   const uint64_t base = word0 * 32 + lane;
   const bool full = (word0 + kScanWordsPerWarp) * 32 <= n;
+  // rows past n read as an impossible triple (never matches: tail words are masked below)
   uint32_t vs[kScanWordsPerWarp], vp[kScanWordsPerWarp], vo[kScanWordsPerWarp];
-#pragma unroll
-  for (int w = 0; w < kScanWordsPerWarp; w++) {
-    const uint64_t i = base + (uint64_t)w * 32;
-    const bool in = full || i < n;
-    vs[w] = ((NEED & 1) && in) ? __ldcs(S + i) : 0u;
-    vp[w] = ((NEED & 2) && in) ? __ldcs(P + i) : 0u;
-    vo[w] = ((NEED & 4) && in) ? __ldcs(O + i) : 0u;
-  }
-  const uint64_t my_word = word0 + lane;
-  for (int j = 0; j < a.k; j++) {
-    const PatTest t = pat_test(a.pat[j]);
-    uint32_t mine = 0;
+  if (full) {
 #pragma unroll
     for (int w = 0; w < kScanWordsPerWarp; w++) {
-      const bool in = full || base + (uint64_t)w * 32 < n;
-      const uint32_t m = __ballot_sync(0xffffffffu, in && pat_eval(t, vs[w], vp[w], vo[w]));
-      mine = (lane == w) ? m : mine;
+      const uint64_t i = base + (uint64_t)w * 32;
+      vs[w] = (NEED & 1) ? __ldcs(S + i) : 0u;
+      vp[w] = (NEED & 2) ? __ldcs(P + i) : 0u;
+      vo[w] = (NEED & 4) ? __ldcs(O + i) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < kScanWordsPerWarp; w++) {
+      const uint64_t i = base + (uint64_t)w * 32;
+      const bool in = i < n;
+      vs[w] = ((NEED & 1) && in) ? __ldcs(S + i) : 0u;
+      vp[w] = ((NEED & 2) && in) ? __ldcs(P + i) : 0u;
+      vo[w] = ((NEED & 4) && in) ? __ldcs(O + i) : 0u;
+    }
+  }
+  // valid-lane mask of word w: all lanes for full warps, else lanes with index < n
+  const uint64_t nlim = n;
+  const uint64_t my_word = word0 + lane;
+  for (int j = 0; j < a.k; j++) {
+    uint32_t c[3], m[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      c[q] = a.pat[j].c[q];
+      m[q] = a.pat[j].m[q];
+    }
+    const uint32_t eq = a.pat[j].eq_mask;
+    uint32_t mine = 0;
+    if (eq == 0) {
+#pragma unroll
+      for (int w = 0; w < kScanWordsPerWarp; w++) {
+        const uint32_t bw = __ballot_sync(0xffffffffu, const_test<NEED>(c, m, vs[w], vp[w], vo[w]));
+        mine = (lane == w) ? bw : mine;
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < kScanWordsPerWarp; w++) {
+        bool ok = const_test<NEED>(c, m, vs[w], vp[w], vo[w]);
+        if (eq & 1) ok &= vs[w] == vp[w];
+        if (eq & 2) ok &= vs[w] == vo[w];
+        if (eq & 4) ok &= vp[w] == vo[w];
+        const uint32_t bw = __ballot_sync(0xffffffffu, ok);
+        mine = (lane == w) ? bw : mine;
+      }
+    }
+    if (!full) {  // clear bits of rows >= n
+      const uint64_t first = my_word * 32;
+      mine = first >= nlim ? 0u : (nlim - first >= 32 ? mine : mine & ((1u << (nlim - first)) - 1u));
     }
     if (my_word < mask_words) masks[(uint64_t)j * mask_words + my_word] = mine;
-    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(mine));
-    if (lane == 0) s_cnt[warp][j] = c;
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(mine));
+    if (lane == 0) s_cnt[warp][j] = cnt;
   }
   __syncthreads();
   if (threadIdx.x < (unsigned)a.k) {
@@ -89,8 +108,15 @@ scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
   }
 }
 
-// Pass 2 (gather), pattern-outer: for pattern j the warp walks its 32 words with the output
-// cursor and the column bounds in registers, loading s/p/o only for matching lanes.
+// Pass 2 (gather), pattern-outer: for pattern j the warp walks its 32 words in batches of 8,
+// first issuing every matching lane's loads of the batch (independent, so their latency
+// overlaps), then writing them at the output cursor; cursor and column bounds live in
+// registers.  Only the 32 B sectors holding matches are read.
+__device__ __forceinline__ uint32_t pick(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
+                                         const uint32_t *__restrict__ O, uint32_t src, uint64_t i) {
+  return __ldcs((src == 0 ? S : (src == 1 ? P : O)) + i);
+}
+
 __global__ void __launch_bounds__(kScanThreads)
 scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
                   const uint32_t *__restrict__ O, uint64_t n, const ScanArgs a,
@@ -114,38 +140,54 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
   const uint32_t lt = lanemask_lt();
   for (int j = 0; j < k; j++) {
     const uint32_t mine = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
+    if (__ballot_sync(0xffffffffu, mine != 0) == 0) {
+      if (lane == 0) {
+        for (int c = 0; c < 3; c++) {
+          s_min[warp][j * 3 + c] = ~0u;
+          s_max[warp][j * 3 + c] = 0;
+        }
+      }
+      continue;
+    }
     // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
     uint64_t cur = tile_off[(uint64_t)j * ntiles + tile] - tile_off[(uint64_t)j * ntiles];
     for (int w = 0; w < warp; w++) cur += s_wcnt[w][j];
-    const ScanPat &pt = a.pat[j];
-    const uint32_t nc = pt.ncols, src0 = pt.src[0], src1 = pt.src[1], src2 = pt.src[2];
+    const uint32_t nc = a.pat[j].ncols, src0 = a.pat[j].src[0], src1 = a.pat[j].src[1],
+                   src2 = a.pat[j].src[2];
     uint32_t *o0 = out.col[j * 3], *o1 = out.col[j * 3 + 1], *o2 = out.col[j * 3 + 2];
     uint32_t mn0 = ~0u, mn1 = ~0u, mn2 = ~0u, mx0 = 0, mx1 = 0, mx2 = 0;
-#pragma unroll 4
-    for (int w = 0; w < kScanWordsPerWarp; w++) {
-      const uint32_t m = __shfl_sync(0xffffffffu, mine, w);
-      if (m == 0) continue;  // warp-uniform
-      if ((m >> lane) & 1u) {
-        const uint64_t i = base + (uint64_t)w * 32;
-        const uint64_t pos = cur + __popc(m & lt);
-        const uint32_t v0 = src0 == 0 ? __ldcs(S + i) : (src0 == 1 ? __ldcs(P + i) : __ldcs(O + i));
-        st_cs_u32(o0 + pos, v0);
-        mn0 = min(mn0, v0);
-        mx0 = max(mx0, v0);
-        if (nc > 1) {
-          const uint32_t v1 = src1 == 0 ? __ldcs(S + i) : (src1 == 1 ? __ldcs(P + i) : __ldcs(O + i));
-          st_cs_u32(o1 + pos, v1);
-          mn1 = min(mn1, v1);
-          mx1 = max(mx1, v1);
+#pragma unroll 1
+    for (int w0 = 0; w0 < kScanWordsPerWarp; w0 += 8) {
+      uint32_t mw[8], v0[8], v1[8], v2[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        mw[u] = __shfl_sync(0xffffffffu, mine, w0 + u);
+        const bool hit = (mw[u] >> lane) & 1u;
+        const uint64_t i = base + (uint64_t)(w0 + u) * 32;
+        v0[u] = hit ? pick(S, P, O, src0, i) : 0u;
+        v1[u] = (hit && nc > 1) ? pick(S, P, O, src1, i) : 0u;
+        v2[u] = (hit && nc > 2) ? pick(S, P, O, src2, i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        if ((mw[u] >> lane) & 1u) {
+          const uint64_t pos = cur + __popc(mw[u] & lt);
+          st_cs_u32(o0 + pos, v0[u]);
+          mn0 = min(mn0, v0[u]);
+          mx0 = max(mx0, v0[u]);
+          if (nc > 1) {
+            st_cs_u32(o1 + pos, v1[u]);
+            mn1 = min(mn1, v1[u]);
+            mx1 = max(mx1, v1[u]);
+          }
           if (nc > 2) {
-            const uint32_t v2 = src2 == 0 ? __ldcs(S + i) : (src2 == 1 ? __ldcs(P + i) : __ldcs(O + i));
-            st_cs_u32(o2 + pos, v2);
-            mn2 = min(mn2, v2);
-            mx2 = max(mx2, v2);
+            st_cs_u32(o2 + pos, v2[u]);
+            mn2 = min(mn2, v2[u]);
+            mx2 = max(mx2, v2[u]);
           }
         }
+        cur += __popc(mw[u]);
       }
-      cur += __popc(m);
     }
     mn0 = __reduce_min_sync(0xffffffffu, mn0);
     mx0 = __reduce_max_sync(0xffffffffu, mx0);
