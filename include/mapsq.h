@@ -94,10 +94,15 @@ typedef struct mapsq_ctx mapsq_ctx;
 /* Host-side join spec.  Derived from the two schemas and column bounds:
  *   shared = vars(tp1) ∩ vars(tp2) ascending by id ("the key of them is their shared
  *   variable"; generalised to >= 1 shared variables, reading R5);
- *   key' = concatenation of (value - lo) of each shared column, first shared variable most
- *   significant, each in key_bits[c] = bits(hi - lo) bits; kb = sum of key_bits;
- *   ib = bits(n1 + n2 - 1) index bits; path P64 when kb + ib <= 64 (one packed word
- *   key' << ib | rowid per row, rowid >= n1 meaning RIGHT), else KV (u64 key' + u32 rowid). */
+ *   key' = concatenation of (value - lo) of each PACKED shared column, first one most
+ *   significant, each in key_bits[c] = bits(hi - lo) bits; kb = sum over packed columns;
+ *   ib = bits(n1 + n2 - 1) index bits.
+ *   path P64 when every shared column fits (kb + ib <= 64): one word key' << ib | rowid per row,
+ *   rowid >= n1 meaning RIGHT.  When the full key does not fit, path RESIDUAL packs the
+ *   widest shared columns that fit (packed_mask bit c set for shared[c]) and the remaining
+ *   "residual" shared columns are compared exactly inside each packed-key group during
+ *   ReduceDuplicate; path KV (u64 key' + u32 rowid pairs, every shared column packed) is the
+ *   alternative selected with MAPSQ_OPT_WIDE_KEY = MAPSQ_WIDE_KEY_KV. */
 typedef struct {
   uint64_t n1, n2;
   uint32_t nshared;
@@ -113,9 +118,11 @@ typedef struct {
   uint32_t path;    /* MAPSQ_PATH_* */
   uint32_t passes;  /* radix digit passes over the kb key bits */
   uint32_t disjoint;/* 1 when the key bounds do not overlap: the join is empty */
+  uint32_t packed_mask; /* bit c: shared[c] is packed into key' (all bits set unless RESIDUAL) */
 } mapsq_join_plan;
 #define MAPSQ_PATH_P64 0u
 #define MAPSQ_PATH_KV 1u
+#define MAPSQ_PATH_RESIDUAL 2u
 #define MAPSQ_RADIX_BITS 8u
 
 /* Per-kernel timing (recorded with CUDA events on the launching stream while profiling is on)
@@ -227,6 +234,12 @@ mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in, const int32_
 /* Compute exact inclusive bounds lo[]/hi[] of every column of a (caller-built) table and set
  * MAPSQ_TABLE_BOUNDS (one min/max pass, blocking).  An empty table gets lo = hi = 0. */
 mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
+
+/* ---- options ---- */
+#define MAPSQ_OPT_WIDE_KEY 1      /* how a join whose full key does not fit 64 - ib bits runs: */
+#define MAPSQ_WIDE_KEY_RESIDUAL 0 /*   packed widest columns + residual check (default) */
+#define MAPSQ_WIDE_KEY_KV 1       /*   (u64 key, u32 rowid) pair sort over every key bit */
+mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value);
 
 /* ---- statistics ---- */
 mapsq_status mapsq_set_profiling(mapsq_ctx *ctx, int on);

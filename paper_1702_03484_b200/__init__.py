@@ -20,7 +20,8 @@ _LIB_PATH = os.path.join(_HERE, "libmapsq.so")
 MAX_COLS = 16
 MAX_PATTERNS = 16
 TABLE_BOUNDS = 1
-PATH_P64, PATH_KV = 0, 1
+PATH_P64, PATH_KV, PATH_RESIDUAL = 0, 1, 2
+OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV = 1, 0, 1
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_UNSUPPORTED"}
 
@@ -58,7 +59,7 @@ class JoinPlan(ctypes.Structure):
                 ("rest_col2", ctypes.c_int32 * MAX_COLS), ("out_ncols", ctypes.c_uint32),
                 ("out_var", ctypes.c_int32 * MAX_COLS), ("kb", ctypes.c_uint32),
                 ("ib", ctypes.c_uint32), ("path", ctypes.c_uint32), ("passes", ctypes.c_uint32),
-                ("disjoint", ctypes.c_uint32)]
+                ("disjoint", ctypes.c_uint32), ("packed_mask", ctypes.c_uint32)]
 
 
 class _KStat(ctypes.Structure):
@@ -113,6 +114,7 @@ def lib():
                                      ctypes.POINTER(u64), vp]),
             "mapsq_table_bounds": (st, [vp, PT, vp]),
             "mapsq_set_profiling": (st, [vp, ctypes.c_int]),
+            "mapsq_set_option": (st, [vp, ctypes.c_int, ctypes.c_int64]),
             "mapsq_stats_reset": (st, [vp]),
             "mapsq_get_stats": (st, [vp, ctypes.POINTER(_Stats)]),
         }
@@ -392,6 +394,9 @@ class Context:
     def table_bounds(self, table: DeviceTable, stream=None):
         self._check(lib().mapsq_table_bounds(self.handle, ctypes.byref(table._c), _stream(stream)))
         return table.bounds
+
+    def set_option(self, option: int, value: int):
+        self._check(lib().mapsq_set_option(self.handle, option, value))
 
     # ---- statistics
     def set_profiling(self, on: bool):

@@ -199,7 +199,7 @@ mapsq_status alloc_table(mapsq_ctx *ctx, mapsq_table *t, uint64_t rows, uint32_t
 
 // ------------------------------------------------------------------------------ join plan
 mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
-                       mapsq_join_plan *pl) {
+                       mapsq_join_plan *pl, int wide_mode = MAPSQ_WIDE_KEY_RESIDUAL) {
   std::memset(pl, 0, sizeof *pl);
   TRY(check_table(ctx, a, "tp1"));
   TRY(check_table(ctx, b, "tp2"));
@@ -237,7 +237,7 @@ mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *
   for (uint32_t c = 0; c < pl->nrest2; c++) pl->out_var[k++] = b->var[pl->rest_col2[c]];
   // key packing over the UNION of both sides' bounds (every row stays representable); the
   // output's key bounds are the intersection
-  uint32_t kb = 0;
+  uint32_t kb_all = 0;
   for (uint32_t c = 0; c < ns; c++) {
     pl->shared[c] = sh[c];
     const int32_t ca = colof(a, sh[c]), cb = colof(b, sh[c]);
@@ -247,19 +247,47 @@ mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *
     pl->key_lo[c] = ulo;
     pl->key_hi[c] = uhi;
     pl->key_bits[c] = bits_for((uint64_t)uhi - ulo);
-    kb += pl->key_bits[c];
+    kb_all += pl->key_bits[c];
     if (std::max(a->lo[ca], b->lo[cb]) > std::min(a->hi[ca], b->hi[cb])) pl->disjoint = 1;
   }
-  uint32_t sft = 0;
-  for (int c = (int)ns - 1; c >= 0; c--) {  // first shared variable most significant
-    pl->key_shift[c] = sft;
-    sft += pl->key_bits[c];
-  }
-  pl->kb = kb;
   const uint64_t n = a->nrows + b->nrows;
   pl->ib = n > 1 ? bits_for(n - 1) : 1;
-  if (kb > 64) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "packed join key wider than 64 bits");
-  pl->path = (kb + pl->ib <= 64) ? MAPSQ_PATH_P64 : MAPSQ_PATH_KV;
+  uint32_t packed = (ns >= 32) ? ~0u : ((1u << ns) - 1u);
+  if (kb_all + pl->ib <= 64) {
+    pl->path = MAPSQ_PATH_P64;
+  } else if (wide_mode == MAPSQ_WIDE_KEY_KV) {
+    if (kb_all > 64) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "packed join key wider than 64 bits");
+    pl->path = MAPSQ_PATH_KV;
+  } else {
+    // RESIDUAL: pack the widest shared columns that fit 64 - ib bits (ties: lower var id first);
+    // the rest are compared exactly inside each packed-key group
+    uint32_t order[MAPSQ_MAX_COLS];
+    for (uint32_t c = 0; c < ns; c++) order[c] = c;
+    std::stable_sort(order, order + ns,
+                     [&](uint32_t x, uint32_t y) { return pl->key_bits[x] > pl->key_bits[y]; });
+    packed = 0;
+    uint32_t used = 0;
+    for (uint32_t q = 0; q < ns; q++) {
+      const uint32_t c = order[q];
+      if (used + pl->key_bits[c] + pl->ib <= 64) {
+        packed |= 1u << c;
+        used += pl->key_bits[c];
+      }
+    }
+    pl->path = MAPSQ_PATH_RESIDUAL;
+  }
+  pl->packed_mask = packed;
+  uint32_t kb = 0, sft = 0;
+  for (int c = (int)ns - 1; c >= 0; c--) {  // first packed shared variable most significant
+    if (!(packed >> c & 1u)) {
+      pl->key_shift[c] = 0;
+      continue;
+    }
+    pl->key_shift[c] = sft;
+    sft += pl->key_bits[c];
+    kb += pl->key_bits[c];
+  }
+  pl->kb = kb;
   pl->passes = (kb + MAPSQ_RADIX_BITS - 1) / MAPSQ_RADIX_BITS;
   return MAPSQ_OK;
 }
@@ -364,12 +392,13 @@ void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const maps
 PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b) {
   PackArgs pa;
   std::memset(&pa, 0, sizeof pa);
-  pa.nkey = pl.nshared;
   for (uint32_t c = 0; c < pl.nshared; c++) {
-    pa.key1[c] = a->col[pl.key_col1[c]];
-    pa.key2[c] = b->col[pl.key_col2[c]];
-    pa.lo[c] = pl.key_lo[c];
-    pa.shift[c] = pl.key_shift[c];
+    if (!(pl.packed_mask >> c & 1u)) continue;
+    pa.key1[pa.nkey] = a->col[pl.key_col1[c]];
+    pa.key2[pa.nkey] = b->col[pl.key_col2[c]];
+    pa.lo[pa.nkey] = pl.key_lo[c];
+    pa.shift[pa.nkey] = pl.key_shift[c];
+    pa.nkey++;
   }
   pa.n1 = pl.n1;
   pa.n2 = pl.n2;
@@ -392,7 +421,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   TRY(bounds_of(ctx, &a, s));
   TRY(bounds_of(ctx, &b, s));
   mapsq_join_plan pl;
-  TRY(plan_join(ctx, &a, &b, &pl));
+  TRY(plan_join(ctx, &a, &b, &pl, ctx->wide_key_mode));
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
   ctx->counters.joins++;
   ctx->counters.join_in_rows += n;
@@ -454,6 +483,27 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
                        gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
     CKL("find_groups");
   }
+  const bool residual = pl.path == MAPSQ_PATH_RESIDUAL;
+  ResidualArgs ra;
+  std::memset(&ra, 0, sizeof ra);
+  if (residual) {
+    ra.words = words;
+    ra.n1 = n1;
+    ra.ib = pl.ib;
+    ra.gstart = gs;
+    ra.gsplit = gp;
+    ra.gend = ge;
+    ra.ngroups_dev = scal;
+    for (uint32_t c = 0; c < pl.nshared; c++)
+      if (!(pl.packed_mask >> c & 1u)) {
+        ra.res1[ra.nres] = a.col[pl.key_col1[c]];
+        ra.res2[ra.nres] = b.col[pl.key_col2[c]];
+        ra.nres++;
+      }
+    KTimer kt(ctx, s, "residual_count", 8ull * n);
+    launch_residual_count(ra, cap, gc, s);  // exact pair counts replace nL * nR
+    CKL("residual_count");
+  }
   {
     KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
     launch_exclusive_scan_u64_dev(gc, go, scal, cap, tmp, scal + 1, s);
@@ -463,6 +513,38 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   CK(cudaMemcpyAsync(ctx->pinned, scal, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));  // the one blocking read: |RS| sizes the output
   const uint64_t ngroups = ctx->pinned[0], m = ctx->pinned[1];
+  if (residual) {
+    fill_empty_join(pl, &a, &b, rs);
+    TRY(alloc_table(ctx, rs, m, pl.out_ncols, s));
+    if (m) {
+      uint32_t k = 0;
+      for (uint32_t c = 0; c < pl.nshared; c++, k++) {
+        ra.src_side[k] = 0;
+        ra.src[k] = a.col[pl.key_col1[c]];
+      }
+      for (uint32_t c = 0; c < pl.nrest1; c++, k++) {
+        ra.src_side[k] = 0;
+        ra.src[k] = a.col[pl.rest_col1[c]];
+      }
+      for (uint32_t c = 0; c < pl.nrest2; c++, k++) {
+        ra.src_side[k] = 1;
+        ra.src[k] = b.col[pl.rest_col2[c]];
+      }
+      ra.nout = k;
+      for (uint32_t c = 0; c < k; c++) ra.out[c] = rs->col[c];
+      ra.goff = go;
+      KTimer kt(ctx, s, "residual_expand", 4ull * m * pl.out_ncols);
+      launch_residual_expand(ra, ngroups, s);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        dfree(ctx, rs->owner, s);
+        clear_table(rs);
+        return cuda_check(ctx, e, "residual_expand");
+      }
+    }
+    ctx->counters.join_out_rows += m;
+    return MAPSQ_OK;
+  }
   // ---- ReduceDuplicate 2 (row a6): expand into RS
   fill_empty_join(pl, &a, &b, rs);
   TRY(alloc_table(ctx, rs, m, pl.out_ncols, s));
@@ -1042,6 +1124,15 @@ MAPSQ_API mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in,
   CK(cudaStreamSynchronize(s));
   for (int d = 0; d < nparts; d++) counts_host[d] = ctx->pinned[d + 1] - ctx->pinned[d];
   return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value) {
+  if (!ctx) return MAPSQ_E_INVALID;
+  if (option == MAPSQ_OPT_WIDE_KEY && (value == MAPSQ_WIDE_KEY_RESIDUAL || value == MAPSQ_WIDE_KEY_KV)) {
+    ctx->wide_key_mode = (int)value;
+    return MAPSQ_OK;
+  }
+  return set_error(ctx, MAPSQ_E_INVALID, "unknown option or value");
 }
 
 MAPSQ_API mapsq_status mapsq_set_profiling(mapsq_ctx *ctx, int on) {

@@ -48,6 +48,7 @@ struct mapsq_ctx {
   std::string err;
   bool cuda_broken = false;
   bool profiling = false;
+  int wide_key_mode = MAPSQ_WIDE_KEY_RESIDUAL;
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
   std::map<std::string, mapsq::KAgg> kagg;
@@ -301,6 +302,27 @@ struct ExpandArgs {
   uint32_t *out[MAPSQ_MAX_COLS];  // nkey + nrest1 + nrest2 columns
 };
 void launch_expand(const ExpandArgs &a, cudaStream_t s);
+
+// RESIDUAL path (wide keys): groups are equal on the packed key; the residual shared columns are
+// compared exactly, pair by pair, inside each group.
+struct ResidualArgs {
+  const uint64_t *words;  // sorted P64 words over the packed columns
+  uint64_t n1;
+  uint32_t ib;
+  const uint32_t *gstart, *gsplit, *gend;
+  const uint64_t *ngroups_dev;  // group count (device)
+  uint32_t nres;
+  const uint32_t *res1[MAPSQ_MAX_COLS];  // residual columns of tp1 / tp2, same variable order
+  const uint32_t *res2[MAPSQ_MAX_COLS];
+  // expand: output column c comes from side src_side[c] (0 = tp1, 1 = tp2), column src[c]
+  uint32_t nout;
+  uint32_t src_side[MAPSQ_MAX_COLS];
+  const uint32_t *src[MAPSQ_MAX_COLS];
+  uint32_t *out[MAPSQ_MAX_COLS];
+  const uint64_t *goff;  // exclusive offsets of the exact pair counts
+};
+void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, cudaStream_t s);
+void launch_residual_expand(const ResidualArgs &a, uint64_t cap, cudaStream_t s);
 uint64_t find_groups_tiles(uint64_t n);
 
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,

@@ -258,6 +258,56 @@ expand_kernel(const ExpandArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ RESIDUAL path (wide keys)
+// One thread per packed-key group: the exact pair count of the group is the number of
+// (LEFT, RIGHT) row pairs that also agree on every residual shared column.  Groups of wide-key
+// joins (e.g. C5's (?x, ?z) with ?x packed) are a handful of rows, so the pair loop is short.
+__device__ __forceinline__ bool residual_equal(const ResidualArgs &a, uint32_t li, uint32_t ri) {
+  for (uint32_t c = 0; c < a.nres; c++)
+    if (__ldg(a.res1[c] + li) != __ldg(a.res2[c] + ri)) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(256)
+residual_count_kernel(const ResidualArgs a, uint64_t *__restrict__ cnt) {
+  const uint64_t ng = *a.ngroups_dev;
+  const uint64_t mask = (1ull << a.ib) - 1;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
+    uint64_t c = 0;
+    for (uint32_t l = st; l < sp; l++) {
+      const uint32_t li = (uint32_t)(a.words[l] & mask);
+      for (uint32_t r = sp; r < en; r++) {
+        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
+        c += residual_equal(a, li, ri);
+      }
+    }
+    cnt[g] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+residual_expand_kernel(const ResidualArgs a) {
+  const uint64_t ng = *a.ngroups_dev;
+  const uint64_t mask = (1ull << a.ib) - 1;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
+    uint64_t pos = a.goff[g];
+    for (uint32_t l = st; l < sp; l++) {
+      const uint32_t li = (uint32_t)(a.words[l] & mask);
+      for (uint32_t r = sp; r < en; r++) {
+        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
+        if (!residual_equal(a, li, ri)) continue;
+        for (uint32_t c = 0; c < a.nout; c++)
+          a.out[c][pos] = __ldg(a.src[c] + (a.src_side[c] ? ri : li));
+        pos++;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint32_t *vals,
@@ -276,6 +326,18 @@ void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint3
 }
 
 uint64_t find_groups_tiles(uint64_t n) { return ceil_div(n, kGTile); }
+
+static unsigned residual_grid(uint64_t cap) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(cap, 256), 148 * 16));
+}
+
+void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, cudaStream_t s) {
+  residual_count_kernel<<<residual_grid(cap), 256, 0, s>>>(a, cnt);
+}
+
+void launch_residual_expand(const ResidualArgs &a, uint64_t cap, cudaStream_t s) {
+  residual_expand_kernel<<<residual_grid(cap), 256, 0, s>>>(a);
+}
 
 void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   if (a.m == 0) return;

@@ -57,20 +57,27 @@ def test_plan_composite_key_order_and_shifts():
     assert pl.kb == 18 and pl.ib == 8 and pl.passes == 3
 
 
-def test_plan_kv_path_when_key_and_index_exceed_64_bits():
+def test_plan_residual_path_when_key_and_index_exceed_64_bits():
+    # two 32-bit key columns + 5 index bits do not fit one word: the wider/first column is
+    # packed, the other is checked exactly inside each packed-key group
     full = (0, 0xFFFFFFFF)
     pl = mq.plan_join([0, 1], [full, full], 10, [0, 1], [full, full], 10)
-    assert pl.kb == 64 and pl.path == mq.PATH_KV and pl.passes == 8
+    assert pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b01
+    assert pl.kb == 32 and pl.ib == 5 and pl.passes == 4
+    # the widest column is packed first, whatever its position
+    pl = mq.plan_join([0, 1], [(0, 255), full], 1 << 26, [0, 1], [(0, 255), full], 1 << 26)
+    assert pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b10 and pl.kb == 32
+    # 3 columns: the two widest that fit 64 - ib are packed
+    pl = mq.plan_join([0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000,
+                      [0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000)
+    assert pl.ib == 11 and pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b101
+    assert pl.kb == 21 + 25
 
 
 def test_plan_errors():
     with pytest.raises(mq.MapsqError) as e:
         mq.plan_join([0], [(0, 1)], 1, [1], [(0, 1)], 1)
     assert e.value.status == "E_NO_SHARED"
-    full = (0, 0xFFFFFFFF)
-    with pytest.raises(mq.MapsqError) as e:
-        mq.plan_join([0, 1, 2], [full] * 3, 1, [0, 1, 2], [full] * 3, 1)
-    assert e.value.status == "E_UNSUPPORTED"
     with pytest.raises(mq.MapsqError) as e:
         mq.plan_join([0], [(0, 1)], 2 ** 31, [0], [(0, 1)], 2 ** 31)
     assert e.value.status == "E_INVALID"

@@ -117,15 +117,41 @@ def test_join_composite_keys_and_kv_path(ctx):
     B = np.concatenate([base[rng.integers(0, 500, 3000)][:, ::-1], rng.integers(0, 9, (3000, 1)).astype(np.uint32)], 1)
     B[:2, :2] = [[0, 0], [0xFFFFFFFF, 0xFFFFFFFF]]
     ta, tb = oracle.Table([4, 5, 6], A), oracle.Table([5, 4, 7], np.ascontiguousarray(B))
+    ref = oracle.join(ta, tb)
+    # default: RESIDUAL path (x packed, z verified per group); rows ordered by (x', l, r)
     got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
-    st = ctx.stats()
-    assert st["last_path"] == mq.PATH_KV
-    assert_same(got, oracle.join(ta, tb))
+    assert ctx.stats()["last_path"] == mq.PATH_RESIDUAL
+    assert_same(got, ref, ordered=False)
+    # forced KV path: (u64 key', u32 rowid) pairs over all 64 key bits, lexicographic order
+    ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_KV)
+    try:
+        got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
+        assert ctx.stats()["last_path"] == mq.PATH_KV
+        assert_same(got, ref)
+    finally:
+        ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_RESIDUAL)
     # three shared variables
     A = rng.integers(0, 3, (2000, 4)).astype(np.uint32)
     B = rng.integers(0, 3, (1500, 3)).astype(np.uint32)
     ref = oracle.join(oracle.Table([0, 1, 2, 9], A), oracle.Table([2, 1, 0], B))
     assert_same(ctx.join(dtable([0, 1, 2, 9], A), dtable([2, 1, 0], B)), ref)
+
+
+def test_join_residual_path_collisions_and_skew(ctx):
+    # packed column x with few values and a residual column z: many packed-key groups mix
+    # several z values, so the per-group exact residual check decides every pair
+    rng = np.random.default_rng(13)
+    for n1, n2, dx, dz in [(3000, 2000, 50, 7), (500, 40000, 3, 1 << 32), (20000, 20000, 5000, 3)]:
+        x1 = rng.integers(0, dx, n1); z1 = rng.integers(0, dz, n1, dtype=np.uint64)
+        x2 = rng.integers(0, dx, n2); z2 = rng.integers(0, dz, n2, dtype=np.uint64)
+        # force both key columns to span 32 bits so the plan cannot pack both
+        x1[0] = 0xFFFFFFFF; z1[0] = 0xFFFFFFFF; x2[0] = 0; z2[0] = 0
+        A = np.stack([x1, z1, rng.integers(0, 100, n1)], 1).astype(np.uint32)
+        B = np.stack([z2, rng.integers(0, 100, n2), x2], 1).astype(np.uint32)
+        ref = oracle.join(oracle.Table([0, 1, 2], A), oracle.Table([1, 3, 0], B))
+        got = ctx.join(dtable([0, 1, 2], A), dtable([1, 3, 0], B))
+        assert ctx.stats()["last_path"] == mq.PATH_RESIDUAL
+        assert_same(got, ref, ordered=False)
 
 
 def test_join_skewed_hot_key_large_groups(ctx):
@@ -244,7 +270,8 @@ def test_query_configs_small_scale(ctx, cfg):
     ref = oracle.query(s, p, o, pats)
     got = ctx.query(trip, pats)
     assert got.nrows == config_expected_counts(cfg, st)[-1]
-    assert_same(got, ref)
+    # wide-key joins (RESIDUAL path) emit (packed key, l, r) order: compare canonically there
+    assert_same(got, ref, ordered=ctx.stats()["last_path"] != mq.PATH_RESIDUAL)
     # chained joins one by one agree with the generator's bookkeeping
     tabs = ctx.scan_patterns(trip, pats)
     acc = tabs[0]
