@@ -60,25 +60,36 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   __shared__ uint32_t s_ball[kGItems][kGWarps];
   // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane.  Each
   // element is loaded once; its predecessor comes from the neighbouring lane (lane 0 loads it).
+  // Loads are issued kGBatch items at a time so their latencies overlap.
+  constexpr int kGBatch = 8;
+#pragma unroll 1
+  for (int it0 = 0; it0 < kGItems; it0 += kGBatch) {
+    uint64_t kk[kGBatch], kp[kGBatch];
+    bool rr[kGBatch], rp[kGBatch];
 #pragma unroll
-  for (int it = 0; it < kGItems; it++) {
-    const uint64_t i = base + (uint64_t)it * kGThreads + tid;
-    uint64_t k = ~0ull;
-    bool r = false;
-    if (i < n) W.load(i, &k, &r);
-    uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1);
-    bool rp = __shfl_up_sync(0xffffffffu, r, 1);
-    if (lane == 0) {
-      kp = ~0ull;
-      rp = true;
-      if (i > 0 && i < n) W.load(i - 1, &kp, &rp);
+    for (int u = 0; u < kGBatch; u++) {
+      const uint64_t i = base + (uint64_t)(it0 + u) * kGThreads + tid;
+      kk[u] = ~0ull;
+      rr[u] = false;
+      kp[u] = ~0ull;
+      rp[u] = true;
+      if (i < n) W.load(i, &kk[u], &rr[u]);
+      if (lane == 0 && i > 0 && i < n) W.load(i - 1, &kp[u], &rp[u]);
     }
-    // split: word i is RIGHT, word i-1 is LEFT, same key
-    const bool split = i > 0 && i < n && r && !rp && k == kp;
-    const uint32_t bl = __ballot_sync(0xffffffffu, split);
-    if (lane == 0) {
-      s_ball[it][warp] = bl;
-      s_cnt[it][warp] = __popc(bl);
+#pragma unroll
+    for (int u = 0; u < kGBatch; u++) {
+      const uint64_t i = base + (uint64_t)(it0 + u) * kGThreads + tid;
+      const uint64_t kup = __shfl_up_sync(0xffffffffu, kk[u], 1);
+      const bool rup = __shfl_up_sync(0xffffffffu, rr[u], 1);
+      const uint64_t kprev = lane == 0 ? kp[u] : kup;
+      const bool rprev = lane == 0 ? rp[u] : rup;
+      // split: word i is RIGHT, word i-1 is LEFT, same key
+      const bool split = i > 0 && i < n && rr[u] && !rprev && kk[u] == kprev;
+      const uint32_t bl = __ballot_sync(0xffffffffu, split);
+      if (lane == 0) {
+        s_ball[it0 + u][warp] = bl;
+        s_cnt[it0 + u][warp] = __popc(bl);
+      }
     }
   }
   __syncthreads();
