@@ -130,6 +130,9 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+__device__ __forceinline__ uint32_t lt_or_eq_mask(uint32_t lane) {  // lanes 0..lane
+  return lane >= 31 ? 0xffffffffu : ((2u << lane) - 1u);
+}
 __device__ __forceinline__ void st_cs_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -18,9 +18,11 @@ namespace mapsq {
 namespace {
 
 constexpr int kGThreads = 256;
-constexpr int kGItems = 64;
+constexpr int kGItems = 16;
 constexpr uint64_t kGTile = kGThreads * kGItems;
 constexpr int kGWarps = kGThreads / 32;
+constexpr int kGSlice = 32 * kGItems;       // elements per warp slice
+constexpr int kGMaxRec = kGSlice / 2;       // at most one split per two elements
 
 struct WordView {
   const uint64_t *words, *keys;
@@ -30,9 +32,6 @@ struct WordView {
   uint64_t idx_mask;
   __device__ __forceinline__ uint64_t key(uint64_t i) const {
     return words ? (words[i] >> ib) : keys[i];
-  }
-  __device__ __forceinline__ bool right(uint64_t i) const {
-    return (words ? (words[i] & idx_mask) : (uint64_t)vals[i]) >= n1;
   }
   __device__ __forceinline__ void load(uint64_t i, uint64_t *k, bool *r) const {
     if (words) {
@@ -46,125 +45,164 @@ struct WordView {
   }
 };
 
+// first index of the run of key k that contains position `from` (key(from) == k), by galloping
+__device__ uint64_t run_start(const WordView &W, uint64_t from, uint64_t k) {
+  int64_t lo = (int64_t)from, step = 1;
+  while (true) {
+    const int64_t c = lo - step;
+    if (c < 0 || W.key((uint64_t)c) != k) break;
+    lo = c;
+    step <<= 1;
+  }
+  int64_t L = (lo - step > -1) ? lo - step : -1, R = lo;  // key(L) != k (or -1), key(R) == k
+  while (R - L > 1) {
+    const int64_t m = (L + R) >> 1;
+    if (W.key((uint64_t)m) == k) R = m; else L = m;
+  }
+  return (uint64_t)R;
+}
+// one past the last index of the run of key k that contains position `from`
+__device__ uint64_t run_end(const WordView &W, uint64_t from, uint64_t k, uint64_t n) {
+  int64_t hi = (int64_t)from, step = 1;
+  while (true) {
+    const int64_t c = hi + step;
+    if (c >= (int64_t)n || W.key((uint64_t)c) != k) break;
+    hi = c;
+    step <<= 1;
+  }
+  int64_t L = hi, R = (hi + step < (int64_t)n) ? hi + step : (int64_t)n;
+  while (R - L > 1) {
+    const int64_t m = (L + R) >> 1;
+    if (W.key((uint64_t)m) == k) L = m; else R = m;
+  }
+  return (uint64_t)R;
+}
+
+// K4.  Warp w sweeps its contiguous slice of the tile item by item (32 consecutive words per
+// item).  Ballots give the run heads (key differs from the previous word) and the splits
+// (LEFT word followed by a RIGHT word of the same key); a split's run starts at the last head
+// at or before it and ends at the next head after it, both tracked across items in registers
+// ("pending" end).  Only a run crossing the slice boundary needs a gallop (at most one start and
+// one end per slice).  Records go to shared memory, the tile's split count is resolved with a
+// warp-parallel decoupled look-back, and records are stored in key order.
 __global__ void __launch_bounds__(kGThreads)
 find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restrict__ status,
                    uint32_t *__restrict__ tile_counter, uint64_t *__restrict__ ngroups_dev) {
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_cnt[kGItems][kGWarps];
+  __shared__ uint32_t s_nrec[kGWarps];
   __shared__ uint64_t s_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ uint32_t s_start[kGWarps][kGMaxRec], s_split[kGWarps][kGMaxRec], s_end[kGWarps][kGMaxRec];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
-  const uint64_t base = tile * kGTile;
-  __shared__ uint32_t s_ball[kGItems][kGWarps];
-  // element order inside the tile: (it, warp, lane) -> base + it*256 + warp*32 + lane.  Each
-  // element is loaded once; its predecessor comes from the neighbouring lane (lane 0 loads it).
-  // Loads are issued kGBatch items at a time so their latencies overlap.
-  constexpr int kGBatch = 8;
+  const uint64_t sbeg = tile * kGTile + (uint64_t)warp * kGSlice;  // slice [sbeg, send)
+  const uint64_t send = sbeg + kGSlice < n ? sbeg + kGSlice : n;
+  const uint32_t le = lt_or_eq_mask(lane), lt = lanemask_lt();
+  uint32_t nrec = 0;
+  int32_t pending = -1;             // record whose run has not ended yet
+  uint64_t last_head = ~0ull;       // last head seen in this slice (~0: none yet)
+  int32_t first_unknown = -1;       // first record whose run started before the slice
+  uint64_t carry_k = ~0ull;
+  bool carry_r = true;
+  if (sbeg < n && sbeg > 0) {
+    uint64_t k;
+    bool r;
+    W.load(sbeg - 1, &k, &r);
+    carry_k = k;
+    carry_r = r;
+  }
+  constexpr int kB = 8;
 #pragma unroll 1
-  for (int it0 = 0; it0 < kGItems; it0 += kGBatch) {
-    uint64_t kk[kGBatch], kp[kGBatch];
-    bool rr[kGBatch], rp[kGBatch];
+  for (int it0 = 0; it0 < kGItems; it0 += kB) {
+    uint64_t kk[kB];
+    bool rr[kB];
 #pragma unroll
-    for (int u = 0; u < kGBatch; u++) {
-      const uint64_t i = base + (uint64_t)(it0 + u) * kGThreads + tid;
+    for (int u = 0; u < kB; u++) {
+      const uint64_t i = sbeg + (uint64_t)(it0 + u) * 32 + lane;
       kk[u] = ~0ull;
       rr[u] = false;
-      kp[u] = ~0ull;
-      rp[u] = true;
-      if (i < n) W.load(i, &kk[u], &rr[u]);
-      if (lane == 0 && i > 0 && i < n) W.load(i - 1, &kp[u], &rp[u]);
+      if (i < send) W.load(i, &kk[u], &rr[u]);
     }
 #pragma unroll
-    for (int u = 0; u < kGBatch; u++) {
-      const uint64_t i = base + (uint64_t)(it0 + u) * kGThreads + tid;
+    for (int u = 0; u < kB; u++) {
+      const uint64_t ibase = sbeg + (uint64_t)(it0 + u) * 32;
+      if (ibase >= send) break;  // warp-uniform
+      const uint64_t i = ibase + lane;
+      const bool in = i < send;
       const uint64_t kup = __shfl_up_sync(0xffffffffu, kk[u], 1);
       const bool rup = __shfl_up_sync(0xffffffffu, rr[u], 1);
-      const uint64_t kprev = lane == 0 ? kp[u] : kup;
-      const bool rprev = lane == 0 ? rp[u] : rup;
-      // split: word i is RIGHT, word i-1 is LEFT, same key
-      const bool split = i > 0 && i < n && rr[u] && !rprev && kk[u] == kprev;
-      const uint32_t bl = __ballot_sync(0xffffffffu, split);
-      if (lane == 0) {
-        s_ball[it0 + u][warp] = bl;
-        s_cnt[it0 + u][warp] = __popc(bl);
+      const uint64_t kprev = lane == 0 ? carry_k : kup;
+      const bool rprev = lane == 0 ? carry_r : rup;
+      const bool head = in && (i == 0 || kk[u] != kprev);
+      const bool split = in && i > 0 && rr[u] && !rprev && kk[u] == kprev;
+      const uint32_t hm = __ballot_sync(0xffffffffu, head);
+      const uint32_t sm = __ballot_sync(0xffffffffu, split);
+      if (pending >= 0 && hm) {  // the pending run ends at this item's first head
+        if (lane == 0) s_end[warp][pending] = (uint32_t)(ibase + __ffs(hm) - 1);
+        pending = -1;
       }
+      if (split) {
+        const uint32_t idx = nrec + __popc(sm & lt);
+        const uint32_t hb = hm & le;  // heads at or before this lane
+        uint64_t st;
+        if (hb) st = ibase + 31 - __clz(hb);
+        else st = last_head;      // ~0 when the run began before the slice
+        const uint32_t ha = hm & ~le;  // heads after this lane
+        s_start[warp][idx] = (uint32_t)st;
+        s_split[warp][idx] = (uint32_t)i;
+        if (ha) s_end[warp][idx] = (uint32_t)(ibase + __ffs(ha) - 1);  // else: pending
+      }
+      if (sm) {
+        const int hi_lane = 31 - __clz(sm);
+        const uint32_t ha = hm & ~lt_or_eq_mask(hi_lane);
+        if (!ha) pending = (int32_t)(nrec + __popc(sm) - 1);
+        if (first_unknown < 0 && last_head == ~0ull && !(hm & lt_or_eq_mask(__ffs(sm) - 1)))
+          first_unknown = (int32_t)nrec;
+      }
+      nrec += __popc(sm);
+      if (hm) last_head = ibase + 31 - __clz(hm);
+      carry_k = __shfl_sync(0xffffffffu, kk[u], 31);
+      carry_r = __shfl_sync(0xffffffffu, rr[u], 31);
     }
   }
-  __syncthreads();
-  // exclusive scan of the (it, warp) counts in element order; warp 0 also does the look-back
-  if (tid < 32) {
-    uint32_t v[kGItems * kGWarps / 32];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int q = 0; q < kGItems * kGWarps / 32; q++) {
-      v[q] = (&s_cnt[0][0])[tid * (kGItems * kGWarps / 32) + q];
-      sum += v[q];
+  __syncwarp();
+  // runs crossing the slice boundary: gallop (at most one start and one end per slice)
+  if (lane == 0) {
+    if (first_unknown >= 0) {
+      const uint32_t sp = s_split[warp][first_unknown];
+      s_start[warp][first_unknown] = (uint32_t)run_start(W, sp, W.key(sp));
     }
-    uint32_t x = sum;
+    if (pending >= 0) {
+      const uint32_t sp = s_split[warp][pending];
+      s_end[warp][pending] = (uint32_t)run_end(W, sp, W.key(sp), n);
+    }
+    s_nrec[warp] = nrec;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t c = lane < kGWarps ? s_nrec[lane] : 0u;
+    uint32_t x = c;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      if (lane >= (uint32_t)o) x += y;
     }
     const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
-    uint32_t run = x - sum;
-#pragma unroll
-    for (int q = 0; q < kGItems * kGWarps / 32; q++) {
-      (&s_cnt[0][0])[tid * (kGItems * kGWarps / 32) + q] = run;
-      run += v[q];
-    }
+    if (lane < kGWarps) s_nrec[lane] = x - c;  // exclusive prefix over warps
     const uint64_t excl = warp_lookback(status, tile, total);
-    if (tid == 0) {
+    if (lane == 0) {
       s_base = excl;
       if (tile == gridDim.x - 1) *ngroups_dev = excl + total;
     }
   }
   __syncthreads();
-  const uint64_t out_base = s_base;
-  const uint32_t lt = lanemask_lt();
-#pragma unroll 1
-  for (int it = 0; it < kGItems; it++) {
-    const uint32_t bl = s_ball[it][warp];
-    if (!((bl >> lane) & 1u)) continue;
-    const uint64_t i = base + (uint64_t)it * kGThreads + tid;
-    const uint64_t pos = out_base + s_cnt[it][warp] + __popc(bl & lt);
-    const uint64_t k = W.key(i);
-    // gallop back from i-1 to the first element of the key's run
-    int64_t lo = (int64_t)i - 1;  // key(lo) == k
-    int64_t step = 1;
-    while (true) {
-      const int64_t c = lo - step;
-      if (c < 0 || W.key((uint64_t)c) != k) break;
-      lo = c;
-      step <<= 1;
-    }
-    int64_t L = (lo - step > -1) ? lo - step : -1, R = lo;  // key(L) != k (or L = -1), key(R) == k
-    while (R - L > 1) {
-      const int64_t m = (L + R) >> 1;
-      if (W.key((uint64_t)m) == k) R = m; else L = m;
-    }
-    const uint64_t start = (uint64_t)R;
-    // gallop forward from i to one past the run's last element
-    int64_t hi = (int64_t)i;  // key(hi) == k
-    step = 1;
-    while (true) {
-      const int64_t c = hi + step;
-      if (c >= (int64_t)n || W.key((uint64_t)c) != k) break;
-      hi = c;
-      step <<= 1;
-    }
-    L = hi;
-    R = (hi + step < (int64_t)n) ? hi + step : (int64_t)n;  // key(L) == k, key(R) != k (or R = n)
-    while (R - L > 1) {
-      const int64_t m = (L + R) >> 1;
-      if (W.key((uint64_t)m) == k) L = m; else R = m;
-    }
-    const uint64_t end = (uint64_t)R;
-    g.start[pos] = (uint32_t)start;
-    g.split[pos] = (uint32_t)i;
-    g.end[pos] = (uint32_t)end;
-    g.cnt[pos] = (i - start) * (end - i);
+  const uint64_t out0 = s_base + s_nrec[warp];
+  for (uint32_t q = lane; q < nrec; q += 32) {
+    const uint64_t st = s_start[warp][q], sp = s_split[warp][q], en = s_end[warp][q];
+    g.start[out0 + q] = (uint32_t)st;
+    g.split[out0 + q] = (uint32_t)sp;
+    g.end[out0 + q] = (uint32_t)en;
+    g.cnt[out0 + q] = (sp - st) * (en - sp);
   }
 }
 
