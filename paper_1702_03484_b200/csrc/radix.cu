@@ -122,20 +122,21 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
   h[threadIdx.x] = pre + x - v;
 }
 
-// One stable digit pass.  Tile = kSortThreads x kSortItems keys; warp w owns the contiguous
+// One stable digit pass.  Tile = kSortThreads x ITEMS keys; warp w owns the contiguous
 // slice [w*32*ITEMS, (w+1)*32*ITEMS) of its tile and reads it item-major (item it, lane l ->
 // slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
 // full tiles skip every bounds check (the first version spent most of its issue slots on 64-bit
 // index arithmetic).
-template <bool KV>
-__global__ void __launch_bounds__(kSortThreads, 3)
+template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false>
+__global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
                   uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
                   uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
+  constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
-  uint32_t *s_vals = reinterpret_cast<uint32_t *>(smem_raw + kSortTile * sizeof(uint64_t));
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(smem_raw + TILE * sizeof(uint64_t));
   __shared__ uint32_t s_warp_hist[kWarps][kRadix];
   __shared__ uint32_t s_digit_start[kRadix];
   __shared__ uint64_t s_global_base[kRadix];
@@ -148,49 +149,59 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   for (int q = 0; q < kWarps; q++) s_warp_hist[q][tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
   const uint64_t tile = s_tile;
-  const uint64_t tile_base = tile * kSortTile;
+  const uint64_t tile_base = tile * TILE;
   const uint64_t rem = n - tile_base;
-  const uint32_t tile_n = rem < (uint64_t)kSortTile ? (uint32_t)rem : (uint32_t)kSortTile;
-  const uint32_t wslice = warp * 32 * kSortItems;
+  const uint32_t tile_n = rem < (uint64_t)TILE ? (uint32_t)rem : (uint32_t)TILE;
+  const uint32_t wslice = warp * 32 * ITEMS;
   const uint32_t dmask = (1u << bits) - 1u;
   const uint64_t *src = kin + tile_base + wslice + lane;
 
-  uint64_t k[kSortItems];
-  uint32_t v[KV ? kSortItems : 1];
-  uint32_t r[kSortItems];
-  uint32_t peers[kSortItems];
-  if (tile_n == (uint32_t)kSortTile) {
+  uint64_t k[ITEMS];
+  uint32_t v[KV ? ITEMS : 1];
+  uint32_t r[ITEMS];
+  const bool full = tile_n == (uint32_t)TILE;
+  if (full) {
 #pragma unroll
-    for (int it = 0; it < kSortItems; it++) k[it] = __ldcs(src + it * 32);
+    for (int it = 0; it < ITEMS; it++) k[it] = RELOAD ? __ldcg(src + it * 32) : __ldcs(src + it * 32);
     if (KV) {
 #pragma unroll
-      for (int it = 0; it < kSortItems; it++) v[KV ? it : 0] = __ldcs(vin + tile_base + wslice + lane + it * 32);
+      for (int it = 0; it < ITEMS; it++) v[KV ? it : 0] = __ldcs(vin + tile_base + wslice + lane + it * 32);
     }
-#pragma unroll
-    for (int it = 0; it < kSortItems; it++)
-      peers[it] = __match_any_sync(0xffffffffu, (uint32_t)(k[it] >> shift) & dmask);
   } else {
 #pragma unroll
-    for (int it = 0; it < kSortItems; it++) {
+    for (int it = 0; it < ITEMS; it++) {
       const bool in = wslice + it * 32 + lane < tile_n;
-      k[it] = in ? __ldcs(src + it * 32) : 0ull;
+      k[it] = in ? (RELOAD ? __ldcg(src + it * 32) : __ldcs(src + it * 32)) : 0ull;
       if (KV) v[KV ? it : 0] = in ? __ldcs(vin + tile_base + wslice + lane + it * 32) : 0u;
-      peers[it] = __match_any_sync(0xffffffffu, in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u);
     }
   }
-  // warp-level multisplit: one leader lane per digit group bumps the warp's counter
+  // warp-level multisplit in batches of kMB items: the batch's match-any operations are issued
+  // together (their latency overlaps), then one leader lane per digit group bumps the warp's
+  // counter; batching keeps only kMB match masks live.
+  constexpr int kMB = 8;
   const uint32_t lt = lanemask_lt();
 #pragma unroll
-  for (int it = 0; it < kSortItems; it++) {
-    const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
-    const uint32_t leader = 31 - __clz(peers[it]);
-    const bool in = wslice + it * 32 + lane < tile_n;
-    uint32_t base = 0;
-    if (in && lane == leader) {
-      base = s_warp_hist[warp][d];
-      s_warp_hist[warp][d] = base + __popc(peers[it]);
+  for (int b0 = 0; b0 < ITEMS; b0 += kMB) {
+    uint32_t peers[kMB];
+#pragma unroll
+    for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
+      const int it = b0 + u;
+      const bool in = full || wslice + it * 32 + lane < tile_n;
+      peers[u] = __match_any_sync(0xffffffffu, in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u);
     }
-    r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[it] & lt);
+#pragma unroll
+    for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
+      const int it = b0 + u;
+      const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
+      const uint32_t leader = 31 - __clz(peers[u]);
+      const bool in = full || wslice + it * 32 + lane < tile_n;
+      uint32_t base = 0;
+      if (in && lane == leader) {
+        base = s_warp_hist[warp][d];
+        s_warp_hist[warp][d] = base + __popc(peers[u]);
+      }
+      r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[u] & lt);
+    }
   }
   __syncthreads();
 
@@ -209,19 +220,19 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     st_relaxed_u64(my_status, kFlagInc | total);
   } else {
     st_relaxed_u64(my_status, kFlagAgg | total);
-    // Windowed look-back: kLookWin predecessors are read at once (independent loads).
+    // Windowed look-back: WIN predecessors are read at once (independent loads).
     int64_t t0 = (int64_t)tile - 1;
     while (true) {
-      uint64_t sv[kLookWin];
+      uint64_t sv[WIN];
 #pragma unroll
-      for (int w = 0; w < kLookWin; w++) {
+      for (int w = 0; w < WIN; w++) {
         const int64_t t = t0 - w;
         sv[w] = t >= 0 ? ld_relaxed_u64(status + (uint64_t)t * kRadix + d) : kFlagInc;
       }
       int consumed = 0;
       bool done = false;
 #pragma unroll
-      for (int w = 0; w < kLookWin; w++) {
+      for (int w = 0; w < WIN; w++) {
         if (consumed != w || done) continue;
         const uint64_t flag = sv[w] & ~kValMask;
         if (flag == 0) continue;  // not published yet: stop consuming here
@@ -231,7 +242,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
       }
       if (done) break;
       t0 -= consumed;
-      if (consumed < kLookWin) __nanosleep(32);
+      if (consumed < WIN) __nanosleep(32);
     }
     st_relaxed_u64(my_status, kFlagInc | (excl + total));
   }
@@ -255,11 +266,14 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
 
   // place keys at their tile-local sorted slot
 #pragma unroll
-  for (int it = 0; it < kSortItems; it++) {
+  for (int it = 0; it < ITEMS; it++) {
     if (wslice + it * 32 + lane < tile_n) {
-      const uint32_t dd = (uint32_t)(k[it] >> shift) & dmask;
+      // RELOAD: the key is read again (an L2 hit) instead of being held in registers across the
+      // look-back, which lets more CTAs share an SM
+      const uint64_t key = RELOAD ? __ldcs(src + it * 32) : k[it];
+      const uint32_t dd = (uint32_t)(key >> shift) & dmask;
       const uint32_t slot = s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
-      s_keys[slot] = k[it];
+      s_keys[slot] = key;
       if (KV) s_vals[slot] = v[KV ? it : 0];
     }
   }
@@ -312,8 +326,9 @@ void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s) {
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, cudaStream_t s) {
-  const uint64_t ntiles = ceil_div(n, kSortTile);
   if (vin) {
+    // (key, rowid) pairs: 4096-key tiles (the payload needs the registers)
+    const uint64_t ntiles = ceil_div(n, kSortTile);
     const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
     static bool attr = false;
     if (!attr) {
@@ -324,9 +339,19 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     radix_pass_kernel<true><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter);
   } else {
-    const size_t smem = kSortTile * sizeof(uint64_t);
-    radix_pass_kernel<false><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
-        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter);
+    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement (best of the
+    // tile-size / window / occupancy sweep in tools/radix_ablate.cu)
+    constexpr int kItems = 32;
+    const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
+    const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
+    auto kern = radix_pass_kernel<false, kItems, 4, 2, true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
+                                                      hist_pass, status, tile_counter);
   }
 }
 

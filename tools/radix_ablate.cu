@@ -343,6 +343,7 @@ void report(const char *name, const uint64_t *kin, uint64_t *kout, uint64_t n, u
 }
 
 int main(int argc, char **argv) {
+  setvbuf(stdout, nullptr, _IONBF, 0);
   const uint64_t n = (argc > 1 ? strtoull(argv[1], 0, 10) : 200000000ull) / kSortTile * kSortTile;
   std::vector<uint64_t> h(n);
   uint64_t x = 88172645463325252ull;
@@ -354,7 +355,7 @@ int main(int argc, char **argv) {
   uint32_t *hist, *ctr;
   cudaMalloc(&kin, n * 8);
   cudaMalloc(&kout, n * 8);
-  cudaMalloc(&status, (n / kSortTile) * kRadix * 8);
+  cudaMalloc(&status, (n / 2048 + 2) * kRadix * 8);
   cudaMalloc(&hist, 8 * kRadix * 4);
   cudaMalloc(&ctr, 4);
   cudaMemcpy(kin, h.data(), n * 8, cudaMemcpyHostToDevice);
@@ -372,6 +373,38 @@ int main(int argc, char **argv) {
   report<4>("tile copy (same shape)", kin, kout, n, hist, status, ctr);
   report<8>("no write-out", kin, kout, n, hist, status, ctr);
   report<9>("no write-out, no look-back", kin, kout, n, hist, status, ctr);
+  // production kernel variants: ITEMS (tile = 256 x ITEMS), look-back window, CTAs/SM
+  {
+    auto timeit = [&](auto kern, int items, const char *name) {
+      const uint64_t tile = 256ull * items;
+      const uint64_t ntiles = (n + tile - 1) / tile;
+      const size_t smem = tile * 8;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      float best = 1e9;
+      for (int rep = 0; rep < 5; rep++) {
+        cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
+        cudaMemsetAsync(ctr, 0, 4);
+        cudaEventRecord(a);
+        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        best = ms < best ? ms : best;
+      }
+      printf("%-34s %8.3f ms  %7.1f GB/s  %s\n", name, best, 16.0 * n / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+    };
+    timeit(radix_pass_kernel<false, 16, 8, 3>, 16, "items16 win8 minb3 (prod)");
+    timeit(radix_pass_kernel<false, 32, 4, 2>, 32, "items32 win4 minb2");
+    timeit(radix_pass_kernel<false, 32, 4, 2, true>, 32, "items32 win4 minb2 reload");
+    timeit(radix_pass_kernel<false, 32, 4, 3, true>, 32, "items32 win4 minb3 reload");
+    timeit(radix_pass_kernel<false, 24, 4, 3, true>, 24, "items24 win4 minb3 reload");
+    timeit(radix_pass_kernel<false, 16, 4, 4, true>, 16, "items16 win4 minb4 reload");
+    timeit(radix_pass_kernel<false, 48, 4, 2, true>, 48, "items48 win4 minb2 reload");
+  }
   // the library's real pass for comparison
   {
     cudaEvent_t a, b;
