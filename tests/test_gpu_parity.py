@@ -321,3 +321,20 @@ def test_stats_and_launch_count(ctx):
     ctx.set_profiling(False)
     assert st["launches"] >= 6 and st["joins"] == 1
     assert "radix_pass" in st["kernels"] and st["kernels"]["radix_pass"]["ms"] > 0
+
+
+def test_query_dist_world1_nccl(ctx, tmp_path):
+    """The distributed orchestration (K8 partition + NCCL all-to-all + local join) on one GPU."""
+    import torch.distributed as tdist
+    from paper_1702_03484_b200 import dist as mqd
+    if not tdist.is_initialized():
+        tdist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    s, p, o, st = datagen.lubm(2)
+    trip = (dev(s), dev(p), dev(o))
+    for cfg in ("C3", "C5"):
+        pats = config_query(cfg)
+        got = mqd.query_dist(ctx, trip, pats)
+        ref = oracle.query(s, p, o, pats)
+        assert got.vars == ref.vars
+        assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
+    tdist.destroy_process_group()
