@@ -140,7 +140,7 @@ def oracle_sample(cfg: str, budget_s: float = 20.0):
         return tuples / dt, f"rows [0,{n}) of both C4 sides (Zipf(1.1), same generator/seed)", tuples, dt
     pats = query_patterns(qname)
     # universities [0, k) of the same dataset: identical triples to the full workload's prefix
-    k = {"C1": 1, "C2": 100, "C3": 150, "C5": 300}[cfg]
+    k = {"C1": 1, "C2": 100, "C3": 300, "C5": 2500}[cfg]
     k = min(k, nu)
     (s, p, o), st, _ = lubm_host(nu, 0, k, pinned=False)
     t0 = time.perf_counter()

@@ -1,0 +1,38 @@
+"""Summarise an ncu --set full report (raw page CSV) per kernel: time, DRAM bytes, throughput.
+Usage: ncu -i X.ncu-rep --page raw --csv > raw.csv; python tools/ncu_summary.py raw.csv [traffic.json]"""
+import csv
+import json
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+h, units = rows[0], rows[1]
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+tscale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1}
+
+
+def get(r, name):
+    i = h.index(name)
+    return r[i], units[i]
+
+
+traffic = {}
+print("| kernel | grid | regs | time ms | DRAM read GB | DRAM write GB | DRAM GB/s | DRAM % peak | SM % | issued inst |")
+print("|---|---|---|---|---|---|---|---|---|---|")
+for r in rows[2:]:
+    name = get(r, "Kernel Name")[0].split("(")[0].split("::")[-1]
+    short = name.split("<")[0].replace("_kernel", "")
+    t, tu = get(r, "gpu__time_duration.sum")
+    t = float(t) * tscale[tu]
+    rd, ru = get(r, "dram__bytes_read.sum")
+    wr, wu = get(r, "dram__bytes_write.sum")
+    rd, wr = float(rd) * scale[ru], float(wr) * scale[wu]
+    dpct = get(r, "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed")[0]
+    smpct = get(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed")[0]
+    regs = get(r, "launch__registers_per_thread")[0]
+    grid = get(r, "launch__grid_size")[0]
+    inst = get(r, "smsp__inst_executed.sum")[0]
+    print(f"| {name} | {grid} | {regs} | {t*1e3:.3f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
+          f"{(rd+wr)/t/1e9:.0f} | {dpct} | {smpct} | {inst} |")
+    traffic.setdefault(short, rd + wr)
+if len(sys.argv) > 2:
+    json.dump(traffic, open(sys.argv[2], "w"), indent=1)
