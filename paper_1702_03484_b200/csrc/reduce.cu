@@ -18,7 +18,7 @@ namespace mapsq {
 namespace {
 
 constexpr int kGThreads = 256;
-constexpr int kGItems = 16;
+constexpr int kGItems = 32;
 constexpr uint64_t kGTile = kGThreads * kGItems;
 constexpr int kGWarps = kGThreads / 32;
 constexpr int kGSlice = 32 * kGItems;       // elements per warp slice
@@ -91,7 +91,8 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_nrec[kGWarps];
   __shared__ uint64_t s_base;
-  __shared__ uint32_t s_start[kGWarps][kGMaxRec], s_split[kGWarps][kGMaxRec], s_end[kGWarps][kGMaxRec];
+  __shared__ uint32_t s_start[kGWarps][kGMaxRec], s_end[kGWarps][kGMaxRec];
+  __shared__ uint16_t s_split[kGWarps][kGMaxRec];  // offset inside the warp's slice
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
@@ -150,7 +151,7 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
         else st = last_head;      // ~0 when the run began before the slice
         const uint32_t ha = hm & ~le;  // heads after this lane
         s_start[warp][idx] = (uint32_t)st;
-        s_split[warp][idx] = (uint32_t)i;
+        s_split[warp][idx] = (uint16_t)(i - sbeg);
         if (ha) s_end[warp][idx] = (uint32_t)(ibase + __ffs(ha) - 1);  // else: pending
       }
       if (sm) {
@@ -170,11 +171,11 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   // runs crossing the slice boundary: gallop (at most one start and one end per slice)
   if (lane == 0) {
     if (first_unknown >= 0) {
-      const uint32_t sp = s_split[warp][first_unknown];
+      const uint64_t sp = sbeg + s_split[warp][first_unknown];
       s_start[warp][first_unknown] = (uint32_t)run_start(W, sp, W.key(sp));
     }
     if (pending >= 0) {
-      const uint32_t sp = s_split[warp][pending];
+      const uint64_t sp = sbeg + s_split[warp][pending];
       s_end[warp][pending] = (uint32_t)run_end(W, sp, W.key(sp), n);
     }
     s_nrec[warp] = nrec;
@@ -198,7 +199,7 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   __syncthreads();
   const uint64_t out0 = s_base + s_nrec[warp];
   for (uint32_t q = lane; q < nrec; q += 32) {
-    const uint64_t st = s_start[warp][q], sp = s_split[warp][q], en = s_end[warp][q];
+    const uint64_t st = s_start[warp][q], sp = sbeg + s_split[warp][q], en = s_end[warp][q];
     g.start[out0 + q] = (uint32_t)st;
     g.split[out0 + q] = (uint32_t)sp;
     g.end[out0 + q] = (uint32_t)en;

@@ -108,14 +108,17 @@ scan_count_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
   }
 }
 
-// Pass 2 (gather), pattern-outer: for pattern j the warp walks its 32 words in batches of 8,
-// first issuing every matching lane's loads of the batch (independent, so their latency
-// overlaps), then writing them at the output cursor; cursor and column bounds live in
-// registers.  Only the 32 B sectors holding matches are read.
+// Pass 2 (gather), pattern-outer, as warp-level stream compaction: the hit positions of 8 match
+// words (256 triples) are compacted into a per-warp shared list, then processed densely — every
+// lane active, consecutive output positions, increasing input positions — instead of one
+// divergent block per word.  Only the 32 B sectors holding matches are read; the output cursor
+// and column bounds live in registers.
 __device__ __forceinline__ uint32_t pick(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
                                          const uint32_t *__restrict__ O, uint32_t src, uint64_t i) {
   return __ldcs((src == 0 ? S : (src == 1 ? P : O)) + i);
 }
+
+constexpr int kGatherWords = 8;
 
 __global__ void __launch_bounds__(kScanThreads)
 scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P,
@@ -125,12 +128,13 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
                   uint32_t *__restrict__ bmin, uint32_t *__restrict__ bmax) {
   __shared__ uint32_t s_wcnt[kWarps][MAPSQ_MAX_PATTERNS];
   __shared__ uint32_t s_min[kWarps][MAPSQ_MAX_PATTERNS * 3], s_max[kWarps][MAPSQ_MAX_PATTERNS * 3];
+  __shared__ uint16_t s_list[kWarps][kGatherWords * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.k;
   const uint64_t tile = blockIdx.x;
   const uint64_t word0 = tile * (kWarps * kScanWordsPerWarp) + (uint64_t)warp * kScanWordsPerWarp;
   const uint64_t my_word = word0 + lane;
-  const uint64_t base = word0 * 32 + lane;
+  const uint64_t row0 = word0 * 32;
   for (int j = 0; j < k; j++) {
     const uint32_t m = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
     const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(m));
@@ -138,55 +142,49 @@ scan_write_kernel(const uint32_t *__restrict__ S, const uint32_t *__restrict__ P
   }
   __syncthreads();
   const uint32_t lt = lanemask_lt();
+  uint16_t *list = s_list[warp];
   for (int j = 0; j < k; j++) {
     const uint32_t mine = my_word < mask_words ? masks[(uint64_t)j * mask_words + my_word] : 0u;
-    if (__ballot_sync(0xffffffffu, mine != 0) == 0) {
-      if (lane == 0) {
-        for (int c = 0; c < 3; c++) {
-          s_min[warp][j * 3 + c] = ~0u;
-          s_max[warp][j * 3 + c] = 0;
-        }
-      }
-      continue;
-    }
-    // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
-    uint64_t cur = tile_off[(uint64_t)j * ntiles + tile] - tile_off[(uint64_t)j * ntiles];
-    for (int w = 0; w < warp; w++) cur += s_wcnt[w][j];
-    const uint32_t nc = a.pat[j].ncols, src0 = a.pat[j].src[0], src1 = a.pat[j].src[1],
-                   src2 = a.pat[j].src[2];
-    uint32_t *o0 = out.col[j * 3], *o1 = out.col[j * 3 + 1], *o2 = out.col[j * 3 + 2];
     uint32_t mn0 = ~0u, mn1 = ~0u, mn2 = ~0u, mx0 = 0, mx1 = 0, mx2 = 0;
+    if (__ballot_sync(0xffffffffu, mine != 0) != 0) {
+      // tile_off is one scan over all patterns' tile counts: subtract pattern j's base
+      uint64_t cur = tile_off[(uint64_t)j * ntiles + tile] - tile_off[(uint64_t)j * ntiles];
+      for (int w = 0; w < warp; w++) cur += s_wcnt[w][j];
+      const uint32_t nc = a.pat[j].ncols, src0 = a.pat[j].src[0], src1 = a.pat[j].src[1],
+                     src2 = a.pat[j].src[2];
+      uint32_t *o0 = out.col[j * 3], *o1 = out.col[j * 3 + 1], *o2 = out.col[j * 3 + 2];
 #pragma unroll 1
-    for (int w0 = 0; w0 < kScanWordsPerWarp; w0 += 8) {
-      uint32_t mw[8], v0[8], v1[8], v2[8];
+      for (int w0 = 0; w0 < kScanWordsPerWarp; w0 += kGatherWords) {
+        uint32_t h = 0;
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        mw[u] = __shfl_sync(0xffffffffu, mine, w0 + u);
-        const bool hit = (mw[u] >> lane) & 1u;
-        const uint64_t i = base + (uint64_t)(w0 + u) * 32;
-        v0[u] = hit ? pick(S, P, O, src0, i) : 0u;
-        v1[u] = (hit && nc > 1) ? pick(S, P, O, src1, i) : 0u;
-        v2[u] = (hit && nc > 2) ? pick(S, P, O, src2, i) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        if ((mw[u] >> lane) & 1u) {
-          const uint64_t pos = cur + __popc(mw[u] & lt);
-          st_cs_u32(o0 + pos, v0[u]);
-          mn0 = min(mn0, v0[u]);
-          mx0 = max(mx0, v0[u]);
+        for (int u = 0; u < kGatherWords; u++) {
+          const uint32_t m = __shfl_sync(0xffffffffu, mine, w0 + u);
+          if ((m >> lane) & 1u) list[h + __popc(m & lt)] = (uint16_t)((w0 + u) * 32 + lane);
+          h += __popc(m);
+        }
+        __syncwarp();
+        for (uint32_t q = lane; q < h; q += 32) {
+          const uint64_t i = row0 + list[q];
+          const uint64_t pos = cur + q;
+          const uint32_t v0 = pick(S, P, O, src0, i);
+          st_cs_u32(o0 + pos, v0);
+          mn0 = min(mn0, v0);
+          mx0 = max(mx0, v0);
           if (nc > 1) {
-            st_cs_u32(o1 + pos, v1[u]);
-            mn1 = min(mn1, v1[u]);
-            mx1 = max(mx1, v1[u]);
+            const uint32_t v1 = pick(S, P, O, src1, i);
+            st_cs_u32(o1 + pos, v1);
+            mn1 = min(mn1, v1);
+            mx1 = max(mx1, v1);
           }
           if (nc > 2) {
-            st_cs_u32(o2 + pos, v2[u]);
-            mn2 = min(mn2, v2[u]);
-            mx2 = max(mx2, v2[u]);
+            const uint32_t v2 = pick(S, P, O, src2, i);
+            st_cs_u32(o2 + pos, v2);
+            mn2 = min(mn2, v2);
+            mx2 = max(mx2, v2);
           }
         }
-        cur += __popc(mw[u]);
+        cur += h;
+        __syncwarp();
       }
     }
     mn0 = __reduce_min_sync(0xffffffffu, mn0);
