@@ -102,6 +102,11 @@ def lubm_id_end(n_univ: int, u_hi: int | None = None, seed: int = 42) -> int:
     return int(_lib().lubm_id_end(seed, n_univ, n_univ if u_hi is None else u_hi))
 
 
+def lubm_univ_base(n_univ: int, u: int, seed: int = 42) -> int:
+    """First dictionary ID of university u's block (entities + literals of u follow)."""
+    return int(_lib().lubm_univ_base(seed, n_univ, u))
+
+
 def lubm_pool_size(n_univ: int) -> int:
     return int(_lib().lubm_pool_size(n_univ))
 
