@@ -34,36 +34,35 @@ def ctx():
     return mq.Context(0)
 
 
-@pytest.fixture(scope="module")
-def lubm10000():
-    s, p, o, st = datagen.lubm(10000)
-    return s, p, o, st
+_DATA = {}
 
 
-@pytest.mark.parametrize("cfg", ["C5", "C3", "C2", "C1"])
-def test_lubm10000_sampled_universities(ctx, lubm10000, cfg):
-    s, p, o, st = lubm10000
+def lubm_full(nu):
+    if nu not in _DATA:
+        _DATA.clear()
+        _DATA[nu] = datagen.lubm(nu)
+    return _DATA[nu]
+
+
+# (config, its BASELINE.json scale)
+@pytest.mark.parametrize("cfg,nu", [("C5", 10000), ("C3", 1000), ("C2", 100), ("C1", 1)])
+def test_lubm_full_size_sampled_universities(ctx, cfg, nu):
+    s, p, o, st = lubm_full(nu)
     trip = (dev(s), dev(p), dev(o))
     pats = config_query(cfg)
     got = ctx.query(trip, pats)
-    if cfg == "C5":
-        assert got.nrows == st["c5_j2"]
-    elif cfg == "C3":
-        assert got.nrows == st["c3_j3"]
-    elif cfg == "C2":
-        assert got.nrows == st["c2_j2"]
-    else:
-        assert got.nrows == st["c1_rs"]
+    assert got.nrows == config_expected_counts(cfg, st)[-1]
     rows = got.to_numpy()
     del trip
     # the variable whose value identifies the university block: a person (C1/C2/C5 ?x, ?X) or a
     # department (C3 ?x) — always variable 0
     col0 = rows[:, got.vars.index(0)].astype(np.int64)
     rng = np.random.default_rng(5)
-    for u in sorted(rng.choice(10000, 4, replace=False).tolist()) + [9999]:
-        lo, hi = datagen.lubm_univ_base(10000, u), datagen.lubm_univ_base(10000, u + 1)
+    picks = sorted(set(rng.choice(nu, min(nu, 4), replace=False).tolist()) | {nu - 1})
+    for u in picks:
+        lo, hi = datagen.lubm_univ_base(nu, u), datagen.lubm_univ_base(nu, u + 1)
         mine = rows[(col0 >= lo) & (col0 < hi)]
-        su, pu, ou, _ = datagen.lubm(10000, u, u + 1)
+        su, pu, ou, _ = datagen.lubm(nu, u, u + 1)
         ref = oracle.query(su, pu, ou, pats)
         assert ref.vars == got.vars
         assert np.array_equal(oracle.canonical_rows(mine), oracle.canonical(ref).rows), (cfg, u)
