@@ -84,9 +84,12 @@ __device__ uint64_t run_end(const WordView &W, uint64_t from, uint64_t k, uint64
 // at or before it and ends at the next head after it, both tracked across items in registers
 // ("pending" end).  Only a run crossing the slice boundary needs a gallop (at most one start and
 // one end per slice).  Records go to shared memory, the tile's split count is resolved with a
-// warp-parallel decoupled look-back, and records are stored in key order.
+// warp-parallel decoupled look-back, and records are stored in key order.  Positions are 32-bit
+// (n < 2^32); for P64 words "same key" is ((w ^ w_prev) >> ib) == 0 and the label is the low
+// word's rowid compared with n1.
+template <bool KV>
 __global__ void __launch_bounds__(kGThreads)
-find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restrict__ status,
+find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restrict__ status,
                    uint32_t *__restrict__ tile_counter, uint64_t *__restrict__ ngroups_dev) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_nrec[kGWarps];
@@ -96,75 +99,91 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
+  const uint32_t n = (uint32_t)n64;
   const uint64_t tile = s_tile;
-  const uint64_t sbeg = tile * kGTile + (uint64_t)warp * kGSlice;  // slice [sbeg, send)
-  const uint64_t send = sbeg + kGSlice < n ? sbeg + kGSlice : n;
+  const uint64_t sbeg64 = tile * kGTile + (uint64_t)warp * kGSlice;
+  const uint32_t sbeg = sbeg64 < n64 ? (uint32_t)sbeg64 : n;  // slice [sbeg, send)
+  const uint32_t send = (n - sbeg) > (uint32_t)kGSlice ? sbeg + kGSlice : n;
   const uint32_t le = lt_or_eq_mask(lane), lt = lanemask_lt();
+  const uint32_t imask = (uint32_t)W.idx_mask, n1 = (uint32_t)W.n1, ib = W.ib;
   uint32_t nrec = 0;
   int32_t pending = -1;             // record whose run has not ended yet
-  uint64_t last_head = ~0ull;       // last head seen in this slice (~0: none yet)
+  uint32_t last_head = 0xffffffffu; // last head seen in this slice (none yet)
   int32_t first_unknown = -1;       // first record whose run started before the slice
-  uint64_t carry_k = ~0ull;
-  bool carry_r = true;
-  if (sbeg < n && sbeg > 0) {
-    uint64_t k;
-    bool r;
-    W.load(sbeg - 1, &k, &r);
-    carry_k = k;
-    carry_r = r;
+  // previous element: (key, label) as one comparable pair
+  uint64_t carry_w = 0, carry_k = ~0ull;
+  uint32_t carry_v = 0;
+  if (sbeg < send && sbeg > 0) {
+    if (KV) { carry_k = W.keys[sbeg - 1]; carry_v = W.vals[sbeg - 1]; }
+    else carry_w = W.words[sbeg - 1];
   }
   constexpr int kB = 8;
 #pragma unroll 1
-  for (int it0 = 0; it0 < kGItems; it0 += kB) {
-    uint64_t kk[kB];
-    bool rr[kB];
+  for (uint32_t it0 = 0; it0 < (uint32_t)kGItems; it0 += kB) {
+    uint64_t ww[kB];
+    uint32_t vv[KV ? kB : 1];
 #pragma unroll
     for (int u = 0; u < kB; u++) {
-      const uint64_t i = sbeg + (uint64_t)(it0 + u) * 32 + lane;
-      kk[u] = ~0ull;
-      rr[u] = false;
-      if (i < send) W.load(i, &kk[u], &rr[u]);
+      const uint32_t i = sbeg + (it0 + u) * 32 + lane;
+      if (KV) {
+        ww[u] = i < send ? __ldcs(W.keys + i) : 0ull;
+        vv[KV ? u : 0] = i < send ? __ldcs(W.vals + i) : 0u;
+      } else {
+        ww[u] = i < send ? __ldcs(W.words + i) : 0ull;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kB; u++) {
-      const uint64_t ibase = sbeg + (uint64_t)(it0 + u) * 32;
+      const uint32_t ibase = sbeg + (it0 + u) * 32;
       if (ibase >= send) break;  // warp-uniform
-      const uint64_t i = ibase + lane;
+      const uint32_t i = ibase + lane;
       const bool in = i < send;
-      const uint64_t kup = __shfl_up_sync(0xffffffffu, kk[u], 1);
-      const bool rup = __shfl_up_sync(0xffffffffu, rr[u], 1);
-      const uint64_t kprev = lane == 0 ? carry_k : kup;
-      const bool rprev = lane == 0 ? carry_r : rup;
-      const bool head = in && (i == 0 || kk[u] != kprev);
-      const bool split = in && i > 0 && rr[u] && !rprev && kk[u] == kprev;
+      const uint64_t w = ww[u];
+      uint64_t wp = __shfl_up_sync(0xffffffffu, w, 1);
+      bool same, r, rp;
+      if (KV) {
+        const uint32_t v = vv[KV ? u : 0];
+        uint32_t vp = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0) { wp = carry_k; vp = carry_v; }
+        same = w == wp;
+        r = v >= n1;
+        rp = vp >= n1;
+      } else {
+        if (lane == 0) wp = carry_w;
+        same = ((w ^ wp) >> ib) == 0;
+        r = ((uint32_t)w & imask) >= n1;
+        rp = ((uint32_t)wp & imask) >= n1;
+      }
+      const bool head = in && (i == 0 || !same || (lane == 0 && sbeg == 0 && i == 0));
+      const bool split = in && i > 0 && r && !rp && same;
       const uint32_t hm = __ballot_sync(0xffffffffu, head);
       const uint32_t sm = __ballot_sync(0xffffffffu, split);
       if (pending >= 0 && hm) {  // the pending run ends at this item's first head
-        if (lane == 0) s_end[warp][pending] = (uint32_t)(ibase + __ffs(hm) - 1);
+        if (lane == 0) s_end[warp][pending] = ibase + __ffs(hm) - 1;
         pending = -1;
       }
-      if (split) {
-        const uint32_t idx = nrec + __popc(sm & lt);
-        const uint32_t hb = hm & le;  // heads at or before this lane
-        uint64_t st;
-        if (hb) st = ibase + 31 - __clz(hb);
-        else st = last_head;      // ~0 when the run began before the slice
-        const uint32_t ha = hm & ~le;  // heads after this lane
-        s_start[warp][idx] = (uint32_t)st;
-        s_split[warp][idx] = (uint16_t)(i - sbeg);
-        if (ha) s_end[warp][idx] = (uint32_t)(ibase + __ffs(ha) - 1);  // else: pending
-      }
-      if (sm) {
+      if (sm) {  // warp-uniform: rare relative to elements
+        if (split) {
+          const uint32_t idx = nrec + __popc(sm & lt);
+          const uint32_t hb = hm & le;  // heads at or before this lane
+          const uint32_t ha = hm & ~le;  // heads after this lane
+          s_start[warp][idx] = hb ? ibase + 31 - __clz(hb) : last_head;
+          s_split[warp][idx] = (uint16_t)(i - sbeg);
+          if (ha) s_end[warp][idx] = ibase + __ffs(ha) - 1;  // else: pending
+        }
         const int hi_lane = 31 - __clz(sm);
-        const uint32_t ha = hm & ~lt_or_eq_mask(hi_lane);
-        if (!ha) pending = (int32_t)(nrec + __popc(sm) - 1);
-        if (first_unknown < 0 && last_head == ~0ull && !(hm & lt_or_eq_mask(__ffs(sm) - 1)))
+        if (!(hm & ~lt_or_eq_mask(hi_lane))) pending = (int32_t)(nrec + __popc(sm) - 1);
+        if (first_unknown < 0 && last_head == 0xffffffffu && !(hm & lt_or_eq_mask(__ffs(sm) - 1)))
           first_unknown = (int32_t)nrec;
+        nrec += __popc(sm);
       }
-      nrec += __popc(sm);
       if (hm) last_head = ibase + 31 - __clz(hm);
-      carry_k = __shfl_sync(0xffffffffu, kk[u], 31);
-      carry_r = __shfl_sync(0xffffffffu, rr[u], 31);
+      if (KV) {
+        carry_k = __shfl_sync(0xffffffffu, w, 31);
+        carry_v = __shfl_sync(0xffffffffu, vv[KV ? u : 0], 31);
+      } else {
+        carry_w = __shfl_sync(0xffffffffu, w, 31);
+      }
     }
   }
   __syncwarp();
@@ -176,7 +195,7 @@ find_groups_kernel(const WordView W, uint64_t n, GroupOut g, uint64_t *__restric
     }
     if (pending >= 0) {
       const uint64_t sp = sbeg + s_split[warp][pending];
-      s_end[warp][pending] = (uint32_t)run_end(W, sp, W.key(sp), n);
+      s_end[warp][pending] = (uint32_t)run_end(W, sp, W.key(sp), n64);
     }
     s_nrec[warp] = nrec;
   }
@@ -371,8 +390,12 @@ void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint3
   W.ib = ib;
   W.idx_mask = (ib >= 64) ? ~0ull : ((1ull << ib) - 1);
   const uint64_t ntiles = ceil_div(n, kGTile);
-  find_groups_kernel<<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
-                                                            ngroups_dev);
+  if (words)
+    find_groups_kernel<false><<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
+                                                                   ngroups_dev);
+  else
+    find_groups_kernel<true><<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
+                                                                  ngroups_dev);
 }
 
 uint64_t find_groups_tiles(uint64_t n) { return ceil_div(n, kGTile); }
