@@ -349,8 +349,11 @@ mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *v
     uint32_t *vout = va ? ((*which == 0) ? vb : va) : nullptr;
     {
       KTimer kt(ctx, s, va ? "radix_pass_kv" : "radix_pass", bytes);
+      const bool more = p + 1 < passes;
+      const uint32_t nbits_next = more ? std::min<uint32_t>(8, nbits - 8 * (p + 1)) : 0;
       launch_radix_pass(kin, kout, vin, vout, n, shift, bits, hist + p * kRadix, status,
-                        counters + p, s);
+                        counters + p, more ? hist + (p + 1) * kRadix : nullptr, shift + 8,
+                        nbits_next, s);
       CKL("radix_pass");
     }
     *which ^= 1;
@@ -405,9 +408,9 @@ PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_
   pa.ib = pl.ib;
   pa.kv = pl.path == MAPSQ_PATH_KV;
   pa.bit_lo = pa.kv ? 0 : pl.ib;
-  pa.passes = pl.passes;
-  const uint32_t last_bits = pl.kb - 8 * (pl.passes ? pl.passes - 1 : 0);
-  pa.last_mask = pl.passes ? ((1u << last_bits) - 1u) : 0xffu;
+  // the Map kernel counts only the first digit; each digit pass counts the next one
+  pa.passes = pl.passes ? 1 : 0;
+  pa.last_mask = pl.passes == 1 ? ((1u << pl.kb) - 1u) : 0xffu;
   return pa;
 }
 
@@ -452,11 +455,6 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
     launch_pack_hist(pa, wa, va, hist, s);
     CKL("pack_hist");
-  }
-  if (pl.passes) {
-    KTimer kt(ctx, s, "hist_scan", 8ull * kRadix * pl.passes);
-    launch_hist_scan(hist, (int)pl.passes, s);
-    CKL("hist_scan");
   }
   // ---- Sort (row a4)
   int which = 0;
@@ -990,13 +988,8 @@ static mapsq_status sort_entry(mapsq_ctx *ctx, uint64_t *keys, uint32_t *vals, u
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
   {
     KTimer kt(ctx, s, "key_hist", 8ull * n);
-    launch_key_hist(keys, n, bit_lo, passes, nbits - 8 * (passes - 1), hist, s);
+    launch_key_hist(keys, n, bit_lo, 1, passes == 1 ? nbits : 8, hist, s);  // first digit only
     CKL("key_hist");
-  }
-  {
-    KTimer kt(ctx, s, "hist_scan", 8ull * kRadix * passes);
-    launch_hist_scan(hist, (int)passes, s);
-    CKL("hist_scan");
   }
   int which = 0;
   TRY(radix_sort(ctx, keys, kb_, vals, vb, n, bit_lo, nbits, hist, sc, s, &which));

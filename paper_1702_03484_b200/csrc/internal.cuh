@@ -274,9 +274,12 @@ void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32
 void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t passes,
                      uint32_t last_bits, uint32_t *hist, cudaStream_t s);
 // One onesweep digit pass (K3).
+// hist_pass: this pass's RAW digit counts (the kernel scans them); hist_next (may be NULL):
+// zeroed counts the pass fills with the next digit (bits [next_shift, next_shift + next_bits)).
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
-                       uint64_t *status, uint32_t *tile_counter, cudaStream_t s);
+                       uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s);
 
 // ReduceDuplicate (K4): groups present on both sides, in key order.
 struct GroupOut {

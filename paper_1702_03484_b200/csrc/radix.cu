@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
                   uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
-                  uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
+                  uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter,
+                  uint32_t *__restrict__ hist_next, uint32_t next_shift, uint32_t next_mask) {
   constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
@@ -142,11 +143,13 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   __shared__ uint64_t s_global_base[kRadix];
   __shared__ uint32_t s_wsum[kWarps];
   __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_next[kRadix];
 
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
 #pragma unroll
   for (int q = 0; q < kWarps; q++) s_warp_hist[q][tid] = 0;  // kSortThreads == kRadix
+  s_next[tid] = 0;
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t tile_base = tile * TILE;
@@ -201,6 +204,9 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
         s_warp_hist[warp][d] = base + __popc(peers[u]);
       }
       r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[u] & lt);
+      // the NEXT pass's digit histogram, from the keys already in registers (one shared atomic
+      // per key; these issue slots are otherwise idle while the tile waits on its look-back)
+      if (hist_next && in) atomicAdd(&s_next[(uint32_t)(k[it] >> next_shift) & next_mask], 1u);
     }
   }
   __syncthreads();
@@ -261,7 +267,23 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     if ((uint32_t)w < warp) pre += s_wsum[w];
   const uint32_t dstart = pre + x - total;
   s_digit_start[d] = dstart;
-  s_global_base[d] = (uint64_t)hist_pass[d] + excl - dstart;
+  // exclusive scan of this pass's global digit counts (each CTA scans the 256 totals itself)
+  const uint32_t hc = __ldg(hist_pass + d);
+  uint32_t hx = hc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, hx, o);
+    if (lane >= (uint32_t)o) hx += y;
+  }
+  __syncthreads();  // s_wsum reuse
+  if (lane == 31) s_wsum[warp] = hx;
+  __syncthreads();
+  uint32_t hpre = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; w++)
+    if ((uint32_t)w < warp) hpre += s_wsum[w];
+  s_global_base[d] = (uint64_t)(hpre + hx - hc) + excl - dstart;
+  if (hist_next && s_next[d]) atomicAdd(hist_next + d, s_next[d]);
   __syncthreads();
 
   // place keys at their tile-local sorted slot
@@ -325,7 +347,9 @@ void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s) {
 
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
-                       uint64_t *status, uint32_t *tile_counter, cudaStream_t s) {
+                       uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s) {
+  const uint32_t next_mask = (1u << next_bits) - 1u;
   if (vin) {
     // (key, rowid) pairs: 4096-key tiles (the payload needs the registers)
     const uint64_t ntiles = ceil_div(n, kSortTile);
@@ -337,7 +361,8 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
       attr = true;
     }
     radix_pass_kernel<true><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
-        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter);
+        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
+        next_shift, next_mask);
   } else {
     // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement (best of the
     // tile-size / window / occupancy sweep in tools/radix_ablate.cu)
@@ -351,7 +376,8 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
       attr = true;
     }
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
-                                                      hist_pass, status, tile_counter);
+                                                      hist_pass, status, tile_counter, hist_next,
+                                                      next_shift, next_mask);
   }
 }
 

@@ -362,9 +362,10 @@ int main(int argc, char **argv) {
   // exact digit offsets of bits [8,16) for the real pass
   std::vector<uint32_t> hh(kRadix, 0);
   for (uint64_t i = 0; i < n; i++) hh[(h[i] >> 8) & 255]++;
+  std::vector<uint32_t> hx(hh);  // exclusive offsets for the ablation kernels, raw counts for the library pass
   uint32_t run_ = 0;
-  for (int d = 0; d < kRadix; d++) { uint32_t c = hh[d]; hh[d] = run_; run_ += c; }
-  cudaMemcpy(hist, hh.data(), kRadix * 4, cudaMemcpyHostToDevice);
+  for (int d = 0; d < kRadix; d++) { uint32_t c = hx[d]; hx[d] = run_; run_ += c; }
+  cudaMemcpy(hist, hx.data(), kRadix * 4, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(ablate_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortTile * 8);
   report<0>("full pass", kin, kout, n, hist, status, ctr);
   report<1>("no look-back", kin, kout, n, hist, status, ctr);
@@ -388,7 +389,7 @@ int main(int argc, char **argv) {
         cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
         cudaMemsetAsync(ctr, 0, 4);
         cudaEventRecord(a);
-        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr);
+        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, nullptr, 16, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -415,7 +416,7 @@ int main(int argc, char **argv) {
       cudaMemsetAsync(status, 0, (n / kSortTile) * kRadix * 8);
       cudaMemsetAsync(ctr, 0, 4);
       cudaEventRecord(a);
-      launch_radix_pass(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, 0);
+      launch_radix_pass(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, nullptr, 16, 8, 0);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
