@@ -20,7 +20,7 @@ namespace {
 constexpr int kWarps = kSortThreads / 32;
 constexpr int kLookWin = 8;
 constexpr int kHistThreads = 256;
-constexpr int kHistItems = 8;
+constexpr int kHistItems = 16;
 
 constexpr int kHistCopies = 4;
 
@@ -38,20 +38,22 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
   const uint64_t n = a.n1 + a.n2;
   const uint64_t chunk = (uint64_t)kHistThreads * kHistItems;
   for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    // key columns outermost, items innermost: all kHistItems loads of a column are in flight
+    // together (a per-item column loop serialized them on load latency)
     uint64_t key[kHistItems];
 #pragma unroll
-    for (int it = 0; it < kHistItems; it++) {
-      const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
-      uint64_t kk = 0;
-      if (i < n) {
-        const bool left = i < a.n1;
-        const uint64_t r = left ? i : i - a.n1;
-        for (uint32_t c = 0; c < a.nkey; c++) {
-          const uint32_t v = left ? __ldcs(a.key1[c] + r) : __ldcs(a.key2[c] + r);
-          kk |= (uint64_t)(v - a.lo[c]) << a.shift[c];
-        }
+    for (int it = 0; it < kHistItems; it++) key[it] = 0;
+    for (uint32_t c = 0; c < a.nkey; c++) {
+      const uint32_t *k1 = a.key1[c], *k2 = a.key2[c] - a.n1;
+      const uint32_t lo = a.lo[c], sh = a.shift[c];
+      uint32_t v[kHistItems];
+#pragma unroll
+      for (int it = 0; it < kHistItems; it++) {
+        const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
+        v[it] = i < n ? __ldcs((i < a.n1 ? k1 : k2) + i) : lo;
       }
-      key[it] = kk;
+#pragma unroll
+      for (int it = 0; it < kHistItems; it++) key[it] |= (uint64_t)(v[it] - lo) << sh;
     }
 #pragma unroll
     for (int it = 0; it < kHistItems; it++) {

@@ -228,8 +228,10 @@ find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restr
 
 // ------------------------------------------------------------------------------ expand (K6)
 constexpr int kEThreads = 256;
-constexpr int kERows = 4;
-constexpr uint64_t kETile = kEThreads * kERows;
+constexpr int kERows = 4;                    // consecutive rows per chunk (one 16 B store)
+constexpr int kEChunks = 2;                  // chunks per thread
+constexpr uint64_t kETile = (uint64_t)kEThreads * kERows * kEChunks;
+constexpr int kEGroups = 1024;               // groups staged in shared memory per tile
 
 __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, uint64_t hi,
                                              uint64_t r) {
@@ -241,11 +243,20 @@ __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, u
   return lo;
 }
 
+// K6.  A CTA owns kETile consecutive output rows; two threads bracket its group range [g0, g1]
+// with binary searches and, when it has at most kEGroups groups (always, except for tiles full of
+// 1-row groups), the groups' (offset, start, split, end) are staged in shared memory.  Each
+// thread owns kEChunks chunks of kERows consecutive rows (chunk c of thread t starts at row
+// t0 + (c * kEThreads + t) * kERows, so a warp's chunks are contiguous): it locates its group in
+// shared memory, then computes the 8 (LEFT, RIGHT) positions, issues all word loads, then all
+// column gathers, then 16 B streaming stores — so the latencies of one thread's rows overlap.
 __global__ void __launch_bounds__(kEThreads)
 expand_kernel(const ExpandArgs a) {
   __shared__ const uint32_t *s_src[MAPSQ_MAX_COLS];
   __shared__ uint32_t *s_dst[MAPSQ_MAX_COLS];
   __shared__ uint64_t s_g[2];
+  __shared__ uint64_t s_off[kEGroups + 1];
+  __shared__ uint32_t s_start[kEGroups], s_split[kEGroups], s_end[kEGroups];
   const int tid = threadIdx.x;
   const uint32_t nout = a.nkey + a.nrest1 + a.nrest2;
   if (tid < MAPSQ_MAX_COLS) {
@@ -258,71 +269,128 @@ expand_kernel(const ExpandArgs a) {
   const uint64_t t1 = (t0 + kETile < a.m ? t0 + kETile : a.m) - 1;
   if (tid < 2) s_g[tid] = group_of(a.goff, 0, a.ngroups - 1, tid == 0 ? t0 : t1);
   __syncthreads();
-  const uint64_t r0 = t0 + (uint64_t)tid * kERows;
-  if (r0 >= a.m) return;
-  uint64_t g = group_of(a.goff, s_g[0], s_g[1], r0);
+  const uint64_t g0 = s_g[0], g1 = s_g[1];
+  const bool staged = g1 - g0 + 1 <= (uint64_t)kEGroups;
+  if (staged) {
+    for (uint64_t q = tid; q <= g1 - g0; q += kEThreads) {
+      const uint64_t g = g0 + q;
+      s_off[q] = a.goff[g];
+      s_start[q] = a.gstart[g];
+      s_split[q] = a.gsplit[g];
+      s_end[q] = a.gend[g];
+    }
+    if (tid == 0) s_off[g1 - g0 + 1] = (g1 + 1 < a.ngroups) ? a.goff[g1 + 1] : a.m;
+  }
+  __syncthreads();
   const uint64_t idx_mask = (a.ib >= 64) ? ~0ull : ((1ull << a.ib) - 1);
-
-  uint64_t lkey[kERows];
-  uint32_t lidx[kERows], ridx[kERows];
-  int nrow = 0;
-  uint64_t gbeg = a.goff[g];
-  uint64_t gend = (g + 1 < a.ngroups) ? a.goff[g + 1] : a.m;
-  uint32_t start = a.gstart[g], split = a.gsplit[g], end = a.gend[g];
-  uint64_t nR = end - split;
-  uint64_t local = r0 - gbeg;
-  uint64_t li = local / nR, ri = local - li * nR;
+  constexpr int R = kERows * kEChunks;
+  uint64_t lpos[R], rpos[R];
+  int nrow[kEChunks];
 #pragma unroll
-  for (int j = 0; j < kERows; j++) {
-    const uint64_t r = r0 + j;
-    if (r >= a.m) break;
-    if (r >= gend) {  // next group (groups are never empty)
-      g++;
-      gbeg = gend;
-      gend = (g + 1 < a.ngroups) ? a.goff[g + 1] : a.m;
-      start = a.gstart[g];
-      split = a.gsplit[g];
-      end = a.gend[g];
-      nR = end - split;
-      li = 0;
-      ri = 0;
-    }
-    const uint64_t lpos = start + li, rpos = split + ri;
-    if (a.words) {
-      const uint64_t lw = a.words[lpos], rw = a.words[rpos];
-      lkey[j] = lw >> a.ib;
-      lidx[j] = (uint32_t)(lw & idx_mask);
-      ridx[j] = (uint32_t)((rw & idx_mask) - a.n1);
+  for (int c = 0; c < kEChunks; c++) {
+    const uint64_t r0 = t0 + ((uint64_t)c * kEThreads + tid) * kERows;
+    nrow[c] = 0;
+    if (r0 >= a.m) continue;
+    // locate r0's group
+    uint64_t gl, gbeg, gend;
+    uint32_t start, split, end;
+    if (staged) {
+      uint32_t lo = 0, hi = (uint32_t)(g1 - g0);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (s_off[mid] <= r0) lo = mid; else hi = mid - 1;
+      }
+      gl = lo;
+      gbeg = s_off[gl];
+      gend = s_off[gl + 1];
+      start = s_start[gl]; split = s_split[gl]; end = s_end[gl];
     } else {
-      lkey[j] = a.keys[lpos];
-      lidx[j] = a.vals[lpos];
-      ridx[j] = a.vals[rpos] - (uint32_t)a.n1;
+      gl = group_of(a.goff, g0, g1, r0);
+      gbeg = a.goff[gl];
+      gend = (gl + 1 < a.ngroups) ? a.goff[gl + 1] : a.m;
+      start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
     }
-    nrow++;
-    if (++ri == nR) {
-      ri = 0;
-      li++;
+    uint64_t nR = end - split;
+    const uint64_t local = r0 - gbeg;
+    uint64_t li, ri;
+    if ((local >> 32) == 0 && (nR >> 32) == 0) {
+      li = (uint32_t)local / (uint32_t)nR;
+      ri = (uint32_t)local - (uint32_t)li * (uint32_t)nR;
+    } else {
+      li = local / nR;
+      ri = local - li * nR;
+    }
+#pragma unroll
+    for (int j = 0; j < kERows; j++) {
+      const uint64_t r = r0 + j;
+      if (r >= a.m) break;
+      if (r >= gend) {  // next group (groups are never empty)
+        gl++;
+        gbeg = gend;
+        if (staged) {
+          gend = s_off[gl + 1];
+          start = s_start[gl]; split = s_split[gl]; end = s_end[gl];
+        } else {
+          gend = (gl + 1 < a.ngroups) ? a.goff[gl + 1] : a.m;
+          start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
+        }
+        nR = end - split;
+        li = 0;
+        ri = 0;
+      }
+      lpos[c * kERows + j] = start + li;
+      rpos[c * kERows + j] = split + ri;
+      nrow[c]++;
+      if (++ri == nR) {
+        ri = 0;
+        li++;
+      }
     }
   }
-  const bool full = (nrow == kERows);
-  for (uint32_t c = 0; c < nout; c++) {
-    uint32_t v[kERows];
-    if (c < a.nkey) {
-      const uint32_t sh = a.key_shift[c], mk = a.key_mask[c], lo = a.key_lo[c];
+  // all word loads of the thread's rows, then decode
+  uint64_t lkey[R];
+  uint32_t lidx[R], ridx[R];
 #pragma unroll
-      for (int j = 0; j < kERows; j++) v[j] = (uint32_t)(lkey[j] >> sh & mk) + lo;
+  for (int q = 0; q < R; q++) {
+    const bool v = (q % kERows) < nrow[q / kERows];
+    if (a.words) {
+      const uint64_t lw = v ? __ldg(a.words + lpos[q]) : 0ull;
+      const uint64_t rw = v ? __ldg(a.words + rpos[q]) : 0ull;
+      lkey[q] = lw >> a.ib;
+      lidx[q] = (uint32_t)(lw & idx_mask);
+      ridx[q] = (uint32_t)((rw & idx_mask) - a.n1);
     } else {
-      const uint32_t *src = s_src[c];
-      const bool left = c < a.nkey + a.nrest1;
-#pragma unroll
-      for (int j = 0; j < kERows; j++)
-        v[j] = (j < nrow) ? __ldg(src + (left ? lidx[j] : ridx[j])) : 0u;
+      lkey[q] = v ? __ldg(a.keys + lpos[q]) : 0ull;
+      lidx[q] = v ? __ldg(a.vals + lpos[q]) : 0u;
+      ridx[q] = v ? __ldg(a.vals + rpos[q]) - (uint32_t)a.n1 : 0u;
     }
-    uint32_t *dst = s_dst[c] + r0;
-    if (full) {
-      st_cs_v4(dst, make_uint4(v[0], v[1], v[2], v[3]));
+  }
+  for (uint32_t col = 0; col < nout; col++) {
+    uint32_t val[R];
+    if (col < a.nkey) {
+      const uint32_t sh = a.key_shift[col], mk = a.key_mask[col], lo = a.key_lo[col];
+#pragma unroll
+      for (int q = 0; q < R; q++) val[q] = (uint32_t)(lkey[q] >> sh & mk) + lo;
     } else {
-      for (int j = 0; j < nrow; j++) st_cs_u32(dst + j, v[j]);
+      const uint32_t *src = s_src[col];
+      const bool left = col < a.nkey + a.nrest1;
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        const bool v = (q % kERows) < nrow[q / kERows];
+        val[q] = v ? __ldg(src + (left ? lidx[q] : ridx[q])) : 0u;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kEChunks; c++) {
+      if (nrow[c] == 0) continue;
+      const uint64_t r0 = t0 + ((uint64_t)c * kEThreads + tid) * kERows;
+      uint32_t *dst = s_dst[col] + r0;
+      if (nrow[c] == kERows) {
+        st_cs_v4(dst, make_uint4(val[c * kERows], val[c * kERows + 1], val[c * kERows + 2],
+                                 val[c * kERows + 3]));
+      } else {
+        for (int j = 0; j < nrow[c]; j++) st_cs_u32(dst + j, val[c * kERows + j]);
+      }
     }
   }
 }
