@@ -389,7 +389,9 @@ expand_kernel(const ExpandArgs a) {
         st_cs_v4(dst, make_uint4(val[c * kERows], val[c * kERows + 1], val[c * kERows + 2],
                                  val[c * kERows + 3]));
       } else {
-        for (int j = 0; j < nrow[c]; j++) st_cs_u32(dst + j, val[c * kERows + j]);
+#pragma unroll
+        for (int j = 0; j < kERows; j++)  // (static indices: no local-memory copy of val[])
+          if (j < nrow[c]) st_cs_u32(dst + j, val[c * kERows + j]);
       }
     }
   }
