@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
 // slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
 // full tiles skip every bounds check (the first version spent most of its issue slots on 64-bit
 // index arithmetic).
-template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false>
+template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false,
+          bool BALLOT = false>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
@@ -192,7 +193,19 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
       const int it = b0 + u;
       const bool in = full || wslice + it * 32 + lane < tile_n;
-      peers[u] = __match_any_sync(0xffffffffu, in ? ((uint32_t)(k[it] >> shift) & dmask) : 0x100u);
+      const uint32_t dg = (uint32_t)(k[it] >> shift) & dmask;
+      if (BALLOT) {  // peers from one ballot per digit bit (short-latency votes)
+        uint32_t pm = __ballot_sync(0xffffffffu, in);
+        pm = in ? pm : ~pm;
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          const uint32_t bb = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
+          pm &= ((dg >> b) & 1u) ? bb : ~bb;
+        }
+        peers[u] = pm;
+      } else {
+        peers[u] = __match_any_sync(0xffffffffu, in ? dg : 0x100u);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
@@ -356,22 +369,23 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     // (key, rowid) pairs: 4096-key tiles (the payload needs the registers)
     const uint64_t ntiles = ceil_div(n, kSortTile);
     const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+    auto kern = radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(radix_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    radix_pass_kernel<true><<<(unsigned)ntiles, kSortThreads, smem, s>>>(
+    kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
         next_shift, next_mask);
   } else {
-    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement (best of the
-    // tile-size / window / occupancy sweep in tools/radix_ablate.cu)
-    constexpr int kItems = 32;
+    // P64 words: 4096-key tiles, 4 CTAs/SM, keys re-read from L2 for placement, peers from
+    // ballots (best of the sweep in tools/radix_ablate.cu on uniformly random digits:
+    // 1.35 ms per 2e8-word pass vs 2.03 ms with match.any)
+    constexpr int kItems = 16;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = radix_pass_kernel<false, kItems, 4, 2, true>;
+    auto kern = radix_pass_kernel<false, kItems, 4, 4, true, true>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -325,7 +325,7 @@ float run(const uint64_t *kin, uint64_t *kout, uint64_t n, uint32_t *hist, uint6
     cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
     cudaMemsetAsync(ctr, 0, 4);
     cudaEventRecord(a);
-    ablate_kernel<MODE><<<(unsigned)ntiles, kSortThreads, smem>>>(kin, kout, n, 8, 8, hist, status, ctr);
+    ablate_kernel<MODE><<<(unsigned)ntiles, kSortThreads, smem>>>(kin, kout, n, 40, 8, hist, status, ctr);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -347,9 +347,12 @@ int main(int argc, char **argv) {
   const uint64_t n = (argc > 1 ? strtoull(argv[1], 0, 10) : 200000000ull) / kSortTile * kSortTile;
   std::vector<uint64_t> h(n);
   uint64_t x = 88172645463325252ull;
+  const double hot = argc > 2 ? atof(argv[2]) : 0.0;  // fraction of keys equal to one hot key
   for (uint64_t i = 0; i < n; i++) {
     x ^= x << 13; x ^= x >> 7; x ^= x << 17;
-    h[i] = (x & ~0xffffffffull) | i;  // random high bits, index low bits
+    const bool is_hot = (double)(x >> 11) * 0x1.0p-53 < hot;
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    h[i] = ((is_hot ? 0x123456789abcull << 16 : x) & ~0xffffffffull) | i;  // high bits key, index low bits
   }
   uint64_t *kin, *kout, *status;
   uint32_t *hist, *ctr;
@@ -361,11 +364,14 @@ int main(int argc, char **argv) {
   cudaMemcpy(kin, h.data(), n * 8, cudaMemcpyHostToDevice);
   // exact digit offsets of bits [8,16) for the real pass
   std::vector<uint32_t> hh(kRadix, 0);
-  for (uint64_t i = 0; i < n; i++) hh[(h[i] >> 8) & 255]++;
+  for (uint64_t i = 0; i < n; i++) hh[(h[i] >> 40) & 255]++;
   std::vector<uint32_t> hx(hh);  // exclusive offsets for the ablation kernels, raw counts for the library pass
   uint32_t run_ = 0;
   for (int d = 0; d < kRadix; d++) { uint32_t c = hx[d]; hx[d] = run_; run_ += c; }
   cudaMemcpy(hist, hx.data(), kRadix * 4, cudaMemcpyHostToDevice);
+  uint32_t *histraw;
+  cudaMalloc(&histraw, kRadix * 4);
+  cudaMemcpy(histraw, hh.data(), kRadix * 4, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(ablate_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortTile * 8);
   report<0>("full pass", kin, kout, n, hist, status, ctr);
   report<1>("no look-back", kin, kout, n, hist, status, ctr);
@@ -389,7 +395,7 @@ int main(int argc, char **argv) {
         cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
         cudaMemsetAsync(ctr, 0, 4);
         cudaEventRecord(a);
-        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, nullptr, 16, 0);
+        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 40, 8, histraw, status, ctr, nullptr, 48, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -398,13 +404,14 @@ int main(int argc, char **argv) {
       }
       printf("%-34s %8.3f ms  %7.1f GB/s  %s\n", name, best, 16.0 * n / best / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
-    timeit(radix_pass_kernel<false, 16, 8, 3>, 16, "items16 win8 minb3 (prod)");
-    timeit(radix_pass_kernel<false, 32, 4, 2>, 32, "items32 win4 minb2");
-    timeit(radix_pass_kernel<false, 32, 4, 2, true>, 32, "items32 win4 minb2 reload");
-    timeit(radix_pass_kernel<false, 32, 4, 3, true>, 32, "items32 win4 minb3 reload");
-    timeit(radix_pass_kernel<false, 24, 4, 3, true>, 24, "items24 win4 minb3 reload");
-    timeit(radix_pass_kernel<false, 16, 4, 4, true>, 16, "items16 win4 minb4 reload");
-    timeit(radix_pass_kernel<false, 48, 4, 2, true>, 48, "items48 win4 minb2 reload");
+    timeit(radix_pass_kernel<false, 16, 4, 4, true, true>, 16, "items16 minb4 reload ballot");
+    timeit(radix_pass_kernel<false, 16, 4, 5, true, true>, 16, "items16 minb5 reload ballot");
+    timeit(radix_pass_kernel<false, 12, 4, 5, true, true>, 12, "items12 minb5 reload ballot");
+    timeit(radix_pass_kernel<false, 12, 4, 6, true, true>, 12, "items12 minb6 reload ballot");
+    timeit(radix_pass_kernel<false, 8, 4, 8, true, true>, 8, "items8 minb8 reload ballot");
+    timeit(radix_pass_kernel<false, 16, 8, 4, true, true>, 16, "items16 minb4 win8 reload ballot");
+    timeit(radix_pass_kernel<false, 16, 4, 4, false, true>, 16, "items16 minb4 noreload ballot");
+    timeit(radix_pass_kernel<false, 20, 4, 4, true, true>, 20, "items20 minb4 reload ballot");
   }
   // the library's real pass for comparison
   {
@@ -416,7 +423,7 @@ int main(int argc, char **argv) {
       cudaMemsetAsync(status, 0, (n / kSortTile) * kRadix * 8);
       cudaMemsetAsync(ctr, 0, 4);
       cudaEventRecord(a);
-      launch_radix_pass(kin, kout, nullptr, nullptr, n, 8, 8, hist, status, ctr, nullptr, 16, 8, 0);
+      launch_radix_pass(kin, kout, nullptr, nullptr, n, 40, 8, histraw, status, ctr, nullptr, 48, 8, 0);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
@@ -427,7 +434,7 @@ int main(int argc, char **argv) {
     std::vector<uint64_t> o(n);
     cudaMemcpy(o.data(), kout, n * 8, cudaMemcpyDeviceToHost);
     bool ok = true;
-    for (uint64_t i = 1; i < n && ok; i++) ok = ((o[i - 1] >> 8) & 255) <= ((o[i] >> 8) & 255);
+    for (uint64_t i = 1; i < n && ok; i++) ok = ((o[i - 1] >> 40) & 255) <= ((o[i] >> 40) & 255);
     printf("library pass digit order ok: %d  err=%s\n", (int)ok, cudaGetErrorString(cudaGetLastError()));
   }
   // plain copy reference
