@@ -379,13 +379,14 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
         next_shift, next_mask);
   } else {
-    // P64 words: 4096-key tiles, 4 CTAs/SM, keys re-read from L2 for placement, peers from
-    // ballots (best of the sweep in tools/radix_ablate.cu on uniformly random digits:
-    // 1.35 ms per 2e8-word pass vs 2.03 ms with match.any)
-    constexpr int kItems = 16;
+    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement, match.any peers.
+    // tools/radix_ablate.cu: on uniformly random digits ballot peers at 4096-key tiles are faster
+    // (1.35 vs 2.03 ms per 2e8 words), but on the benchmark workloads' concentrated digits this
+    // configuration wins (C4 pass 6.55 vs 6.86 ms, C5 1.44 vs 1.66 ms).
+    constexpr int kItems = 32;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = radix_pass_kernel<false, kItems, 4, 4, true, true>;
+    auto kern = radix_pass_kernel<false, kItems, 4, 2, true, false>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
