@@ -437,22 +437,17 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     // tools/radix_ablate.cu: on uniformly random digits ballot peers at 4096-key tiles are faster
     // (1.35 vs 2.03 ms per 2e8 words), but on the benchmark workloads' concentrated digits this
     // configuration wins (C4 pass 6.55 vs 6.86 ms, C5 1.44 vs 1.66 ms).
-    // The fused Map pass keeps its freshly built words in registers (4096-word tiles, 3 CTAs/SM):
-    // rebuilding them from the columns for placement serialized on L2 latency.
-    constexpr int kItems = 32, kItemsMap = 16;
-    const int items = first ? kItemsMap : kItems;
-    const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * items);
-    const size_t smem = (size_t)kSortThreads * items * sizeof(uint64_t);
-    auto kern = first ? radix_pass_kernel<false, kItemsMap, 4, 3, false, false, true>
+    constexpr int kItems = 32;
+    const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
+    const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
+    auto kern = first ? radix_pass_kernel<false, kItems, 4, 2, true, false, true>
                       : radix_pass_kernel<false, kItems, 4, 2, true, false, false>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(radix_pass_kernel<false, kItemsMap, 4, 3, false, false, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((size_t)kSortThreads * kItemsMap * sizeof(uint64_t)));
+      cudaFuncSetAttribute(radix_pass_kernel<false, kItems, 4, 2, true, false, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(radix_pass_kernel<false, kItems, 4, 2, true, false, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((size_t)kSortThreads * kItems * sizeof(uint64_t)));
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
