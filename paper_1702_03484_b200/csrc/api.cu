@@ -329,7 +329,7 @@ mapsq_status bounds_of(mapsq_ctx *ctx, mapsq_table *t, cudaStream_t s) {
 // buffers; returns in *which the buffer (0 = a, 1 = b) holding the result.
 mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *va, uint32_t *vb,
                         uint64_t n, uint32_t bit_lo, uint32_t nbits, uint32_t *hist, Scratch &sc,
-                        cudaStream_t s, int *which, const PackArgs *first = nullptr) {
+                        cudaStream_t s, int *which) {
   *which = 0;
   const uint32_t passes = (nbits + 7) / 8;
   if (passes == 0 || n == 0) return MAPSQ_OK;
@@ -339,29 +339,24 @@ mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *v
   NEED(status);
   NEED(counters);
   CK(cudaMemsetAsync(counters, 0, kMaxPasses * sizeof(uint32_t), s));
-  const bool kv = va != nullptr;
-  const uint64_t bytes = n * (kv ? 24ull : 16ull);
+  const uint64_t bytes = n * (va ? 24ull : 16ull);
   for (uint32_t p = 0; p < passes; p++) {
     const uint32_t shift = bit_lo + 8 * p;
     const uint32_t bits = std::min<uint32_t>(8, nbits - 8 * p);
     CK(cudaMemsetAsync(status, 0, ntiles * kRadix * sizeof(uint64_t), s));
-    // the fused first pass builds the words from the key columns and writes buffer a
-    const bool fused = first && p == 0;
-    uint64_t *kin = fused ? nullptr : ((*which == 0) ? ka : kb_);
-    uint64_t *kout = fused ? ka : ((*which == 0) ? kb_ : ka);
-    uint32_t *vin = (kv && !fused) ? ((*which == 0) ? va : vb) : nullptr;
-    uint32_t *vout = kv ? (fused ? va : ((*which == 0) ? vb : va)) : nullptr;
-    const uint64_t pbytes = fused ? n * (4ull * first->nkey + (kv ? 12ull : 8ull)) : bytes;
+    uint64_t *kin = (*which == 0) ? ka : kb_, *kout = (*which == 0) ? kb_ : ka;
+    uint32_t *vin = va ? ((*which == 0) ? va : vb) : nullptr;
+    uint32_t *vout = va ? ((*which == 0) ? vb : va) : nullptr;
     {
-      KTimer kt(ctx, s, fused ? (kv ? "radix_pass_kv_map" : "radix_pass_map") : (kv ? "radix_pass_kv" : "radix_pass"), pbytes);
+      KTimer kt(ctx, s, va ? "radix_pass_kv" : "radix_pass", bytes);
       const bool more = p + 1 < passes;
       const uint32_t nbits_next = more ? std::min<uint32_t>(8, nbits - 8 * (p + 1)) : 0;
       launch_radix_pass(kin, kout, vin, vout, n, shift, bits, hist + p * kRadix, status,
                         counters + p, more ? hist + (p + 1) * kRadix : nullptr, shift + 8,
-                        nbits_next, fused ? first : nullptr, s);
+                        nbits_next, s);
       CKL("radix_pass");
     }
-    if (!fused) *which ^= 1;
+    *which ^= 1;
   }
   return MAPSQ_OK;
 }
@@ -454,21 +449,17 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     NEED(va);
     NEED(vb);
   }
-  // ---- Map (row a3), fused into the first digit pass: this kernel only counts the first digit
-  // (it writes the words itself only when there is no digit pass at all, kb == 0)
+  // ---- Map (row a3) + upfront histograms
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
-  const PackArgs pa = pack_args(pl, &a, &b);
-  const bool fuse_map = pl.passes > 0;
   {
-    KTimer kt(ctx, s, fuse_map ? "map_hist" : "pack_hist",
-              4ull * pa.nkey * n + (fuse_map ? 0ull : (kv ? 12ull : 8ull) * n));
-    launch_pack_hist(pa, fuse_map ? nullptr : wa, fuse_map ? nullptr : va, hist, s);
+    const PackArgs pa = pack_args(pl, &a, &b);
+    KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
+    launch_pack_hist(pa, wa, va, hist, s);
     CKL("pack_hist");
   }
   // ---- Sort (row a4)
   int which = 0;
-  TRY(radix_sort(ctx, wa, wb, va, vb, n, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which,
-                 fuse_map ? &pa : nullptr));
+  TRY(radix_sort(ctx, wa, wb, va, vb, n, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
   uint64_t *words = which ? wb : wa;
   uint32_t *vals = kv ? (which ? vb : va) : nullptr;
   sc.release(which ? wa : wb);

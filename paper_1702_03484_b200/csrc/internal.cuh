@@ -267,7 +267,7 @@ struct PackArgs {
   uint32_t last_mask;  // digit mask of the last pass ((1 << bits) - 1)
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
 };
-// Map (K2): pack words (or KV pairs; skipped when words == NULL) and count the first digit.
+// Map (K2): pack words (or KV pairs) and build the digit histograms of every pass.
 void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32_t *hist,
                       cudaStream_t s);
 // Histograms of existing keys (for mapsq_sort_words on caller data).
@@ -276,12 +276,10 @@ void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t
 // One onesweep digit pass (K3).
 // hist_pass: this pass's RAW digit counts (the kernel scans them); hist_next (may be NULL):
 // zeroed counts the pass fills with the next digit (bits [next_shift, next_shift + next_bits)).
-// first != NULL: the fused Map pass — words are built from first's key columns (kin unused).
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
-                       uint32_t next_shift, uint32_t next_bits, const PackArgs *first,
-                       cudaStream_t s);
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s);
 
 // ReduceDuplicate (K4): groups present on both sides, in key order.
 struct GroupOut {

@@ -12,8 +12,6 @@
 // ranked in shared memory with warp match-any multisplit, and their global digit offsets are
 // resolved by decoupled look-back over per-(tile, digit) status words; all P passes' global
 // digit offsets come from ONE upfront histogram fused into the Map kernel.
-#include <cstring>
-
 #include "internal.cuh"
 
 namespace mapsq {
@@ -63,13 +61,11 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
       if (i >= n) continue;
       uint64_t kk = key[it];
       if (KV) {
-        if (words) {
-          __stcs(words + i, kk);
-          __stcs(vals + i, (uint32_t)i);
-        }
+        __stcs(words + i, kk);
+        __stcs(vals + i, (uint32_t)i);
       } else {
         kk = (kk << a.ib) | i;
-        if (words) __stcs(words + i, kk);
+        __stcs(words + i, kk);
       }
       for (uint32_t p = 0; p < a.passes; p++) {
         const uint32_t d = (uint32_t)(kk >> (a.bit_lo + 8 * p)) & (p + 1 == a.passes ? a.last_mask : 0xffu);
@@ -133,42 +129,14 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
 // slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
 // full tiles skip every bounds check (the first version spent most of its issue slots on 64-bit
 // index arithmetic).
-// FIRST pass (Map fused): the words are built from the join's key columns here
-// instead of being read — key' = concatenation of (value - lo) of the packed key columns, word =
-// key' << ib | rowid (P64) or (key', rowid) (KV), rowid >= n1 meaning RIGHT.  Columns outermost,
-// items innermost, so all of a column's loads of a thread are in flight together.
-template <bool KV, int N>
-__device__ __forceinline__ void map_rows(const PackArgs &pk, uint64_t i0, uint32_t stride,
-                                         uint64_t n, uint64_t (&k)[N]) {
-#pragma unroll
-  for (int it = 0; it < N; it++) k[it] = 0;
-  for (uint32_t c = 0; c < pk.nkey; c++) {
-    const uint32_t *k1 = pk.key1[c], *k2 = pk.key2[c] - pk.n1;
-    const uint32_t lo = pk.lo[c], sh = pk.shift[c];
-    uint32_t v[N];
-#pragma unroll
-    for (int it = 0; it < N; it++) {
-      const uint64_t i = i0 + (uint64_t)it * stride;
-      v[it] = i < n ? __ldcg((i < pk.n1 ? k1 : k2) + i) : lo;
-    }
-#pragma unroll
-    for (int it = 0; it < N; it++) k[it] |= (uint64_t)(v[it] - lo) << sh;
-  }
-  if (!KV) {
-#pragma unroll
-    for (int it = 0; it < N; it++) k[it] = (k[it] << pk.ib) | (i0 + (uint64_t)it * stride);
-  }
-}
-
 template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false,
-          bool BALLOT = false, bool FIRST = false>
+          bool BALLOT = false>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
                   uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
                   uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter,
-                  uint32_t *__restrict__ hist_next, uint32_t next_shift, uint32_t next_mask,
-                  const PackArgs pk) {
+                  uint32_t *__restrict__ hist_next, uint32_t next_shift, uint32_t next_mask) {
   constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
@@ -198,13 +166,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   uint32_t v[KV ? ITEMS : 1];
   uint32_t r[ITEMS];
   const bool full = tile_n == (uint32_t)TILE;
-  if (FIRST) {
-    map_rows<KV, ITEMS>(pk, tile_base + wslice + lane, 32, n, k);
-    if (KV) {
-#pragma unroll
-      for (int it = 0; it < ITEMS; it++) v[KV ? it : 0] = (uint32_t)(tile_base + wslice + lane + it * 32);
-    }
-  } else if (full) {
+  if (full) {
 #pragma unroll
     for (int it = 0; it < ITEMS; it++) k[it] = RELOAD ? __ldcg(src + it * 32) : __ldcs(src + it * 32);
     if (KV) {
@@ -345,16 +307,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     if (wslice + it * 32 + lane < tile_n) {
       // RELOAD: the key is read again (an L2 hit) instead of being held in registers across the
       // look-back, which lets more CTAs share an SM
-      uint64_t key = k[it];
-      if (RELOAD) {
-        if (FIRST) {
-          uint64_t kk[1];
-          map_rows<KV, 1>(pk, tile_base + wslice + lane + it * 32, 32, n, kk);
-          key = kk[0];
-        } else {
-          key = __ldcs(src + it * 32);
-        }
-      }
+      const uint64_t key = RELOAD ? __ldcs(src + it * 32) : k[it];
       const uint32_t dd = (uint32_t)(key >> shift) & dmask;
       const uint32_t slot = s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
       s_keys[slot] = key;
@@ -410,28 +363,21 @@ void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s) {
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
-                       uint32_t next_shift, uint32_t next_bits, const PackArgs *first,
-                       cudaStream_t s) {
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s) {
   const uint32_t next_mask = (1u << next_bits) - 1u;
-  PackArgs pk;
-  if (first) pk = *first; else std::memset(&pk, 0, sizeof pk);
-  if (vout) {
-    // (key, rowid) pairs: 4096-key tiles (the payload needs the registers), ballot peers
+  if (vin) {
+    // (key, rowid) pairs: 4096-key tiles (the payload needs the registers)
     const uint64_t ntiles = ceil_div(n, kSortTile);
     const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
-    auto kern = first ? radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true, true>
-                      : radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true, false>;
+    auto kern = radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
-                                                      hist_pass, status, tile_counter, hist_next,
-                                                      next_shift, next_mask, pk);
+    kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(
+        kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
+        next_shift, next_mask);
   } else {
     // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement, match.any peers.
     // tools/radix_ablate.cu: on uniformly random digits ballot peers at 4096-key tiles are faster
@@ -440,19 +386,15 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     constexpr int kItems = 32;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = first ? radix_pass_kernel<false, kItems, 4, 2, true, false, true>
-                      : radix_pass_kernel<false, kItems, 4, 2, true, false, false>;
+    auto kern = radix_pass_kernel<false, kItems, 4, 2, true, false>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(radix_pass_kernel<false, kItems, 4, 2, true, false, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(radix_pass_kernel<false, kItems, 4, 2, true, false, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,
-                                                      next_shift, next_mask, pk);
+                                                      next_shift, next_mask);
   }
 }
 
