@@ -242,29 +242,35 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    ctx.stats_reset()
-    ctx.set_profiling(True)
-    evs = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            if flush is not None:
-                flush.fill_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            m_final = step()
-            e1.record(stream)
-            evs.append((e0, e1))
-        torch.cuda.synchronize()
-    ctx.set_profiling(False)
-    st_k = ctx.stats()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
+
+    def timed(profile: bool):
+        ctx.stats_reset()
+        ctx.set_profiling(profile)
+        evs = []
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                if flush is not None:
+                    flush.fill_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                m = step()
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+        ctx.set_profiling(False)
+        return [a.elapsed_time(b) for a, b in evs], ctx.stats(), clk.summary(), m
+
+    # region 1 (the reported value): no per-kernel events; region 2: per-kernel CUDA events on
+    # the library's stream for the roofline and the kernel shares
+    step_ms, st_plain, clocks, m_final = timed(False)
+    prof_ms, st_k, _, _ = timed(True)
     total_s = sum(step_ms) / 1e3
-    tuples = st_k["join_in_rows"] + st_k["join_out_rows"]
+    tuples = st_plain["join_in_rows"] + st_plain["join_out_rows"]
     value = tuples / total_s
     algo_bytes = sum(k["bytes"] for k in st_k["kernels"].values())
     peak, peak_src = measured_peaks()
     hbm_gbs = algo_bytes / total_s / 1e9
-    # dominant kernel by time
+    # dominant kernel by time (profiled region)
     name, kd = max(st_k["kernels"].items(), key=lambda kv: kv[1]["ms"])
     avg_ms = kd["ms"] / kd["launches"]
     achieved = (kd["bytes"] / kd["launches"]) / (avg_ms / 1e3) / 1e9
@@ -272,7 +278,6 @@ def run_gpu(args):
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg}.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(name)
-    clocks = clk.summary()
 
     line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup,
@@ -286,10 +291,11 @@ def run_gpu(args):
                     "frac_of_peak": hbm_gbs / peak, "peak_gbs": peak},
             "roofline": {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "share_of_step": kd["ms"] / sum(step_ms)},
+                         "traffic": traffic, "share_of_step": kd["ms"] / sum(prof_ms),
+                         "timing": "per-kernel CUDA events on the library stream, second timed region"},
             "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
-                            "share": v["ms"] / sum(step_ms)} for k, v in st_k["kernels"].items()},
-            "clocks": clocks, "gpu_launches": st_k["launches"]}
+                            "share": v["ms"] / sum(prof_ms)} for k, v in st_k["kernels"].items()},
+            "clocks": clocks, "gpu_launches": st_plain["launches"]}
 
     # e2e through the public API from pinned host buffers (H2D + query + D2H inside the region)
     if host is not None and not args.no_e2e:

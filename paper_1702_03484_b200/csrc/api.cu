@@ -485,7 +485,9 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   const bool residual = pl.path == MAPSQ_PATH_RESIDUAL;
   ResidualArgs ra;
   std::memset(&ra, 0, sizeof ra);
+  uint64_t *pmask = residual ? sc.get<uint64_t>(cap) : nullptr;
   if (residual) {
+    NEED(pmask);
     ra.words = words;
     ra.n1 = n1;
     ra.ib = pl.ib;
@@ -500,7 +502,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
         ra.nres++;
       }
     KTimer kt(ctx, s, "residual_count", 8ull * n);
-    launch_residual_count(ra, cap, gc, s);  // exact pair counts replace nL * nR
+    launch_residual_count(ra, cap, gc, pmask, s);  // exact pair counts replace nL * nR
     CKL("residual_count");
   }
   {
@@ -533,7 +535,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       for (uint32_t c = 0; c < k; c++) ra.out[c] = rs->col[c];
       ra.goff = go;
       KTimer kt(ctx, s, "residual_expand", 4ull * m * pl.out_ncols);
-      launch_residual_expand(ra, ngroups, s);
+      launch_residual_expand(ra, ngroups, pmask, s);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         dfree(ctx, rs->owner, s);

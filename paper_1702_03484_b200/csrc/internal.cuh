@@ -327,8 +327,10 @@ struct ResidualArgs {
   uint32_t *out[MAPSQ_MAX_COLS];
   const uint64_t *goff;  // exclusive offsets of the exact pair counts
 };
-void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, cudaStream_t s);
-void launch_residual_expand(const ResidualArgs &a, uint64_t cap, cudaStream_t s);
+void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, uint64_t *pmask,
+                           cudaStream_t s);
+void launch_residual_expand(const ResidualArgs &a, uint64_t cap, const uint64_t *pmask,
+                            cudaStream_t s);
 uint64_t find_groups_tiles(uint64_t n);
 
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,

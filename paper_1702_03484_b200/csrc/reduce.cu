@@ -407,33 +407,56 @@ __device__ __forceinline__ bool residual_equal(const ResidualArgs &a, uint32_t l
   return true;
 }
 
+// Groups with nL * nR <= 64 also record which pairs matched (bit l * nR + r of a 64-bit mask),
+// so the expansion touches only matched pairs and never re-reads the residual columns.
 __global__ void __launch_bounds__(256)
-residual_count_kernel(const ResidualArgs a, uint64_t *__restrict__ cnt) {
+residual_count_kernel(const ResidualArgs a, uint64_t *__restrict__ cnt,
+                      uint64_t *__restrict__ pmask) {
   const uint64_t ng = *a.ngroups_dev;
   const uint64_t mask = (1ull << a.ib) - 1;
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
-    uint64_t c = 0;
+    const bool small = (uint64_t)(sp - st) * (en - sp) <= 64;
+    uint64_t c = 0, bits = 0;
+    uint32_t q = 0;
     for (uint32_t l = st; l < sp; l++) {
       const uint32_t li = (uint32_t)(a.words[l] & mask);
-      for (uint32_t r = sp; r < en; r++) {
+      for (uint32_t r = sp; r < en; r++, q++) {
         const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
-        c += residual_equal(a, li, ri);
+        const bool eq = residual_equal(a, li, ri);
+        c += eq;
+        if (small && eq) bits |= 1ull << q;
       }
     }
     cnt[g] = c;
+    pmask[g] = bits;
   }
 }
 
 __global__ void __launch_bounds__(256)
-residual_expand_kernel(const ResidualArgs a) {
+residual_expand_kernel(const ResidualArgs a, const uint64_t *__restrict__ pmask) {
   const uint64_t ng = *a.ngroups_dev;
   const uint64_t mask = (1ull << a.ib) - 1;
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
+    const uint32_t nR = en - sp;
     uint64_t pos = a.goff[g];
+    if ((uint64_t)(sp - st) * nR <= 64) {
+      uint64_t bits = pmask[g];
+      while (bits) {  // matched pairs only, in (l, r) order
+        const uint32_t q = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        const uint32_t l = st + q / nR, r = sp + q % nR;
+        const uint32_t li = (uint32_t)(a.words[l] & mask);
+        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
+        for (uint32_t c = 0; c < a.nout; c++)
+          a.out[c][pos] = __ldg(a.src[c] + (a.src_side[c] ? ri : li));
+        pos++;
+      }
+      continue;
+    }
     for (uint32_t l = st; l < sp; l++) {
       const uint32_t li = (uint32_t)(a.words[l] & mask);
       for (uint32_t r = sp; r < en; r++) {
@@ -474,12 +497,14 @@ static unsigned residual_grid(uint64_t cap) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(cap, 256), 148 * 16));
 }
 
-void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, cudaStream_t s) {
-  residual_count_kernel<<<residual_grid(cap), 256, 0, s>>>(a, cnt);
+void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, uint64_t *pmask,
+                           cudaStream_t s) {
+  residual_count_kernel<<<residual_grid(cap), 256, 0, s>>>(a, cnt, pmask);
 }
 
-void launch_residual_expand(const ResidualArgs &a, uint64_t cap, cudaStream_t s) {
-  residual_expand_kernel<<<residual_grid(cap), 256, 0, s>>>(a);
+void launch_residual_expand(const ResidualArgs &a, uint64_t cap, const uint64_t *pmask,
+                            cudaStream_t s) {
+  residual_expand_kernel<<<residual_grid(cap), 256, 0, s>>>(a, pmask);
 }
 
 void launch_expand(const ExpandArgs &a, cudaStream_t s) {
