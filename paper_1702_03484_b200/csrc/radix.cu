@@ -153,12 +153,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
 #pragma unroll
   for (int q = 0; q < kWarps; q++) s_warp_hist[q][tid] = 0;  // kSortThreads == kRadix
   s_next[tid] = 0;
-  // Ranking strategy from this pass's global digit histogram: when most of the 256 digits are
-  // well populated (spread digits), peers come from ballots (short latency, fixed cost); when few
-  // digits dominate, match.any is cheaper (tools/radix_ablate.cu, profiles/README.md).
-  const uint32_t hcount = __ldg(hist_pass + tid);
-  const int spread = __syncthreads_count(hcount >= (uint32_t)(n >> 10) && hcount > 0);
-  const bool use_ballot = BALLOT || spread >= 192;
+  __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t tile_base = tile * TILE;
   const uint64_t rem = n - tile_base;
@@ -199,7 +194,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
       const int it = b0 + u;
       const bool in = full || wslice + it * 32 + lane < tile_n;
       const uint32_t dg = (uint32_t)(k[it] >> shift) & dmask;
-      if (use_ballot) {  // peers from one ballot per digit bit (short-latency votes)
+      if (BALLOT) {  // peers from one ballot per digit bit (short-latency votes)
         uint32_t pm = __ballot_sync(0xffffffffu, in);
         pm = in ? pm : ~pm;
 #pragma unroll
@@ -288,7 +283,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   const uint32_t dstart = pre + x - total;
   s_digit_start[d] = dstart;
   // exclusive scan of this pass's global digit counts (each CTA scans the 256 totals itself)
-  const uint32_t hc = hcount;
+  const uint32_t hc = __ldg(hist_pass + d);
   uint32_t hx = hc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
