@@ -223,14 +223,39 @@ mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words, uint64_t
                                  uint32_t *group_end, uint64_t *group_off, uint64_t *ngroups,
                                  uint64_t *total, void *stream);
 
-/* ---- multi-GPU exchange support (SURVEY §8 row e) ----
- * Hash-partition `in` on the variables key_vars[0..nkey) into nparts destinations,
- * dest = fmix32(h) mod nparts with h the FNV-1a-style fold of the key values.
- * `out` receives a table with the same schema whose rows are grouped by destination (stable
- * within a destination); counts_host[d] receives destination d's row count (blocking). */
+/* ---- multi-GPU exchange (SURVEY §8 row e) ----
+ * Hash partition on the join key, fused with the all-to-all: every rank sends each row to rank
+ * dest = fmix32(h) mod nparts, h the FNV-1a-style fold (h = (h ^ v) * 16777619 from 2166136261)
+ * of the row's values of key_vars[0..nkey) in that order.
+ *
+ * mapsq_partition_plan: per-tile destination histogram + scan; counts_host[d] receives the number
+ * of rows for destination d (blocking read).  *state keeps the plan for the scatter (free it with
+ * mapsq_partition_state_free; `in` must stay valid until then).
+ * mapsq_partition_scatter: ONE kernel writes every row straight into its destination: column c of
+ * destination d starts at dest_cols[d * ncols + c] — a local device pointer or a peer rank's
+ * arena opened with mapsq_ipc_open (NVLink stores) — and this rank's rows for d occupy rows
+ * [dest_row[d], dest_row[d] + counts[d]) of it, stable within the destination.  Returns when
+ * the kernel has completed (the caller then synchronises the ranks before reading). */
+typedef struct mapsq_partition_state mapsq_partition_state;
+mapsq_status mapsq_partition_plan(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
+                                  int nkey, int nparts, uint64_t *counts_host,
+                                  mapsq_partition_state **state, void *stream);
+mapsq_status mapsq_partition_scatter(mapsq_ctx *ctx, mapsq_partition_state *state,
+                                     const uint64_t *dest_row, uint32_t *const *dest_cols,
+                                     void *stream);
+void mapsq_partition_state_free(mapsq_ctx *ctx, mapsq_partition_state *state);
+/* Local convenience: `out` receives a table with the same schema whose rows are grouped by
+ * destination (destination-major, stable within a destination); counts_host[d] as above. */
 mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
                              int nkey, int nparts, mapsq_table *out, uint64_t *counts_host,
                              void *stream);
+/* CUDA IPC of a device allocation (64-byte handle) so peer ranks can store into it.  Export only
+ * pointers returned by mapsq_ipc_alloc (a whole cudaMalloc allocation: the handle maps its base). */
+mapsq_status mapsq_ipc_alloc(mapsq_ctx *ctx, size_t bytes, void **dev_ptr);
+mapsq_status mapsq_ipc_free(mapsq_ctx *ctx, void *dev_ptr);
+mapsq_status mapsq_ipc_export(mapsq_ctx *ctx, void *dev_ptr, void *handle64);
+mapsq_status mapsq_ipc_open(mapsq_ctx *ctx, const void *handle64, void **dev_ptr);
+mapsq_status mapsq_ipc_close(mapsq_ctx *ctx, void *dev_ptr);
 /* Compute exact inclusive bounds lo[]/hi[] of every column of a (caller-built) table and set
  * MAPSQ_TABLE_BOUNDS (one min/max pass, blocking).  An empty table gets lo = hi = 0. */
 mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);

@@ -113,6 +113,15 @@ def lib():
             "mapsq_partition": (st, [vp, PT, ctypes.POINTER(i32), ctypes.c_int, ctypes.c_int, PT,
                                      ctypes.POINTER(u64), vp]),
             "mapsq_table_bounds": (st, [vp, PT, vp]),
+            "mapsq_partition_plan": (st, [vp, PT, ctypes.POINTER(i32), ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(u64), ctypes.POINTER(vp), vp]),
+            "mapsq_partition_scatter": (st, [vp, vp, ctypes.POINTER(u64), ctypes.POINTER(vp), vp]),
+            "mapsq_partition_state_free": (None, [vp, vp]),
+            "mapsq_ipc_alloc": (st, [vp, ctypes.c_size_t, ctypes.POINTER(vp)]),
+            "mapsq_ipc_free": (st, [vp, vp]),
+            "mapsq_ipc_export": (st, [vp, vp, ctypes.c_char_p]),
+            "mapsq_ipc_open": (st, [vp, ctypes.c_char_p, ctypes.POINTER(vp)]),
+            "mapsq_ipc_close": (st, [vp, vp]),
             "mapsq_set_profiling": (st, [vp, ctypes.c_int]),
             "mapsq_set_option": (st, [vp, ctypes.c_int, ctypes.c_int64]),
             "mapsq_stats_reset": (st, [vp]),
@@ -391,6 +400,46 @@ class Context:
                                           nparts, ctypes.byref(out), counts, _stream(stream)))
         return _wrap(self, out), [int(c) for c in counts]
 
+    def partition_plan(self, table: DeviceTable, key_vars, nparts: int, stream=None):
+        """K8 plan: per-destination row counts + an opaque state for partition_scatter."""
+        kv = (ctypes.c_int32 * len(key_vars))(*key_vars)
+        counts = (ctypes.c_uint64 * nparts)()
+        st = ctypes.c_void_p()
+        self._check(lib().mapsq_partition_plan(self.handle, ctypes.byref(table._c), kv, len(key_vars),
+                                               nparts, counts, ctypes.byref(st), _stream(stream)))
+        return st, [int(c) for c in counts]
+
+    def partition_scatter(self, state, dest_row, dest_cols, stream=None):
+        """The fused partition + exchange kernel: rows go straight to dest_cols (device or peer
+        pointers, destination-major: dest_cols[d * ncols + c]) at dest_row[d] onwards."""
+        rows = (ctypes.c_uint64 * len(dest_row))(*dest_row)
+        cols = (ctypes.c_void_p * len(dest_cols))(*dest_cols)
+        try:
+            self._check(lib().mapsq_partition_scatter(self.handle, state, rows, cols, _stream(stream)))
+        finally:
+            lib().mapsq_partition_state_free(self.handle, state)
+
+    def ipc_alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        self._check(lib().mapsq_ipc_alloc(self.handle, nbytes, ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_free(self, ptr: int):
+        self._check(lib().mapsq_ipc_free(self.handle, ctypes.c_void_p(ptr)))
+
+    def ipc_export(self, ptr: int) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        self._check(lib().mapsq_ipc_export(self.handle, ctypes.c_void_p(ptr), buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        self._check(lib().mapsq_ipc_open(self.handle, handle, ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, ptr: int):
+        self._check(lib().mapsq_ipc_close(self.handle, ctypes.c_void_p(ptr)))
+
     def table_bounds(self, table: DeviceTable, stream=None):
         self._check(lib().mapsq_table_bounds(self.handle, ctypes.byref(table._c), _stream(stream)))
         return table.bounds
@@ -414,6 +463,15 @@ class Context:
                                                          bytes=int(st.kernel[i].algo_bytes))
                         for i in range(st.nkernels)}
         return d
+
+
+def device_columns(ptr: int, nrows: int, ncols: int, stride: int, owner=None):
+    """Zero-copy uint32 torch views of `ncols` columns of `nrows` at ptr + c * stride * 4."""
+    import torch
+    if nrows == 0:
+        return [torch.empty(0, dtype=torch.uint32, device="cuda") for _ in range(ncols)]
+    return [torch.as_tensor(_CAI(ptr + c * stride * 4, nrows, owner), device="cuda")
+            for c in range(ncols)]
 
 
 def plan_join(vars1, bounds1, n1, vars2, bounds2, n2) -> JoinPlan:

@@ -1059,66 +1059,194 @@ MAPSQ_API mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words
   return MAPSQ_OK;
 }
 
-MAPSQ_API mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in,
-                                       const int32_t *key_vars, int nkey, int nparts,
-                                       mapsq_table *out, uint64_t *counts_host, void *stream) {
+// ------------------------------------------------------------------ partition (row e, K8)
+struct mapsq_partition_state {
+  PartArgs pa;
+  uint64_t ntiles;
+  uint64_t *tile_off;   // dest-major exclusive offsets of the per-tile counts (+ total)
+  uint64_t *tables;     // device: dst_row[nparts] then dst_cols[nparts * ncols]
+  uint64_t counts[kMaxParts];
+};
+
+MAPSQ_API void mapsq_partition_state_free(mapsq_ctx *ctx, mapsq_partition_state *st) {
+  if (!ctx || !st) return;
+  cudaStream_t s = nullptr;
+  if (st->tile_off) dfree(ctx, st->tile_off, s);
+  if (st->tables) dfree(ctx, st->tables, s);
+  delete st;
+}
+
+MAPSQ_API mapsq_status mapsq_partition_plan(mapsq_ctx *ctx, const mapsq_table *in,
+                                            const int32_t *key_vars, int nkey, int nparts,
+                                            uint64_t *counts_host, mapsq_partition_state **state,
+                                            void *stream) {
   TRY(enter(ctx));
-  if (!out || !counts_host || !key_vars) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
-  clear_table(out);
+  if (!state || !counts_host || !key_vars) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  *state = nullptr;
   TRY(check_table(ctx, in, "in"));
   if (nparts < 1 || nparts > kMaxParts || nkey < 1 || nkey > (int)in->ncols)
     return set_error(ctx, MAPSQ_E_INVALID, "bad partition arguments");
   cudaStream_t s = S(stream);
-  PartArgs pa;
+  auto *st = new (std::nothrow) mapsq_partition_state();
+  if (!st) return set_error(ctx, MAPSQ_E_NOMEM, "host allocation failed");
+  PartArgs &pa = st->pa;
   std::memset(&pa, 0, sizeof pa);
   pa.nkey = (uint32_t)nkey;
   for (int q = 0; q < nkey; q++) {
     int c = -1;
     for (uint32_t j = 0; j < in->ncols; j++)
       if (in->var[j] == key_vars[q]) c = (int)j;
-    if (c < 0) return set_error(ctx, MAPSQ_E_INVALID, "partition key variable not in table");
+    if (c < 0) {
+      delete st;
+      return set_error(ctx, MAPSQ_E_INVALID, "partition key variable not in table");
+    }
     pa.key[q] = in->col[c];
   }
   pa.ncols = in->ncols;
   pa.n = in->nrows;
   pa.nparts = (uint32_t)nparts;
   for (uint32_t c = 0; c < in->ncols; c++) pa.in[c] = in->col[c];
-  *out = *in;
-  out->owner = nullptr;
-  TRY(alloc_table(ctx, out, in->nrows, in->ncols, s));
-  for (int d = 0; d < nparts; d++) counts_host[d] = 0;
-  if (in->nrows == 0) return MAPSQ_OK;
-  for (uint32_t c = 0; c < in->ncols; c++) pa.out[c] = out->col[c];
-  Scratch sc(ctx, s);
-  const uint64_t ntiles = ceil_div(in->nrows, kPartTile);
-  uint32_t *th = sc.get<uint32_t>(ntiles * nparts);
-  uint64_t *to = sc.get<uint64_t>(ntiles * nparts + 1);
-  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(ntiles * nparts));
-  if (!th || !to || !tmp) {
-    dfree(ctx, out->owner, s);
-    clear_table(out);
+  for (int d = 0; d < nparts; d++) counts_host[d] = st->counts[d] = 0;
+  if (in->nrows == 0) {
+    *state = st;
+    return MAPSQ_OK;
+  }
+  st->ntiles = ceil_div(in->nrows, kPartTile);
+  st->tile_off = static_cast<uint64_t *>(dalloc(ctx, (st->ntiles * nparts + 1) * 8, s));
+  st->tables = static_cast<uint64_t *>(dalloc(ctx, (size_t)nparts * (1 + in->ncols) * 8, s));
+  if (!st->tile_off || !st->tables) {
+    mapsq_partition_state_free(ctx, st);
     return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed");
   }
+  Scratch sc(ctx, s);
+  uint32_t *th = sc.get<uint32_t>(st->ntiles * nparts);
+  uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(st->ntiles * nparts));
+  if (!th || !tmp) {
+    mapsq_partition_state_free(ctx, st);
+    return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed");
+  }
+  mapsq_status rc = MAPSQ_OK;
   {
     KTimer kt(ctx, s, "partition_hist", 4ull * nkey * in->nrows);
-    launch_partition_hist(pa, th, ntiles, s);
-    CKL("partition_hist");
+    launch_partition_hist(pa, th, st->ntiles, s);
   }
   {
-    KTimer kt(ctx, s, "scan_tiles", 12ull * ntiles * nparts, 3);
-    launch_exclusive_scan_u32(th, to, ntiles * nparts, tmp, to + ntiles * nparts, s);
-    CKL("scan_tiles");
+    KTimer kt(ctx, s, "scan_tiles", 12ull * st->ntiles * nparts, 3);
+    launch_exclusive_scan_u32(th, st->tile_off, st->ntiles * nparts, tmp,
+                              st->tile_off + st->ntiles * nparts, s);
   }
+  rc = cuda_check(ctx, cudaGetLastError(), "partition_plan");
+  if (rc == MAPSQ_OK) rc = ensure_pinned(ctx, nparts + 1);
+  for (int d = 0; d <= nparts && rc == MAPSQ_OK; d++)
+    rc = cuda_check(ctx, cudaMemcpyAsync(ctx->pinned + d, st->tile_off + (uint64_t)d * st->ntiles, 8,
+                                         cudaMemcpyDeviceToHost, s), "counts D2H");
+  if (rc == MAPSQ_OK) rc = cuda_check(ctx, cudaStreamSynchronize(s), "counts sync");
+  if (rc != MAPSQ_OK) {
+    mapsq_partition_state_free(ctx, st);
+    return rc;
+  }
+  for (int d = 0; d < nparts; d++) counts_host[d] = st->counts[d] = ctx->pinned[d + 1] - ctx->pinned[d];
+  *state = st;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_partition_scatter(mapsq_ctx *ctx, mapsq_partition_state *st,
+                                               const uint64_t *dest_row,
+                                               uint32_t *const *dest_cols, void *stream) {
+  TRY(enter(ctx));
+  if (!st || !dest_row || !dest_cols) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  if (st->pa.n == 0) return MAPSQ_OK;
+  cudaStream_t s = S(stream);
+  const uint32_t np = st->pa.nparts, nc = st->pa.ncols;
+  TRY(ensure_pinned(ctx, (size_t)np * (1 + nc)));
+  for (uint32_t d = 0; d < np; d++) {
+    ctx->pinned[d] = dest_row[d];
+    for (uint32_t c = 0; c < nc; c++) {
+      const uint32_t *p = dest_cols[d * nc + c];
+      if (!p && st->counts[d]) return set_error(ctx, MAPSQ_E_INVALID, "NULL destination column");
+      ctx->pinned[np + d * nc + c] = (uint64_t)(uintptr_t)p;
+    }
+  }
+  CK(cudaMemcpyAsync(st->tables, ctx->pinned, (size_t)np * (1 + nc) * 8, cudaMemcpyHostToDevice, s));
   {
-    KTimer kt(ctx, s, "partition_scatter", 8ull * in->ncols * in->nrows);
-    launch_partition_scatter(pa, to, ntiles, s);
+    KTimer kt(ctx, s, "partition_scatter", 8ull * nc * st->pa.n);
+    launch_partition_scatter(st->pa, st->tile_off, st->ntiles, st->tables, st->tables + np, s);
     CKL("partition_scatter");
   }
-  TRY(ensure_pinned(ctx, nparts + 1));
-  for (int d = 0; d <= nparts; d++)
-    CK(cudaMemcpyAsync(ctx->pinned + d, to + (uint64_t)d * ntiles, 8, cudaMemcpyDeviceToHost, s));
+  // the pinned staging buffer is reused by the next call: make sure the copy has been consumed
   CK(cudaStreamSynchronize(s));
-  for (int d = 0; d < nparts; d++) counts_host[d] = ctx->pinned[d + 1] - ctx->pinned[d];
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_partition(mapsq_ctx *ctx, const mapsq_table *in,
+                                       const int32_t *key_vars, int nkey, int nparts,
+                                       mapsq_table *out, uint64_t *counts_host, void *stream) {
+  TRY(enter(ctx));
+  if (!out || !counts_host) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  clear_table(out);
+  mapsq_partition_state *st = nullptr;
+  TRY(mapsq_partition_plan(ctx, in, key_vars, nkey, nparts, counts_host, &st, stream));
+  cudaStream_t s = S(stream);
+  *out = *in;
+  out->owner = nullptr;
+  mapsq_status rc = alloc_table(ctx, out, in->nrows, in->ncols, s);
+  if (rc == MAPSQ_OK && in->nrows) {
+    // local destination: every destination's block lives in `out`, destination-major
+    uint64_t rows[kMaxParts];
+    uint32_t *cols[kMaxParts * MAPSQ_MAX_COLS];
+    uint64_t run = 0;
+    for (int d = 0; d < nparts; d++) {
+      rows[d] = run;
+      run += counts_host[d];
+      for (uint32_t c = 0; c < in->ncols; c++) cols[d * in->ncols + c] = out->col[c];
+    }
+    rc = mapsq_partition_scatter(ctx, st, rows, cols, stream);
+  }
+  mapsq_partition_state_free(ctx, st);
+  if (rc != MAPSQ_OK) {
+    dfree(ctx, out->owner, s);
+    clear_table(out);
+  }
+  return rc;
+}
+
+// ------------------------------------------------------------------ CUDA IPC (peer arenas)
+MAPSQ_API mapsq_status mapsq_ipc_alloc(mapsq_ctx *ctx, size_t bytes, void **dev_ptr) {
+  TRY(enter(ctx));
+  if (!dev_ptr) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  *dev_ptr = nullptr;
+  CK(cudaMalloc(dev_ptr, bytes ? bytes : 256));
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_ipc_free(mapsq_ctx *ctx, void *dev_ptr) {
+  TRY(enter(ctx));
+  if (dev_ptr) CK(cudaFree(dev_ptr));
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_ipc_export(mapsq_ctx *ctx, void *dev_ptr, void *handle64) {
+  TRY(enter(ctx));
+  if (!dev_ptr || !handle64) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dev_ptr));
+  std::memcpy(handle64, &h, 64);
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_ipc_open(mapsq_ctx *ctx, const void *handle64, void **dev_ptr) {
+  TRY(enter(ctx));
+  if (!dev_ptr || !handle64) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_ipc_close(mapsq_ctx *ctx, void *dev_ptr) {
+  TRY(enter(ctx));
+  CK(cudaIpcCloseMemHandle(dev_ptr));
   return MAPSQ_OK;
 }
 

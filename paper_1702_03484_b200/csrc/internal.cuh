@@ -341,14 +341,15 @@ struct PartArgs {
   const uint32_t *key[MAPSQ_MAX_COLS];
   uint32_t ncols;
   const uint32_t *in[MAPSQ_MAX_COLS];
-  uint32_t *out[MAPSQ_MAX_COLS];
   uint64_t n;
   uint32_t nparts;
 };
 void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntiles,
                            cudaStream_t s);
+// dst_row[d]: first row of this rank's block in destination d's arena; dst_cols[d * ncols + c]:
+// column c of d's arena (a device or an NVLink peer pointer)
 void launch_partition_scatter(const PartArgs &a, const uint64_t *tile_off, uint64_t ntiles,
-                              cudaStream_t s);
+                              const uint64_t *dst_row, const uint64_t *dst_cols, cudaStream_t s);
 constexpr int kPartThreads = 256;
 constexpr int kPartItems = 16;
 constexpr uint64_t kPartTile = kPartThreads * kPartItems;

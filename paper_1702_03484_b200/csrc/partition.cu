@@ -1,4 +1,6 @@
-// partition.cu — K8: hash partition of a partial-match table on its join key (SURVEY §8 row e).
+// partition.cu — K8: hash partition of a partial-match table on its join key (SURVEY §8 row e),
+// fused with the exchange: the scatter stores every row straight into its destination rank's
+// receive arena through NVLink peer pointers (one kernel does the partition and the all-to-all).
 //
 // An equi-join decomposes over disjoint key sets, so on G GPUs each rank sends every row to
 // rank dest = fmix32(fold(key)) mod G and then runs the local sort-join on what it receives.
@@ -47,7 +49,9 @@ partition_hist_kernel(const PartArgs a, uint32_t *__restrict__ tile_hist, uint64
 }
 
 __global__ void __launch_bounds__(kPartThreads)
-partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off, uint64_t ntiles) {
+partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off, uint64_t ntiles,
+                         const uint64_t *__restrict__ dst_row,
+                         const uint64_t *__restrict__ dst_cols) {
   __shared__ uint32_t s_wh[kWarps][kMaxParts];
   __shared__ uint64_t s_base[kMaxParts];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -81,16 +85,23 @@ partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off
       s_wh[w][tid] = run;
       run += c;
     }
-    s_base[tid] = tile_off[(uint64_t)tid * ntiles + blockIdx.x];
+    // this tile's first row for destination tid inside its arena block
+    s_base[tid] = tile_off[(uint64_t)tid * ntiles + blockIdx.x] - tile_off[(uint64_t)tid * ntiles] +
+                  dst_row[tid];
   }
   __syncthreads();
+  // destination: column c of destination d starts at dst_cols[d * ncols + c] (a local or an
+  // NVLink peer pointer); the row lands at dst_row[d] + (its rank among this rank's rows for d)
 #pragma unroll
   for (int it = 0; it < kPartItems; it++) {
     const uint64_t i = wbase + (uint64_t)it * 32 + lane;
     if (i >= a.n) continue;
     const uint32_t d = dst[it];
     const uint64_t pos = s_base[d] + s_wh[warp][d] + rank[it];
-    for (uint32_t c = 0; c < a.ncols; c++) a.out[c][pos] = __ldg(a.in[c] + i);
+    for (uint32_t c = 0; c < a.ncols; c++) {
+      uint32_t *col = reinterpret_cast<uint32_t *>(dst_cols[d * a.ncols + c]);
+      col[pos] = __ldg(a.in[c] + i);
+    }
   }
 }
 
@@ -102,8 +113,9 @@ void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntil
 }
 
 void launch_partition_scatter(const PartArgs &a, const uint64_t *tile_off, uint64_t ntiles,
-                              cudaStream_t s) {
-  partition_scatter_kernel<<<(unsigned)ntiles, kPartThreads, 0, s>>>(a, tile_off, ntiles);
+                              const uint64_t *dst_row, const uint64_t *dst_cols, cudaStream_t s) {
+  partition_scatter_kernel<<<(unsigned)ntiles, kPartThreads, 0, s>>>(a, tile_off, ntiles, dst_row,
+                                                                     dst_cols);
 }
 
 }  // namespace mapsq

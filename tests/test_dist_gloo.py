@@ -123,3 +123,21 @@ def test_join_dist_gloo_world2():
         # every key lives on exactly one rank
         keys = [set(tuple(x) for x in r[2][step][1][:, :len(res[0][3][step])].tolist()) for r in res]
         assert not (keys[0] & keys[1])
+
+
+def test_exchange_layout_matches_all_to_all_order():
+    """The fused exchange writes rank s's rows for d at rows sum_{s'<s} C[s'][d] of d's arena:
+    exactly the source-rank-grouped order all_to_all_single produces."""
+    from paper_1702_03484_b200.dist import exchange_layout
+    C = [[3, 0, 5], [1, 2, 0], [4, 4, 4]]
+    rows = [exchange_layout(C, r, 2)[0] for r in range(3)]
+    _, recv, need = exchange_layout(C, 0, 2)
+    assert recv == [8, 6, 9] and need == [64, 48, 72]
+    assert [rows[r][0] for r in range(3)] == [0, 3, 4]
+    assert [rows[r][1] for r in range(3)] == [0, 0, 2]
+    assert [rows[r][2] for r in range(3)] == [0, 5, 5]
+    # blocks tile every destination arena exactly
+    for d in range(3):
+        spans = sorted((rows[r][d], rows[r][d] + C[r][d]) for r in range(3))
+        assert spans[0][0] == 0 and spans[-1][1] == recv[d]
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(2))

@@ -325,17 +325,39 @@ def test_stats_and_launch_count(ctx):
 
 
 def test_query_dist_world1_nccl(ctx, tmp_path):
-    """The distributed orchestration (K8 partition + NCCL all-to-all + local join) on one GPU."""
+    """The distributed orchestration on one GPU: fused partition + exchange kernel into the
+    IPC-exported arena (fused=True) and K8 partition + NCCL all-to-all (fused=False)."""
     import torch.distributed as tdist
     from paper_1702_03484_b200 import dist as mqd
     if not tdist.is_initialized():
-        tdist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+        tdist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                                 device_id=torch.device("cuda", 0))
     s, p, o, st = datagen.lubm(2)
     trip = (dev(s), dev(p), dev(o))
-    for cfg in ("C3", "C5"):
-        pats = config_query(cfg)
-        got = mqd.query_dist(ctx, trip, pats)
-        ref = oracle.query(s, p, o, pats)
-        assert got.vars == ref.vars
-        assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
+    for fused in (True, False):
+        for cfg in ("C3", "C5", "C2"):
+            pats = config_query(cfg)
+            got = mqd.query_dist(ctx, trip, pats, fused=fused)
+            ref = oracle.query(s, p, o, pats)
+            assert got.vars == ref.vars
+            assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
     tdist.destroy_process_group()
+
+
+def test_partition_scatter_into_external_columns(ctx):
+    """mapsq_partition_scatter writes destination d's rows at dest_row[d] of arbitrary column
+    pointers (the peer-store contract), stable within each destination."""
+    rng = np.random.default_rng(21)
+    A = rng.integers(0, 1 << 16, (30_000, 2)).astype(np.uint32)
+    t = dtable([0, 1], A)
+    G = 3
+    state, counts = ctx.partition_plan(t, [0], G)
+    ref, ref_counts = ctx.partition(t, [0], G)
+    assert counts == ref_counts
+    # three separate "arenas", each with a 7-row gap before this rank's block
+    arenas = [torch.zeros((2, counts[d] + 7), dtype=torch.int32, device="cuda") for d in range(G)]
+    cols = [arenas[d][c].data_ptr() for d in range(G) for c in range(2)]
+    ctx.partition_scatter(state, [7] * G, cols)
+    got = np.concatenate([arenas[d][:, 7:].cpu().numpy().view(np.uint32).T for d in range(G)])
+    assert np.array_equal(got, ref.to_numpy())
+    assert all(int(arenas[d][:, :7].abs().sum()) == 0 for d in range(G))
