@@ -574,9 +574,11 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     for (uint32_t c = 0; c < pl.nrest1; c++) ea.rest1[c] = a.col[pl.rest_col1[c]];
     for (uint32_t c = 0; c < pl.nrest2; c++) ea.rest2[c] = b.col[pl.rest_col2[c]];
     for (uint32_t c = 0; c < pl.out_ncols; c++) ea.out[c] = rs->col[c];
+    ea.tile_g0 = sc.get<uint64_t>(expand_tiles(m) + 1);
+    NEED(ea.tile_g0);
     const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * n +
                            4ull * (n1 * pl.nrest1 + n2 * pl.nrest2);
-    KTimer kt(ctx, s, "expand", bytes);
+    KTimer kt(ctx, s, "expand", bytes, 2);
     launch_expand(ea, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -306,8 +306,11 @@ struct ExpandArgs {
   const uint32_t *rest1[MAPSQ_MAX_COLS];
   const uint32_t *rest2[MAPSQ_MAX_COLS];
   uint32_t *out[MAPSQ_MAX_COLS];  // nkey + nrest1 + nrest2 columns
+  const uint64_t *tile_g0;        // scratch of expand_tiles(m) words: first group of each tile
 };
+// launches the tile -> first-group kernel, then the expansion (2 launches)
 void launch_expand(const ExpandArgs &a, cudaStream_t s);
+uint64_t expand_tiles(uint64_t m);
 
 // RESIDUAL path (wide keys): groups are equal on the packed key; the residual shared columns are
 // compared exactly, pair by pair, inside each group.

@@ -233,6 +233,18 @@ constexpr int kEChunks = 2;                  // chunks per thread
 constexpr uint64_t kETile = (uint64_t)kEThreads * kERows * kEChunks;
 constexpr int kEGroups = 1024;               // groups staged in shared memory per tile
 
+// K5b: tile t of the expansion (rows [t * kETile, ...)) starts inside group tile_g0[t].  One thread
+// per group marks the tiles whose first row falls in the group's output range.
+__global__ void __launch_bounds__(256)
+tile_groups_kernel(const uint64_t *__restrict__ goff, uint64_t ngroups, uint64_t m,
+                   uint64_t *__restrict__ tile_g0) {
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = goff[g], e = g + 1 < ngroups ? goff[g + 1] : m;
+    for (uint64_t t = (b + kETile - 1) / kETile; t * kETile < e; t++) tile_g0[t] = g;
+  }
+}
+
 __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, uint64_t hi,
                                              uint64_t r) {
   // largest g in [lo, hi] with off[g] <= r  (off strictly increasing, off[lo] <= r)
@@ -266,8 +278,12 @@ expand_kernel(const ExpandArgs a) {
                : (c < a.nkey + a.nrest1 ? a.rest1[c - a.nkey] : a.rest2[c - a.nkey - a.nrest1]);
   }
   const uint64_t t0 = (uint64_t)blockIdx.x * kETile;
-  const uint64_t t1 = (t0 + kETile < a.m ? t0 + kETile : a.m) - 1;
-  if (tid < 2) s_g[tid] = group_of(a.goff, 0, a.ngroups - 1, tid == 0 ? t0 : t1);
+  // the tile's group range from the precomputed first group of every tile (tile_groups_kernel):
+  // the groups of rows [t0, t0 + kETile) lie in [first(t), first(t + 1)]
+  if (tid == 0) {
+    s_g[0] = a.tile_g0[blockIdx.x];
+    s_g[1] = blockIdx.x + 1 < gridDim.x ? a.tile_g0[blockIdx.x + 1] : a.ngroups - 1;
+  }
   __syncthreads();
   const uint64_t g0 = s_g[0], g1 = s_g[1];
   const bool staged = g1 - g0 + 1 <= (uint64_t)kEGroups;
@@ -507,9 +523,13 @@ void launch_residual_expand(const ResidualArgs &a, uint64_t cap, const uint64_t 
   residual_expand_kernel<<<residual_grid(cap), 256, 0, s>>>(a, pmask);
 }
 
+uint64_t expand_tiles(uint64_t m) { return ceil_div(m, kETile); }
+
 void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   if (a.m == 0) return;
   const uint64_t nblocks = ceil_div(a.m, kETile);
+  const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(a.ngroups, 256), 148 * 16));
+  tile_groups_kernel<<<gg, 256, 0, s>>>(a.goff, a.ngroups, a.m, const_cast<uint64_t *>(a.tile_g0));
   expand_kernel<<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
 }
 
