@@ -8,6 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "internal.cuh"
 
@@ -48,6 +51,16 @@ void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s) {
     ctx->alloc.free(ctx->alloc.ctx, p, (void *)s);
   else
     cudaFreeAsync(p, s);
+}
+
+void set_smem_limit(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void *>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({dev, kernel}).second)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 Scratch::Scratch(mapsq_ctx *c, cudaStream_t st) : ctx(c), s(st), mark(c->arena_used) {

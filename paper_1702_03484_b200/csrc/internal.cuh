@@ -109,6 +109,10 @@ struct KTimer {
   ~KTimer();
 };
 
+// Raise a kernel's dynamic shared-memory limit once per (device, kernel) (the attribute is per
+// device context; a process-wide flag would skip the second device).
+void set_smem_limit(const void *kernel, size_t bytes);
+
 inline uint32_t bits_for(uint64_t range_max) {  // bits needed to represent 0..range_max
   uint32_t b = 0;
   while (b < 64 && (range_max >> b) != 0) b++;

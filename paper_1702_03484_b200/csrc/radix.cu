@@ -338,12 +338,8 @@ void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32
   const uint64_t n = a.n1 + a.n2;
   const int g = grid_for(n, kHistThreads * kHistItems);
   const size_t smem = kHistCopies * std::max<uint32_t>(a.passes, 1) * kRadix * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pack_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-    cudaFuncSetAttribute(pack_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-    attr = true;
-  }
+  set_smem_limit((const void *)pack_hist_kernel<true>, 65536);
+  set_smem_limit((const void *)pack_hist_kernel<false>, 65536);
   if (a.kv)
     pack_hist_kernel<true><<<g, kHistThreads, smem, s>>>(a, words, vals, hist);
   else
@@ -370,11 +366,7 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     const uint64_t ntiles = ceil_div(n, kSortTile);
     const size_t smem = kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
     auto kern = radix_pass_kernel<true, kSortItems, kLookWin, 3, false, true>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
         next_shift, next_mask);
@@ -387,11 +379,7 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
     auto kern = radix_pass_kernel<false, kItems, 4, 2, true, false>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,
                                                       next_shift, next_mask);
