@@ -9,6 +9,9 @@
 
 using namespace mapsq;
 namespace mapsq {
+void set_smem_limit(const void *kernel, size_t bytes) {  // (defined in api.cu for the library)
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 // Persistent one-sweep digit pass (P64 words).  Each CTA loops over tiles claimed in order from
 // the atomic counter; while it ranks / looks back / scatters tile t, the TMA engine already
 // streams the NEXT claimed tile into the other shared-memory buffer (cp.async.bulk + mbarrier),
@@ -407,10 +410,9 @@ int main(int argc, char **argv) {
       }
       printf("%-34s %8.3f ms  %7.1f GB/s  %s\n", name, best, 16.0 * n / best / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
-    timeit(radix_pass_kernel<false, 32, 4, 2, true, false>, 32, "items32 minb2 reload match (prev)");
+    timeit(radix_pass_kernel<false, 32, 4, 2, true, false>, 32, "items32 minb2 reload match (prod)");
     timeit(radix_pass_kernel<false, 32, 4, 2, true, true>, 32, "items32 minb2 reload ballot");
-    timeit(radix_pass_kernel<false, 16, 4, 4, true, true>, 16, "items16 minb4 reload ballot (new)");
-    timeit(radix_pass_kernel<false, 16, 4, 3, true, true>, 16, "items16 minb3 reload ballot");
+    timeit(radix_pass_kernel<false, 16, 4, 4, true, true>, 16, "items16 minb4 reload ballot");
   }
   // the library's real pass for comparison
   {
