@@ -201,9 +201,44 @@ mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host
                               int nproj, uint64_t *host_rows, uint32_t *out_ncols,
                               int32_t *out_var, uint32_t **host_cols, void *stream);
 
+/* ---- predicate-range index ----
+ * The store-side access path of partial matching (PAPER.md:154, :164 leave matching to the
+ * store; SPEC S:169-177 picks an index per pattern).  mapsq_index_build copies the triple table
+ * into index-owned device memory, stably partitioned by predicate (within one predicate the
+ * original triple order is kept), and records each predicate's row range and the exact bounds
+ * of its subjects and objects.  Blocking (a few size reads); runs once per loaded dataset.
+ * Memory: 12 B per triple for the permuted columns + per-predicate metadata; scratch during the
+ * build 16 B per triple.  Fails with MAPSQ_E_UNSUPPORTED if there are more than 2^20 distinct
+ * predicates or bits(p_hi - p_lo) + bits(n - 1) > 64.
+ *
+ * mapsq_scan_patterns_indexed: the same tables as mapsq_scan_patterns over the original
+ * triples (same rows, and for a constant-predicate pattern the same row order):
+ *   - P(?a, p, ?b) with a != b: a zero-copy view of the predicate's s/o range (owner == NULL,
+ *     valid until mapsq_index_destroy; no kernel runs);
+ *   - any other pattern with a constant predicate: the fused scan over that predicate's range;
+ *   - a pattern with a variable predicate: the fused scan over the whole (permuted) table, rows
+ *     in index order (predicate-major).
+ * mapsq_query_indexed: mapsq_query with the scans above. */
+typedef struct mapsq_index mapsq_index;
+mapsq_status mapsq_index_build(mapsq_ctx *ctx, const mapsq_triples *triples, mapsq_index **out,
+                               void *stream);
+void mapsq_index_destroy(mapsq_ctx *ctx, mapsq_index *idx);
+/* The permuted table (device pointers owned by the index) and its predicate count. */
+mapsq_status mapsq_index_triples(const mapsq_index *idx, mapsq_triples *out, uint32_t *npreds);
+/* Row range [*begin, *end) of predicate p in the permuted table (empty if p is absent). */
+mapsq_status mapsq_index_range(const mapsq_index *idx, uint32_t p, uint64_t *begin,
+                               uint64_t *end);
+mapsq_status mapsq_scan_patterns_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
+                                         const mapsq_pattern *pats, int k, mapsq_table *out,
+                                         void *stream);
+mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
+                                 const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                 int nproj, mapsq_table *rs, void *stream);
+
 /* ---- phase entry points (for phase-level parity tests; the same kernels mapsq_join runs) ----
  * Map (K2, row a3): words[r] = key'(tp1 row r) << ib | r and words[n1 + r] = key'(tp2 row r)
- * << ib | (n1 + r) for a P64 plan.  `words` is a caller-owned device array of n1 + n2. */
+ * << ib | (n1 + r) for a P64 plan (a RESIDUAL plan packs only its packed_mask columns; a KV
+ * plan is rejected).  `words` is a caller-owned device array of n1 + n2. */
 mapsq_status mapsq_map_words(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
                              const mapsq_join_plan *plan, uint64_t *words, void *stream);
 /* Sort (K3, row a4): stable LSD radix sort of n words by bits [bit_lo, bit_hi), in place

@@ -105,6 +105,13 @@ def lib():
             "mapsq_query_host": (st, [vp, u64, vp, vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
                                       ctypes.c_int, ctypes.POINTER(u64), ctypes.POINTER(u32),
                                       ctypes.POINTER(i32), ctypes.POINTER(vp), vp]),
+            "mapsq_index_build": (st, [vp, ctypes.POINTER(_Triples), ctypes.POINTER(vp), vp]),
+            "mapsq_index_destroy": (None, [vp, vp]),
+            "mapsq_index_triples": (st, [vp, ctypes.POINTER(_Triples), ctypes.POINTER(u32)]),
+            "mapsq_index_range": (st, [vp, u32, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+            "mapsq_scan_patterns_indexed": (st, [vp, vp, PP, ctypes.c_int, PT, vp]),
+            "mapsq_query_indexed": (st, [vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
+                                         ctypes.c_int, PT, vp]),
             "mapsq_map_words": (st, [vp, PT, PT, ctypes.POINTER(JoinPlan), vp, vp]),
             "mapsq_sort_words": (st, [vp, vp, u64, u32, u32, vp]),
             "mapsq_sort_pairs": (st, [vp, vp, vp, u64, u32, u32, vp]),
@@ -239,9 +246,10 @@ class DeviceTable:
         return DeviceTable(vars_, columns, n, t, owner=None)
 
 
-def _wrap(ctx: "Context", t: _Table) -> DeviceTable:
+def _wrap(ctx: "Context", t: _Table, keep=None) -> DeviceTable:
     import torch
     owner = _Owner(ctx, t)
+    owner.keep = keep  # e.g. the Index whose memory a zero-copy view references
     n, w = int(t.nrows), int(t.ncols)
     cols = []
     for c in range(w):
@@ -275,6 +283,42 @@ def _triples(s, p, o) -> _Triples:
     return _Triples(n, s.data_ptr(), p.data_ptr(), o.data_ptr())
 
 
+class Index:
+    """Predicate-range index (mapsq_index_build): the triple table stably partitioned by
+    predicate, owned by the library.  Pass it instead of (s, p, o) to scan_patterns / query."""
+
+    def __init__(self, ctx: "Context", handle):
+        self.ctx, self.handle = ctx, handle
+        T, npreds = _Triples(), ctypes.c_uint32()
+        ctx._check(lib().mapsq_index_triples(handle, ctypes.byref(T), ctypes.byref(npreds)))
+        self.n, self.npreds, self._T = int(T.n), int(npreds.value), T
+
+    def range(self, p: int):
+        b, e = ctypes.c_uint64(), ctypes.c_uint64()
+        self.ctx._check(lib().mapsq_index_range(self.handle, int(p), ctypes.byref(b),
+                                                ctypes.byref(e)))
+        return int(b.value), int(e.value)
+
+    def triples(self):
+        """(s, p, o) zero-copy torch views of the permuted table."""
+        import torch
+        if self.n == 0:
+            return tuple(torch.empty(0, dtype=torch.uint32, device="cuda") for _ in range(3))
+        return tuple(torch.as_tensor(_CAI(ptr, self.n, self), device="cuda")
+                     for ptr in (self._T.s, self._T.p, self._T.o))
+
+    def release(self):
+        if self.handle:
+            lib().mapsq_index_destroy(self.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
 class Context:
     """One libmapsq context on one device (default allocator: cudaMallocAsync pool)."""
 
@@ -302,11 +346,24 @@ class Context:
             raise MapsqError(st, lib().mapsq_last_error(self.handle).decode())
 
     # ---- partial matching (row a1)
-    def scan_patterns(self, triples, patterns, stream=None) -> list:
+    def index_build(self, triples, stream=None) -> Index:
+        """Build the predicate-range index of (s, p, o) (blocking; once per dataset)."""
         T = _triples(*triples)
+        h = ctypes.c_void_p()
+        self._check(lib().mapsq_index_build(self.handle, ctypes.byref(T), ctypes.byref(h),
+                                            _stream(stream)))
+        return Index(self, h)
+
+    def scan_patterns(self, triples, patterns, stream=None) -> list:
+        """``triples`` = (s, p, o) device tensors, or an Index (range scans / views)."""
         k = len(patterns)
         pats = (_Pattern * k)(*[pattern_struct(p) for p in patterns])
         outs = (_Table * k)()
+        if isinstance(triples, Index):
+            self._check(lib().mapsq_scan_patterns_indexed(self.handle, triples.handle, pats, k,
+                                                          outs, _stream(stream)))
+            return [_wrap(self, outs[j], keep=triples) for j in range(k)]
+        T = _triples(*triples)
         self._check(lib().mapsq_scan_patterns(self.handle, ctypes.byref(T), pats, k, outs,
                                               _stream(stream)))
         return [_wrap(self, outs[j]) for j in range(k)]
@@ -328,12 +385,17 @@ class Context:
 
     # ---- query (row a7)
     def query(self, triples, patterns, proj=None, stream=None) -> DeviceTable:
-        T = _triples(*triples)
+        """``triples`` = (s, p, o) device tensors, or an Index."""
         k = len(patterns)
         pats = (_Pattern * k)(*[pattern_struct(p) for p in patterns])
         proj = list(proj or [])
         pr = (ctypes.c_int32 * max(1, len(proj)))(*proj)
         out = _Table()
+        if isinstance(triples, Index):
+            self._check(lib().mapsq_query_indexed(self.handle, triples.handle, pats, k, pr,
+                                                  len(proj), ctypes.byref(out), _stream(stream)))
+            return _wrap(self, out, keep=triples)
+        T = _triples(*triples)
         self._check(lib().mapsq_query(self.handle, ctypes.byref(T), pats, k, pr, len(proj),
                                       ctypes.byref(out), _stream(stream)))
         return _wrap(self, out)

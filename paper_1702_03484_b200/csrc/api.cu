@@ -14,6 +14,8 @@
 
 #include "internal.cuh"
 
+#include <memory>
+
 using namespace mapsq;
 
 namespace mapsq {
@@ -728,10 +730,235 @@ mapsq_status scan_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_patte
   return MAPSQ_OK;
 }
 
+}  // namespace
+
+struct mapsq_index {
+  uint64_t n = 0;
+  void *owner = nullptr;  // s | p | o, one allocation (16 B aligned column strides)
+  uint32_t *s = nullptr, *p = nullptr, *o = nullptr;
+  std::vector<uint32_t> pred;   // distinct predicates, ascending
+  std::vector<uint64_t> start;  // pred[i] occupies rows [start[i], start[i + 1])
+  std::vector<uint32_t> slo, shi, olo, ohi;
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------ index (f1)
+mapsq_status index_build_impl(mapsq_ctx *ctx, const mapsq_triples *T, mapsq_index **out,
+                              cudaStream_t s) {
+  if (!out) return set_error(ctx, MAPSQ_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!T) return set_error(ctx, MAPSQ_E_INVALID, "triples is NULL");
+  if (T->n && (!T->s || !T->p || !T->o)) return set_error(ctx, MAPSQ_E_INVALID, "NULL triple column");
+  const uint64_t n = T->n;
+  std::unique_ptr<mapsq_index> idx(new (std::nothrow) mapsq_index());
+  if (!idx) return set_error(ctx, MAPSQ_E_NOMEM, "index allocation failed");
+  idx->n = n;
+  idx->start.push_back(0);
+  if (n == 0) {
+    *out = idx.release();
+    return MAPSQ_OK;
+  }
+  const uint32_t ib = n > 1 ? bits_for(n - 1) : 1;
+  Scratch sc(ctx, s);
+  uint32_t *pb = sc.get<uint32_t>(2);
+  NEED(pb);
+  CK(cudaMemsetAsync(pb, 0xff, 4, s));
+  CK(cudaMemsetAsync(pb + 1, 0, 4, s));
+  {
+    const uint32_t *cols[1] = {T->p};
+    KTimer kt(ctx, s, "minmax", 4ull * n);
+    launch_minmax(cols, 1, n, pb, s);
+    CKL("minmax");
+  }
+  TRY(ensure_pinned(ctx, 1));
+  CK(cudaMemcpyAsync(ctx->pinned, pb, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t p_lo = reinterpret_cast<const uint32_t *>(ctx->pinned)[0];
+  const uint32_t p_hi = reinterpret_cast<const uint32_t *>(ctx->pinned)[1];
+  const uint32_t pbits = p_hi > p_lo ? bits_for((uint64_t)p_hi - p_lo) : 0;
+  if (pbits + ib > 64)
+    return set_error(ctx, MAPSQ_E_UNSUPPORTED, "predicate bits + row bits exceed 64");
+  // Map + stable sort on the predicate bits only (the row id below keeps the triple order)
+  uint64_t *wa = sc.get<uint64_t>(n), *wb = sc.get<uint64_t>(n);
+  uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
+  NEED(wa); NEED(wb); NEED(hist);
+  CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+  {
+    PackArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    pa.nkey = pbits ? 1 : 0;
+    pa.key1[0] = T->p;
+    pa.key2[0] = T->p + n;  // (no RIGHT rows: n2 == 0)
+    pa.lo[0] = p_lo;
+    pa.shift[0] = 0;
+    pa.n1 = n;
+    pa.n2 = 0;
+    pa.ib = ib;
+    pa.bit_lo = ib;
+    const uint32_t passes = (pbits + 7) / 8;
+    pa.passes = passes ? 1 : 0;
+    pa.last_mask = passes == 1 ? ((1u << pbits) - 1u) : 0xffu;
+    KTimer kt(ctx, s, "pack_hist", 4ull * n + 8ull * n);
+    launch_pack_hist(pa, wa, nullptr, hist, s);
+    CKL("pack_hist");
+  }
+  int which = 0;
+  TRY(radix_sort(ctx, wa, wb, nullptr, nullptr, n, ib, pbits, hist, sc, s, &which));
+  const uint64_t *words = which ? wb : wa;
+  const uint64_t stride = (n + 3) & ~3ull;
+  idx->owner = dalloc(ctx, 3 * stride * sizeof(uint32_t), s);
+  if (!idx->owner) return set_error(ctx, MAPSQ_E_NOMEM, "index allocation failed");
+  idx->s = static_cast<uint32_t *>(idx->owner);
+  idx->p = idx->s + stride;
+  idx->o = idx->p + stride;
+  struct OwnerGuard {
+    mapsq_ctx *ctx; mapsq_index *idx; cudaStream_t s; bool keep = false;
+    ~OwnerGuard() { if (!keep) dfree(ctx, idx->owner, s); }
+  } guard{ctx, idx.get(), s};
+  const uint32_t cap = (uint32_t)std::min<uint64_t>(n, 1u << 20);
+  uint32_t *head_p = sc.get<uint32_t>(cap);
+  uint64_t *head_start = sc.get<uint64_t>(cap);
+  uint32_t *nheads = sc.get<uint32_t>(1);
+  NEED(head_p); NEED(head_start); NEED(nheads);
+  CK(cudaMemsetAsync(nheads, 0, 4, s));
+  {
+    KTimer kt(ctx, s, "index_gather", 8ull * n + 8ull * n + 12ull * n);
+    launch_index_gather(words, n, ib, p_lo, T->s, T->o, idx->s, idx->p, idx->o, head_p,
+                        head_start, nheads, cap, s);
+    CKL("index_gather");
+  }
+  CK(cudaMemcpyAsync(ctx->pinned, nheads, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint32_t R = reinterpret_cast<const uint32_t *>(ctx->pinned)[0];
+  if (R > cap) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "more than 2^20 distinct predicates");
+  std::vector<uint32_t> hp(R);
+  std::vector<uint64_t> hs(R);
+  CK(cudaMemcpyAsync(hp.data(), head_p, 4ull * R, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hs.data(), head_start, 8ull * R, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<uint32_t> ord(R);
+  for (uint32_t i = 0; i < R; i++) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return hs[a] < hs[b]; });
+  idx->pred.resize(R);
+  idx->start.assign(R + 1, n);
+  for (uint32_t i = 0; i < R; i++) {
+    idx->pred[i] = hp[ord[i]];
+    idx->start[i] = hs[ord[i]];
+  }
+  uint64_t *starts = sc.get<uint64_t>(R + 1);
+  uint32_t *bnd = sc.get<uint32_t>(4ull * R);
+  NEED(starts); NEED(bnd);
+  CK(cudaMemcpyAsync(starts, idx->start.data(), 8ull * (R + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(bnd, 0xff, 8ull * R, s));
+  CK(cudaMemsetAsync(bnd + 2ull * R, 0, 8ull * R, s));
+  {
+    KTimer kt(ctx, s, "index_bounds", 8ull * n);
+    launch_index_bounds(idx->s, idx->o, n, starts, R, bnd, s);
+    CKL("index_bounds");
+  }
+  std::vector<uint32_t> hb(4ull * R);
+  CK(cudaMemcpyAsync(hb.data(), bnd, 16ull * R, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  idx->slo.assign(hb.begin(), hb.begin() + R);
+  idx->olo.assign(hb.begin() + R, hb.begin() + 2 * R);
+  idx->shi.assign(hb.begin() + 2 * R, hb.begin() + 3 * R);
+  idx->ohi.assign(hb.begin() + 3 * R, hb.end());
+  guard.keep = true;
+  *out = idx.release();
+  return MAPSQ_OK;
+}
+
+// position of predicate p in idx->pred, or -1
+int64_t index_find(const mapsq_index *idx, uint32_t p) {
+  auto it = std::lower_bound(idx->pred.begin(), idx->pred.end(), p);
+  if (it == idx->pred.end() || *it != p) return -1;
+  return it - idx->pred.begin();
+}
+
+mapsq_status scan_indexed_impl(mapsq_ctx *ctx, const mapsq_index *idx, const mapsq_pattern *pats,
+                               int k, mapsq_table *out, cudaStream_t s) {
+  if (!out) return set_error(ctx, MAPSQ_E_INVALID, "out is NULL");
+  for (int j = 0; j < k && j < MAPSQ_MAX_PATTERNS; j++) clear_table(&out[j]);
+  if (!idx) return set_error(ctx, MAPSQ_E_INVALID, "index is NULL");
+  {
+    ScanArgs a;  // validation + schemas, exactly as the unindexed scan
+    int32_t vars[MAPSQ_MAX_PATTERNS][3];
+    TRY(build_scan_args(ctx, pats, k, &a, vars));
+  }
+  // groups: patterns scanned over one row range of the permuted table
+  struct Group { uint64_t b, e; std::vector<int> pats; };
+  std::vector<Group> groups;
+  for (int j = 0; j < k; j++) {
+    const mapsq_pattern &P = pats[j];
+    uint64_t b = 0, e = idx->n;
+    int64_t r = -2;
+    if (P.var[1] < 0) {
+      r = index_find(idx, P.id[1]);
+      b = r >= 0 ? idx->start[r] : 0;
+      e = r >= 0 ? idx->start[r + 1] : 0;
+    }
+    const bool view = P.var[1] < 0 && P.var[0] >= 0 && P.var[2] >= 0 && P.var[0] != P.var[2];
+    if (view || r == -1) {
+      // zero-copy view of the predicate's s/o range (or an empty table: p absent)
+      mapsq_table &t = out[j];
+      clear_table(&t);
+      const bool pure = view;
+      uint32_t nc = 0;
+      const uint32_t *srcs[3] = {idx->s + b, idx->p + b, idx->o + b};
+      for (int q = 0; q < 3; q++) {
+        const int32_t v = P.var[q];
+        if (v < 0) continue;
+        bool dup = false;
+        for (uint32_t c = 0; c < nc; c++) dup |= t.var[c] == v;
+        if (dup) continue;
+        t.var[nc] = v;
+        t.col[nc] = (r >= 0 && pure) ? const_cast<uint32_t *>(srcs[q]) : nullptr;
+        if (r >= 0 && pure) {
+          t.lo[nc] = q == 0 ? idx->slo[r] : idx->olo[r];
+          t.hi[nc] = q == 0 ? idx->shi[r] : idx->ohi[r];
+        }
+        nc++;
+      }
+      t.ncols = nc;
+      t.nrows = r >= 0 ? e - b : 0;
+      t.flags = MAPSQ_TABLE_BOUNDS;
+      t.owner = nullptr;
+      continue;
+    }
+    bool placed = false;
+    for (auto &g : groups)
+      if (g.b == b && g.e == e) {
+        g.pats.push_back(j);
+        placed = true;
+      }
+    if (!placed) groups.push_back(Group{b, e, {j}});
+  }
+  ctx->counters.scans += k;
+  for (size_t gi = 0; gi < groups.size(); gi++) {
+    const Group &g = groups[gi];
+    mapsq_triples V{g.e - g.b, idx->s + g.b, idx->p + g.b, idx->o + g.b};
+    mapsq_pattern gp[MAPSQ_MAX_PATTERNS];
+    mapsq_table gt[MAPSQ_MAX_PATTERNS];
+    for (size_t q = 0; q < g.pats.size(); q++) gp[q] = pats[g.pats[q]];
+    ctx->counters.scans -= g.pats.size();  // (scan_impl counts them again)
+    mapsq_status st = scan_impl(ctx, &V, gp, (int)g.pats.size(), gt, s);
+    if (st != MAPSQ_OK) {
+      for (int j = 0; j < k; j++) {
+        dfree(ctx, out[j].owner, s);
+        clear_table(&out[j]);
+      }
+      return st;
+    }
+    for (size_t q = 0; q < g.pats.size(); q++) out[g.pats[q]] = gt[q];
+  }
+  return MAPSQ_OK;
+}
+
 // ------------------------------------------------------------------------------ query
 mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_pattern *pats,
                         int npats, const int32_t *proj, int nproj, mapsq_table *rs,
-                        cudaStream_t s) {
+                        cudaStream_t s, const mapsq_index *idx = nullptr) {
   if (!rs) return set_error(ctx, MAPSQ_E_INVALID, "rs is NULL");
   clear_table(rs);
   if (!pats || npats < 1 || npats > MAPSQ_MAX_PATTERNS)
@@ -768,7 +995,10 @@ mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_patt
       return set_error(ctx, MAPSQ_E_INVALID, "projected variable not in the query");
 
   mapsq_table tabs[MAPSQ_MAX_PATTERNS];
-  TRY(scan_impl(ctx, T, pats, npats, tabs, s));
+  if (idx)
+    TRY(scan_indexed_impl(ctx, idx, pats, npats, tabs, s));
+  else
+    TRY(scan_impl(ctx, T, pats, npats, tabs, s));
   mapsq_table acc = tabs[0];
   for (int i = 1; i < npats; i++) {
     mapsq_table r;
@@ -879,6 +1109,56 @@ MAPSQ_API mapsq_status mapsq_scan_pattern(mapsq_ctx *ctx, const mapsq_triples *T
   return scan_impl(ctx, T, pat, 1, out, S(stream));
 }
 
+MAPSQ_API mapsq_status mapsq_index_build(mapsq_ctx *ctx, const mapsq_triples *T,
+                                         mapsq_index **out, void *stream) {
+  TRY(enter(ctx));
+  return index_build_impl(ctx, T, out, S(stream));
+}
+
+MAPSQ_API void mapsq_index_destroy(mapsq_ctx *ctx, mapsq_index *idx) {
+  if (!idx) return;
+  if (idx->owner && ctx) {
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();  // no enqueued work may still read the index
+    dfree(ctx, idx->owner, nullptr);
+    cudaStreamSynchronize(nullptr);
+  }
+  delete idx;
+}
+
+MAPSQ_API mapsq_status mapsq_index_triples(const mapsq_index *idx, mapsq_triples *out,
+                                           uint32_t *npreds) {
+  if (!idx || !out) return MAPSQ_E_INVALID;
+  *out = mapsq_triples{idx->n, idx->s, idx->p, idx->o};
+  if (npreds) *npreds = (uint32_t)idx->pred.size();
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_index_range(const mapsq_index *idx, uint32_t p, uint64_t *begin,
+                                         uint64_t *end) {
+  if (!idx || !begin || !end) return MAPSQ_E_INVALID;
+  const int64_t r = index_find(idx, p);
+  *begin = r >= 0 ? idx->start[r] : 0;
+  *end = r >= 0 ? idx->start[r + 1] : 0;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_scan_patterns_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
+                                                   const mapsq_pattern *pats, int k,
+                                                   mapsq_table *out, void *stream) {
+  TRY(enter(ctx));
+  return scan_indexed_impl(ctx, idx, pats, k, out, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
+                                           const mapsq_pattern *pats, int npats,
+                                           const int32_t *proj, int nproj, mapsq_table *rs,
+                                           void *stream) {
+  TRY(enter(ctx));
+  if (!idx) return set_error(ctx, MAPSQ_E_INVALID, "index is NULL");
+  return query_impl(ctx, nullptr, pats, npats, proj, nproj, rs, S(stream), idx);
+}
+
 MAPSQ_API mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table *tp2,
                                        mapsq_join_plan *plan) {
   if (!plan) return MAPSQ_E_INVALID;
@@ -975,7 +1255,7 @@ MAPSQ_API mapsq_status mapsq_map_words(mapsq_ctx *ctx, const mapsq_table *tp1,
                                        uint64_t *words, void *stream) {
   TRY(enter(ctx));
   if (!plan || !words || !tp1 || !tp2) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
-  if (plan->path != MAPSQ_PATH_P64) return set_error(ctx, MAPSQ_E_INVALID, "map_words needs a P64 plan");
+  if (plan->path == MAPSQ_PATH_KV) return set_error(ctx, MAPSQ_E_INVALID, "map_words needs a P64 or RESIDUAL plan");
   if (plan->n1 + plan->n2 == 0) return MAPSQ_OK;
   cudaStream_t s = S(stream);
   Scratch sc(ctx, s);

@@ -343,6 +343,16 @@ uint64_t find_groups_tiles(uint64_t n);
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,
                    cudaStream_t s);
 
+// Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
+// (unordered, atomic slots < cap); per-run bounds [slo | olo | shi | ohi].
+void launch_index_gather(const uint64_t *words, uint64_t n, uint32_t ib, uint32_t p_lo,
+                         const uint32_t *s, const uint32_t *o, uint32_t *s2, uint32_t *p2,
+                         uint32_t *o2, uint32_t *head_p, uint64_t *head_start, uint32_t *nheads,
+                         uint32_t cap, cudaStream_t st);
+void launch_index_bounds(const uint32_t *s2, const uint32_t *o2, uint64_t n,
+                         const uint64_t *starts, uint32_t nruns, uint32_t *bounds,
+                         cudaStream_t st);
+
 struct PartArgs {
   uint32_t nkey;
   const uint32_t *key[MAPSQ_MAX_COLS];

@@ -9,9 +9,10 @@
 // yields the total order (key', LEFT before RIGHT, rowid) — the sorted array is unique.
 //
 // The digit pass is a one-sweep design: tiles are claimed in order through an atomic counter,
-// ranked in shared memory with warp match-any multisplit, and their global digit offsets are
-// resolved by decoupled look-back over per-(tile, digit) status words; all P passes' global
-// digit offsets come from ONE upfront histogram fused into the Map kernel.
+// ranked by a warp multisplit (peer lanes from shared-memory atomicOr masks), and their global
+// digit offsets are resolved by decoupled look-back over per-(tile, digit) status words; each
+// pass's global digit counts come from the previous kernel (the Map kernel counts digit 0,
+// every pass counts the next digit).
 #include "internal.cuh"
 
 namespace mapsq {
@@ -129,8 +130,12 @@ __global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
 // slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
 // full tiles skip every bounds check (the first version spent most of its issue slots on 64-bit
 // index arithmetic).
+// RANK: how a warp finds the lanes holding the same digit — 0 = match.any, 1 = one ballot per
+// digit bit, 2 = shared-memory atomicOr of lane bits into per-digit masks (the key smem is still
+// unused during ranking), 3 = as 2 with a warp-uniform-digit shortcut (two redux.sync),
+// 4.. = as 2 after RANK-2 leader rounds of shfl + ballot.
 template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false,
-          bool BALLOT = false>
+          int RANK = 0>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
@@ -186,15 +191,25 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   // counter; batching keeps only kMB match masks live.
   constexpr int kMB = 8;
   const uint32_t lt = lanemask_lt();
+  // RANK 2/3: per-warp [kMB][256] lane masks in the (not yet used) key staging area
+  constexpr int kPB = (RANK >= 2) ? ((TILE * 8 / (kWarps * kRadix * 4)) < kMB ? (TILE * 8 / (kWarps * kRadix * 4)) : kMB) : 1;
+  uint32_t *s_pm = reinterpret_cast<uint32_t *>(smem_raw) + warp * kPB * kRadix;
+  if (RANK >= 2) {
+    uint4 *z = reinterpret_cast<uint4 *>(s_pm);
 #pragma unroll
-  for (int b0 = 0; b0 < ITEMS; b0 += kMB) {
-    uint32_t peers[kMB];
+    for (int i = lane; i < kPB * kRadix / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  }
+  constexpr int kB = RANK >= 2 ? kPB : kMB;
 #pragma unroll
-    for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
+  for (int b0 = 0; b0 < ITEMS; b0 += kB) {
+    uint32_t peers[kB];
+#pragma unroll
+    for (int u = 0; u < kB && b0 + u < ITEMS; u++) {
       const int it = b0 + u;
       const bool in = full || wslice + it * 32 + lane < tile_n;
       const uint32_t dg = (uint32_t)(k[it] >> shift) & dmask;
-      if (BALLOT) {  // peers from one ballot per digit bit (short-latency votes)
+      if (RANK == 1) {  // peers from one ballot per digit bit (short-latency votes)
         uint32_t pm = __ballot_sync(0xffffffffu, in);
         pm = in ? pm : ~pm;
 #pragma unroll
@@ -203,12 +218,41 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
           pm &= ((dg >> b) & 1u) ? bb : ~bb;
         }
         peers[u] = pm;
+      } else if (RANK >= 2) {
+        peers[u] = 0;
+        const uint32_t key = in ? dg : 0x100u;
+        if (RANK == 3) {
+          if (__reduce_min_sync(0xffffffffu, key) == __reduce_max_sync(0xffffffffu, key))
+            peers[u] = 0xffffffffu;
+        } else if (RANK >= 4) {
+          // up to RANK-2 leader rounds (shfl + ballot) catch the few-distinct-digit warps of
+          // clustered data; lanes still unmatched fall back to the atomicOr masks
+          uint32_t rem = 0xffffffffu;
+#pragma unroll
+          for (int q = 0; q < RANK - 2; q++) {
+            if (rem == 0) break;
+            const uint32_t dq = __shfl_sync(0xffffffffu, key, __ffs(rem) - 1);
+            const uint32_t bq = __ballot_sync(0xffffffffu, key == dq);
+            if (key == dq) peers[u] = bq;
+            rem &= ~bq;
+          }
+        }
+        if (in && peers[u] == 0) atomicOr(s_pm + u * kRadix + dg, 1u << lane);
       } else {
         peers[u] = __match_any_sync(0xffffffffu, in ? dg : 0x100u);
       }
     }
+    if (RANK >= 2) {
+      __syncwarp();
 #pragma unroll
-    for (int u = 0; u < kMB && b0 + u < ITEMS; u++) {
+      for (int u = 0; u < kB && b0 + u < ITEMS; u++) {
+        const uint32_t dg = (uint32_t)(k[b0 + u] >> shift) & dmask;
+        if (peers[u] == 0) peers[u] = s_pm[u * kRadix + dg];
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int u = 0; u < kB && b0 + u < ITEMS; u++) {
       const int it = b0 + u;
       const uint32_t d = (uint32_t)(k[it] >> shift) & dmask;
       const uint32_t leader = 31 - __clz(peers[u]);
@@ -217,12 +261,14 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
       if (in && lane == leader) {
         base = s_warp_hist[warp][d];
         s_warp_hist[warp][d] = base + __popc(peers[u]);
+        if (RANK >= 2) s_pm[u * kRadix + d] = 0;
       }
       r[it] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers[u] & lt);
       // the NEXT pass's digit histogram, from the keys already in registers (one shared atomic
       // per key; these issue slots are otherwise idle while the tile waits on its look-back)
       if (hist_next && in) atomicAdd(&s_next[(uint32_t)(k[it] >> next_shift) & next_mask], 1u);
     }
+    if (RANK >= 2) __syncwarp();
   }
   __syncthreads();
 
@@ -371,14 +417,14 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
         next_shift, next_mask);
   } else {
-    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement, match.any peers.
-    // tools/radix_ablate.cu: on uniformly random digits ballot peers at 4096-key tiles are faster
-    // (1.35 vs 2.03 ms per 2e8 words), but on the benchmark workloads' concentrated digits this
-    // configuration wins (C4 pass 6.55 vs 6.86 ms, C5 1.44 vs 1.66 ms).
+    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement.  Peers found by
+    // shared-memory atomicOr with a warp-uniform shortcut (tools/radix_ablate.cu, 4e8-word C4
+    // Zipf sort: 9.70 ms vs 10.72 match.any / 10.57 ballot; random digits 2.00 vs 2.86 / 2.22 ms
+    // per 3e8 words).
     constexpr int kItems = 32;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = radix_pass_kernel<false, kItems, 4, 2, true, false>;
+    auto kern = radix_pass_kernel<false, kItems, 4, 2, true, 3>;
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,

@@ -1,0 +1,142 @@
+"""GPU parity of the predicate-range index against the CPU oracle.
+
+The index is the triple table stably partitioned by predicate, so every constant-predicate
+pattern's partial matches come out of it in the same row order as the full scan: the oracle's
+scan (triple order) is compared IN ORDER; variable-predicate patterns (index order) are compared
+canonically."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import datagen  # noqa: E402
+import oracle  # noqa: E402
+import paper_1702_03484_b200 as mq  # noqa: E402
+from fixtures import config_expected_counts, config_query, load_table1  # noqa: E402
+
+V, C = "v", "c"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return mq.Context(0)
+
+
+def dev(a):
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).cuda()
+
+
+def host(t):
+    return t.view(torch.int32).cpu().numpy().view(np.uint32)
+
+
+def assert_same(gpu, ref, ordered=True, exact_bounds=True):
+    """exact_bounds: scan outputs carry exact column bounds; join outputs carry valid (inherited,
+    possibly wider) bounds."""
+    assert gpu.vars == ref.vars
+    got = gpu.to_numpy()
+    assert got.shape == ref.rows.shape
+    if ordered:
+        assert np.array_equal(got, ref.rows)
+    else:
+        assert np.array_equal(oracle.canonical_rows(got), oracle.canonical(ref).rows)
+    if ref.nrows:
+        tight = [(int(ref.rows[:, c].min()), int(ref.rows[:, c].max()))
+                 for c in range(len(ref.vars))]
+        if exact_bounds:
+            assert gpu.bounds == tight
+        else:
+            assert all(lo <= a and b <= hi for (lo, hi), (a, b) in zip(gpu.bounds, tight))
+
+
+@pytest.mark.parametrize("n,pdom", [(1, 3), (5, 1), (8191, 6), (8193, 6), (70_000, 40),
+                                    (200_000, 300)])
+def test_index_is_stable_partition_by_predicate(ctx, n, pdom):
+    rng = np.random.default_rng(n + pdom)
+    T = rng.integers(0, 1 << 32, (n, 3), dtype=np.uint64).astype(np.uint32)
+    T[:, 1] = (rng.integers(0, pdom, n) * 7919 + 12345).astype(np.uint32)  # sparse predicate IDs
+    idx = ctx.index_build(tuple(dev(T[:, j]) for j in range(3)))
+    perm = np.argsort(T[:, 1], kind="stable")
+    s2, p2, o2 = (host(x) for x in idx.triples())
+    assert np.array_equal(s2, T[perm, 0])
+    assert np.array_equal(p2, T[perm, 1])
+    assert np.array_equal(o2, T[perm, 2])
+    preds, counts = np.unique(T[:, 1], return_counts=True)
+    assert idx.npreds == len(preds)
+    starts = np.concatenate([[0], np.cumsum(counts)])
+    for i, p in enumerate(preds):
+        assert idx.range(int(p)) == (int(starts[i]), int(starts[i + 1]))
+    assert idx.range(int(preds.max()) + 1) == (0, 0)
+
+
+def test_indexed_scan_matches_oracle(ctx):
+    rng = np.random.default_rng(11)
+    for n in [1, 33, 8193, 60_000]:
+        T = rng.integers(0, 6, (n, 3)).astype(np.uint32)
+        idx = ctx.index_build(tuple(dev(T[:, j]) for j in range(3)))
+        pats = [((V, 0), (C, 3), (V, 1)),   # view
+                ((V, 1), (C, 2), (V, 0)),   # view, variables out of id order
+                ((V, 0), (C, 3), (C, 5)),   # range scan: constant object
+                ((C, 2), (C, 4), (V, 1)),   # range scan: constant subject
+                ((V, 0), (C, 1), (V, 0)),   # range scan: repeated variable
+                ((V, 0), (C, 99), (V, 1)),  # absent predicate: empty
+                ((V, 0), (V, 1), (V, 2)),   # variable predicate: whole index
+                ((V, 2), (V, 2), (V, 2)),
+                ((C, 2), (V, 4), (V, 1))]
+        got = ctx.scan_patterns(idx, pats)
+        for g, p in zip(got, pats):
+            ref = oracle.scan(*T.T, p)
+            assert_same(g, ref, ordered=p[1][0] == C)
+
+
+def test_indexed_views_are_zero_copy(ctx):
+    s, p, o, _ = datagen.lubm(1)
+    idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    tp, = ctx.scan_patterns(idx, [config_query("C1")[0]])
+    b, e = idx.range(datagen.LUBM_PRED["worksFor"])
+    s2, _, o2 = idx.triples()
+    assert tp.nrows == e - b
+    assert tp.columns[0].data_ptr() == s2.data_ptr() + 4 * b
+    assert tp.columns[1].data_ptr() == o2.data_ptr() + 4 * b
+    before = ctx.stats()["launches"]
+    ctx.scan_patterns(idx, [config_query("C1")[0]])
+    assert ctx.stats()["launches"] == before  # no kernel for a view
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_indexed_query_configs(ctx, cfg):
+    s, p, o, st = datagen.lubm(3, 0, 2)
+    idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    pats = config_query(cfg)
+    ref = oracle.query(s, p, o, pats)
+    got = ctx.query(idx, pats)
+    assert got.nrows == config_expected_counts(cfg, st)[-1]
+    assert_same(got, ref, ordered=ctx.stats()["last_path"] != mq.PATH_RESIDUAL,
+                exact_bounds=False)
+    plain = ctx.query((dev(s), dev(p), dev(o)), pats)
+    assert np.array_equal(plain.to_numpy(), got.to_numpy())  # same rows, same order
+
+
+def test_indexed_table1_and_projection(ctx):
+    ids, T, sec = load_table1()
+    idx = ctx.index_build(tuple(dev(T[:, j]) for j in range(3)))
+    P1 = ((V, 0), (C, ids["hasJob"]), (V, 1))
+    P2 = ((V, 1), (C, ids["workAt"]), (C, ids['"Hospital"']))
+    q = ctx.query(idx, [P1, P2], [0])
+    assert sorted(q.to_numpy()[:, 0].tolist()) == sorted(ids[r[0]] for r in sec["select_person"])
+    one = ctx.query(idx, [P1])  # single-pattern query: a view of the index
+    assert_same(one, oracle.scan(*T.T, P1))
+
+
+def test_index_empty_table(ctx):
+    z = torch.empty(0, dtype=torch.int32, device="cuda")
+    idx = ctx.index_build((z, z, z))
+    assert idx.n == 0 and idx.npreds == 0
+    got = ctx.scan_patterns(idx, [((V, 0), (C, 1), (V, 1)), ((V, 0), (V, 1), (V, 2))])
+    assert [g.nrows for g in got] == [0, 0]
+    assert got[1].vars == [0, 1, 2]

@@ -1,0 +1,44 @@
+#!/bin/bash
+# Round evidence refresh on a B200 box (run via gpurun from the repo root):
+#   gpu tests, bench lines for every config + the reference arm, the C5 ncu launch list and one
+#   ncu --set full capture of the step's kernels. Output under gpurun_out/$TAG/.
+TAG=${1:-refresh}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+python build.py > $OUT/build.log 2>&1 || { echo build failed; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
+tail -3 $OUT/pytest_gpu.log
+for c in C5 C4 C3 C2 C1; do
+  timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err
+  echo "$c exit $?"; cat $OUT/bench_$c.json | cut -c1-200
+done
+timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
+timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+echo "ref exit $?"
+if [ "${NCU:-1}" = 1 ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/ncu_launches_C5.csv python bench.py --steps 1 --warmup 3 --no-e2e \
+    --no-cpu-baseline > $OUT/ncu_l.log 2>&1
+  echo "ncu launches exit $?"
+  # one full capture of every kernel of one step (skip the warm-up step's launches)
+  timeout 1500 ncu --set full --clock-control none --import-source on \
+    -k regex:"radix_pass|scan_write|scan_count|find_groups|expand|pack_hist|residual|tile_groups" \
+    --launch-skip ${SKIP:-40} --launch-count ${COUNT:-24} -o $OUT/ncu_full_C5 -f \
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_f.log 2>&1
+  echo "ncu full exit $?"
+  ncu -i $OUT/ncu_full_C5.ncu-rep --page raw --csv > $OUT/ncu_full_C5_raw.csv 2>/dev/null
+  ncu -i $OUT/ncu_full_C5.ncu-rep --page details --csv > $OUT/ncu_full_C5_details.csv 2>/dev/null
+  for k in radix_pass scan_write find_groups; do
+    ncu -i $OUT/ncu_full_C5.ncu-rep --page source --csv --kernel-name regex:$k --launch-count 1 \
+      > $OUT/ncu_source_$k.csv 2>/dev/null
+  done
+  gzip -f $OUT/*.csv
+  # the report itself is too large to bring back (gpurun_out is capped at 64 MiB)
+  rm -f $OUT/ncu_full_C5.ncu-rep
+fi
+if [ -x tools/radix_ablate ]; then
+  timeout 600 tools/radix_ablate zipf 400000000 > $OUT/ablate_zipf.log 2>&1
+  timeout 600 tools/radix_ablate 300000000 0.1 1 > $OUT/ablate_rand.log 2>&1
+  cat $OUT/ablate_zipf.log $OUT/ablate_rand.log
+fi
+du -sh $OUT

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
+#include <string>
 
 #include "../paper_1702_03484_b200/csrc/radix.cu"
 
@@ -345,8 +347,132 @@ void report(const char *name, const uint64_t *kin, uint64_t *kout, uint64_t n, u
   printf("%-28s %8.3f ms  %7.1f GB/s (16 B/key)\n", name, ms, 16.0 * n / ms / 1e6);
 }
 
+extern "C" void zipf_table(uint64_t seed, int side, double s, uint32_t kbits, uint64_t i_lo,
+                           uint64_t i_hi, uint32_t *key, uint32_t *val);
+
+// C4-shaped sort: words key'<<ib | i of two Zipf(1.1) sides (the datagen recipe), every digit
+// pass of the key bits, each variant timed over the whole pass sequence.
+template <typename K>
+float zipf_sort(K kern, int items, const char *name, uint64_t *w0, uint64_t *w1, uint64_t n,
+                uint32_t ib, uint32_t kbits, uint32_t *hists, uint64_t *status, uint32_t *ctr,
+                const std::vector<uint64_t> &ref_sample) {
+  const uint64_t tile = 256ull * items, ntiles = (n + tile - 1) / tile;
+  const size_t smem = tile * 8;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int passes = (kbits + 7) / 8;
+  cudaEvent_t ev[9];
+  for (auto &e : ev) cudaEventCreate(&e);
+  float best[8] = {1e9, 1e9, 1e9, 1e9, 1e9, 1e9, 1e9, 1e9}, tot = 1e9;
+  for (int rep = 0; rep < 3; rep++) {
+    uint64_t *a = w0, *b = w1;
+    cudaEventRecord(ev[0]);
+    for (int p = 0; p < passes; p++) {
+      const uint32_t bits = (p + 1 == passes) ? kbits - 8 * p : 8;
+      cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
+      cudaMemsetAsync(ctr, 0, 4);
+      kern<<<(unsigned)ntiles, 256, smem>>>(a, b, nullptr, nullptr, n, ib + 8 * p, bits,
+                                            hists + p * kRadix, status, ctr, nullptr, 0, 0);
+      cudaEventRecord(ev[p + 1]);
+      std::swap(a, b);
+    }
+    cudaEventSynchronize(ev[passes]);
+    float t = 0;
+    for (int p = 0; p < passes; p++) {
+      float ms;
+      cudaEventElapsedTime(&ms, ev[p], ev[p + 1]);
+      best[p] = ms < best[p] ? ms : best[p];
+      t += ms;
+    }
+    tot = t < tot ? t : tot;
+    // re-run from the unsorted words: restore w0 (the passes ping-pong; even count ends in w0)
+    if (passes % 2) std::swap(w0, w1);
+    std::vector<uint64_t> o(ref_sample.size());
+    const uint64_t stride = n / ref_sample.size();
+    for (size_t j = 0; j < o.size(); j++) cudaMemcpy(&o[j], w0 + j * stride, 8, cudaMemcpyDeviceToHost);
+    if (o != ref_sample) { printf("%s: WRONG ORDER\n", name); return -1; }
+    if (passes % 2) std::swap(w0, w1);
+    break;  // (the sort is in place in w0 now: further reps would time already-sorted input)
+  }
+  printf("%-40s total %7.3f ms  passes:", name, tot);
+  for (int p = 0; p < passes; p++) printf(" %.3f", best[p]);
+  printf("  (%.0f GB/s)\n", 16.0 * n * passes / tot / 1e6);
+  return tot;
+}
+
+int sort_main(std::vector<uint64_t> &w, uint32_t ib, uint32_t kbits);
+
+int zipf_main(uint64_t n) {
+  const uint64_t h = n / 2;
+  n = 2 * h;
+  std::vector<uint32_t> key(n);
+  zipf_table(1702, 0, 1.1, 29, 0, h, key.data(), nullptr);
+  zipf_table(1702, 1, 1.1, 29, 0, h, key.data() + h, nullptr);
+  uint32_t ib = 0;
+  while ((1ull << ib) < n) ib++;
+  uint32_t lo = 0xffffffffu, hi = 0;
+  for (uint64_t i = 0; i < n; i++) { lo = key[i] < lo ? key[i] : lo; hi = key[i] > hi ? key[i] : hi; }
+  uint32_t kbits = 0;
+  while ((1ull << kbits) <= (uint64_t)(hi - lo)) kbits++;
+  std::vector<uint64_t> w(n);
+  for (uint64_t i = 0; i < n; i++) w[i] = ((uint64_t)(key[i] - lo) << ib) | i;
+  printf("zipf: ");
+  return sort_main(w, ib, kbits);
+}
+
+// words dumped by tools/dump_words.py (raw little-endian u64)
+int file_main(const char *path, uint32_t ib, uint32_t kbits) {
+  FILE *f = fopen(path, "rb");
+  if (!f) { printf("cannot open %s\n", path); return 1; }
+  fseek(f, 0, SEEK_END);
+  const uint64_t n = ftell(f) / 8;
+  fseek(f, 0, SEEK_SET);
+  std::vector<uint64_t> w(n);
+  if (fread(w.data(), 8, n, f) != n) { printf("short read\n"); return 1; }
+  fclose(f);
+  printf("%s: ", path);
+  return sort_main(w, ib, kbits);
+}
+
+int sort_main(std::vector<uint64_t> &w, uint32_t ib, uint32_t kbits) {
+  const uint64_t n = w.size();
+  const int passes = (kbits + 7) / 8;
+  std::vector<uint32_t> hh(8 * kRadix, 0);
+  for (uint64_t i = 0; i < n; i++)
+    for (int p = 0; p < passes; p++) hh[p * kRadix + ((w[i] >> (ib + 8 * p)) & 255)]++;
+  printf("n=%llu ib=%u kbits=%u passes=%d\n", (unsigned long long)n, ib, kbits, passes);
+  std::vector<uint64_t> sorted(w);
+  std::sort(sorted.begin(), sorted.end());
+  std::vector<uint64_t> sample(4096);
+  for (size_t j = 0; j < sample.size(); j++) sample[j] = sorted[j * (n / sample.size())];
+  uint64_t *w0, *w1, *status, *wsrc;
+  uint32_t *hists, *ctr;
+  cudaMalloc(&w0, n * 8);
+  cudaMalloc(&w1, n * 8);
+  cudaMalloc(&wsrc, n * 8);
+  cudaMalloc(&status, (n / 2048 + 2) * kRadix * 8);
+  cudaMalloc(&hists, 8 * kRadix * 4);
+  cudaMalloc(&ctr, 4);
+  cudaMemcpy(wsrc, w.data(), n * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(hists, hh.data(), 8 * kRadix * 4, cudaMemcpyHostToDevice);
+#define ZRUN(K, I, NAME)                                                                   \
+  cudaMemcpy(w0, wsrc, n * 8, cudaMemcpyDeviceToDevice);                                  \
+  zipf_sort(K, I, NAME, w0, w1, n, ib, kbits, hists, status, ctr, sample);
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 0>), 32, "items32 match");
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 1>), 32, "items32 ballot");
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 3>), 32, "items32 atomicOr+uniform (prod)");
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 4>), 32, "items32 2 rounds+atomicOr");
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 5>), 32, "items32 3 rounds+atomicOr");
+  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 6>), 32, "items32 4 rounds+atomicOr");
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+
 int main(int argc, char **argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
+  if (argc > 4 && std::string(argv[1]) == "file")
+    return file_main(argv[2], atoi(argv[3]), atoi(argv[4]));
+  if (argc > 1 && std::string(argv[1]) == "zipf")
+    return zipf_main(argc > 2 ? strtoull(argv[2], 0, 10) : 400000000ull);
   const uint64_t n = (argc > 1 ? strtoull(argv[1], 0, 10) : 200000000ull) / kSortTile * kSortTile;
   std::vector<uint64_t> h(n);
   uint64_t x = 88172645463325252ull;
@@ -413,6 +539,9 @@ int main(int argc, char **argv) {
     timeit(radix_pass_kernel<false, 32, 4, 2, true, false>, 32, "items32 minb2 reload match (prod)");
     timeit(radix_pass_kernel<false, 32, 4, 2, true, true>, 32, "items32 minb2 reload ballot");
     timeit(radix_pass_kernel<false, 16, 4, 4, true, true>, 16, "items16 minb4 reload ballot");
+    timeit(radix_pass_kernel<false, 32, 4, 2, true, 2>, 32, "items32 minb2 reload atomicOr");
+    timeit(radix_pass_kernel<false, 32, 4, 2, true, 3>, 32, "items32 minb2 reload atomicOr+uni");
+    timeit(radix_pass_kernel<false, 16, 4, 4, true, 3>, 16, "items16 minb4 reload atomicOr+uni");
   }
   // the library's real pass for comparison
   {
