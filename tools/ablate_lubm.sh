@@ -1,3 +1,4 @@
+# digit-pass ablation on real join words (C5 at LUBM(2000)) and the C4-shaped Zipf sort; run via gpurun
 mkdir -p gpurun_out/q2
 python build.py > gpurun_out/q2/build.log 2>&1 || exit 1
 timeout 900 python -m pytest tests/test_gpu_index.py -x -q 2>&1 | tail -3
