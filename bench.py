@@ -196,6 +196,8 @@ def run_gpu(args):
     if args.univ:
         nu = args.univ
     ctx = mq.Context(local)
+    ctx.set_option(mq.OPT_SEMIJOIN, {"auto": mq.SEMIJOIN_AUTO, "on": mq.SEMIJOIN_ON,
+                                     "off": mq.SEMIJOIN_OFF}[args.semijoin])
     index_build_ms = None
     stream = torch.cuda.current_stream()
     t_gen = time.perf_counter()
@@ -299,6 +301,7 @@ def run_gpu(args):
                        "store": ("pos-index (mapsq_query_indexed; built once at load in "
                                  f"{index_build_ms:.0f} ms)" if kind != "zipf" and args.store == "index"
                                  else "triple table scan (mapsq_query)") if kind != "zipf" else None,
+                       "semijoin_filter": args.semijoin,
                        "join_tuples_per_step": tuples // args.steps,
                        "result_rows": m_final},
             "hbm": {"algo_bytes_per_step": algo_bytes // args.steps, "gbs": hbm_gbs,
@@ -417,6 +420,9 @@ def main():
     ap.add_argument("--store", default="index", choices=["index", "scan"],
                     help="LUBM configs: answer patterns from the predicate-range index (default) "
                          "or scan the whole triple table every step")
+    ap.add_argument("--semijoin", default="auto", choices=["auto", "on", "off"],
+                    help="semi-join key-presence filter in front of the Map (auto: joins of "
+                         ">= 2^20 rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

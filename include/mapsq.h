@@ -141,6 +141,8 @@ typedef struct {
   uint64_t scanned_triples;
   uint64_t joins, scans;
   uint64_t last_kb, last_ib, last_passes, last_path;
+  uint64_t last_groups;    /* groups (keys on both sides) of the last join */
+  uint64_t last_filtered;  /* rows the semi-join filter dropped in the last join */
   uint32_t nkernels;
   mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
 } mapsq_stats;
@@ -299,6 +301,14 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
 #define MAPSQ_OPT_WIDE_KEY 1      /* how a join whose full key does not fit 64 - ib bits runs: */
 #define MAPSQ_WIDE_KEY_RESIDUAL 0 /*   packed widest columns + residual check (default) */
 #define MAPSQ_WIDE_KEY_KV 1       /*   (u64 key, u32 rowid) pair sort over every key bit */
+/* Semi-join filter in front of the Map (SURVEY §8 row f2's reducer): rows whose packed key is
+ * absent from the other side produce nothing in ReduceDuplicate and
+ * are dropped before the sort; RS and its row order are unchanged.  Costs one extra read of the
+ * key columns, two key-presence bitmaps (<= 64 MB each) and one more blocking read per join. */
+#define MAPSQ_OPT_SEMIJOIN 2
+#define MAPSQ_SEMIJOIN_OFF 0
+#define MAPSQ_SEMIJOIN_AUTO 1     /*   default: joins with n1 + n2 >= 2^20 rows (P64 / RESIDUAL) */
+#define MAPSQ_SEMIJOIN_ON 2       /*   every P64 / RESIDUAL join */
 mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value);
 
 /* ---- statistics ---- */

@@ -22,6 +22,7 @@ MAX_PATTERNS = 16
 TABLE_BOUNDS = 1
 PATH_P64, PATH_KV, PATH_RESIDUAL = 0, 1, 2
 OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV = 1, 0, 1
+OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_UNSUPPORTED"}
 
@@ -73,6 +74,7 @@ class _Stats(ctypes.Structure):
                 ("joins", ctypes.c_uint64), ("scans", ctypes.c_uint64),
                 ("last_kb", ctypes.c_uint64), ("last_ib", ctypes.c_uint64),
                 ("last_passes", ctypes.c_uint64), ("last_path", ctypes.c_uint64),
+                ("last_groups", ctypes.c_uint64), ("last_filtered", ctypes.c_uint64),
                 ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
 
 

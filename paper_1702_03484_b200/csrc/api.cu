@@ -421,6 +421,7 @@ PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_
   pa.n1 = pl.n1;
   pa.n2 = pl.n2;
   pa.ib = pl.ib;
+  pa.kb = pl.kb;
   pa.kv = pl.path == MAPSQ_PATH_KV;
   pa.bit_lo = pa.kv ? 0 : pl.ib;
   // the Map kernel counts only the first digit; each digit pass counts the next one (measured
@@ -448,6 +449,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   ctx->counters.last_ib = pl.ib;
   ctx->counters.last_passes = pl.passes;
   ctx->counters.last_path = pl.path;
+  ctx->counters.last_groups = 0;
+  ctx->counters.last_filtered = 0;
   if (n1 == 0 || n2 == 0 || pl.disjoint) {
     fill_empty_join(pl, &a, &b, rs);
     return MAPSQ_OK;
@@ -464,9 +467,54 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     NEED(va);
     NEED(vb);
   }
-  // ---- Map (row a3) + upfront histograms
+  // ---- Map (row a3) + first-digit histogram; optionally behind the semi-join filter
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
-  {
+  uint64_t nw = n;  // words entering the sort
+  const bool filt = !kv && pl.kb > 0 &&
+                    (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
+                     (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
+  if (filt) {
+    const PackArgs pa = pack_args(pl, &a, &b);
+    const uint32_t bbits = std::min<uint32_t>(pl.kb, kSemijoinBits);
+    const uint32_t hashed = pl.kb > bbits;
+    const uint64_t bmw = std::max<uint64_t>(1, (1ull << bbits) / 32);
+    const uint64_t nsl = filter_slices(n1, n2);
+    uint32_t *bm = sc.get<uint32_t>(2 * bmw);
+    uint32_t *fmask = sc.get<uint32_t>(filter_mask_words(n1, n2));
+    uint32_t *fcnt = sc.get<uint32_t>(nsl);
+    uint64_t *foff = sc.get<uint64_t>(nsl);
+    uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
+    uint64_t *fsc = sc.get<uint64_t>(1);  // surviving words
+    NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
+    CK(cudaMemsetAsync(bm, 0, 2 * bmw * sizeof(uint32_t), s));
+    {
+      KTimer kt(ctx, s, "filter", 2ull * 4 * pa.nkey * std::min(n1, n2) +
+                                      4ull * pa.nkey * std::max(n1, n2) + 16ull * bmw + n / 8,
+                3);
+      launch_filter(pa, bm, bm + bmw, bbits, hashed, fmask, fcnt, s);
+      CKL("filter");
+    }
+    {
+      KTimer kt(ctx, s, "filter_scan", 12ull * nsl, 3);
+      launch_exclusive_scan_u32(fcnt, foff, nsl, ftmp, fsc, s);
+      CKL("filter_scan");
+    }
+    {
+      KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * nsl);
+      launch_filter_emit(pa, fmask, fcnt, foff, wa, hist, s);
+      CKL("filter_emit");
+      TRY(ensure_pinned(ctx, 1));
+      CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));  // the surviving word count sizes the sort
+      nw = ctx->pinned[0];
+      kt.t.bytes += (4ull * pa.nkey + 8ull) * nw;
+    }
+    ctx->counters.last_filtered = n - nw;
+    if (nw == 0) {
+      fill_empty_join(pl, &a, &b, rs);
+      return MAPSQ_OK;
+    }
+  } else {
     const PackArgs pa = pack_args(pl, &a, &b);
     KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
     launch_pack_hist(pa, wa, va, hist, s);
@@ -474,7 +522,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   // ---- Sort (row a4)
   int which = 0;
-  TRY(radix_sort(ctx, wa, wb, va, vb, n, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
+  TRY(radix_sort(ctx, wa, wb, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
   uint64_t *words = which ? wb : wa;
   uint32_t *vals = kv ? (which ? vb : va) : nullptr;
   sc.release(which ? wa : wb);
@@ -483,7 +531,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   const uint64_t cap = std::min(n1, n2);
   uint32_t *gs = sc.get<uint32_t>(cap), *gp = sc.get<uint32_t>(cap), *ge = sc.get<uint32_t>(cap);
   uint64_t *gc = sc.get<uint64_t>(cap), *go = sc.get<uint64_t>(cap);
-  const uint64_t gtiles = find_groups_tiles(n);
+  const uint64_t gtiles = find_groups_tiles(nw);
   uint64_t *gstatus = sc.get<uint64_t>(gtiles);
   uint64_t *scal = sc.get<uint64_t>(4);  // [0] ngroups, [1] |RS|, [2] tile counter
   uint64_t *tmp = sc.get<uint64_t>(scan_tmp_words(cap));
@@ -491,9 +539,9 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   CK(cudaMemsetAsync(gstatus, 0, gtiles * sizeof(uint64_t), s));
   CK(cudaMemsetAsync(scal, 0, 4 * sizeof(uint64_t), s));
   {
-    KTimer kt(ctx, s, "find_groups", n * 8ull);
+    KTimer kt(ctx, s, "find_groups", nw * 8ull);
     GroupOut g{gs, gp, ge, gc};
-    launch_find_groups(kv ? nullptr : words, kv ? words : nullptr, vals, n, n1, pl.ib, g,
+    launch_find_groups(kv ? nullptr : words, kv ? words : nullptr, vals, nw, n1, pl.ib, g,
                        gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
     CKL("find_groups");
   }
@@ -516,7 +564,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
         ra.res2[ra.nres] = b.col[pl.key_col2[c]];
         ra.nres++;
       }
-    KTimer kt(ctx, s, "residual_count", 8ull * n);
+    KTimer kt(ctx, s, "residual_count", 8ull * nw);
     launch_residual_count(ra, cap, gc, pmask, s);  // exact pair counts replace nL * nR
     CKL("residual_count");
   }
@@ -529,6 +577,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   CK(cudaMemcpyAsync(ctx->pinned, scal, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));  // the one blocking read: |RS| sizes the output
   const uint64_t ngroups = ctx->pinned[0], m = ctx->pinned[1];
+  ctx->counters.last_groups = ngroups;
   if (residual) {
     fill_empty_join(pl, &a, &b, rs);
     TRY(alloc_table(ctx, rs, m, pl.out_ncols, s));
@@ -591,7 +640,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     for (uint32_t c = 0; c < pl.out_ncols; c++) ea.out[c] = rs->col[c];
     ea.tile_g0 = sc.get<uint64_t>(expand_tiles(m) + 1);
     NEED(ea.tile_g0);
-    const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * n +
+    const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * nw +
                            4ull * (n1 * pl.nrest1 + n2 * pl.nrest2);
     KTimer kt(ctx, s, "expand", bytes, 2);
     launch_expand(ea, s);
@@ -1549,6 +1598,10 @@ MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t valu
   if (!ctx) return MAPSQ_E_INVALID;
   if (option == MAPSQ_OPT_WIDE_KEY && (value == MAPSQ_WIDE_KEY_RESIDUAL || value == MAPSQ_WIDE_KEY_KV)) {
     ctx->wide_key_mode = (int)value;
+    return MAPSQ_OK;
+  }
+  if (option == MAPSQ_OPT_SEMIJOIN && value >= MAPSQ_SEMIJOIN_OFF && value <= MAPSQ_SEMIJOIN_ON) {
+    ctx->semijoin = (int)value;
     return MAPSQ_OK;
   }
   return set_error(ctx, MAPSQ_E_INVALID, "unknown option or value");

@@ -1,0 +1,255 @@
+// filter.cu — semi-join key-presence filter in front of the Map (SURVEY §8 row f2's semi-join
+// reducer, applied on one GPU as well).
+//
+// ReduceDuplicate emits nothing for a key that occurs on one side only (Alg. 1 l.6-11,
+// PAPER.md:127-133; the LEFT/RIGHT flag exists "to reduce unnecessary computation"), so
+// such rows can be dropped before the sort without changing RS.  Key-presence bitmaps over the
+// packed key key' (exact when kb <= bbits, else indexed by a multiplicative hash of key' —
+// false positives only let rows through, they never drop a match) are built in three passes:
+//   1. build:  bm_S = keys of the smaller side S;
+//   2. probe L (the larger side) against bm_S; every surviving L row also sets its bit in bm_L
+//      (so bm_L holds exactly the keys of L that occur in S);
+//   3. probe S against bm_L.
+// Each probe records one survivor bit per row and a count per 512-row warp slice (side A's rows
+// fill slices [0, nslA), side B's the slices after), the counts are scanned, and an emit pass
+// writes each slice's survivors at its offset in row order.  The compaction is stable, so the
+// surviving words keep ascending row ids and the sort's (key', label, rowid) order — and
+// therefore RS and its row order — are exactly those of the unfiltered join.
+#include <type_traits>
+
+#include "internal.cuh"
+
+namespace mapsq {
+namespace {
+
+constexpr int kFThreads = 256;
+constexpr int kFWarps = kFThreads / 32;
+constexpr int kFItems = 16;                    // rows per lane per slice
+constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
+constexpr int kFCopies = 4;                    // private digit-histogram copies
+
+// FAST: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic) — every
+// config's joins; otherwise the generic 64-bit composite key.
+template <bool FAST>
+using KeyT = typename std::conditional<FAST, uint32_t, uint64_t>::type;
+
+__device__ __forceinline__ uint32_t bit_index(uint64_t key, uint32_t bbits, uint32_t hashed) {
+  return hashed ? (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bbits)) : (uint32_t)key;
+}
+
+// One side of the join as the filter kernels see it: rows j in [0, rows), key column c at
+// col[c][j], row id (in the word) j + id0, slices starting at slice0.
+struct Side {
+  const uint32_t *col[MAPSQ_MAX_COLS];
+  uint64_t rows, id0, slice0;
+};
+
+// key' of rows base + it * 32 + lane (it < kFItems), column-outer loads (all of a column's
+// loads in flight together); rows >= rows get key' 0 (callers mask them)
+template <bool FAST>
+__device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
+                                          uint32_t lane, KeyT<FAST> key[kFItems]) {
+#pragma unroll
+  for (int it = 0; it < kFItems; it++) key[it] = 0;
+  const uint32_t nk = FAST ? 1u : a.nkey;
+  for (uint32_t c = 0; c < nk; c++) {
+    const uint32_t *p = sd.col[c];
+    const uint32_t lo = a.lo[c], sh = a.shift[c];
+    uint32_t v[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      v[it] = j < sd.rows ? __ldcs(p + j) : lo;
+    }
+#pragma unroll
+    for (int it = 0; it < kFItems; it++)
+      key[it] = FAST ? (KeyT<FAST>)(v[it] - lo)
+                     : (KeyT<FAST>)(key[it] | (uint64_t)(v[it] - lo) << sh);
+  }
+}
+
+// Set bit(key') in bm for the rows whose `keep` bit is set.  Test before set (a plain atomicOr
+// per row serialises on hot keys: 40 ms vs 5.9 ms for 5e8 Zipf rows, tools/bitmap_bench.cu), and
+// runs of equal keys in consecutive rows (clustered data) set their bit once: a lane whose left
+// neighbour holds the same bit skips.
+__device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFItems],
+                                         uint32_t keep, uint32_t lane) {
+  uint32_t word[kFItems];
+#pragma unroll
+  for (int it = 0; it < kFItems; it++)  // (read-only path: a stale word costs one more atomic)
+    word[it] = (keep >> it & 1u) ? __ldg(bm + (bidx[it] >> 5)) : 0xffffffffu;
+#pragma unroll
+  for (int it = 0; it < kFItems; it++) {
+    const uint32_t b = bidx[it];
+    const uint32_t k = keep >> it & 1u;
+    const uint32_t bp = __shfl_up_sync(0xffffffffu, b, 1);
+    const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    const bool dup = lane > 0 && kp && bp == b;
+    if (k && !dup && !(word[it] >> (b & 31) & 1u)) atomicOr(bm + (b >> 5), 1u << (b & 31));
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(kFThreads)
+filter_build_kernel(const PackArgs a, const Side sd, uint32_t *__restrict__ bm, uint32_t bbits,
+                    uint32_t hashed) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<FAST> key[kFItems];
+    load_keys<FAST>(a, sd, base, lane, key);
+    uint32_t bidx[kFItems], keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      bidx[it] = bit_index(key[it], bbits, hashed);
+      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+    }
+    set_bits(bm, bidx, keep, lane);
+  }
+}
+
+// Probe the side's rows against bm_probe: survivor bits -> mask[(slice0 + ws) * 16 ..], counts
+// -> cnt[slice0 + ws]; with SET the survivors also set their bit in bm_set.
+template <bool FAST, bool SET>
+__global__ void __launch_bounds__(kFThreads)
+filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm_probe,
+                    uint32_t *__restrict__ bm_set, uint32_t bbits, uint32_t hashed,
+                    uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<FAST> key[kFItems];
+    load_keys<FAST>(a, sd, base, lane, key);
+    uint32_t word[kFItems], bidx[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      bidx[it] = bit_index(key[it], bbits, hashed);
+      word[it] = j < sd.rows ? __ldg(bm_probe + (bidx[it] >> 5)) : 0u;
+    }
+    uint32_t my = 0, c = 0, keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const bool k = word[it] >> (bidx[it] & 31) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      keep |= (uint32_t)k << it;
+      if (lane == (uint32_t)it) my = bal;
+      c += __popc(bal);
+    }
+    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
+    if (lane == 0) cnt[sd.slice0 + ws] = c;
+    if (SET && c) set_bits(bm_set, bidx, keep, lane);
+  }
+}
+
+// Emit: the survivors of slice s go to words[off[s] ..] in row order (stable), as
+// key' << ib | row id; digit 0 of the survivors is counted into hist.
+template <bool FAST>
+__global__ void __launch_bounds__(kFThreads)
+filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
+                   const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
+                   const uint64_t *__restrict__ off, uint64_t *__restrict__ words,
+                   uint32_t *__restrict__ hist) {
+  __shared__ uint32_t s_h[kFCopies][kRadix];
+  for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  const uint64_t nslices = sb.slice0 + ceil_div(sb.rows, kFWarpRows);
+  const uint32_t nk = FAST ? 1u : a.nkey;
+  for (uint64_t s = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); s < nslices;
+       s += nwarps) {
+    if (__ldg(cnt + s) == 0) continue;  // warp-uniform
+    const bool is_b = s >= sb.slice0;
+    const Side &sd = is_b ? sb : sa;
+    const uint64_t base = (s - sd.slice0) * kFWarpRows;
+    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + s * kFItems + lane) : 0u;
+    uint64_t pos = __ldg(off + s);
+#pragma unroll 4
+    for (int it = 0; it < kFItems; it++) {
+      const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
+      if (!bal) continue;
+      if (bal >> lane & 1u) {
+        const uint64_t j = base + (uint64_t)it * 32 + lane;
+        uint64_t key = 0;
+        for (uint32_t c = 0; c < nk; c++) {
+          const uint32_t v = __ldg(sd.col[c] + j) - a.lo[c];
+          key |= FAST ? (uint64_t)v : (uint64_t)v << a.shift[c];
+        }
+        const uint64_t w = (key << a.ib) | (j + sd.id0);
+        __stcs(words + pos + __popc(bal & lt), w);
+        if (a.passes) atomicAdd(h + ((uint32_t)(w >> a.bit_lo) & a.last_mask), 1u);
+      }
+      pos += __popc(bal);
+    }
+  }
+  __syncthreads();
+  if (a.passes)
+    for (uint32_t d = threadIdx.x; d < kRadix; d += kFThreads) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int q = 0; q < kFCopies; q++) c += s_h[q][d];
+      if (c) atomicAdd(hist + d, c);
+    }
+}
+
+Side side_of(const PackArgs &a, bool b) {
+  Side sd;
+  for (uint32_t c = 0; c < MAPSQ_MAX_COLS; c++)
+    sd.col[c] = c < a.nkey ? (b ? a.key2[c] : a.key1[c]) : nullptr;
+  sd.rows = b ? a.n2 : a.n1;
+  sd.id0 = b ? a.n1 : 0;
+  sd.slice0 = b ? ceil_div(a.n1, kFWarpRows) : 0;
+  return sd;
+}
+
+int grid_for_rows(uint64_t rows) {
+  const uint64_t blocks = ceil_div(ceil_div(rows, kFWarpRows), kFWarps);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148 * 8));
+}
+
+bool filter_fast(const PackArgs &a) { return a.nkey == 1 && a.kb <= 32; }
+
+}  // namespace
+
+uint64_t filter_slices(uint64_t n1, uint64_t n2) {
+  return ceil_div(n1, kFWarpRows) + ceil_div(n2, kFWarpRows);
+}
+uint64_t filter_mask_words(uint64_t n1, uint64_t n2) { return filter_slices(n1, n2) * kFItems; }
+
+void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
+                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
+  const bool b_small = a.n2 < a.n1;
+  const Side S = side_of(a, b_small), L = side_of(a, !b_small);
+  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
+  if (filter_fast(a)) {
+    filter_build_kernel<true><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
+    filter_probe_kernel<true, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed,
+                                                              mask, cnt);
+    filter_probe_kernel<true, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
+                                                               mask, cnt);
+  } else {
+    filter_build_kernel<false><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
+    filter_probe_kernel<false, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed,
+                                                               mask, cnt);
+    filter_probe_kernel<false, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits,
+                                                                hashed, mask, cnt);
+  }
+}
+
+void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
+                        const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s) {
+  const Side A = side_of(a, false), B = side_of(a, true);
+  const int g = grid_for_rows(a.n1 + a.n2);
+  if (filter_fast(a))
+    filter_emit_kernel<true><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist);
+  else
+    filter_emit_kernel<false><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist);
+}
+
+}  // namespace mapsq

@@ -49,6 +49,7 @@ struct mapsq_ctx {
   bool cuda_broken = false;
   bool profiling = false;
   int wide_key_mode = MAPSQ_WIDE_KEY_RESIDUAL;
+  int semijoin = MAPSQ_SEMIJOIN_AUTO;
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
   std::map<std::string, mapsq::KAgg> kagg;
@@ -270,6 +271,7 @@ struct PackArgs {
   uint32_t passes;
   uint32_t last_mask;  // digit mask of the last pass ((1 << bits) - 1)
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
+  uint32_t kb;       // packed key bits
 };
 // Map (K2): pack words (or KV pairs) and build the digit histograms of every pass.
 void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32_t *hist,
@@ -342,6 +344,20 @@ uint64_t find_groups_tiles(uint64_t n);
 
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,
                    cudaStream_t s);
+
+// Semi-join filter (filter.cu): per-side key-presence bitmaps of 2^bbits bits (bit = key' when
+// hashed == 0, else a multiplicative hash of key'), then the Map of the rows whose key is present
+// on the other side, compacted stably (probe -> scan of per-slice counts -> emit).
+constexpr uint64_t kSemijoinMinRows = 1ull << 20;  // AUTO: joins of at least this many rows
+constexpr uint32_t kSemijoinBits = 29;             // 2 x 64 MB bitmaps at most (L2-sized)
+uint64_t filter_slices(uint64_t n1, uint64_t n2);      // 512-row warp slices (per side)
+uint64_t filter_mask_words(uint64_t n1, uint64_t n2);  // survivor-bit words
+// build bmS from the smaller side, probe the larger (setting bmL for its survivors), probe the
+// smaller against bmL: survivor bits + per-slice counts
+void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
+                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s);
+void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
+                        const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s);
 
 // Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
 // (unordered, atomic slots < cap); per-run bounds [slo | olo | shi | ohi].

@@ -1,0 +1,110 @@
+// bitmap_bench.cu — developer micro-benchmark: cost of a key-presence bitmap (semi-join filter)
+// on B200: build (atomicOr per row, with/without test-before-set) and probe, for C4-shaped
+// Zipf keys.   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/bitmap_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+extern "C" void zipf_table(uint64_t seed, int side, double s, uint32_t kbits, uint64_t i_lo,
+                           uint64_t i_hi, uint32_t *key, uint32_t *val);
+
+__global__ void build_atomic(const uint32_t *k, uint64_t n, uint32_t *bm, uint32_t mask) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = __ldcs(k + i) & mask;
+    atomicOr(bm + (x >> 5), 1u << (x & 31));
+  }
+}
+__global__ void build_test(const uint32_t *k, uint64_t n, uint32_t *bm, uint32_t mask) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = __ldcs(k + i) & mask;
+    const uint32_t b = 1u << (x & 31);
+    if (!(__ldcg(bm + (x >> 5)) & b)) atomicOr(bm + (x >> 5), b);
+  }
+}
+__global__ void probe(const uint32_t *k, uint64_t n, const uint32_t *bm, uint32_t mask, unsigned long long *cnt) {
+  uint32_t c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = __ldcs(k + i) & mask;
+    c += (__ldcg(bm + (x >> 5)) >> (x & 31)) & 1u;
+  }
+  atomicAdd(cnt, (unsigned long long)c);
+}
+
+template <int ILP, bool NC>
+__global__ void probe_ilp(const uint32_t *k, uint64_t n, const uint32_t *bm, uint32_t mask, unsigned long long *cnt) {
+  uint32_t c = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * ILP;
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x) * ILP + threadIdx.x; i0 < n; i0 += stride) {
+    uint32_t x[ILP], w[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+      x[u] = i < n ? (__ldcs(k + i) & mask) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; u++) w[u] = NC ? __ldg(bm + (x[u] >> 5)) : __ldcg(bm + (x[u] >> 5));
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+      c += (i < n) & (w[u] >> (x[u] & 31));
+    }
+  }
+  atomicAdd(cnt, (unsigned long long)c);
+}
+
+int main(int argc, char **argv) {
+  const uint64_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 500000000ull;
+  std::vector<uint32_t> a(n), b(n);
+  zipf_table(1702, 0, 1.1, 29, 0, n, a.data(), nullptr);
+  zipf_table(1702, 1, 1.1, 29, 0, n, b.data(), nullptr);
+  uint32_t *da, *db, *bm;
+  unsigned long long *cnt;
+  cudaMalloc(&da, n * 4);
+  cudaMalloc(&db, n * 4);
+  cudaMalloc(&bm, (1u << 29) / 8);
+  cudaMalloc(&cnt, 8);
+  cudaMemcpy(da, a.data(), n * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, b.data(), n * 4, cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto t = [&](const char *name, auto f) {
+    float best = 1e9;
+    for (int r = 0; r < 3; r++) {
+      cudaMemset(bm, 0, (1u << 29) / 8);
+      cudaMemset(cnt, 0, 8);
+      cudaEventRecord(e0);
+      f();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    unsigned long long c = 0;
+    cudaMemcpy(&c, cnt, 8, cudaMemcpyDeviceToHost);
+    printf("%-36s %8.3f ms  (%.2f G rows/s) cnt=%llu %s\n", name, best, n / best / 1e6, c,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  const uint32_t mask = (1u << 29) - 1;
+  const int g = 148 * 16;
+  t("build atomicOr", [&] { build_atomic<<<g, 256>>>(da, n, bm, mask); });
+  t("build test+atomicOr", [&] { build_test<<<g, 256>>>(da, n, bm, mask); });
+  t("build test+atomicOr, then probe B", [&] {
+    build_test<<<g, 256>>>(da, n, bm, mask);
+    probe<<<g, 256>>>(db, n, bm, mask, cnt);
+  });
+  t("probe only (empty bitmap)", [&] { probe<<<g, 256>>>(db, n, bm, mask, cnt); });
+  for (uint32_t bits : {29u, 28u, 26u, 24u, 20u}) {
+    const uint32_t m = (1u << bits) - 1;
+    char name[64];
+    snprintf(name, sizeof name, "probe ilp16 cg 2^%u bits", bits);
+    t(name, [&] { probe_ilp<16, false><<<g, 256>>>(db, n, bm, m, cnt); });
+    snprintf(name, sizeof name, "probe ilp16 nc 2^%u bits", bits);
+    t(name, [&] { probe_ilp<16, true><<<g, 256>>>(db, n, bm, m, cnt); });
+    snprintf(name, sizeof name, "probe ilp4 nc 2^%u bits", bits);
+    t(name, [&] { probe_ilp<4, true><<<g, 256>>>(db, n, bm, m, cnt); });
+  }
+  return 0;
+}
