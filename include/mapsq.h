@@ -102,7 +102,12 @@ typedef struct mapsq_ctx mapsq_ctx;
  *   widest shared columns that fit (packed_mask bit c set for shared[c]) and the remaining
  *   "residual" shared columns are compared exactly inside each packed-key group during
  *   ReduceDuplicate; path KV (u64 key' + u32 rowid pairs, every shared column packed) is the
- *   alternative selected with MAPSQ_OPT_WIDE_KEY = MAPSQ_WIDE_KEY_KV. */
+ *   alternative selected with MAPSQ_OPT_WIDE_KEY = MAPSQ_WIDE_KEY_KV.
+ *   path HASH (the default for keys wider than 32 bits or than 64 - ib bits):
+ *   key' = the top kb = min(32, 64 - ib) bits of a 64-bit mix of the raw values of EVERY shared
+ *   column (packed_mask = 0); equal keys share key', and ReduceDuplicate compares all shared
+ *   columns of every (LEFT, RIGHT) pair of a key' group, so hash collisions never produce a
+ *   wrong row.  Output rows are grouped by key' (not in key order). */
 typedef struct {
   uint64_t n1, n2;
   uint32_t nshared;
@@ -123,6 +128,7 @@ typedef struct {
 #define MAPSQ_PATH_P64 0u
 #define MAPSQ_PATH_KV 1u
 #define MAPSQ_PATH_RESIDUAL 2u
+#define MAPSQ_PATH_HASH 3u
 #define MAPSQ_RADIX_BITS 8u
 
 /* Per-kernel timing (recorded with CUDA events on the launching stream while profiling is on)
@@ -178,9 +184,12 @@ mapsq_status mapsq_scan_pattern(mapsq_ctx *ctx, const mapsq_triples *triples,
  * min/max pass (one more blocking read). */
 mapsq_status mapsq_join(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
                         mapsq_table *rs, void *stream);
-/* Host-only: the join spec for two tables that carry bounds (no device work). */
+/* Host-only: the join spec for two tables that carry bounds (no device work), for the default
+ * wide-key mode (mapsq_plan_join) or a given MAPSQ_WIDE_KEY_* mode. */
 mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table *tp2,
                              mapsq_join_plan *plan);
+mapsq_status mapsq_plan_join_mode(const mapsq_table *tp1, const mapsq_table *tp2, int wide_mode,
+                                  mapsq_join_plan *plan);
 
 /* ---- query (row a7) ----
  * Scan all patterns in one fused pass (mapsq_scan_patterns), fold the joins left-deep in the
@@ -299,8 +308,9 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
 
 /* ---- options ---- */
 #define MAPSQ_OPT_WIDE_KEY 1      /* how a join whose full key does not fit 64 - ib bits runs: */
-#define MAPSQ_WIDE_KEY_RESIDUAL 0 /*   packed widest columns + residual check (default) */
+#define MAPSQ_WIDE_KEY_RESIDUAL 0 /*   packed widest columns + residual check */
 #define MAPSQ_WIDE_KEY_KV 1       /*   (u64 key, u32 rowid) pair sort over every key bit */
+#define MAPSQ_WIDE_KEY_HASH 2     /*   hashed composite key + exact pair check (default) */
 /* Semi-join filter in front of the Map (SURVEY §8 row f2's reducer): rows whose packed key is
  * absent from the other side produce nothing in ReduceDuplicate and
  * are dropped before the sort; RS and its row order are unchanged.  Costs one extra read of the

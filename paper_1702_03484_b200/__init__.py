@@ -20,8 +20,8 @@ _LIB_PATH = os.path.join(_HERE, "libmapsq.so")
 MAX_COLS = 16
 MAX_PATTERNS = 16
 TABLE_BOUNDS = 1
-PATH_P64, PATH_KV, PATH_RESIDUAL = 0, 1, 2
-OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV = 1, 0, 1
+PATH_P64, PATH_KV, PATH_RESIDUAL, PATH_HASH = 0, 1, 2, 3
+OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_UNSUPPORTED"}
@@ -102,6 +102,7 @@ def lib():
             "mapsq_scan_pattern": (st, [vp, ctypes.POINTER(_Triples), PP, PT, vp]),
             "mapsq_join": (st, [vp, PT, PT, PT, vp]),
             "mapsq_plan_join": (st, [PT, PT, ctypes.POINTER(JoinPlan)]),
+            "mapsq_plan_join_mode": (st, [PT, PT, ctypes.c_int, ctypes.POINTER(JoinPlan)]),
             "mapsq_query": (st, [vp, ctypes.POINTER(_Triples), PP, ctypes.c_int,
                                  ctypes.POINTER(i32), ctypes.c_int, PT, vp]),
             "mapsq_query_host": (st, [vp, u64, vp, vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
@@ -538,8 +539,9 @@ def device_columns(ptr: int, nrows: int, ncols: int, stride: int, owner=None):
             for c in range(ncols)]
 
 
-def plan_join(vars1, bounds1, n1, vars2, bounds2, n2) -> JoinPlan:
-    """Host-only join spec (row a2) from two schemas with column bounds; no GPU needed."""
+def plan_join(vars1, bounds1, n1, vars2, bounds2, n2, wide_mode=None) -> JoinPlan:
+    """Host-only join spec (row a2) from two schemas with column bounds; no GPU needed.
+    wide_mode: None = the library default, else WIDE_KEY_RESIDUAL / _KV / _HASH."""
     t1, t2 = _Table(), _Table()
     for t, vs, bs, n in ((t1, vars1, bounds1, n1), (t2, vars2, bounds2, n2)):
         t.nrows, t.ncols, t.flags = n, len(vs), TABLE_BOUNDS
@@ -547,7 +549,11 @@ def plan_join(vars1, bounds1, n1, vars2, bounds2, n2) -> JoinPlan:
             t.var[c], t.lo[c], t.hi[c] = v, lo, hi
             t.col[c] = 16  # never dereferenced by the host-only planner
     plan = JoinPlan()
-    st = lib().mapsq_plan_join(ctypes.byref(t1), ctypes.byref(t2), ctypes.byref(plan))
+    if wide_mode is None:
+        st = lib().mapsq_plan_join(ctypes.byref(t1), ctypes.byref(t2), ctypes.byref(plan))
+    else:
+        st = lib().mapsq_plan_join_mode(ctypes.byref(t1), ctypes.byref(t2), int(wide_mode),
+                                        ctypes.byref(plan))
     if st:
         raise MapsqError(st, "plan_join")
     return plan

@@ -214,7 +214,7 @@ mapsq_status alloc_table(mapsq_ctx *ctx, mapsq_table *t, uint64_t rows, uint32_t
 
 // ------------------------------------------------------------------------------ join plan
 mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
-                       mapsq_join_plan *pl, int wide_mode = MAPSQ_WIDE_KEY_RESIDUAL) {
+                       mapsq_join_plan *pl, int wide_mode = MAPSQ_WIDE_KEY_HASH) {
   std::memset(pl, 0, sizeof *pl);
   TRY(check_table(ctx, a, "tp1"));
   TRY(check_table(ctx, b, "tp2"));
@@ -268,6 +268,16 @@ mapsq_status plan_join(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *
   const uint64_t n = a->nrows + b->nrows;
   pl->ib = n > 1 ? bits_for(n - 1) : 1;
   uint32_t packed = (ns >= 32) ? ~0u : ((1u << ns) - 1u);
+  if (wide_mode == MAPSQ_WIDE_KEY_HASH && (kb_all + pl->ib > 64 || kb_all > 32)) {
+    // HASH: key' = the top min(32, 64 - ib) bits of a 64-bit mix of every shared column (at most
+    // 4 digit passes however wide the key); ReduceDuplicate verifies each pair's columns
+    pl->path = MAPSQ_PATH_HASH;
+    pl->packed_mask = 0;
+    pl->kb = std::min<uint32_t>(32, 64 - pl->ib);
+    pl->passes = (pl->kb + MAPSQ_RADIX_BITS - 1) / MAPSQ_RADIX_BITS;
+    for (uint32_t c = 0; c < ns; c++) pl->key_shift[c] = 0;
+    return MAPSQ_OK;
+  }
   if (kb_all + pl->ib <= 64) {
     pl->path = MAPSQ_PATH_P64;
   } else if (wide_mode == MAPSQ_WIDE_KEY_KV) {
@@ -410,8 +420,9 @@ void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const maps
 PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b) {
   PackArgs pa;
   std::memset(&pa, 0, sizeof pa);
+  const bool hash = pl.path == MAPSQ_PATH_HASH;
   for (uint32_t c = 0; c < pl.nshared; c++) {
-    if (!(pl.packed_mask >> c & 1u)) continue;
+    if (!hash && !(pl.packed_mask >> c & 1u)) continue;
     pa.key1[pa.nkey] = a->col[pl.key_col1[c]];
     pa.key2[pa.nkey] = b->col[pl.key_col2[c]];
     pa.lo[pa.nkey] = pl.key_lo[c];
@@ -422,6 +433,7 @@ PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_
   pa.n2 = pl.n2;
   pa.ib = pl.ib;
   pa.kb = pl.kb;
+  pa.hash = hash;
   pa.kv = pl.path == MAPSQ_PATH_KV;
   pa.bit_lo = pa.kv ? 0 : pl.ib;
   // the Map kernel counts only the first digit; each digit pass counts the next one (measured
@@ -469,45 +481,108 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   // ---- Map (row a3) + first-digit histogram; optionally behind the semi-join filter
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
-  uint64_t nw = n;  // words entering the sort
+  uint64_t *cur = wa, *alt = wb;  // the words entering the sort are in cur
+  uint64_t nw = n;
   const bool filt = !kv && pl.kb > 0 &&
                     (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
                      (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
   if (filt) {
-    const PackArgs pa = pack_args(pl, &a, &b);
-    const uint32_t bbits = std::min<uint32_t>(pl.kb, kSemijoinBits);
-    const uint32_t hashed = pl.kb > bbits;
-    const uint64_t bmw = std::max<uint64_t>(1, (1ull << bbits) / 32);
-    const uint64_t nsl = filter_slices(n1, n2);
+    PackArgs pa = pack_args(pl, &a, &b);
+    const uint64_t nsl = n / 512 + 4;  // warp slices of any round (filter_slices <= this)
+    const uint64_t bmw = std::max<uint64_t>(1, (1ull << kSemijoinBits) / 32);
     uint32_t *bm = sc.get<uint32_t>(2 * bmw);
-    uint32_t *fmask = sc.get<uint32_t>(filter_mask_words(n1, n2));
+    uint32_t *fmask = sc.get<uint32_t>(nsl * 16);
     uint32_t *fcnt = sc.get<uint32_t>(nsl);
     uint64_t *foff = sc.get<uint64_t>(nsl);
     uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
-    uint64_t *fsc = sc.get<uint64_t>(1);  // surviving words
+    uint64_t *fsc = sc.get<uint64_t>(2);  // [0] survivors, [1] survivors of side A
     NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
-    CK(cudaMemsetAsync(bm, 0, 2 * bmw * sizeof(uint32_t), s));
-    {
-      KTimer kt(ctx, s, "filter", 2ull * 4 * pa.nkey * std::min(n1, n2) +
-                                      4ull * pa.nkey * std::max(n1, n2) + 16ull * bmw + n / 8,
-                3);
-      launch_filter(pa, bm, bm + bmw, bbits, hashed, fmask, fcnt, s);
-      CKL("filter");
-    }
-    {
-      KTimer kt(ctx, s, "filter_scan", 12ull * nsl, 3);
-      launch_exclusive_scan_u32(fcnt, foff, nsl, ftmp, fsc, s);
-      CKL("filter_scan");
-    }
-    {
-      KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * nsl);
-      launch_filter_emit(pa, fmask, fcnt, foff, wa, hist, s);
-      CKL("filter_emit");
-      TRY(ensure_pinned(ctx, 1));
+    const uint32_t dmask = pa.last_mask;
+    uint64_t split = n1;     // words [0, split) are side A's
+    bool exact = false;      // the last round's bitmaps were exact (no false positives)
+    // survivors + side-A survivors after a round: one blocking read
+    auto read_counts = [&](uint64_t nslA) -> mapsq_status {
+      TRY(ensure_pinned(ctx, 2));
       CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));  // the surviving word count sizes the sort
+      CK(cudaMemcpyAsync(ctx->pinned + 1, foff + nslA, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      return MAPSQ_OK;
+    };
+    const bool colpath = pa.nkey == 1 && pl.kb <= 32 && !pa.hash;
+    if (colpath) {
+      // round 0 on the key column (no word is written for a dropped row)
+      const uint32_t bbits = std::min<uint32_t>(pl.kb, kSemijoinBits);
+      const uint32_t hashed = pl.kb > bbits;
+      const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
+      const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
+      CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+      {
+        KTimer kt(ctx, s, "filter", 2ull * 4 * std::min(n1, n2) + 4ull * std::max(n1, n2) +
+                                        16ull * bw + n / 8, 3);
+        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, s);
+        CKL("filter");
+      }
+      {
+        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
+        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
+        CKL("filter_scan");
+      }
+      {
+        KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
+        launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
+        CKL("filter_emit");
+        TRY(read_counts(nslA));
+        kt.t.bytes += 12ull * ctx->pinned[0];
+      }
       nw = ctx->pinned[0];
-      kt.t.bytes += (4ull * pa.nkey + 8ull) * nw;
+      split = nslA < ns ? ctx->pinned[1] : nw;
+      // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
+      // says the keys mostly match, so refinement rounds would not pay
+      exact = !hashed || nw * 10 > n * 9;
+    } else {
+      // composite / hashed keys: Map every row, then filter the words
+      pa.passes = 0;  // (the histogram is counted by the last round's emit)
+      KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
+      launch_pack_hist(pa, cur, nullptr, hist, s);
+      CKL("pack_hist");
+    }
+    // word rounds: the first one for non-column keys, then refinements while a hashed round
+    // still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per key of the
+    // smaller side, with a fresh hash seed)
+    // (the first word round of a non-column key always runs: its emit counts the histogram)
+    for (int round = colpath ? 1 : 0;
+         round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
+      const uint64_t small = std::min(split, nw - split);
+      uint32_t bbits = bits_for(8 * std::max<uint64_t>(small, 1));
+      bbits = std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, bbits));
+      const uint64_t bw = (1ull << bbits) / 32;
+      const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
+      CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+      {
+        KTimer kt(ctx, s, "wfilter", 2ull * 8 * small + 8ull * (nw - small) + 16ull * bw + nw / 8, 3);
+        launch_wfilter(cur, nw, split, pl.ib, 0x632BE59BD9B4E019ull * (round + 1), bbits, bm,
+                       bm + bw, fmask, fcnt, s);
+        CKL("wfilter");
+      }
+      {
+        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
+        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
+        CKL("filter_scan");
+      }
+      CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
+      {
+        KTimer kt(ctx, s, "wfilter_emit", nw / 8 + 12ull * ns);
+        launch_wfilter_emit(cur, nw, split, fmask, fcnt, foff, alt, pl.passes ? hist : nullptr,
+                            pl.ib, dmask, s);
+        CKL("wfilter_emit");
+        TRY(read_counts(nslA));
+        kt.t.bytes += 16ull * ctx->pinned[0];
+      }
+      const uint64_t before = nw;
+      nw = ctx->pinned[0];
+      split = nslA < ns ? ctx->pinned[1] : nw;
+      std::swap(cur, alt);
+      if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
     }
     ctx->counters.last_filtered = n - nw;
     if (nw == 0) {
@@ -517,15 +592,15 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   } else {
     const PackArgs pa = pack_args(pl, &a, &b);
     KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
-    launch_pack_hist(pa, wa, va, hist, s);
+    launch_pack_hist(pa, cur, va, hist, s);
     CKL("pack_hist");
   }
   // ---- Sort (row a4)
   int which = 0;
-  TRY(radix_sort(ctx, wa, wb, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
-  uint64_t *words = which ? wb : wa;
+  TRY(radix_sort(ctx, cur, alt, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
+  uint64_t *words = which ? alt : cur;
   uint32_t *vals = kv ? (which ? vb : va) : nullptr;
-  sc.release(which ? wa : wb);
+  sc.release(which ? cur : alt);
   if (kv) sc.release(which ? va : vb);
   // ---- ReduceDuplicate 1 (row a5): groups + counts + exclusive scan
   const uint64_t cap = std::min(n1, n2);
@@ -545,7 +620,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
                        gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
     CKL("find_groups");
   }
-  const bool residual = pl.path == MAPSQ_PATH_RESIDUAL;
+  // RESIDUAL and HASH verify the shared columns not (exactly) in key' for every pair
+  const bool residual = pl.path == MAPSQ_PATH_RESIDUAL || pl.path == MAPSQ_PATH_HASH;
   ResidualArgs ra;
   std::memset(&ra, 0, sizeof ra);
   uint64_t *pmask = residual ? sc.get<uint64_t>(cap) : nullptr;
@@ -1214,6 +1290,13 @@ MAPSQ_API mapsq_status mapsq_plan_join(const mapsq_table *tp1, const mapsq_table
   return plan_join(nullptr, tp1, tp2, plan);
 }
 
+MAPSQ_API mapsq_status mapsq_plan_join_mode(const mapsq_table *tp1, const mapsq_table *tp2,
+                                            int wide_mode, mapsq_join_plan *plan) {
+  if (!plan || wide_mode < MAPSQ_WIDE_KEY_RESIDUAL || wide_mode > MAPSQ_WIDE_KEY_HASH)
+    return MAPSQ_E_INVALID;
+  return plan_join(nullptr, tp1, tp2, plan, wide_mode);
+}
+
 MAPSQ_API mapsq_status mapsq_join(mapsq_ctx *ctx, const mapsq_table *tp1, const mapsq_table *tp2,
                                   mapsq_table *rs, void *stream) {
   TRY(enter(ctx));
@@ -1596,7 +1679,7 @@ MAPSQ_API mapsq_status mapsq_ipc_close(mapsq_ctx *ctx, void *dev_ptr) {
 
 MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value) {
   if (!ctx) return MAPSQ_E_INVALID;
-  if (option == MAPSQ_OPT_WIDE_KEY && (value == MAPSQ_WIDE_KEY_RESIDUAL || value == MAPSQ_WIDE_KEY_KV)) {
+  if (option == MAPSQ_OPT_WIDE_KEY && value >= MAPSQ_WIDE_KEY_RESIDUAL && value <= MAPSQ_WIDE_KEY_HASH) {
     ctx->wide_key_mode = (int)value;
     return MAPSQ_OK;
   }

@@ -27,6 +27,7 @@ constexpr int kFWarps = kFThreads / 32;
 constexpr int kFItems = 16;                    // rows per lane per slice
 constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
+constexpr uint32_t kDenseSlice = 160;          // survivors above which the emit walks items
 
 // FAST: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic) — every
 // config's joins; otherwise the generic 64-bit composite key.
@@ -49,8 +50,9 @@ struct Side {
 template <bool FAST>
 __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
                                           uint32_t lane, KeyT<FAST> key[kFItems]) {
+  const bool hash = !FAST && a.hash;
 #pragma unroll
-  for (int it = 0; it < kFItems; it++) key[it] = 0;
+  for (int it = 0; it < kFItems; it++) key[it] = hash ? kKeyHashSeed : 0;
   const uint32_t nk = FAST ? 1u : a.nkey;
   for (uint32_t c = 0; c < nk; c++) {
     const uint32_t *p = sd.col[c];
@@ -64,7 +66,12 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
 #pragma unroll
     for (int it = 0; it < kFItems; it++)
       key[it] = FAST ? (KeyT<FAST>)(v[it] - lo)
-                     : (KeyT<FAST>)(key[it] | (uint64_t)(v[it] - lo) << sh);
+                     : (KeyT<FAST>)(hash ? key_hash_step(key[it], v[it])
+                                         : (key[it] | (uint64_t)(v[it] - lo) << sh));
+  }
+  if (hash) {
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) key[it] = (KeyT<FAST>)key_hash_final(key[it], a.kb);
   }
 }
 
@@ -72,12 +79,15 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
 // per row serialises on hot keys: 40 ms vs 5.9 ms for 5e8 Zipf rows, tools/bitmap_bench.cu), and
 // runs of equal keys in consecutive rows (clustered data) set their bit once: a lane whose left
 // neighbour holds the same bit skips.
+// TEST = false (keys mostly distinct, e.g. hashed composite keys): fire-and-forget RED.OR only
+// (208 vs 75 G rows/s for distinct keys, tools/bitmap_bench.cu).
+template <bool TEST = true>
 __device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFItems],
                                          uint32_t keep, uint32_t lane) {
   uint32_t word[kFItems];
 #pragma unroll
   for (int it = 0; it < kFItems; it++)  // (read-only path: a stale word costs one more atomic)
-    word[it] = (keep >> it & 1u) ? __ldg(bm + (bidx[it] >> 5)) : 0xffffffffu;
+    word[it] = (TEST && (keep >> it & 1u)) ? __ldg(bm + (bidx[it] >> 5)) : 0u;
 #pragma unroll
   for (int it = 0; it < kFItems; it++) {
     const uint32_t b = bidx[it];
@@ -146,6 +156,38 @@ filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict_
   }
 }
 
+// Warp-cooperative survivor addressing: lanes 0..15 hold the slice's 16 survivor-bit words
+// (`my`, bit l of word it = row it * 32 + l survives).  slice_prefix returns each lane's
+// exclusive prefix of the popcounts; survivor_row maps survivor r (< count) to its row in the
+// slice, so a warp emits 32 survivors per step with consecutive (coalesced) stores.
+__device__ __forceinline__ uint32_t slice_prefix(uint32_t my, uint32_t lane) {
+  const uint32_t c = __popc(my);
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  return x - c;
+}
+__device__ __forceinline__ uint32_t survivor_row(uint32_t my, uint32_t pre, uint32_t r) {
+  uint32_t it = 0;  // the item holding survivor r: the last q with pre_q <= r
+#pragma unroll
+  for (int q = 1; q < kFItems; q++) it += __shfl_sync(0xffffffffu, pre, q) <= r;
+  uint32_t m = __shfl_sync(0xffffffffu, my, it);
+  uint32_t k = r - __shfl_sync(0xffffffffu, pre, it), pos = 0;
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) {  // k-th set bit of m
+    const uint32_t low = __popc(m & ((1u << sh) - 1u));
+    if (k >= low) {
+      k -= low;
+      m >>= sh;
+      pos += sh;
+    }
+  }
+  return it * 32 + pos;
+}
+
 // Emit: the survivors of slice s go to words[off[s] ..] in row order (stable), as
 // key' << ib | row id; digit 0 of the survivors is counted into hist.
 template <bool FAST>
@@ -169,27 +211,180 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
     const Side &sd = is_b ? sb : sa;
     const uint64_t base = (s - sd.slice0) * kFWarpRows;
     const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + s * kFItems + lane) : 0u;
-    uint64_t pos = __ldg(off + s);
+    const uint32_t pre = slice_prefix(my, lane);
+    const uint32_t c = __shfl_sync(0xffffffffu, pre + __popc(my), kFItems - 1);
+    const uint64_t pos = __ldg(off + s);
+    if (c > kDenseSlice) {  // dense slice: walk the 16 items (lanes = rows of the item)
+      uint64_t p = pos;
 #pragma unroll 4
-    for (int it = 0; it < kFItems; it++) {
-      const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
-      if (!bal) continue;
-      if (bal >> lane & 1u) {
-        const uint64_t j = base + (uint64_t)it * 32 + lane;
-        uint64_t key = 0;
-        for (uint32_t c = 0; c < nk; c++) {
-          const uint32_t v = __ldg(sd.col[c] + j) - a.lo[c];
-          key |= FAST ? (uint64_t)v : (uint64_t)v << a.shift[c];
+      for (int it = 0; it < kFItems; it++) {
+        const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
+        if (bal >> lane & 1u) {
+          const uint64_t j = base + (uint64_t)it * 32 + lane;
+          const bool hash = !FAST && a.hash;
+          uint64_t key = hash ? kKeyHashSeed : 0;
+          for (uint32_t q = 0; q < nk; q++) {
+            const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
+            key = hash ? key_hash_step(key, raw) : (key | (FAST ? (uint64_t)v : (uint64_t)v << a.shift[q]));
+          }
+          if (hash) key = key_hash_final(key, a.kb);
+          const uint64_t w = (key << a.ib) | (j + sd.id0);
+          __stcs(words + p + __popc(bal & lt), w);
+          if (a.passes) atomicAdd(h + ((uint32_t)(w >> a.bit_lo) & a.last_mask), 1u);
         }
+        p += __popc(bal);
+      }
+      continue;
+    }
+    for (uint32_t r0 = 0; r0 < c; r0 += 32) {  // sparse slice: 32 survivors per step
+      const uint32_t r = r0 + lane;
+      const uint32_t row = survivor_row(my, pre, r < c ? r : 0);
+      if (r < c) {
+        const uint64_t j = base + row;
+        const bool hash = !FAST && a.hash;
+        uint64_t key = hash ? kKeyHashSeed : 0;
+        for (uint32_t q = 0; q < nk; q++) {
+          const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
+          key = hash ? key_hash_step(key, raw) : (key | (FAST ? (uint64_t)v : (uint64_t)v << a.shift[q]));
+        }
+        if (hash) key = key_hash_final(key, a.kb);
         const uint64_t w = (key << a.ib) | (j + sd.id0);
-        __stcs(words + pos + __popc(bal & lt), w);
+        __stcs(words + pos + r, w);
         if (a.passes) atomicAdd(h + ((uint32_t)(w >> a.bit_lo) & a.last_mask), 1u);
       }
-      pos += __popc(bal);
     }
   }
   __syncthreads();
   if (a.passes)
+    for (uint32_t d = threadIdx.x; d < kRadix; d += kFThreads) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int q = 0; q < kFCopies; q++) c += s_h[q][d];
+      if (c) atomicAdd(hist + d, c);
+    }
+}
+
+// ---- refinement rounds on packed words (key' = w >> ib): words [0, split) are side A's,
+// [split, n) side B's (the emit keeps the sides contiguous).  The bit index mixes key' with a
+// per-round seed, so a second round's false positives are independent of the first's.
+struct WSide {
+  const uint64_t *w;
+  uint64_t rows, slice0;
+};
+
+__device__ __forceinline__ uint32_t wbit(uint64_t w, uint32_t ib, uint64_t seed, uint32_t bbits) {
+  return (uint32_t)((((w >> ib) ^ seed) * 0x9E3779B97F4A7C15ull) >> (64 - bbits));
+}
+
+__global__ void __launch_bounds__(kFThreads)
+wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+                     uint32_t *__restrict__ bm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    uint32_t bidx[kFItems], keep = 0;
+    uint64_t w[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
+    }
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      bidx[it] = wbit(w[it], ib, seed, bbits);
+      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+    }
+    set_bits<false>(bm, bidx, keep, lane);
+  }
+}
+
+template <bool SET>
+__global__ void __launch_bounds__(kFThreads)
+wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+                     const uint32_t *__restrict__ bm_probe, uint32_t *__restrict__ bm_set,
+                     uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    uint64_t w[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
+    }
+    uint32_t word[kFItems], bidx[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      bidx[it] = wbit(w[it], ib, seed, bbits);
+      word[it] = j < sd.rows ? __ldg(bm_probe + (bidx[it] >> 5)) : 0u;
+    }
+    uint32_t my = 0, c = 0, keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const bool k = word[it] >> (bidx[it] & 31) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      keep |= (uint32_t)k << it;
+      if (lane == (uint32_t)it) my = bal;
+      c += __popc(bal);
+    }
+    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
+    if (lane == 0) cnt[sd.slice0 + ws] = c;
+    if (SET && c) set_bits<false>(bm_set, bidx, keep, lane);
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads)
+wfilter_emit_kernel(const WSide sa, const WSide sb, const uint32_t *__restrict__ mask,
+                    const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ off,
+                    uint64_t *__restrict__ out, uint32_t *__restrict__ hist, uint32_t bit_lo,
+                    uint32_t dmask) {
+  __shared__ uint32_t s_h[kFCopies][kRadix];
+  for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  const uint64_t nslices = sb.slice0 + ceil_div(sb.rows, kFWarpRows);
+  for (uint64_t s = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); s < nslices;
+       s += nwarps) {
+    if (__ldg(cnt + s) == 0) continue;  // warp-uniform
+    const WSide &sd = s >= sb.slice0 ? sb : sa;
+    const uint64_t base = (s - sd.slice0) * kFWarpRows;
+    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + s * kFItems + lane) : 0u;
+    const uint32_t pre = slice_prefix(my, lane);
+    const uint32_t c = __shfl_sync(0xffffffffu, pre + __popc(my), kFItems - 1);
+    const uint64_t pos = __ldg(off + s);
+    if (c > kDenseSlice) {  // dense slice: walk the 16 items (lanes = rows of the item)
+      uint64_t p = pos;
+#pragma unroll 4
+      for (int it = 0; it < kFItems; it++) {
+        const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
+        if (bal >> lane & 1u) {
+          const uint64_t w = __ldg(sd.w + base + (uint64_t)it * 32 + lane);
+          __stcs(out + p + __popc(bal & lt), w);
+          if (hist) atomicAdd(h + ((uint32_t)(w >> bit_lo) & dmask), 1u);
+        }
+        p += __popc(bal);
+      }
+      continue;
+    }
+    for (uint32_t r0 = 0; r0 < c; r0 += 32) {  // sparse slice: 32 survivors per step
+      const uint32_t r = r0 + lane;
+      const uint32_t row = survivor_row(my, pre, r < c ? r : 0);
+      if (r < c) {
+        const uint64_t w = __ldg(sd.w + base + row);
+        __stcs(out + pos + r, w);
+        if (hist) atomicAdd(h + ((uint32_t)(w >> bit_lo) & dmask), 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (hist)
     for (uint32_t d = threadIdx.x; d < kRadix; d += kFThreads) {
       uint32_t c = 0;
 #pragma unroll
@@ -213,7 +408,7 @@ int grid_for_rows(uint64_t rows) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148 * 8));
 }
 
-bool filter_fast(const PackArgs &a) { return a.nkey == 1 && a.kb <= 32; }
+bool filter_fast(const PackArgs &a) { return a.nkey == 1 && a.kb <= 32 && !a.hash; }
 
 }  // namespace
 
@@ -240,6 +435,29 @@ void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbi
     filter_probe_kernel<false, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits,
                                                                 hashed, mask, cnt);
   }
+}
+
+void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
+                    uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
+                    uint32_t *cnt, cudaStream_t s) {
+  const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
+  const bool b_small = B.rows < A.rows;
+  const WSide S = b_small ? B : A, L = b_small ? A : B;
+  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
+  if (S.rows) wfilter_build_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmS);
+  if (L.rows)
+    wfilter_probe_kernel<true><<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, bmL, mask, cnt);
+  if (S.rows)
+    wfilter_probe_kernel<false><<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmL, nullptr, mask,
+                                                         cnt);
+}
+
+void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
+                         const uint32_t *cnt, const uint64_t *off, uint64_t *out, uint32_t *hist,
+                         uint32_t bit_lo, uint32_t dmask, cudaStream_t s) {
+  const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
+  wfilter_emit_kernel<<<grid_for_rows(n), kFThreads, 0, s>>>(A, B, mask, cnt, off, out, hist,
+                                                            bit_lo, dmask);
 }
 
 void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,

@@ -48,7 +48,7 @@ struct mapsq_ctx {
   std::string err;
   bool cuda_broken = false;
   bool profiling = false;
-  int wide_key_mode = MAPSQ_WIDE_KEY_RESIDUAL;
+  int wide_key_mode = MAPSQ_WIDE_KEY_HASH;
   int semijoin = MAPSQ_SEMIJOIN_AUTO;
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
@@ -272,7 +272,23 @@ struct PackArgs {
   uint32_t last_mask;  // digit mask of the last pass ((1 << bits) - 1)
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
   uint32_t kb;       // packed key bits
+  uint32_t hash;     // 1 (PATH_HASH): key' = key_hash over the raw values of all nkey columns
 };
+
+// PATH_HASH key': a 64-bit mix of the shared columns' raw values, top kb bits.  Equal keys get
+// equal key'; ReduceDuplicate verifies every pair's columns, so collisions cost time only.
+__host__ __device__ __forceinline__ uint64_t key_hash_step(uint64_t h, uint32_t v) {
+  h ^= v;
+  h *= 0xbf58476d1ce4e5b9ull;
+  return h ^ (h >> 29);
+}
+__host__ __device__ __forceinline__ uint64_t key_hash_final(uint64_t h, uint32_t kb) {
+  h ^= h >> 32;
+  h *= 0x94d049bb133111ebull;
+  h ^= h >> 29;
+  return h >> (64 - kb);
+}
+constexpr uint64_t kKeyHashSeed = 0x9E3779B97F4A7C15ull;
 // Map (K2): pack words (or KV pairs) and build the digit histograms of every pass.
 void launch_pack_hist(const PackArgs &a, uint64_t *words, uint32_t *vals, uint32_t *hist,
                       cudaStream_t s);
@@ -358,6 +374,15 @@ void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbi
                    uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s);
 void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
                         const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s);
+// Refinement round on packed words ([0, split) side A, [split, n) side B; key' = w >> ib, bit =
+// mix(key' ^ seed)): the same three passes, then the emit copies the survivors to `out`
+// (sides stay contiguous) and counts their digit 0 into hist (if not NULL).
+void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
+                    uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
+                    uint32_t *cnt, cudaStream_t s);
+void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
+                         const uint32_t *cnt, const uint64_t *off, uint64_t *out, uint32_t *hist,
+                         uint32_t bit_lo, uint32_t dmask, cudaStream_t s);
 
 // Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
 // (unordered, atomic slots < cap); per-run bounds [slo | olo | shi | ohi].

@@ -43,7 +43,7 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
     // together (a per-item column loop serialized them on load latency)
     uint64_t key[kHistItems];
 #pragma unroll
-    for (int it = 0; it < kHistItems; it++) key[it] = 0;
+    for (int it = 0; it < kHistItems; it++) key[it] = a.hash ? kKeyHashSeed : 0;
     for (uint32_t c = 0; c < a.nkey; c++) {
       const uint32_t *k1 = a.key1[c], *k2 = a.key2[c] - a.n1;
       const uint32_t lo = a.lo[c], sh = a.shift[c];
@@ -53,8 +53,17 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
         const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
         v[it] = i < n ? __ldcs((i < a.n1 ? k1 : k2) + i) : lo;
       }
+      if (a.hash) {
 #pragma unroll
-      for (int it = 0; it < kHistItems; it++) key[it] |= (uint64_t)(v[it] - lo) << sh;
+        for (int it = 0; it < kHistItems; it++) key[it] = key_hash_step(key[it], v[it]);
+      } else {
+#pragma unroll
+        for (int it = 0; it < kHistItems; it++) key[it] |= (uint64_t)(v[it] - lo) << sh;
+      }
+    }
+    if (a.hash) {
+#pragma unroll
+      for (int it = 0; it < kHistItems; it++) key[it] = key_hash_final(key[it], a.kb);
     }
 #pragma unroll
     for (int it = 0; it < kHistItems; it++) {

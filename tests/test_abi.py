@@ -60,18 +60,36 @@ def test_plan_composite_key_order_and_shifts():
 def test_plan_residual_path_when_key_and_index_exceed_64_bits():
     # two 32-bit key columns + 5 index bits do not fit one word: the wider/first column is
     # packed, the other is checked exactly inside each packed-key group
+    R = mq.WIDE_KEY_RESIDUAL
     full = (0, 0xFFFFFFFF)
-    pl = mq.plan_join([0, 1], [full, full], 10, [0, 1], [full, full], 10)
+    pl = mq.plan_join([0, 1], [full, full], 10, [0, 1], [full, full], 10, R)
     assert pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b01
     assert pl.kb == 32 and pl.ib == 5 and pl.passes == 4
     # the widest column is packed first, whatever its position
-    pl = mq.plan_join([0, 1], [(0, 255), full], 1 << 26, [0, 1], [(0, 255), full], 1 << 26)
+    pl = mq.plan_join([0, 1], [(0, 255), full], 1 << 26, [0, 1], [(0, 255), full], 1 << 26, R)
     assert pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b10 and pl.kb == 32
     # 3 columns: the two widest that fit 64 - ib are packed
     pl = mq.plan_join([0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000,
-                      [0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000)
+                      [0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000, R)
     assert pl.ib == 11 and pl.path == mq.PATH_RESIDUAL and pl.packed_mask == 0b101
     assert pl.kb == 21 + 25
+
+
+def test_plan_hash_path_is_the_default_for_wide_keys():
+    # keys wider than 64 - ib bits, or wider than 32 bits, sort on a 32-bit (or 64 - ib) hash of
+    # every shared column; narrower composite keys keep the exact P64 packing
+    full = (0, 0xFFFFFFFF)
+    pl = mq.plan_join([0, 1], [full, full], 10, [0, 1], [full, full], 10)
+    assert pl.path == mq.PATH_HASH and pl.packed_mask == 0 and pl.kb == 32 and pl.passes == 4
+    pl = mq.plan_join([0, 1], [full, full], (1 << 31) - 1, [0, 1], [full, full], 1 << 31)
+    assert pl.path == mq.PATH_HASH and pl.ib == 32 and pl.kb == 32
+    pl = mq.plan_join([0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000,
+                      [0, 1, 2], [(0, 2**20), (0, 2**12), (0, 2**24)], 1000)
+    assert pl.path == mq.PATH_HASH and pl.kb == 32          # 59 key bits > 32: hashed
+    pl = mq.plan_join([0, 1], [(0, 2**20), (0, 2**10)], 1000, [0, 1], [(0, 2**20), (0, 2**10)], 1)
+    assert pl.path == mq.PATH_P64 and pl.kb == 21 + 11      # 32 bits: packed exactly
+    with pytest.raises(mq.MapsqError):
+        mq.plan_join([0], [(0, 1)], 1, [0], [(0, 1)], 1, 7)
 
 
 def test_plan_errors():

@@ -118,18 +118,21 @@ def test_join_composite_keys_and_kv_path(ctx):
     B[:2, :2] = [[0, 0], [0xFFFFFFFF, 0xFFFFFFFF]]
     ta, tb = oracle.Table([4, 5, 6], A), oracle.Table([5, 4, 7], np.ascontiguousarray(B))
     ref = oracle.join(ta, tb)
-    # default: RESIDUAL path (x packed, z verified per group); rows ordered by (x', l, r)
+    # default: HASH path (32-bit hash of (x, z), every pair verified); rows grouped by hash
     got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
-    assert ctx.stats()["last_path"] == mq.PATH_RESIDUAL
+    assert ctx.stats()["last_path"] == mq.PATH_HASH
     assert_same(got, ref, ordered=False)
-    # forced KV path: (u64 key', u32 rowid) pairs over all 64 key bits, lexicographic order
-    ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_KV)
-    try:
-        got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
-        assert ctx.stats()["last_path"] == mq.PATH_KV
-        assert_same(got, ref)
-    finally:
-        ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_RESIDUAL)
+    # RESIDUAL path (x packed, z verified per group); rows ordered by (x', l, r)
+    # KV path: (u64 key', u32 rowid) pairs over all 64 key bits, lexicographic order
+    for mode, path, ordered in ((mq.WIDE_KEY_RESIDUAL, mq.PATH_RESIDUAL, False),
+                                (mq.WIDE_KEY_KV, mq.PATH_KV, True)):
+        ctx.set_option(mq.OPT_WIDE_KEY, mode)
+        try:
+            got = ctx.join(dtable([4, 5, 6], A), dtable([5, 4, 7], np.ascontiguousarray(B)))
+            assert ctx.stats()["last_path"] == path
+            assert_same(got, ref, ordered=ordered)
+        finally:
+            ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_HASH)
     # three shared variables
     A = rng.integers(0, 3, (2000, 4)).astype(np.uint32)
     B = rng.integers(0, 3, (1500, 3)).astype(np.uint32)
@@ -137,9 +140,12 @@ def test_join_composite_keys_and_kv_path(ctx):
     assert_same(ctx.join(dtable([0, 1, 2, 9], A), dtable([2, 1, 0], B)), ref)
 
 
-def test_join_residual_path_collisions_and_skew(ctx):
-    # packed column x with few values and a residual column z: many packed-key groups mix
-    # several z values, so the per-group exact residual check decides every pair
+@pytest.mark.parametrize("mode,path", [("RESIDUAL", "RESIDUAL"), ("HASH", "HASH")])
+def test_join_residual_path_collisions_and_skew(ctx, mode, path):
+    # RESIDUAL: packed column x with few values and a residual column z: many packed-key groups
+    # mix several z values, so the per-group exact residual check decides every pair.
+    # HASH: key' = 32-bit hash of (x, z); every pair's columns are verified
+    ctx.set_option(mq.OPT_WIDE_KEY, getattr(mq, "WIDE_KEY_" + mode))
     rng = np.random.default_rng(13)
     for n1, n2, dx, dz in [(3000, 2000, 50, 7), (500, 40000, 3, 1 << 32), (20000, 20000, 5000, 3)]:
         x1 = rng.integers(0, dx, n1); z1 = rng.integers(0, dz, n1, dtype=np.uint64)
@@ -150,8 +156,9 @@ def test_join_residual_path_collisions_and_skew(ctx):
         B = np.stack([z2, rng.integers(0, 100, n2), x2], 1).astype(np.uint32)
         ref = oracle.join(oracle.Table([0, 1, 2], A), oracle.Table([1, 3, 0], B))
         got = ctx.join(dtable([0, 1, 2], A), dtable([1, 3, 0], B))
-        assert ctx.stats()["last_path"] == mq.PATH_RESIDUAL
+        assert ctx.stats()["last_path"] == getattr(mq, "PATH_" + path)
         assert_same(got, ref, ordered=False)
+    ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_HASH)
 
 
 def test_join_skewed_hot_key_large_groups(ctx):
@@ -271,7 +278,7 @@ def test_query_configs_small_scale(ctx, cfg):
     got = ctx.query(trip, pats)
     assert got.nrows == config_expected_counts(cfg, st)[-1]
     # wide-key joins (RESIDUAL path) emit (packed key, l, r) order: compare canonically there
-    assert_same(got, ref, ordered=ctx.stats()["last_path"] != mq.PATH_RESIDUAL)
+    assert_same(got, ref, ordered=ctx.stats()["last_path"] not in (mq.PATH_RESIDUAL, mq.PATH_HASH))
     # chained joins one by one agree with the generator's bookkeeping
     tabs = ctx.scan_patterns(trip, pats)
     acc = tabs[0]
@@ -286,7 +293,7 @@ def test_query_projection_and_errors(ctx):
     pats = config_query("C5")
     got = ctx.query(trip, pats, [2, 0])
     ref = oracle.query(s, p, o, pats, [2, 0])
-    assert_same(got, ref)
+    assert_same(got, ref, ordered=False)  # (?x, ?z) join key: HASH path
     with pytest.raises(mq.MapsqError) as e:
         ctx.query(trip, [((V, 0), (C, 5), (V, 1)), ((V, 2), (C, 5), (V, 3))])
     assert e.value.status == "E_NO_SHARED"

@@ -40,7 +40,7 @@ __global__ void probe_ilp(const uint32_t *k, uint64_t n, const uint32_t *bm, uin
 #pragma unroll
     for (int u = 0; u < ILP; u++) {
       const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-      x[u] = i < n ? (__ldcs(k + i) & mask) : 0;
+      x[u] = i < n ? (uint32_t)((__ldcs(k + i) * 0x9E3779B97F4A7C15ull) >> 32) & mask : 0;
     }
 #pragma unroll
     for (int u = 0; u < ILP; u++) w[u] = NC ? __ldg(bm + (x[u] >> 5)) : __ldcg(bm + (x[u] >> 5));
@@ -53,6 +53,24 @@ __global__ void probe_ilp(const uint32_t *k, uint64_t n, const uint32_t *bm, uin
   atomicAdd(cnt, (unsigned long long)c);
 }
 
+// distinct random bits: one RED.OR per row (no test), or test-then-set
+template <bool TEST>
+__global__ void build_distinct(uint64_t n, uint32_t *bm, uint32_t mask) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 8;
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x) * 8 + threadIdx.x; i0 < n; i0 += stride) {
+    uint32_t x[8], w[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) x[u] = (uint32_t)(((i0 + u * blockDim.x) * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+    if (TEST) {
+#pragma unroll
+      for (int u = 0; u < 8; u++) w[u] = __ldg(bm + (x[u] >> 5));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (i0 + u * blockDim.x < n && (!TEST || !(w[u] >> (x[u] & 31) & 1u))) atomicOr(bm + (x[u] >> 5), 1u << (x[u] & 31));
+  }
+}
+
 int main(int argc, char **argv) {
   const uint64_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 500000000ull;
   std::vector<uint32_t> a(n), b(n);
@@ -62,7 +80,7 @@ int main(int argc, char **argv) {
   unsigned long long *cnt;
   cudaMalloc(&da, n * 4);
   cudaMalloc(&db, n * 4);
-  cudaMalloc(&bm, (1u << 29) / 8);
+  cudaMalloc(&bm, (1ull << 32) / 8);
   cudaMalloc(&cnt, 8);
   cudaMemcpy(da, a.data(), n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(db, b.data(), n * 4, cudaMemcpyHostToDevice);
@@ -72,7 +90,7 @@ int main(int argc, char **argv) {
   auto t = [&](const char *name, auto f) {
     float best = 1e9;
     for (int r = 0; r < 3; r++) {
-      cudaMemset(bm, 0, (1u << 29) / 8);
+      cudaMemset(bm, 0, (1ull << 32) / 8);
       cudaMemset(cnt, 0, 8);
       cudaEventRecord(e0);
       f();
@@ -96,11 +114,17 @@ int main(int argc, char **argv) {
     probe<<<g, 256>>>(db, n, bm, mask, cnt);
   });
   t("probe only (empty bitmap)", [&] { probe<<<g, 256>>>(db, n, bm, mask, cnt); });
-  for (uint32_t bits : {29u, 28u, 26u, 24u, 20u}) {
-    const uint32_t m = (1u << bits) - 1;
+  for (uint32_t bits : {32u, 30u, 29u, 28u, 24u}) {
+    const uint32_t m = (uint32_t)((1ull << bits) - 1);
     char name[64];
-    snprintf(name, sizeof name, "probe ilp16 cg 2^%u bits", bits);
-    t(name, [&] { probe_ilp<16, false><<<g, 256>>>(db, n, bm, m, cnt); });
+    snprintf(name, sizeof name, "RED.OR distinct 2^%u bits", bits);
+    t(name, [&] { build_distinct<false><<<g, 256>>>(n, bm, m); });
+    snprintf(name, sizeof name, "test+RED.OR distinct 2^%u bits", bits);
+    t(name, [&] { build_distinct<true><<<g, 256>>>(n, bm, m); });
+  }
+  for (uint32_t bits : {32u, 31u, 30u, 29u, 28u}) {
+    const uint32_t m = (uint32_t)((1ull << bits) - 1);
+    char name[64];
     snprintf(name, sizeof name, "probe ilp16 nc 2^%u bits", bits);
     t(name, [&] { probe_ilp<16, true><<<g, 256>>>(db, n, bm, m, cnt); });
     snprintf(name, sizeof name, "probe ilp4 nc 2^%u bits", bits);
