@@ -29,10 +29,14 @@ constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
 constexpr uint32_t kDenseSlice = 160;          // survivors above which the emit walks items
 
-// FAST: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic) — every
-// config's joins; otherwise the generic 64-bit composite key.
-template <bool FAST>
-using KeyT = typename std::conditional<FAST, uint32_t, uint64_t>::type;
+// MODE 0: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic); 1: generic
+// packed composite key; 2: PATH_HASH key over exactly 2 columns; 3: PATH_HASH over nkey columns.
+template <int MODE>
+using KeyT = typename std::conditional<MODE == 0, uint32_t, uint64_t>::type;
+template <int MODE>
+__device__ __forceinline__ uint32_t mode_nkey(const PackArgs &a) {
+  return MODE == 0 ? 1u : (MODE == 2 ? 2u : a.nkey);
+}
 
 __device__ __forceinline__ uint32_t bit_index(uint64_t key, uint32_t bbits, uint32_t hashed) {
   return hashed ? (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bbits)) : (uint32_t)key;
@@ -47,13 +51,13 @@ struct Side {
 
 // key' of rows base + it * 32 + lane (it < kFItems), column-outer loads (all of a column's
 // loads in flight together); rows >= rows get key' 0 (callers mask them)
-template <bool FAST>
+template <int MODE>
 __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
-                                          uint32_t lane, KeyT<FAST> key[kFItems]) {
-  const bool hash = !FAST && a.hash;
+                                          uint32_t lane, KeyT<MODE> key[kFItems]) {
+  constexpr bool hash = MODE >= 2;
 #pragma unroll
   for (int it = 0; it < kFItems; it++) key[it] = hash ? kKeyHashSeed : 0;
-  const uint32_t nk = FAST ? 1u : a.nkey;
+  const uint32_t nk = mode_nkey<MODE>(a);
   for (uint32_t c = 0; c < nk; c++) {
     const uint32_t *p = sd.col[c];
     const uint32_t lo = a.lo[c], sh = a.shift[c];
@@ -65,13 +69,13 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++)
-      key[it] = FAST ? (KeyT<FAST>)(v[it] - lo)
-                     : (KeyT<FAST>)(hash ? key_hash_step(key[it], v[it])
+      key[it] = MODE == 0 ? (KeyT<MODE>)(v[it] - lo)
+                     : (KeyT<MODE>)(hash ? key_hash_step(key[it], v[it])
                                          : (key[it] | (uint64_t)(v[it] - lo) << sh));
   }
   if (hash) {
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) key[it] = (KeyT<FAST>)key_hash_final(key[it], a.kb);
+    for (int it = 0; it < kFItems; it++) key[it] = (KeyT<MODE>)key_hash_final(key[it], a.kb);
   }
 }
 
@@ -99,7 +103,7 @@ __device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFIte
   }
 }
 
-template <bool FAST>
+template <int MODE>
 __global__ void __launch_bounds__(kFThreads)
 filter_build_kernel(const PackArgs a, const Side sd, uint32_t *__restrict__ bm, uint32_t bbits,
                     uint32_t hashed) {
@@ -108,8 +112,8 @@ filter_build_kernel(const PackArgs a, const Side sd, uint32_t *__restrict__ bm, 
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < sd.rows; ws += nwarps) {
     const uint64_t base = ws * kFWarpRows;
-    KeyT<FAST> key[kFItems];
-    load_keys<FAST>(a, sd, base, lane, key);
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
     uint32_t bidx[kFItems], keep = 0;
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
@@ -122,7 +126,7 @@ filter_build_kernel(const PackArgs a, const Side sd, uint32_t *__restrict__ bm, 
 
 // Probe the side's rows against bm_probe: survivor bits -> mask[(slice0 + ws) * 16 ..], counts
 // -> cnt[slice0 + ws]; with SET the survivors also set their bit in bm_set.
-template <bool FAST, bool SET>
+template <int MODE, bool SET>
 __global__ void __launch_bounds__(kFThreads)
 filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm_probe,
                     uint32_t *__restrict__ bm_set, uint32_t bbits, uint32_t hashed,
@@ -132,8 +136,8 @@ filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict_
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < sd.rows; ws += nwarps) {
     const uint64_t base = ws * kFWarpRows;
-    KeyT<FAST> key[kFItems];
-    load_keys<FAST>(a, sd, base, lane, key);
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
     uint32_t word[kFItems], bidx[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
@@ -190,7 +194,7 @@ __device__ __forceinline__ uint32_t survivor_row(uint32_t my, uint32_t pre, uint
 
 // Emit: the survivors of slice s go to words[off[s] ..] in row order (stable), as
 // key' << ib | row id; digit 0 of the survivors is counted into hist.
-template <bool FAST>
+template <int MODE>
 __global__ void __launch_bounds__(kFThreads)
 filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
                    const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
@@ -203,7 +207,7 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
   uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   const uint64_t nslices = sb.slice0 + ceil_div(sb.rows, kFWarpRows);
-  const uint32_t nk = FAST ? 1u : a.nkey;
+  const uint32_t nk = mode_nkey<MODE>(a);
   for (uint64_t s = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); s < nslices;
        s += nwarps) {
     if (__ldg(cnt + s) == 0) continue;  // warp-uniform
@@ -221,11 +225,11 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
         const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
         if (bal >> lane & 1u) {
           const uint64_t j = base + (uint64_t)it * 32 + lane;
-          const bool hash = !FAST && a.hash;
+          constexpr bool hash = MODE >= 2;
           uint64_t key = hash ? kKeyHashSeed : 0;
           for (uint32_t q = 0; q < nk; q++) {
             const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
-            key = hash ? key_hash_step(key, raw) : (key | (FAST ? (uint64_t)v : (uint64_t)v << a.shift[q]));
+            key = hash ? key_hash_step(key, raw) : (key | (MODE == 0 ? (uint64_t)v : (uint64_t)v << a.shift[q]));
           }
           if (hash) key = key_hash_final(key, a.kb);
           const uint64_t w = (key << a.ib) | (j + sd.id0);
@@ -241,11 +245,11 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
       const uint32_t row = survivor_row(my, pre, r < c ? r : 0);
       if (r < c) {
         const uint64_t j = base + row;
-        const bool hash = !FAST && a.hash;
+        constexpr bool hash = MODE >= 2;
         uint64_t key = hash ? kKeyHashSeed : 0;
         for (uint32_t q = 0; q < nk; q++) {
           const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
-          key = hash ? key_hash_step(key, raw) : (key | (FAST ? (uint64_t)v : (uint64_t)v << a.shift[q]));
+          key = hash ? key_hash_step(key, raw) : (key | (MODE == 0 ? (uint64_t)v : (uint64_t)v << a.shift[q]));
         }
         if (hash) key = key_hash_final(key, a.kb);
         const uint64_t w = (key << a.ib) | (j + sd.id0);
@@ -408,7 +412,21 @@ int grid_for_rows(uint64_t rows) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148 * 8));
 }
 
-bool filter_fast(const PackArgs &a) { return a.nkey == 1 && a.kb <= 32 && !a.hash; }
+int filter_mode(const PackArgs &a) {
+  if (a.hash) return a.nkey == 2 ? 2 : 3;
+  return (a.nkey == 1 && a.kb <= 32) ? 0 : 1;
+}
+
+template <int MODE>
+void filter_passes(const PackArgs &a, const Side &S, const Side &L, uint32_t *bmS, uint32_t *bmL,
+                   uint32_t bbits, uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
+  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
+  filter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
+  filter_probe_kernel<MODE, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed, mask,
+                                                           cnt);
+  filter_probe_kernel<MODE, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
+                                                            mask, cnt);
+}
 
 }  // namespace
 
@@ -421,19 +439,11 @@ void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbi
                    uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
   const bool b_small = a.n2 < a.n1;
   const Side S = side_of(a, b_small), L = side_of(a, !b_small);
-  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  if (filter_fast(a)) {
-    filter_build_kernel<true><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
-    filter_probe_kernel<true, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed,
-                                                              mask, cnt);
-    filter_probe_kernel<true, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
-                                                               mask, cnt);
-  } else {
-    filter_build_kernel<false><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
-    filter_probe_kernel<false, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed,
-                                                               mask, cnt);
-    filter_probe_kernel<false, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits,
-                                                                hashed, mask, cnt);
+  switch (filter_mode(a)) {
+    case 0: filter_passes<0>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
+    case 1: filter_passes<1>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
+    case 2: filter_passes<2>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
+    default: filter_passes<3>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
   }
 }
 
@@ -464,10 +474,12 @@ void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t 
                         const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s) {
   const Side A = side_of(a, false), B = side_of(a, true);
   const int g = grid_for_rows(a.n1 + a.n2);
-  if (filter_fast(a))
-    filter_emit_kernel<true><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist);
-  else
-    filter_emit_kernel<false><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist);
+  switch (filter_mode(a)) {
+    case 0: filter_emit_kernel<0><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
+    case 1: filter_emit_kernel<1><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
+    case 2: filter_emit_kernel<2><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
+    default: filter_emit_kernel<3><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
+  }
 }
 
 }  // namespace mapsq
