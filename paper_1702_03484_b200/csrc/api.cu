@@ -562,7 +562,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
       CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
       {
-        KTimer kt(ctx, s, "wfilter", 2ull * 8 * small + 8ull * (nw - small) + 16ull * bw + nw / 8, 3);
+        KTimer kt(ctx, s, "wfilter", 2ull * 8 * small + 8ull * (nw - small) + 16ull * bw + nw / 8, 4);
         launch_wfilter(cur, nw, split, pl.ib, 0x632BE59BD9B4E019ull * (round + 1), bbits, bm,
                        bm + bw, fmask, fcnt, s);
         CKL("wfilter");

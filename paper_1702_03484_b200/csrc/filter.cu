@@ -53,7 +53,8 @@ struct Side {
 // loads in flight together); rows >= rows get key' 0 (callers mask them)
 template <int MODE>
 __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
-                                          uint32_t lane, KeyT<MODE> key[kFItems]) {
+                                          uint32_t lane, KeyT<MODE> key[kFItems],
+                                          uint32_t keep = 0xffffu) {
   constexpr bool hash = MODE >= 2;
 #pragma unroll
   for (int it = 0; it < kFItems; it++) key[it] = hash ? kKeyHashSeed : 0;
@@ -65,7 +66,7 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
-      v[it] = j < sd.rows ? __ldcs(p + j) : lo;
+      v[it] = (j < sd.rows && (keep >> it & 1u)) ? __ldcs(p + j) : lo;
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++)
@@ -342,6 +343,33 @@ wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
   }
 }
 
+// Set bit(key') in bm for the survivors recorded in mask — a separate pass after
+// the probe, so only one bitmap is hot in L2 at a time (two 64 MB bitmaps overflow it):
+// C5's (?x, ?z) join 5.7 -> 4.7 ms over its three rounds.
+__global__ void __launch_bounds__(kFThreads)
+wfilter_setmask_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+                       const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
+                       uint32_t *__restrict__ bm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    if (__ldg(cnt + sd.slice0 + ws) == 0) continue;  // warp-uniform
+    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + (sd.slice0 + ws) * kFItems + lane) : 0u;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
+    const uint64_t base = ws * kFWarpRows;
+    uint32_t bidx[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t w = (keep >> it & 1u) ? __ldcs(sd.w + base + (uint64_t)it * 32 + lane) : 0ull;
+      bidx[it] = wbit(w, ib, seed, bbits);
+    }
+    set_bits<false>(bm, bidx, keep, lane);
+  }
+}
+
 __global__ void __launch_bounds__(kFThreads)
 wfilter_emit_kernel(const WSide sa, const WSide sb, const uint32_t *__restrict__ mask,
                     const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ off,
@@ -422,6 +450,8 @@ void filter_passes(const PackArgs &a, const Side &S, const Side &L, uint32_t *bm
                    uint32_t bbits, uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
   const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
   filter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
+  // the survivors of L set bmL inside the probe (C4: 3.9 ms vs 4.2 ms with a separate
+  // survivor pass; the word rounds, whose L survivors are denser, use the separate pass)
   filter_probe_kernel<MODE, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed, mask,
                                                            cnt);
   filter_probe_kernel<MODE, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
@@ -455,8 +485,11 @@ void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t 
   const WSide S = b_small ? B : A, L = b_small ? A : B;
   const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
   if (S.rows) wfilter_build_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmS);
-  if (L.rows)
-    wfilter_probe_kernel<true><<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, bmL, mask, cnt);
+  if (L.rows) {
+    wfilter_probe_kernel<false><<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, nullptr, mask,
+                                                         cnt);
+    wfilter_setmask_kernel<<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, mask, cnt, bmL);
+  }
   if (S.rows)
     wfilter_probe_kernel<false><<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmL, nullptr, mask,
                                                          cnt);
