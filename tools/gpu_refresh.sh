@@ -12,6 +12,10 @@ for c in C5 C4 C3 C2 C1; do
   timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err
   echo "$c exit $?"; cat $OUT/bench_$c.json | cut -c1-200
 done
+# the same with the full-table scan and with the semi-join filter off (for the record)
+timeout 600 python bench.py --store scan --no-cpu-baseline > $OUT/bench_C5_scan.json 2> $OUT/bench_C5_scan.err
+timeout 600 python bench.py --semijoin off --no-cpu-baseline --no-e2e > $OUT/bench_C5_nofilter.json 2> $OUT/bench_C5_nofilter.err
+timeout 600 python bench.py --config C4 --semijoin off --no-cpu-baseline > $OUT/bench_C4_nofilter.json 2> $OUT/bench_C4_nofilter.err
 timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 echo "ref exit $?"
@@ -22,13 +26,13 @@ if [ "${NCU:-1}" = 1 ]; then
   echo "ncu launches exit $?"
   # one full capture of every kernel of one step (skip the warm-up step's launches)
   timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"radix_pass|scan_write|scan_count|find_groups|expand|pack_hist|residual|tile_groups" \
-    --launch-skip ${SKIP:-40} --launch-count ${COUNT:-24} -o $OUT/ncu_full_C5 -f \
+    -k regex:"radix_pass|wfilter|filter_|find_groups|expand|residual|pack_hist" \
+    --launch-skip ${SKIP:-101} --launch-count ${COUNT:-33} -o $OUT/ncu_full_C5 -f \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_f.log 2>&1
   echo "ncu full exit $?"
   ncu -i $OUT/ncu_full_C5.ncu-rep --page raw --csv > $OUT/ncu_full_C5_raw.csv 2>/dev/null
   ncu -i $OUT/ncu_full_C5.ncu-rep --page details --csv > $OUT/ncu_full_C5_details.csv 2>/dev/null
-  for k in radix_pass scan_write find_groups; do
+  for k in radix_pass wfilter_probe wfilter_build find_groups; do
     ncu -i $OUT/ncu_full_C5.ncu-rep --page source --csv --kernel-name regex:$k --launch-count 1 \
       > $OUT/ncu_source_$k.csv 2>/dev/null
   done
@@ -36,7 +40,7 @@ if [ "${NCU:-1}" = 1 ]; then
   # the report itself is too large to bring back (gpurun_out is capped at 64 MiB)
   rm -f $OUT/ncu_full_C5.ncu-rep
 fi
-if [ -x tools/radix_ablate ]; then
+if [ "${ABLATE:-0}" = 1 ] && [ -x tools/radix_ablate ]; then
   timeout 600 tools/radix_ablate zipf 400000000 > $OUT/ablate_zipf.log 2>&1
   timeout 600 tools/radix_ablate 300000000 0.1 1 > $OUT/ablate_rand.log 2>&1
   cat $OUT/ablate_zipf.log $OUT/ablate_rand.log

@@ -33,6 +33,28 @@ for r in rows[2:]:
     inst = get(r, "smsp__inst_executed.sum")[0]
     print(f"| {name} | {grid} | {regs} | {t*1e3:.3f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
           f"{(rd+wr)/t/1e9:.0f} | {dpct} | {smpct} | {inst} |")
-    traffic.setdefault(short, rd + wr)
+    traffic.setdefault(short, []).append(rd + wr)
+# DRAM bytes per invocation of each library timer (bench.py's kernel names): a timer may cover
+# several kernels; its invocations are counted by its anchor kernel
+TIMERS = {  # timer: (member kernels, anchor)
+    "radix_pass": (["radix_pass"], "radix_pass"),
+    "wfilter": (["wfilter_build", "wfilter_probe", "wfilter_setmask"], "wfilter_setmask"),
+    "filter": (["filter_build", "filter_probe"], "filter_build"),
+    "filter_emit": (["filter_emit"], "filter_emit"),
+    "wfilter_emit": (["wfilter_emit"], "wfilter_emit"),
+    "pack_hist": (["pack_hist"], "pack_hist"),
+    "find_groups": (["find_groups"], "find_groups"),
+    "expand": (["tile_groups", "expand"], "expand"),
+    "residual_count": (["residual_count"], "residual_count"),
+    "residual_expand": (["residual_expand"], "residual_expand"),
+    "scan_write": (["scan_write"], "scan_write"),
+}
+per_timer = {}
+for timer, (members, anchor) in TIMERS.items():
+    inv = len(traffic.get(anchor, []))
+    if inv:
+        per_timer[timer] = sum(sum(traffic.get(m, [])) for m in members) / inv
 if len(sys.argv) > 2:
-    json.dump(traffic, open(sys.argv[2], "w"), indent=1)
+    per_timer["_note"] = ("DRAM bytes read+written per invocation of each library timer, from one "
+                          "ncu --set full capture of one bench step (tools/ncu_summary.py)")
+    json.dump(per_timer, open(sys.argv[2], "w"), indent=1)
