@@ -486,6 +486,15 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   const bool filt = !kv && pl.kb > 0 &&
                     (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
                      (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
+  if (filt && pl.path == MAPSQ_PATH_HASH && pl.kb < 64 - pl.ib) {
+    // with the filter, hash collisions are what survive it: widen key' to every free bit
+    // (C5 J2: |L|·|R| / 2^32 = 8e6 colliding pairs at 32 bits); the extra digit pass then runs
+    // on the few surviving words only
+    pl.kb = std::min<uint32_t>(64 - pl.ib, 40);
+    pl.passes = (pl.kb + MAPSQ_RADIX_BITS - 1) / MAPSQ_RADIX_BITS;
+    ctx->counters.last_kb = pl.kb;
+    ctx->counters.last_passes = pl.passes;
+  }
   if (filt) {
     PackArgs pa = pack_args(pl, &a, &b);
     const uint64_t nsl = n / 512 + 4;  // warp slices of any round (filter_slices <= this)
