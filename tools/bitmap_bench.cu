@@ -107,6 +107,11 @@ int main(int argc, char **argv) {
   };
   const uint32_t mask = (1u << 29) - 1;
   const int g = 148 * 16;
+  int maxp = 0, maxw = 0, l2 = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, 0);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0);
+  printf("L2 %d B, max persisting L2 %d B, max access policy window %d B\n", l2, maxp, maxw);
   t("build atomicOr", [&] { build_atomic<<<g, 256>>>(da, n, bm, mask); });
   t("build test+atomicOr", [&] { build_test<<<g, 256>>>(da, n, bm, mask); });
   t("build test+atomicOr, then probe B", [&] {
@@ -121,6 +126,28 @@ int main(int argc, char **argv) {
     t(name, [&] { build_distinct<false><<<g, 256>>>(n, bm, m); });
     snprintf(name, sizeof name, "test+RED.OR distinct 2^%u bits", bits);
     t(name, [&] { build_distinct<true><<<g, 256>>>(n, bm, m); });
+  }
+  // the same probes with the bitmap marked persisting in L2 (stream access policy window)
+  for (uint32_t bits : {29u, 28u}) {
+    const size_t bytes = (1ull << bits) / 8;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = bm;
+    v.accessPolicyWindow.num_bytes = bytes < (size_t)maxw ? bytes : (size_t)maxw;
+    v.accessPolicyWindow.hitRatio = (float)((double)maxp / (double)bytes > 1.0 ? 1.0 : (double)maxp / (double)bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &v);
+    const uint32_t m = (uint32_t)((1ull << bits) - 1);
+    char name[64];
+    snprintf(name, sizeof name, "PERSIST probe ilp4 nc 2^%u bits", bits);
+    t(name, [&] { probe_ilp<4, true><<<g, 256>>>(db, n, bm, m, cnt); });
+    snprintf(name, sizeof name, "PERSIST RED.OR distinct 2^%u bits", bits);
+    t(name, [&] { build_distinct<false><<<g, 256>>>(n, bm, m); });
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+    printf("  (%s)\n", cudaGetErrorString(cudaGetLastError()));
   }
   for (uint32_t bits : {32u, 31u, 30u, 29u, 28u}) {
     const uint32_t m = (uint32_t)((1ull << bits) - 1);
