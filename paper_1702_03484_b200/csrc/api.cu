@@ -504,17 +504,29 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     uint32_t *fcnt = sc.get<uint32_t>(nsl);
     uint64_t *foff = sc.get<uint64_t>(nsl);
     uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
-    uint64_t *fsc = sc.get<uint64_t>(2);  // [0] survivors, [1] survivors of side A
+    uint64_t *fsc = sc.get<uint64_t>(4);  // [0] survivors, [2..3] sampled survivors / rows
     NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
+    unsigned long long *sample = reinterpret_cast<unsigned long long *>(fsc + 2);
     const uint32_t dmask = pa.last_mask;
     uint64_t split = n1;     // words [0, split) are side A's
     bool exact = false;      // the last round's bitmaps were exact (no false positives)
+    bool skipped = false;    // the sampled probe said the filter would drop < 10%
     // survivors + side-A survivors after a round: one blocking read
     auto read_counts = [&](uint64_t nslA) -> mapsq_status {
       TRY(ensure_pinned(ctx, 2));
       CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(ctx->pinned + 1, foff + nslA, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      return MAPSQ_OK;
+    };
+    // after building the smaller side's bitmap, a 1/16 sample of the larger side is probed; if
+    // >= 90% of it survives the filter cannot pay (C5 J1 drops 6%) and the join goes unfiltered
+    auto sample_says_skip = [&](bool *skip) -> mapsq_status {
+      TRY(ensure_pinned(ctx, 2));
+      CK(cudaMemcpyAsync(ctx->pinned, sample, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const uint64_t surv = ctx->pinned[0], rows = ctx->pinned[1];
+      *skip = ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9;
       return MAPSQ_OK;
     };
     // round 0 reads the key column directly for a single packed column; other keys are Mapped
@@ -528,29 +540,39 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
       const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
       CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+      CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
       {
-        KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (2 * std::min(n1, n2) + std::max(n1, n2)) +
-                                        16ull * bw + n / 8, 3);
-        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, s);
-        CKL("filter");
+        KTimer kt(ctx, s, "filter_sample", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2) / 16) +
+                                               8ull * bw, 2);
+        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 0, sample, s);
+        CKL("filter_sample");
       }
-      {
-        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
-        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
-        CKL("filter_scan");
+      TRY(sample_says_skip(&skipped));
+      if (!skipped) {
+        {
+          KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2)) +
+                                          16ull * bw + n / 8, 2);
+          launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 1, sample, s);
+          CKL("filter");
+        }
+        {
+          KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
+          launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
+          CKL("filter_scan");
+        }
+        {
+          KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
+          launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
+          CKL("filter_emit");
+          TRY(read_counts(nslA));
+          kt.t.bytes += 12ull * ctx->pinned[0];
+        }
+        nw = ctx->pinned[0];
+        split = nslA < ns ? ctx->pinned[1] : nw;
+        // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
+        // says the keys mostly match, so refinement rounds would not pay
+        exact = !hashed || nw * 10 > n * 9;
       }
-      {
-        KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
-        launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
-        CKL("filter_emit");
-        TRY(read_counts(nslA));
-        kt.t.bytes += 12ull * ctx->pinned[0];
-      }
-      nw = ctx->pinned[0];
-      split = nslA < ns ? ctx->pinned[1] : nw;
-      // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
-      // says the keys mostly match, so refinement rounds would not pay
-      exact = !hashed || nw * 10 > n * 9;
     } else {
       // composite / hashed keys: Map every row, then filter the words
       pa.passes = 0;  // (the histogram is counted by the last round's emit)
@@ -558,22 +580,33 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       launch_pack_hist(pa, cur, nullptr, hist, s);
       CKL("pack_hist");
     }
-    // word rounds: the first one for non-column keys, then refinements while a hashed round
-    // still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per key of the
-    // smaller side, with a fresh hash seed)
-    // (the first word round of a non-column key always runs: its emit counts the histogram)
+    // word rounds: the first one for non-column keys (sampled first), then refinements while a
+    // hashed round still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per
+    // key of the smaller side, with a fresh hash seed)
     for (int round = colpath ? 1 : 0;
-         round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
+         !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
       const uint64_t small = std::min(split, nw - split);
       uint32_t bbits = bits_for(8 * std::max<uint64_t>(small, 1));
       bbits = std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, bbits));
       const uint64_t bw = (1ull << bbits) / 32;
       const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
+      const uint64_t seed = 0x632BE59BD9B4E019ull * (round + 1);
       CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+      if (round == 0) {
+        CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+        {
+          KTimer kt(ctx, s, "filter_sample", 8ull * (small + (nw - small) / 16) + 8ull * bw, 2);
+          launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt, 0, sample, s);
+          CKL("filter_sample");
+        }
+        TRY(sample_says_skip(&skipped));
+        if (skipped) break;
+      }
       {
-        KTimer kt(ctx, s, "wfilter", 2ull * 8 * small + 8ull * (nw - small) + 16ull * bw + nw / 8, 4);
-        launch_wfilter(cur, nw, split, pl.ib, 0x632BE59BD9B4E019ull * (round + 1), bbits, bm,
-                       bm + bw, fmask, fcnt, s);
+        KTimer kt(ctx, s, "wfilter", (round ? 16ull : 8ull) * small + 8ull * (nw - small) +
+                                         16ull * bw + nw / 8, round ? 4 : 3);
+        launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt,
+                       round ? 2 : 1, sample, s);
         CKL("wfilter");
       }
       {
@@ -595,6 +628,20 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       split = nslA < ns ? ctx->pinned[1] : nw;
       std::swap(cur, alt);
       if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
+    }
+    if (skipped) {  // unfiltered: every row's word, the first digit's histogram
+      nw = n;
+      CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
+      if (colpath) {
+        const PackArgs pm = pack_args(pl, &a, &b);
+        KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
+        launch_pack_hist(pm, cur, nullptr, hist, s);
+        CKL("pack_hist");
+      } else {
+        KTimer kt(ctx, s, "key_hist", 8ull * n);
+        launch_key_hist(cur, n, pl.ib, 1, pl.passes == 1 ? pl.kb : 8, hist, s);
+        CKL("key_hist");
+      }
     }
     ctx->counters.last_filtered = n - nw;
     if (nw == 0) {

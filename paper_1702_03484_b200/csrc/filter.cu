@@ -28,6 +28,7 @@ constexpr int kFItems = 16;                    // rows per lane per slice
 constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
 constexpr uint32_t kDenseSlice = 160;          // survivors above which the emit walks items
+constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice
 
 // MODE 0: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic); 1: generic
 // packed composite key; 2: PATH_HASH key over exactly 2 columns; 3: PATH_HASH over nkey columns.
@@ -158,6 +159,42 @@ filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict_
     if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
     if (lane == 0) cnt[sd.slice0 + ws] = c;
     if (SET && c) set_bits(bm_set, bidx, keep, lane);
+  }
+}
+
+// Sampled probe: every `stride`-th warp slice of the side is probed against bm; sample[0] +=
+// survivors, sample[1] += rows probed.  Lets the host skip a filter that would drop little.
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads)
+filter_sample_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm,
+                     uint32_t bbits, uint32_t hashed, uint32_t stride,
+                     unsigned long long *__restrict__ sample) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  uint32_t c = 0, rows = 0;
+  for (uint64_t ws = ((uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5)) * stride;
+       ws * kFWarpRows < sd.rows; ws += nwarps * stride) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
+    uint32_t word[kFItems], bidx[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {  // all probes in flight together
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      bidx[it] = bit_index(key[it], bbits, hashed);
+      word[it] = j < sd.rows ? __ldg(bm + (bidx[it] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      rows += base + (uint64_t)it * 32 + lane < sd.rows;
+      c += word[it] >> (bidx[it] & 31) & 1u;
+    }
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  rows = __reduce_add_sync(0xffffffffu, rows);
+  if (lane == 0 && rows) {
+    atomicAdd(sample, (unsigned long long)c);
+    atomicAdd(sample + 1, (unsigned long long)rows);
   }
 }
 
@@ -371,6 +408,43 @@ wfilter_setmask_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbit
 }
 
 __global__ void __launch_bounds__(kFThreads)
+wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+                      const uint32_t *__restrict__ bm, uint32_t stride,
+                      unsigned long long *__restrict__ sample) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  uint32_t c = 0, rows = 0;
+  for (uint64_t ws = ((uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5)) * stride;
+       ws * kFWarpRows < sd.rows; ws += nwarps * stride) {
+    const uint64_t base = ws * kFWarpRows;
+    uint64_t w[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
+    }
+    uint32_t word[kFItems], bidx[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {  // all probes in flight together
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      bidx[it] = wbit(w[it], ib, seed, bbits);
+      word[it] = j < sd.rows ? __ldg(bm + (bidx[it] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      rows += base + (uint64_t)it * 32 + lane < sd.rows;
+      c += word[it] >> (bidx[it] & 31) & 1u;
+    }
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  rows = __reduce_add_sync(0xffffffffu, rows);
+  if (lane == 0 && rows) {
+    atomicAdd(sample, (unsigned long long)c);
+    atomicAdd(sample + 1, (unsigned long long)rows);
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads)
 wfilter_emit_kernel(const WSide sa, const WSide sb, const uint32_t *__restrict__ mask,
                     const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ off,
                     uint64_t *__restrict__ out, uint32_t *__restrict__ hist, uint32_t bit_lo,
@@ -435,6 +509,11 @@ Side side_of(const PackArgs &a, bool b) {
   return sd;
 }
 
+int sample_grid(uint64_t rows) {  // one warp per sampled slice (up to 148 x 8 CTAs)
+  const uint64_t sampled = ceil_div(ceil_div(rows, kFWarpRows), kSampleStride);
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(sampled, kFWarps), 148 * 8));
+}
+
 int grid_for_rows(uint64_t rows) {
   const uint64_t blocks = ceil_div(ceil_div(rows, kFWarpRows), kFWarps);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148 * 8));
@@ -447,11 +526,15 @@ int filter_mode(const PackArgs &a) {
 
 template <int MODE>
 void filter_passes(const PackArgs &a, const Side &S, const Side &L, uint32_t *bmS, uint32_t *bmL,
-                   uint32_t bbits, uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
+                   uint32_t bbits, uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
+                   unsigned long long *sample, cudaStream_t s) {
   const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  filter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
-  // the survivors of L set bmL inside the probe (C4: 3.9 ms vs 4.2 ms with a separate
-  // survivor pass; the word rounds, whose L survivors are denser, use the separate pass)
+  if (phase == 0) {  // build S, sample L
+    filter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
+    filter_sample_kernel<MODE><<<sample_grid(L.rows), kFThreads, 0, s>>>(
+        a, L, bmS, bbits, hashed, kSampleStride, sample);
+    return;
+  }
   filter_probe_kernel<MODE, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed, mask,
                                                            cnt);
   filter_probe_kernel<MODE, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
@@ -466,25 +549,34 @@ uint64_t filter_slices(uint64_t n1, uint64_t n2) {
 uint64_t filter_mask_words(uint64_t n1, uint64_t n2) { return filter_slices(n1, n2) * kFItems; }
 
 void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
-                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s) {
+                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
+                   unsigned long long *sample, cudaStream_t s) {
   const bool b_small = a.n2 < a.n1;
   const Side S = side_of(a, b_small), L = side_of(a, !b_small);
   switch (filter_mode(a)) {
-    case 0: filter_passes<0>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
-    case 1: filter_passes<1>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
-    case 2: filter_passes<2>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
-    default: filter_passes<3>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, s); break;
+    case 0: filter_passes<0>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
+    case 1: filter_passes<1>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
+    case 2: filter_passes<2>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
+    default: filter_passes<3>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
   }
 }
 
 void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
                     uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
-                    uint32_t *cnt, cudaStream_t s) {
+                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s) {
   const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
   const bool b_small = B.rows < A.rows;
   const WSide S = b_small ? B : A, L = b_small ? A : B;
   const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  if (S.rows) wfilter_build_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmS);
+  if (phase != 1) {  // build S (and, phase 0, sample L)
+    if (S.rows) wfilter_build_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmS);
+    if (phase == 0) {
+      if (L.rows)
+        wfilter_sample_kernel<<<sample_grid(L.rows), kFThreads, 0, s>>>(
+            L, ib, seed, bbits, bmS, kSampleStride, sample);
+      return;
+    }
+  }
   if (L.rows) {
     wfilter_probe_kernel<false><<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, nullptr, mask,
                                                          cnt);

@@ -368,18 +368,21 @@ constexpr uint64_t kSemijoinMinRows = 1ull << 20;  // AUTO: joins of at least th
 constexpr uint32_t kSemijoinBits = 29;             // 2 x 64 MB bitmaps at most (L2-sized)
 uint64_t filter_slices(uint64_t n1, uint64_t n2);      // 512-row warp slices (per side)
 uint64_t filter_mask_words(uint64_t n1, uint64_t n2);  // survivor-bit words
-// build bmS from the smaller side, probe the larger (setting bmL for its survivors), probe the
-// smaller against bmL: survivor bits + per-slice counts
+// Column round in two phases: phase 0 builds bmS from the smaller side S and probes a 1/16
+// sample of the larger side L (sample[0] += survivors, sample[1] += rows); phase 1 probes L
+// (setting bmL for its survivors) and then S against bmL: survivor bits + per-slice counts.
 void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
-                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, cudaStream_t s);
+                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
+                   unsigned long long *sample, cudaStream_t s);
 void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
                         const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s);
 // Refinement round on packed words ([0, split) side A, [split, n) side B; key' = w >> ib, bit =
 // mix(key' ^ seed)): the same three passes, then the emit copies the survivors to `out`
 // (sides stay contiguous) and counts their digit 0 into hist (if not NULL).
+// phase 0 = build + sample (as launch_filter), 1 = the rest, 2 = all of a round
 void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
                     uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
-                    uint32_t *cnt, cudaStream_t s);
+                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s);
 void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
                          const uint32_t *cnt, const uint64_t *off, uint64_t *out, uint32_t *hist,
                          uint32_t bit_lo, uint32_t dmask, cudaStream_t s);
