@@ -307,27 +307,49 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
 }
 
 // ---- refinement rounds on packed words (key' = w >> ib): words [0, split) are side A's,
-// [split, n) side B's (the emit keeps the sides contiguous).  The bit index mixes key' with a
+// [split, n) side B's (the emit keeps the sides contiguous).  The bitmaps are blocked Bloom
+// filters: a key sets/tests TWO bits of one 64-bit word (one memory access, like a plain bitmap,
+// but ~2/3 of its false positives at C5's load factor), chosen by a mix of key' with a
 // per-round seed, so a second round's false positives are independent of the first's.
 struct WSide {
   const uint64_t *w;
   uint64_t rows, slice0;
 };
 
-__device__ __forceinline__ uint32_t wbit(uint64_t w, uint32_t ib, uint64_t seed, uint32_t bbits) {
-  return (uint32_t)((((w >> ib) ^ seed) * 0x9E3779B97F4A7C15ull) >> (64 - bbits));
+__device__ __forceinline__ void wblock(uint64_t w, uint32_t ib, uint64_t seed, uint32_t bbits,
+                                       uint32_t &idx, uint64_t &m) {
+  const uint64_t h = ((w >> ib) ^ seed) * 0x9E3779B97F4A7C15ull;
+  idx = (uint32_t)(h >> (70 - bbits));  // 2^(bbits - 6) 64-bit words
+  const uint64_t g = h * 0xD6E8FEB86659FD93ull;
+  m = (1ull << (g >> 58)) | (1ull << ((g >> 52) & 63));
+}
+
+// set (idx, m) for the rows whose keep bit is set (fire-and-forget RED.OR: keys mostly distinct);
+// a lane whose left neighbour sets the same block bits skips
+__device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_t idx[kFItems],
+                                           const uint64_t m[kFItems], uint32_t keep,
+                                           uint32_t lane) {
+#pragma unroll
+  for (int it = 0; it < kFItems; it++) {
+    const uint32_t k = keep >> it & 1u;
+    const uint32_t ip = __shfl_up_sync(0xffffffffu, idx[it], 1);
+    const uint64_t mp = __shfl_up_sync(0xffffffffu, m[it], 1);
+    const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    const bool dup = lane > 0 && kp && ip == idx[it] && mp == m[it];
+    if (k && !dup) atomicOr(bm + idx[it], (unsigned long long)m[it]);
+  }
 }
 
 __global__ void __launch_bounds__(kFThreads)
 wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
-                     uint32_t *__restrict__ bm) {
+                     unsigned long long *__restrict__ bm) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < sd.rows; ws += nwarps) {
     const uint64_t base = ws * kFWarpRows;
-    uint32_t bidx[kFItems], keep = 0;
-    uint64_t w[kFItems];
+    uint32_t idx[kFItems], keep = 0;
+    uint64_t w[kFItems], m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
@@ -335,17 +357,16 @@ wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
-      bidx[it] = wbit(w[it], ib, seed, bbits);
+      wblock(w[it], ib, seed, bbits, idx[it], m[it]);
       keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
     }
-    set_bits<false>(bm, bidx, keep, lane);
+    set_blocks(bm, idx, m, keep, lane);
   }
 }
 
-template <bool SET>
 __global__ void __launch_bounds__(kFThreads)
 wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
-                     const uint32_t *__restrict__ bm_probe, uint32_t *__restrict__ bm_set,
+                     const unsigned long long *__restrict__ bm_probe,
                      uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
@@ -358,35 +379,34 @@ wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
     }
-    uint32_t word[kFItems], bidx[kFItems];
+    uint64_t v[kFItems], m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
-      bidx[it] = wbit(w[it], ib, seed, bbits);
-      word[it] = j < sd.rows ? __ldg(bm_probe + (bidx[it] >> 5)) : 0u;
+      uint32_t idx;
+      wblock(w[it], ib, seed, bbits, idx, m[it]);
+      v[it] = j < sd.rows ? __ldg(bm_probe + idx) : 0ull;
     }
-    uint32_t my = 0, c = 0, keep = 0;
+    uint32_t my = 0, c = 0;
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
-      const bool k = word[it] >> (bidx[it] & 31) & 1u;
+      const bool k = (v[it] & m[it]) == m[it] && base + (uint64_t)it * 32 + lane < sd.rows;
       const uint32_t bal = __ballot_sync(0xffffffffu, k);
-      keep |= (uint32_t)k << it;
       if (lane == (uint32_t)it) my = bal;
       c += __popc(bal);
     }
     if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
     if (lane == 0) cnt[sd.slice0 + ws] = c;
-    if (SET && c) set_bits<false>(bm_set, bidx, keep, lane);
   }
 }
 
-// Set bit(key') in bm for the survivors recorded in mask — a separate pass after
-// the probe, so only one bitmap is hot in L2 at a time (two 64 MB bitmaps overflow it):
-// C5's (?x, ?z) join 5.7 -> 4.7 ms over its three rounds.
+// Set the survivors' block bits in bm (recorded in mask) — a separate pass after the probe, so
+// only one bitmap is hot in L2 at a time (two 64 MB bitmaps overflow it): C5's (?x, ?z) join
+// 5.7 -> 4.7 ms over its three rounds.
 __global__ void __launch_bounds__(kFThreads)
 wfilter_setmask_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                        const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
-                       uint32_t *__restrict__ bm) {
+                       unsigned long long *__restrict__ bm) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
@@ -397,19 +417,20 @@ wfilter_setmask_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbit
 #pragma unroll
     for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
     const uint64_t base = ws * kFWarpRows;
-    uint32_t bidx[kFItems];
+    uint32_t idx[kFItems];
+    uint64_t m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
       const uint64_t w = (keep >> it & 1u) ? __ldcs(sd.w + base + (uint64_t)it * 32 + lane) : 0ull;
-      bidx[it] = wbit(w, ib, seed, bbits);
+      wblock(w, ib, seed, bbits, idx[it], m[it]);
     }
-    set_bits<false>(bm, bidx, keep, lane);
+    set_blocks(bm, idx, m, keep, lane);
   }
 }
 
 __global__ void __launch_bounds__(kFThreads)
 wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
-                      const uint32_t *__restrict__ bm, uint32_t stride,
+                      const unsigned long long *__restrict__ bm, uint32_t stride,
                       unsigned long long *__restrict__ sample) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
@@ -423,17 +444,19 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
     }
-    uint32_t word[kFItems], bidx[kFItems];
+    uint64_t v[kFItems], m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {  // all probes in flight together
       const uint64_t j = base + (uint64_t)it * 32 + lane;
-      bidx[it] = wbit(w[it], ib, seed, bbits);
-      word[it] = j < sd.rows ? __ldg(bm + (bidx[it] >> 5)) : 0u;
+      uint32_t idx;
+      wblock(w[it], ib, seed, bbits, idx, m[it]);
+      v[it] = j < sd.rows ? __ldg(bm + idx) : 0ull;
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
-      rows += base + (uint64_t)it * 32 + lane < sd.rows;
-      c += word[it] >> (bidx[it] & 31) & 1u;
+      const bool in = base + (uint64_t)it * 32 + lane < sd.rows;
+      rows += in;
+      c += in && (v[it] & m[it]) == m[it];
     }
   }
   c = __reduce_add_sync(0xffffffffu, c);
@@ -562,8 +585,11 @@ void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbi
 }
 
 void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
-                    uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
-                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s) {
+                    uint64_t seed, uint32_t bbits, uint32_t *bmS32, uint32_t *bmL32,
+                    uint32_t *mask, uint32_t *cnt, int phase, unsigned long long *sample,
+                    cudaStream_t s) {
+  unsigned long long *bmS = reinterpret_cast<unsigned long long *>(bmS32);
+  unsigned long long *bmL = reinterpret_cast<unsigned long long *>(bmL32);
   const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
   const bool b_small = B.rows < A.rows;
   const WSide S = b_small ? B : A, L = b_small ? A : B;
@@ -578,13 +604,10 @@ void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t 
     }
   }
   if (L.rows) {
-    wfilter_probe_kernel<false><<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, nullptr, mask,
-                                                         cnt);
+    wfilter_probe_kernel<<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, mask, cnt);
     wfilter_setmask_kernel<<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, mask, cnt, bmL);
   }
-  if (S.rows)
-    wfilter_probe_kernel<false><<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmL, nullptr, mask,
-                                                         cnt);
+  if (S.rows) wfilter_probe_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmL, mask, cnt);
 }
 
 void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
