@@ -426,14 +426,14 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
         next_shift, next_mask);
   } else {
-    // P64 words: 8192-key tiles, 2 CTAs/SM, keys re-read from L2 for placement.  Peers found by
-    // shared-memory atomicOr with a warp-uniform shortcut (tools/radix_ablate.cu, 4e8-word C4
-    // Zipf sort: 9.70 ms vs 10.72 match.any / 10.57 ballot; random digits 2.00 vs 2.86 / 2.22 ms
-    // per 3e8 words).
-    constexpr int kItems = 32;
+    // P64 words: 6144-key tiles, 3 CTAs/SM, keys re-read from L2 for placement.  Peers found by
+    // shared-memory atomicOr with a warp-uniform shortcut (tools/radix_ablate.cu: a C4-shaped
+    // 4e8-word Zipf sort 9.70 ms vs 10.72 with match.any / 10.57 with ballots at 8192-key tiles;
+    // 6144-key tiles at 3 CTAs/SM then 8.89 ms, C5's join words -7%).
+    constexpr int kItems = 24;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = radix_pass_kernel<false, kItems, 4, 2, true, 3>;
+    auto kern = radix_pass_kernel<false, kItems, 4, 3, true, 3>;
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,

@@ -8,4 +8,4 @@ for j in 1 2; do
 import json; [print('J%d'%m['join'], m['path'], m['ib'], m['kb']) for m in json.load(open('/tmp/c5w_meta.json'))]"))"
   timeout 600 tools/radix_ablate file $path $ib $kb
 done
-timeout 600 tools/radix_ablate zipf 400000000
+timeout 900 tools/radix_ablate zipf 400000000
