@@ -25,6 +25,18 @@ import torch
 import torch.distributed as dist
 
 
+# bytes and rows this process sent to OTHER ranks (both exchange paths), for reporting the
+# exchange volume against NVLink bandwidth (bench.py)
+EXCHANGE = {"bytes_sent": 0, "rows_sent": 0, "exchanges": 0}
+
+
+def _account(counts: Sequence[int], rank: int, ncols: int):
+    rows = sum(int(c) for d, c in enumerate(counts) if d != rank)
+    EXCHANGE["rows_sent"] += rows
+    EXCHANGE["bytes_sent"] += 4 * ncols * rows
+    EXCHANGE["exchanges"] += 1
+
+
 def exchange_counts(counts: Sequence[int], group=None) -> List[int]:
     """all-to-all of per-destination row counts: returns the per-source counts received."""
     world = dist.get_world_size(group)
@@ -136,6 +148,7 @@ def redistribute_fused(ctx, table, key_vars, slot: int, group=None):
     import paper_1702_03484_b200 as mq
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     state, counts = ctx.partition_plan(table, list(key_vars), world)
+    _account(counts, rank, len(table.vars))
     dev = torch.device("cuda", torch.cuda.current_device())
     mine = torch.tensor(counts, dtype=torch.int64, device=dev)
     allc = [torch.empty_like(mine) for _ in range(world)]
@@ -162,6 +175,7 @@ def redistribute(ctx, table, key_vars, group=None, partition_fn: Callable = None
         cols, vars_ = part.columns, part.vars
     else:
         vars_, cols, counts = partition_fn(table, list(key_vars), world)
+    _account(counts, dist.get_rank(group), len(vars_))
     recv = exchange_counts(counts, group)
     return vars_, exchange_columns(cols, counts, recv, group), recv
 
