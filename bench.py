@@ -181,6 +181,26 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+# random bitmap probes/s one B200 sustains from a 2^29-bit (L2-resident) bitmap through the
+# read-only path, 5e8 probes (tools/bitmap_bench.cu, `probe ilp4 nc 2^29 bits`)
+FILTER_PROBE_PEAK = 418e9
+
+
+def filter_rate(st, steps, step_ms_total):
+    """The semi-join filter kernels are bound by random L1/L2 bitmap accesses, not by HBM: their
+    access rate against the measured probe rate (the HBM roofline understates them)."""
+    names = ("filter_sample", "filter", "wfilter")
+    ms = sum(st["kernels"][k]["ms"] for k in names if k in st["kernels"])
+    acc = st.get("filter_accesses", 0)
+    if not ms or not acc:
+        return None
+    rate = acc / (ms / 1e3)
+    return {"accesses_per_step": acc / steps, "rate": rate, "peak": FILTER_PROBE_PEAK,
+            "unit": "accesses/s", "frac": rate / FILTER_PROBE_PEAK,
+            "share_of_step": ms / step_ms_total, "kernels": [k for k in names if k in st["kernels"]],
+            "peak_source": "tools/bitmap_bench.cu probe ilp4 nc 2^29 bits (B200, measured)"}
+
+
 def run_gpu(args):
     import torch
     import paper_1702_03484_b200 as mq
@@ -312,6 +332,7 @@ def run_gpu(args):
                          "timing": "per-kernel CUDA events on the library stream, second timed region"},
             "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
                             "share": v["ms"] / sum(prof_ms)} for k, v in st_k["kernels"].items()},
+            "filter": filter_rate(st_k, args.steps, sum(prof_ms)),
             "clocks": clocks, "gpu_launches": st_plain["launches"]}
 
     # e2e through the public API from pinned host buffers (H2D + query + D2H inside the region)

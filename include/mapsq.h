@@ -149,6 +149,8 @@ typedef struct {
   uint64_t last_kb, last_ib, last_passes, last_path;
   uint64_t last_groups;    /* groups (keys on both sides) of the last join */
   uint64_t last_filtered;  /* rows the semi-join filter dropped in the last join */
+  uint64_t filter_accesses;/* random bitmap accesses of the filter since the reset: builds and
+                              probes (survivors setting the larger side's bits not counted) */
   uint32_t nkernels;
   mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
 } mapsq_stats;

@@ -75,6 +75,7 @@ class _Stats(ctypes.Structure):
                 ("last_kb", ctypes.c_uint64), ("last_ib", ctypes.c_uint64),
                 ("last_passes", ctypes.c_uint64), ("last_path", ctypes.c_uint64),
                 ("last_groups", ctypes.c_uint64), ("last_filtered", ctypes.c_uint64),
+                ("filter_accesses", ctypes.c_uint64),
                 ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
 
 

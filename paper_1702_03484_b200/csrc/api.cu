@@ -546,6 +546,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
                                                8ull * bw, 2);
         launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 0, sample, s);
         CKL("filter_sample");
+        ctx->counters.filter_accesses += std::min(n1, n2) + std::max(n1, n2) / 16;
       }
       TRY(sample_says_skip(&skipped));
       if (!skipped) {
@@ -554,6 +555,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
                                           16ull * bw + n / 8, 2);
           launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 1, sample, s);
           CKL("filter");
+          ctx->counters.filter_accesses += std::max(n1, n2) + std::min(n1, n2);
         }
         {
           KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
@@ -598,6 +600,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
           KTimer kt(ctx, s, "filter_sample", 8ull * (small + (nw - small) / 16) + 8ull * bw, 2);
           launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt, 0, sample, s);
           CKL("filter_sample");
+          ctx->counters.filter_accesses += small + (nw - small) / 16;
         }
         TRY(sample_says_skip(&skipped));
         if (skipped) break;
@@ -608,6 +611,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
         launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt,
                        round ? 2 : 1, sample, s);
         CKL("wfilter");
+        ctx->counters.filter_accesses += (round ? small : 0) + (nw - small) + small;
       }
       {
         KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
