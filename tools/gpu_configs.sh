@@ -1,3 +1,4 @@
+# all GPU tests, then every config (and the filter-off variants) with per-kernel times
 python build.py > /dev/null 2>&1 || exit 1
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 for c in "C5" "C4" "C3" "C4 --semijoin off" "C5 --semijoin off" "C2" "C1"; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e 2>/dev/null | python -c "

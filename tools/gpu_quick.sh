@@ -1,3 +1,4 @@
+# quick GPU check: semi-join/parity/index tests, C5 per-join diagnostics, C4/C5 with the filter on/off
 python build.py > /dev/null 2>&1 || exit 1
 mkdir -p gpurun_out/q3; rm -f gpurun_out/q3/*
 timeout 900 python -m pytest tests/test_gpu_semijoin.py tests/test_gpu_parity.py tests/test_gpu_index.py -x -q > gpurun_out/q3/pytest.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/q3/pytest.log
