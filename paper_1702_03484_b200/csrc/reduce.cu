@@ -228,9 +228,8 @@ find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restr
 
 // ------------------------------------------------------------------------------ expand (K6)
 constexpr int kEThreads = 256;
-constexpr int kERows = 4;                    // consecutive rows per chunk (one 16 B store)
-constexpr int kEChunks = 2;                  // chunks per thread
-constexpr uint64_t kETile = (uint64_t)kEThreads * kERows * kEChunks;
+constexpr int kERowsPerThread = 8;           // rows per thread = chunks x rows per chunk
+constexpr uint64_t kETile = (uint64_t)kEThreads * kERowsPerThread;
 constexpr int kEGroups = 1024;               // groups staged in shared memory per tile
 
 // K5b: tile t of the expansion (rows [t * kETile, ...)) starts inside group tile_g0[t].  One thread
@@ -262,8 +261,10 @@ __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, u
 // t0 + (c * kEThreads + t) * kERows, so a warp's chunks are contiguous): it locates its group in
 // shared memory, then computes the 8 (LEFT, RIGHT) positions, issues all word loads, then all
 // column gathers, then 16 B streaming stores — so the latencies of one thread's rows overlap.
+template <int kERows, int kEChunks>
 __global__ void __launch_bounds__(kEThreads)
 expand_kernel(const ExpandArgs a) {
+  static_assert(kERows * kEChunks == kERowsPerThread && kERows % 4 == 0, "tile shape");
   __shared__ const uint32_t *s_src[MAPSQ_MAX_COLS];
   __shared__ uint32_t *s_dst[MAPSQ_MAX_COLS];
   __shared__ uint64_t s_g[2];
@@ -402,8 +403,10 @@ expand_kernel(const ExpandArgs a) {
       const uint64_t r0 = t0 + ((uint64_t)c * kEThreads + tid) * kERows;
       uint32_t *dst = s_dst[col] + r0;
       if (nrow[c] == kERows) {
-        st_cs_v4(dst, make_uint4(val[c * kERows], val[c * kERows + 1], val[c * kERows + 2],
-                                 val[c * kERows + 3]));
+#pragma unroll
+        for (int v4 = 0; v4 < kERows; v4 += 4)
+          st_cs_v4(dst + v4, make_uint4(val[c * kERows + v4], val[c * kERows + v4 + 1],
+                                        val[c * kERows + v4 + 2], val[c * kERows + v4 + 3]));
       } else {
 #pragma unroll
         for (int j = 0; j < kERows; j++)  // (static indices: no local-memory copy of val[])
@@ -530,7 +533,13 @@ void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   const uint64_t nblocks = ceil_div(a.m, kETile);
   const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(a.ngroups, 256), 148 * 16));
   tile_groups_kernel<<<gg, 256, 0, s>>>(a.goff, a.ngroups, a.m, const_cast<uint64_t *>(a.tile_g0));
-  expand_kernel<<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
+  // long runs of one group (C3's star: ~2e4 rows per group) favour 2 chunks of 4 rows per
+  // thread; short groups (C5's first join: ~20 rows) one chunk of 8 rows (C3 2.50 vs 2.72 ms,
+  // C5 J1 0.88 vs 0.81 ms)
+  if (a.m >= 256 * a.ngroups)
+    expand_kernel<4, 2><<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
+  else
+    expand_kernel<8, 1><<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
 }
 
 }  // namespace mapsq
