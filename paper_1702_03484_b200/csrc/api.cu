@@ -443,6 +443,14 @@ PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_
   return pa;
 }
 
+// filter rounds with hashed bitmaps: ~8 bits per key of the smaller side (at most 2^29 bits, so
+// one bitmap stays L2-resident) and a fresh seed per round
+uint32_t word_round_bits(uint64_t small) {
+  const uint32_t b = bits_for(8 * std::max<uint64_t>(small, 1));
+  return std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, b));
+}
+uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(round + 1); }
+
 // ------------------------------------------------------------------------------ join
 mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_table *tp2_in,
                        mapsq_table *rs, cudaStream_t s) {
@@ -529,22 +537,30 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       *skip = ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9;
       return MAPSQ_OK;
     };
-    // round 0 reads the key column directly for a single packed column; other keys are Mapped
-    // first and filtered as words (on C5's (?x, ?z) join: pack + word round 5.6 ms vs 6.9 ms
-    // for hashing the two columns inside the filter passes)
-    const bool colpath = pa.nkey == 1 && pl.kb <= 32 && !pa.hash;
+    // round 0 reads the key columns directly — a single packed column (exact or hashed bitmap),
+    // or a hashed composite key (blocked Bloom bitmaps, key_hash computed from the columns); other
+    // packed composite keys are Mapped first and filtered as words
+    const bool colhash = pa.hash;
+    const bool colpath = (pa.nkey == 1 && pl.kb <= 32 && !pa.hash) || colhash;
     if (colpath) {
-      // round 0 on the key column (no word is written for a dropped row)
-      const uint32_t bbits = std::min<uint32_t>(pl.kb, kSemijoinBits);
-      const uint32_t hashed = pl.kb > bbits;
+      // round 0 on the key columns (no word is written for a dropped row)
+      const uint32_t bbits = colhash ? word_round_bits(std::min(n1, n2))
+                                     : std::min<uint32_t>(pl.kb, kSemijoinBits);
+      const uint32_t hashed = colhash || pl.kb > bbits;
       const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
       const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
       CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
       CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+      auto col_round = [&](int phase) {
+        if (colhash)
+          launch_cfilter(pa, bm, bm + bw, bbits, word_round_seed(0), fmask, fcnt, phase, sample, s);
+        else
+          launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, phase, sample, s);
+      };
       {
         KTimer kt(ctx, s, "filter_sample", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2) / 16) +
                                                8ull * bw, 2);
-        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 0, sample, s);
+        col_round(0);
         CKL("filter_sample");
         ctx->counters.filter_accesses += std::min(n1, n2) + std::max(n1, n2) / 16;
       }
@@ -552,8 +568,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       if (!skipped) {
         {
           KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2)) +
-                                          16ull * bw + n / 8, 2);
-          launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, 1, sample, s);
+                                          16ull * bw + n / 8, colhash ? 3 : 2);
+          col_round(1);
           CKL("filter");
           ctx->counters.filter_accesses += std::max(n1, n2) + std::min(n1, n2);
         }
@@ -573,7 +589,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
         split = nslA < ns ? ctx->pinned[1] : nw;
         // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
         // says the keys mostly match, so refinement rounds would not pay
-        exact = !hashed || nw * 10 > n * 9;
+        exact = (!hashed && !colhash) || nw * 10 > n * 9;
       }
     } else {
       // composite / hashed keys: Map every row, then filter the words
@@ -588,11 +604,10 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     for (int round = colpath ? 1 : 0;
          !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
       const uint64_t small = std::min(split, nw - split);
-      uint32_t bbits = bits_for(8 * std::max<uint64_t>(small, 1));
-      bbits = std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, bbits));
+      const uint32_t bbits = word_round_bits(small);
       const uint64_t bw = (1ull << bbits) / 32;
       const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
-      const uint64_t seed = 0x632BE59BD9B4E019ull * (round + 1);
+      const uint64_t seed = word_round_seed(round);
       CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
       if (round == 0) {
         CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));

@@ -467,6 +467,130 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
   }
 }
 
+// ---- hashed composite keys, first round on the key columns (no word is written for a dropped
+// row): the word rounds' blocked Bloom bitmaps and pass structure, with key' = key_hash of the
+// row's shared columns computed from the columns (load_keys<MODE>, MODE 2/3).
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads)
+cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+                     unsigned long long *__restrict__ bm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
+    uint32_t idx[kFItems], keep = 0;
+    uint64_t m[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      wblock(key[it], 0, seed, bbits, idx[it], m[it]);
+      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+    }
+    set_blocks(bm, idx, m, keep, lane);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads)
+cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+                     const unsigned long long *__restrict__ bm_probe,
+                     uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
+    uint64_t v[kFItems], m[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      uint32_t idx;
+      wblock(key[it], 0, seed, bbits, idx, m[it]);
+      v[it] = j < sd.rows ? __ldg(bm_probe + idx) : 0ull;
+    }
+    uint32_t my = 0, c = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const bool k = (v[it] & m[it]) == m[it] && base + (uint64_t)it * 32 + lane < sd.rows;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      if (lane == (uint32_t)it) my = bal;
+      c += __popc(bal);
+    }
+    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
+    if (lane == 0) cnt[sd.slice0 + ws] = c;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads)
+cfilter_setmask_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+                       const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
+                       unsigned long long *__restrict__ bm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    if (__ldg(cnt + sd.slice0 + ws) == 0) continue;  // warp-uniform
+    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + (sd.slice0 + ws) * kFItems + lane) : 0u;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key, keep);
+    uint32_t idx[kFItems];
+    uint64_t m[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) wblock(key[it], 0, seed, bbits, idx[it], m[it]);
+    set_blocks(bm, idx, m, keep, lane);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads)
+cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+                      const unsigned long long *__restrict__ bm, uint32_t stride,
+                      unsigned long long *__restrict__ sample) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  uint32_t c = 0, rows = 0;
+  for (uint64_t ws = ((uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5)) * stride;
+       ws * kFWarpRows < sd.rows; ws += nwarps * stride) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE>(a, sd, base, lane, key);
+    uint64_t v[kFItems], m[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const uint64_t j = base + (uint64_t)it * 32 + lane;
+      uint32_t idx;
+      wblock(key[it], 0, seed, bbits, idx, m[it]);
+      v[it] = j < sd.rows ? __ldg(bm + idx) : 0ull;
+    }
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      const bool in = base + (uint64_t)it * 32 + lane < sd.rows;
+      rows += in;
+      c += in && (v[it] & m[it]) == m[it];
+    }
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  rows = __reduce_add_sync(0xffffffffu, rows);
+  if (lane == 0 && rows) {
+    atomicAdd(sample, (unsigned long long)c);
+    atomicAdd(sample + 1, (unsigned long long)rows);
+  }
+}
+
+template <int MODE>
+void cfilter_passes(const PackArgs &a, const Side &S, const Side &L, unsigned long long *bmS,
+                    unsigned long long *bmL, uint32_t bbits, uint64_t seed, uint32_t *mask,
+                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s);
+
 __global__ void __launch_bounds__(kFThreads)
 wfilter_emit_kernel(const WSide sa, const WSide sb, const uint32_t *__restrict__ mask,
                     const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ off,
@@ -564,6 +688,22 @@ void filter_passes(const PackArgs &a, const Side &S, const Side &L, uint32_t *bm
                                                             mask, cnt);
 }
 
+template <int MODE>
+void cfilter_passes(const PackArgs &a, const Side &S, const Side &L, unsigned long long *bmS,
+                    unsigned long long *bmL, uint32_t bbits, uint64_t seed, uint32_t *mask,
+                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s) {
+  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
+  if (phase == 0) {  // build S, sample L
+    cfilter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, seed, bbits, bmS);
+    cfilter_sample_kernel<MODE><<<sample_grid(L.rows), kFThreads, 0, s>>>(
+        a, L, seed, bbits, bmS, kSampleStride, sample);
+    return;
+  }
+  cfilter_probe_kernel<MODE><<<gl, kFThreads, 0, s>>>(a, L, seed, bbits, bmS, mask, cnt);
+  cfilter_setmask_kernel<MODE><<<gl, kFThreads, 0, s>>>(a, L, seed, bbits, mask, cnt, bmL);
+  cfilter_probe_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, seed, bbits, bmL, mask, cnt);
+}
+
 }  // namespace
 
 uint64_t filter_slices(uint64_t n1, uint64_t n2) {
@@ -582,6 +722,19 @@ void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbi
     case 2: filter_passes<2>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
     default: filter_passes<3>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
   }
+}
+
+void launch_cfilter(const PackArgs &a, uint32_t *bmS32, uint32_t *bmL32, uint32_t bbits,
+                    uint64_t seed, uint32_t *mask, uint32_t *cnt, int phase,
+                    unsigned long long *sample, cudaStream_t s) {
+  unsigned long long *bmS = reinterpret_cast<unsigned long long *>(bmS32);
+  unsigned long long *bmL = reinterpret_cast<unsigned long long *>(bmL32);
+  const bool b_small = a.n2 < a.n1;
+  const Side S = side_of(a, b_small), L = side_of(a, !b_small);
+  if (a.nkey == 2)
+    cfilter_passes<2>(a, S, L, bmS, bmL, bbits, seed, mask, cnt, phase, sample, s);
+  else
+    cfilter_passes<3>(a, S, L, bmS, bmL, bbits, seed, mask, cnt, phase, sample, s);
 }
 
 void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,

@@ -379,6 +379,11 @@ void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t 
 // Refinement round on packed words ([0, split) side A, [split, n) side B; key' = w >> ib, bit =
 // mix(key' ^ seed)): the same three passes, then the emit copies the survivors to `out`
 // (sides stay contiguous) and counts their digit 0 into hist (if not NULL).
+// Hashed composite keys (PATH_HASH): the first round on the key columns with the word rounds'
+// blocked Bloom bitmaps (bbits, seed); phases as launch_filter; launch_filter_emit writes words.
+void launch_cfilter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
+                    uint64_t seed, uint32_t *mask, uint32_t *cnt, int phase,
+                    unsigned long long *sample, cudaStream_t s);
 // phase 0 = build + sample (as launch_filter), 1 = the rest, 2 = all of a round
 void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
                     uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
