@@ -36,22 +36,27 @@ for r in rows[2:]:
     traffic.setdefault(short, []).append(rd + wr)
 # DRAM bytes per invocation of each library timer (bench.py's kernel names): a timer may cover
 # several kernels; its invocations are counted by its anchor kernel
-TIMERS = {  # timer: (member kernels, anchor)
-    "radix_pass": (["radix_pass"], "radix_pass"),
-    "wfilter": (["wfilter_build", "wfilter_probe", "wfilter_setmask"], "wfilter_setmask"),
-    "filter": (["filter_build", "filter_probe"], "filter_build"),
-    "filter_emit": (["filter_emit"], "filter_emit"),
-    "wfilter_emit": (["wfilter_emit"], "wfilter_emit"),
-    "pack_hist": (["pack_hist"], "pack_hist"),
-    "find_groups": (["find_groups"], "find_groups"),
-    "expand": (["tile_groups", "expand"], "expand"),
-    "residual_count": (["residual_count"], "residual_count"),
-    "residual_expand": (["residual_expand"], "residual_expand"),
-    "scan_write": (["scan_write"], "scan_write"),
+TIMERS = {  # timer: (member kernels, invocations from the launch counts)
+    "radix_pass": (["radix_pass"], lambda c: c("radix_pass")),
+    "wfilter": (["wfilter_build", "wfilter_probe", "wfilter_setmask"],
+                lambda c: c("wfilter_setmask")),
+    "filter_sample": (["filter_build", "filter_sample", "cfilter_build", "cfilter_sample",
+                       "wfilter_sample"],
+                      lambda c: c("filter_sample") + c("cfilter_sample") + c("wfilter_sample")),
+    "filter": (["filter_probe", "cfilter_probe", "cfilter_setmask"],
+               lambda c: c("filter_probe") // 2 + c("cfilter_setmask")),
+    "filter_emit": (["filter_emit"], lambda c: c("filter_emit")),
+    "wfilter_emit": (["wfilter_emit"], lambda c: c("wfilter_emit")),
+    "pack_hist": (["pack_hist"], lambda c: c("pack_hist")),
+    "find_groups": (["find_groups"], lambda c: c("find_groups")),
+    "expand": (["tile_groups", "expand"], lambda c: c("expand")),
+    "residual_count": (["residual_count"], lambda c: c("residual_count")),
+    "residual_expand": (["residual_expand"], lambda c: c("residual_expand")),
+    "scan_write": (["scan_write"], lambda c: c("scan_write")),
 }
 per_timer = {}
-for timer, (members, anchor) in TIMERS.items():
-    inv = len(traffic.get(anchor, []))
+for timer, (members, inv_of) in TIMERS.items():
+    inv = inv_of(lambda k: len(traffic.get(k, [])))
     if inv:
         per_timer[timer] = sum(sum(traffic.get(m, [])) for m in members) / inv
 if len(sys.argv) > 2:
