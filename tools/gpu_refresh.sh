@@ -24,7 +24,21 @@ if [ "${NCU:-1}" = 1 ]; then
     --log-file $OUT/ncu_launches_C5.csv python bench.py --steps 1 --warmup 3 --no-e2e \
     --no-cpu-baseline > $OUT/ncu_l.log 2>&1
   echo "ncu launches exit $?"
-  # one full capture of every kernel of one step (skip the warm-up step's launches)
+  # one full capture of every kernel of one step: skip/count from the launch list (the step ends
+  # with residual_expand; the first timed step follows the 3 warm-up steps)
+  read SKIP COUNT <<< "$(python - $OUT/ncu_launches_C5.csv <<'PY'
+import csv, re, sys
+rows = list(csv.reader(open(sys.argv[1])))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+ki = rows[hi].index("Kernel Name")
+names = [r[ki] for r in rows[hi + 1:] if len(r) > ki]
+rx = re.compile("radix_pass|wfilter|filter_|find_groups|expand|residual|pack_hist")
+ends = [i for i, n in enumerate(names) if "residual_expand" in n]
+start, end = ends[2] + 1, ends[3] + 1
+print(sum(bool(rx.search(n)) for n in names[:start]), sum(bool(rx.search(n)) for n in names[start:end]))
+PY
+)"
+  echo "full capture: skip $SKIP count $COUNT"
   timeout 1500 ncu --set full --clock-control none --import-source on \
     -k regex:"radix_pass|wfilter|filter_|find_groups|expand|residual|pack_hist" \
     --launch-skip ${SKIP:-101} --launch-count ${COUNT:-33} -o $OUT/ncu_full_C5 -f \
@@ -32,7 +46,7 @@ if [ "${NCU:-1}" = 1 ]; then
   echo "ncu full exit $?"
   ncu -i $OUT/ncu_full_C5.ncu-rep --page raw --csv > $OUT/ncu_full_C5_raw.csv 2>/dev/null
   ncu -i $OUT/ncu_full_C5.ncu-rep --page details --csv > $OUT/ncu_full_C5_details.csv 2>/dev/null
-  for k in radix_pass wfilter_probe wfilter_build find_groups; do
+  for k in radix_pass cfilter_probe wfilter_probe find_groups; do
     ncu -i $OUT/ncu_full_C5.ncu-rep --page source --csv --kernel-name regex:$k --launch-count 1 \
       > $OUT/ncu_source_$k.csv 2>/dev/null
   done
