@@ -256,8 +256,6 @@ int launch_exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uin
 int launch_exclusive_scan_u64_dev(const uint64_t *in, uint64_t *out, const uint64_t *n_dev,
                                   uint64_t cap, uint64_t *tmp, uint64_t *total_dev,
                                   cudaStream_t s);
-// exclusive scan over kMaxPasses x 256 digit histograms (in place, one block per pass)
-void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s);
 
 struct PackArgs {
   uint32_t nkey;

@@ -117,23 +117,6 @@ key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, 
   }
 }
 
-__global__ void __launch_bounds__(kRadix) hist_scan_kernel(uint32_t *hist) {
-  __shared__ uint32_t s_w[kRadix / 32];
-  uint32_t *h = hist + (uint64_t)blockIdx.x * kRadix;
-  const uint32_t v = h[threadIdx.x];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  uint32_t pre = 0;
-  for (int w = 0; w < warp; w++) pre += s_w[w];
-  h[threadIdx.x] = pre + x - v;
-}
-
 // One stable digit pass.  Tile = kSortThreads x ITEMS keys; warp w owns the contiguous
 // slice [w*32*ITEMS, (w+1)*32*ITEMS) of its tile and reads it item-major (item it, lane l ->
 // slice[it*32 + l]) so every load is a coalesced 256 B row.  Intra-tile indices are 32-bit and
@@ -405,10 +388,6 @@ void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t
                      uint32_t last_bits, uint32_t *hist, cudaStream_t s) {
   const int g = grid_for(n, kHistThreads * kHistItems);
   key_hist_kernel<<<g, kHistThreads, 0, s>>>(keys, n, bit_lo, passes, (1u << last_bits) - 1u, hist);
-}
-
-void launch_hist_scan(uint32_t *hist, int passes, cudaStream_t s) {
-  hist_scan_kernel<<<passes, kRadix, 0, s>>>(hist);
 }
 
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,

@@ -33,16 +33,6 @@ struct WordView {
   __device__ __forceinline__ uint64_t key(uint64_t i) const {
     return words ? (words[i] >> ib) : keys[i];
   }
-  __device__ __forceinline__ void load(uint64_t i, uint64_t *k, bool *r) const {
-    if (words) {
-      const uint64_t w = __ldcs(words + i);
-      *k = w >> ib;
-      *r = (w & idx_mask) >= n1;
-    } else {
-      *k = __ldcs(keys + i);
-      *r = __ldcs(vals + i) >= n1;
-    }
-  }
 };
 
 // first index of the run of key k that contains position `from` (key(from) == k), by galloping
