@@ -208,7 +208,7 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_gpu_dist(args, world, rank, local)
     torch.cuda.set_device(local)
     cfg = args.config
@@ -473,6 +473,8 @@ def main():
                     help="semi-join key-presence filter in front of the Map (auto: joins of "
                          ">= 2^20 rows)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="testing: run the multi-GPU path (exchange per join) even at world size 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
