@@ -83,7 +83,15 @@ def _worker(rank, world, port, q):
         C = HostTable([0, 3], [rng.integers(0, 50, 300 + 7 * rank), rng.integers(0, 5, 300 + 7 * rank)])
         D = HostTable([1, 3], [rng.integers(0, 9, 200), rng.integers(0, 5, 200)])
         kw = dict(partition_fn=np_partition, join_fn=oracle_join, wrap_fn=wrap)
+        x0 = dict(mqd.EXCHANGE)
+        _, _, ca = np_partition(A, [0], world)
+        _, _, cb = np_partition(B, [0], world)
         r1, key1 = mqd.join_dist(None, A, B, **kw)
+        # exchange accounting: bytes of the rows this rank sent to the OTHER rank
+        other = 1 - rank
+        assert mqd.EXCHANGE["exchanges"] - x0["exchanges"] == 2
+        assert mqd.EXCHANGE["rows_sent"] - x0["rows_sent"] == ca[other] + cb[other]
+        assert mqd.EXCHANGE["bytes_sent"] - x0["bytes_sent"] == 8 * (ca[other] + cb[other])
         # same key (?0): acc is not re-partitioned
         r2, key2 = mqd.join_dist(None, r1, C, tp1_partitioned_on=key1, **kw)
         # key change (?1, ?3): both sides exchanged on the composite key
