@@ -52,7 +52,9 @@ struct Side {
 
 // key' of rows base + it * 32 + lane (it < kFItems), column-outer loads (all of a column's
 // loads in flight together); rows >= rows get key' 0 (callers mask them)
-template <int MODE>
+// FINAL = false (hash modes, filter-only uses): the key_hash chain without its final mix — the
+// filter's bitmap index mixes again, and only the words need the exact key'.
+template <int MODE, bool FINAL = true>
 __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
                                           uint32_t lane, KeyT<MODE> key[kFItems],
                                           uint32_t keep = 0xffffu) {
@@ -75,7 +77,7 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
                      : (KeyT<MODE>)(hash ? key_hash_step(key[it], v[it])
                                          : (key[it] | (uint64_t)(v[it] - lo) << sh));
   }
-  if (hash) {
+  if (hash && FINAL) {
 #pragma unroll
     for (int it = 0; it < kFItems; it++) key[it] = (KeyT<MODE>)key_hash_final(key[it], a.kb);
   }
@@ -480,7 +482,7 @@ cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
        ws * kFWarpRows < sd.rows; ws += nwarps) {
     const uint64_t base = ws * kFWarpRows;
     KeyT<MODE> key[kFItems];
-    load_keys<MODE>(a, sd, base, lane, key);
+    load_keys<MODE, false>(a, sd, base, lane, key);
     uint32_t idx[kFItems], keep = 0;
     uint64_t m[kFItems];
 #pragma unroll
@@ -503,7 +505,7 @@ cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
        ws * kFWarpRows < sd.rows; ws += nwarps) {
     const uint64_t base = ws * kFWarpRows;
     KeyT<MODE> key[kFItems];
-    load_keys<MODE>(a, sd, base, lane, key);
+    load_keys<MODE, false>(a, sd, base, lane, key);
     uint64_t v[kFItems], m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
@@ -541,7 +543,7 @@ cfilter_setmask_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t 
     for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
     const uint64_t base = ws * kFWarpRows;
     KeyT<MODE> key[kFItems];
-    load_keys<MODE>(a, sd, base, lane, key, keep);
+    load_keys<MODE, false>(a, sd, base, lane, key, keep);
     uint32_t idx[kFItems];
     uint64_t m[kFItems];
 #pragma unroll
@@ -562,7 +564,7 @@ cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t b
        ws * kFWarpRows < sd.rows; ws += nwarps * stride) {
     const uint64_t base = ws * kFWarpRows;
     KeyT<MODE> key[kFItems];
-    load_keys<MODE>(a, sd, base, lane, key);
+    load_keys<MODE, false>(a, sd, base, lane, key);
     uint64_t v[kFItems], m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
