@@ -472,6 +472,13 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
 // ---- hashed composite keys, first round on the key columns (no word is written for a dropped
 // row): the word rounds' blocked Bloom bitmaps and pass structure, with key' = key_hash of the
 // row's shared columns computed from the columns (load_keys<MODE>, MODE 2/3).
+// the column round's block index and bit pair straight from the 64-bit key_hash chain value
+// (already mixed: no further multiply)
+__device__ __forceinline__ void cblock(uint64_t h, uint32_t bbits, uint32_t &idx, uint64_t &m) {
+  idx = (uint32_t)(h >> (70 - bbits));
+  m = (1ull << (h & 63)) | (1ull << ((h >> 6) & 63));
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kFThreads)
 cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
@@ -487,7 +494,7 @@ cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
     uint64_t m[kFItems];
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
-      wblock(key[it], 0, seed, bbits, idx[it], m[it]);
+      cblock(key[it], bbits, idx[it], m[it]);
       keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
     }
     set_blocks(bm, idx, m, keep, lane);
@@ -511,7 +518,7 @@ cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
-      wblock(key[it], 0, seed, bbits, idx, m[it]);
+      cblock(key[it], bbits, idx, m[it]);
       v[it] = j < sd.rows ? __ldg(bm_probe + idx) : 0ull;
     }
     uint32_t my = 0, c = 0;
@@ -547,7 +554,7 @@ cfilter_setmask_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t 
     uint32_t idx[kFItems];
     uint64_t m[kFItems];
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) wblock(key[it], 0, seed, bbits, idx[it], m[it]);
+    for (int it = 0; it < kFItems; it++) cblock(key[it], bbits, idx[it], m[it]);
     set_blocks(bm, idx, m, keep, lane);
   }
 }
@@ -570,7 +577,7 @@ cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t b
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
-      wblock(key[it], 0, seed, bbits, idx, m[it]);
+      cblock(key[it], bbits, idx, m[it]);
       v[it] = j < sd.rows ? __ldg(bm + idx) : 0ull;
     }
 #pragma unroll
