@@ -471,7 +471,7 @@ def main():
                          "or scan the whole triple table every step")
     ap.add_argument("--semijoin", default="auto", choices=["auto", "on", "off"],
                     help="semi-join key-presence filter in front of the Map (auto: joins of "
-                         ">= 2^20 rows)")
+                         ">= 2^22 rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU path (exchange per join) even at world size 1")

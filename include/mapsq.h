@@ -315,12 +315,13 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
 #define MAPSQ_WIDE_KEY_HASH 2     /*   hashed composite key + exact pair check (default) */
 /* Semi-join filter in front of the Map (SURVEY §8 row f2's reducer): rows whose packed key is
  * absent from the other side produce nothing in ReduceDuplicate and
- * are dropped before the sort; RS and its row order are unchanged.  Costs one extra read of the
- * key columns, two key-presence bitmaps (<= 64 MB each) and one more blocking read per join. */
+ * are dropped before the sort; RS and its row order are unchanged.  Costs extra reads of the key
+ * columns, two key-presence bitmaps (<= 64 MB each) and a few more blocking reads per join. */
 #define MAPSQ_OPT_SEMIJOIN 2
 #define MAPSQ_SEMIJOIN_OFF 0
-#define MAPSQ_SEMIJOIN_AUTO 1     /*   default: joins with n1 + n2 >= 2^20 rows (P64 / RESIDUAL) */
-#define MAPSQ_SEMIJOIN_ON 2       /*   every P64 / RESIDUAL join */
+#define MAPSQ_SEMIJOIN_AUTO 1     /*   default: joins with n1 + n2 >= 2^22 rows, unless a 1/16
+                                       sample says >= 90% of the rows would survive */
+#define MAPSQ_SEMIJOIN_ON 2       /*   every P64 / RESIDUAL / HASH join */
 mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value);
 
 /* ---- statistics ---- */

@@ -362,7 +362,7 @@ void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint
 // Semi-join filter (filter.cu): per-side key-presence bitmaps of 2^bbits bits (bit = key' when
 // hashed == 0, else a multiplicative hash of key'), then the Map of the rows whose key is present
 // on the other side, compacted stably (probe -> scan of per-slice counts -> emit).
-constexpr uint64_t kSemijoinMinRows = 1ull << 20;  // AUTO: joins of at least this many rows
+constexpr uint64_t kSemijoinMinRows = 1ull << 22;  // AUTO: joins of at least this many rows
 constexpr uint32_t kSemijoinBits = 29;             // 2 x 64 MB bitmaps at most (L2-sized)
 uint64_t filter_slices(uint64_t n1, uint64_t n2);      // 512-row warp slices (per side)
 uint64_t filter_mask_words(uint64_t n1, uint64_t n2);  // survivor-bit words

@@ -457,13 +457,11 @@ int sort_main(std::vector<uint64_t> &w, uint32_t ib, uint32_t kbits) {
 #define ZRUN(K, I, NAME)                                                                   \
   cudaMemcpy(w0, wsrc, n * 8, cudaMemcpyDeviceToDevice);                                  \
   zipf_sort(K, I, NAME, w0, w1, n, ib, kbits, hists, status, ctr, sample);
-  ZRUN((radix_pass_kernel<false, 32, 4, 2, true, 3>), 32, "items32 minb2 atomicOr+uni (prod)");
-  ZRUN((radix_pass_kernel<false, 24, 4, 3, true, 3>), 24, "items24 minb3 atomicOr+uni");
-  ZRUN((radix_pass_kernel<false, 20, 4, 3, true, 3>), 20, "items20 minb3 atomicOr+uni");
-  ZRUN((radix_pass_kernel<false, 16, 4, 4, true, 3>), 16, "items16 minb4 atomicOr+uni");
-  ZRUN((radix_pass_kernel<false, 32, 8, 2, true, 3>), 32, "items32 minb2 win8 atomicOr+uni");
-  ZRUN((radix_pass_kernel<false, 24, 8, 3, true, 3>), 24, "items24 minb3 win8 atomicOr+uni");
-  ZRUN((radix_pass_kernel<false, 32, 4, 2, false, 3>), 32, "items32 minb2 noreload atomicOr+uni");
+  ZRUN((radix_pass_kernel<false, 24, 4, 3, true, 3>), 24, "items24 minb3 (prod)");
+  ZRUN((radix_pass_kernel<false, 28, 4, 3, true, 3>), 28, "items28 minb3");
+  ZRUN((radix_pass_kernel<false, 24, 2, 3, true, 3>), 24, "items24 minb3 win2");
+  ZRUN((radix_pass_kernel<false, 24, 4, 3, false, 3>), 24, "items24 minb3 noreload");
+  ZRUN((radix_pass_kernel<false, 20, 4, 3, true, 3>), 20, "items20 minb3");
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
