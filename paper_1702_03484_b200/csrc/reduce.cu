@@ -252,7 +252,7 @@ __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, u
 // shared memory, then computes the 8 (LEFT, RIGHT) positions, issues all word loads, then all
 // column gathers, then 16 B streaming stores — so the latencies of one thread's rows overlap.
 template <int kERows, int kEChunks>
-__global__ void __launch_bounds__(kEThreads)
+__global__ void __launch_bounds__(kEThreads, 5)
 expand_kernel(const ExpandArgs a) {
   static_assert(kERows * kEChunks == kERowsPerThread && kERows % 4 == 0, "tile shape");
   __shared__ const uint32_t *s_src[MAPSQ_MAX_COLS];
