@@ -451,6 +451,176 @@ uint32_t word_round_bits(uint64_t small) {
 }
 uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(round + 1); }
 
+// Semi-join filter in front of the Map (row f2's reducer, reading R18): leaves the
+// surviving words key' << ib | rowid in cur (cur/alt may be swapped) with side A's words first and
+// row order kept, their first radix digit counted into hist, and their number in *nw.
+mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *a,
+                        const mapsq_table *b, Scratch &sc, cudaStream_t s, uint64_t *&cur,
+                        uint64_t *&alt, uint32_t *hist, uint64_t *nw_out) {
+  const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
+  uint64_t nw = n;
+  PackArgs pa = pack_args(pl, a, b);
+  const uint64_t nsl = n / 512 + 4;  // warp slices of any round (filter_slices <= this)
+  const uint64_t bmw = std::max<uint64_t>(1, (1ull << kSemijoinBits) / 32);
+  uint32_t *bm = sc.get<uint32_t>(2 * bmw);
+  uint32_t *fmask = sc.get<uint32_t>(nsl * 16);
+  uint32_t *fcnt = sc.get<uint32_t>(nsl);
+  uint64_t *foff = sc.get<uint64_t>(nsl);
+  uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
+  uint64_t *fsc = sc.get<uint64_t>(4);  // [0] survivors, [2..3] sampled survivors / rows
+  NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
+  unsigned long long *sample = reinterpret_cast<unsigned long long *>(fsc + 2);
+  const uint32_t dmask = pa.last_mask;
+  uint64_t split = n1;     // words [0, split) are side A's
+  bool exact = false;      // the last round's bitmaps were exact (no false positives)
+  bool skipped = false;    // the sampled probe said the filter would drop < 10%
+  // survivors + side-A survivors after a round: one blocking read
+  auto read_counts = [&](uint64_t nslA) -> mapsq_status {
+    TRY(ensure_pinned(ctx, 2));
+    CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->pinned + 1, foff + nslA, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MAPSQ_OK;
+  };
+  // after building the smaller side's bitmap, a 1/16 sample of the larger side is probed; if
+  // >= 90% of it survives the filter cannot pay (C5 J1 drops 6%) and the join goes unfiltered
+  auto sample_says_skip = [&](bool *skip) -> mapsq_status {
+    TRY(ensure_pinned(ctx, 2));
+    CK(cudaMemcpyAsync(ctx->pinned, sample, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t surv = ctx->pinned[0], rows = ctx->pinned[1];
+    *skip = ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9;
+    return MAPSQ_OK;
+  };
+  // round 0 reads the key columns directly — a single packed column (exact or hashed bitmap),
+  // or a hashed composite key (blocked Bloom bitmaps, key_hash computed from the columns); other
+  // packed composite keys are Mapped first and filtered as words
+  const bool colhash = pa.hash;
+  const bool colpath = (pa.nkey == 1 && pl.kb <= 32 && !pa.hash) || colhash;
+  if (colpath) {
+    // round 0 on the key columns (no word is written for a dropped row)
+    const uint32_t bbits = colhash ? word_round_bits(std::min(n1, n2))
+                                   : std::min<uint32_t>(pl.kb, kSemijoinBits);
+    const uint32_t hashed = colhash || pl.kb > bbits;
+    const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
+    const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
+    CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+    auto col_round = [&](int phase) {
+      if (colhash)
+        launch_cfilter(pa, bm, bm + bw, bbits, word_round_seed(0), fmask, fcnt, phase, sample, s);
+      else
+        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, phase, sample, s);
+    };
+    {
+      KTimer kt(ctx, s, "filter_sample", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2) / 16) +
+                                             8ull * bw, 2);
+      col_round(0);
+      CKL("filter_sample");
+      ctx->counters.filter_accesses += std::min(n1, n2) + std::max(n1, n2) / 16;
+    }
+    TRY(sample_says_skip(&skipped));
+    if (!skipped) {
+      {
+        KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2)) +
+                                        16ull * bw + n / 8, colhash ? 3 : 2);
+        col_round(1);
+        CKL("filter");
+        ctx->counters.filter_accesses += std::max(n1, n2) + std::min(n1, n2);
+      }
+      {
+        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
+        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
+        CKL("filter_scan");
+      }
+      {
+        KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
+        launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
+        CKL("filter_emit");
+        TRY(read_counts(nslA));
+        kt.t.bytes += 12ull * ctx->pinned[0];
+      }
+      nw = ctx->pinned[0];
+      split = nslA < ns ? ctx->pinned[1] : nw;
+      // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
+      // says the keys mostly match, so refinement rounds would not pay
+      exact = (!hashed && !colhash) || nw * 10 > n * 9;
+    }
+  } else {
+    // composite / hashed keys: Map every row, then filter the words
+    pa.passes = 0;  // (the histogram is counted by the last round's emit)
+    KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
+    launch_pack_hist(pa, cur, nullptr, hist, s);
+    CKL("pack_hist");
+  }
+  // word rounds: the first one for non-column keys (sampled first), then refinements while a
+  // hashed round still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per
+  // key of the smaller side, with a fresh hash seed)
+  for (int round = colpath ? 1 : 0;
+       !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
+    const uint64_t small = std::min(split, nw - split);
+    const uint32_t bbits = word_round_bits(small);
+    const uint64_t bw = (1ull << bbits) / 32;
+    const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
+    const uint64_t seed = word_round_seed(round);
+    CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+    if (round == 0) {
+      CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+      {
+        KTimer kt(ctx, s, "filter_sample", 8ull * (small + (nw - small) / 16) + 8ull * bw, 2);
+        launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt, 0, sample, s);
+        CKL("filter_sample");
+        ctx->counters.filter_accesses += small + (nw - small) / 16;
+      }
+      TRY(sample_says_skip(&skipped));
+      if (skipped) break;
+    }
+    {
+      KTimer kt(ctx, s, "wfilter", (round ? 16ull : 8ull) * small + 8ull * (nw - small) +
+                                       16ull * bw + nw / 8, round ? 4 : 3);
+      launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt,
+                     round ? 2 : 1, sample, s);
+      CKL("wfilter");
+      ctx->counters.filter_accesses += (round ? small : 0) + (nw - small) + small;
+    }
+    {
+      KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
+      launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
+      CKL("filter_scan");
+    }
+    CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
+    {
+      KTimer kt(ctx, s, "wfilter_emit", nw / 8 + 12ull * ns);
+      launch_wfilter_emit(cur, nw, split, fmask, fcnt, foff, alt, pl.passes ? hist : nullptr,
+                          pl.ib, dmask, s);
+      CKL("wfilter_emit");
+      TRY(read_counts(nslA));
+      kt.t.bytes += 16ull * ctx->pinned[0];
+    }
+    const uint64_t before = nw;
+    nw = ctx->pinned[0];
+    split = nslA < ns ? ctx->pinned[1] : nw;
+    std::swap(cur, alt);
+    if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
+  }
+  if (skipped) {  // unfiltered: every row's word, the first digit's histogram
+    nw = n;
+    CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
+    if (colpath) {
+      const PackArgs pm = pack_args(pl, a, b);
+      KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
+      launch_pack_hist(pm, cur, nullptr, hist, s);
+      CKL("pack_hist");
+    } else {
+      KTimer kt(ctx, s, "key_hist", 8ull * n);
+      launch_key_hist(cur, n, pl.ib, 1, pl.passes == 1 ? pl.kb : 8, hist, s);
+      CKL("key_hist");
+    }
+  }
+  *nw_out = nw;
+  return MAPSQ_OK;
+}
+
 // ------------------------------------------------------------------------------ join
 mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_table *tp2_in,
                        mapsq_table *rs, cudaStream_t s) {
@@ -504,164 +674,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     ctx->counters.last_passes = pl.passes;
   }
   if (filt) {
-    PackArgs pa = pack_args(pl, &a, &b);
-    const uint64_t nsl = n / 512 + 4;  // warp slices of any round (filter_slices <= this)
-    const uint64_t bmw = std::max<uint64_t>(1, (1ull << kSemijoinBits) / 32);
-    uint32_t *bm = sc.get<uint32_t>(2 * bmw);
-    uint32_t *fmask = sc.get<uint32_t>(nsl * 16);
-    uint32_t *fcnt = sc.get<uint32_t>(nsl);
-    uint64_t *foff = sc.get<uint64_t>(nsl);
-    uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
-    uint64_t *fsc = sc.get<uint64_t>(4);  // [0] survivors, [2..3] sampled survivors / rows
-    NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
-    unsigned long long *sample = reinterpret_cast<unsigned long long *>(fsc + 2);
-    const uint32_t dmask = pa.last_mask;
-    uint64_t split = n1;     // words [0, split) are side A's
-    bool exact = false;      // the last round's bitmaps were exact (no false positives)
-    bool skipped = false;    // the sampled probe said the filter would drop < 10%
-    // survivors + side-A survivors after a round: one blocking read
-    auto read_counts = [&](uint64_t nslA) -> mapsq_status {
-      TRY(ensure_pinned(ctx, 2));
-      CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(ctx->pinned + 1, foff + nslA, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      return MAPSQ_OK;
-    };
-    // after building the smaller side's bitmap, a 1/16 sample of the larger side is probed; if
-    // >= 90% of it survives the filter cannot pay (C5 J1 drops 6%) and the join goes unfiltered
-    auto sample_says_skip = [&](bool *skip) -> mapsq_status {
-      TRY(ensure_pinned(ctx, 2));
-      CK(cudaMemcpyAsync(ctx->pinned, sample, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      const uint64_t surv = ctx->pinned[0], rows = ctx->pinned[1];
-      *skip = ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9;
-      return MAPSQ_OK;
-    };
-    // round 0 reads the key columns directly — a single packed column (exact or hashed bitmap),
-    // or a hashed composite key (blocked Bloom bitmaps, key_hash computed from the columns); other
-    // packed composite keys are Mapped first and filtered as words
-    const bool colhash = pa.hash;
-    const bool colpath = (pa.nkey == 1 && pl.kb <= 32 && !pa.hash) || colhash;
-    if (colpath) {
-      // round 0 on the key columns (no word is written for a dropped row)
-      const uint32_t bbits = colhash ? word_round_bits(std::min(n1, n2))
-                                     : std::min<uint32_t>(pl.kb, kSemijoinBits);
-      const uint32_t hashed = colhash || pl.kb > bbits;
-      const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
-      const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
-      CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
-      CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
-      auto col_round = [&](int phase) {
-        if (colhash)
-          launch_cfilter(pa, bm, bm + bw, bbits, word_round_seed(0), fmask, fcnt, phase, sample, s);
-        else
-          launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, phase, sample, s);
-      };
-      {
-        KTimer kt(ctx, s, "filter_sample", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2) / 16) +
-                                               8ull * bw, 2);
-        col_round(0);
-        CKL("filter_sample");
-        ctx->counters.filter_accesses += std::min(n1, n2) + std::max(n1, n2) / 16;
-      }
-      TRY(sample_says_skip(&skipped));
-      if (!skipped) {
-        {
-          KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2)) +
-                                          16ull * bw + n / 8, colhash ? 3 : 2);
-          col_round(1);
-          CKL("filter");
-          ctx->counters.filter_accesses += std::max(n1, n2) + std::min(n1, n2);
-        }
-        {
-          KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
-          launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
-          CKL("filter_scan");
-        }
-        {
-          KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
-          launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
-          CKL("filter_emit");
-          TRY(read_counts(nslA));
-          kt.t.bytes += 12ull * ctx->pinned[0];
-        }
-        nw = ctx->pinned[0];
-        split = nslA < ns ? ctx->pinned[1] : nw;
-        // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
-        // says the keys mostly match, so refinement rounds would not pay
-        exact = (!hashed && !colhash) || nw * 10 > n * 9;
-      }
-    } else {
-      // composite / hashed keys: Map every row, then filter the words
-      pa.passes = 0;  // (the histogram is counted by the last round's emit)
-      KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
-      launch_pack_hist(pa, cur, nullptr, hist, s);
-      CKL("pack_hist");
-    }
-    // word rounds: the first one for non-column keys (sampled first), then refinements while a
-    // hashed round still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per
-    // key of the smaller side, with a fresh hash seed)
-    for (int round = colpath ? 1 : 0;
-         !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
-      const uint64_t small = std::min(split, nw - split);
-      const uint32_t bbits = word_round_bits(small);
-      const uint64_t bw = (1ull << bbits) / 32;
-      const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
-      const uint64_t seed = word_round_seed(round);
-      CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
-      if (round == 0) {
-        CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
-        {
-          KTimer kt(ctx, s, "filter_sample", 8ull * (small + (nw - small) / 16) + 8ull * bw, 2);
-          launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt, 0, sample, s);
-          CKL("filter_sample");
-          ctx->counters.filter_accesses += small + (nw - small) / 16;
-        }
-        TRY(sample_says_skip(&skipped));
-        if (skipped) break;
-      }
-      {
-        KTimer kt(ctx, s, "wfilter", (round ? 16ull : 8ull) * small + 8ull * (nw - small) +
-                                         16ull * bw + nw / 8, round ? 4 : 3);
-        launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt,
-                       round ? 2 : 1, sample, s);
-        CKL("wfilter");
-        ctx->counters.filter_accesses += (round ? small : 0) + (nw - small) + small;
-      }
-      {
-        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
-        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
-        CKL("filter_scan");
-      }
-      CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
-      {
-        KTimer kt(ctx, s, "wfilter_emit", nw / 8 + 12ull * ns);
-        launch_wfilter_emit(cur, nw, split, fmask, fcnt, foff, alt, pl.passes ? hist : nullptr,
-                            pl.ib, dmask, s);
-        CKL("wfilter_emit");
-        TRY(read_counts(nslA));
-        kt.t.bytes += 16ull * ctx->pinned[0];
-      }
-      const uint64_t before = nw;
-      nw = ctx->pinned[0];
-      split = nslA < ns ? ctx->pinned[1] : nw;
-      std::swap(cur, alt);
-      if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
-    }
-    if (skipped) {  // unfiltered: every row's word, the first digit's histogram
-      nw = n;
-      CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
-      if (colpath) {
-        const PackArgs pm = pack_args(pl, &a, &b);
-        KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
-        launch_pack_hist(pm, cur, nullptr, hist, s);
-        CKL("pack_hist");
-      } else {
-        KTimer kt(ctx, s, "key_hist", 8ull * n);
-        launch_key_hist(cur, n, pl.ib, 1, pl.passes == 1 ? pl.kb : 8, hist, s);
-        CKL("key_hist");
-      }
-    }
+    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nw));
     ctx->counters.last_filtered = n - nw;
     if (nw == 0) {
       fill_empty_join(pl, &a, &b, rs);
