@@ -365,8 +365,8 @@ def run_gpu(args):
 
 def run_gpu_dist(args, world, rank, local):
     """N > 1: one process per GPU over NCCL.  Each rank generates its own contiguous university
-    range of the same dataset (identical triples for any N), runs the distributed query (local
-    fused scan, hash exchange per join key, local joins); time = max over ranks of the device
+    range of the same dataset (identical triples for any N), runs the distributed query
+    (mapsq_query_dist[_indexed]: local scan, hash exchange per join key, local joins); time = max over ranks of the device
     time; value = join tuples summed over ranks / that time (strong scaling: fixed dataset)."""
     import torch
     import torch.distributed as tdist
@@ -406,7 +406,6 @@ def run_gpu_dist(args, world, rank, local):
     def timed(profile: bool):
         ctx.stats_reset()
         ctx.set_profiling(profile)
-        x0 = dict(mqd.EXCHANGE)
         ms = []
         with ClockSampler(local) as clk:
             for _ in range(args.steps):
@@ -419,8 +418,8 @@ def run_gpu_dist(args, world, rank, local):
                 torch.cuda.synchronize()
                 ms.append(e0.elapsed_time(e1))
         ctx.set_profiling(False)
-        sent = mqd.EXCHANGE["bytes_sent"] - x0["bytes_sent"]
-        return ms, ctx.stats(), clk.summary(), sent
+        st_ = ctx.stats()
+        return ms, st_, clk.summary(), st_["exchange_bytes"]
 
     # region 1 (the value): no per-kernel events; region 2: per-kernel events for the roofline
     ms, st_plain, clocks, sent = timed(False)
@@ -483,7 +482,9 @@ def run_gpu_dist(args, world, rank, local):
                     "ms_per_step": e2e[0],
                     "path": "per rank: pinned shard H2D, full-table scan, distributed joins, "
                             "result shard D2H; max over ranks"},
-                "clocks": clocks, "gpu_launches": int(launches)}
+                "clocks": clocks, "gpu_launches": int(launches),
+                "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
+                                "rank": 0} for k, v in st_k["kernels"].items()}}
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
 

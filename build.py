@@ -65,7 +65,7 @@ def build_mapsq(force: bool = False) -> str:
                   "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
                   "-I", os.path.join(ROOT, "include"), "-c", f, "-o", o])
             objs.append(o)
-        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-cudart", "static"])
+        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-cudart", "static", "-ldl"])
     return out
 
 

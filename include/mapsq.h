@@ -41,7 +41,9 @@ typedef enum {
                               patterns before it */
   MAPSQ_E_NOMEM = 3,       /* the allocator returned NULL; nothing is partially written */
   MAPSQ_E_CUDA = 4,        /* CUDA error (text in mapsq_last_error); sticky for the context */
-  MAPSQ_E_UNSUPPORTED = 5  /* packed key wider than 64 bits after range compression */
+  MAPSQ_E_UNSUPPORTED = 5, /* packed key wider than 64 bits after range compression */
+  MAPSQ_E_NCCL = 6         /* NCCL missing or a collective failed (text in mapsq_last_error);
+                              distributed entry points only */
 } mapsq_status;
 
 #define MAPSQ_MAX_COLS 16
@@ -151,6 +153,9 @@ typedef struct {
   uint64_t last_filtered;  /* rows the semi-join filter dropped in the last join */
   uint64_t filter_accesses;/* random bitmap accesses of the filter since the reset: builds and
                               probes (survivors setting the larger side's bits not counted) */
+  uint64_t exchanges;      /* hash exchanges run by mapsq_join_dist / mapsq_query_dist */
+  uint64_t exchange_rows;  /* rows this rank stored into OTHER ranks' arenas */
+  uint64_t exchange_bytes; /* bytes of those rows (4 B per column) */
   uint32_t nkernels;
   mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
 } mapsq_stats;
@@ -273,7 +278,7 @@ mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words, uint64_t
 
 /* ---- multi-GPU exchange (SURVEY §8 row e) ----
  * Hash partition on the join key, fused with the all-to-all: every rank sends each row to rank
- * dest = fmix32(h) mod nparts, h the FNV-1a-style fold (h = (h ^ v) * 16777619 from 2166136261)
+ * dest = (fmix32(h) * nparts) >> 32 (multiply-shift range reduction), h the FNV-1a-style fold (h = (h ^ v) * 16777619 from 2166136261)
  * of the row's values of key_vars[0..nkey) in that order.
  *
  * mapsq_partition_plan: per-tile destination histogram + scan; counts_host[d] receives the number
@@ -304,6 +309,52 @@ mapsq_status mapsq_ipc_free(mapsq_ctx *ctx, void *dev_ptr);
 mapsq_status mapsq_ipc_export(mapsq_ctx *ctx, void *dev_ptr, void *handle64);
 mapsq_status mapsq_ipc_open(mapsq_ctx *ctx, const void *handle64, void **dev_ptr);
 mapsq_status mapsq_ipc_close(mapsq_ctx *ctx, void *dev_ptr);
+/* Host-only layout of one exchange (no device work): from the world x world count matrix
+ * (count_matrix[s * world + d] = rows rank s sends to rank d), dest_row[d] = this rank's first row
+ * in rank d's receive block (sources s < rank come first, so a received table is grouped by
+ * source rank), recv[d] = rows rank d receives, and need_bytes[d] = bytes of rank d's receive
+ * block: ncols columns of stride_rows(recv[d]) = recv[d] rounded up to a multiple of 4 rows
+ * (16 B aligned columns). */
+mapsq_status mapsq_exchange_layout(int world, int rank, int ncols, const uint64_t *count_matrix,
+                                   uint64_t *dest_row, uint64_t *recv, uint64_t *need_bytes);
+
+/* ---- distributed join and query (SURVEY §8 rows b and e) ----
+ * One process per GPU, one context per process.  The equi-join decomposes over disjoint key
+ * sets (PAPER.md:126-133 join each key's group independently), so each join is one hash
+ * exchange of both inputs on ALL shared variables (mapsq_partition_plan's destination function)
+ * followed by the local Algorithm-1 join; RS stays sharded (the union over ranks is RS).
+ * The exchange is the fused kernel above: every rank owns two receive arenas (one per join side,
+ * grow-only cudaMalloc allocations exported with CUDA IPC and opened by every peer), the ranks
+ * all-gather the count matrix with NCCL, and mapsq_partition_scatter stores each row straight
+ * into its destination's arena over NVLink / NVSwitch.  NCCL (libnccl.so.2, loaded at
+ * mapsq_dist_init) carries only the count matrix, the arena handles, the column bounds (min/max
+ * all-reduce, so the local join range-compresses keys without a min/max pass) and the two
+ * barriers around each scatter.  Every call is collective: all ranks call it in the same order.
+ *
+ * mapsq_dist_unique_id: a fresh 128-byte NCCL unique id (one rank creates it; the caller
+ *   broadcasts it, e.g. with torch.distributed).
+ * mapsq_dist_init: join the communicator (blocking, collective).  Returns MAPSQ_E_NCCL if NCCL
+ *   cannot be loaded or the init fails; MAPSQ_E_INVALID if already initialised.  The state is
+ *   freed by mapsq_destroy.
+ * mapsq_join_dist: rs_shard = this rank's part of tp1 ⋈ tp2 (tp1_shard, tp2_shard are this
+ *   rank's rows of each input, any distribution).  Blocking.  Output owned by the caller.
+ * mapsq_query_dist / mapsq_query_dist_indexed: every rank scans its shard of the triple table
+ *   (rows of the triple table distributed in any way: a pattern matches each triple where it
+ *   lives, no exchange), then folds the joins left-deep with one exchange per join; an input
+ *   already partitioned on the join's key (the previous join's result, when the key is unchanged)
+ *   is not exchanged again.  Projection as mapsq_query. */
+#define MAPSQ_DIST_ID_BYTES 128
+mapsq_status mapsq_dist_unique_id(void *id128);
+mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int rank, int world);
+mapsq_status mapsq_join_dist(mapsq_ctx *ctx, const mapsq_table *tp1_shard,
+                             const mapsq_table *tp2_shard, mapsq_table *rs_shard, void *stream);
+mapsq_status mapsq_query_dist(mapsq_ctx *ctx, const mapsq_triples *shard,
+                              const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
+                              mapsq_table *rs_shard, void *stream);
+mapsq_status mapsq_query_dist_indexed(mapsq_ctx *ctx, const mapsq_index *shard,
+                                      const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                      int nproj, mapsq_table *rs_shard, void *stream);
+
 /* Compute exact inclusive bounds lo[]/hi[] of every column of a (caller-built) table and set
  * MAPSQ_TABLE_BOUNDS (one min/max pass, blocking).  An empty table gets lo = hi = 0. */
 mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);

@@ -24,7 +24,8 @@ PATH_P64, PATH_KV, PATH_RESIDUAL, PATH_HASH = 0, 1, 2, 3
 OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
-          5: "E_UNSUPPORTED"}
+          5: "E_UNSUPPORTED", 6: "E_NCCL"}
+DIST_ID_BYTES = 128
 
 
 class MapsqError(RuntimeError):
@@ -75,7 +76,8 @@ class _Stats(ctypes.Structure):
                 ("last_kb", ctypes.c_uint64), ("last_ib", ctypes.c_uint64),
                 ("last_passes", ctypes.c_uint64), ("last_path", ctypes.c_uint64),
                 ("last_groups", ctypes.c_uint64), ("last_filtered", ctypes.c_uint64),
-                ("filter_accesses", ctypes.c_uint64),
+                ("filter_accesses", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
+                ("exchange_rows", ctypes.c_uint64), ("exchange_bytes", ctypes.c_uint64),
                 ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
 
 
@@ -124,6 +126,16 @@ def lib():
             "mapsq_partition": (st, [vp, PT, ctypes.POINTER(i32), ctypes.c_int, ctypes.c_int, PT,
                                      ctypes.POINTER(u64), vp]),
             "mapsq_table_bounds": (st, [vp, PT, vp]),
+            "mapsq_exchange_layout": (st, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                           ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+            "mapsq_dist_unique_id": (st, [ctypes.c_char_p]),
+            "mapsq_dist_init": (st, [vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+            "mapsq_join_dist": (st, [vp, PT, PT, PT, vp]),
+            "mapsq_query_dist": (st, [vp, ctypes.POINTER(_Triples), PP, ctypes.c_int,
+                                      ctypes.POINTER(i32), ctypes.c_int, PT, vp]),
+            "mapsq_query_dist_indexed": (st, [vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
+                                              ctypes.c_int, PT, vp]),
             "mapsq_partition_plan": (st, [vp, PT, ctypes.POINTER(i32), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(u64), ctypes.POINTER(vp), vp]),
             "mapsq_partition_scatter": (st, [vp, vp, ctypes.POINTER(u64), ctypes.POINTER(vp), vp]),
@@ -506,6 +518,50 @@ class Context:
     def ipc_close(self, ptr: int):
         self._check(lib().mapsq_ipc_close(self.handle, ctypes.c_void_p(ptr)))
 
+    # ---- distributed join and query (rows b, e): collective calls, one context per rank
+    def dist_init(self, group=None):
+        """Join this context to an NCCL communicator over the ranks of ``group`` (a
+        torch.distributed group): the group's first rank creates the unique id, torch.distributed
+        broadcasts it, every rank calls mapsq_dist_init.  Collective; once per context."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [None]
+        if rank == 0:
+            buf = ctypes.create_string_buffer(DIST_ID_BYTES)
+            st = lib().mapsq_dist_unique_id(buf)
+            if st:
+                raise MapsqError(st, "mapsq_dist_unique_id failed (NCCL not loadable?)")
+            obj[0] = buf.raw
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
+        self._check(lib().mapsq_dist_init(self.handle, obj[0], rank, world))
+        self.dist_rank, self.dist_world = rank, world
+
+    def join_dist(self, tp1: DeviceTable, tp2: DeviceTable, stream=None) -> DeviceTable:
+        """This rank's shard of tp1 ⋈ tp2 (inputs: this rank's rows, any distribution)."""
+        out = _Table()
+        self._check(lib().mapsq_join_dist(self.handle, ctypes.byref(tp1._c), ctypes.byref(tp2._c),
+                                          ctypes.byref(out), _stream(stream)))
+        return _wrap(self, out)
+
+    def query_dist(self, shard, patterns, proj=None, stream=None) -> DeviceTable:
+        """This rank's shard of the query result over this rank's triples ((s, p, o) device
+        tensors or an Index of them)."""
+        k = len(patterns)
+        pats = (_Pattern * k)(*[pattern_struct(p) for p in patterns])
+        proj = list(proj or [])
+        pr = (ctypes.c_int32 * max(1, len(proj)))(*proj)
+        out = _Table()
+        if isinstance(shard, Index):
+            self._check(lib().mapsq_query_dist_indexed(self.handle, shard.handle, pats, k, pr,
+                                                       len(proj), ctypes.byref(out),
+                                                       _stream(stream)))
+            return _wrap(self, out, keep=shard)
+        T = _triples(*shard)
+        self._check(lib().mapsq_query_dist(self.handle, ctypes.byref(T), pats, k, pr, len(proj),
+                                           ctypes.byref(out), _stream(stream)))
+        return _wrap(self, out)
+
     def table_bounds(self, table: DeviceTable, stream=None):
         self._check(lib().mapsq_table_bounds(self.handle, ctypes.byref(table._c), _stream(stream)))
         return table.bounds
@@ -538,6 +594,17 @@ def device_columns(ptr: int, nrows: int, ncols: int, stride: int, owner=None):
         return [torch.empty(0, dtype=torch.uint32, device="cuda") for _ in range(ncols)]
     return [torch.as_tensor(_CAI(ptr + c * stride * 4, nrows, owner), device="cuda")
             for c in range(ncols)]
+
+
+def exchange_layout(count_matrix, rank: int, ncols: int):
+    """mapsq_exchange_layout (host only): (dest_row, recv, need_bytes) per destination rank."""
+    world = len(count_matrix)
+    flat = (ctypes.c_uint64 * (world * world))(*[int(x) for row in count_matrix for x in row])
+    dr, rc, nd = ((ctypes.c_uint64 * world)() for _ in range(3))
+    st = lib().mapsq_exchange_layout(world, rank, ncols, flat, dr, rc, nd)
+    if st:
+        raise MapsqError(st, "mapsq_exchange_layout: bad arguments")
+    return list(dr), list(rc), list(nd)
 
 
 def plan_join(vars1, bounds1, n1, vars2, bounds2, n2, wide_mode=None) -> JoinPlan:

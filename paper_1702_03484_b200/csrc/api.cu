@@ -1174,7 +1174,8 @@ mapsq_status scan_indexed_impl(mapsq_ctx *ctx, const mapsq_index *idx, const map
 // ------------------------------------------------------------------------------ query
 mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_pattern *pats,
                         int npats, const int32_t *proj, int nproj, mapsq_table *rs,
-                        cudaStream_t s, const mapsq_index *idx = nullptr) {
+                        cudaStream_t s, const mapsq_index *idx = nullptr,
+                        const JoinStep *step = nullptr) {
   if (!rs) return set_error(ctx, MAPSQ_E_INVALID, "rs is NULL");
   clear_table(rs);
   if (!pats || npats < 1 || npats > MAPSQ_MAX_PATTERNS)
@@ -1218,7 +1219,7 @@ mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_patt
   mapsq_table acc = tabs[0];
   for (int i = 1; i < npats; i++) {
     mapsq_table r;
-    mapsq_status st = join_impl(ctx, &acc, &tabs[i], &r, s);
+    mapsq_status st = step ? (*step)(&acc, &tabs[i], &r, s) : join_impl(ctx, &acc, &tabs[i], &r, s);
     dfree(ctx, acc.owner, s);
     dfree(ctx, tabs[i].owner, s);
     if (st != MAPSQ_OK) {
@@ -1248,6 +1249,24 @@ mapsq_status query_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_patt
 }
 
 }  // namespace
+
+// entry points for dist.cu (the distributed join and query reuse the single-GPU operators)
+namespace mapsq {
+mapsq_status api_enter(mapsq_ctx *ctx) { return enter(ctx); }
+mapsq_status api_check_table(mapsq_ctx *ctx, const mapsq_table *t, const char *name) {
+  return check_table(ctx, t, name);
+}
+mapsq_status api_ensure_pinned(mapsq_ctx *ctx, size_t words) { return ensure_pinned(ctx, words); }
+mapsq_status join_tables(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
+                         mapsq_table *rs, cudaStream_t s) {
+  return join_impl(ctx, a, b, rs, s);
+}
+mapsq_status query_fold(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_index *idx,
+                        const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
+                        mapsq_table *rs, cudaStream_t s, const JoinStep *step) {
+  return query_impl(ctx, T, pats, npats, proj, nproj, rs, s, idx, step);
+}
+}  // namespace mapsq
 
 // ================================================================================ C ABI
 MAPSQ_API const char *mapsq_version(void) { return "mapsq-b200 0.1 (sm_100a)"; }
@@ -1298,6 +1317,7 @@ MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
   if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->arena_ev) cudaEventDestroy(ctx->arena_ev);
+  dist_free(ctx);
   delete ctx;
 }
 

@@ -1,0 +1,420 @@
+// dist.cu — distributed join and query over NCCL + CUDA IPC (SURVEY §8 rows b and e).
+//
+// An equi-join decomposes over disjoint key sets: Algorithm 1 joins each key's group on its own
+// (PAPER.md:126-133), so hash-partitioning both inputs on the shared variables and joining locally
+// on every rank yields RS as the union of the rank outputs.  The paper runs on one GPU
+// (PAPER.md:170); this is the B200 extension.  Per exchange:
+//   1. mapsq_partition_plan (K8 histogram + scan) -> this rank's per-destination row counts;
+//   2. NCCL all-gather of the counts -> the world x world count matrix (every rank derives the
+//      same layout from it, mapsq_exchange_layout);
+//   3. receive arenas grown where too small (new cudaMalloc, IPC handle all-gathered, peers open
+//      it; the old allocation is freed only after every peer closed its mapping);
+//   4. barrier, ONE kernel (mapsq_partition_scatter) stores every row into its destination
+//      rank's arena over NVLink, barrier;
+//   5. column bounds min/max all-reduced, so the receiving side's local join range-compresses
+//      its keys without a min/max pass.
+// NCCL is loaded with dlopen at mapsq_dist_init (libnccl.so.2: the copy torch already loaded,
+// else the system one), so single-GPU users of the library never need it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "internal.cuh"
+
+using namespace mapsq;
+
+namespace {
+
+constexpr int kDistMaxRanks = 64;  // = partition.cu's kMaxParts
+constexpr size_t kHandleRec = 80;  // {u64 grew, u64 bytes, 64 B cudaIpcMemHandle_t}
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi &nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char *e = dlerror();
+      api.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return;
+    }
+#define SYM(field, name)                                          \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name)); \
+  if (!api.field) {                                               \
+    api.why = "libnccl lacks " name;                              \
+    return;                                                       \
+  }
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(AllGather, "ncclAllGather");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    api.ok = true;
+  });
+  return api;
+}
+
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      return set_error(ctx, MAPSQ_E_NCCL, std::string(#call ": ") + nccl().GetErrorString(_r)); \
+  } while (0)
+#define CK(call)                                \
+  do {                                          \
+    cudaError_t _e = (call);                    \
+    if (_e != cudaSuccess) return cuda_check(ctx, _e, #call); \
+  } while (0)
+#define TRY(x)                                  \
+  do {                                          \
+    mapsq_status _st = (x);                     \
+    if (_st != MAPSQ_OK) return _st;            \
+  } while (0)
+
+inline cudaStream_t S(void *stream) { return (cudaStream_t)stream; }
+inline uint64_t stride_rows(uint64_t n) { return (n + 3) & ~3ull; }
+
+}  // namespace
+
+namespace mapsq {
+
+// One receive arena per join side: this rank's allocation and every rank's mapped pointer.
+struct Arena {
+  void *own = nullptr;
+  uint64_t cap[kDistMaxRanks] = {};
+  void *ptr[kDistMaxRanks] = {};
+};
+
+struct DistState {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // device staging for the collectives: count matrix | handle records | bounds | barrier word
+  uint64_t *dmat = nullptr;
+  unsigned char *dhandles = nullptr;
+  uint32_t *dbounds = nullptr;
+  uint64_t *dbar = nullptr;
+  void *dbuf = nullptr;
+  Arena slot[2];
+};
+
+void dist_free(mapsq_ctx *ctx) {
+  DistState *d = ctx->dist;
+  if (!d) return;
+  cudaDeviceSynchronize();
+  for (Arena &a : d->slot) {
+    for (int r = 0; r < d->world; r++)
+      if (r != d->rank && a.ptr[r]) cudaIpcCloseMemHandle(a.ptr[r]);
+    if (a.own) cudaFree(a.own);
+  }
+  if (d->dbuf) cudaFree(d->dbuf);
+  if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+  delete d;
+  ctx->dist = nullptr;
+}
+
+}  // namespace mapsq
+
+namespace {
+
+// Blocking barrier over the communicator: everything this rank enqueued on `s` has completed and
+// so has every other rank's work before its matching barrier.
+mapsq_status barrier(mapsq_ctx *ctx, DistState *d, cudaStream_t s) {
+  CK(cudaStreamSynchronize(s));
+  NC(nccl().AllReduce(d->dbar, d->dbar, 1, ncclUint64, ncclSum, d->comm, s));
+  CK(cudaStreamSynchronize(s));
+  return MAPSQ_OK;
+}
+
+// Grow the arenas of `slot` that are smaller than need[] (collective; every rank passes the same
+// need[]).  New allocations are exported, their handles all-gathered and opened by the peers; a
+// replaced allocation is freed after a barrier, when no peer maps it any more.
+mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t *need,
+                          cudaStream_t s) {
+  Arena &a = d->slot[slot];
+  bool any = false;
+  for (int r = 0; r < d->world; r++) any |= need[r] > a.cap[r];
+  if (!any) return MAPSQ_OK;
+  unsigned char rec[kHandleRec] = {};
+  void *old = nullptr;
+  const bool grow = need[d->rank] > a.cap[d->rank];
+  uint64_t nbytes = a.cap[d->rank];
+  if (grow) {
+    nbytes = std::max<uint64_t>(1ull << 20, need[d->rank] + need[d->rank] / 4);
+    nbytes = (nbytes + (2ull << 20) - 1) & ~((2ull << 20) - 1);
+    void *p = nullptr;
+    CK(cudaMalloc(&p, nbytes));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, p));
+    const uint64_t one = 1;
+    std::memcpy(rec, &one, 8);
+    std::memcpy(rec + 16, &h, 64);
+    old = a.own;
+    a.own = p;
+  }
+  std::memcpy(rec + 8, &nbytes, 8);
+  const int W = d->world;
+  TRY(api_ensure_pinned(ctx, (kHandleRec * W + 7) / 8));
+  unsigned char *hp = reinterpret_cast<unsigned char *>(ctx->pinned);
+  std::memcpy(hp, rec, kHandleRec);
+  CK(cudaMemcpyAsync(d->dhandles + kHandleRec * d->rank, hp, kHandleRec, cudaMemcpyHostToDevice, s));
+  NC(nccl().AllGather(d->dhandles + kHandleRec * d->rank, d->dhandles, kHandleRec, ncclUint8,
+                      d->comm, s));
+  CK(cudaMemcpyAsync(hp, d->dhandles, kHandleRec * W, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int r = 0; r < W; r++) {
+    const unsigned char *q = hp + kHandleRec * r;
+    uint64_t grew, nb;
+    std::memcpy(&grew, q, 8);
+    std::memcpy(&nb, q + 8, 8);
+    if (!grew) continue;
+    if (r == d->rank) {
+      a.ptr[r] = a.own;
+    } else {
+      if (a.ptr[r]) CK(cudaIpcCloseMemHandle(a.ptr[r]));
+      a.ptr[r] = nullptr;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, q + 16, 64);
+      CK(cudaIpcOpenMemHandle(&a.ptr[r], h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    a.cap[r] = nb;
+  }
+  TRY(barrier(ctx, d, s));  // every peer has closed its mapping of `old`
+  if (old) CK(cudaFree(old));
+  return MAPSQ_OK;
+}
+
+// Hash-exchange `in` on key_vars into arena `slot`: *out is a view (owner NULL) of this rank's
+// received rows, grouped by source rank, with bounds valid over every rank's input.
+mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
+                      const std::vector<int32_t> &key, int slot, mapsq_table *out, cudaStream_t s) {
+  const int W = d->world, R = d->rank;
+  const uint32_t nc = in->ncols;
+  uint64_t counts[kDistMaxRanks];
+  mapsq_partition_state *st = nullptr;
+  TRY(mapsq_partition_plan(ctx, in, key.data(), (int)key.size(), W, counts, &st, s));
+  struct Guard {
+    mapsq_ctx *c;
+    mapsq_partition_state *p;
+    ~Guard() { mapsq_partition_state_free(c, p); }
+  } guard{ctx, st};
+
+  // (2) count matrix and (5) bounds in one staging round trip: ~lo and hi under one max-reduce,
+  // plus a flag word set by a rank whose non-empty input carries no bounds
+  const uint32_t nb = 2 * nc + 1;
+  TRY(api_ensure_pinned(ctx, (size_t)W * W + nb));
+  uint64_t *pin = ctx->pinned;
+  for (int q = 0; q < W; q++) pin[q] = counts[q];
+  uint32_t *pb = reinterpret_cast<uint32_t *>(pin + W);
+  const bool has_b = (in->flags & MAPSQ_TABLE_BOUNDS) != 0;
+  for (uint32_t c = 0; c < nc; c++) {
+    pb[c] = has_b && in->nrows ? ~in->lo[c] : 0u;  // empty input: the identity of max
+    pb[nc + c] = has_b && in->nrows ? in->hi[c] : 0u;
+  }
+  pb[2 * nc] = (!has_b && in->nrows) ? 1u : 0u;
+  CK(cudaMemcpyAsync(d->dmat + (size_t)R * W, pin, 8ull * W, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d->dbounds, pb, 4ull * nb, cudaMemcpyHostToDevice, s));
+  NC(nccl().AllGather(d->dmat + (size_t)R * W, d->dmat, W, ncclUint64, d->comm, s));
+  NC(nccl().AllReduce(d->dbounds, d->dbounds, nb, ncclUint32, ncclMax, d->comm, s));
+  CK(cudaMemcpyAsync(pin, d->dmat, 8ull * W * W, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(pin + (size_t)W * W, d->dbounds, 4ull * nb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const std::vector<uint64_t> mat(pin, pin + (size_t)W * W);
+  const uint32_t *rb = reinterpret_cast<const uint32_t *>(pin + (size_t)W * W);
+  const std::vector<uint32_t> bnd(rb, rb + nb);
+
+  uint64_t dest_row[kDistMaxRanks], recv[kDistMaxRanks], need[kDistMaxRanks];
+  TRY(mapsq_exchange_layout(W, R, (int)nc, mat.data(), dest_row, recv, need));
+  TRY(ensure_arena(ctx, d, slot, need, s));
+  Arena &a = d->slot[slot];
+  std::vector<uint32_t *> dest_cols((size_t)W * nc);
+  for (int q = 0; q < W; q++)
+    for (uint32_t c = 0; c < nc; c++)
+      dest_cols[(size_t)q * nc + c] =
+          reinterpret_cast<uint32_t *>(static_cast<char *>(a.ptr[q]) + 4ull * c * stride_rows(recv[q]));
+
+  // (4) no rank still reads the arena it is about to receive into; then the fused scatter
+  TRY(barrier(ctx, d, s));
+  TRY(mapsq_partition_scatter(ctx, st, dest_row, dest_cols.data(), s));
+  TRY(barrier(ctx, d, s));  // every peer's stores into this rank's arena have landed
+  for (int q = 0; q < W; q++)
+    if (q != R) {
+      ctx->counters.exchange_rows += counts[q];
+      ctx->counters.exchange_bytes += 4ull * nc * counts[q];
+    }
+  ctx->counters.exchanges++;
+
+  std::memset(out, 0, sizeof *out);
+  out->nrows = recv[R];
+  out->ncols = nc;
+  for (uint32_t c = 0; c < nc; c++) {
+    out->var[c] = in->var[c];
+    out->col[c] = dest_cols[(size_t)R * nc + c];
+  }
+  // a rank whose input carried no bounds makes the all-reduced bounds incomplete: then every
+  // rank takes exact bounds of its received rows with a min/max pass
+  if (bnd[2 * nc] || out->nrows == 0) {
+    TRY(mapsq_table_bounds(ctx, out, s));
+  } else {
+    for (uint32_t c = 0; c < nc; c++) {
+      out->lo[c] = ~bnd[c];
+      out->hi[c] = bnd[nc + c];
+    }
+    out->flags = MAPSQ_TABLE_BOUNDS;
+  }
+  return MAPSQ_OK;
+}
+
+std::vector<int32_t> shared_key(const mapsq_table *a, const mapsq_table *b) {
+  std::vector<int32_t> k;
+  for (uint32_t i = 0; i < a->ncols; i++)
+    for (uint32_t j = 0; j < b->ncols; j++)
+      if (a->var[i] == b->var[j]) k.push_back(a->var[i]);
+  std::sort(k.begin(), k.end());
+  return k;
+}
+
+// Distributed join step: exchange both sides (tp1 skipped when it is already partitioned on this
+// key), local Algorithm-1 join.  *part_key receives the key RS is partitioned on.
+mapsq_status join_dist_step(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
+                            mapsq_table *rs, cudaStream_t s, std::vector<int32_t> *part_key) {
+  DistState *d = ctx->dist;
+  std::memset(rs, 0, sizeof *rs);
+  TRY(api_check_table(ctx, a, "tp1"));
+  TRY(api_check_table(ctx, b, "tp2"));
+  const std::vector<int32_t> key = shared_key(a, b);
+  if (key.empty()) return set_error(ctx, MAPSQ_E_NO_SHARED, "join inputs share no variable");
+  mapsq_table ea, eb;
+  if (part_key && *part_key == key) {
+    ea = *a;
+  } else {
+    TRY(exchange(ctx, d, a, key, 0, &ea, s));
+  }
+  TRY(exchange(ctx, d, b, key, 1, &eb, s));
+  TRY(join_tables(ctx, &ea, &eb, rs, s));
+  if (part_key) *part_key = key;
+  return MAPSQ_OK;
+}
+
+mapsq_status dist_enter(mapsq_ctx *ctx) {
+  TRY(api_enter(ctx));
+  if (!ctx->dist) return set_error(ctx, MAPSQ_E_INVALID, "mapsq_dist_init has not been called");
+  return MAPSQ_OK;
+}
+
+mapsq_status query_dist_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_index *idx,
+                             const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
+                             mapsq_table *rs, cudaStream_t s) {
+  TRY(dist_enter(ctx));
+  std::vector<int32_t> part;  // key the accumulated result is partitioned on (none: scan output)
+  JoinStep step = [ctx, &part](const mapsq_table *acc, const mapsq_table *t, mapsq_table *out,
+                               cudaStream_t st) { return join_dist_step(ctx, acc, t, out, st, &part); };
+  return query_fold(ctx, T, idx, pats, npats, proj, nproj, rs, s, &step);
+}
+
+}  // namespace
+
+// ================================================================================ C ABI
+MAPSQ_API mapsq_status mapsq_exchange_layout(int world, int rank, int ncols,
+                                             const uint64_t *m, uint64_t *dest_row, uint64_t *recv,
+                                             uint64_t *need) {
+  if (world < 1 || world > kDistMaxRanks || rank < 0 || rank >= world || ncols < 1 ||
+      ncols > MAPSQ_MAX_COLS || !m || !dest_row || !recv || !need)
+    return MAPSQ_E_INVALID;
+  for (int q = 0; q < world; q++) {
+    uint64_t r = 0, before = 0;
+    for (int src = 0; src < world; src++) {
+      r += m[(size_t)src * world + q];
+      if (src < rank) before += m[(size_t)src * world + q];
+    }
+    recv[q] = r;
+    dest_row[q] = before;
+    need[q] = 4ull * ncols * stride_rows(r);
+  }
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_dist_unique_id(void *id128) {
+  if (!id128) return MAPSQ_E_INVALID;
+  static_assert(sizeof(ncclUniqueId) == MAPSQ_DIST_ID_BYTES, "ncclUniqueId size");
+  if (!nccl().ok) return MAPSQ_E_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return MAPSQ_E_NCCL;
+  std::memcpy(id128, &id, sizeof id);
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int rank, int world) {
+  TRY(api_enter(ctx));
+  if (!id128 || world < 1 || world > kDistMaxRanks || rank < 0 || rank >= world)
+    return set_error(ctx, MAPSQ_E_INVALID, "bad mapsq_dist_init arguments");
+  if (ctx->dist) return set_error(ctx, MAPSQ_E_INVALID, "distributed state already initialised");
+  if (!nccl().ok) return set_error(ctx, MAPSQ_E_NCCL, nccl().why);
+  auto *d = new (std::nothrow) DistState();
+  if (!d) return set_error(ctx, MAPSQ_E_NOMEM, "host allocation failed");
+  d->rank = rank;
+  d->world = world;
+  const size_t mat = 8ull * world * world, hnd = kHandleRec * world,
+               bnd = 8ull * MAPSQ_MAX_COLS + 16, bar = 16;
+  cudaError_t e = cudaMalloc(&d->dbuf, mat + hnd + bnd + bar + 64);
+  if (e != cudaSuccess) {
+    delete d;
+    return cuda_check(ctx, e, "cudaMalloc(dist staging)");
+  }
+  char *b = static_cast<char *>(d->dbuf);
+  d->dmat = reinterpret_cast<uint64_t *>(b);
+  d->dhandles = reinterpret_cast<unsigned char *>(b + mat);
+  d->dbounds = reinterpret_cast<uint32_t *>(b + ((mat + hnd + 15) & ~size_t(15)));
+  d->dbar = reinterpret_cast<uint64_t *>(b + ((mat + hnd + 15) & ~size_t(15)) + bnd);
+  cudaMemset(d->dbuf, 0, mat + hnd + bnd + bar + 64);
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclResult_t r = nccl().CommInitRank(&d->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    cudaFree(d->dbuf);
+    delete d;
+    return set_error(ctx, MAPSQ_E_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+  }
+  ctx->dist = d;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_join_dist(mapsq_ctx *ctx, const mapsq_table *tp1,
+                                       const mapsq_table *tp2, mapsq_table *rs, void *stream) {
+  if (!rs) return ctx ? set_error(ctx, MAPSQ_E_INVALID, "rs is NULL") : MAPSQ_E_INVALID;
+  std::memset(rs, 0, sizeof *rs);
+  TRY(dist_enter(ctx));
+  return join_dist_step(ctx, tp1, tp2, rs, S(stream), nullptr);
+}
+
+MAPSQ_API mapsq_status mapsq_query_dist(mapsq_ctx *ctx, const mapsq_triples *shard,
+                                        const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                        int nproj, mapsq_table *rs, void *stream) {
+  if (!shard) return ctx ? set_error(ctx, MAPSQ_E_INVALID, "shard is NULL") : MAPSQ_E_INVALID;
+  return query_dist_impl(ctx, shard, nullptr, pats, npats, proj, nproj, rs, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_query_dist_indexed(mapsq_ctx *ctx, const mapsq_index *shard,
+                                                const mapsq_pattern *pats, int npats,
+                                                const int32_t *proj, int nproj, mapsq_table *rs,
+                                                void *stream) {
+  if (!shard) return ctx ? set_error(ctx, MAPSQ_E_INVALID, "shard is NULL") : MAPSQ_E_INVALID;
+  return query_dist_impl(ctx, nullptr, shard, pats, npats, proj, nproj, rs, S(stream));
+}

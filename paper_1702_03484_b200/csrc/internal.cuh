@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -36,6 +37,7 @@ struct KAgg {
   double ms = 0;
   uint64_t bytes = 0;
 };
+struct DistState;
 
 }  // namespace mapsq
 
@@ -65,12 +67,25 @@ struct mapsq_ctx {
   int arena_depth = 0;
   cudaStream_t arena_stream = nullptr;
   cudaEvent_t arena_ev = nullptr;
+  mapsq::DistState *dist = nullptr;  // communicator + exchange arenas (dist.cu), or NULL
 };
 
 namespace mapsq {
 
 // ---------------------------------------------------------------- host helpers
 mapsq_status set_error(mapsq_ctx *ctx, mapsq_status st, const std::string &msg);
+// operators shared with dist.cu (api.cu)
+using JoinStep = std::function<mapsq_status(const mapsq_table *acc, const mapsq_table *t,
+                                            mapsq_table *out, cudaStream_t s)>;
+mapsq_status api_enter(mapsq_ctx *ctx);
+mapsq_status api_check_table(mapsq_ctx *ctx, const mapsq_table *t, const char *name);
+mapsq_status api_ensure_pinned(mapsq_ctx *ctx, size_t words);
+mapsq_status join_tables(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
+                         mapsq_table *rs, cudaStream_t s);
+mapsq_status query_fold(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_index *idx,
+                        const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
+                        mapsq_table *rs, cudaStream_t s, const JoinStep *step);
+void dist_free(mapsq_ctx *ctx);  // dist.cu: communicator, arenas, peer mappings
 mapsq_status cuda_check(mapsq_ctx *ctx, cudaError_t e, const char *what);
 void *dalloc(mapsq_ctx *ctx, size_t bytes, cudaStream_t s);
 void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s);

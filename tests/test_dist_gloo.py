@@ -41,12 +41,12 @@ def fmix32(h):
 
 
 def np_partition(table, key_vars, world):
-    """The K8 contract: dest = fmix32(FNV-style fold of the key) mod world, stable within dest."""
+    """The K8 contract: dest = (fmix32(FNV-style fold of the key) * world) >> 32, stable within dest."""
     rows = table.rows()
     h = np.full(len(rows), 0x811C9DC5, np.uint64)
     for v in key_vars:
         h = ((h ^ rows[:, table.vars.index(v)].astype(np.uint64)) * np.uint64(0x01000193)) & np.uint64(0xFFFFFFFF)
-    dest = (fmix32(h) % np.uint64(world)).astype(np.int64)
+    dest = ((fmix32(h) * np.uint64(world)) >> np.uint64(32)).astype(np.int64)
     order = np.argsort(dest, kind="stable")
     counts = np.bincount(dest, minlength=world).tolist()
     part = rows[order]
@@ -140,7 +140,7 @@ def test_exchange_layout_matches_all_to_all_order():
     C = [[3, 0, 5], [1, 2, 0], [4, 4, 4]]
     rows = [exchange_layout(C, r, 2)[0] for r in range(3)]
     _, recv, need = exchange_layout(C, 0, 2)
-    assert recv == [8, 6, 9] and need == [64, 48, 72]
+    assert recv == [8, 6, 9] and need == [64, 64, 96]  # columns padded to 4 rows (16 B)
     assert [rows[r][0] for r in range(3)] == [0, 3, 4]
     assert [rows[r][1] for r in range(3)] == [0, 0, 2]
     assert [rows[r][2] for r in range(3)] == [0, 5, 5]
@@ -151,68 +151,22 @@ def test_exchange_layout_matches_all_to_all_order():
         assert all(spans[i][1] == spans[i + 1][0] for i in range(2))
 
 
-class FakeIpcCtx:
-    """Stands in for the CUDA IPC calls: allocations are integers, handles encode (rank, ptr)."""
-
-    def __init__(self, rank):
-        self.rank, self.next, self.opened, self.freed = rank, 1000 * (rank + 1), {}, []
-
-    def ipc_alloc(self, nbytes):
-        self.next += 1
-        return self.next
-
-    def ipc_free(self, ptr):
-        self.freed.append(ptr)
-
-    def ipc_export(self, ptr):
-        return f"{self.rank}:{ptr}".encode()
-
-    def ipc_open(self, handle):
-        r, p = handle.decode().split(":")
-        mapped = 10 ** 6 + int(p)
-        self.opened[mapped] = (int(r), int(p))
-        return mapped
-
-    def ipc_close(self, ptr):
-        self.opened.pop(ptr)
-
-
-def _arena_worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from paper_1702_03484_b200.dist import PeerArenas
-        ctx = FakeIpcCtx(rank)
-        ar = PeerArenas(ctx, None, nslots=2)
-        log = []
-        for need in ([100, 5 << 20], [100, 7 << 20], [9 << 20, 7 << 20], [1, 1]):
-            ar.ensure(0, need)
-            log.append((list(ar.cap[0]), list(ar.ptr[0]), ar.own[0]))
-        q.put((rank, log, dict(ctx.opened)))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_peer_arenas_collective_growth_gloo():
-    world, port = 2, _free_port()
-    mpc = mp.get_context("spawn")
-    q = mpc.Queue()
-    procs = [mpc.Process(target=_arena_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    (_, log0, opened0), (_, log1, opened1) = res
-    for step in range(4):
-        assert log0[step][0] == log1[step][0]          # every rank agrees on every capacity
-        cap = log0[step][0]
-        assert cap[0] >= [100, 100, 9 << 20, 1][step] and cap[1] >= [5 << 20, 7 << 20, 7 << 20, 1][step]
-        # own arena mapped locally, the peer's through its (latest) handle
-        assert log0[step][1][0] == log0[step][2] and log1[step][1][1] == log1[step][2]
-        assert opened0[log0[-1][1][1]] == (1, log1[-1][2])
-        assert opened1[log1[-1][1][0]] == (0, log0[-1][2])
-    # rank 1 regrew at step 1 (7 MiB > 1.25 * 5 MiB + 4 KiB); nothing grows when needs shrink
-    assert log1[1][2] != log1[0][2] and log1[3][2] == log1[2][2]
+def test_exchange_layout_c_abi_definition():
+    """mapsq_exchange_layout against its definition, written out as brute force over the matrix."""
+    import paper_1702_03484_b200 as mq
+    rng = np.random.default_rng(7)
+    for world in (1, 2, 3, 8, 64):
+        C = rng.integers(0, 1000, (world, world)).tolist()
+        for rank in {0, world - 1, world // 2}:
+            for ncols in (1, 3, 16):
+                dest_row, recv, need = mq.exchange_layout(C, rank, ncols)
+                for d in range(world):
+                    assert recv[d] == sum(C[s][d] for s in range(world))
+                    assert dest_row[d] == sum(C[s][d] for s in range(rank))
+                    stride = -(-recv[d] // 4) * 4            # 16 B aligned columns
+                    assert need[d] == 4 * ncols * stride and need[d] % 16 == 0
+    for bad in ((2, 1), (0, 17), (0, 0)):                     # (rank, ncols) out of range
+        with pytest.raises(mq.MapsqError):
+            mq.exchange_layout([[1, 2], [3, 4]], *bad)
+    with pytest.raises(mq.MapsqError):
+        mq.exchange_layout([[0] * 65] * 65, 0, 1)             # more ranks than partitions

@@ -302,7 +302,7 @@ def test_query_projection_and_errors(ctx):
 def test_partition_hash_and_stability(ctx):
     rng = np.random.default_rng(9)
     A = rng.integers(0, 1 << 20, (50_000, 3)).astype(np.uint32)
-    for G in (1, 2, 3, 8):
+    for G in (1, 2, 3, 8, 37, 64):
         part, counts = ctx.partition(dtable([0, 1, 2], A), [0, 2], G)
         got = part.to_numpy()
 
@@ -313,7 +313,7 @@ def test_partition_hash_and_stability(ctx):
         h = np.full(len(A), 0x811C9DC5, np.uint64)
         for c in (0, 2):
             h = ((h ^ A[:, c].astype(np.uint64)) * np.uint64(0x01000193)) & np.uint64(0xFFFFFFFF)
-        dest = fmix32(h) % np.uint64(G)
+        dest = (fmix32(h) * np.uint64(G)) >> np.uint64(32)
         assert counts == np.bincount(dest.astype(np.int64), minlength=G).tolist()
         want = A[np.argsort(dest, kind="stable")]
         assert np.array_equal(got, want)
@@ -332,22 +332,56 @@ def test_stats_and_launch_count(ctx):
 
 
 def test_query_dist_world1_nccl(ctx, tmp_path):
-    """The distributed orchestration on one GPU: fused partition + exchange kernel into the
-    IPC-exported arena (fused=True) and K8 partition + NCCL all-to-all (fused=False)."""
+    """The distributed path on one GPU: mapsq_query_dist[_indexed] / mapsq_join_dist (NCCL
+    communicator, fused partition + exchange kernel into the IPC-exported arena, all-reduced
+    bounds, local join) and the torch-orchestrated K8 partition + NCCL all-to-all (fused=False)."""
     import torch.distributed as tdist
     from paper_1702_03484_b200 import dist as mqd
     if not tdist.is_initialized():
         tdist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
                                  device_id=torch.device("cuda", 0))
+    c2 = mq.Context(0)
+    with pytest.raises(mq.MapsqError) as e:      # collective entry points need mapsq_dist_init
+        c2.join_dist(dtable([0, 1], np.zeros((3, 2), np.uint32)), dtable([0, 2], np.zeros((3, 2), np.uint32)))
+    assert e.value.code == 1
     s, p, o, st = datagen.lubm(2)
     trip = (dev(s), dev(p), dev(o))
+    store = c2.index_build(trip)
     for fused in (True, False):
-        for cfg in ("C3", "C5", "C2"):
-            pats = config_query(cfg)
-            got = mqd.query_dist(ctx, trip, pats, fused=fused)
-            ref = oracle.query(s, p, o, pats)
-            assert got.vars == ref.vars
-            assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
+        for source in (trip, store):
+            for cfg in ("C3", "C5", "C2", "C1"):
+                pats = config_query(cfg)
+                c2.stats_reset()
+                got = mqd.query_dist(c2, source, pats, fused=fused)
+                ref = oracle.query(s, p, o, pats)
+                assert got.vars == ref.vars
+                assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
+                if fused:
+                    x = c2.stats()
+                    # one exchange per side per join, minus tp1 when the key is unchanged (C3's
+                    # star on ?x exchanges the accumulated result once); world 1 sends nothing
+                    assert x["exchange_rows"] == 0 and x["exchange_bytes"] == 0
+                    assert len(pats) <= x["exchanges"] <= 2 * (len(pats) - 1)
+    # direct join_dist: caller-built inputs without bounds (min/max pass after the exchange),
+    # ragged sizes, an empty side, a composite key
+    rng = np.random.default_rng(5)
+    A = rng.integers(0, 300, (12_345, 3)).astype(np.uint32)
+    B = rng.integers(0, 300, (777, 2)).astype(np.uint32)
+    for ta, tb in (([0, 1, 2], [2, 0]), ([0, 1, 2], [1, 3])):
+        a = mq.DeviceTable.from_torch(ta, [torch.from_numpy(A[:, c].view(np.int32)).cuda() for c in range(3)])
+        b = mq.DeviceTable.from_torch(tb, [torch.from_numpy(B[:, c].view(np.int32)).cuda() for c in range(2)])
+        got = c2.join_dist(a, b)
+        ref = oracle.join(oracle.Table(ta, A), oracle.Table(tb, B))
+        assert got.vars == ref.vars
+        assert np.array_equal(oracle.canonical_rows(got.to_numpy()), oracle.canonical(ref).rows)
+    empty = dtable([0, 7], np.zeros((0, 2), np.uint32))
+    assert c2.join_dist(a, empty).nrows == 0
+    with pytest.raises(mq.MapsqError) as e:
+        c2.join_dist(a, dtable([8, 9], B))
+    assert e.value.code == 2
+    with pytest.raises(mq.MapsqError) as e:
+        c2.dist_init()                           # once per context
+    assert e.value.code == 1
     tdist.destroy_process_group()
 
 
