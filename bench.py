@@ -377,26 +377,47 @@ def run_gpu_dist(args, world, rank, local):
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
     kind, nu, qname, desc = CONFIGS[cfg]
-    if kind != "lubm":
-        raise SystemExit("multi-GPU bench runs the LUBM configs")
     if args.univ:
         nu = args.univ
-    lo, hi = nu * rank // world, nu * (rank + 1) // world
     ctx = mq.Context(local)
     ctx.set_option(mq.OPT_SEMIJOIN, {"auto": mq.SEMIJOIN_AUTO, "on": mq.SEMIJOIN_ON,
                                      "off": mq.SEMIJOIN_OFF}[args.semijoin])
-    (s, p, o), st, pinned_bufs = lubm_host(nu, lo, hi, pinned=not args.no_e2e)
-    trip = tuple(torch.from_numpy(a.view(np.int32)).cuda() for a in (s, p, o))
-    pats = query_patterns(qname)
-    source = trip
-    if args.store == "index":  # each rank indexes its own shard once, at load time
-        source = ctx.index_build(trip)
-        del trip
-        torch.cuda.empty_cache()
+    mqd.ensure_dist(ctx)
+    if kind == "zipf":
+        # C4: each rank generates its contiguous row range of both sides (identical tables for any
+        # N), step = mapsq_join_dist (both sides exchanged on the key, local join)
+        import datagen
+        n = args.rows or nu
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        k1, v1 = datagen.zipf(hi - lo, 0, i_lo=lo)
+        k2, v2 = datagen.zipf(hi - lo, 1, i_lo=lo)
+        cols = [torch.from_numpy(a.view(np.int32)).cuda() for a in (k1, v1, k2, v2)]
+        A = mq.DeviceTable.from_torch([0, 1], cols[:2])
+        B = mq.DeviceTable.from_torch([0, 2], cols[2:])
+        ctx.table_bounds(A)
+        ctx.table_bounds(B)
+        pinned_bufs = None
+        args.no_e2e = True  # e2e is the LUBM query's host-buffer path
 
-    def step():
-        r = mqd.query_dist(ctx, source, pats)
-        return r.nrows
+        def step():
+            r = ctx.join_dist(A, B)
+            m = r.nrows
+            r.release()
+            return m
+    else:
+        lo, hi = nu * rank // world, nu * (rank + 1) // world
+        (s, p, o), st, pinned_bufs = lubm_host(nu, lo, hi, pinned=not args.no_e2e)
+        trip = tuple(torch.from_numpy(a.view(np.int32)).cuda() for a in (s, p, o))
+        pats = query_patterns(qname)
+        source = trip
+        if args.store == "index":  # each rank indexes its own shard once, at load time
+            source = ctx.index_build(trip)
+            del trip
+            torch.cuda.empty_cache()
+
+        def step():
+            r = mqd.query_dist(ctx, source, pats)
+            return r.nrows
 
     for _ in range(args.warmup):
         step()
@@ -467,8 +488,8 @@ def run_gpu_dist(args, world, rank, local):
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": {"workload": cfg, "description": desc,
                            "parallelism": f"hash-partitioned x{world}",
-                           "store": args.store, "semijoin_filter": args.semijoin,
-                           "l2": "inputs larger than L2"},
+                           "store": args.store if kind == "lubm" else None,
+                           "semijoin_filter": args.semijoin, "l2": "inputs larger than L2"},
                 "exchange": {"bytes_per_step": sent_all / args.steps,
                              "gbs_over_step_time": sent_all / total_s / 1e9,
                              "note": "bytes all ranks sent to peers per step (fused partition + "

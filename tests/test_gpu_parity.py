@@ -402,3 +402,35 @@ def test_partition_scatter_into_external_columns(ctx):
     got = np.concatenate([arenas[d][:, 7:].cpu().numpy().view(np.uint32).T for d in range(G)])
     assert np.array_equal(got, ref.to_numpy())
     assert all(int(arenas[d][:, :7].abs().sum()) == 0 for d in range(G))
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_virtual_ranks_partition_invariance(ctx, G):
+    """SURVEY T4's virtual-rank mode on one GPU: hash-partition both inputs into G parts (K8),
+    join part g with part g for every g, and the union of the G local joins is the full join —
+    the property the distributed join rests on (keys disjoint across parts)."""
+    rng = np.random.default_rng(40 + G)
+    A = np.stack([datagen_keys(rng, 20_011), rng.integers(0, 1 << 20, 20_011)], 1).astype(np.uint32)
+    B = np.stack([rng.integers(0, 1 << 20, 9_001), datagen_keys(rng, 9_001)], 1).astype(np.uint32)
+    ref = oracle.canonical(oracle.join(oracle.Table([0, 1], A), oracle.Table([2, 0], B))).rows
+    pa, ca = ctx.partition(dtable([0, 1], A), [0], G)
+    pb, cb = ctx.partition(dtable([2, 0], B), [0], G)
+    parts, keysets, oa, ob = [], [], 0, 0
+    for g in range(G):
+        ta = mq.DeviceTable.from_torch([0, 1], [c[oa:oa + ca[g]] for c in pa.columns])
+        tb = mq.DeviceTable.from_torch([2, 0], [c[ob:ob + cb[g]] for c in pb.columns])
+        oa, ob = oa + ca[g], ob + cb[g]
+        keysets.append(set(ta.to_numpy()[:, 0].tolist()) | set(tb.to_numpy()[:, 1].tolist()))
+        if ca[g] and cb[g]:
+            parts.append(ctx.join(ta, tb).to_numpy())
+    assert sum(len(k) for k in keysets) == len(set().union(*keysets))  # keys disjoint across parts
+    assert sum(1 for k in keysets if k) == G                           # every part is used
+    got = oracle.canonical_rows(np.concatenate(parts)) if parts else np.zeros((0, 3), np.uint32)
+    assert np.array_equal(got, ref)
+
+
+def datagen_keys(rng, n):
+    """Skewed keys (a few hot ones) over a small domain, so every part gets several groups."""
+    hot = rng.integers(0, 50, n)
+    cold = rng.integers(0, 3000, n)
+    return np.where(rng.random(n) < 0.3, hot, cold)
