@@ -313,6 +313,37 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
 // filters: a key sets/tests TWO bits of one 64-bit word (one memory access, like a plain bitmap,
 // but ~2/3 of its false positives at C5's load factor), chosen by a mix of key' with a
 // per-round seed, so a second round's false positives are independent of the first's.
+// Bitmap accesses of the blocked-Bloom kernels carry an L2 evict_last policy: the bitmap (up to
+// 64 MB) should survive the key columns streaming past it (those are loaded evict-first, __ldcs).
+#ifndef MAPSQ_L2_HINT
+#define MAPSQ_L2_HINT 1
+#endif
+__device__ __forceinline__ uint64_t bm_policy() {
+  uint64_t p = 0;
+#if MAPSQ_L2_HINT
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ uint64_t ld_bm(const unsigned long long *p, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  uint64_t v;
+  asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void red_or_bm(unsigned long long *p, uint64_t m, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  asm volatile("red.global.or.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(m), "l"(pol) : "memory");
+#else
+  (void)pol;
+  atomicOr(p, (unsigned long long)m);
+#endif
+}
+
 struct WSide {
   const uint64_t *w;
   uint64_t rows, slice0;
@@ -331,6 +362,7 @@ __device__ __forceinline__ void wblock(uint64_t w, uint32_t ib, uint64_t seed, u
 __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_t idx[kFItems],
                                            const uint64_t m[kFItems], uint32_t keep,
                                            uint32_t lane) {
+  const uint64_t pol = bm_policy();
 #pragma unroll
   for (int it = 0; it < kFItems; it++) {
     const uint32_t k = keep >> it & 1u;
@@ -338,7 +370,7 @@ __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_
     const uint64_t mp = __shfl_up_sync(0xffffffffu, m[it], 1);
     const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
     const bool dup = lane > 0 && kp && ip == idx[it] && mp == m[it];
-    if (k && !dup) atomicOr(bm + idx[it], (unsigned long long)m[it]);
+    if (k && !dup) red_or_bm(bm + idx[it], m[it], pol);
   }
 }
 
@@ -370,6 +402,7 @@ __global__ void __launch_bounds__(kFThreads)
 wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                      const unsigned long long *__restrict__ bm_probe,
                      uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
@@ -387,7 +420,7 @@ wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
       wblock(w[it], ib, seed, bbits, idx, m[it]);
-      v[it] = j < sd.rows ? __ldg(bm_probe + idx) : 0ull;
+      v[it] = j < sd.rows ? ld_bm(bm_probe + idx, pol) : 0ull;
     }
     uint32_t my = 0, c = 0;
 #pragma unroll
@@ -434,6 +467,7 @@ __global__ void __launch_bounds__(kFThreads)
 wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                       const unsigned long long *__restrict__ bm, uint32_t stride,
                       unsigned long long *__restrict__ sample) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   uint32_t c = 0, rows = 0;
@@ -452,7 +486,7 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
       wblock(w[it], ib, seed, bbits, idx, m[it]);
-      v[it] = j < sd.rows ? __ldg(bm + idx) : 0ull;
+      v[it] = j < sd.rows ? ld_bm(bm + idx, pol) : 0ull;
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
@@ -506,6 +540,7 @@ __global__ void __launch_bounds__(kFThreads)
 cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
                      const unsigned long long *__restrict__ bm_probe,
                      uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
@@ -519,7 +554,7 @@ cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
       cblock(key[it], bbits, idx, m[it]);
-      v[it] = j < sd.rows ? __ldg(bm_probe + idx) : 0ull;
+      v[it] = j < sd.rows ? ld_bm(bm_probe + idx, pol) : 0ull;
     }
     uint32_t my = 0, c = 0;
 #pragma unroll
@@ -564,6 +599,7 @@ __global__ void __launch_bounds__(kFThreads)
 cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
                       const unsigned long long *__restrict__ bm, uint32_t stride,
                       unsigned long long *__restrict__ sample) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   uint32_t c = 0, rows = 0;
@@ -578,7 +614,7 @@ cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t b
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
       cblock(key[it], bbits, idx, m[it]);
-      v[it] = j < sd.rows ? __ldg(bm + idx) : 0ull;
+      v[it] = j < sd.rows ? ld_bm(bm + idx, pol) : 0ull;
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
