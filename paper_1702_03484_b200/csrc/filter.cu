@@ -83,19 +83,72 @@ __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uin
   }
 }
 
+// Bitmap accesses of the filter kernels carry an L2 evict_last policy: the bitmap (up to
+// 64 MB) should survive the key columns streaming past it (those are loaded evict-first, __ldcs).
+#ifndef MAPSQ_L2_HINT
+#define MAPSQ_L2_HINT 1
+#endif
+__device__ __forceinline__ uint64_t bm_policy() {
+  uint64_t p = 0;
+#if MAPSQ_L2_HINT
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ uint64_t ld_bm(const unsigned long long *p, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  uint64_t v;
+  asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void red_or_bm(unsigned long long *p, uint64_t m, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  asm volatile("red.global.or.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(m), "l"(pol) : "memory");
+#else
+  (void)pol;
+  atomicOr(p, (unsigned long long)m);
+#endif
+}
+
+__device__ __forceinline__ uint32_t ld_bm32(const uint32_t *p, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void red_or_bm32(uint32_t *p, uint32_t m, uint64_t pol) {
+#if MAPSQ_L2_HINT
+  asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(m), "l"(pol) : "memory");
+#else
+  (void)pol;
+  atomicOr(p, m);
+#endif
+}
+
 // Set bit(key') in bm for the rows whose `keep` bit is set.  Test before set (a plain atomicOr
 // per row serialises on hot keys: 40 ms vs 5.9 ms for 5e8 Zipf rows, tools/bitmap_bench.cu), and
 // runs of equal keys in consecutive rows (clustered data) set their bit once: a lane whose left
 // neighbour holds the same bit skips.
 // TEST = false (keys mostly distinct, e.g. hashed composite keys): fire-and-forget RED.OR only
 // (208 vs 75 G rows/s for distinct keys, tools/bitmap_bench.cu).
-template <bool TEST = true>
+// HINT = false: no L2 policy (the probe's SET bitmap: with the probed one also hot, two 64 MB
+// evict_last bitmaps overflow L2 — C4's column probe 2.28 -> 2.57 ms with both hinted).
+template <bool TEST = true, bool HINT = true>
 __device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFItems],
                                          uint32_t keep, uint32_t lane) {
+  const uint64_t pol = HINT ? bm_policy() : 0;
   uint32_t word[kFItems];
 #pragma unroll
   for (int it = 0; it < kFItems; it++)  // (read-only path: a stale word costs one more atomic)
-    word[it] = (TEST && (keep >> it & 1u)) ? __ldg(bm + (bidx[it] >> 5)) : 0u;
+    word[it] = (TEST && (keep >> it & 1u)) ? (HINT ? ld_bm32(bm + (bidx[it] >> 5), pol) : __ldg(bm + (bidx[it] >> 5))) : 0u;
 #pragma unroll
   for (int it = 0; it < kFItems; it++) {
     const uint32_t b = bidx[it];
@@ -103,7 +156,12 @@ __device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFIte
     const uint32_t bp = __shfl_up_sync(0xffffffffu, b, 1);
     const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
     const bool dup = lane > 0 && kp && bp == b;
-    if (k && !dup && !(word[it] >> (b & 31) & 1u)) atomicOr(bm + (b >> 5), 1u << (b & 31));
+    if (k && !dup && !(word[it] >> (b & 31) & 1u)) {
+      if (HINT)
+        red_or_bm32(bm + (b >> 5), 1u << (b & 31), pol);
+      else
+        atomicOr(bm + (b >> 5), 1u << (b & 31));
+    }
   }
 }
 
@@ -135,6 +193,7 @@ __global__ void __launch_bounds__(kFThreads)
 filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm_probe,
                     uint32_t *__restrict__ bm_set, uint32_t bbits, uint32_t hashed,
                     uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
@@ -147,7 +206,7 @@ filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict_
     for (int it = 0; it < kFItems; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       bidx[it] = bit_index(key[it], bbits, hashed);
-      word[it] = j < sd.rows ? __ldg(bm_probe + (bidx[it] >> 5)) : 0u;
+      word[it] = j < sd.rows ? ld_bm32(bm_probe + (bidx[it] >> 5), pol) : 0u;
     }
     uint32_t my = 0, c = 0, keep = 0;
 #pragma unroll
@@ -160,7 +219,7 @@ filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict_
     }
     if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
     if (lane == 0) cnt[sd.slice0 + ws] = c;
-    if (SET && c) set_bits(bm_set, bidx, keep, lane);
+    if (SET && c) set_bits<true, false>(bm_set, bidx, keep, lane);
   }
 }
 
@@ -171,6 +230,7 @@ __global__ void __launch_bounds__(kFThreads)
 filter_sample_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm,
                      uint32_t bbits, uint32_t hashed, uint32_t stride,
                      unsigned long long *__restrict__ sample) {
+  const uint64_t pol = bm_policy();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   uint32_t c = 0, rows = 0;
@@ -184,7 +244,7 @@ filter_sample_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict
     for (int it = 0; it < kFItems; it++) {  // all probes in flight together
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       bidx[it] = bit_index(key[it], bbits, hashed);
-      word[it] = j < sd.rows ? __ldg(bm + (bidx[it] >> 5)) : 0u;
+      word[it] = j < sd.rows ? ld_bm32(bm + (bidx[it] >> 5), pol) : 0u;
     }
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
@@ -313,37 +373,6 @@ filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
 // filters: a key sets/tests TWO bits of one 64-bit word (one memory access, like a plain bitmap,
 // but ~2/3 of its false positives at C5's load factor), chosen by a mix of key' with a
 // per-round seed, so a second round's false positives are independent of the first's.
-// Bitmap accesses of the blocked-Bloom kernels carry an L2 evict_last policy: the bitmap (up to
-// 64 MB) should survive the key columns streaming past it (those are loaded evict-first, __ldcs).
-#ifndef MAPSQ_L2_HINT
-#define MAPSQ_L2_HINT 1
-#endif
-__device__ __forceinline__ uint64_t bm_policy() {
-  uint64_t p = 0;
-#if MAPSQ_L2_HINT
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-#endif
-  return p;
-}
-__device__ __forceinline__ uint64_t ld_bm(const unsigned long long *p, uint64_t pol) {
-#if MAPSQ_L2_HINT
-  uint64_t v;
-  asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
-  return v;
-#else
-  (void)pol;
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ void red_or_bm(unsigned long long *p, uint64_t m, uint64_t pol) {
-#if MAPSQ_L2_HINT
-  asm volatile("red.global.or.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(m), "l"(pol) : "memory");
-#else
-  (void)pol;
-  atomicOr(p, (unsigned long long)m);
-#endif
-}
-
 struct WSide {
   const uint64_t *w;
   uint64_t rows, slice0;
