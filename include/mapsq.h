@@ -330,6 +330,10 @@ mapsq_status mapsq_exchange_layout(int world, int rank, int ncols, const uint64_
  * mapsq_dist_init) carries only the count matrix, the arena handles, the column bounds (min/max
  * all-reduce, so the local join range-compresses keys without a min/max pass) and the two
  * barriers around each scatter.  Every call is collective: all ranks call it in the same order.
+ * Errors: argument errors are detected before the first collective on every rank alike (same
+ * tables' schemas); a rank that fails later (allocation, CUDA, NCCL) returns its status while its
+ * peers may stay blocked in the next collective — the caller aborts the job (queries are
+ * stateless and are simply re-run).
  *
  * mapsq_dist_unique_id: a fresh 128-byte NCCL unique id (one rank creates it; the caller
  *   broadcasts it, e.g. with torch.distributed).
