@@ -253,6 +253,27 @@ mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
                                  const mapsq_pattern *pats, int npats, const int32_t *proj,
                                  int nproj, mapsq_table *rs, void *stream);
 
+/* ---- host-resident store (end-to-end path over host memory) ----
+ * The paper's division of labour: the store answers partial matching on the host and the GPU
+ * joins the partial matches.  mapsq_index_to_host mirrors an index into
+ * pinned host memory (12 B per triple + metadata; blocking, once per dataset).
+ * mapsq_query_host_indexed answers a query from that mirror: it copies to the device ONLY the
+ * predicate ranges the query's patterns touch (s and o of every constant-predicate range; p too
+ * when a pattern scans the range instead of viewing it; the whole table if a pattern has a
+ * variable predicate), runs mapsq_query_indexed's path on them, and reads the result back into the
+ * context's pinned result arena exactly as mapsq_query_host does (same output contract, same
+ * result rows as mapsq_query_indexed over the device index).  *h2d_bytes (optional) receives the
+ * bytes copied host -> device.  Synchronous. */
+typedef struct mapsq_host_index mapsq_host_index;
+mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *idx, mapsq_host_index **out,
+                                 void *stream);
+void mapsq_host_index_destroy(mapsq_host_index *h);
+mapsq_status mapsq_query_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *h,
+                                      const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                      int nproj, uint64_t *host_rows, uint32_t *out_ncols,
+                                      int32_t *out_var, uint32_t **host_cols, uint64_t *h2d_bytes,
+                                      void *stream);
+
 /* ---- phase entry points (for phase-level parity tests; the same kernels mapsq_join runs) ----
  * Map (K2, row a3): words[r] = key'(tp1 row r) << ib | r and words[n1 + r] = key'(tp2 row r)
  * << ib | (n1 + r) for a P64 plan (a RESIDUAL plan packs only its packed_mask columns; a KV

@@ -118,6 +118,12 @@ def lib():
             "mapsq_scan_patterns_indexed": (st, [vp, vp, PP, ctypes.c_int, PT, vp]),
             "mapsq_query_indexed": (st, [vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
                                          ctypes.c_int, PT, vp]),
+            "mapsq_index_to_host": (st, [vp, vp, ctypes.POINTER(vp), vp]),
+            "mapsq_host_index_destroy": (None, [vp]),
+            "mapsq_query_host_indexed": (st, [vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
+                                              ctypes.c_int, ctypes.POINTER(u64),
+                                              ctypes.POINTER(u32), ctypes.POINTER(i32),
+                                              ctypes.POINTER(vp), ctypes.POINTER(u64), vp]),
             "mapsq_map_words": (st, [vp, PT, PT, ctypes.POINTER(JoinPlan), vp, vp]),
             "mapsq_sort_words": (st, [vp, vp, u64, u32, u32, vp]),
             "mapsq_sort_pairs": (st, [vp, vp, vp, u64, u32, u32, vp]),
@@ -335,6 +341,26 @@ class Index:
             pass
 
 
+class HostIndex:
+    """Pinned host mirror of an Index (mapsq_index_to_host): pass it to Context.query_host to
+    answer a query from host memory, copying only the predicate ranges the query touches."""
+
+    def __init__(self, handle):
+        self.handle = handle
+        self.last_h2d_bytes = 0
+
+    def release(self):
+        if self.handle:
+            lib().mapsq_host_index_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
 class Context:
     """One libmapsq context on one device (default allocator: cudaMallocAsync pool)."""
 
@@ -416,11 +442,22 @@ class Context:
                                       ctypes.byref(out), _stream(stream)))
         return _wrap(self, out)
 
-    def query_host(self, s, p, o, patterns, proj=None, stream=None, copy=False):
-        """End to end over host (numpy, ideally pinned) triples: returns (vars, rows) where rows
-        is an (nrows, ncols) view of the context's pinned result arena (valid until the next
-        query_host on this context) or, with copy=True, an independent array."""
+    def index_to_host(self, index: Index, stream=None) -> HostIndex:
+        """Mirror a device Index into pinned host memory (blocking, once per dataset)."""
+        h = ctypes.c_void_p()
+        self._check(lib().mapsq_index_to_host(self.handle, index.handle, ctypes.byref(h),
+                                              _stream(stream)))
+        return HostIndex(h)
+
+    def query_host(self, s, p=None, o=None, patterns=None, proj=None, stream=None, copy=False):
+        """End to end over host memory: ``s, p, o`` (numpy, ideally pinned) triples, or a
+        HostIndex as the first argument (then only the ranges the query touches are copied;
+        ``HostIndex.last_h2d_bytes`` records how many bytes).  Returns (vars, rows) where rows is an
+        (nrows, ncols) view of the context's pinned result arena (valid until the next query_host
+        on this context) or, with copy=True, an independent array."""
         import numpy as np
+        if isinstance(s, HostIndex) and patterns is None:
+            patterns, p = p, None
         k = len(patterns)
         pats = (_Pattern * k)(*[pattern_struct(q) for q in patterns])
         proj = list(proj or [])
@@ -429,10 +466,16 @@ class Context:
         ovar = (ctypes.c_int32 * MAX_COLS)()
         ocol = (ctypes.c_void_p * MAX_COLS)()
         ptr = lambda a: a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr()  # noqa: E731
-        n = len(s)
-        self._check(lib().mapsq_query_host(self.handle, n, ptr(s), ptr(p), ptr(o), pats, k, pr,
-                                           len(proj), ctypes.byref(nrows), ctypes.byref(ncols),
-                                           ovar, ocol, _stream(stream)))
+        if isinstance(s, HostIndex):
+            h2d = ctypes.c_uint64()
+            self._check(lib().mapsq_query_host_indexed(
+                self.handle, s.handle, pats, k, pr, len(proj), ctypes.byref(nrows),
+                ctypes.byref(ncols), ovar, ocol, ctypes.byref(h2d), _stream(stream)))
+            s.last_h2d_bytes = int(h2d.value)
+        else:
+            self._check(lib().mapsq_query_host(self.handle, len(s), ptr(s), ptr(p), ptr(o), pats, k,
+                                               pr, len(proj), ctypes.byref(nrows),
+                                               ctypes.byref(ncols), ovar, ocol, _stream(stream)))
         m, w = int(nrows.value), int(ncols.value)
         vars_ = [int(ovar[c]) for c in range(w)]
         if m == 0 or w == 0:

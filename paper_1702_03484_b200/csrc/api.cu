@@ -1422,6 +1422,45 @@ MAPSQ_API mapsq_status mapsq_query(mapsq_ctx *ctx, const mapsq_triples *T,
   return query_impl(ctx, T, pats, npats, proj, nproj, rs, S(stream));
 }
 
+// Copy a result table into the context's pinned result arena (grown on demand) and release it;
+// synchronous.  Shared by the host-buffer entry points.
+static mapsq_status result_to_host(mapsq_ctx *ctx, mapsq_table *rs, cudaStream_t s,
+                                   uint64_t *host_rows, uint32_t *out_ncols, int32_t *out_var,
+                                   uint32_t **host_cols) {
+  const uint64_t m = rs->nrows;
+  const uint32_t w = rs->ncols;
+  const size_t need = std::max<size_t>(16, (size_t)m * w * sizeof(uint32_t));
+  if (need > ctx->host_arena_bytes) {
+    if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
+    ctx->host_arena = nullptr;
+    ctx->host_arena_bytes = 0;
+    cudaError_t e = cudaMallocHost(&ctx->host_arena, need);
+    if (e != cudaSuccess) {
+      ctx->host_arena = nullptr;
+      mapsq_table_release(ctx, rs, s);
+      return cuda_check(ctx, e, "cudaMallocHost(result arena)");
+    }
+    ctx->host_arena_bytes = need;
+  }
+  uint32_t *arena = static_cast<uint32_t *>(ctx->host_arena);
+  mapsq_status st = MAPSQ_OK;
+  for (uint32_t c = 0; c < w; c++) {
+    out_var[c] = rs->var[c];
+    host_cols[c] = arena + (size_t)c * m;
+    if (m && st == MAPSQ_OK) {
+      cudaError_t e = cudaMemcpyAsync(host_cols[c], rs->col[c], m * 4, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) st = cuda_check(ctx, e, "D2H result");
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  mapsq_table_release(ctx, rs, s);
+  if (st == MAPSQ_OK && e != cudaSuccess) st = cuda_check(ctx, e, "sync");
+  if (st != MAPSQ_OK) return st;
+  *out_ncols = w;
+  *host_rows = m;
+  return MAPSQ_OK;
+}
+
 MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32_t *s_host,
                                         const uint32_t *p_host, const uint32_t *o_host,
                                         const mapsq_pattern *pats, int npats,
@@ -1451,38 +1490,123 @@ MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32
     mapsq_triples T{n, ds, dp, dob};
     TRY(query_impl(ctx, &T, pats, npats, proj, nproj, &rs, s));
   }
-  const uint64_t m = rs.nrows;
-  const uint32_t w = rs.ncols;
-  const size_t need = std::max<size_t>(16, (size_t)m * w * sizeof(uint32_t));
-  if (need > ctx->host_arena_bytes) {
-    if (ctx->host_arena) cudaFreeHost(ctx->host_arena);
-    ctx->host_arena = nullptr;
-    ctx->host_arena_bytes = 0;
-    const size_t bytes = std::max(need, ctx->host_arena_bytes * 2);
-    cudaError_t e = cudaMallocHost(&ctx->host_arena, bytes);
-    if (e != cudaSuccess) {
-      ctx->host_arena = nullptr;
-      mapsq_table_release(ctx, &rs, stream);
-      return cuda_check(ctx, e, "cudaMallocHost(result arena)");
-    }
-    ctx->host_arena_bytes = bytes;
+  return result_to_host(ctx, &rs, s, host_rows, out_ncols, out_var, host_cols);
+}
+
+// ------------------------------------------------------------------ host-resident index (e2e)
+struct mapsq_host_index {
+  uint64_t n = 0;
+  uint32_t *s = nullptr, *p = nullptr, *o = nullptr;  // pinned, one allocation at s
+  std::vector<uint32_t> pred;
+  std::vector<uint64_t> start;
+  std::vector<uint32_t> slo, shi, olo, ohi;
+};
+
+MAPSQ_API void mapsq_host_index_destroy(mapsq_host_index *h) {
+  if (!h) return;
+  if (h->s) cudaFreeHost(h->s);
+  delete h;
+}
+
+MAPSQ_API mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *idx,
+                                           mapsq_host_index **out, void *stream) {
+  TRY(enter(ctx));
+  if (!idx || !out) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
+  *out = nullptr;
+  std::unique_ptr<mapsq_host_index> h(new (std::nothrow) mapsq_host_index());
+  if (!h) return set_error(ctx, MAPSQ_E_NOMEM, "host allocation failed");
+  h->n = idx->n;
+  h->pred = idx->pred;
+  h->start = idx->start;
+  h->slo = idx->slo;
+  h->shi = idx->shi;
+  h->olo = idx->olo;
+  h->ohi = idx->ohi;
+  if (idx->n) {
+    void *p = nullptr;
+    CK(cudaMallocHost(&p, 12 * idx->n));
+    h->s = static_cast<uint32_t *>(p);
+    h->p = h->s + idx->n;
+    h->o = h->p + idx->n;
+    cudaStream_t s = S(stream);
+    CK(cudaMemcpyAsync(h->s, idx->s, 4 * idx->n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h->p, idx->p, 4 * idx->n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h->o, idx->o, 4 * idx->n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   }
-  uint32_t *arena = static_cast<uint32_t *>(ctx->host_arena);
-  mapsq_status st = MAPSQ_OK;
-  for (uint32_t c = 0; c < w; c++) {
-    out_var[c] = rs.var[c];
-    host_cols[c] = arena + (size_t)c * m;
-    if (m && st == MAPSQ_OK) {
-      cudaError_t e = cudaMemcpyAsync(host_cols[c], rs.col[c], m * 4, cudaMemcpyDeviceToHost, s);
-      if (e != cudaSuccess) st = cuda_check(ctx, e, "D2H result");
+  *out = h.release();
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_query_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *h,
+                                                const mapsq_pattern *pats, int npats,
+                                                const int32_t *proj, int nproj,
+                                                uint64_t *host_rows, uint32_t *out_ncols,
+                                                int32_t *out_var, uint32_t **host_cols,
+                                                uint64_t *h2d_bytes, void *stream) {
+  TRY(enter(ctx));
+  if (!h || !host_rows || !out_ncols || !out_var || !host_cols || !pats || npats < 1 ||
+      npats > MAPSQ_MAX_PATTERNS)
+    return set_error(ctx, MAPSQ_E_INVALID, "bad argument");
+  *host_rows = 0;
+  *out_ncols = 0;
+  if (h2d_bytes) *h2d_bytes = 0;
+  cudaStream_t s = S(stream);
+  // the predicate ranges the query touches (every row if a pattern has a variable predicate) and
+  // whether a pattern scans the range (then its p column is needed; views read only s and o)
+  const size_t np = h->pred.size();
+  bool all = false;
+  std::vector<int> need(np, 0);  // 0 no, 1 s/o, 2 s/p/o
+  for (int j = 0; j < npats; j++) {
+    const mapsq_pattern &P = pats[j];
+    if (P.var[1] >= 0) {
+      all = true;
+      continue;
     }
+    auto it = std::lower_bound(h->pred.begin(), h->pred.end(), P.id[1]);
+    if (it == h->pred.end() || *it != P.id[1]) continue;  // absent: matches nothing
+    const bool view = P.var[0] >= 0 && P.var[2] >= 0 && P.var[0] != P.var[2];
+    int &nd = need[it - h->pred.begin()];
+    nd = std::max(nd, view ? 1 : 2);
   }
-  mapsq_table_release(ctx, &rs, stream);
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (st == MAPSQ_OK && e != cudaSuccess) st = cuda_check(ctx, e, "sync");
-  if (st != MAPSQ_OK) return st;
-  *out_ncols = w;
-  *host_rows = m;
+  mapsq_index D;  // device-side index over the copied ranges (columns owned by the scratch)
+  mapsq_table rs;
+  uint64_t bytes = 0;
+  {
+    Scratch sc(ctx, s);
+    uint64_t rows = 0;
+    for (size_t r = 0; r < np; r++)
+      if (all || need[r]) rows += h->start[r + 1] - h->start[r];
+    const uint64_t stride = (rows + 3) & ~3ull;
+    uint32_t *d = sc.get<uint32_t>(3 * stride + 12);
+    NEED(d);
+    D.n = rows;
+    D.s = d;
+    D.p = d + stride;
+    D.o = d + 2 * stride;
+    D.start.push_back(0);
+    for (size_t r = 0; r < np; r++) {
+      if (!all && !need[r]) continue;
+      const uint64_t b = h->start[r], c = h->start[r + 1] - b, at = D.start.back();
+      CK(cudaMemcpyAsync(D.s + at, h->s + b, 4 * c, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(D.o + at, h->o + b, 4 * c, cudaMemcpyHostToDevice, s));
+      bytes += 8 * c;
+      if (all || need[r] == 2) {
+        CK(cudaMemcpyAsync(D.p + at, h->p + b, 4 * c, cudaMemcpyHostToDevice, s));
+        bytes += 4 * c;
+      }
+      D.pred.push_back(h->pred[r]);
+      D.start.push_back(at + c);
+      D.slo.push_back(h->slo[r]);
+      D.shi.push_back(h->shi[r]);
+      D.olo.push_back(h->olo[r]);
+      D.ohi.push_back(h->ohi[r]);
+    }
+    TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D));
+    // the result may be a zero-copy view of the copied ranges: read it back inside this scope
+    TRY(result_to_host(ctx, &rs, s, host_rows, out_ncols, out_var, host_cols));
+  }
+  if (h2d_bytes) *h2d_bytes = bytes;
   return MAPSQ_OK;
 }
 
