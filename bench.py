@@ -418,14 +418,18 @@ def run_gpu_dist(args, world, rank, local):
             return m
     else:
         lo, hi = nu * rank // world, nu * (rank + 1) // world
-        (s, p, o), st, pinned_bufs = lubm_host(nu, lo, hi, pinned=not args.no_e2e)
+        (s, p, o), st, pinned_bufs = lubm_host(
+            nu, lo, hi, pinned=not args.no_e2e and args.store == "scan")
         trip = tuple(torch.from_numpy(a.view(np.int32)).cuda() for a in (s, p, o))
         pats = query_patterns(qname)
         source = trip
+        hidx = None
         if args.store == "index":  # each rank indexes its own shard once, at load time
             source = ctx.index_build(trip)
             del trip
             torch.cuda.empty_cache()
+            if not args.no_e2e:  # and mirrors it into pinned host memory (the e2e store)
+                hidx = ctx.index_to_host(source)
 
         def step():
             r = mqd.query_dist(ctx, source, pats)
@@ -457,24 +461,30 @@ def run_gpu_dist(args, world, rank, local):
     # region 1 (the value): no per-kernel events; region 2: per-kernel events for the roofline
     ms, st_plain, clocks, sent = timed(False)
     _, st_k, _, _ = timed(True)
-    # e2e at N GPUs: every step each rank copies its shard's triples from pinned host memory,
-    # runs the distributed query (full-table scan: the data arrives fresh) and reads its result
-    # shard back; the step time is the max over ranks
+    # e2e at N GPUs: every step each rank copies from pinned host memory what its shard's query
+    # needs (index store: the touched predicate ranges of its host-resident store; scan store:
+    # its whole shard), runs the distributed query and reads its result shard back; the step
+    # time is the max over ranks
     e2e = None
     if not args.no_e2e:
-        dev_bufs = [torch.empty(len(s), dtype=torch.int32, device="cuda") for _ in range(3)]
+        if hidx is None:
+            dev_bufs = [torch.empty(len(s), dtype=torch.int32, device="cuda") for _ in range(3)]
         e2e_ms, h2d, d2h = [], 12 * len(s), 0
         for i in range(max(1, min(args.steps, 3)) + 1):
             tdist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for d, h in zip(dev_bufs, pinned_bufs):
-                d.copy_(h, non_blocking=True)
-            r = mqd.query_dist(ctx, tuple(dev_bufs), pats)
-            host = [c.cpu() for c in r.columns]
+            if hidx is not None:
+                _, rows = ctx.query_dist_host(hidx, pats)
+                h2d, d2h = hidx.last_h2d_bytes, rows.nbytes
+            else:
+                for d, h in zip(dev_bufs, pinned_bufs):
+                    d.copy_(h, non_blocking=True)
+                r = mqd.query_dist(ctx, tuple(dev_bufs), pats)
+                host = [c.cpu() for c in r.columns]
+                d2h = sum(x.numel() * 4 for x in host)
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) * 1e3
-            d2h = sum(x.numel() * 4 for x in host)
             if i:
                 e2e_ms.append(dt)
         tm = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
@@ -513,8 +523,11 @@ def run_gpu_dist(args, world, rank, local):
                     "value": (tup / args.steps) / (e2e[0] / 1e3), "unit": "tuples/s",
                     "h2d_bytes_per_step": e2e[1], "d2h_bytes_per_step": e2e[2],
                     "ms_per_step": e2e[0],
-                    "path": "per rank: pinned shard H2D, full-table scan, distributed joins, "
-                            "result shard D2H; max over ranks"},
+                    "path": ("per rank: mapsq_query_dist_host_indexed (touched predicate ranges "
+                             "of the rank's host store H2D, distributed joins, result shard D2H)"
+                             if args.store == "index" else
+                             "per rank: pinned shard H2D, full-table scan, distributed joins, "
+                             "result shard D2H") + "; max over ranks"},
                 "clocks": clocks, "gpu_launches": int(launches),
                 "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
                                 "rank": 0} for k, v in st_k["kernels"].items()}}

@@ -368,6 +368,9 @@ mapsq_status mapsq_exchange_layout(int world, int rank, int ncols, const uint64_
  *   lives, no exchange), then folds the joins left-deep with one exchange per join; an input
  *   already partitioned on the join's key (the previous join's result, when the key is unchanged)
  *   is not exchanged again.  Projection as mapsq_query. */
+/* mapsq_query_dist_host_indexed: the end-to-end form over this rank's host-resident store
+ *   (mapsq_query_host_indexed's contract: only the touched predicate ranges go host -> device;
+ *   this rank's result shard lands in the context's pinned result arena). */
 #define MAPSQ_DIST_ID_BYTES 128
 mapsq_status mapsq_dist_unique_id(void *id128);
 mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int rank, int world);
@@ -379,6 +382,12 @@ mapsq_status mapsq_query_dist(mapsq_ctx *ctx, const mapsq_triples *shard,
 mapsq_status mapsq_query_dist_indexed(mapsq_ctx *ctx, const mapsq_index *shard,
                                       const mapsq_pattern *pats, int npats, const int32_t *proj,
                                       int nproj, mapsq_table *rs_shard, void *stream);
+mapsq_status mapsq_query_dist_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *shard,
+                                           const mapsq_pattern *pats, int npats,
+                                           const int32_t *proj, int nproj, uint64_t *host_rows,
+                                           uint32_t *out_ncols, int32_t *out_var,
+                                           uint32_t **host_cols, uint64_t *h2d_bytes,
+                                           void *stream);
 
 /* Compute exact inclusive bounds lo[]/hi[] of every column of a (caller-built) table and set
  * MAPSQ_TABLE_BOUNDS (one min/max pass, blocking).  An empty table gets lo = hi = 0. */

@@ -124,6 +124,10 @@ def lib():
                                               ctypes.c_int, ctypes.POINTER(u64),
                                               ctypes.POINTER(u32), ctypes.POINTER(i32),
                                               ctypes.POINTER(vp), ctypes.POINTER(u64), vp]),
+            "mapsq_query_dist_host_indexed": (st, [vp, vp, PP, ctypes.c_int, ctypes.POINTER(i32),
+                                                   ctypes.c_int, ctypes.POINTER(u64),
+                                                   ctypes.POINTER(u32), ctypes.POINTER(i32),
+                                                   ctypes.POINTER(vp), ctypes.POINTER(u64), vp]),
             "mapsq_map_words": (st, [vp, PT, PT, ctypes.POINTER(JoinPlan), vp, vp]),
             "mapsq_sort_words": (st, [vp, vp, u64, u32, u32, vp]),
             "mapsq_sort_pairs": (st, [vp, vp, vp, u64, u32, u32, vp]),
@@ -449,7 +453,13 @@ class Context:
                                               _stream(stream)))
         return HostIndex(h)
 
-    def query_host(self, s, p=None, o=None, patterns=None, proj=None, stream=None, copy=False):
+    def query_dist_host(self, shard: "HostIndex", patterns, proj=None, stream=None, copy=False):
+        """mapsq_query_dist_host_indexed: this rank's result shard, end to end over its
+        host-resident store (collective).  Returns (vars, rows) like query_host."""
+        return self.query_host(shard, patterns, proj=proj, stream=stream, copy=copy, _dist=True)
+
+    def query_host(self, s, p=None, o=None, patterns=None, proj=None, stream=None, copy=False,
+                   _dist=False):
         """End to end over host memory: ``s, p, o`` (numpy, ideally pinned) triples, or a
         HostIndex as the first argument (then only the ranges the query touches are copied;
         ``HostIndex.last_h2d_bytes`` records how many bytes).  Returns (vars, rows) where rows is an
@@ -468,9 +478,9 @@ class Context:
         ptr = lambda a: a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr()  # noqa: E731
         if isinstance(s, HostIndex):
             h2d = ctypes.c_uint64()
-            self._check(lib().mapsq_query_host_indexed(
-                self.handle, s.handle, pats, k, pr, len(proj), ctypes.byref(nrows),
-                ctypes.byref(ncols), ovar, ocol, ctypes.byref(h2d), _stream(stream)))
+            fn = lib().mapsq_query_dist_host_indexed if _dist else lib().mapsq_query_host_indexed
+            self._check(fn(self.handle, s.handle, pats, k, pr, len(proj), ctypes.byref(nrows),
+                           ctypes.byref(ncols), ovar, ocol, ctypes.byref(h2d), _stream(stream)))
             s.last_h2d_bytes = int(h2d.value)
         else:
             self._check(lib().mapsq_query_host(self.handle, len(s), ptr(s), ptr(p), ptr(o), pats, k,

@@ -1538,12 +1538,12 @@ MAPSQ_API mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *id
   return MAPSQ_OK;
 }
 
-MAPSQ_API mapsq_status mapsq_query_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *h,
-                                                const mapsq_pattern *pats, int npats,
-                                                const int32_t *proj, int nproj,
-                                                uint64_t *host_rows, uint32_t *out_ncols,
-                                                int32_t *out_var, uint32_t **host_cols,
-                                                uint64_t *h2d_bytes, void *stream) {
+namespace mapsq {
+mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
+                                     const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                     int nproj, uint64_t *host_rows, uint32_t *out_ncols,
+                                     int32_t *out_var, uint32_t **host_cols, uint64_t *h2d_bytes,
+                                     void *stream, const JoinStep *step) {
   TRY(enter(ctx));
   if (!h || !host_rows || !out_ncols || !out_var || !host_cols || !pats || npats < 1 ||
       npats > MAPSQ_MAX_PATTERNS)
@@ -1602,12 +1602,23 @@ MAPSQ_API mapsq_status mapsq_query_host_indexed(mapsq_ctx *ctx, const mapsq_host
       D.olo.push_back(h->olo[r]);
       D.ohi.push_back(h->ohi[r]);
     }
-    TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D));
+    TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D, step));
     // the result may be a zero-copy view of the copied ranges: read it back inside this scope
     TRY(result_to_host(ctx, &rs, s, host_rows, out_ncols, out_var, host_cols));
   }
   if (h2d_bytes) *h2d_bytes = bytes;
   return MAPSQ_OK;
+}
+}  // namespace mapsq
+
+MAPSQ_API mapsq_status mapsq_query_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *h,
+                                                const mapsq_pattern *pats, int npats,
+                                                const int32_t *proj, int nproj,
+                                                uint64_t *host_rows, uint32_t *out_ncols,
+                                                int32_t *out_var, uint32_t **host_cols,
+                                                uint64_t *h2d_bytes, void *stream) {
+  return query_host_indexed_impl(ctx, h, pats, npats, proj, nproj, host_rows, out_ncols, out_var,
+                                 host_cols, h2d_bytes, stream, nullptr);
 }
 
 MAPSQ_API mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream) {

@@ -319,13 +319,17 @@ mapsq_status dist_enter(mapsq_ctx *ctx) {
   return MAPSQ_OK;
 }
 
+JoinStep dist_step(mapsq_ctx *ctx, std::vector<int32_t> *part) {
+  return [ctx, part](const mapsq_table *acc, const mapsq_table *t, mapsq_table *out,
+                     cudaStream_t st) { return join_dist_step(ctx, acc, t, out, st, part); };
+}
+
 mapsq_status query_dist_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_index *idx,
                              const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
                              mapsq_table *rs, cudaStream_t s) {
   TRY(dist_enter(ctx));
   std::vector<int32_t> part;  // key the accumulated result is partitioned on (none: scan output)
-  JoinStep step = [ctx, &part](const mapsq_table *acc, const mapsq_table *t, mapsq_table *out,
-                               cudaStream_t st) { return join_dist_step(ctx, acc, t, out, st, &part); };
+  const JoinStep step = dist_step(ctx, &part);
   return query_fold(ctx, T, idx, pats, npats, proj, nproj, rs, s, &step);
 }
 
@@ -417,4 +421,17 @@ MAPSQ_API mapsq_status mapsq_query_dist_indexed(mapsq_ctx *ctx, const mapsq_inde
                                                 void *stream) {
   if (!shard) return ctx ? set_error(ctx, MAPSQ_E_INVALID, "shard is NULL") : MAPSQ_E_INVALID;
   return query_dist_impl(ctx, nullptr, shard, pats, npats, proj, nproj, rs, S(stream));
+}
+
+MAPSQ_API mapsq_status mapsq_query_dist_host_indexed(mapsq_ctx *ctx, const mapsq_host_index *shard,
+                                                     const mapsq_pattern *pats, int npats,
+                                                     const int32_t *proj, int nproj,
+                                                     uint64_t *host_rows, uint32_t *out_ncols,
+                                                     int32_t *out_var, uint32_t **host_cols,
+                                                     uint64_t *h2d_bytes, void *stream) {
+  TRY(dist_enter(ctx));
+  std::vector<int32_t> part;
+  const JoinStep step = dist_step(ctx, &part);
+  return query_host_indexed_impl(ctx, shard, pats, npats, proj, nproj, host_rows, out_ncols,
+                                 out_var, host_cols, h2d_bytes, stream, &step);
 }

@@ -86,6 +86,11 @@ mapsq_status query_fold(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_inde
                         const mapsq_pattern *pats, int npats, const int32_t *proj, int nproj,
                         mapsq_table *rs, cudaStream_t s, const JoinStep *step);
 void dist_free(mapsq_ctx *ctx);  // dist.cu: communicator, arenas, peer mappings
+mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
+                                     const mapsq_pattern *pats, int npats, const int32_t *proj,
+                                     int nproj, uint64_t *host_rows, uint32_t *out_ncols,
+                                     int32_t *out_var, uint32_t **host_cols, uint64_t *h2d_bytes,
+                                     void *stream, const JoinStep *step);
 mapsq_status cuda_check(mapsq_ctx *ctx, cudaError_t e, const char *what);
 void *dalloc(mapsq_ctx *ctx, size_t bytes, cudaStream_t s);
 void dfree(mapsq_ctx *ctx, void *p, cudaStream_t s);

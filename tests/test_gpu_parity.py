@@ -382,6 +382,14 @@ def test_query_dist_world1_nccl(ctx, tmp_path):
     with pytest.raises(mq.MapsqError) as e:
         c2.dist_init()                           # once per context
     assert e.value.code == 1
+    hidx = c2.index_to_host(store)               # end to end over the host-resident store
+    for cfg in ("C5", "C2"):
+        pats = config_query(cfg)
+        vars_, rows = c2.query_dist_host(hidx, pats, copy=True)
+        ref = oracle.query(s, p, o, pats)
+        assert vars_ == ref.vars
+        assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows)
+        assert 0 < hidx.last_h2d_bytes < 12 * len(s)
     tdist.destroy_process_group()
 
 
