@@ -412,7 +412,7 @@ def run_gpu_dist(args, world, rank, local):
         args.no_e2e = True  # e2e is the LUBM query's host-buffer path
 
         def step():
-            r = ctx.join_dist(A, B)
+            r, _ = mqd.join_dist(ctx, A, B)
             m = r.nrows
             r.release()
             return m
@@ -466,7 +466,7 @@ def run_gpu_dist(args, world, rank, local):
     # its whole shard), runs the distributed query and reads its result shard back; the step
     # time is the max over ranks
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not (hidx is not None and getattr(ctx, "ipc_unavailable", None)):
         if hidx is None:
             dev_bufs = [torch.empty(len(s), dtype=torch.int32, device="cuda") for _ in range(3)]
         e2e_ms, h2d, d2h = [], 12 * len(s), 0
@@ -511,7 +511,12 @@ def run_gpu_dist(args, world, rank, local):
                 "config": {"workload": cfg, "description": desc,
                            "parallelism": f"hash-partitioned x{world}",
                            "store": args.store if kind == "lubm" else None,
-                           "semijoin_filter": args.semijoin, "l2": "inputs larger than L2"},
+                           "semijoin_filter": args.semijoin, "l2": "inputs larger than L2",
+                           "exchange_path": ("torch all_to_all (CUDA IPC unavailable: "
+                                             f"{ctx.ipc_unavailable})"
+                                             if getattr(ctx, "ipc_unavailable", None) else
+                                             "fused K8 scatter into CUDA-IPC peer arenas "
+                                             "(mapsq_*_dist)")},
                 "exchange": {"bytes_per_step": sent_all / args.steps,
                              "gbs_over_step_time": sent_all / total_s / 1e9,
                              "note": "bytes all ranks sent to peers per step (fused partition + "

@@ -89,6 +89,19 @@ const NcclApi &nccl() {
     if (_st != MAPSQ_OK) return _st;            \
   } while (0)
 
+// CUDA IPC failures (e.g. a container without IPC between the rank processes) are reported as
+// MAPSQ_E_CUDA with "CUDA IPC" in the message but do NOT poison the context: the caller can fall
+// back to an exchange without peer mappings (paper_1702_03484_b200.dist does).
+#define CKIPC(call)                                                                        \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      cudaGetLastError();                                                                  \
+      return set_error(ctx, MAPSQ_E_CUDA,                                                  \
+                       std::string("CUDA IPC: " #call ": ") + cudaGetErrorString(_e));     \
+    }                                                                                      \
+  } while (0)
+
 inline cudaStream_t S(void *stream) { return (cudaStream_t)stream; }
 inline uint64_t stride_rows(uint64_t n) { return (n + 3) & ~3ull; }
 
@@ -162,7 +175,7 @@ mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t
     void *p = nullptr;
     CK(cudaMalloc(&p, nbytes));
     cudaIpcMemHandle_t h;
-    CK(cudaIpcGetMemHandle(&h, p));
+    CKIPC(cudaIpcGetMemHandle(&h, p));
     const uint64_t one = 1;
     std::memcpy(rec, &one, 8);
     std::memcpy(rec + 16, &h, 64);
@@ -188,11 +201,11 @@ mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t
     if (r == d->rank) {
       a.ptr[r] = a.own;
     } else {
-      if (a.ptr[r]) CK(cudaIpcCloseMemHandle(a.ptr[r]));
+      if (a.ptr[r]) CKIPC(cudaIpcCloseMemHandle(a.ptr[r]));
       a.ptr[r] = nullptr;
       cudaIpcMemHandle_t h;
       std::memcpy(&h, q + 16, 64);
-      CK(cudaIpcOpenMemHandle(&a.ptr[r], h, cudaIpcMemLazyEnablePeerAccess));
+      CKIPC(cudaIpcOpenMemHandle(&a.ptr[r], h, cudaIpcMemLazyEnablePeerAccess));
     }
     a.cap[r] = nb;
   }

@@ -85,6 +85,23 @@ def ensure_dist(ctx, group=None):
         ctx.dist_init(group)
 
 
+def _fused_call(ctx, fn):
+    """Run a library distributed call; if CUDA IPC between the rank processes is unavailable (the
+    error is the same on every rank: it happens while opening the peers' arenas), remember it and
+    return None so the caller falls back to the torch all_to_all exchange."""
+    import warnings
+
+    import paper_1702_03484_b200 as mq
+    try:
+        return fn()
+    except mq.MapsqError as e:
+        if "CUDA IPC" not in str(e):
+            raise
+        ctx.ipc_unavailable = str(e)
+        warnings.warn(f"fused NVLink exchange unavailable ({e}); using torch all_to_all")
+        return None
+
+
 def redistribute(ctx, table, key_vars, group=None, partition_fn: Callable = None):
     """Hash-partition `table` on `key_vars` across the group; returns (vars, received columns)."""
     world = dist.get_world_size(group)
@@ -111,9 +128,11 @@ def join_dist(ctx, tp1, tp2, group=None, tp1_partitioned_on=None, partition_fn: 
         raise mq.MapsqError(2, "join inputs share no variable")
     if fused is None:
         fused = partition_fn is None and dist.get_backend(group) == "nccl"
-    if fused:
+    if fused and not getattr(ctx, "ipc_unavailable", None):
         ensure_dist(ctx, group)
-        return ctx.join_dist(tp1, tp2), key
+        rs = _fused_call(ctx, lambda: ctx.join_dist(tp1, tp2))
+        if rs is not None:
+            return rs, key
     wrap = wrap_fn or (lambda vars_, cols: mq.DeviceTable.from_torch(vars_, cols))
 
     def move(t, slot):
@@ -137,9 +156,11 @@ def query_dist(ctx, triples_shard, patterns, proj=None, group=None, fused: bool 
     import paper_1702_03484_b200 as mq
     if fused is None:
         fused = dist.get_backend(group) == "nccl"
-    if fused:
+    if fused and not getattr(ctx, "ipc_unavailable", None):
         ensure_dist(ctx, group)
-        return ctx.query_dist(triples_shard, patterns, proj)
+        rs = _fused_call(ctx, lambda: ctx.query_dist(triples_shard, patterns, proj))
+        if rs is not None:
+            return rs
     tabs = ctx.scan_patterns(triples_shard, patterns)
     acc, part_key = tabs[0], None
     for t in tabs[1:]:
