@@ -170,3 +170,32 @@ def test_exchange_layout_c_abi_definition():
             mq.exchange_layout([[1, 2], [3, 4]], *bad)
     with pytest.raises(mq.MapsqError):
         mq.exchange_layout([[0] * 65] * 65, 0, 1)             # more ranks than partitions
+
+
+def test_fused_call_falls_back_only_on_ipc_errors():
+    """dist._fused_call: a CUDA IPC failure (same on every rank) switches the context to the
+    torch all_to_all exchange; any other library error propagates."""
+    import warnings
+
+    import paper_1702_03484_b200 as mq
+    from paper_1702_03484_b200 import dist as mqd
+
+    class Ctx:
+        pass
+
+    ctx = Ctx()
+    assert mqd._fused_call(ctx, lambda: 42) == 42 and not hasattr(ctx, "ipc_unavailable")
+
+    def ipc_fail():
+        raise mq.MapsqError(4, "CUDA IPC: cudaIpcOpenMemHandle(...): invalid device context")
+
+    with warnings.catch_warnings(record=True):
+        warnings.simplefilter("always")
+        assert mqd._fused_call(ctx, ipc_fail) is None
+    assert "cudaIpcOpenMemHandle" in ctx.ipc_unavailable
+
+    def other_fail():
+        raise mq.MapsqError(3, "device allocation failed")
+
+    with pytest.raises(mq.MapsqError):
+        mqd._fused_call(Ctx(), other_fail)
