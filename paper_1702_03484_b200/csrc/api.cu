@@ -1318,6 +1318,7 @@ MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->arena_ev) cudaEventDestroy(ctx->arena_ev);
   dist_free(ctx);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
 }
 
@@ -1569,11 +1570,32 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
     int &nd = need[it - h->pred.begin()];
     nd = std::max(nd, view ? 1 : 2);
   }
+  // pattern -> predicate range (-1: absent predicate, or the whole table when `all`)
+  std::vector<int> prange(npats, -1);
+  for (int j = 0; j < npats; j++)
+    if (!all && pats[j].var[1] < 0) {
+      auto it = std::lower_bound(h->pred.begin(), h->pred.end(), pats[j].id[1]);
+      if (it != h->pred.end() && *it == pats[j].id[1]) prange[j] = (int)(it - h->pred.begin());
+    }
+  if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->copy_stream;
   mapsq_index D;  // device-side index over the copied ranges (columns owned by the scratch)
   mapsq_table rs;
   uint64_t bytes = 0;
   {
     Scratch sc(ctx, s);
+    // the H2D copies run on the copy stream in the order the query first uses the ranges; the
+    // compute stream waits for a range only where it first reads it (scans: up front; views: at
+    // the join that consumes them), so later ranges stream in while the first joins run
+    struct Copies {
+      cudaStream_t cs;
+      std::vector<cudaEvent_t> ev;
+      ~Copies() {
+        cudaStreamSynchronize(cs);  // no copy may outlive the scratch it writes
+        for (cudaEvent_t e : ev)
+          if (e) cudaEventDestroy(e);
+      }
+    } cp{cs, std::vector<cudaEvent_t>(np + 1, nullptr)};
     uint64_t rows = 0;
     for (size_t r = 0; r < np; r++)
       if (all || need[r]) rows += h->start[r + 1] - h->start[r];
@@ -1585,24 +1607,68 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
     D.p = d + stride;
     D.o = d + 2 * stride;
     D.start.push_back(0);
+    std::vector<uint64_t> at(np, 0);
     for (size_t r = 0; r < np; r++) {
       if (!all && !need[r]) continue;
-      const uint64_t b = h->start[r], c = h->start[r + 1] - b, at = D.start.back();
-      CK(cudaMemcpyAsync(D.s + at, h->s + b, 4 * c, cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(D.o + at, h->o + b, 4 * c, cudaMemcpyHostToDevice, s));
-      bytes += 8 * c;
-      if (all || need[r] == 2) {
-        CK(cudaMemcpyAsync(D.p + at, h->p + b, 4 * c, cudaMemcpyHostToDevice, s));
-        bytes += 4 * c;
-      }
+      at[r] = D.start.back();
       D.pred.push_back(h->pred[r]);
-      D.start.push_back(at + c);
+      D.start.push_back(at[r] + h->start[r + 1] - h->start[r]);
       D.slo.push_back(h->slo[r]);
       D.shi.push_back(h->shi[r]);
       D.olo.push_back(h->olo[r]);
       D.ohi.push_back(h->ohi[r]);
     }
-    TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D, step));
+    // the scratch may still be read by earlier work on s: the copies start after it
+    CK(cudaEventCreateWithFlags(&cp.ev[np], cudaEventDisableTiming));
+    CK(cudaEventRecord(cp.ev[np], s));
+    CK(cudaStreamWaitEvent(cs, cp.ev[np], 0));
+    auto copy_range = [&](size_t r) -> mapsq_status {
+      const uint64_t b = h->start[r], c = h->start[r + 1] - b;
+      CK(cudaMemcpyAsync(D.s + at[r], h->s + b, 4 * c, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemcpyAsync(D.o + at[r], h->o + b, 4 * c, cudaMemcpyHostToDevice, cs));
+      bytes += 8 * c;
+      if (all || need[r] == 2) {
+        CK(cudaMemcpyAsync(D.p + at[r], h->p + b, 4 * c, cudaMemcpyHostToDevice, cs));
+        bytes += 4 * c;
+      }
+      CK(cudaEventCreateWithFlags(&cp.ev[r], cudaEventDisableTiming));
+      CK(cudaEventRecord(cp.ev[r], cs));
+      return MAPSQ_OK;
+    };
+    std::vector<char> copied(np, 0);
+    for (int j = 0; j < npats; j++)  // first-use order
+      if (prange[j] >= 0 && !copied[prange[j]]) {
+        TRY(copy_range(prange[j]));
+        copied[prange[j]] = 1;
+      }
+    for (size_t r = 0; r < np; r++)  // everything else the query reads (variable predicates)
+      if ((all || need[r]) && !copied[r]) TRY(copy_range(r));
+    auto wait_range = [&](int r) -> mapsq_status {
+      if (r >= 0 && cp.ev[r]) CK(cudaStreamWaitEvent(s, cp.ev[r], 0));
+      return MAPSQ_OK;
+    };
+    // scans read their ranges before the first join; so does a variable-predicate pattern
+    for (int j = 0; j < npats; j++) {
+      const mapsq_pattern &P = pats[j];
+      const bool view = P.var[1] < 0 && P.var[0] >= 0 && P.var[2] >= 0 && P.var[0] != P.var[2];
+      if (!view || all)
+        for (size_t r = 0; r < np; r++)
+          if (all ? true : (int)r == prange[j]) TRY(wait_range((int)r));
+    }
+    int jn = 0;
+    const JoinStep inner = step ? *step : JoinStep([ctx](const mapsq_table *a, const mapsq_table *t,
+                                                         mapsq_table *out, cudaStream_t st) {
+      return join_tables(ctx, a, t, out, st);
+    });
+    const JoinStep waited = [&](const mapsq_table *a, const mapsq_table *t, mapsq_table *out,
+                                cudaStream_t st) -> mapsq_status {
+      ++jn;  // join jn consumes pattern jn (and pattern 0 at the first join)
+      if (jn == 1) TRY(wait_range(prange[0]));
+      if (jn < npats) TRY(wait_range(prange[jn]));
+      return inner(a, t, out, st);
+    };
+    TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D, &waited));
+    for (size_t r = 0; r < np; r++) TRY(wait_range((int)r));  // (a one-pattern view result)
     // the result may be a zero-copy view of the copied ranges: read it back inside this scope
     TRY(result_to_host(ctx, &rs, s, host_rows, out_ncols, out_var, host_cols));
   }

@@ -68,6 +68,7 @@ struct mapsq_ctx {
   cudaStream_t arena_stream = nullptr;
   cudaEvent_t arena_ev = nullptr;
   mapsq::DistState *dist = nullptr;  // communicator + exchange arenas (dist.cu), or NULL
+  cudaStream_t copy_stream = nullptr;  // H2D copies of mapsq_query_host_indexed (lazily created)
 };
 
 namespace mapsq {
