@@ -263,7 +263,9 @@ mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
  * variable predicate), runs mapsq_query_indexed's path on them, and reads the result back into the
  * context's pinned result arena exactly as mapsq_query_host does (same output contract, same
  * result rows as mapsq_query_indexed over the device index).  *h2d_bytes (optional) receives the
- * bytes copied host -> device.  Synchronous. */
+ * bytes copied host -> device.  The copies run on a context-owned copy stream in the order the
+ * query first uses the ranges, and `stream` waits for each range only where it first reads it
+ * (later ranges stream in while the first joins run).  Synchronous. */
 typedef struct mapsq_host_index mapsq_host_index;
 mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *idx, mapsq_host_index **out,
                                  void *stream);
