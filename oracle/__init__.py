@@ -76,6 +76,12 @@ def _lib():
         L.oracle_canonical_sort.restype = None
         L.oracle_free.argtypes = [PT]
         L.oracle_free.restype = None
+        PU64 = ctypes.POINTER(ctypes.c_uint64)
+        L.oracle_fingerprint.argtypes = [PT, PU64]
+        L.oracle_fingerprint.restype = None
+        L.oracle_fingerprint_cols.argtypes = [ctypes.c_uint64, ctypes.c_uint32,
+                                              ctypes.POINTER(P32), PU64]
+        L.oracle_fingerprint_cols.restype = None
         for f in (L.oracle_scan, L.oracle_join_nested, L.oracle_join_sortmerge, L.oracle_query):
             f.restype = ctypes.c_int
         _LIB = L
@@ -172,6 +178,37 @@ def canonical(t: Table) -> Table:
     c.rows = _p32(rows)
     _lib().oracle_canonical_sort(ctypes.byref(c))
     return Table(list(t.vars), rows)
+
+
+class Fingerprint:
+    """Accumulating multiset fingerprint (count, sum mod 2^64, xor) of per-row splitmix64 hashes
+    (definition in oracle.h).  Feed it row-major tables or SoA column chunks
+    in any order; equal multisets of rows give equal fingerprints."""
+
+    def __init__(self):
+        self.acc = (ctypes.c_uint64 * 3)(0, 0, 0)
+
+    def add_table(self, t: Table) -> "Fingerprint":
+        keep: list = []
+        c = _to_c(t, keep)
+        _lib().oracle_fingerprint(ctypes.byref(c), self.acc)
+        return self
+
+    def add_cols(self, cols) -> "Fingerprint":
+        cols = [_u32(c) for c in cols]
+        n = len(cols[0]) if cols else 0
+        assert all(len(c) == n for c in cols)
+        arr = (ctypes.POINTER(ctypes.c_uint32) * max(1, len(cols)))(*[_p32(c) for c in cols])
+        _lib().oracle_fingerprint_cols(n, len(cols), arr, self.acc)
+        return self
+
+    @property
+    def value(self) -> tuple:
+        return int(self.acc[0]), int(self.acc[1]), int(self.acc[2])
+
+
+def fingerprint(t: Table) -> tuple:
+    return Fingerprint().add_table(t).value
 
 
 def canonical_rows(rows: np.ndarray) -> np.ndarray:

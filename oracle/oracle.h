@@ -47,6 +47,13 @@ int oracle_query(uint64_t n, const uint32_t *s, const uint32_t *p, const uint32_
 /* Sort rows lexicographically (ascending u32 tuples) in place. */
 void oracle_canonical_sort(oracle_table *t);
 void oracle_free(oracle_table *t);
+/* Multiset fingerprint of a table's rows, ACCUMULATED into acc = {count, sum mod 2^64, xor} of
+ * the per-row hash h = fold(h := splitmix64_step(h ^ v)) over the row's values in column order
+ * (SURVEY §8(c) step 6).  Order-independent; call repeatedly over chunks of one table. */
+void oracle_fingerprint(const oracle_table *t, uint64_t acc[3]);
+/* The same over SoA columns cols[0..ncols), each nrows long (device results copied to host). */
+void oracle_fingerprint_cols(uint64_t nrows, uint32_t ncols, const uint32_t *const *cols,
+                             uint64_t acc[3]);
 
 #ifdef __cplusplus
 }

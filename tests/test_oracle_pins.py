@@ -231,3 +231,105 @@ def test_oracle_matches_generator_bookkeeping(cfg):
         assert acc.nrows == want[i], (cfg, i)
     q = oracle.query(s, p, o, pats)
     assert q.nrows == want[-1]
+
+
+# -------------------------------------- composite keys of 3, 4 and 5 shared variables (R5)
+# sortmerge_fixed<3> and sortmerge_generic (>= 4 key columns) pinned to brute force and to the
+# cardinality law of the equivalent single-key join (the key tuple encoded as one integer).
+def test_exhaustive_tiny_three_shared_vars():
+    # A = (x, y, z), B = (z, b, x, y): key (x, y, z) at different positions on each side
+    tabs_a = list(_tables(3, (0, 1), 2))
+    tabs_b = list(_tables(4, (0, 1), 2))
+    for A in tabs_a:
+        for B in tabs_b:
+            rs = _check_join((0, 1, 2), A, (2, 7, 0, 1), B)
+            assert rs.vars == [0, 1, 2, 7]
+
+
+def test_exhaustive_tiny_four_shared_vars():
+    # A = (w, x, y, z, a) with a fixed per row, B = (z, y, x, w): the generic (>= 4) tier
+    tabs_a = list(_tables(4, (0, 1), 2))
+    tabs_b = list(_tables(4, (0, 1), 2))
+    for i, A in enumerate(tabs_a):
+        A5 = np.concatenate([A, (np.arange(len(A), dtype=np.uint32) % 2)[:, None]], 1)
+        for B in tabs_b[i % 3::3]:
+            rs = _check_join((3, 4, 5, 6, 9), A5, (6, 5, 4, 3), B)
+            assert rs.vars == [3, 4, 5, 6, 9]
+
+
+@pytest.mark.parametrize("nkey", [3, 4, 5])
+def test_random_wide_keys_bruteforce_and_encoded_single_key(nkey):
+    rng = np.random.default_rng(100 + nkey)
+    D = 2
+    for case in range(40):
+        n1, n2 = (int(x) for x in rng.integers(0, 14, 2))
+        # A: key columns in order 0..nkey-1 plus one rest column; B: keys reversed plus one rest
+        A = rng.integers(0, D, (n1, nkey + 1)).astype(np.uint32)
+        B = rng.integers(0, D, (n2, nkey + 1)).astype(np.uint32)
+        a_vars = list(range(nkey)) + [20]
+        b_vars = [21] + list(range(nkey))[::-1]
+        rs = _check_join(a_vars, A, b_vars, B)
+        assert rs.vars == list(range(nkey)) + [20, 21]
+        # cardinality law on the encoded key: code = sum_i key_i * D^i
+        wa = D ** np.arange(nkey)
+        ca = (A[:, :nkey].astype(np.int64) * wa).sum(1)
+        cb = (B[:, 1:][:, ::-1].astype(np.int64) * wa).sum(1)
+        L = np.bincount(ca, minlength=D ** nkey)
+        R = np.bincount(cb, minlength=D ** nkey)
+        assert rs.nrows == int((L * R).sum())
+
+
+@pytest.mark.parametrize("nkey", [3, 4, 5])
+def test_wide_key_equals_single_key_join_on_encoded_key(nkey):
+    # The natural join on nkey shared columns equals the single-key join (pinned above) on the
+    # key tuple encoded as one integer, with the tuple decoded back: a transposed or dropped key
+    # column in either tier would break the equality.
+    rng = np.random.default_rng(7 * nkey)
+    D = 3
+    for case in range(15):
+        n1, n2 = (int(x) for x in rng.integers(0, 300, 2))
+        KA = rng.integers(0, D, (n1, nkey)).astype(np.uint32)
+        KB = rng.integers(0, D, (n2, nkey)).astype(np.uint32)
+        va = rng.integers(0, 1 << 31, n1).astype(np.uint32)
+        vb = rng.integers(0, 1 << 31, n2).astype(np.uint32)
+        perm = rng.permutation(nkey)            # B stores its key columns in a shuffled order
+        A = np.concatenate([KA, va[:, None]], 1)
+        B = np.concatenate([vb[:, None], KB[:, perm]], 1)
+        wide = oracle.join(oracle.Table(list(range(nkey)) + [40], A),
+                           oracle.Table([41] + [int(v) for v in perm], B))
+        w = D ** np.arange(nkey)[::-1]
+        code_a = (KA.astype(np.int64) * w).sum(1).astype(np.uint32)
+        code_b = (KB.astype(np.int64) * w).sum(1).astype(np.uint32)
+        single = oracle.join(oracle.Table([50, 40], np.stack([code_a, va], 1)),
+                             oracle.Table([41, 50], np.stack([vb, code_b], 1)), "nested")
+        code = single.rows[:, 0].astype(np.int64)
+        dec = np.stack([(code // D ** (nkey - 1 - i)) % D for i in range(nkey)], 1)
+        want = np.concatenate([dec.astype(np.uint32), single.rows[:, 1:]], 1)
+        assert wide.vars == list(range(nkey)) + [40, 41]
+        assert np.array_equal(oracle.canonical(wide).rows, oracle.canonical_rows(want))
+
+
+# ----------------------------------------------- whole-output fingerprint
+def test_fingerprint_row_hash_is_splitmix64():
+    # One row (0): h = splitmix64 output from state 0 = 0xE220A8397B1DCDAF (the generator's
+    # published first output for seed 0).
+    t = oracle.Table([0], np.zeros((1, 1), np.uint32))
+    assert oracle.fingerprint(t) == (1, 0xE220A8397B1DCDAF, 0xE220A8397B1DCDAF)
+    assert oracle.fingerprint(oracle.Table([0], np.zeros((0, 1), np.uint32))) == (0, 0, 0)
+
+
+def test_fingerprint_is_a_multiset_function():
+    rng = np.random.default_rng(1)
+    rows = rng.integers(0, 1 << 32, (5000, 4), dtype=np.uint64).astype(np.uint32)
+    base = oracle.fingerprint(oracle.Table([0, 1, 2, 3], rows))
+    # order-independent, chunkable, and the SoA entry point agrees with the row-major one
+    assert oracle.fingerprint(oracle.Table([0, 1, 2, 3], rows[rng.permutation(5000)])) == base
+    f = oracle.Fingerprint()
+    for lo in range(0, 5000, 1234):
+        f.add_cols([rows[lo:lo + 1234, c] for c in range(4)])
+    assert f.value == base
+    # sensitive to a duplicated row, a changed value and swapped columns
+    assert oracle.fingerprint(oracle.Table([0, 1, 2, 3], np.concatenate([rows, rows[:1]]))) != base
+    r2 = rows.copy(); r2[17, 2] ^= 1
+    assert oracle.fingerprint(oracle.Table([0, 1, 2, 3], r2)) != base
+    assert oracle.fingerprint(oracle.Table([0, 1, 2, 3], rows[:, [1, 0, 2, 3]])) != base
