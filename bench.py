@@ -229,7 +229,7 @@ FILTER_PROBE_PEAK = 418e9
 def filter_rate(st, steps, step_ms_total):
     """The semi-join filter kernels are bound by random L1/L2 bitmap accesses, not by HBM: their
     access rate against the measured probe rate (the HBM roofline understates them)."""
-    names = ("filter_sample", "filter", "wfilter")
+    names = ("filter_build", "filter_probe", "filter_set")
     ms = sum(st["kernels"][k]["ms"] for k in names if k in st["kernels"])
     acc = st.get("filter_accesses", 0)
     if not ms or not acc:

@@ -351,12 +351,16 @@ mapsq_status bounds_of(mapsq_ctx *ctx, mapsq_table *t, cudaStream_t s) {
 // ------------------------------------------------------------------------------ sort driver
 // Stable LSD sort of keys (and optional vals) by `passes` 8-bit digits starting at bit_lo, the
 // digit histograms `hist` (passes x 256, exclusive-scanned) already built.  a/b are ping-pong
-// buffers; returns in *which the buffer (0 = a, 1 = b) holding the result.
+// buffers; returns in *which the buffer (0 = a, 1 = b) holding the result.  (n0, gap): the input
+// in ka is two segments — key i >= n0 sits at ka[i + gap] (the semi-join filter's output); the
+// first pass reads both and writes one contiguous array.
 mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *va, uint32_t *vb,
                         uint64_t n, uint32_t bit_lo, uint32_t nbits, uint32_t *hist, Scratch &sc,
-                        cudaStream_t s, int *which) {
+                        cudaStream_t s, int *which, uint64_t n0 = ~0ull, uint64_t gap = 0) {
   *which = 0;
   const uint32_t passes = (nbits + 7) / 8;
+  if (gap && n0 < n && (passes == 0 || va))
+    return set_error(ctx, MAPSQ_E_INVALID, "internal: a two-segment sort input needs a P64 pass");
   if (passes == 0 || n == 0) return MAPSQ_OK;
   const uint64_t ntiles = ceil_div(n, kSortTile);
   uint64_t *status = sc.get<uint64_t>(ntiles * kRadix);
@@ -378,7 +382,7 @@ mapsq_status radix_sort(mapsq_ctx *ctx, uint64_t *ka, uint64_t *kb_, uint32_t *v
       const uint32_t nbits_next = more ? std::min<uint32_t>(8, nbits - 8 * (p + 1)) : 0;
       launch_radix_pass(kin, kout, vin, vout, n, shift, bits, hist + p * kRadix, status,
                         counters + p, more ? hist + (p + 1) * kRadix : nullptr, shift + 8,
-                        nbits_next, s);
+                        nbits_next, s, p == 0 ? n0 : ~0ull, p == 0 ? gap : 0);
       CKL("radix_pass");
     }
     *which ^= 1;
@@ -445,43 +449,49 @@ PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_
 
 // filter rounds with hashed bitmaps: ~8 bits per key of the smaller side (at most 2^29 bits, so
 // one bitmap stays L2-resident) and a fresh seed per round
+// MAPSQ_DEBUG=1 in the environment: per-join diagnostics on stderr (filter rounds)
+bool debug_on() {
+  static const bool on = [] {
+    const char *e = std::getenv("MAPSQ_DEBUG");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
 uint32_t word_round_bits(uint64_t small) {
   const uint32_t b = bits_for(8 * std::max<uint64_t>(small, 1));
   return std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, b));
 }
 uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(round + 1); }
 
-// Semi-join filter in front of the Map (row f2's reducer, reading R18): leaves the
-// surviving words key' << ib | rowid in cur (cur/alt may be swapped) with side A's words first and
-// row order kept, their first radix digit counted into hist, and their number in *nw.
+// Semi-join filter in front of the Map (row f2's reducer, reading R18).  Leaves the
+// surviving words key' << ib | rowid in cur as two segments — side A's at cur[0, *nA), side B's
+// at cur[*offB, *offB + *nB) — each in row order, with their first radix digit counted into hist;
+// alt is free for the sort.  cur/alt may be replaced.  A round: probe the larger side L against
+// the smaller side's bitmap (survivors staged per 512-row slice in the stage buffer), scan its
+// slice counts and gather its survivors into their segment, set bm_L from those words, then the
+// same for the smaller side against bm_L; one blocking read of the two survivor counts.
 mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *a,
                         const mapsq_table *b, Scratch &sc, cudaStream_t s, uint64_t *&cur,
-                        uint64_t *&alt, uint32_t *hist, uint64_t *nw_out) {
+                        uint64_t *&alt, uint32_t *hist, uint64_t *nA_out, uint64_t *offB_out,
+                        uint64_t *nB_out) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
-  uint64_t nw = n;
   PackArgs pa = pack_args(pl, a, b);
-  const uint64_t nsl = n / 512 + 4;  // warp slices of any round (filter_slices <= this)
   const uint64_t bmw = std::max<uint64_t>(1, (1ull << kSemijoinBits) / 32);
+  const uint64_t nsl_max = sj_slices(n1) + sj_slices(n2) + 2;
   uint32_t *bm = sc.get<uint32_t>(2 * bmw);
-  uint32_t *fmask = sc.get<uint32_t>(nsl * 16);
-  uint32_t *fcnt = sc.get<uint32_t>(nsl);
-  uint64_t *foff = sc.get<uint64_t>(nsl);
-  uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl));
-  uint64_t *fsc = sc.get<uint64_t>(4);  // [0] survivors, [2..3] sampled survivors / rows
-  NEED(bm); NEED(fmask); NEED(fcnt); NEED(foff); NEED(ftmp); NEED(fsc);
+  uint32_t *cnt = sc.get<uint32_t>(nsl_max);
+  uint64_t *off = sc.get<uint64_t>(nsl_max);
+  uint64_t *ftmp = sc.get<uint64_t>(scan_tmp_words(nsl_max));
+  uint64_t *fsc = sc.get<uint64_t>(4);  // [0] / [1] survivors of side A / B, [2..3] sample
+  NEED(bm); NEED(cnt); NEED(off); NEED(ftmp); NEED(fsc);
   unsigned long long *sample = reinterpret_cast<unsigned long long *>(fsc + 2);
+  uint64_t *stage = alt;       // survivors staged per slice (free again when the filter ends)
+  uint64_t *spare = nullptr;   // the word rounds' output buffer (allocated on first use)
   const uint32_t dmask = pa.last_mask;
-  uint64_t split = n1;     // words [0, split) are side A's
-  bool exact = false;      // the last round's bitmaps were exact (no false positives)
-  bool skipped = false;    // the sampled probe said the filter would drop < 10%
-  // survivors + side-A survivors after a round: one blocking read
-  auto read_counts = [&](uint64_t nslA) -> mapsq_status {
-    TRY(ensure_pinned(ctx, 2));
-    CK(cudaMemcpyAsync(ctx->pinned, fsc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->pinned + 1, foff + nslA, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return MAPSQ_OK;
-  };
+  uint64_t nA = n1, offB = n1, nB = n2, nw = n;  // the current segments (in cur)
+  bool exact = false;    // the last round's bitmaps were exact (no false positives)
+  bool skipped = false;  // the sampled probe said the filter would drop < 10%
   // after building the smaller side's bitmap, a 1/16 sample of the larger side is probed; if
   // >= 90% of it survives the filter cannot pay (C5 J1 drops 6%) and the join goes unfiltered
   auto sample_says_skip = [&](bool *skip) -> mapsq_status {
@@ -492,119 +502,193 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     *skip = ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9;
     return MAPSQ_OK;
   };
+  auto pending_pos = [&]() -> size_t { return ctx->profiling ? ctx->pending.size() - 1 : ~size_t(0); };
+  auto add_bytes = [&](size_t pos, uint64_t bytes) {
+    if (pos < ctx->pending.size()) ctx->pending[pos].bytes += bytes;
+  };
+  // scan one side's slice counts (slices [sl0, sl0 + nsl)) and gather its staged survivors to
+  // out; fsc[side] receives their number
+  std::vector<size_t> gpos;
+  auto scan_gather = [&](int side, uint64_t sl0, uint64_t nsl, uint64_t *out) -> mapsq_status {
+    {
+      KTimer kt(ctx, s, "filter_scan", 12ull * nsl, 3);
+      launch_exclusive_scan_u32(cnt + sl0, off + sl0, nsl, ftmp, fsc + side, s);
+      CKL("filter_scan");
+    }
+    {
+      KTimer kt(ctx, s, "filter_gather", 12ull * nsl);
+      launch_sj_gather(stage + sl0 * kSjSlice, cnt + sl0, off + sl0, nsl, out,
+                       pl.passes ? hist : nullptr, pl.ib, dmask, s);
+      CKL("filter_gather");
+    }
+    gpos.push_back(pending_pos());
+    return MAPSQ_OK;
+  };
+  // the round's one blocking read: both sides' survivors; the staged / gathered bytes go to the
+  // probe and gather timers
+  auto read_counts = [&](size_t posL, size_t posS, size_t posSet, int sideL) -> mapsq_status {
+    TRY(ensure_pinned(ctx, 2));
+    CK(cudaMemcpyAsync(ctx->pinned, fsc, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t before = nw, sa = ctx->pinned[0], sb = ctx->pinned[1];
+    const uint64_t survL = sideL ? sb : sa, survS = sideL ? sa : sb;
+    add_bytes(posL, 8ull * survL);
+    add_bytes(posS, 8ull * survS);
+    add_bytes(posSet, 8ull * survL);
+    if (gpos.size() == 2) {
+      add_bytes(gpos[0], 16ull * survL);
+      add_bytes(gpos[1], 16ull * survS);
+    }
+    gpos.clear();
+    if (debug_on())
+      std::fprintf(stderr, "[mapsq] filter round: %llu -> %llu words (A %llu, B %llu)\n",
+                   (unsigned long long)before, (unsigned long long)(sa + sb),
+                   (unsigned long long)sa, (unsigned long long)sb);
+    return MAPSQ_OK;
+  };
+  CK(cudaMemsetAsync(fsc, 0, 2 * sizeof(uint64_t), s));
   // round 0 reads the key columns directly — a single packed column (exact or hashed bitmap),
   // or a hashed composite key (blocked Bloom bitmaps, key_hash computed from the columns); other
   // packed composite keys are Mapped first and filtered as words
   const bool colhash = pa.hash;
   const bool colpath = (pa.nkey == 1 && pl.kb <= 32 && !pa.hash) || colhash;
   if (colpath) {
-    // round 0 on the key columns (no word is written for a dropped row)
-    const uint32_t bbits = colhash ? word_round_bits(std::min(n1, n2))
-                                   : std::min<uint32_t>(pl.kb, kSemijoinBits);
+    const bool s_is_b = n2 <= n1;  // S = the smaller side (ties: B)
+    const uint64_t nS = s_is_b ? n2 : n1, nL = s_is_b ? n1 : n2;
+    const uint32_t bbits = colhash ? word_round_bits(nS) : std::min<uint32_t>(pl.kb, kSemijoinBits);
     const uint32_t hashed = colhash || pl.kb > bbits;
-    const uint64_t bw = std::max<uint64_t>(1, (1ull << bbits) / 32);
-    const uint64_t ns = filter_slices(n1, n2), nslA = filter_slices(n1, 0);
+    const uint64_t bw = std::max<uint64_t>(2, (1ull << bbits) / 32);
+    uint32_t *bmS = bm, *bmL = bm + bw;
+    const uint64_t kbytes = 4ull * pa.nkey;
     CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
-    auto col_round = [&](int phase) {
-      if (colhash)
-        launch_cfilter(pa, bm, bm + bw, bbits, word_round_seed(0), fmask, fcnt, phase, sample, s);
-      else
-        launch_filter(pa, bm, bm + bw, bbits, hashed, fmask, fcnt, phase, sample, s);
-    };
     {
-      KTimer kt(ctx, s, "filter_sample", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2) / 16) +
-                                             8ull * bw, 2);
-      col_round(0);
-      CKL("filter_sample");
-      ctx->counters.filter_accesses += std::min(n1, n2) + std::max(n1, n2) / 16;
+      KTimer kt(ctx, s, "filter_build", kbytes * (nS + nL / 16), 2);
+      launch_sj_build_sample_cols(pa, s_is_b, bmS, bbits, hashed, sample, s);
+      CKL("filter_build");
+      ctx->counters.filter_accesses += nS + nL / 16;
     }
     TRY(sample_says_skip(&skipped));
     if (!skipped) {
+      const uint64_t slA = sj_slices(n1), slB = sj_slices(n2);
+      const uint64_t seedL = word_round_seed(0);
+      // plain bitmaps: L's survivors set bm_L while probed (bit = key'); hashed composite keys:
+      // bm_L (a wblock of the survivors' key') is set from L's gathered survivor words
+      const bool set_in_probe = !colhash;
+      const int sideL = s_is_b ? 0 : 1, sideS = 1 - sideL;
+      uint64_t *outL = cur + (sideL ? n1 : 0), *outS = cur + (sideS ? n1 : 0);
+      size_t posL, posS, posSet = ~size_t(0);
+      CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
       {
-        KTimer kt(ctx, s, "filter", 4ull * pa.nkey * (std::min(n1, n2) + std::max(n1, n2)) +
-                                        16ull * bw + n / 8, colhash ? 3 : 2);
-        col_round(1);
-        CKL("filter");
-        ctx->counters.filter_accesses += std::max(n1, n2) + std::min(n1, n2);
+        KTimer kt(ctx, s, "filter_probe", kbytes * nL);
+        launch_sj_probe_cols(pa, sideL == 1, colhash ? 1 : 0, bmS, bbits, hashed, 0,
+                             set_in_probe ? bmL : nullptr, stage, cnt, s);
+        CKL("filter_probe");
+      }
+      posL = pending_pos();
+      TRY(scan_gather(sideL, sideL ? slA : 0, sideL ? slB : slA, outL));
+      if (!set_in_probe) {
+        KTimer kt(ctx, s, "filter_set", 0);
+        launch_sj_set_words(outL, fsc + sideL, nL, 2, bmL, pl.ib, bbits, 0, seedL, s);
+        CKL("filter_set");
+        posSet = pending_pos();
       }
       {
-        KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
-        launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
-        CKL("filter_scan");
+        KTimer kt(ctx, s, "filter_probe", kbytes * nS);
+        launch_sj_probe_cols(pa, sideS == 1, colhash ? 2 : 0, bmL, bbits, hashed, seedL, nullptr,
+                             stage, cnt, s);
+        CKL("filter_probe");
       }
-      {
-        KTimer kt(ctx, s, "filter_emit", n / 8 + 12ull * ns);
-        launch_filter_emit(pa, fmask, fcnt, foff, cur, hist, s);
-        CKL("filter_emit");
-        TRY(read_counts(nslA));
-        kt.t.bytes += 12ull * ctx->pinned[0];
-      }
-      nw = ctx->pinned[0];
-      split = nslA < ns ? ctx->pinned[1] : nw;
+      posS = pending_pos();
+      TRY(scan_gather(sideS, sideS ? slA : 0, sideS ? slB : slA, outS));
+      ctx->counters.filter_accesses += nL + nS;
+      TRY(read_counts(posL, posS, posSet, sideL));
+      nA = ctx->pinned[0];
+      nB = ctx->pinned[1];
+      offB = n1;
+      nw = nA + nB;
       // exact bitmaps leave no false positive; a hashed round that dropped < 10% of the rows
       // says the keys mostly match, so refinement rounds would not pay
       exact = (!hashed && !colhash) || nw * 10 > n * 9;
     }
   } else {
-    // composite / hashed keys: Map every row, then filter the words
-    pa.passes = 0;  // (the histogram is counted by the last round's emit)
+    // composite packed keys: Map every row, then filter the words
+    pa.passes = 0;  // (the histogram is counted by the last round's gathers)
     KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
     launch_pack_hist(pa, cur, nullptr, hist, s);
     CKL("pack_hist");
   }
   // word rounds: the first one for non-column keys (sampled first), then refinements while a
   // hashed round still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per
-  // key of the smaller side, with a fresh hash seed)
+  // key of the smaller side, with a fresh hash seed).  Input segments in cur, output in spare.
   for (int round = colpath ? 1 : 0;
-       !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows); round++) {
-    const uint64_t small = std::min(split, nw - split);
-    const uint32_t bbits = word_round_bits(small);
+       !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows) && nA && nB;
+       round++) {
+    const SjSeg A{cur, nA}, B{cur + offB, nB};
+    const uint64_t slA = sj_slices(nA), slB = sj_slices(nB);
+    const bool s_is_b = nB <= nA;
+    const int sideL = s_is_b ? 0 : 1, sideS = 1 - sideL;
+    const SjSeg S = s_is_b ? B : A, L = s_is_b ? A : B;
+    const uint64_t sl0S = s_is_b ? slA : 0, sl0L = s_is_b ? 0 : slA;
+    const uint32_t bbits = word_round_bits(S.rows);
     const uint64_t bw = (1ull << bbits) / 32;
-    const uint64_t ns = filter_slices(split, nw - split), nslA = filter_slices(split, 0);
+    uint32_t *bmS = bm, *bmL = bm + bw;
     const uint64_t seed = word_round_seed(round);
     CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
+    if (round == 0) CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+    {
+      KTimer kt(ctx, s, "filter_build", 8ull * (S.rows + (round == 0 ? L.rows / 16 : 0)),
+                round == 0 ? 2 : 1);
+      launch_sj_build_words(S, pl.ib, seed, bbits, bmS, s);
+      if (round == 0) launch_sj_sample_words(L, pl.ib, seed, bbits, bmS, sample, s);
+      CKL("filter_build");
+      ctx->counters.filter_accesses += S.rows + (round == 0 ? L.rows / 16 : 0);
+    }
     if (round == 0) {
-      CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
-      {
-        KTimer kt(ctx, s, "filter_sample", 8ull * (small + (nw - small) / 16) + 8ull * bw, 2);
-        launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt, 0, sample, s);
-        CKL("filter_sample");
-        ctx->counters.filter_accesses += small + (nw - small) / 16;
-      }
       TRY(sample_says_skip(&skipped));
       if (skipped) break;
     }
-    {
-      KTimer kt(ctx, s, "wfilter", (round ? 16ull : 8ull) * small + 8ull * (nw - small) +
-                                       16ull * bw + nw / 8, round ? 4 : 3);
-      launch_wfilter(cur, nw, split, pl.ib, seed, bbits, bm, bm + bw, fmask, fcnt,
-                     round ? 2 : 1, sample, s);
-      CKL("wfilter");
-      ctx->counters.filter_accesses += (round ? small : 0) + (nw - small) + small;
+    if (!spare) {
+      spare = sc.get<uint64_t>(nw + 2 * kSjSlice);
+      NEED(spare);
     }
-    {
-      KTimer kt(ctx, s, "filter_scan", 12ull * ns, 3);
-      launch_exclusive_scan_u32(fcnt, foff, ns, ftmp, fsc, s);
-      CKL("filter_scan");
-    }
+    uint64_t *outL = spare + (sideL ? nA : 0), *outS = spare + (sideS ? nA : 0);
     CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
     {
-      KTimer kt(ctx, s, "wfilter_emit", nw / 8 + 12ull * ns);
-      launch_wfilter_emit(cur, nw, split, fmask, fcnt, foff, alt, pl.passes ? hist : nullptr,
-                          pl.ib, dmask, s);
-      CKL("wfilter_emit");
-      TRY(read_counts(nslA));
-      kt.t.bytes += 16ull * ctx->pinned[0];
+      KTimer kt(ctx, s, "filter_probe", 8ull * L.rows);
+      launch_sj_probe_words(L, sl0L, pl.ib, bmS, bbits, seed, stage, cnt, s);
+      CKL("filter_probe");
     }
+    const size_t posL = pending_pos();
+    TRY(scan_gather(sideL, sl0L, sideL ? slB : slA, outL));
+    {
+      KTimer kt(ctx, s, "filter_set", 0);
+      launch_sj_set_words(outL, fsc + sideL, L.rows, 2, bmL, pl.ib, bbits, 0, seed, s);
+      CKL("filter_set");
+    }
+    const size_t posSet = pending_pos();
+    {
+      KTimer kt(ctx, s, "filter_probe", 8ull * S.rows);
+      launch_sj_probe_words(S, sl0S, pl.ib, bmL, bbits, seed, stage, cnt, s);
+      CKL("filter_probe");
+    }
+    const size_t posS = pending_pos();
+    TRY(scan_gather(sideS, sl0S, sideS ? slB : slA, outS));
+    ctx->counters.filter_accesses += L.rows + S.rows;
     const uint64_t before = nw;
-    nw = ctx->pinned[0];
-    split = nslA < ns ? ctx->pinned[1] : nw;
-    std::swap(cur, alt);
+    TRY(read_counts(posL, posS, posSet, sideL));
+    offB = nA;
+    nA = ctx->pinned[0];
+    nB = ctx->pinned[1];
+    nw = nA + nB;
+    std::swap(cur, spare);  // the output segments become the input; the old input is free
     if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
   }
   if (skipped) {  // unfiltered: every row's word, the first digit's histogram
     nw = n;
+    nA = n1;
+    offB = n1;
+    nB = n2;
     CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
     if (colpath) {
       const PackArgs pm = pack_args(pl, a, b);
@@ -617,7 +701,9 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
       CKL("key_hist");
     }
   }
-  *nw_out = nw;
+  *nA_out = nA;
+  *offB_out = offB;
+  *nB_out = nB;
   return MAPSQ_OK;
 }
 
@@ -647,7 +733,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   Scratch sc(ctx, s);
   const bool kv = pl.path == MAPSQ_PATH_KV;
-  uint64_t *wa = sc.get<uint64_t>(n), *wb = sc.get<uint64_t>(n);
+  // (+2 slices: the semi-join filter stages each side's survivors at slice-aligned offsets)
+  uint64_t *wa = sc.get<uint64_t>(n + 2 * kSjSlice), *wb = sc.get<uint64_t>(n + 2 * kSjSlice);
   uint32_t *va = kv ? sc.get<uint32_t>(n) : nullptr, *vb = kv ? sc.get<uint32_t>(n) : nullptr;
   uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
   NEED(wa);
@@ -660,7 +747,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   // ---- Map (row a3) + first-digit histogram; optionally behind the semi-join filter
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
   uint64_t *cur = wa, *alt = wb;  // the words entering the sort are in cur
-  uint64_t nw = n;
+  uint64_t nw = n, seg_n0 = n, seg_gap = 0;
   const bool filt = !kv && pl.kb > 0 &&
                     (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
                      (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
@@ -674,9 +761,13 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     ctx->counters.last_passes = pl.passes;
   }
   if (filt) {
-    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nw));
+    uint64_t nA = 0, offB = 0, nB = 0;
+    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB));
+    nw = nA + nB;
+    seg_n0 = nA;
+    seg_gap = offB - nA;
     ctx->counters.last_filtered = n - nw;
-    if (nw == 0) {
+    if (nA == 0 || nB == 0) {  // a side without survivors: no key on both sides
       fill_empty_join(pl, &a, &b, rs);
       return MAPSQ_OK;
     }
@@ -688,7 +779,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   // ---- Sort (row a4)
   int which = 0;
-  TRY(radix_sort(ctx, cur, alt, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which));
+  TRY(radix_sort(ctx, cur, alt, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which, seg_n0,
+                 seg_gap));
   uint64_t *words = which ? alt : cur;
   uint32_t *vals = kv ? (which ? vb : va) : nullptr;
   sc.release(which ? cur : alt);
@@ -996,7 +1088,8 @@ mapsq_status index_build_impl(mapsq_ctx *ctx, const mapsq_triples *T, mapsq_inde
   if (pbits + ib > 64)
     return set_error(ctx, MAPSQ_E_UNSUPPORTED, "predicate bits + row bits exceed 64");
   // Map + stable sort on the predicate bits only (the row id below keeps the triple order)
-  uint64_t *wa = sc.get<uint64_t>(n), *wb = sc.get<uint64_t>(n);
+  // (+2 slices: the semi-join filter stages each side's survivors at slice-aligned offsets)
+  uint64_t *wa = sc.get<uint64_t>(n + 2 * kSjSlice), *wb = sc.get<uint64_t>(n + 2 * kSjSlice);
   uint32_t *hist = sc.get<uint32_t>(kMaxPasses * kRadix);
   NEED(wa); NEED(wb); NEED(hist);
   CK(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));

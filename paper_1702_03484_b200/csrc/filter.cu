@@ -3,18 +3,21 @@
 //
 // ReduceDuplicate emits nothing for a key that occurs on one side only (Alg. 1 l.6-11,
 // PAPER.md:127-133; the LEFT/RIGHT flag exists "to reduce unnecessary computation"), so
-// such rows can be dropped before the sort without changing RS.  Key-presence bitmaps over the
-// packed key key' (exact when kb <= bbits, else indexed by a multiplicative hash of key' —
-// false positives only let rows through, they never drop a match) are built in three passes:
-//   1. build:  bm_S = keys of the smaller side S;
-//   2. probe L (the larger side) against bm_S; every surviving L row also sets its bit in bm_L
-//      (so bm_L holds exactly the keys of L that occur in S);
-//   3. probe S against bm_L.
-// Each probe records one survivor bit per row and a count per 512-row warp slice (side A's rows
-// fill slices [0, nslA), side B's the slices after), the counts are scanned, and an emit pass
-// writes each slice's survivors at its offset in row order.  The compaction is stable, so the
-// surviving words keep ascending row ids and the sort's (key', label, rowid) order — and
-// therefore RS and its row order — are exactly those of the unfiltered join.
+// such rows can be dropped before the sort without changing RS (reading R18).  One round:
+//   1. build:  bm_S = key-presence bitmap of the smaller side S (exact bit = key' when it fits,
+//      else a hash of key' — false positives only let rows through, they never drop a match);
+//   2. probe L (the larger side) against bm_S: every warp stages its 512-row slice's survivors'
+//      words key' << ib | rowid, compacted in row order, plus the slice's count;
+//   3. bm_L = bits of L's survivors — set during the probe (exact bitmaps) or from the staged
+//      words (8 B per survivor instead of re-reading L's key columns);
+//   4. probe S against bm_L, staging its survivors the same way;
+//   5. scan the slice counts (side A's slices first) and gather the staged survivors into one
+//      contiguous array.
+// Within a side the compaction is stable, so the words keep the (key', label, rowid) order of the
+// unfiltered join after the stable sort — RS and its row order are unchanged.  Hashed rounds are
+// refined by further rounds on the surviving words with fresh seeds (blocked Bloom bitmaps).
+#include <cstring>
+#include <map>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -27,7 +30,6 @@ constexpr int kFWarps = kFThreads / 32;
 constexpr int kFItems = 16;                    // rows per lane per slice
 constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
-constexpr uint32_t kDenseSlice = 160;          // survivors above which the emit walks items
 constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice
 
 // MODE 0: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic); 1: generic
@@ -186,43 +188,6 @@ filter_build_kernel(const PackArgs a, const Side sd, uint32_t *__restrict__ bm, 
   }
 }
 
-// Probe the side's rows against bm_probe: survivor bits -> mask[(slice0 + ws) * 16 ..], counts
-// -> cnt[slice0 + ws]; with SET the survivors also set their bit in bm_set.
-template <int MODE, bool SET>
-__global__ void __launch_bounds__(kFThreads)
-filter_probe_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict__ bm_probe,
-                    uint32_t *__restrict__ bm_set, uint32_t bbits, uint32_t hashed,
-                    uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
-  const uint64_t pol = bm_policy();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
-       ws * kFWarpRows < sd.rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    KeyT<MODE> key[kFItems];
-    load_keys<MODE>(a, sd, base, lane, key);
-    uint32_t word[kFItems], bidx[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      bidx[it] = bit_index(key[it], bbits, hashed);
-      word[it] = j < sd.rows ? ld_bm32(bm_probe + (bidx[it] >> 5), pol) : 0u;
-    }
-    uint32_t my = 0, c = 0, keep = 0;
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const bool k = word[it] >> (bidx[it] & 31) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, k);
-      keep |= (uint32_t)k << it;
-      if (lane == (uint32_t)it) my = bal;
-      c += __popc(bal);
-    }
-    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
-    if (lane == 0) cnt[sd.slice0 + ws] = c;
-    if (SET && c) set_bits<true, false>(bm_set, bidx, keep, lane);
-  }
-}
-
 // Sampled probe: every `stride`-th warp slice of the side is probed against bm; sample[0] +=
 // survivors, sample[1] += rows probed.  Lets the host skip a filter that would drop little.
 template <int MODE>
@@ -260,130 +225,24 @@ filter_sample_kernel(const PackArgs a, const Side sd, const uint32_t *__restrict
   }
 }
 
-// Warp-cooperative survivor addressing: lanes 0..15 hold the slice's 16 survivor-bit words
-// (`my`, bit l of word it = row it * 32 + l survives).  slice_prefix returns each lane's
-// exclusive prefix of the popcounts; survivor_row maps survivor r (< count) to its row in the
-// slice, so a warp emits 32 survivors per step with consecutive (coalesced) stores.
-__device__ __forceinline__ uint32_t slice_prefix(uint32_t my, uint32_t lane) {
-  const uint32_t c = __popc(my);
-  uint32_t x = c;
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= (uint32_t)o) x += y;
-  }
-  return x - c;
-}
-__device__ __forceinline__ uint32_t survivor_row(uint32_t my, uint32_t pre, uint32_t r) {
-  uint32_t it = 0;  // the item holding survivor r: the last q with pre_q <= r
-#pragma unroll
-  for (int q = 1; q < kFItems; q++) it += __shfl_sync(0xffffffffu, pre, q) <= r;
-  uint32_t m = __shfl_sync(0xffffffffu, my, it);
-  uint32_t k = r - __shfl_sync(0xffffffffu, pre, it), pos = 0;
-#pragma unroll
-  for (int sh = 16; sh > 0; sh >>= 1) {  // k-th set bit of m
-    const uint32_t low = __popc(m & ((1u << sh) - 1u));
-    if (k >= low) {
-      k -= low;
-      m >>= sh;
-      pos += sh;
-    }
-  }
-  return it * 32 + pos;
-}
-
-// Emit: the survivors of slice s go to words[off[s] ..] in row order (stable), as
-// key' << ib | row id; digit 0 of the survivors is counted into hist.
-template <int MODE>
-__global__ void __launch_bounds__(kFThreads)
-filter_emit_kernel(const PackArgs a, const Side sa, const Side sb,
-                   const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
-                   const uint64_t *__restrict__ off, uint64_t *__restrict__ words,
-                   uint32_t *__restrict__ hist) {
-  __shared__ uint32_t s_h[kFCopies][kRadix];
-  for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
-  uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  const uint64_t nslices = sb.slice0 + ceil_div(sb.rows, kFWarpRows);
-  const uint32_t nk = mode_nkey<MODE>(a);
-  for (uint64_t s = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); s < nslices;
-       s += nwarps) {
-    if (__ldg(cnt + s) == 0) continue;  // warp-uniform
-    const bool is_b = s >= sb.slice0;
-    const Side &sd = is_b ? sb : sa;
-    const uint64_t base = (s - sd.slice0) * kFWarpRows;
-    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + s * kFItems + lane) : 0u;
-    const uint32_t pre = slice_prefix(my, lane);
-    const uint32_t c = __shfl_sync(0xffffffffu, pre + __popc(my), kFItems - 1);
-    const uint64_t pos = __ldg(off + s);
-    if (c > kDenseSlice) {  // dense slice: walk the 16 items (lanes = rows of the item)
-      uint64_t p = pos;
-#pragma unroll 4
-      for (int it = 0; it < kFItems; it++) {
-        const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
-        if (bal >> lane & 1u) {
-          const uint64_t j = base + (uint64_t)it * 32 + lane;
-          constexpr bool hash = MODE >= 2;
-          uint64_t key = hash ? kKeyHashSeed : 0;
-          for (uint32_t q = 0; q < nk; q++) {
-            const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
-            key = hash ? key_hash_step(key, raw) : (key | (MODE == 0 ? (uint64_t)v : (uint64_t)v << a.shift[q]));
-          }
-          if (hash) key = key_hash_final(key, a.kb);
-          const uint64_t w = (key << a.ib) | (j + sd.id0);
-          __stcs(words + p + __popc(bal & lt), w);
-          if (a.passes) atomicAdd(h + ((uint32_t)(w >> a.bit_lo) & a.last_mask), 1u);
-        }
-        p += __popc(bal);
-      }
-      continue;
-    }
-    for (uint32_t r0 = 0; r0 < c; r0 += 32) {  // sparse slice: 32 survivors per step
-      const uint32_t r = r0 + lane;
-      const uint32_t row = survivor_row(my, pre, r < c ? r : 0);
-      if (r < c) {
-        const uint64_t j = base + row;
-        constexpr bool hash = MODE >= 2;
-        uint64_t key = hash ? kKeyHashSeed : 0;
-        for (uint32_t q = 0; q < nk; q++) {
-          const uint32_t raw = __ldg(sd.col[q] + j), v = raw - a.lo[q];
-          key = hash ? key_hash_step(key, raw) : (key | (MODE == 0 ? (uint64_t)v : (uint64_t)v << a.shift[q]));
-        }
-        if (hash) key = key_hash_final(key, a.kb);
-        const uint64_t w = (key << a.ib) | (j + sd.id0);
-        __stcs(words + pos + r, w);
-        if (a.passes) atomicAdd(h + ((uint32_t)(w >> a.bit_lo) & a.last_mask), 1u);
-      }
-    }
-  }
-  __syncthreads();
-  if (a.passes)
-    for (uint32_t d = threadIdx.x; d < kRadix; d += kFThreads) {
-      uint32_t c = 0;
-#pragma unroll
-      for (int q = 0; q < kFCopies; q++) c += s_h[q][d];
-      if (c) atomicAdd(hist + d, c);
-    }
-}
-
-// ---- refinement rounds on packed words (key' = w >> ib): words [0, split) are side A's,
-// [split, n) side B's (the emit keeps the sides contiguous).  The bitmaps are blocked Bloom
-// filters: a key sets/tests TWO bits of one 64-bit word (one memory access, like a plain bitmap,
-// but ~2/3 of its false positives at C5's load factor), chosen by a mix of key' with a
-// per-round seed, so a second round's false positives are independent of the first's.
-struct WSide {
-  const uint64_t *w;
-  uint64_t rows, slice0;
-};
-
-__device__ __forceinline__ void wblock(uint64_t w, uint32_t ib, uint64_t seed, uint32_t bbits,
-                                       uint32_t &idx, uint64_t &m) {
-  const uint64_t h = ((w >> ib) ^ seed) * 0x9E3779B97F4A7C15ull;
+// ---- blocked Bloom bitmaps (hashed keys): a key sets/tests TWO bits of one 64-bit word (one
+// memory access, like a plain bitmap, but ~2/3 of its false positives at C5's load factor).
+// wblock: chosen by a mix of key' with a per-round seed (rounds on packed words and the larger
+// side's bitmap of the column round), so a later round's false positives are independent of an
+// earlier one's.
+__device__ __forceinline__ void wblock_key(uint64_t key, uint64_t seed, uint32_t bbits,
+                                           uint32_t &idx, uint64_t &m) {
+  const uint64_t h = (key ^ seed) * 0x9E3779B97F4A7C15ull;
   idx = (uint32_t)(h >> (70 - bbits));  // 2^(bbits - 6) 64-bit words
   const uint64_t g = h * 0xD6E8FEB86659FD93ull;
   m = (1ull << (g >> 58)) | (1ull << ((g >> 52) & 63));
+}
+// cblock: the column round's smaller-side bitmap, indexed straight from the 64-bit key_hash
+// chain value of the shared columns (already mixed: no further multiply; being wider than the
+// words' key' it also removes most key' collisions)
+__device__ __forceinline__ void cblock(uint64_t h, uint32_t bbits, uint32_t &idx, uint64_t &m) {
+  idx = (uint32_t)(h >> (70 - bbits));
+  m = (1ull << (h & 63)) | (1ull << ((h >> 6) & 63));
 }
 
 // set (idx, m) for the rows whose keep bit is set (fire-and-forget RED.OR: keys mostly distinct);
@@ -403,8 +262,18 @@ __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_
   }
 }
 
+// Word segment of one side (packed words key' << ib | row id of that side's rows, ascending).
+__device__ __forceinline__ void load_words(const SjSeg &sd, uint64_t base, uint32_t lane,
+                                           uint64_t w[kFItems]) {
+#pragma unroll
+  for (int it = 0; it < kFItems; it++) {
+    const uint64_t j = base + (uint64_t)it * 32 + lane;
+    w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
+  }
+}
+
 __global__ void __launch_bounds__(kFThreads)
-wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+wfilter_build_kernel(const SjSeg sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                      unsigned long long *__restrict__ bm) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
@@ -413,14 +282,10 @@ wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
     const uint64_t base = ws * kFWarpRows;
     uint32_t idx[kFItems], keep = 0;
     uint64_t w[kFItems], m[kFItems];
+    load_words(sd, base, lane, w);
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
-    }
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      wblock(w[it], ib, seed, bbits, idx[it], m[it]);
+      wblock_key(w[it] >> ib, seed, bbits, idx[it], m[it]);
       keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
     }
     set_blocks(bm, idx, m, keep, lane);
@@ -428,72 +293,7 @@ wfilter_build_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
 }
 
 __global__ void __launch_bounds__(kFThreads)
-wfilter_probe_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
-                     const unsigned long long *__restrict__ bm_probe,
-                     uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
-  const uint64_t pol = bm_policy();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
-       ws * kFWarpRows < sd.rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    uint64_t w[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
-    }
-    uint64_t v[kFItems], m[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      uint32_t idx;
-      wblock(w[it], ib, seed, bbits, idx, m[it]);
-      v[it] = j < sd.rows ? ld_bm(bm_probe + idx, pol) : 0ull;
-    }
-    uint32_t my = 0, c = 0;
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const bool k = (v[it] & m[it]) == m[it] && base + (uint64_t)it * 32 + lane < sd.rows;
-      const uint32_t bal = __ballot_sync(0xffffffffu, k);
-      if (lane == (uint32_t)it) my = bal;
-      c += __popc(bal);
-    }
-    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
-    if (lane == 0) cnt[sd.slice0 + ws] = c;
-  }
-}
-
-// Set the survivors' block bits in bm (recorded in mask) — a separate pass after the probe, so
-// only one bitmap is hot in L2 at a time (two 64 MB bitmaps overflow it): C5's (?x, ?z) join
-// 5.7 -> 4.7 ms over its three rounds.
-__global__ void __launch_bounds__(kFThreads)
-wfilter_setmask_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
-                       const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
-                       unsigned long long *__restrict__ bm) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
-       ws * kFWarpRows < sd.rows; ws += nwarps) {
-    if (__ldg(cnt + sd.slice0 + ws) == 0) continue;  // warp-uniform
-    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + (sd.slice0 + ws) * kFItems + lane) : 0u;
-    uint32_t keep = 0;
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
-    const uint64_t base = ws * kFWarpRows;
-    uint32_t idx[kFItems];
-    uint64_t m[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t w = (keep >> it & 1u) ? __ldcs(sd.w + base + (uint64_t)it * 32 + lane) : 0ull;
-      wblock(w, ib, seed, bbits, idx[it], m[it]);
-    }
-    set_blocks(bm, idx, m, keep, lane);
-  }
-}
-
-__global__ void __launch_bounds__(kFThreads)
-wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits,
+wfilter_sample_kernel(const SjSeg sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                       const unsigned long long *__restrict__ bm, uint32_t stride,
                       unsigned long long *__restrict__ sample) {
   const uint64_t pol = bm_policy();
@@ -503,18 +303,13 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
   for (uint64_t ws = ((uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5)) * stride;
        ws * kFWarpRows < sd.rows; ws += nwarps * stride) {
     const uint64_t base = ws * kFWarpRows;
-    uint64_t w[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
-    }
-    uint64_t v[kFItems], m[kFItems];
+    uint64_t w[kFItems], v[kFItems], m[kFItems];
+    load_words(sd, base, lane, w);
 #pragma unroll
     for (int it = 0; it < kFItems; it++) {  // all probes in flight together
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       uint32_t idx;
-      wblock(w[it], ib, seed, bbits, idx, m[it]);
+      wblock_key(w[it] >> ib, seed, bbits, idx, m[it]);
       v[it] = j < sd.rows ? ld_bm(bm + idx, pol) : 0ull;
     }
 #pragma unroll
@@ -532,19 +327,11 @@ wfilter_sample_kernel(const WSide sd, uint32_t ib, uint64_t seed, uint32_t bbits
   }
 }
 
-// ---- hashed composite keys, first round on the key columns (no word is written for a dropped
-// row): the word rounds' blocked Bloom bitmaps and pass structure, with key' = key_hash of the
-// row's shared columns computed from the columns (load_keys<MODE>, MODE 2/3).
-// the column round's block index and bit pair straight from the 64-bit key_hash chain value
-// (already mixed: no further multiply)
-__device__ __forceinline__ void cblock(uint64_t h, uint32_t bbits, uint32_t &idx, uint64_t &m) {
-  idx = (uint32_t)(h >> (70 - bbits));
-  m = (1ull << (h & 63)) | (1ull << ((h >> 6) & 63));
-}
-
+// ---- hashed composite keys (PATH_HASH), first round on the key columns: the smaller side's
+// blocked Bloom bitmap from the key_hash chain of its shared columns (load_keys<MODE, false>)
 template <int MODE>
 __global__ void __launch_bounds__(kFThreads)
-cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+cfilter_build_kernel(const PackArgs a, const Side sd, uint32_t bbits,
                      unsigned long long *__restrict__ bm) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
@@ -566,66 +353,7 @@ cfilter_build_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bb
 
 template <int MODE>
 __global__ void __launch_bounds__(kFThreads)
-cfilter_probe_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
-                     const unsigned long long *__restrict__ bm_probe,
-                     uint32_t *__restrict__ mask, uint32_t *__restrict__ cnt) {
-  const uint64_t pol = bm_policy();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
-       ws * kFWarpRows < sd.rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    KeyT<MODE> key[kFItems];
-    load_keys<MODE, false>(a, sd, base, lane, key);
-    uint64_t v[kFItems], m[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const uint64_t j = base + (uint64_t)it * 32 + lane;
-      uint32_t idx;
-      cblock(key[it], bbits, idx, m[it]);
-      v[it] = j < sd.rows ? ld_bm(bm_probe + idx, pol) : 0ull;
-    }
-    uint32_t my = 0, c = 0;
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      const bool k = (v[it] & m[it]) == m[it] && base + (uint64_t)it * 32 + lane < sd.rows;
-      const uint32_t bal = __ballot_sync(0xffffffffu, k);
-      if (lane == (uint32_t)it) my = bal;
-      c += __popc(bal);
-    }
-    if (lane < (uint32_t)kFItems) mask[(sd.slice0 + ws) * kFItems + lane] = my;
-    if (lane == 0) cnt[sd.slice0 + ws] = c;
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kFThreads)
-cfilter_setmask_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
-                       const uint32_t *__restrict__ mask, const uint32_t *__restrict__ cnt,
-                       unsigned long long *__restrict__ bm) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
-       ws * kFWarpRows < sd.rows; ws += nwarps) {
-    if (__ldg(cnt + sd.slice0 + ws) == 0) continue;  // warp-uniform
-    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + (sd.slice0 + ws) * kFItems + lane) : 0u;
-    uint32_t keep = 0;
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) keep |= (__shfl_sync(0xffffffffu, my, it) >> lane & 1u) << it;
-    const uint64_t base = ws * kFWarpRows;
-    KeyT<MODE> key[kFItems];
-    load_keys<MODE, false>(a, sd, base, lane, key, keep);
-    uint32_t idx[kFItems];
-    uint64_t m[kFItems];
-#pragma unroll
-    for (int it = 0; it < kFItems; it++) cblock(key[it], bbits, idx[it], m[it]);
-    set_blocks(bm, idx, m, keep, lane);
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kFThreads)
-cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t bbits,
+cfilter_sample_kernel(const PackArgs a, const Side sd, uint32_t bbits,
                       const unsigned long long *__restrict__ bm, uint32_t stride,
                       unsigned long long *__restrict__ sample) {
   const uint64_t pol = bm_policy();
@@ -660,64 +388,194 @@ cfilter_sample_kernel(const PackArgs a, const Side sd, uint64_t seed, uint32_t b
   }
 }
 
-template <int MODE>
-void cfilter_passes(const PackArgs &a, const Side &S, const Side &L, unsigned long long *bmS,
-                    unsigned long long *bmL, uint32_t bbits, uint64_t seed, uint32_t *mask,
-                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s);
+// ---- probe + slice-local compaction: ONE pass over a side's keys ------------------------------
+// Each warp owns 512-row slices (grid-stride, no CTA barrier, every load of a column in flight
+// together): it probes the bitmap and writes its slice's survivors' words key' << ib | row id,
+// compacted in row order, to stage[slice * 512 ..] plus the slice's survivor count.  No key column
+// is read twice and no survivor mask is stored; a scan of the slice counts and sj_gather then move
+// only the survivors (8 B each) to their final, contiguous positions.  With SET the survivors
+// also set their bit in a second (plain) bitmap.
+//   KM (key mode): 0 one packed column (plain bitmap), 2 / 3 PATH_HASH over 2 / nkey columns,
+//                  4 packed words of a previous round;
+//   BM (probed bitmap): 0 plain bit (bit_index of key'), 1 cblock of the key_hash chain,
+//                  2 wblock of key' with `seed`.
+__device__ __forceinline__ uint64_t opaque(uint64_t x) {
+  asm volatile("mov.b64 %0, %0;" : "+l"(x));
+  return x;
+}
 
-__global__ void __launch_bounds__(kFThreads)
-wfilter_emit_kernel(const WSide sa, const WSide sb, const uint32_t *__restrict__ mask,
-                    const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ off,
-                    uint64_t *__restrict__ out, uint32_t *__restrict__ hist, uint32_t bit_lo,
-                    uint32_t dmask) {
-  __shared__ uint32_t s_h[kFCopies][kRadix];
-  for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
-  __syncthreads();
+// bitmap slot of key' (or the chain, BM 1): idx and the bit mask tested / set there
+template <int BM>
+__device__ __forceinline__ void probe_slot(uint64_t key, uint32_t bbits, uint32_t hashed,
+                                           uint64_t seed, uint32_t &idx, uint64_t &m) {
+  if (BM == 0) {
+    const uint32_t b = bit_index(key, bbits, hashed);
+    idx = b >> 5;
+    m = 1ull << (b & 31);
+  } else if (BM == 1) {
+    cblock(key, bbits, idx, m);
+  } else {
+    wblock_key(key, seed, bbits, idx, m);
+  }
+}
+
+template <int KM, int BM, bool SET>
+__global__ void __launch_bounds__(kFThreads, KM == 0 ? 4 : 2)
+sj_probe_stage_kernel(const PackArgs a, const Side sd, const SjSeg ws, const void *__restrict__ bm,
+                      uint32_t bbits, uint32_t hashed, uint64_t seed,
+                      uint32_t *__restrict__ bm_set, uint64_t *__restrict__ stage,
+                      uint32_t *__restrict__ cnt) {
+  // registers: the keys and the probed bitmap words only (slots and masks are recomputed from
+  // the key, a few ALU ops) — 32-bit for a single packed column against a plain bitmap
+  using KT = typename std::conditional<KM == 0, uint32_t, uint64_t>::type;
+  using VT = typename std::conditional<BM == 0, uint32_t, uint64_t>::type;
   const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  const uint64_t rows = KM == 4 ? ws.rows : sd.rows;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  const uint64_t pol = bm_policy();
+  constexpr int CM = KM == 4 ? 1 : KM;  // column mode for load_keys (unused for words)
+  for (uint64_t wsl = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); wsl * kFWarpRows < rows;
+       wsl += nwarps) {
+    const uint64_t base = wsl * kFWarpRows;
+    // key' (the words themselves for KM 4; the key_hash chain for BM 1) of every item
+    KT key[kFItems];
+    if (KM == 4) {
+      uint64_t w[kFItems];
+      load_words(ws, base, lane, w);
+#pragma unroll
+      for (int it = 0; it < kFItems; it++) key[it] = (KT)w[it];
+    } else {
+      KeyT<CM> k[kFItems];
+      load_keys<CM, BM != 1>(a, sd, base, lane, k);
+#pragma unroll
+      for (int it = 0; it < kFItems; it++) key[it] = (KT)k[it];
+    }
+    const uint32_t lim = (uint32_t)std::min<uint64_t>(rows - base, kFWarpRows);
+    VT v[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {  // all probes in flight together
+      const bool in = (uint32_t)it * 32 + lane < lim;
+      uint32_t idx;
+      uint64_t m;
+      probe_slot<BM>(KM == 4 ? (uint64_t)key[it] >> a.ib : (uint64_t)key[it], bbits, hashed, seed,
+                     idx, m);
+      if (BM == 0)
+        v[it] = in ? (VT)ld_bm32(reinterpret_cast<const uint32_t *>(bm) + idx, pol) : (VT)0;
+      else
+        v[it] = in ? (VT)ld_bm(reinterpret_cast<const unsigned long long *>(bm) + idx, pol) : (VT)0;
+    }
+    uint32_t keep = 0, r = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      uint32_t idx;
+      uint64_t m;
+      // (an opaque copy: the slot is recomputed here instead of being kept live across the probes)
+      const uint64_t kq = opaque((uint64_t)key[it]);
+      probe_slot<BM>(KM == 4 ? kq >> a.ib : kq, bbits, hashed, seed, idx, m);
+      const bool k = ((uint64_t)v[it] & m) == m && (uint32_t)it * 32 + lane < lim;
+      keep |= (uint32_t)k << it;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      if (k) {
+        uint64_t w;
+        if (KM == 4) {
+          w = key[it];
+        } else {
+          const uint64_t kp = (BM == 1) ? key_hash_final(key[it], a.kb) : (uint64_t)key[it];
+          w = (kp << a.ib) | (base + (uint64_t)it * 32 + lane + sd.id0);
+        }
+        __stcg(stage + base + r + __popc(bal & lt), w);
+      }
+      r += __popc(bal);
+    }
+    if (lane == 0) cnt[sd.slice0 + wsl] = r;
+    if (SET) {
+      uint32_t bidx[kFItems];
+#pragma unroll
+      for (int it = 0; it < kFItems; it++) bidx[it] = bit_index((uint64_t)key[it], bbits, hashed);
+      set_bits<true, false>(bm_set, bidx, keep, lane);
+    }
+  }
+}
+
+// Gather: slice s's staged survivors (cnt[s] words at stage[s * 512 ..]) go to out[off[s] ..]
+// (the exclusive scan of the counts over side A's slices then side B's: the output is
+// contiguous, side A first, row order kept); digit 0 of the words is counted into hist.
+__global__ void __launch_bounds__(kFThreads)
+sj_gather_kernel(const uint64_t *__restrict__ stage, const uint32_t *__restrict__ cnt,
+                 const uint64_t *__restrict__ off, uint64_t nslices, uint64_t *__restrict__ out,
+                 uint32_t *__restrict__ hist, uint32_t bit_lo, uint32_t dmask) {
+  __shared__ uint32_t s_h[kFCopies][kRadix];
+  if (hist)
+    for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
   uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  const uint64_t nslices = sb.slice0 + ceil_div(sb.rows, kFWarpRows);
-  for (uint64_t s = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); s < nslices;
-       s += nwarps) {
-    if (__ldg(cnt + s) == 0) continue;  // warp-uniform
-    const WSide &sd = s >= sb.slice0 ? sb : sa;
-    const uint64_t base = (s - sd.slice0) * kFWarpRows;
-    const uint32_t my = lane < (uint32_t)kFItems ? __ldg(mask + s * kFItems + lane) : 0u;
-    const uint32_t pre = slice_prefix(my, lane);
-    const uint32_t c = __shfl_sync(0xffffffffu, pre + __popc(my), kFItems - 1);
-    const uint64_t pos = __ldg(off + s);
-    if (c > kDenseSlice) {  // dense slice: walk the 16 items (lanes = rows of the item)
-      uint64_t p = pos;
-#pragma unroll 4
-      for (int it = 0; it < kFItems; it++) {
-        const uint32_t bal = __shfl_sync(0xffffffffu, my, it);
-        if (bal >> lane & 1u) {
-          const uint64_t w = __ldg(sd.w + base + (uint64_t)it * 32 + lane);
-          __stcs(out + p + __popc(bal & lt), w);
-          if (hist) atomicAdd(h + ((uint32_t)(w >> bit_lo) & dmask), 1u);
-        }
-        p += __popc(bal);
+  for (uint64_t sl = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); sl < nslices;
+       sl += nwarps) {
+    const uint32_t c = __ldg(cnt + sl);
+    if (c == 0) continue;  // warp-uniform
+    const uint64_t pos = __ldg(off + sl);
+    const uint64_t *src = stage + sl * kFWarpRows;
+    for (uint32_t r0 = 0; r0 < c; r0 += 4 * 32) {  // 4 rows per lane in flight
+      uint64_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t r = r0 + q * 32 + lane;
+        w[q] = r < c ? __ldcs(src + r) : 0ull;
       }
-      continue;
-    }
-    for (uint32_t r0 = 0; r0 < c; r0 += 32) {  // sparse slice: 32 survivors per step
-      const uint32_t r = r0 + lane;
-      const uint32_t row = survivor_row(my, pre, r < c ? r : 0);
-      if (r < c) {
-        const uint64_t w = __ldg(sd.w + base + row);
-        __stcs(out + pos + r, w);
-        if (hist) atomicAdd(h + ((uint32_t)(w >> bit_lo) & dmask), 1u);
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t r = r0 + q * 32 + lane;
+        if (r < c) {
+          __stcs(out + pos + r, w[q]);
+          if (hist) atomicAdd(h + ((uint32_t)(w[q] >> bit_lo) & dmask), 1u);
+        }
       }
     }
   }
-  __syncthreads();
-  if (hist)
+  if (hist) {
+    __syncthreads();
     for (uint32_t d = threadIdx.x; d < kRadix; d += kFThreads) {
       uint32_t c = 0;
 #pragma unroll
       for (int q = 0; q < kFCopies; q++) c += s_h[q][d];
       if (c) atomicAdd(hist + d, c);
     }
+  }
+}
+
+// Set the bits of the words w[0 .. *count) (a side's survivors, gathered) in bm: KIND 0 = plain
+// bit of key' (test before set), 2 = wblock of key' with `seed`.  Reads 8 B per survivor
+// instead of the side's key columns.
+template <int KIND>
+__global__ void __launch_bounds__(kFThreads)
+sj_set_words_kernel(const uint64_t *__restrict__ w, const uint64_t *__restrict__ count,
+                    uint32_t ib, uint32_t bbits, uint32_t hashed, uint64_t seed, void *bm) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t rows = *count;
+  const SjSeg sd{w, rows};
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    uint64_t wv[kFItems];
+    load_words(sd, base, lane, wv);
+    uint32_t idx[kFItems], keep = 0;
+    uint64_t m[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < rows) << it;
+      if (KIND == 0)
+        idx[it] = bit_index(wv[it] >> ib, bbits, hashed);
+      else
+        wblock_key(wv[it] >> ib, seed, bbits, idx[it], m[it]);
+    }
+    if (KIND == 0)
+      set_bits(reinterpret_cast<uint32_t *>(bm), idx, keep, lane);
+    else
+      set_blocks(reinterpret_cast<unsigned long long *>(bm), idx, m, keep, lane);
+  }
 }
 
 Side side_of(const PackArgs &a, bool b) {
@@ -745,116 +603,113 @@ int filter_mode(const PackArgs &a) {
   return (a.nkey == 1 && a.kb <= 32) ? 0 : 1;
 }
 
-template <int MODE>
-void filter_passes(const PackArgs &a, const Side &S, const Side &L, uint32_t *bmS, uint32_t *bmL,
-                   uint32_t bbits, uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
-                   unsigned long long *sample, cudaStream_t s) {
-  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  if (phase == 0) {  // build S, sample L
-    filter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, bmS, bbits, hashed);
-    filter_sample_kernel<MODE><<<sample_grid(L.rows), kFThreads, 0, s>>>(
-        a, L, bmS, bbits, hashed, kSampleStride, sample);
-    return;
-  }
-  filter_probe_kernel<MODE, true><<<gl, kFThreads, 0, s>>>(a, L, bmS, bmL, bbits, hashed, mask,
-                                                           cnt);
-  filter_probe_kernel<MODE, false><<<gs, kFThreads, 0, s>>>(a, S, bmL, nullptr, bbits, hashed,
-                                                            mask, cnt);
-}
-
-template <int MODE>
-void cfilter_passes(const PackArgs &a, const Side &S, const Side &L, unsigned long long *bmS,
-                    unsigned long long *bmL, uint32_t bbits, uint64_t seed, uint32_t *mask,
-                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s) {
-  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  if (phase == 0) {  // build S, sample L
-    cfilter_build_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, seed, bbits, bmS);
-    cfilter_sample_kernel<MODE><<<sample_grid(L.rows), kFThreads, 0, s>>>(
-        a, L, seed, bbits, bmS, kSampleStride, sample);
-    return;
-  }
-  cfilter_probe_kernel<MODE><<<gl, kFThreads, 0, s>>>(a, L, seed, bbits, bmS, mask, cnt);
-  cfilter_setmask_kernel<MODE><<<gl, kFThreads, 0, s>>>(a, L, seed, bbits, mask, cnt, bmL);
-  cfilter_probe_kernel<MODE><<<gs, kFThreads, 0, s>>>(a, S, seed, bbits, bmL, mask, cnt);
+template <int KM, int BM, bool SET>
+void probe_launch(const PackArgs &a, const Side &sd, const SjSeg &ws, const void *bm,
+                  uint32_t bbits, uint32_t hashed, uint64_t seed, uint32_t *bm_set,
+                  uint64_t *stage, uint32_t *cnt, cudaStream_t s) {
+  const uint64_t rows = KM == 4 ? ws.rows : sd.rows;
+  if (rows == 0) return;
+  sj_probe_stage_kernel<KM, BM, SET><<<grid_for_rows(rows), kFThreads, 0, s>>>(
+      a, sd, ws, bm, bbits, hashed, seed, bm_set, stage, cnt);
 }
 
 }  // namespace
 
-uint64_t filter_slices(uint64_t n1, uint64_t n2) {
-  return ceil_div(n1, kFWarpRows) + ceil_div(n2, kFWarpRows);
-}
-uint64_t filter_mask_words(uint64_t n1, uint64_t n2) { return filter_slices(n1, n2) * kFItems; }
+uint64_t sj_slices(uint64_t rows) { return ceil_div(rows, kFWarpRows); }
 
-void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
-                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
-                   unsigned long long *sample, cudaStream_t s) {
-  const bool b_small = a.n2 < a.n1;
-  const Side S = side_of(a, b_small), L = side_of(a, !b_small);
-  switch (filter_mode(a)) {
-    case 0: filter_passes<0>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
-    case 1: filter_passes<1>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
-    case 2: filter_passes<2>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
-    default: filter_passes<3>(a, S, L, bmS, bmL, bbits, hashed, mask, cnt, phase, sample, s); break;
+void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
+                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s) {
+  const Side S = side_of(a, s_is_b), L = side_of(a, !s_is_b);
+  const int gs = grid_for_rows(S.rows);
+  const int mode = filter_mode(a);
+  if (mode == 0) {
+    filter_build_kernel<0><<<gs, kFThreads, 0, s>>>(a, S, (uint32_t *)bmS, bbits, hashed);
+    if (L.rows)
+      filter_sample_kernel<0><<<sample_grid(L.rows), kFThreads, 0, s>>>(
+          a, L, (const uint32_t *)bmS, bbits, hashed, kSampleStride, sample);
+  } else if (mode == 2) {
+    cfilter_build_kernel<2><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
+    if (L.rows)
+      cfilter_sample_kernel<2><<<sample_grid(L.rows), kFThreads, 0, s>>>(
+          a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
+  } else {
+    cfilter_build_kernel<3><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
+    if (L.rows)
+      cfilter_sample_kernel<3><<<sample_grid(L.rows), kFThreads, 0, s>>>(
+          a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
   }
 }
 
-void launch_cfilter(const PackArgs &a, uint32_t *bmS32, uint32_t *bmL32, uint32_t bbits,
-                    uint64_t seed, uint32_t *mask, uint32_t *cnt, int phase,
-                    unsigned long long *sample, cudaStream_t s) {
-  unsigned long long *bmS = reinterpret_cast<unsigned long long *>(bmS32);
-  unsigned long long *bmL = reinterpret_cast<unsigned long long *>(bmL32);
-  const bool b_small = a.n2 < a.n1;
-  const Side S = side_of(a, b_small), L = side_of(a, !b_small);
-  if (a.nkey == 2)
-    cfilter_passes<2>(a, S, L, bmS, bmL, bbits, seed, mask, cnt, phase, sample, s);
+void launch_sj_probe_cols(const PackArgs &a, bool side_b, int bm_kind, const void *bm,
+                          uint32_t bbits, uint32_t hashed, uint64_t seed, uint32_t *bm_set,
+                          uint64_t *stage, uint32_t *cnt, cudaStream_t s) {
+  const Side sd = side_of(a, side_b);
+  const SjSeg none{nullptr, 0};
+  // the side's slices: stage[slice * 512 ..] and cnt[slice], side B after side A's slices
+  stage += sd.slice0 * kFWarpRows;
+  const int mode = filter_mode(a);
+  if (mode == 0) {
+    if (bm_set)
+      probe_launch<0, 0, true>(a, sd, none, bm, bbits, hashed, seed, bm_set, stage, cnt, s);
+    else
+      probe_launch<0, 0, false>(a, sd, none, bm, bbits, hashed, seed, nullptr, stage, cnt, s);
+  } else if (mode == 2) {
+    if (bm_kind == 1)
+      probe_launch<2, 1, false>(a, sd, none, bm, bbits, hashed, seed, nullptr, stage, cnt, s);
+    else
+      probe_launch<2, 2, false>(a, sd, none, bm, bbits, hashed, seed, nullptr, stage, cnt, s);
+  } else {
+    if (bm_kind == 1)
+      probe_launch<3, 1, false>(a, sd, none, bm, bbits, hashed, seed, nullptr, stage, cnt, s);
+    else
+      probe_launch<3, 2, false>(a, sd, none, bm, bbits, hashed, seed, nullptr, stage, cnt, s);
+  }
+}
+
+void launch_sj_probe_words(const SjSeg &in, uint64_t slice0, uint32_t ib, const void *bm,
+                           uint32_t bbits, uint64_t seed, uint64_t *stage, uint32_t *cnt,
+                           cudaStream_t s) {
+  PackArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.ib = ib;
+  Side sd;
+  std::memset(&sd, 0, sizeof sd);
+  sd.slice0 = slice0;
+  probe_launch<4, 2, false>(a, sd, in, bm, bbits, 0, seed, nullptr, stage + slice0 * kFWarpRows,
+                            cnt, s);
+}
+
+void launch_sj_set_words(const uint64_t *w, const uint64_t *count, uint64_t max_rows, int kind,
+                         void *bm, uint32_t ib, uint32_t bbits, uint32_t hashed, uint64_t seed,
+                         cudaStream_t s) {
+  if (max_rows == 0) return;
+  const int g = grid_for_rows(max_rows);
+  if (kind == 0)
+    sj_set_words_kernel<0><<<g, kFThreads, 0, s>>>(w, count, ib, bbits, hashed, seed, bm);
   else
-    cfilter_passes<3>(a, S, L, bmS, bmL, bbits, seed, mask, cnt, phase, sample, s);
+    sj_set_words_kernel<2><<<g, kFThreads, 0, s>>>(w, count, ib, bbits, hashed, seed, bm);
 }
 
-void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
-                    uint64_t seed, uint32_t bbits, uint32_t *bmS32, uint32_t *bmL32,
-                    uint32_t *mask, uint32_t *cnt, int phase, unsigned long long *sample,
-                    cudaStream_t s) {
-  unsigned long long *bmS = reinterpret_cast<unsigned long long *>(bmS32);
-  unsigned long long *bmL = reinterpret_cast<unsigned long long *>(bmL32);
-  const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
-  const bool b_small = B.rows < A.rows;
-  const WSide S = b_small ? B : A, L = b_small ? A : B;
-  const int gs = grid_for_rows(S.rows), gl = grid_for_rows(L.rows);
-  if (phase != 1) {  // build S (and, phase 0, sample L)
-    if (S.rows) wfilter_build_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmS);
-    if (phase == 0) {
-      if (L.rows)
-        wfilter_sample_kernel<<<sample_grid(L.rows), kFThreads, 0, s>>>(
-            L, ib, seed, bbits, bmS, kSampleStride, sample);
-      return;
-    }
-  }
-  if (L.rows) {
-    wfilter_probe_kernel<<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, bmS, mask, cnt);
-    wfilter_setmask_kernel<<<gl, kFThreads, 0, s>>>(L, ib, seed, bbits, mask, cnt, bmL);
-  }
-  if (S.rows) wfilter_probe_kernel<<<gs, kFThreads, 0, s>>>(S, ib, seed, bbits, bmL, mask, cnt);
+void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t *off,
+                      uint64_t nslices, uint64_t *out, uint32_t *hist, uint32_t bit_lo,
+                      uint32_t dmask, cudaStream_t s) {
+  if (nslices == 0) return;
+  sj_gather_kernel<<<grid_for_rows(nslices * kFWarpRows), kFThreads, 0, s>>>(
+      stage, cnt, off, nslices, out, hist, bit_lo, dmask);
 }
 
-void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
-                         const uint32_t *cnt, const uint64_t *off, uint64_t *out, uint32_t *hist,
-                         uint32_t bit_lo, uint32_t dmask, cudaStream_t s) {
-  const WSide A{words, split, 0}, B{words + split, n - split, ceil_div(split, kFWarpRows)};
-  wfilter_emit_kernel<<<grid_for_rows(n), kFThreads, 0, s>>>(A, B, mask, cnt, off, out, hist,
-                                                            bit_lo, dmask);
+void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t bbits, void *bm,
+                           cudaStream_t s) {
+  if (S.rows == 0) return;
+  wfilter_build_kernel<<<grid_for_rows(S.rows), kFThreads, 0, s>>>(
+      S, ib, seed, bbits, reinterpret_cast<unsigned long long *>(bm));
 }
 
-void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
-                        const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s) {
-  const Side A = side_of(a, false), B = side_of(a, true);
-  const int g = grid_for_rows(a.n1 + a.n2);
-  switch (filter_mode(a)) {
-    case 0: filter_emit_kernel<0><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
-    case 1: filter_emit_kernel<1><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
-    case 2: filter_emit_kernel<2><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
-    default: filter_emit_kernel<3><<<g, kFThreads, 0, s>>>(a, A, B, mask, cnt, off, words, hist); break;
-  }
+void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t bbits,
+                            const void *bm, unsigned long long *sample, cudaStream_t s) {
+  if (L.rows == 0) return;
+  wfilter_sample_kernel<<<sample_grid(L.rows), kFThreads, 0, s>>>(
+      L, ib, seed, bbits, reinterpret_cast<const unsigned long long *>(bm), kSampleStride, sample);
 }
 
 }  // namespace mapsq

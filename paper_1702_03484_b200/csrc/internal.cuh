@@ -320,7 +320,10 @@ void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
-                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s);
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s,
+                       uint64_t n0 = ~0ull, uint64_t gap = 0);
+// (n0, gap): two-segment input — key i >= n0 is read at kin[i + gap] (P64 words only: the
+// semi-join filter leaves side A's and side B's survivors as two segments)
 
 // ReduceDuplicate (K4): groups present on both sides, in key order.
 struct GroupOut {
@@ -380,36 +383,48 @@ uint64_t find_groups_tiles(uint64_t n);
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,
                    cudaStream_t s);
 
-// Semi-join filter (filter.cu): per-side key-presence bitmaps of 2^bbits bits (bit = key' when
-// hashed == 0, else a multiplicative hash of key'), then the Map of the rows whose key is present
-// on the other side, compacted stably (probe -> scan of per-slice counts -> emit).
+// Semi-join filter (filter.cu, reading R18): key-presence bitmaps of 2^bbits bits; per side a
+// probe that stages its survivors' words (key' << ib | rowid) compacted per 512-row slice, then a
+// scan of the slice counts and a gather of the survivors into one contiguous array (A then B).
 constexpr uint64_t kSemijoinMinRows = 1ull << 22;  // AUTO: joins of at least this many rows
 constexpr uint32_t kSemijoinBits = 29;             // 2 x 64 MB bitmaps at most (L2-sized)
-uint64_t filter_slices(uint64_t n1, uint64_t n2);      // 512-row warp slices (per side)
-uint64_t filter_mask_words(uint64_t n1, uint64_t n2);  // survivor-bit words
-// Column round in two phases: phase 0 builds bmS from the smaller side S and probes a 1/16
-// sample of the larger side L (sample[0] += survivors, sample[1] += rows); phase 1 probes L
-// (setting bmL for its survivors) and then S against bmL: survivor bits + per-slice counts.
-void launch_filter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
-                   uint32_t hashed, uint32_t *mask, uint32_t *cnt, int phase,
-                   unsigned long long *sample, cudaStream_t s);
-void launch_filter_emit(const PackArgs &a, const uint32_t *mask, const uint32_t *cnt,
-                        const uint64_t *off, uint64_t *words, uint32_t *hist, cudaStream_t s);
-// Refinement round on packed words ([0, split) side A, [split, n) side B; key' = w >> ib, bit =
-// mix(key' ^ seed)): the same three passes, then the emit copies the survivors to `out`
-// (sides stay contiguous) and counts their digit 0 into hist (if not NULL).
-// Hashed composite keys (PATH_HASH): the first round on the key columns with the word rounds'
-// blocked Bloom bitmaps (bbits, seed); phases as launch_filter; launch_filter_emit writes words.
-void launch_cfilter(const PackArgs &a, uint32_t *bmS, uint32_t *bmL, uint32_t bbits,
-                    uint64_t seed, uint32_t *mask, uint32_t *cnt, int phase,
-                    unsigned long long *sample, cudaStream_t s);
-// phase 0 = build + sample (as launch_filter), 1 = the rest, 2 = all of a round
-void launch_wfilter(const uint64_t *words, uint64_t n, uint64_t split, uint32_t ib,
-                    uint64_t seed, uint32_t bbits, uint32_t *bmS, uint32_t *bmL, uint32_t *mask,
-                    uint32_t *cnt, int phase, unsigned long long *sample, cudaStream_t s);
-void launch_wfilter_emit(const uint64_t *words, uint64_t n, uint64_t split, const uint32_t *mask,
-                         const uint32_t *cnt, const uint64_t *off, uint64_t *out, uint32_t *hist,
-                         uint32_t bit_lo, uint32_t dmask, cudaStream_t s);
+constexpr uint64_t kSjSlice = 512;                 // rows per warp slice
+struct SjSeg {                                     // one side's packed words (ascending row ids)
+  const uint64_t *w;
+  uint64_t rows;
+};
+uint64_t sj_slices(uint64_t rows);  // ceil(rows / 512)
+// Stage layout: side A's slices first (slice s at stage[s * 512 ..], count cnt[s]), then side
+// B's from slice sj_slices(n1) on; stage needs (sj_slices(n1) + sj_slices(n2)) * 512 words.
+// Column round, phase 0: build bmS from the smaller side's key columns (side B if s_is_b) and
+// probe a 1/16 sample of the larger side against it: sample[0] += survivors, sample[1] += rows.
+// Single packed column: plain bitmap (bit_index); PATH_HASH: blocked Bloom (cblock of the
+// key_hash chain).
+void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
+                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s);
+// Probe one side's key columns (side B if side_b) against bm (bm_kind 0 plain / 1 cblock of the
+// chain / 2 wblock of key' with seed) and stage its survivors; bm_set (plain, single-column keys
+// only): survivors also set their bit there.
+void launch_sj_probe_cols(const PackArgs &a, bool side_b, int bm_kind, const void *bm,
+                          uint32_t bbits, uint32_t hashed, uint64_t seed, uint32_t *bm_set,
+                          uint64_t *stage, uint32_t *cnt, cudaStream_t s);
+// Word rounds: probe packed words (their slices start at slice0) against a wblock bitmap.
+void launch_sj_probe_words(const SjSeg &in, uint64_t slice0, uint32_t ib, const void *bm,
+                           uint32_t bbits, uint64_t seed, uint64_t *stage, uint32_t *cnt,
+                           cudaStream_t s);
+// Set the bits of w[0 .. *count) (count on the device, <= max_rows): kind 0 plain bit_index of
+// key' = w >> ib, kind 2 wblock of key' with seed.
+void launch_sj_set_words(const uint64_t *w, const uint64_t *count, uint64_t max_rows, int kind,
+                         void *bm, uint32_t ib, uint32_t bbits, uint32_t hashed, uint64_t seed,
+                         cudaStream_t s);
+// out[off[s] ..] = the staged survivors of slice s (off = exclusive scan of cnt); hist += digit 0.
+void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t *off,
+                      uint64_t nslices, uint64_t *out, uint32_t *hist, uint32_t bit_lo,
+                      uint32_t dmask, cudaStream_t s);
+void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t bbits, void *bm,
+                           cudaStream_t s);
+void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t bbits,
+                            const void *bm, unsigned long long *sample, cudaStream_t s);
 
 // Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
 // (unordered, atomic slots < cap); per-run bounds [slo | olo | shi | ohi].

@@ -127,13 +127,14 @@ key_hist_kernel(const uint64_t *__restrict__ keys, uint64_t n, uint32_t bit_lo, 
 // unused during ranking), 3 = as 2 with a warp-uniform-digit shortcut (two redux.sync),
 // 4.. = as 2 after RANK-2 leader rounds of shfl + ballot.
 template <bool KV, int ITEMS = kSortItems, int WIN = kLookWin, int MINB = 3, bool RELOAD = false,
-          int RANK = 0>
+          int RANK = 0, bool SEG = false>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                   const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout, uint64_t n,
                   uint32_t shift, uint32_t bits, const uint32_t *__restrict__ hist_pass,
                   uint64_t *__restrict__ status, uint32_t *__restrict__ tile_counter,
-                  uint32_t *__restrict__ hist_next, uint32_t next_shift, uint32_t next_mask) {
+                  uint32_t *__restrict__ hist_next, uint32_t next_shift, uint32_t next_mask,
+                  uint64_t n0, uint64_t gap) {
   constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem_raw);
@@ -157,7 +158,16 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   const uint32_t tile_n = rem < (uint64_t)TILE ? (uint32_t)rem : (uint32_t)TILE;
   const uint32_t wslice = warp * 32 * ITEMS;
   const uint32_t dmask = (1u << bits) - 1u;
-  const uint64_t *src = kin + tile_base + wslice + lane;
+  // two-segment input (the semi-join filter's output): key i >= n0 is read at kin[i + gap]; a
+  // warp slice lies wholly in one segment except at the seam, where items pick their segment
+  const uint64_t g0 = tile_base + wslice;
+  const uint64_t *src = kin + g0 + lane + ((SEG && g0 >= n0) ? gap : 0);
+  const bool seam = SEG && g0 < n0 && g0 + 32 * ITEMS > n0;
+  auto ld_src = [&](int it) -> const uint64_t * {
+    if (!SEG || !seam) return src + it * 32;
+    const uint64_t g = g0 + it * 32 + lane;
+    return kin + g + (g >= n0 ? gap : 0);
+  };
 
   uint64_t k[ITEMS];
   uint32_t v[KV ? ITEMS : 1];
@@ -165,7 +175,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
   const bool full = tile_n == (uint32_t)TILE;
   if (full) {
 #pragma unroll
-    for (int it = 0; it < ITEMS; it++) k[it] = RELOAD ? __ldcg(src + it * 32) : __ldcs(src + it * 32);
+    for (int it = 0; it < ITEMS; it++) k[it] = RELOAD ? __ldcg(ld_src(it)) : __ldcs(ld_src(it));
     if (KV) {
 #pragma unroll
       for (int it = 0; it < ITEMS; it++) v[KV ? it : 0] = __ldcs(vin + tile_base + wslice + lane + it * 32);
@@ -174,7 +184,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
 #pragma unroll
     for (int it = 0; it < ITEMS; it++) {
       const bool in = wslice + it * 32 + lane < tile_n;
-      k[it] = in ? (RELOAD ? __ldcg(src + it * 32) : __ldcs(src + it * 32)) : 0ull;
+      k[it] = in ? (RELOAD ? __ldcg(ld_src(it)) : __ldcs(ld_src(it))) : 0ull;
       if (KV) v[KV ? it : 0] = in ? __ldcs(vin + tile_base + wslice + lane + it * 32) : 0u;
     }
   }
@@ -345,7 +355,7 @@ radix_pass_kernel(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
     if (wslice + it * 32 + lane < tile_n) {
       // RELOAD: the key is read again (an L2 hit) instead of being held in registers across the
       // look-back, which lets more CTAs share an SM
-      const uint64_t key = RELOAD ? __ldcs(src + it * 32) : k[it];
+      const uint64_t key = RELOAD ? __ldcs(ld_src(it)) : k[it];
       const uint32_t dd = (uint32_t)(key >> shift) & dmask;
       const uint32_t slot = s_digit_start[dd] + s_warp_hist[warp][dd] + r[it];
       s_keys[slot] = key;
@@ -393,7 +403,9 @@ void launch_key_hist(const uint64_t *keys, uint64_t n, uint32_t bit_lo, uint32_t
 void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
                        uint64_t n, uint32_t shift, uint32_t bits, const uint32_t *hist_pass,
                        uint64_t *status, uint32_t *tile_counter, uint32_t *hist_next,
-                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s) {
+                       uint32_t next_shift, uint32_t next_bits, cudaStream_t s, uint64_t n0,
+                       uint64_t gap) {
+  if (n0 > n || gap == 0) n0 = n;  // one segment
   const uint32_t next_mask = (1u << next_bits) - 1u;
   if (vin) {
     // (key, rowid) pairs: 4096-key tiles (the payload needs the registers)
@@ -403,7 +415,7 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(
         kin, kout, vin, vout, n, shift, bits, hist_pass, status, tile_counter, hist_next,
-        next_shift, next_mask);
+        next_shift, next_mask, n, 0);
   } else {
     // P64 words: 6144-key tiles, 3 CTAs/SM, keys re-read from L2 for placement.  Peers found by
     // shared-memory atomicOr with a warp-uniform shortcut (tools/radix_ablate.cu: a C4-shaped
@@ -412,11 +424,12 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     constexpr int kItems = 24;
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = radix_pass_kernel<false, kItems, 4, 3, true, 3>;
+    auto kern = (gap && n0 < n) ? radix_pass_kernel<false, kItems, 4, 3, true, 3, true>
+                                : radix_pass_kernel<false, kItems, 4, 3, true, 3, false>;
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,
-                                                      next_shift, next_mask);
+                                                      next_shift, next_mask, n0, gap);
   }
 }
 
