@@ -803,30 +803,9 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
                        gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
     CKL("find_groups");
   }
-  // RESIDUAL and HASH verify the shared columns not (exactly) in key' for every pair
+  // RESIDUAL and HASH: the nL * nR pairs of a key' group are candidates, verified on the shared
+  // columns not (exactly) in key'
   const bool residual = pl.path == MAPSQ_PATH_RESIDUAL || pl.path == MAPSQ_PATH_HASH;
-  ResidualArgs ra;
-  std::memset(&ra, 0, sizeof ra);
-  uint64_t *pmask = residual ? sc.get<uint64_t>(cap) : nullptr;
-  if (residual) {
-    NEED(pmask);
-    ra.words = words;
-    ra.n1 = n1;
-    ra.ib = pl.ib;
-    ra.gstart = gs;
-    ra.gsplit = gp;
-    ra.gend = ge;
-    ra.ngroups_dev = scal;
-    for (uint32_t c = 0; c < pl.nshared; c++)
-      if (!(pl.packed_mask >> c & 1u)) {
-        ra.res1[ra.nres] = a.col[pl.key_col1[c]];
-        ra.res2[ra.nres] = b.col[pl.key_col2[c]];
-        ra.nres++;
-      }
-    KTimer kt(ctx, s, "residual_count", 8ull * nw);
-    launch_residual_count(ra, cap, gc, pmask, s);  // exact pair counts replace nL * nR
-    CKL("residual_count");
-  }
   {
     KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
     launch_exclusive_scan_u64_dev(gc, go, scal, cap, tmp, scal + 1, s);
@@ -834,39 +813,93 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   TRY(ensure_pinned(ctx, 2));
   CK(cudaMemcpyAsync(ctx->pinned, scal, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));  // the one blocking read: |RS| sizes the output
+  CK(cudaStreamSynchronize(s));  // the one blocking read: |RS| (candidates) sizes the output
   const uint64_t ngroups = ctx->pinned[0], m = ctx->pinned[1];
   ctx->counters.last_groups = ngroups;
   if (residual) {
+    const uint64_t C = m;  // candidate pairs: an upper bound of |RS|
+    ResidualArgs ra;
+    std::memset(&ra, 0, sizeof ra);
+    ra.words = words;
+    ra.n1 = n1;
+    ra.ib = pl.ib;
+    ra.gstart = gs;
+    ra.gsplit = gp;
+    ra.gend = ge;
+    for (uint32_t c = 0; c < pl.nshared; c++)
+      if (!(pl.packed_mask >> c & 1u)) {
+        ra.res1[ra.nres] = a.col[pl.key_col1[c]];
+        ra.res2[ra.nres] = b.col[pl.key_col2[c]];
+        ra.nres++;
+      }
+    uint32_t k = 0;
+    for (uint32_t c = 0; c < pl.nshared; c++, k++) {
+      ra.src_side[k] = 0;
+      ra.src[k] = a.col[pl.key_col1[c]];
+    }
+    for (uint32_t c = 0; c < pl.nrest1; c++, k++) {
+      ra.src_side[k] = 0;
+      ra.src[k] = a.col[pl.rest_col1[c]];
+    }
+    for (uint32_t c = 0; c < pl.nrest2; c++, k++) {
+      ra.src_side[k] = 1;
+      ra.src[k] = b.col[pl.rest_col2[c]];
+    }
+    ra.nout = k;
     fill_empty_join(pl, &a, &b, rs);
-    TRY(alloc_table(ctx, rs, m, pl.out_ncols, s));
-    if (m) {
-      uint32_t k = 0;
-      for (uint32_t c = 0; c < pl.nshared; c++, k++) {
-        ra.src_side[k] = 0;
-        ra.src[k] = a.col[pl.key_col1[c]];
+    if (C == 0) {
+      ctx->counters.join_out_rows += 0;
+      return MAPSQ_OK;
+    }
+    const uint64_t vt = verify_tiles(C);
+    uint64_t *vstatus = sc.get<uint64_t>(vt + 1), *tile_g0 = sc.get<uint64_t>(vt + 1);
+    uint32_t *vctr = sc.get<uint32_t>(2);
+    unsigned long long *vtot = sc.get<unsigned long long>(2);
+    NEED(vstatus); NEED(tile_g0); NEED(vctr); NEED(vtot);
+    // the output is sized by the candidate count when that is a tight bound (hashed keys: the
+    // candidates are the matches plus the rare key' collisions); otherwise the matches are
+    // counted first (a second candidate-parallel pass without writes)
+    uint64_t cap_rows = C;
+    if (C > 2 * (n1 + n2) + (1ull << 20)) {
+      CK(cudaMemsetAsync(vtot, 0, 2 * sizeof(uint64_t), s));
+      {
+        KTimer kt(ctx, s, "verify_count", 8ull * nw);
+        launch_verify_emit(ra, go, tile_g0, ngroups, C, false, vstatus, vctr, vtot, s);
+        CKL("verify_count");
       }
-      for (uint32_t c = 0; c < pl.nrest1; c++, k++) {
-        ra.src_side[k] = 0;
-        ra.src[k] = a.col[pl.rest_col1[c]];
-      }
-      for (uint32_t c = 0; c < pl.nrest2; c++, k++) {
-        ra.src_side[k] = 1;
-        ra.src[k] = b.col[pl.rest_col2[c]];
-      }
-      ra.nout = k;
-      for (uint32_t c = 0; c < k; c++) ra.out[c] = rs->col[c];
-      ra.goff = go;
-      KTimer kt(ctx, s, "residual_expand", 4ull * m * pl.out_ncols);
-      launch_residual_expand(ra, ngroups, pmask, s);
+      CK(cudaMemcpyAsync(ctx->pinned, vtot, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      cap_rows = ctx->pinned[0];
+      if (cap_rows == 0) return MAPSQ_OK;
+    }
+    TRY(alloc_table(ctx, rs, cap_rows, pl.out_ncols, s));
+    for (uint32_t c = 0; c < k; c++) ra.out[c] = rs->col[c];
+    CK(cudaMemsetAsync(vstatus, 0, (vt + 1) * sizeof(uint64_t), s));
+    CK(cudaMemsetAsync(vctr, 0, 2 * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(vtot, 0, 2 * sizeof(uint64_t), s));
+    size_t pos = ~size_t(0);
+    {
+      KTimer kt(ctx, s, "verify_emit", 8ull * nw, 2);
+      launch_verify_emit(ra, go, tile_g0, ngroups, C, true, vstatus, vctr, vtot, s);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         dfree(ctx, rs->owner, s);
         clear_table(rs);
-        return cuda_check(ctx, e, "residual_expand");
+        return cuda_check(ctx, e, "verify_emit");
       }
     }
-    ctx->counters.join_out_rows += m;
+    if (ctx->profiling) pos = ctx->pending.size() - 1;
+    CK(cudaMemcpyAsync(ctx->pinned, vtot, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // |RS|: the matched candidates
+    const uint64_t mm = ctx->pinned[0];
+    rs->nrows = mm;
+    if (mm == 0) {  // nothing matched: release the allocation, keep the schema
+      dfree(ctx, rs->owner, s);
+      rs->owner = nullptr;
+      for (uint32_t c = 0; c < pl.out_ncols; c++) rs->col[c] = nullptr;
+    }
+    if (pos < ctx->pending.size()) ctx->pending[pos].bytes += 4ull * mm * pl.out_ncols;
+    ctx->counters.join_out_rows += mm;
     return MAPSQ_OK;
   }
   // ---- ReduceDuplicate 2 (row a6): expand into RS

@@ -356,28 +356,30 @@ struct ExpandArgs {
 void launch_expand(const ExpandArgs &a, cudaStream_t s);
 uint64_t expand_tiles(uint64_t m);
 
-// RESIDUAL path (wide keys): groups are equal on the packed key; the residual shared columns are
-// compared exactly, pair by pair, inside each group.
+// RESIDUAL / HASH paths (wide keys): groups are equal on key' (packed columns or a hash); the
+// residual shared columns are compared exactly for every (LEFT, RIGHT) candidate pair.
 struct ResidualArgs {
-  const uint64_t *words;  // sorted P64 words over the packed columns
+  const uint64_t *words;  // sorted P64 words over key'
   uint64_t n1;
   uint32_t ib;
   const uint32_t *gstart, *gsplit, *gend;
-  const uint64_t *ngroups_dev;  // group count (device)
   uint32_t nres;
   const uint32_t *res1[MAPSQ_MAX_COLS];  // residual columns of tp1 / tp2, same variable order
   const uint32_t *res2[MAPSQ_MAX_COLS];
-  // expand: output column c comes from side src_side[c] (0 = tp1, 1 = tp2), column src[c]
+  // output column c comes from side src_side[c] (0 = tp1, 1 = tp2), column src[c]
   uint32_t nout;
   uint32_t src_side[MAPSQ_MAX_COLS];
   const uint32_t *src[MAPSQ_MAX_COLS];
   uint32_t *out[MAPSQ_MAX_COLS];
-  const uint64_t *goff;  // exclusive offsets of the exact pair counts
 };
-void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, uint64_t *pmask,
-                           cudaStream_t s);
-void launch_residual_expand(const ResidualArgs &a, uint64_t cap, const uint64_t *pmask,
-                            cudaStream_t s);
+// Candidate-parallel verification over the C candidate pairs (coff = exclusive scan of nL * nR
+// per group): write = true stores the matched pairs in (key', tp1 row, tp2 row) order at out[0 ..)
+// (capacity C) and their number in *total; write = false only adds the number of matches to
+// *total.  status: verify_tiles(C) zeroed words, tile_ctr zeroed, tile_g0 verify_tiles(C) + 1.
+uint64_t verify_tiles(uint64_t candidates);
+void launch_verify_emit(const ResidualArgs &a, const uint64_t *coff, uint64_t *tile_g0,
+                        uint64_t ngroups, uint64_t C, bool write, uint64_t *status,
+                        uint32_t *tile_ctr, unsigned long long *total, cudaStream_t s);
 uint64_t find_groups_tiles(uint64_t n);
 
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,

@@ -7,6 +7,8 @@
 // with one label only produce nothing and are never visited again.  The splits are compacted in
 // key order with a single-pass decoupled look-back; the thread owning a split gallops outwards
 // to the run's ends and stores (start, split, end) and nL * nR.
+// RESIDUAL / HASH verify-emit: candidate-parallel check of the residual shared columns of every
+// (LEFT, RIGHT) pair of a key' group, writing the matches in order (see below).
 // K6 expand: "GPU's SIMD architectures contribute to accelerate cartesian product in parallel"
 // (P:149).  Output-row parallel, so skewed keys are load balanced: every thread owns 4
 // consecutive output rows, finds its group by a binary search bracketed per CTA, and writes
@@ -222,15 +224,21 @@ constexpr int kERowsPerThread = 8;           // rows per thread = chunks x rows 
 constexpr uint64_t kETile = (uint64_t)kEThreads * kERowsPerThread;
 constexpr int kEGroups = 1024;               // groups staged in shared memory per tile
 
-// K5b: tile t of the expansion (rows [t * kETile, ...)) starts inside group tile_g0[t].  One thread
-// per group marks the tiles whose first row falls in the group's output range.
+// K5b: tile t of the expansion (rows [t * tile_rows, ...)) starts inside group tile_g0[t], the
+// last group whose offset is <= t * tile_rows: one thread per tile, a binary search over the
+// offsets (a hot group spanning many tiles costs nothing extra).
 __global__ void __launch_bounds__(256)
-tile_groups_kernel(const uint64_t *__restrict__ goff, uint64_t ngroups, uint64_t m,
-                   uint64_t *__restrict__ tile_g0) {
-  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups;
-       g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = goff[g], e = g + 1 < ngroups ? goff[g + 1] : m;
-    for (uint64_t t = (b + kETile - 1) / kETile; t * kETile < e; t++) tile_g0[t] = g;
+tile_groups_kernel(const uint64_t *__restrict__ goff, uint64_t ngroups, uint64_t ntiles,
+                   uint64_t *__restrict__ tile_g0, uint64_t tile_rows) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t * tile_rows;
+    uint64_t lo = 0, hi = ngroups - 1;  // goff[0] == 0 <= r
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(goff + mid) <= r) lo = mid; else hi = mid - 1;
+    }
+    tile_g0[t] = lo;
   }
 }
 
@@ -406,76 +414,157 @@ expand_kernel(const ExpandArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ RESIDUAL path (wide keys)
-// One thread per packed-key group: the exact pair count of the group is the number of
-// (LEFT, RIGHT) row pairs that also agree on every residual shared column.  Groups of wide-key
-// joins (e.g. C5's (?x, ?z) with ?x packed) are a handful of rows, so the pair loop is short.
-__device__ __forceinline__ bool residual_equal(const ResidualArgs &a, uint32_t li, uint32_t ri) {
-  for (uint32_t c = 0; c < a.nres; c++)
-    if (__ldg(a.res1[c] + li) != __ldg(a.res2[c] + ri)) return false;
-  return true;
-}
+// ------------------------------------------------------------------ RESIDUAL / HASH paths
+// The sorted words group rows by key' (a packed subset of the shared columns, or a hash of all of
+// them), so a key' group's (LEFT, RIGHT) pairs are CANDIDATES: a pair belongs to RS iff the rows
+// also agree on every residual shared column (reading R19).  "GPU's SIMD architectures contribute
+// to accelerate cartesian product in parallel": the verification is candidate-parallel
+// like the expansion — a CTA owns 2048 consecutive candidates (offsets = exclusive scan of
+// nL * nR), each thread 8 consecutive ones, so a hot key' group is spread over many CTAs.  Each
+// thread compares its candidates' residual columns, the CTA counts the matches, and (WRITE)
+// tiles claimed in order resolve their output offset by decoupled look-back and write the matched
+// pairs in (key', Tp1 row, Tp2 row) order — one pass, the output gathered only for matches.
+// WRITE = false only counts the matches (for joins whose candidate count is too large to size
+// the output by).
+constexpr int kVThreads = 256;
+constexpr int kVPer = 8;
+constexpr uint64_t kVTile = (uint64_t)kVThreads * kVPer;
 
-// Groups with nL * nR <= 64 also record which pairs matched (bit l * nR + r of a 64-bit mask),
-// so the expansion touches only matched pairs and never re-reads the residual columns.
-__global__ void __launch_bounds__(256)
-residual_count_kernel(const ResidualArgs a, uint64_t *__restrict__ cnt,
-                      uint64_t *__restrict__ pmask) {
-  const uint64_t ng = *a.ngroups_dev;
-  const uint64_t mask = (1ull << a.ib) - 1;
-  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
-       g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
-    const bool small = (uint64_t)(sp - st) * (en - sp) <= 64;
-    uint64_t c = 0, bits = 0;
-    uint32_t q = 0;
-    for (uint32_t l = st; l < sp; l++) {
-      const uint32_t li = (uint32_t)(a.words[l] & mask);
-      for (uint32_t r = sp; r < en; r++, q++) {
-        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
-        const bool eq = residual_equal(a, li, ri);
-        c += eq;
-        if (small && eq) bits |= 1ull << q;
-      }
-    }
-    cnt[g] = c;
-    pmask[g] = bits;
+template <bool WRITE>
+__global__ void __launch_bounds__(kVThreads)
+verify_emit_kernel(const ResidualArgs a, const uint64_t *__restrict__ coff,
+                   const uint64_t *__restrict__ tile_g0, uint64_t ngroups, uint64_t C,
+                   uint64_t *__restrict__ status, uint32_t *__restrict__ tile_ctr,
+                   unsigned long long *__restrict__ total) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_g[2], s_base;
+  __shared__ uint64_t s_off[kEGroups + 1];
+  __shared__ uint32_t s_start[kEGroups], s_split[kEGroups], s_end[kEGroups];
+  __shared__ uint32_t s_wsum[kVThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = WRITE ? atomicAdd(tile_ctr, 1u) : blockIdx.x;  // in order (look-back)
+    s_tile = t;
+    s_g[0] = tile_g0[t];
+    s_g[1] = t + 1 < gridDim.x ? tile_g0[t + 1] : ngroups - 1;
   }
-}
-
-__global__ void __launch_bounds__(256)
-residual_expand_kernel(const ResidualArgs a, const uint64_t *__restrict__ pmask) {
-  const uint64_t ng = *a.ngroups_dev;
+  __syncthreads();
+  const uint64_t tile = s_tile, t0 = tile * kVTile;
+  const uint64_t g0 = s_g[0], g1 = s_g[1];
+  const bool staged = g1 - g0 + 1 <= (uint64_t)kEGroups;
+  if (staged) {
+    for (uint64_t q = tid; q <= g1 - g0; q += kVThreads) {
+      const uint64_t g = g0 + q;
+      s_off[q] = coff[g];
+      s_start[q] = a.gstart[g];
+      s_split[q] = a.gsplit[g];
+      s_end[q] = a.gend[g];
+    }
+    if (tid == 0) s_off[g1 - g0 + 1] = (g1 + 1 < ngroups) ? coff[g1 + 1] : C;
+  }
+  __syncthreads();
   const uint64_t mask = (1ull << a.ib) - 1;
-  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng;
-       g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t st = a.gstart[g], sp = a.gsplit[g], en = a.gend[g];
-    const uint32_t nR = en - sp;
-    uint64_t pos = a.goff[g];
-    if ((uint64_t)(sp - st) * nR <= 64) {
-      uint64_t bits = pmask[g];
-      while (bits) {  // matched pairs only, in (l, r) order
-        const uint32_t q = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        const uint32_t l = st + q / nR, r = sp + q % nR;
-        const uint32_t li = (uint32_t)(a.words[l] & mask);
-        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
-        for (uint32_t c = 0; c < a.nout; c++)
-          a.out[c][pos] = __ldg(a.src[c] + (a.src_side[c] ? ri : li));
-        pos++;
+  const uint64_t r0 = t0 + (uint64_t)tid * kVPer;
+  uint32_t lidx[kVPer], ridx[kVPer], match = 0;
+  if (r0 < C) {
+    uint64_t gl, gend;
+    uint32_t start, split, end;
+    if (staged) {
+      uint32_t lo = 0, hi = (uint32_t)(g1 - g0);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (s_off[mid] <= r0) lo = mid; else hi = mid - 1;
       }
-      continue;
+      gl = lo;
+      gend = s_off[gl + 1];
+      start = s_start[gl]; split = s_split[gl]; end = s_end[gl];
+      gl += g0;
+    } else {
+      gl = group_of(coff, g0, g1, r0);
+      gend = (gl + 1 < ngroups) ? coff[gl + 1] : C;
+      start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
     }
-    for (uint32_t l = st; l < sp; l++) {
-      const uint32_t li = (uint32_t)(a.words[l] & mask);
-      for (uint32_t r = sp; r < en; r++) {
-        const uint32_t ri = (uint32_t)((a.words[r] & mask) - a.n1);
-        if (!residual_equal(a, li, ri)) continue;
-        for (uint32_t c = 0; c < a.nout; c++)
-          a.out[c][pos] = __ldg(a.src[c] + (a.src_side[c] ? ri : li));
-        pos++;
+    uint64_t nR = end - split, local = r0 - coff[gl];
+    uint64_t li = local / nR, ri = local - li * nR;
+    uint32_t valid = 0;
+#pragma unroll
+    for (int j = 0; j < kVPer; j++) {  // candidate positions, then all word loads together
+      const uint64_t r = r0 + j;
+      if (r >= C) break;
+      if (r >= gend) {  // next group (groups are never empty)
+        gl++;
+        gend = (gl + 1 < ngroups) ? coff[gl + 1] : C;
+        start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
+        nR = end - split;
+        li = ri = 0;
       }
+      lidx[j] = (uint32_t)(start + li);
+      ridx[j] = (uint32_t)(split + ri);
+      valid |= 1u << j;
+      if (++ri == nR) { ri = 0; li++; }
     }
+#pragma unroll
+    for (int j = 0; j < kVPer; j++) {
+      if (!(valid >> j & 1u)) continue;
+      lidx[j] = (uint32_t)(__ldg(a.words + lidx[j]) & mask);
+      ridx[j] = (uint32_t)((__ldg(a.words + ridx[j]) & mask) - a.n1);
+    }
+    match = valid;
+    for (uint32_t c = 0; c < a.nres; c++) {  // every candidate's loads of a column together
+      uint32_t x[kVPer], y[kVPer];
+#pragma unroll
+      for (int j = 0; j < kVPer; j++) {
+        x[j] = (match >> j & 1u) ? __ldg(a.res1[c] + lidx[j]) : 0u;
+        y[j] = (match >> j & 1u) ? __ldg(a.res2[c] + ridx[j]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kVPer; j++)
+        if (x[j] != y[j]) match &= ~(1u << j);
+    }
+  }
+  // block scan of the per-thread match counts
+  const uint32_t cnt = __popc(match);
+  uint32_t x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kVThreads / 32; w++) {
+    const uint32_t v = s_wsum[w];
+    if ((uint32_t)w < warp) wpre += v;
+    agg += v;
+  }
+  if (!WRITE) {
+    if (tid == 0 && agg) atomicAdd(total, (unsigned long long)agg);
+    return;
+  }
+  if (warp == 0) {
+    const uint64_t excl = warp_lookback(status, tile, agg);
+    if (lane == 0) {
+      s_base = excl;
+      if (tile + 1 == gridDim.x) *total = excl + agg;
+    }
+  }
+  __syncthreads();
+  if (!match) return;
+  const uint64_t pos0 = s_base + wpre + x - cnt;
+  for (uint32_t c = 0; c < a.nout; c++) {  // a column's gathers in flight together, then stores
+    const uint32_t *src = a.src[c];
+    const bool right = a.src_side[c];
+    uint32_t v[kVPer];
+#pragma unroll
+    for (int j = 0; j < kVPer; j++)
+      v[j] = (match >> j & 1u) ? __ldg(src + (right ? ridx[j] : lidx[j])) : 0u;
+    uint32_t *dst = a.out[c] + pos0;
+    uint32_t q = 0;
+#pragma unroll
+    for (int j = 0; j < kVPer; j++)
+      if (match >> j & 1u) dst[q++] = v[j];
   }
 }
 
@@ -502,18 +591,21 @@ void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint3
 
 uint64_t find_groups_tiles(uint64_t n) { return ceil_div(n, kGTile); }
 
-static unsigned residual_grid(uint64_t cap) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(cap, 256), 148 * 16));
-}
+uint64_t verify_tiles(uint64_t candidates) { return ceil_div(candidates, kVTile); }
 
-void launch_residual_count(const ResidualArgs &a, uint64_t cap, uint64_t *cnt, uint64_t *pmask,
-                           cudaStream_t s) {
-  residual_count_kernel<<<residual_grid(cap), 256, 0, s>>>(a, cnt, pmask);
-}
-
-void launch_residual_expand(const ResidualArgs &a, uint64_t cap, const uint64_t *pmask,
-                            cudaStream_t s) {
-  residual_expand_kernel<<<residual_grid(cap), 256, 0, s>>>(a, pmask);
+void launch_verify_emit(const ResidualArgs &a, const uint64_t *coff, uint64_t *tile_g0,
+                        uint64_t ngroups, uint64_t C, bool write, uint64_t *status,
+                        uint32_t *tile_ctr, unsigned long long *total, cudaStream_t s) {
+  if (C == 0 || ngroups == 0) return;
+  const uint64_t ntiles = verify_tiles(C);
+  const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(ntiles, 256), 148 * 16));
+  tile_groups_kernel<<<gg, 256, 0, s>>>(coff, ngroups, ntiles, tile_g0, kVTile);
+  if (write)
+    verify_emit_kernel<true><<<(unsigned)ntiles, kVThreads, 0, s>>>(a, coff, tile_g0, ngroups, C,
+                                                                   status, tile_ctr, total);
+  else
+    verify_emit_kernel<false><<<(unsigned)ntiles, kVThreads, 0, s>>>(a, coff, tile_g0, ngroups, C,
+                                                                    status, tile_ctr, total);
 }
 
 uint64_t expand_tiles(uint64_t m) { return ceil_div(m, kETile); }
@@ -521,8 +613,9 @@ uint64_t expand_tiles(uint64_t m) { return ceil_div(m, kETile); }
 void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   if (a.m == 0) return;
   const uint64_t nblocks = ceil_div(a.m, kETile);
-  const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(a.ngroups, 256), 148 * 16));
-  tile_groups_kernel<<<gg, 256, 0, s>>>(a.goff, a.ngroups, a.m, const_cast<uint64_t *>(a.tile_g0));
+  const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(nblocks, 256), 148 * 16));
+  tile_groups_kernel<<<gg, 256, 0, s>>>(a.goff, a.ngroups, nblocks,
+                                        const_cast<uint64_t *>(a.tile_g0), kETile);
   // long runs of one group (C3's star: ~2e4 rows per group) favour 2 chunks of 4 rows per
   // thread; short groups (C5's first join: ~20 rows) one chunk of 8 rows (C3 2.50 vs 2.72 ms,
   // C5 J1 0.88 vs 0.81 ms)

@@ -161,6 +161,35 @@ def test_join_residual_path_collisions_and_skew(ctx, mode, path):
     ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_HASH)
 
 
+@pytest.mark.parametrize("mode", ["RESIDUAL", "HASH"])
+def test_join_hot_composite_key(ctx, mode):
+    # One hot composite key: x = 7 on 1500 LEFT and 1400 RIGHT rows with z in {5, 6}.  RESIDUAL
+    # packs x and checks z: the hot x-group holds 2.1e6 candidate pairs, about half of them true
+    # (more candidates than 2 (n1 + n2) + 2^20, so the matches are counted before the output is
+    # sized); HASH groups by a hash of (x, z): two hot groups of ~5e5 true pairs.  Both spread a
+    # group's pairs over many CTAs (candidate-parallel verification).
+    ctx.set_option(mq.OPT_WIDE_KEY, getattr(mq, "WIDE_KEY_" + mode))
+    rng = np.random.default_rng(29)
+    nh1, nh2, nc = 1500, 1400, 3000
+    x1 = np.concatenate([np.full(nh1, 7), rng.integers(0, 1 << 32, nc, dtype=np.uint64)])
+    z1 = np.concatenate([rng.integers(5, 7, nh1), rng.integers(0, 1 << 32, nc, dtype=np.uint64)])
+    x2 = np.concatenate([np.full(nh2, 7), rng.integers(0, 1 << 32, nc, dtype=np.uint64)])
+    z2 = np.concatenate([rng.integers(5, 7, nh2), rng.integers(0, 1 << 32, nc, dtype=np.uint64)])
+    x1[-1] = z1[-1] = 0xFFFFFFFF  # both key columns span 32 bits: the plan cannot pack both
+    x2[-1] = z2[-1] = 0
+    p1, p2 = rng.permutation(len(x1)), rng.permutation(len(x2))
+    A = np.stack([x1, z1, np.arange(len(x1))], 1).astype(np.uint32)[p1]
+    B = np.stack([z2, np.arange(len(x2)) + 10 ** 6, x2], 1).astype(np.uint32)[p2]
+    ref = oracle.join(oracle.Table([0, 1, 2], A), oracle.Table([1, 3, 0], B))
+    got = ctx.join(dtable([0, 1, 2], A), dtable([1, 3, 0], B))
+    assert ctx.stats()["last_path"] == getattr(mq, "PATH_" + mode)
+    hot = [(int((A[:, 1][A[:, 0] == 7] == z).sum()), int((B[:, 0][B[:, 2] == 7] == z).sum()))
+           for z in (5, 6)]
+    assert got.nrows == ref.nrows >= sum(a * b for a, b in hot) > 900_000
+    assert_same(got, ref, ordered=False)
+    ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_HASH)
+
+
 def test_join_skewed_hot_key_large_groups(ctx):
     rng = np.random.default_rng(11)
     # one hot key: 6000 x 700 = 4.2e6 output rows, plus a cold tail

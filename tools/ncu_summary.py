@@ -38,20 +38,16 @@ for r in rows[2:]:
 # several kernels; its invocations are counted by its anchor kernel
 TIMERS = {  # timer: (member kernels, invocations from the launch counts)
     "radix_pass": (["radix_pass"], lambda c: c("radix_pass")),
-    "wfilter": (["wfilter_build", "wfilter_probe", "wfilter_setmask"],
-                lambda c: c("wfilter_setmask")),
-    "filter_sample": (["filter_build", "filter_sample", "cfilter_build", "cfilter_sample",
-                       "wfilter_sample"],
-                      lambda c: c("filter_sample") + c("cfilter_sample") + c("wfilter_sample")),
-    "filter": (["filter_probe", "cfilter_probe", "cfilter_setmask"],
-               lambda c: c("filter_probe") // 2 + c("cfilter_setmask")),
-    "filter_emit": (["filter_emit"], lambda c: c("filter_emit")),
-    "wfilter_emit": (["wfilter_emit"], lambda c: c("wfilter_emit")),
+    "filter_build": (["filter_build", "filter_sample", "cfilter_build", "cfilter_sample",
+                      "wfilter_build", "wfilter_sample"],
+                     lambda c: c("filter_build") + c("cfilter_build") + c("wfilter_build")),
+    "filter_probe": (["sj_probe_stage"], lambda c: c("sj_probe_stage")),
+    "filter_gather": (["sj_gather"], lambda c: c("sj_gather")),
+    "filter_set": (["sj_set_words"], lambda c: c("sj_set_words")),
     "pack_hist": (["pack_hist"], lambda c: c("pack_hist")),
     "find_groups": (["find_groups"], lambda c: c("find_groups")),
-    "expand": (["tile_groups", "expand"], lambda c: c("expand")),
-    "residual_count": (["residual_count"], lambda c: c("residual_count")),
-    "residual_expand": (["residual_expand"], lambda c: c("residual_expand")),
+    "expand": (["expand"], lambda c: c("expand")),
+    "verify_emit": (["verify_emit"], lambda c: c("verify_emit")),
     "scan_write": (["scan_write"], lambda c: c("scan_write")),
 }
 per_timer = {}
