@@ -33,6 +33,7 @@ CONFIGS = {
     "C5": ("lubm", 10000, "C5", "LUBM(10000) Q9-core triangle (advisor, teacherOf, takesCourse)"),
 }
 METRIC = "join input+output tuples/s and HBM GB/s (% peak) at 1/2/4/8 B200"
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
 
 
 def log(*a):
@@ -65,7 +66,17 @@ class ClockSampler:
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            # NVML numbers devices ignoring CUDA_VISIBLE_DEVICES: find this rank's GPU by UUID
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+                uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+                h = nv.nvmlDeviceGetHandleByUUID(uuid.encode())
+                self.sampled = uuid
+            except Exception:  # noqa: BLE001 (older torch / NVML: index order)
+                h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+                self.sampled = f"nvml index {self.gpu}"
             bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
@@ -136,7 +147,8 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
                 "sm_max_mhz": max(self.mx) if self.mx else None,
                 "reasons": sorted(self.reasons), "samples": len(self.sm),
-                "source": "nvml" if self.thread is not None else "nvidia-smi"}
+                "source": "nvml" if self.thread is not None else "nvidia-smi",
+                "gpu": getattr(self, "sampled", f"index {self.gpu}")}
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -508,7 +520,10 @@ def run_gpu_dist(args, world, rank, local):
     # its whole shard), runs the distributed query and reads its result shard back; the step
     # time is the max over ranks
     e2e = None
-    if not args.no_e2e and not (hidx is not None and getattr(ctx, "ipc_unavailable", None)):
+    # every rank takes the same branch: the fused-exchange fallback flag is agreed on first
+    fb = torch.tensor([1 if getattr(ctx, "ipc_unavailable", None) else 0], device="cuda")
+    tdist.all_reduce(fb, op=tdist.ReduceOp.MAX)
+    if not args.no_e2e and not (hidx is not None and int(fb.item())):
         if hidx is None:
             dev_bufs = [torch.empty(len(s), dtype=torch.int32, device="cuda") for _ in range(3)]
         e2e_ms, h2d, d2h = [], 12 * len(s), 0
@@ -517,7 +532,10 @@ def run_gpu_dist(args, world, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             if hidx is not None:
-                _, rows = ctx.query_dist_host(hidx, pats)
+                got = mqd._fused_call(ctx, lambda: ctx.query_dist_host(hidx, pats))
+                if got is None:
+                    raise RuntimeError(f"fused exchange unavailable: {ctx.ipc_unavailable}")
+                _, rows = got
                 h2d, d2h = hidx.last_h2d_bytes, rows.nbytes
             else:
                 for d, h in zip(dev_bufs, pinned_bufs):
@@ -539,6 +557,14 @@ def run_gpu_dist(args, world, rank, local):
     agg = torch.tensor([st_plain["join_in_rows"] + st_plain["join_out_rows"], st_plain["launches"],
                         sent], dtype=torch.float64, device="cuda")
     tdist.all_reduce(agg, op=tdist.ReduceOp.SUM)
+    # the fused scatter (partition + NVLink stores into the peers' arenas): bytes this rank sent
+    # to peers over its scatter kernels' event-timed duration (profiled region), max over ranks
+    sc = st_k["kernels"].get("partition_scatter", {"ms": 0.0, "launches": 0})
+    xr = torch.tensor([st_k["exchange_bytes"] / max(sc["ms"], 1e-9) / 1e6 if sc["ms"] else 0.0,
+                       sc["ms"] / args.steps], dtype=torch.float64, device="cuda")
+    xmin = xr.clone()
+    tdist.all_reduce(xr, op=tdist.ReduceOp.MAX)
+    tdist.all_reduce(xmin, op=tdist.ReduceOp.MIN)
     total_s = float(t.item()) / 1e3
     if rank == 0:
         tup, launches, sent_all = (float(x) for x in agg.tolist())
@@ -561,8 +587,16 @@ def run_gpu_dist(args, world, rank, local):
                                              "(mapsq_*_dist)")},
                 "exchange": {"bytes_per_step": sent_all / args.steps,
                              "gbs_over_step_time": sent_all / total_s / 1e9,
+                             "scatter_ms_per_step_max_rank": float(xr[1].item()),
+                             "per_rank_send_gbs": {"min": float(xmin[0].item()),
+                                                   "max": float(xr[0].item())},
+                             "nvlink_peak_gbs": NVLINK_PEER_GBS,
+                             "nvlink_frac_min_rank": float(xmin[0].item()) / NVLINK_PEER_GBS,
                              "note": "bytes all ranks sent to peers per step (fused partition + "
-                                     "NVLink exchange); rate over the whole step time"},
+                                     "NVLink exchange); per-rank send rate = bytes stored into "
+                                     "peers' arenas / that rank's partition_scatter kernel time, "
+                                     "against the measured 770 GB/s per-direction peer copy "
+                                     "(B200_PROFILING.md; 900 nominal)"},
                 "roofline": {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak,
                              "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": None, "rank": 0},
@@ -602,10 +636,33 @@ def main():
                     help="testing: run the multi-GPU path (exchange per join) even at world size 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` started directly: re-exec under torch.distributed.run with N ranks on
+    this node (the driver's launch, 127.0.0.1 rendezvous).  Fails loudly when fewer than N GPUs
+    are visible instead of printing a 1-GPU line."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible")
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("relaunching:", " ".join(cmd))
+    os.execv(sys.executable, cmd)
 
 
 if __name__ == "__main__":

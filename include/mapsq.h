@@ -40,10 +40,12 @@ typedef enum {
   MAPSQ_E_NO_SHARED = 2,   /* join inputs share no variable; query pattern not connected to the
                               patterns before it */
   MAPSQ_E_NOMEM = 3,       /* the allocator returned NULL; nothing is partially written */
-  MAPSQ_E_CUDA = 4,        /* CUDA error (text in mapsq_last_error); sticky for the context */
-  MAPSQ_E_UNSUPPORTED = 5, /* packed key wider than 64 bits after range compression */
-  MAPSQ_E_NCCL = 6         /* NCCL missing or a collective failed (text in mapsq_last_error);
-                              distributed entry points only */
+  MAPSQ_E_CUDA = 4,        /* CUDA error (text in mapsq_last_error); sticky for the context,
+                              except a "CUDA IPC" failure of the fused exchange (see below) */
+  MAPSQ_E_NCCL = 5,        /* NCCL missing or a control-plane collective failed (text in
+                              mapsq_last_error); distributed entry points only */
+  MAPSQ_E_UNSUPPORTED = 6  /* packed key wider than 64 bits after range compression (KV mode), too
+                              many predicates for the index */
 } mapsq_status;
 
 #define MAPSQ_MAX_COLS 16
@@ -156,7 +158,9 @@ typedef struct {
   uint64_t exchanges;      /* hash exchanges run by mapsq_join_dist / mapsq_query_dist */
   uint64_t exchange_rows;  /* rows this rank stored into OTHER ranks' arenas */
   uint64_t exchange_bytes; /* bytes of those rows (4 B per column) */
-  uint32_t nkernels;
+  uint64_t exchange_recv_rows;  /* rows OTHER ranks stored into this rank's arenas */
+  uint64_t exchange_recv_bytes; /* bytes of those rows */
+  uint32_t nkernels;       /* per-kernel (per-phase) device times and algorithmic bytes: */
   mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
 } mapsq_stats;
 
@@ -354,9 +358,12 @@ mapsq_status mapsq_exchange_layout(int world, int rank, int ncols, const uint64_
  * all-reduce, so the local join range-compresses keys without a min/max pass) and the two
  * barriers around each scatter.  Every call is collective: all ranks call it in the same order.
  * Errors: argument errors are detected before the first collective on every rank alike (same
- * tables' schemas); a rank that fails later (allocation, CUDA, NCCL) returns its status while its
- * peers may stay blocked in the next collective — the caller aborts the job (queries are
- * stateless and are simply re-run).
+ * tables' schemas).  Growing the receive arenas is collective in outcome: if any rank cannot
+ * allocate, export or open an arena, EVERY rank returns MAPSQ_E_CUDA with "CUDA IPC" in the
+ * message after the same collectives (the context stays usable; the fused exchange is disabled
+ * for the communicator and the caller may fall back to another exchange).  A rank that fails
+ * later (allocation, CUDA, NCCL) returns its status while its peers may stay blocked in the next
+ * collective — the caller aborts the job (queries are stateless and are simply re-run).
  *
  * mapsq_dist_unique_id: a fresh 128-byte NCCL unique id (one rank creates it; the caller
  *   broadcasts it, e.g. with torch.distributed).
@@ -376,6 +383,24 @@ mapsq_status mapsq_exchange_layout(int world, int rank, int ncols, const uint64_
 #define MAPSQ_DIST_ID_BYTES 128
 mapsq_status mapsq_dist_unique_id(void *id128);
 mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int rank, int world);
+/* The same distributed state with the control plane (count matrix all-gather, bounds max-reduce,
+ * arena-handle all-gather, barriers) carried by caller-supplied blocking collectives over HOST
+ * buffers instead of NCCL — e.g. torch.distributed's gloo backend.  The data plane is unchanged
+ * (the fused scatter kernel stores rows into the peers' CUDA-IPC arenas), and no kernel ever
+ * waits on another rank: every cross-rank dependency is a host-side collective after a stream
+ * synchronisation.  This is also how several rank processes can share one GPU (each rank maps
+ * the others' arenas through CUDA IPC), which NCCL refuses.  Each callback returns 0 on success:
+ *   allgather(user, send, recv, bytes): recv[r * bytes ..] = rank r's `send` (bytes each);
+ *   allreduce_max_u32(user, buf, n): buf[i] = max over ranks of buf[i], in place;
+ *   barrier(user). */
+typedef struct {
+  int (*allgather)(void *user, const void *send, void *recv, size_t bytes);
+  int (*allreduce_max_u32)(void *user, uint32_t *buf, size_t n);
+  int (*barrier)(void *user);
+  void *user;
+} mapsq_collectives;
+mapsq_status mapsq_dist_init_host(mapsq_ctx *ctx, const mapsq_collectives *coll, int rank,
+                                  int world);
 mapsq_status mapsq_join_dist(mapsq_ctx *ctx, const mapsq_table *tp1_shard,
                              const mapsq_table *tp2_shard, mapsq_table *rs_shard, void *stream);
 mapsq_status mapsq_query_dist(mapsq_ctx *ctx, const mapsq_triples *shard,

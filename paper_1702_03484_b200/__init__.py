@@ -24,7 +24,7 @@ PATH_P64, PATH_KV, PATH_RESIDUAL, PATH_HASH = 0, 1, 2, 3
 OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
-          5: "E_UNSUPPORTED", 6: "E_NCCL"}
+          5: "E_NCCL", 6: "E_UNSUPPORTED"}
 DIST_ID_BYTES = 128
 
 
@@ -78,7 +78,21 @@ class _Stats(ctypes.Structure):
                 ("last_groups", ctypes.c_uint64), ("last_filtered", ctypes.c_uint64),
                 ("filter_accesses", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
                 ("exchange_rows", ctypes.c_uint64), ("exchange_bytes", ctypes.c_uint64),
+                ("exchange_recv_rows", ctypes.c_uint64), ("exchange_recv_bytes", ctypes.c_uint64),
                 ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
+
+
+# mapsq_collectives (include/mapsq.h): host-buffer control-plane callbacks
+_AG_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                          ctypes.c_size_t)
+_AR_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
+                          ctypes.c_size_t)
+_BAR_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+
+
+class _Collectives(ctypes.Structure):
+    _fields_ = [("allgather", _AG_FN), ("allreduce_max_u32", _AR_FN), ("barrier", _BAR_FN),
+                ("user", ctypes.c_void_p)]
 
 
 _lib = None
@@ -141,6 +155,8 @@ def lib():
                                            ctypes.POINTER(u64), ctypes.POINTER(u64)]),
             "mapsq_dist_unique_id": (st, [ctypes.c_char_p]),
             "mapsq_dist_init": (st, [vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+            "mapsq_dist_init_host": (st, [vp, ctypes.POINTER(_Collectives), ctypes.c_int,
+                                          ctypes.c_int]),
             "mapsq_join_dist": (st, [vp, PT, PT, PT, vp]),
             "mapsq_query_dist": (st, [vp, ctypes.POINTER(_Triples), PP, ctypes.c_int,
                                       ctypes.POINTER(i32), ctypes.c_int, PT, vp]),
@@ -588,6 +604,48 @@ class Context:
         src = 0 if group is None else dist.get_global_rank(group, 0)
         dist.broadcast_object_list(obj, src=src, group=group)
         self._check(lib().mapsq_dist_init(self.handle, obj[0], rank, world))
+        self.dist_rank, self.dist_world = rank, world
+
+    def dist_init_host(self, group=None):
+        """Join the ranks of ``group`` with the control plane carried by torch.distributed itself
+        (e.g. the gloo backend) instead of NCCL: mapsq_dist_init_host with host-buffer callbacks
+        (argument marshalling only; the exchange, arenas and joins are the library's).  This is
+        how several rank processes can share one GPU.  Collective; once per context."""
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def allgather(_user, send, recv, nbytes):
+            try:
+                src = torch.from_numpy(np.ctypeslib.as_array(
+                    ctypes.cast(send, ctypes.POINTER(ctypes.c_uint8)), shape=(nbytes,)).copy())
+                out = torch.empty(world * nbytes, dtype=torch.uint8)
+                dist.all_gather_into_tensor(out, src, group=group)
+                ctypes.memmove(recv, out.numpy().ctypes.data, world * nbytes)
+                return 0
+            except Exception:  # noqa: BLE001 (reported to the library as a failed collective)
+                return 1
+
+        def allreduce_max(_user, buf, n):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(n,))
+                t = torch.from_numpy(arr.astype(np.int64))
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                arr[:] = t.numpy().astype(np.uint32)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def barrier(_user):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._coll = _Collectives(_AG_FN(allgather), _AR_FN(allreduce_max), _BAR_FN(barrier), None)
+        self._check(lib().mapsq_dist_init_host(self.handle, ctypes.byref(self._coll), rank, world))
         self.dist_rank, self.dist_world = rank, world
 
     def join_dist(self, tp1: DeviceTable, tp2: DeviceTable, stream=None) -> DeviceTable:

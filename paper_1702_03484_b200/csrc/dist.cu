@@ -117,12 +117,14 @@ struct Arena {
 };
 
 struct DistState {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;       // NCCL control plane (mapsq_dist_init), or
+  bool host = false;               // caller-supplied host collectives (mapsq_dist_init_host)
+  mapsq_collectives coll{};
   int rank = 0, world = 1;
-  // device staging for the collectives: count matrix | handle records | bounds | barrier word
-  uint64_t *dmat = nullptr;
-  unsigned char *dhandles = nullptr;
-  uint32_t *dbounds = nullptr;
+  bool ipc_broken = false;         // a peer mapping failed on some rank: no fused exchange
+  // device staging of the NCCL collectives, and the barrier word
+  void *dstage = nullptr;
+  size_t stage_bytes = 0;
   uint64_t *dbar = nullptr;
   void *dbuf = nullptr;
   Arena slot[2];
@@ -138,7 +140,7 @@ void dist_free(mapsq_ctx *ctx) {
     if (a.own) cudaFree(a.own);
   }
   if (d->dbuf) cudaFree(d->dbuf);
-  if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+  if (!d->host && d->comm && nccl().ok) nccl().CommDestroy(d->comm);
   delete d;
   ctx->dist = nullptr;
 }
@@ -147,10 +149,52 @@ void dist_free(mapsq_ctx *ctx) {
 
 namespace {
 
-// Blocking barrier over the communicator: everything this rank enqueued on `s` has completed and
-// so has every other rank's work before its matching barrier.
+// ---- control-plane collectives on HOST buffers (blocking): NCCL through the device staging
+// buffer, or the caller's callbacks.  Every rank calls them in the same order.
+mapsq_status coll_allgather(mapsq_ctx *ctx, DistState *d, const void *send, void *recv,
+                            size_t bytes, cudaStream_t s) {
+  if (d->host) {
+    CK(cudaStreamSynchronize(s));
+    if (d->coll.allgather(d->coll.user, send, recv, bytes))
+      return set_error(ctx, MAPSQ_E_NCCL, "host allgather callback failed");
+    return MAPSQ_OK;
+  }
+  if (bytes * d->world > d->stage_bytes)
+    return set_error(ctx, MAPSQ_E_INVALID, "internal: collective larger than the staging buffer");
+  unsigned char *st = static_cast<unsigned char *>(d->dstage);
+  CK(cudaMemcpyAsync(st + bytes * d->rank, send, bytes, cudaMemcpyHostToDevice, s));
+  NC(nccl().AllGather(st + bytes * d->rank, st, bytes, ncclUint8, d->comm, s));
+  CK(cudaMemcpyAsync(recv, st, bytes * d->world, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return MAPSQ_OK;
+}
+
+mapsq_status coll_allreduce_max(mapsq_ctx *ctx, DistState *d, uint32_t *buf, size_t n,
+                                cudaStream_t s) {
+  if (d->host) {
+    CK(cudaStreamSynchronize(s));
+    if (d->coll.allreduce_max_u32(d->coll.user, buf, n))
+      return set_error(ctx, MAPSQ_E_NCCL, "host allreduce callback failed");
+    return MAPSQ_OK;
+  }
+  if (4 * n > d->stage_bytes)
+    return set_error(ctx, MAPSQ_E_INVALID, "internal: collective larger than the staging buffer");
+  uint32_t *st = static_cast<uint32_t *>(d->dstage);
+  CK(cudaMemcpyAsync(st, buf, 4 * n, cudaMemcpyHostToDevice, s));
+  NC(nccl().AllReduce(st, st, n, ncclUint32, ncclMax, d->comm, s));
+  CK(cudaMemcpyAsync(buf, st, 4 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return MAPSQ_OK;
+}
+
+// Blocking barrier: everything this rank enqueued on `s` has completed and so has every other
+// rank's work before its matching barrier.
 mapsq_status barrier(mapsq_ctx *ctx, DistState *d, cudaStream_t s) {
   CK(cudaStreamSynchronize(s));
+  if (d->host) {
+    if (d->coll.barrier(d->coll.user)) return set_error(ctx, MAPSQ_E_NCCL, "host barrier callback failed");
+    return MAPSQ_OK;
+  }
   NC(nccl().AllReduce(d->dbar, d->dbar, 1, ncclUint64, ncclSum, d->comm, s));
   CK(cudaStreamSynchronize(s));
   return MAPSQ_OK;
@@ -158,54 +202,103 @@ mapsq_status barrier(mapsq_ctx *ctx, DistState *d, cudaStream_t s) {
 
 // Grow the arenas of `slot` that are smaller than need[] (collective; every rank passes the same
 // need[]).  New allocations are exported, their handles all-gathered and opened by the peers; a
-// replaced allocation is freed after a barrier, when no peer maps it any more.
+// replaced allocation is freed after a barrier, when no peer maps it any more.  The outcome is
+// collective: a failure to allocate, export or open on ANY rank makes EVERY rank return the same
+// MAPSQ_E_CUDA "CUDA IPC" error (after the same collectives), so no rank is left waiting in a
+// collective its peers never enter; the fused exchange is then disabled on every rank.
 mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t *need,
                           cudaStream_t s) {
   Arena &a = d->slot[slot];
   bool any = false;
   for (int r = 0; r < d->world; r++) any |= need[r] > a.cap[r];
   if (!any) return MAPSQ_OK;
+  // record: {u64 state (0 unchanged, 1 grew, 2 failed), u64 bytes, 64 B cudaIpcMemHandle_t}
   unsigned char rec[kHandleRec] = {};
-  void *old = nullptr;
+  std::string why;
+  void *p = nullptr;
   const bool grow = need[d->rank] > a.cap[d->rank];
-  uint64_t nbytes = a.cap[d->rank];
+  uint64_t nbytes = a.cap[d->rank], state = 0;
   if (grow) {
     nbytes = std::max<uint64_t>(1ull << 20, need[d->rank] + need[d->rank] / 4);
     nbytes = (nbytes + (2ull << 20) - 1) & ~((2ull << 20) - 1);
-    void *p = nullptr;
-    CK(cudaMalloc(&p, nbytes));
     cudaIpcMemHandle_t h;
-    CKIPC(cudaIpcGetMemHandle(&h, p));
-    const uint64_t one = 1;
-    std::memcpy(rec, &one, 8);
-    std::memcpy(rec + 16, &h, 64);
-    old = a.own;
-    a.own = p;
+    cudaError_t e = cudaMalloc(&p, nbytes);
+    if (e == cudaSuccess) {
+      e = cudaIpcGetMemHandle(&h, p);
+      if (e != cudaSuccess) {
+        cudaFree(p);
+        p = nullptr;
+      }
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      why = std::string("cudaMalloc/cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+      state = 2;
+    } else {
+      state = 1;
+      std::memcpy(rec + 16, &h, 64);
+    }
   }
+  std::memcpy(rec, &state, 8);
   std::memcpy(rec + 8, &nbytes, 8);
   const int W = d->world;
-  TRY(api_ensure_pinned(ctx, (kHandleRec * W + 7) / 8));
-  unsigned char *hp = reinterpret_cast<unsigned char *>(ctx->pinned);
-  std::memcpy(hp, rec, kHandleRec);
-  CK(cudaMemcpyAsync(d->dhandles + kHandleRec * d->rank, hp, kHandleRec, cudaMemcpyHostToDevice, s));
-  NC(nccl().AllGather(d->dhandles + kHandleRec * d->rank, d->dhandles, kHandleRec, ncclUint8,
-                      d->comm, s));
-  CK(cudaMemcpyAsync(hp, d->dhandles, kHandleRec * W, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  std::vector<unsigned char> all((size_t)kHandleRec * W);
+  TRY(coll_allgather(ctx, d, rec, all.data(), kHandleRec, s));
+  int failed_rank = -1;
+  for (int r = 0; r < W && failed_rank < 0; r++) {
+    uint64_t st;
+    std::memcpy(&st, all.data() + kHandleRec * r, 8);
+    if (st == 2) failed_rank = r;
+  }
+  if (failed_rank >= 0) {  // every rank sees it: nothing was opened, nothing changes
+    if (p) cudaFree(p);
+    d->ipc_broken = true;
+    return set_error(ctx, MAPSQ_E_CUDA,
+                     "CUDA IPC: arena export failed on rank " + std::to_string(failed_rank) +
+                         (why.empty() ? std::string() : ": " + why));
+  }
+  // open the peers' new arenas; the local outcome is then agreed on (max of "failed")
+  void *opened[kDistMaxRanks] = {};
+  uint32_t bad = 0;
+  for (int r = 0; r < W && !bad; r++) {
+    if (r == d->rank) continue;
+    uint64_t st;
+    std::memcpy(&st, all.data() + kHandleRec * r, 8);
+    if (st != 1) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, all.data() + kHandleRec * r + 16, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(&opened[r], h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      opened[r] = nullptr;
+      why = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+      bad = 1;
+    }
+  }
+  uint32_t agree = bad;
+  TRY(coll_allreduce_max(ctx, d, &agree, 1, s));
+  if (agree) {  // some rank could not map a peer: undo this round everywhere
+    for (int r = 0; r < W; r++)
+      if (opened[r]) cudaIpcCloseMemHandle(opened[r]);
+    if (p) cudaFree(p);
+    d->ipc_broken = true;
+    return set_error(ctx, MAPSQ_E_CUDA,
+                     "CUDA IPC: a rank could not open a peer's arena" +
+                         (why.empty() ? std::string() : " (this rank: " + why + ")"));
+  }
+  void *old = nullptr;
   for (int r = 0; r < W; r++) {
-    const unsigned char *q = hp + kHandleRec * r;
-    uint64_t grew, nb;
-    std::memcpy(&grew, q, 8);
-    std::memcpy(&nb, q + 8, 8);
-    if (!grew) continue;
+    uint64_t st, nb;
+    std::memcpy(&st, all.data() + kHandleRec * r, 8);
+    std::memcpy(&nb, all.data() + kHandleRec * r + 8, 8);
+    if (st != 1) continue;
     if (r == d->rank) {
-      a.ptr[r] = a.own;
+      old = a.own;
+      a.own = p;
+      a.ptr[r] = p;
     } else {
-      if (a.ptr[r]) CKIPC(cudaIpcCloseMemHandle(a.ptr[r]));
-      a.ptr[r] = nullptr;
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, q + 16, 64);
-      CKIPC(cudaIpcOpenMemHandle(&a.ptr[r], h, cudaIpcMemLazyEnablePeerAccess));
+      if (a.ptr[r]) cudaIpcCloseMemHandle(a.ptr[r]);
+      a.ptr[r] = opened[r];
     }
     a.cap[r] = nb;
   }
@@ -229,29 +322,21 @@ mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
     ~Guard() { mapsq_partition_state_free(c, p); }
   } guard{ctx, st};
 
-  // (2) count matrix and (5) bounds in one staging round trip: ~lo and hi under one max-reduce,
-  // plus a flag word set by a rank whose non-empty input carries no bounds
+  // (2) count matrix (all-gather) and (5) bounds: ~lo and hi under one max-reduce, plus a flag
+  // word set by a rank whose non-empty input carries no bounds
+  if (d->ipc_broken)
+    return set_error(ctx, MAPSQ_E_CUDA, "CUDA IPC: the fused exchange is disabled on this communicator");
   const uint32_t nb = 2 * nc + 1;
-  TRY(api_ensure_pinned(ctx, (size_t)W * W + nb));
-  uint64_t *pin = ctx->pinned;
-  for (int q = 0; q < W; q++) pin[q] = counts[q];
-  uint32_t *pb = reinterpret_cast<uint32_t *>(pin + W);
+  std::vector<uint64_t> mat((size_t)W * W);
+  TRY(coll_allgather(ctx, d, counts, mat.data(), 8ull * W, s));
+  std::vector<uint32_t> bnd(nb);
   const bool has_b = (in->flags & MAPSQ_TABLE_BOUNDS) != 0;
   for (uint32_t c = 0; c < nc; c++) {
-    pb[c] = has_b && in->nrows ? ~in->lo[c] : 0u;  // empty input: the identity of max
-    pb[nc + c] = has_b && in->nrows ? in->hi[c] : 0u;
+    bnd[c] = has_b && in->nrows ? ~in->lo[c] : 0u;  // empty input: the identity of max
+    bnd[nc + c] = has_b && in->nrows ? in->hi[c] : 0u;
   }
-  pb[2 * nc] = (!has_b && in->nrows) ? 1u : 0u;
-  CK(cudaMemcpyAsync(d->dmat + (size_t)R * W, pin, 8ull * W, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d->dbounds, pb, 4ull * nb, cudaMemcpyHostToDevice, s));
-  NC(nccl().AllGather(d->dmat + (size_t)R * W, d->dmat, W, ncclUint64, d->comm, s));
-  NC(nccl().AllReduce(d->dbounds, d->dbounds, nb, ncclUint32, ncclMax, d->comm, s));
-  CK(cudaMemcpyAsync(pin, d->dmat, 8ull * W * W, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(pin + (size_t)W * W, d->dbounds, 4ull * nb, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const std::vector<uint64_t> mat(pin, pin + (size_t)W * W);
-  const uint32_t *rb = reinterpret_cast<const uint32_t *>(pin + (size_t)W * W);
-  const std::vector<uint32_t> bnd(rb, rb + nb);
+  bnd[2 * nc] = (!has_b && in->nrows) ? 1u : 0u;
+  TRY(coll_allreduce_max(ctx, d, bnd.data(), nb, s));
 
   uint64_t dest_row[kDistMaxRanks], recv[kDistMaxRanks], need[kDistMaxRanks];
   TRY(mapsq_exchange_layout(W, R, (int)nc, mat.data(), dest_row, recv, need));
@@ -271,6 +356,8 @@ mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
     if (q != R) {
       ctx->counters.exchange_rows += counts[q];
       ctx->counters.exchange_bytes += 4ull * nc * counts[q];
+      ctx->counters.exchange_recv_rows += mat[(size_t)q * W + R];
+      ctx->counters.exchange_recv_bytes += 4ull * nc * mat[(size_t)q * W + R];
     }
   ctx->counters.exchanges++;
 
@@ -378,29 +465,35 @@ MAPSQ_API mapsq_status mapsq_dist_unique_id(void *id128) {
   return MAPSQ_OK;
 }
 
+static mapsq_status dist_alloc(mapsq_ctx *ctx, int rank, int world, DistState **out) {
+  auto *d = new (std::nothrow) DistState();
+  if (!d) return set_error(ctx, MAPSQ_E_NOMEM, "host allocation failed");
+  d->rank = rank;
+  d->world = world;
+  // staging: the largest collective is the handle all-gather (world x kHandleRec bytes) or the
+  // count matrix (world x world x 8 bytes)
+  d->stage_bytes = std::max<size_t>(kHandleRec * world, 8ull * world * world) + 8ull * MAPSQ_MAX_COLS + 64;
+  d->stage_bytes = (d->stage_bytes + 255) & ~size_t(255);
+  cudaError_t e = cudaMalloc(&d->dbuf, d->stage_bytes + 256);
+  if (e != cudaSuccess) {
+    delete d;
+    return cuda_check(ctx, e, "cudaMalloc(dist staging)");
+  }
+  d->dstage = d->dbuf;
+  d->dbar = reinterpret_cast<uint64_t *>(static_cast<char *>(d->dbuf) + d->stage_bytes);
+  cudaMemset(d->dbuf, 0, d->stage_bytes + 256);
+  *out = d;
+  return MAPSQ_OK;
+}
+
 MAPSQ_API mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int rank, int world) {
   TRY(api_enter(ctx));
   if (!id128 || world < 1 || world > kDistMaxRanks || rank < 0 || rank >= world)
     return set_error(ctx, MAPSQ_E_INVALID, "bad mapsq_dist_init arguments");
   if (ctx->dist) return set_error(ctx, MAPSQ_E_INVALID, "distributed state already initialised");
   if (!nccl().ok) return set_error(ctx, MAPSQ_E_NCCL, nccl().why);
-  auto *d = new (std::nothrow) DistState();
-  if (!d) return set_error(ctx, MAPSQ_E_NOMEM, "host allocation failed");
-  d->rank = rank;
-  d->world = world;
-  const size_t mat = 8ull * world * world, hnd = kHandleRec * world,
-               bnd = 8ull * MAPSQ_MAX_COLS + 16, bar = 16;
-  cudaError_t e = cudaMalloc(&d->dbuf, mat + hnd + bnd + bar + 64);
-  if (e != cudaSuccess) {
-    delete d;
-    return cuda_check(ctx, e, "cudaMalloc(dist staging)");
-  }
-  char *b = static_cast<char *>(d->dbuf);
-  d->dmat = reinterpret_cast<uint64_t *>(b);
-  d->dhandles = reinterpret_cast<unsigned char *>(b + mat);
-  d->dbounds = reinterpret_cast<uint32_t *>(b + ((mat + hnd + 15) & ~size_t(15)));
-  d->dbar = reinterpret_cast<uint64_t *>(b + ((mat + hnd + 15) & ~size_t(15)) + bnd);
-  cudaMemset(d->dbuf, 0, mat + hnd + bnd + bar + 64);
+  DistState *d = nullptr;
+  TRY(dist_alloc(ctx, rank, world, &d));
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof id);
   ncclResult_t r = nccl().CommInitRank(&d->comm, world, id, rank);
@@ -409,6 +502,21 @@ MAPSQ_API mapsq_status mapsq_dist_init(mapsq_ctx *ctx, const void *id128, int ra
     delete d;
     return set_error(ctx, MAPSQ_E_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
   }
+  ctx->dist = d;
+  return MAPSQ_OK;
+}
+
+MAPSQ_API mapsq_status mapsq_dist_init_host(mapsq_ctx *ctx, const mapsq_collectives *coll,
+                                            int rank, int world) {
+  TRY(api_enter(ctx));
+  if (!coll || !coll->allgather || !coll->allreduce_max_u32 || !coll->barrier || world < 1 ||
+      world > kDistMaxRanks || rank < 0 || rank >= world)
+    return set_error(ctx, MAPSQ_E_INVALID, "bad mapsq_dist_init_host arguments");
+  if (ctx->dist) return set_error(ctx, MAPSQ_E_INVALID, "distributed state already initialised");
+  DistState *d = nullptr;
+  TRY(dist_alloc(ctx, rank, world, &d));
+  d->host = true;
+  d->coll = *coll;
   ctx->dist = d;
   return MAPSQ_OK;
 }
