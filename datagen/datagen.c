@@ -322,7 +322,13 @@ uint64_t lubm_generate(uint64_t seed, uint32_t n_univ_total, uint32_t u_lo, uint
   return t;
 }
 
-/* ---------------- Zipf(s) by rejection-inversion (Hörmann & Derflinger 1996) ---------------- */
+/* ---------------- Zipf(s) by rejection-inversion (Hörmann & Derflinger 1996) ----------------
+ * W. Hörmann, G. Derflinger, "Rejection-inversion to generate variates from monotone discrete
+ * distributions", ACM TOMACS 6(3), 1996.  The formulation below (the helper1/helper2 series for
+ * log1p(x)/x and expm1(x)/x near 0, H/H^-1 over [1.5, N + 0.5], the squeeze constant
+ * s = 2 - H^-1(H(2.5) - h(2)) and the acceptance test) follows the structure of Apache Commons
+ * Math's RejectionInversionZipfSampler (Apache License 2.0), re-implemented here in C with a
+ * counter-based uniform per row so any row range is generated independently. */
 static double zh(double x, double s) { return exp(-s * log(x)); }
 static double zhelper1(double x) { return fabs(x) > 1e-8 ? log1p(x) / x : 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x)); }
 static double zhelper2(double x) { return fabs(x) > 1e-8 ? expm1(x) / x : 1.0 + x * 0.5 * (1.0 + x * (1.0 / 3.0) * (1.0 + 0.25 * x)); }
