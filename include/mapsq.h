@@ -320,6 +320,13 @@ typedef struct mapsq_partition_state mapsq_partition_state;
 mapsq_status mapsq_partition_plan(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
                                   int nkey, int nparts, uint64_t *counts_host,
                                   mapsq_partition_state **state, void *stream);
+/* The same with a row mask (device, ceil(nrows / 32) words): row r takes part iff bit (r & 31) of
+ * row_mask[r >> 5] is set; dropped rows are neither counted nor scattered (the distributed
+ * semi-join pre-filter exchanges only rows whose key may occur on the other side).  NULL = all. */
+mapsq_status mapsq_partition_plan_masked(mapsq_ctx *ctx, const mapsq_table *in,
+                                         const int32_t *key_vars, int nkey, int nparts,
+                                         const uint32_t *row_mask, uint64_t *counts_host,
+                                         mapsq_partition_state **state, void *stream);
 mapsq_status mapsq_partition_scatter(mapsq_ctx *ctx, mapsq_partition_state *state,
                                      const uint64_t *dest_row, uint32_t *const *dest_cols,
                                      void *stream);

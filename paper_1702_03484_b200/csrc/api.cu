@@ -1945,6 +1945,14 @@ MAPSQ_API mapsq_status mapsq_partition_plan(mapsq_ctx *ctx, const mapsq_table *i
                                             const int32_t *key_vars, int nkey, int nparts,
                                             uint64_t *counts_host, mapsq_partition_state **state,
                                             void *stream) {
+  return mapsq_partition_plan_masked(ctx, in, key_vars, nkey, nparts, nullptr, counts_host, state,
+                                     stream);
+}
+
+MAPSQ_API mapsq_status mapsq_partition_plan_masked(mapsq_ctx *ctx, const mapsq_table *in,
+                                                   const int32_t *key_vars, int nkey, int nparts,
+                                                   const uint32_t *row_mask, uint64_t *counts_host,
+                                                   mapsq_partition_state **state, void *stream) {
   TRY(enter(ctx));
   if (!state || !counts_host || !key_vars) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
   *state = nullptr;
@@ -1970,6 +1978,7 @@ MAPSQ_API mapsq_status mapsq_partition_plan(mapsq_ctx *ctx, const mapsq_table *i
   pa.ncols = in->ncols;
   pa.n = in->nrows;
   pa.nparts = (uint32_t)nparts;
+  pa.mask = row_mask;
   for (uint32_t c = 0; c < in->ncols; c++) pa.in[c] = in->col[c];
   for (int d = 0; d < nparts; d++) counts_host[d] = st->counts[d] = 0;
   if (in->nrows == 0) {

@@ -127,14 +127,15 @@ struct DistState {
   size_t stage_bytes = 0;
   uint64_t *dbar = nullptr;
   void *dbuf = nullptr;
-  Arena slot[2];
+  Arena slot[3];              // receive arenas of the two join sides; [2]: pre-filter bitmaps
+  uint64_t *dpeers = nullptr; // device copy of slot[2]'s per-rank bitmap pointers (peer_or)
 };
 
 void dist_free(mapsq_ctx *ctx) {
   DistState *d = ctx->dist;
   if (!d) return;
   cudaDeviceSynchronize();
-  for (Arena &a : d->slot) {
+  for (Arena &a : d->slot) {  // (all three slots)
     for (int r = 0; r < d->world; r++)
       if (r != d->rank && a.ptr[r]) cudaIpcCloseMemHandle(a.ptr[r]);
     if (a.own) cudaFree(a.own);
@@ -310,12 +311,13 @@ mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t
 // Hash-exchange `in` on key_vars into arena `slot`: *out is a view (owner NULL) of this rank's
 // received rows, grouped by source rank, with bounds valid over every rank's input.
 mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
-                      const std::vector<int32_t> &key, int slot, mapsq_table *out, cudaStream_t s) {
+                      const std::vector<int32_t> &key, int slot, const uint32_t *mask,
+                      mapsq_table *out, cudaStream_t s) {
   const int W = d->world, R = d->rank;
   const uint32_t nc = in->ncols;
   uint64_t counts[kDistMaxRanks];
   mapsq_partition_state *st = nullptr;
-  TRY(mapsq_partition_plan(ctx, in, key.data(), (int)key.size(), W, counts, &st, s));
+  TRY(mapsq_partition_plan_masked(ctx, in, key.data(), (int)key.size(), W, mask, counts, &st, s));
   struct Guard {
     mapsq_ctx *c;
     mapsq_partition_state *p;
@@ -391,8 +393,128 @@ std::vector<int32_t> shared_key(const mapsq_table *a, const mapsq_table *b) {
   return k;
 }
 
-// Distributed join step: exchange both sides (tp1 skipped when it is already partitioned on this
-// key), local Algorithm-1 join.  *part_key receives the key RS is partitioned on.
+// Distributed semi-join pre-filter (reading R18: a row whose key occurs on
+// neither rank of the other side produces nothing in ReduceDuplicate).
+// The key-presence bitmap of a side is the OR over ranks of the local bitmaps — every rank builds
+// its own from its rows, then each rank OR-reduces its slice of all peers' bitmaps over the CUDA-IPC
+// mappings and stores the result back into all of them (peer_or: reduce-scatter + all-gather in
+// one NVLink kernel).  Blocked Bloom bitmaps over the key_hash chain of the RAW key values (the
+// same function on every rank).  Round: S = the globally smaller side; global bm_S; the larger
+// side's rows probe it (survivor mask) and set the global bm_L; S's rows probe bm_L.  Only
+// survivors are exchanged (mapsq_partition_plan_masked).  *mask_a / *mask_b stay NULL when the
+// filter does not run (off, small join, or a 1/16 sample of L says >= 90% would survive).
+mapsq_status prefilter(mapsq_ctx *ctx, DistState *d, const mapsq_table *a, const mapsq_table *b,
+                       const std::vector<int32_t> &key, Scratch &sc, uint32_t **mask_a,
+                       uint32_t **mask_b, cudaStream_t s) {
+  *mask_a = *mask_b = nullptr;
+  const int W = d->world;
+  // one rank moves nothing over NVLink: the local join's own filter does the same job; auto
+  // mode therefore pre-filters only across ranks (ON forces it, for testing)
+  if (ctx->semijoin == MAPSQ_SEMIJOIN_OFF || (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && W == 1))
+    return MAPSQ_OK;
+  uint64_t mine[2] = {a->nrows, b->nrows};
+  std::vector<uint64_t> all(2 * (size_t)W);
+  TRY(coll_allgather(ctx, d, mine, all.data(), sizeof mine, s));
+  uint64_t N1 = 0, N2 = 0;
+  for (int r = 0; r < W; r++) {
+    N1 += all[2 * r];
+    N2 += all[2 * r + 1];
+  }
+  if (N1 == 0 || N2 == 0) return MAPSQ_OK;
+  if (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && N1 + N2 < kSemijoinMinRows) return MAPSQ_OK;
+  PackArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  for (int32_t v : key) {
+    int ca = -1, cb = -1;
+    for (uint32_t c = 0; c < a->ncols; c++)
+      if (a->var[c] == v) ca = (int)c;
+    for (uint32_t c = 0; c < b->ncols; c++)
+      if (b->var[c] == v) cb = (int)c;
+    pa.key1[pa.nkey] = a->col[ca];
+    pa.key2[pa.nkey] = b->col[cb];
+    pa.nkey++;
+  }
+  pa.n1 = a->nrows;
+  pa.n2 = b->nrows;
+  pa.hash = 1;
+  const bool s_is_b = N2 <= N1;
+  const uint64_t NS = s_is_b ? N2 : N1;
+  const uint32_t bbits = std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, bits_for(8 * NS)));
+  const uint64_t bm_bytes = (1ull << bbits) / 8, bm_max = (1ull << kSemijoinBits) / 8;
+  // the bitmap arena (two bitmaps of the largest size) is exported once and mapped by every peer
+  uint64_t need[kDistMaxRanks];
+  for (int r = 0; r < W; r++) need[r] = 2 * bm_max;
+  TRY(ensure_arena(ctx, d, 2, need, s));
+  Arena &ar = d->slot[2];
+  uint64_t host_peers[2 * kDistMaxRanks];
+  for (int r = 0; r < W; r++) {
+    host_peers[r] = (uint64_t)(uintptr_t)ar.ptr[r];
+    host_peers[W + r] = (uint64_t)(uintptr_t)ar.ptr[r] + bm_max;
+  }
+  CK(cudaMemcpyAsync(d->dpeers, host_peers, 8ull * 2 * W, cudaMemcpyHostToDevice, s));
+  unsigned char *bmS = static_cast<unsigned char *>(ar.own), *bmL = bmS + bm_max;
+  auto *peersS = reinterpret_cast<unsigned long long *const *>(d->dpeers);
+  auto *peersL = reinterpret_cast<unsigned long long *const *>(d->dpeers + W);
+  unsigned long long *sample = sc.get<unsigned long long>(2);
+  uint32_t *ma = sc.get<uint32_t>(a->nrows / 32 + 2), *mb = sc.get<uint32_t>(b->nrows / 32 + 2);
+  if (!sample || !ma || !mb) return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed");
+  CK(cudaMemsetAsync(bmS, 0, bm_bytes, s));
+  CK(cudaMemsetAsync(bmL, 0, bm_bytes, s));
+  CK(cudaMemsetAsync(sample, 0, 16, s));
+  const uint64_t nS = s_is_b ? b->nrows : a->nrows, nL = s_is_b ? a->nrows : b->nrows;
+  {
+    KTimer kt(ctx, s, "dist_filter_build", 4ull * pa.nkey * nS);
+    launch_sj_chain_build(pa, s_is_b, bmS, bbits, s);
+    CK(cudaGetLastError());
+  }
+  auto or_reduce = [&](unsigned long long *const *peers) -> mapsq_status {
+    if (W == 1) return MAPSQ_OK;
+    TRY(barrier(ctx, d, s));  // every rank's local bitmap is complete
+    {
+      KTimer kt(ctx, s, "dist_filter_or", 2ull * bm_bytes);
+      launch_peer_or(peers, W, d->rank, bm_bytes / 8, s);
+      CK(cudaGetLastError());
+    }
+    return barrier(ctx, d, s);  // every slice is reduced into every rank's copy
+  };
+  TRY(or_reduce(peersS));
+  {
+    KTimer kt(ctx, s, "dist_filter_sample", 4ull * pa.nkey * (nL / 16));
+    launch_sj_chain_sample(pa, !s_is_b, bmS, bbits, sample, s);
+    CK(cudaGetLastError());
+  }
+  uint64_t smp[2];
+  CK(cudaMemcpyAsync(smp, sample, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<uint64_t> smp_all(2 * (size_t)W);
+  TRY(coll_allgather(ctx, d, smp, smp_all.data(), sizeof smp, s));
+  uint64_t surv = 0, rows = 0;
+  for (int r = 0; r < W; r++) {
+    surv += smp_all[2 * r];
+    rows += smp_all[2 * r + 1];
+  }
+  if (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && rows > 0 && surv * 10 >= rows * 9) return MAPSQ_OK;
+  uint32_t *mL = s_is_b ? ma : mb, *mS = s_is_b ? mb : ma;
+  {
+    KTimer kt(ctx, s, "dist_filter_probe", 4ull * pa.nkey * nL + nL / 8);
+    launch_sj_chain_probe(pa, !s_is_b, bmS, bbits, bmL, mL, s);
+    CK(cudaGetLastError());
+  }
+  TRY(or_reduce(peersL));
+  {
+    KTimer kt(ctx, s, "dist_filter_probe", 4ull * pa.nkey * nS + nS / 8);
+    launch_sj_chain_probe(pa, s_is_b, bmL, bbits, nullptr, mS, s);
+    CK(cudaGetLastError());
+  }
+  ctx->counters.filter_accesses += nS + nL / 16 + nL + nS;
+  *mask_a = ma;
+  *mask_b = mb;
+  return MAPSQ_OK;
+}
+
+// Distributed join step: pre-filter, exchange both sides (tp1 skipped when it is already
+// partitioned on this key), local Algorithm-1 join.  *part_key receives the key RS is
+// partitioned on.
 mapsq_status join_dist_step(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_table *b,
                             mapsq_table *rs, cudaStream_t s, std::vector<int32_t> *part_key) {
   DistState *d = ctx->dist;
@@ -401,13 +523,16 @@ mapsq_status join_dist_step(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_ta
   TRY(api_check_table(ctx, b, "tp2"));
   const std::vector<int32_t> key = shared_key(a, b);
   if (key.empty()) return set_error(ctx, MAPSQ_E_NO_SHARED, "join inputs share no variable");
+  Scratch sc(ctx, s);
+  uint32_t *ma = nullptr, *mb = nullptr;
+  TRY(prefilter(ctx, d, a, b, key, sc, &ma, &mb, s));
   mapsq_table ea, eb;
   if (part_key && *part_key == key) {
-    ea = *a;
+    ea = *a;  // already partitioned on the key: stays (the local join filters it)
   } else {
-    TRY(exchange(ctx, d, a, key, 0, &ea, s));
+    TRY(exchange(ctx, d, a, key, 0, ma, &ea, s));
   }
-  TRY(exchange(ctx, d, b, key, 1, &eb, s));
+  TRY(exchange(ctx, d, b, key, 1, mb, &eb, s));
   TRY(join_tables(ctx, &ea, &eb, rs, s));
   if (part_key) *part_key = key;
   return MAPSQ_OK;
@@ -474,14 +599,16 @@ static mapsq_status dist_alloc(mapsq_ctx *ctx, int rank, int world, DistState **
   // count matrix (world x world x 8 bytes)
   d->stage_bytes = std::max<size_t>(kHandleRec * world, 8ull * world * world) + 8ull * MAPSQ_MAX_COLS + 64;
   d->stage_bytes = (d->stage_bytes + 255) & ~size_t(255);
-  cudaError_t e = cudaMalloc(&d->dbuf, d->stage_bytes + 256);
+  static_assert(64 + 8 * kDistMaxRanks <= 1024, "dist staging tail");
+  cudaError_t e = cudaMalloc(&d->dbuf, d->stage_bytes + 1024);
   if (e != cudaSuccess) {
     delete d;
     return cuda_check(ctx, e, "cudaMalloc(dist staging)");
   }
   d->dstage = d->dbuf;
   d->dbar = reinterpret_cast<uint64_t *>(static_cast<char *>(d->dbuf) + d->stage_bytes);
-  cudaMemset(d->dbuf, 0, d->stage_bytes + 256);
+  d->dpeers = reinterpret_cast<uint64_t *>(static_cast<char *>(d->dbuf) + d->stage_bytes + 64);
+  cudaMemset(d->dbuf, 0, d->stage_bytes + 1024);
   *out = d;
   return MAPSQ_OK;
 }

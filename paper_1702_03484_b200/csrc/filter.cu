@@ -246,11 +246,19 @@ __device__ __forceinline__ void cblock(uint64_t h, uint32_t bbits, uint32_t &idx
 }
 
 // set (idx, m) for the rows whose keep bit is set (fire-and-forget RED.OR: keys mostly distinct);
-// a lane whose left neighbour sets the same block bits skips
+// a lane whose left neighbour sets the same block bits skips.  TEST: read the word first and skip
+// bits already set (skewed keys: a hot key's word would otherwise serialise its atomics).
+template <bool TEST = false>
 __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_t idx[kFItems],
                                            const uint64_t m[kFItems], uint32_t keep,
                                            uint32_t lane) {
   const uint64_t pol = bm_policy();
+  uint64_t cur[TEST ? kFItems : 1];
+  if (TEST) {
+#pragma unroll
+    for (int it = 0; it < kFItems; it++)
+      cur[TEST ? it : 0] = (keep >> it & 1u) ? ld_bm(bm + idx[it], pol) : 0ull;
+  }
 #pragma unroll
   for (int it = 0; it < kFItems; it++) {
     const uint32_t k = keep >> it & 1u;
@@ -258,7 +266,8 @@ __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_
     const uint64_t mp = __shfl_up_sync(0xffffffffu, m[it], 1);
     const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
     const bool dup = lane > 0 && kp && ip == idx[it] && mp == m[it];
-    if (k && !dup) red_or_bm(bm + idx[it], m[it], pol);
+    const bool have = TEST && (cur[TEST ? it : 0] & m[it]) == m[it];
+    if (k && !dup && !have) red_or_bm(bm + idx[it], m[it], pol);
   }
 }
 
@@ -329,7 +338,7 @@ wfilter_sample_kernel(const SjSeg sd, uint32_t ib, uint64_t seed, uint32_t bbits
 
 // ---- hashed composite keys (PATH_HASH), first round on the key columns: the smaller side's
 // blocked Bloom bitmap from the key_hash chain of its shared columns (load_keys<MODE, false>)
-template <int MODE>
+template <int MODE, bool TEST = false>
 __global__ void __launch_bounds__(kFThreads)
 cfilter_build_kernel(const PackArgs a, const Side sd, uint32_t bbits,
                      unsigned long long *__restrict__ bm) {
@@ -347,7 +356,7 @@ cfilter_build_kernel(const PackArgs a, const Side sd, uint32_t bbits,
       cblock(key[it], bbits, idx[it], m[it]);
       keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
     }
-    set_blocks(bm, idx, m, keep, lane);
+    set_blocks<TEST>(bm, idx, m, keep, lane);
   }
 }
 
@@ -578,6 +587,71 @@ sj_set_words_kernel(const uint64_t *__restrict__ w, const uint64_t *__restrict__
   }
 }
 
+// ---- distributed pre-filter: mask-producing probe over the key_hash chain (cblock bitmaps)
+template <int MODE, bool SET>
+__global__ void __launch_bounds__(kFThreads)
+sj_chain_probe_kernel(const PackArgs a, const Side sd, uint32_t bbits,
+                      const unsigned long long *__restrict__ bm,
+                      unsigned long long *__restrict__ bm_set, uint32_t *__restrict__ mask) {
+  const uint64_t pol = bm_policy();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
+       ws * kFWarpRows < sd.rows; ws += nwarps) {
+    const uint64_t base = ws * kFWarpRows;
+    KeyT<MODE> key[kFItems];
+    load_keys<MODE, false>(a, sd, base, lane, key);
+    uint64_t v[kFItems];
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      uint32_t idx;
+      uint64_t m;
+      cblock(key[it], bbits, idx, m);
+      v[it] = base + (uint64_t)it * 32 + lane < sd.rows ? ld_bm(bm + idx, pol) : 0ull;
+    }
+    uint32_t keep = 0;
+#pragma unroll
+    for (int it = 0; it < kFItems; it++) {
+      uint32_t idx;
+      uint64_t m;
+      cblock(opaque(key[it]), bbits, idx, m);
+      const bool k = (v[it] & m) == m && base + (uint64_t)it * 32 + lane < sd.rows;
+      keep |= (uint32_t)k << it;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      if (lane == 0 && base + (uint64_t)it * 32 < sd.rows) mask[(base >> 5) + it] = bal;
+    }
+    if (SET) {
+      uint32_t idx[kFItems];
+      uint64_t m[kFItems];
+#pragma unroll
+      for (int it = 0; it < kFItems; it++) cblock(key[it], bbits, idx[it], m[it]);
+      set_blocks<true>(bm_set, idx, m, keep, lane);
+    }
+  }
+}
+
+// Every rank reduces its slice of the bitmap words over all peers and writes the OR back to all
+// of them: 16 B vector loads / stores over the NVLink peer mappings.
+__global__ void __launch_bounds__(256)
+peer_or_kernel(unsigned long long *const *__restrict__ peers, int world, uint64_t lo, uint64_t hi) {
+  for (uint64_t w = lo + 2 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x); w < hi;
+       w += 2ull * gridDim.x * blockDim.x) {
+    ulonglong2 v = make_ulonglong2(0, 0);
+    if (w + 1 < hi) {
+      for (int q = 0; q < world; q++) {
+        const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2 *>(peers[q] + w));
+        v.x |= x.x;
+        v.y |= x.y;
+      }
+      for (int q = 0; q < world; q++) *reinterpret_cast<ulonglong2 *>(peers[q] + w) = v;
+    } else {
+      unsigned long long x = 0;
+      for (int q = 0; q < world; q++) x |= __ldcg(peers[q] + w);
+      for (int q = 0; q < world; q++) peers[q][w] = x;
+    }
+  }
+}
+
 Side side_of(const PackArgs &a, bool b) {
   Side sd;
   for (uint32_t c = 0; c < MAPSQ_MAX_COLS; c++)
@@ -696,6 +770,53 @@ void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t
   if (nslices == 0) return;
   sj_gather_kernel<<<grid_for_rows(nslices * kFWarpRows), kFThreads, 0, s>>>(
       stage, cnt, off, nslices, out, hist, bit_lo, dmask);
+}
+
+void launch_sj_chain_build(const PackArgs &a, bool side_b, void *bm, uint32_t bbits, cudaStream_t s) {
+  const Side sd = side_of(a, side_b);
+  if (sd.rows == 0) return;
+  auto *b = reinterpret_cast<unsigned long long *>(bm);
+  // (test before set: the distributed filter also serves skewed single-column keys)
+  if (a.nkey == 2)
+    cfilter_build_kernel<2, true><<<grid_for_rows(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b);
+  else
+    cfilter_build_kernel<3, true><<<grid_for_rows(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b);
+}
+
+void launch_sj_chain_probe(const PackArgs &a, bool side_b, const void *bm, uint32_t bbits,
+                           void *bm_set, uint32_t *mask, cudaStream_t s) {
+  const Side sd = side_of(a, side_b);
+  if (sd.rows == 0) return;
+  const auto *b = reinterpret_cast<const unsigned long long *>(bm);
+  auto *bs = reinterpret_cast<unsigned long long *>(bm_set);
+  const int g = grid_for_rows(sd.rows);
+  if (a.nkey == 2) {
+    if (bs) sj_chain_probe_kernel<2, true><<<g, kFThreads, 0, s>>>(a, sd, bbits, b, bs, mask);
+    else sj_chain_probe_kernel<2, false><<<g, kFThreads, 0, s>>>(a, sd, bbits, b, bs, mask);
+  } else {
+    if (bs) sj_chain_probe_kernel<3, true><<<g, kFThreads, 0, s>>>(a, sd, bbits, b, bs, mask);
+    else sj_chain_probe_kernel<3, false><<<g, kFThreads, 0, s>>>(a, sd, bbits, b, bs, mask);
+  }
+}
+
+void launch_sj_chain_sample(const PackArgs &a, bool side_b, const void *bm, uint32_t bbits,
+                            unsigned long long *sample, cudaStream_t s) {
+  const Side sd = side_of(a, side_b);
+  if (sd.rows == 0) return;
+  const auto *b = reinterpret_cast<const unsigned long long *>(bm);
+  if (a.nkey == 2)
+    cfilter_sample_kernel<2><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, kSampleStride, sample);
+  else
+    cfilter_sample_kernel<3><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, kSampleStride, sample);
+}
+
+void launch_peer_or(unsigned long long *const *peers, int world, int rank, uint64_t words,
+                    cudaStream_t s) {
+  const uint64_t lo = words * rank / world & ~1ull, hi = rank + 1 == world ? words : (words * (rank + 1) / world & ~1ull);
+  if (hi <= lo) return;
+  const uint64_t n2 = (hi - lo + 1) / 2;
+  const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n2, 256), 148 * 8));
+  peer_or_kernel<<<g, 256, 0, s>>>(peers, world, lo, hi);
 }
 
 void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t bbits, void *bm,

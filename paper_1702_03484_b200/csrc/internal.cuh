@@ -423,6 +423,22 @@ void launch_sj_set_words(const uint64_t *w, const uint64_t *count, uint64_t max_
 void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t *off,
                       uint64_t nslices, uint64_t *out, uint32_t *hist, uint32_t bit_lo,
                       uint32_t dmask, cudaStream_t s);
+// Distributed pre-filter (dist.cu, f2): blocked Bloom bitmaps (cblock) of the key_hash chain of
+// the RAW key values — the same on every rank — built / probed on one side's key columns.
+// build: bm |= the side's keys.  probe: mask bit per row (row r -> bit r & 31 of mask[r >> 5]) =
+// key present in bm; with bm_set the survivors also set their bits there.  sample: 1/16 of the
+// side's rows probed, sample[0] += survivors, sample[1] += rows.
+void launch_sj_chain_build(const PackArgs &a, bool side_b, void *bm, uint32_t bbits, cudaStream_t s);
+void launch_sj_chain_probe(const PackArgs &a, bool side_b, const void *bm, uint32_t bbits,
+                           void *bm_set, uint32_t *mask, cudaStream_t s);
+void launch_sj_chain_sample(const PackArgs &a, bool side_b, const void *bm, uint32_t bbits,
+                            unsigned long long *sample, cudaStream_t s);
+// OR-reduce `words` 64-bit words of every rank's bitmap over the peer mappings: this rank reduces
+// the slice [rank, rank + 1) * words / world of all peers and stores the result into all of them
+// (reduce-scatter and all-gather fused in one NVLink kernel).  peers: device array of world
+// pointers (this rank's own included).
+void launch_peer_or(unsigned long long *const *peers, int world, int rank, uint64_t words,
+                    cudaStream_t s);
 void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t bbits, void *bm,
                            cudaStream_t s);
 void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t bbits,
@@ -445,6 +461,7 @@ struct PartArgs {
   const uint32_t *in[MAPSQ_MAX_COLS];
   uint64_t n;
   uint32_t nparts;
+  const uint32_t *mask;  // NULL, or bit r & 31 of mask[r >> 5]: row r is partitioned (else dropped)
 };
 void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntiles,
                            cudaStream_t s);

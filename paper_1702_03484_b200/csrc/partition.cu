@@ -52,6 +52,11 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool in, int nbits) {
 
 __device__ __forceinline__ int dest_bits(uint32_t nparts) { return 32 - __clz((int)nparts - 1); }
 
+// the row participates (no mask, or its bit in the survivor mask is set)
+__device__ __forceinline__ bool row_kept(const PartArgs &a, uint64_t row) {
+  return !a.mask || (__ldg(a.mask + (row >> 5)) >> (row & 31) & 1u);
+}
+
 __device__ __forceinline__ uint32_t rows_left(uint64_t n, uint64_t base, uint32_t cap) {
   const uint64_t r = n > base ? n - base : 0;
   return r < cap ? (uint32_t)r : cap;
@@ -72,6 +77,13 @@ partition_hist_kernel(const PartArgs a, uint32_t *__restrict__ tile_hist, uint64
   for (int it = 0; it < kPartItems; it++) {
     const uint32_t i = it * kPartThreads + threadIdx.x;
     dst[it] = i < rem ? dest_of<NKEY>(a, base, i) : kMaxParts;
+  }
+  if (a.mask) {  // (applied after the key loads, so the mask and key loads overlap)
+#pragma unroll
+    for (int it = 0; it < kPartItems; it++) {
+      const uint32_t i = it * kPartThreads + threadIdx.x;
+      if (i < rem && !row_kept(a, base + i)) dst[it] = kMaxParts;
+    }
   }
 #pragma unroll
   for (int it = 0; it < kPartItems; it++) {
@@ -106,6 +118,13 @@ partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off
   for (int it = 0; it < kPartItems; it++) {
     const uint32_t i = it * 32 + lane;
     m[it] = i < rem ? dest_of<NKEY>(a, wbase, i) : kMaxParts;
+  }
+  if (a.mask) {  // (applied after the key loads, so the mask and key loads overlap)
+#pragma unroll
+    for (int it = 0; it < kPartItems; it++) {
+      const uint32_t i = it * 32 + lane;
+      if (i < rem && !row_kept(a, wbase + i)) m[it] = kMaxParts;
+    }
   }
   __syncthreads();
   // (2) per item: peers, rank among them, and the group leader's shared-memory fetch-add of the
@@ -149,7 +168,8 @@ partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off
     const uint32_t *__restrict__ src = a.in[c] + wbase + lane;
     uint32_t v[kPartItems];
 #pragma unroll
-    for (int it = 0; it < kPartItems; it++) v[it] = it * 32 + lane < rem ? __ldg(src + it * 32) : 0u;
+    for (int it = 0; it < kPartItems; it++)  // (dropped rows: no load, only sectors with a kept row)
+      v[it] = (m[it] & 0xffu) < kMaxParts ? __ldg(src + it * 32) : 0u;
 #pragma unroll
     for (int it = 0; it < kPartItems; it++) {
       const uint32_t d = m[it] & 0xffu;

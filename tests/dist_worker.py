@@ -97,7 +97,10 @@ def main():
         ra, rb = shard_rows(len(A), args.rank, args.world, case), shard_rows(len(B), args.rank, args.world, 0)
         ta = mq.DeviceTable.from_torch(va, [dev(A[ra, c]) for c in range(len(va))])
         tb = mq.DeviceTable.from_torch(vb, [dev(B[rb, c]) for c in range(len(vb))])
-        put(f"j{case}", ctx.join_dist(ta, tb))
+        for mode in ("auto", "on"):  # "on": the cross-rank pre-filter runs (masked exchange)
+            ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_ON if mode == "on" else mq.SEMIJOIN_AUTO)
+            put(f"j{case}_{mode}", ctx.join_dist(ta, tb))
+    ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
     st = ctx.stats()
     for k in ("exchanges", "exchange_rows", "exchange_bytes", "exchange_recv_rows",
               "exchange_recv_bytes"):

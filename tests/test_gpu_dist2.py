@@ -78,9 +78,10 @@ def test_dist_multiprocess_one_gpu(tmp_path, world, nu):
     for case in range(3):
         va, A, vb, B = join_case_tables(case)
         ref = oracle.join(oracle.Table(va, A), oracle.Table(vb, B))
-        vars_, rows = union(shards, f"j{case}")
-        assert vars_ == ref.vars
-        assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), case
+        for mode in ("auto", "on"):
+            vars_, rows = union(shards, f"j{case}_{mode}")
+            assert vars_ == ref.vars
+            assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), (case, mode)
     # rows really crossed between the processes, and what one rank sent the others received
     sent = sum(int(sh["stat_exchange_rows"]) for sh in shards)
     recv = sum(int(sh["stat_exchange_recv_rows"]) for sh in shards)

@@ -1,6 +1,18 @@
-mkdir -p gpurun_out/d1
-python build.py > gpurun_out/d1/build.log 2>&1 || { tail gpurun_out/d1/build.log; exit 1; }
-timeout 900 python -m pytest tests/test_gpu_dist2.py -x -q > gpurun_out/d1/pytest_dist2.log 2>&1; echo "dist2 rc=$?"; tail -30 gpurun_out/d1/pytest_dist2.log
-timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/d1/pytest_fast.log 2>&1; echo "fast rc=$?"; tail -3 gpurun_out/d1/pytest_fast.log
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --force-dist --config C5 --no-cpu-baseline > gpurun_out/d1/bench_force_dist.json 2> gpurun_out/d1/bench_force_dist.err; echo "force-dist rc=$?"; cut -c1-600 gpurun_out/d1/bench_force_dist.json
-timeout 300 python bench.py --gpus 2 --steps 1 --warmup 1 > gpurun_out/d1/bench_g2.json 2> gpurun_out/d1/bench_g2.err; echo "gpus2 rc=$?"; tail -2 gpurun_out/d1/bench_g2.err
+#!/bin/bash
+# multi-rank checks on one GPU: 2/3-process library exchange tests, world-1 NCCL dist bench
+OUT=gpurun_out/${TAG:-d1}; mkdir -p $OUT
+python build.py > $OUT/build.log 2>&1 || { tail $OUT/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_dist2.py -x -q > $OUT/pytest_dist2.log 2>&1; echo "dist2 rc=$?"; tail -30 $OUT/pytest_dist2.log
+if [ "${FAST:-1}" = 1 ]; then
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > $OUT/pytest_fast.log 2>&1; echo "fast rc=$?"; tail -3 $OUT/pytest_fast.log
+fi
+for c in ${CONFIGS:-C5}; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --force-dist --config $c --no-cpu-baseline --no-e2e > $OUT/bench_force_dist_$c.json 2> $OUT/bench_force_dist_$c.err; echo "force-dist $c rc=$?"
+python - $OUT/bench_force_dist_$c.json <<'PY'
+import json, sys
+d = json.loads([l for l in open(sys.argv[1]) if l.startswith("{")][-1])
+print(d["config"]["workload"], round(d["ms_per_step"], 3), "%.3g" % d["value"], "exchange B/step %.3g" % d["exchange"]["bytes_per_step"])
+for k, v in d["kernels"].items():
+    print("   %-18s %3d %.3f ms/step" % (k, v["launches"], v["avg_ms"] * v["launches"] / d["steps"]))
+PY
+done
