@@ -441,6 +441,10 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
 #define MAPSQ_SEMIJOIN_AUTO 1     /*   default: joins with n1 + n2 >= 2^22 rows, unless a 1/16
                                        sample says >= 90% of the rows would survive */
 #define MAPSQ_SEMIJOIN_ON 2       /*   every P64 / RESIDUAL / HASH join */
+/* Joins of at most 4096 input rows on the P64 path run Algorithm 1 in ONE kernel launch (one CTA:
+ * Map, sort and ReduceDuplicate in shared memory; same rows in the same order) with one blocking
+ * read of |RS|; 0 disables it (every join takes the multi-kernel path). */
+#define MAPSQ_OPT_SMALL_JOIN 3    /*   1 (default) / 0 */
 mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value);
 
 /* ---- statistics ---- */

@@ -23,6 +23,7 @@ TABLE_BOUNDS = 1
 PATH_P64, PATH_KV, PATH_RESIDUAL, PATH_HASH = 0, 1, 2, 3
 OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
+OPT_SMALL_JOIN = 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_NCCL", 6: "E_UNSUPPORTED"}
 DIST_ID_BYTES = 128
@@ -233,10 +234,23 @@ class DeviceTable:
 
     def __init__(self, vars_, columns, nrows, c_table: _Table, owner=None):
         self.vars = list(vars_)
-        self.columns = list(columns)
+        # a library result's torch views are built on first use (a caller that only reads nrows,
+        # or passes the table on to the next call, never pays for them)
+        self._columns = list(columns) if not callable(columns) else None
+        self._col_fn = columns if callable(columns) else None
         self.nrows = int(nrows)
         self._c = c_table
         self._owner = owner
+
+    @property
+    def columns(self):
+        if self._columns is None:
+            self._columns = self._col_fn()
+        return self._columns
+
+    @columns.setter
+    def columns(self, cols):
+        self._columns = list(cols)
 
     @property
     def ncols(self) -> int:
@@ -289,16 +303,16 @@ class DeviceTable:
 
 
 def _wrap(ctx: "Context", t: _Table, keep=None) -> DeviceTable:
-    import torch
     owner = _Owner(ctx, t)
     owner.keep = keep  # e.g. the Index whose memory a zero-copy view references
     n, w = int(t.nrows), int(t.ncols)
-    cols = []
-    for c in range(w):
+    ptrs = [t.col[c] for c in range(w)]
+
+    def cols():
+        import torch
         if n == 0:
-            cols.append(torch.empty(0, dtype=torch.uint32, device="cuda"))
-        else:
-            cols.append(torch.as_tensor(_CAI(t.col[c], n, owner), device="cuda"))
+            return [torch.empty(0, dtype=torch.uint32, device="cuda") for _ in range(w)]
+        return [torch.as_tensor(_CAI(p, n, owner), device="cuda") for p in ptrs]
     return DeviceTable([int(t.var[c]) for c in range(w)], cols, n, t, owner)
 
 

@@ -458,6 +458,12 @@ bool debug_on() {
   return on;
 }
 
+// developer knobs for ablations (read once): MAPSQ_SJ_COLBITS caps the hashed column round's bitmaps
+uint32_t env_u32(const char *name, uint32_t dflt) {
+  const char *e = std::getenv(name);
+  return (e && *e) ? (uint32_t)std::strtoul(e, nullptr, 10) : dflt;
+}
+
 uint32_t word_round_bits(uint64_t small) {
   const uint32_t b = bits_for(8 * std::max<uint64_t>(small, 1));
   return std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, b));
@@ -477,7 +483,8 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
                         uint64_t *nB_out) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
   PackArgs pa = pack_args(pl, a, b);
-  const uint64_t bmw = std::max<uint64_t>(1, (1ull << kSemijoinBits) / 32);
+  const uint64_t bmw = std::max<uint64_t>(
+      1, (1ull << std::max(kSemijoinBits, env_u32("MAPSQ_SJ_COLBITS", kSemijoinBits))) / 32);
   const uint64_t nsl_max = sj_slices(n1) + sj_slices(n2) + 2;
   uint32_t *bm = sc.get<uint32_t>(2 * bmw);
   uint32_t *cnt = sc.get<uint32_t>(nsl_max);
@@ -555,7 +562,9 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   if (colpath) {
     const bool s_is_b = n2 <= n1;  // S = the smaller side (ties: B)
     const uint64_t nS = s_is_b ? n2 : n1, nL = s_is_b ? n1 : n2;
-    const uint32_t bbits = colhash ? word_round_bits(nS) : std::min<uint32_t>(pl.kb, kSemijoinBits);
+    const uint32_t colbits = env_u32("MAPSQ_SJ_COLBITS", kSemijoinBits);
+    const uint32_t bbits = colhash ? std::min(std::max<uint32_t>(16, bits_for(8 * std::max<uint64_t>(nS, 1))), colbits)
+                                   : std::min<uint32_t>(pl.kb, kSemijoinBits);
     const uint32_t hashed = colhash || pl.kb > bbits;
     const uint64_t bw = std::max<uint64_t>(2, (1ull << bbits) / 32);
     uint32_t *bmS = bm, *bmL = bm + bw;
@@ -707,6 +716,63 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   return MAPSQ_OK;
 }
 
+// One launch for a tiny P64 join (small.cu): the output is allocated for min(n1 * n2, 2^16) rows;
+// one blocking read of |RS|.  *done = false (nothing allocated) when |RS| exceeds that.
+mapsq_status small_join(mapsq_ctx *ctx, const mapsq_join_plan &pl, const mapsq_table *a,
+                        const mapsq_table *b, mapsq_table *rs, cudaStream_t s, bool *done) {
+  *done = false;
+  const uint64_t cap = std::min<uint64_t>(pl.n1 * pl.n2, 1ull << 16);
+  Scratch sc(ctx, s);
+  unsigned long long *mdev = sc.get<unsigned long long>(1);
+  NEED(mdev);
+  fill_empty_join(pl, a, b, rs);
+  TRY(alloc_table(ctx, rs, cap, pl.out_ncols, s));
+  const PackArgs pa = pack_args(pl, a, b);
+  ExpandArgs ea;
+  std::memset(&ea, 0, sizeof ea);
+  ea.n1 = pl.n1;
+  ea.ib = pl.ib;
+  ea.nkey = pl.nshared;
+  for (uint32_t c = 0; c < pl.nshared; c++) {
+    ea.key_lo[c] = pl.key_lo[c];
+    ea.key_shift[c] = pl.key_shift[c];
+    ea.key_mask[c] = (uint32_t)((1ull << pl.key_bits[c]) - 1);
+  }
+  ea.nrest1 = pl.nrest1;
+  ea.nrest2 = pl.nrest2;
+  for (uint32_t c = 0; c < pl.nrest1; c++) ea.rest1[c] = a->col[pl.rest_col1[c]];
+  for (uint32_t c = 0; c < pl.nrest2; c++) ea.rest2[c] = b->col[pl.rest_col2[c]];
+  for (uint32_t c = 0; c < pl.out_ncols; c++) ea.out[c] = rs->col[c];
+  {
+    KTimer kt(ctx, s, "small_join", 4ull * (pl.n1 * (pl.nshared + pl.nrest1) + pl.n2 * (pl.nshared + pl.nrest2)));
+    launch_small_join(pa, ea, cap, mdev, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      dfree(ctx, rs->owner, s);
+      clear_table(rs);
+      return cuda_check(ctx, e, "small_join");
+    }
+  }
+  TRY(ensure_pinned(ctx, 1));
+  CK(cudaMemcpyAsync(ctx->pinned, mdev, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));  // the one blocking read: |RS|
+  const uint64_t m = ctx->pinned[0];
+  if (m > cap) {  // does not fit the allocation: the regular path
+    dfree(ctx, rs->owner, s);
+    clear_table(rs);
+    return MAPSQ_OK;
+  }
+  rs->nrows = m;
+  if (m == 0) {
+    dfree(ctx, rs->owner, s);
+    rs->owner = nullptr;
+    for (uint32_t c = 0; c < pl.out_ncols; c++) rs->col[c] = nullptr;
+  }
+  ctx->counters.join_out_rows += m;
+  *done = true;
+  return MAPSQ_OK;
+}
+
 // ------------------------------------------------------------------------------ join
 mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_table *tp2_in,
                        mapsq_table *rs, cudaStream_t s) {
@@ -730,6 +796,11 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   if (n1 == 0 || n2 == 0 || pl.disjoint) {
     fill_empty_join(pl, &a, &b, rs);
     return MAPSQ_OK;
+  }
+  if (pl.path == MAPSQ_PATH_P64 && n <= kSmallMaxRows && ctx->small_joins) {
+    bool done = false;
+    TRY(small_join(ctx, pl, &a, &b, rs, s, &done));
+    if (done) return MAPSQ_OK;
   }
   Scratch sc(ctx, s);
   const bool kv = pl.path == MAPSQ_PATH_KV;
@@ -2132,6 +2203,10 @@ MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t valu
   }
   if (option == MAPSQ_OPT_SEMIJOIN && value >= MAPSQ_SEMIJOIN_OFF && value <= MAPSQ_SEMIJOIN_ON) {
     ctx->semijoin = (int)value;
+    return MAPSQ_OK;
+  }
+  if (option == MAPSQ_OPT_SMALL_JOIN && (value == 0 || value == 1)) {
+    ctx->small_joins = value != 0;
     return MAPSQ_OK;
   }
   return set_error(ctx, MAPSQ_E_INVALID, "unknown option or value");

@@ -52,6 +52,7 @@ struct mapsq_ctx {
   bool profiling = false;
   int wide_key_mode = MAPSQ_WIDE_KEY_HASH;
   int semijoin = MAPSQ_SEMIJOIN_AUTO;
+  bool small_joins = true;  // MAPSQ_OPT_SMALL_JOIN: one-CTA path for joins of <= 4096 rows
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
   std::map<std::string, mapsq::KAgg> kagg;
@@ -352,6 +353,12 @@ struct ExpandArgs {
   uint32_t *out[MAPSQ_MAX_COLS];  // nkey + nrest1 + nrest2 columns
   const uint64_t *tile_g0;        // scratch of expand_tiles(m) words: first group of each tile
 };
+// One-CTA Algorithm 1 (small.cu) for joins of at most kSmallMaxRows rows on the P64 path: writes
+// |RS| to *m_out and, when |RS| <= cap, the rows into ea.out (capacity cap rows).
+constexpr uint64_t kSmallMaxRows = 4096;
+size_t small_join_smem(uint64_t n);
+void launch_small_join(const PackArgs &pa, const ExpandArgs &ea, uint64_t cap,
+                       unsigned long long *m_out, cudaStream_t s);
 // launches the tile -> first-group kernel, then the expansion (2 launches)
 void launch_expand(const ExpandArgs &a, cudaStream_t s);
 uint64_t expand_tiles(uint64_t m);

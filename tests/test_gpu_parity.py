@@ -190,6 +190,34 @@ def test_join_hot_composite_key(ctx, mode):
     ctx.set_option(mq.OPT_WIDE_KEY, mq.WIDE_KEY_HASH)
 
 
+def test_small_join_one_launch_equals_multikernel_path(ctx):
+    # joins of <= 4096 rows run Algorithm 1 in one CTA (small.cu): same rows, same order as the
+    # multi-kernel path and the oracle; |RS| above the 2^16-row allocation falls back
+    rng = np.random.default_rng(77)
+    cases = [(1, 1, 3), (17, 5, 4), (700, 320, 300), (2048, 2048, 50), (4000, 96, 7), (300, 300, 1),
+             (2500, 1596, 2000)]
+    for n1, n2, dom in cases:
+        A = np.stack([rng.integers(0, dom, n1), rng.integers(0, 1 << 32, n1, dtype=np.uint64)], 1).astype(np.uint32)
+        B = np.stack([rng.integers(0, 1 << 32, n2, dtype=np.uint64), rng.integers(0, dom, n2)], 1).astype(np.uint32)
+        ref = oracle.join(oracle.Table([0, 1], A), oracle.Table([2, 0], B))
+        outs = []
+        bA = [(int(A[:, c].min()), int(A[:, c].max())) for c in range(2)]
+        bB = [(int(B[:, c].min()), int(B[:, c].max())) for c in range(2)]
+        for small in (1, 0):
+            ctx.set_option(mq.OPT_SMALL_JOIN, small)
+            ctx.stats_reset()
+            ta = mq.DeviceTable.from_torch([0, 1], [dev(A[:, c]) for c in range(2)], bA)
+            tb = mq.DeviceTable.from_torch([2, 0], [dev(B[:, c]) for c in range(2)], bB)
+            got = ctx.join(ta, tb)
+            assert_same(got, ref)  # in order
+            outs.append(got.to_numpy())
+            launches = ctx.stats()["launches"]
+            if small and n1 + n2 <= 4096 and ref.nrows <= (1 << 16):
+                assert launches <= 1, (n1, n2, launches)  # (0: disjoint key ranges)
+        assert np.array_equal(outs[0], outs[1])
+    ctx.set_option(mq.OPT_SMALL_JOIN, 1)
+
+
 def test_join_skewed_hot_key_large_groups(ctx):
     rng = np.random.default_rng(11)
     # one hot key: 6000 x 700 = 4.2e6 output rows, plus a cold tail
