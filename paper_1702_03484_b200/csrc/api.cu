@@ -630,8 +630,10 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   // word rounds: the first one for non-column keys (sampled first), then refinements while a
   // hashed round still drops >= 10% of its input (each round sizes its bitmaps to ~8 bits per
   // key of the smaller side, with a fresh hash seed).  Input segments in cur, output in spare.
+  // (at most two rounds in all: C5's third round removed 19% of 7.1M words for ~0.15 ms, more
+  // than those words cost the sort and the verification)
   for (int round = colpath ? 1 : 0;
-       !skipped && round < 3 && !exact && (round == 0 || nw >= kSemijoinMinRows) && nA && nB;
+       !skipped && round < 2 && !exact && (round == 0 || nw >= kSemijoinMinRows) && nA && nB;
        round++) {
     const SjSeg A{cur, nA}, B{cur + offB, nB};
     const uint64_t slA = sj_slices(nA), slB = sj_slices(nB);
@@ -822,10 +824,11 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   const bool filt = !kv && pl.kb > 0 &&
                     (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
                      (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
-  if (filt && pl.path == MAPSQ_PATH_HASH && pl.kb < 64 - pl.ib) {
-    // with the filter, hash collisions are what survive it: widen key' to every free bit
-    // (C5 J2: |L|·|R| / 2^32 = 8e6 colliding pairs at 32 bits); the extra digit pass then runs
-    // on the few surviving words only
+  if (filt && pl.path == MAPSQ_PATH_HASH && pl.kb < 64 - pl.ib &&
+      env_u32("MAPSQ_HASH_WIDEN", 0)) {
+    // (ablation knob) widen key' beyond 32 bits: after the filter only ~|L'|·|S'| / 2^32
+    // colliding pairs remain (C5 J2: 3.5e6 x 3.5e6 / 2^32 ~ 3e3), so the default keeps 32 bits and
+    // saves a digit pass
     pl.kb = std::min<uint32_t>(64 - pl.ib, 40);
     pl.passes = (pl.kb + MAPSQ_RADIX_BITS - 1) / MAPSQ_RADIX_BITS;
     ctx->counters.last_kb = pl.kb;
