@@ -160,6 +160,7 @@ typedef struct {
   uint64_t exchange_bytes; /* bytes of those rows (4 B per column) */
   uint64_t exchange_recv_rows;  /* rows OTHER ranks stored into this rank's arenas */
   uint64_t exchange_recv_bytes; /* bytes of those rows */
+  uint64_t skew_keys;      /* heavy keys split / broadcast by the distributed joins */
   uint32_t nkernels;       /* per-kernel (per-phase) device times and algorithmic bytes: */
   mapsq_kernel_stat kernel[MAPSQ_MAX_KSTATS];
 } mapsq_stats;
@@ -445,6 +446,9 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
  * Map, sort and ReduceDuplicate in shared memory; same rows in the same order) with one blocking
  * read of |RS|; 0 disables it (every join takes the multi-kernel path). */
 #define MAPSQ_OPT_SMALL_JOIN 3    /*   1 (default) / 0 */
+/* Distributed joins: heavy keys (estimated from a sample to exceed max(1024, N / (4 world)) rows)
+ * keep one side's rows on their rank and broadcast the other side's rows to every rank. */
+#define MAPSQ_OPT_SKEW 4          /*   1 (default) / 0 */
 mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t value);
 
 /* ---- statistics ---- */

@@ -24,6 +24,7 @@ PATH_P64, PATH_KV, PATH_RESIDUAL, PATH_HASH = 0, 1, 2, 3
 OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 OPT_SMALL_JOIN = 3
+OPT_SKEW = 4
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_NCCL", 6: "E_UNSUPPORTED"}
 DIST_ID_BYTES = 128
@@ -80,6 +81,7 @@ class _Stats(ctypes.Structure):
                 ("filter_accesses", ctypes.c_uint64), ("exchanges", ctypes.c_uint64),
                 ("exchange_rows", ctypes.c_uint64), ("exchange_bytes", ctypes.c_uint64),
                 ("exchange_recv_rows", ctypes.c_uint64), ("exchange_recv_bytes", ctypes.c_uint64),
+                ("skew_keys", ctypes.c_uint64),
                 ("nkernels", ctypes.c_uint32), ("kernel", _KStat * 32)]
 
 

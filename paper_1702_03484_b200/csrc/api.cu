@@ -2027,6 +2027,18 @@ MAPSQ_API mapsq_status mapsq_partition_plan_masked(mapsq_ctx *ctx, const mapsq_t
                                                    const int32_t *key_vars, int nkey, int nparts,
                                                    const uint32_t *row_mask, uint64_t *counts_host,
                                                    mapsq_partition_state **state, void *stream) {
+  return mapsq::partition_plan_impl(ctx, in, key_vars, nkey, nparts, row_mask, nullptr, 0, 0,
+                                    counts_host, state, stream);
+}
+
+namespace mapsq {
+// K8 plan; rows whose key equals one of the nheavy keys heavy[h * kMaxHeavyCols ..] (skew
+// handling, dist.cu; nkey <= kMaxHeavyCols) go to destination `self` instead of their hash.
+mapsq_status partition_plan_impl(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
+                                 int nkey, int nparts, const uint32_t *row_mask,
+                                 const uint32_t *heavy, int nheavy, int self,
+                                 uint64_t *counts_host, mapsq_partition_state **state,
+                                 void *stream) {
   TRY(enter(ctx));
   if (!state || !counts_host || !key_vars) return set_error(ctx, MAPSQ_E_INVALID, "NULL argument");
   *state = nullptr;
@@ -2053,6 +2065,15 @@ MAPSQ_API mapsq_status mapsq_partition_plan_masked(mapsq_ctx *ctx, const mapsq_t
   pa.n = in->nrows;
   pa.nparts = (uint32_t)nparts;
   pa.mask = row_mask;
+  if (nheavy > 0) {
+    if (nheavy > kMaxHeavy || nkey > kMaxHeavyCols || self < 0 || self >= nparts) {
+      delete st;
+      return set_error(ctx, MAPSQ_E_INVALID, "bad heavy-key arguments");
+    }
+    pa.nheavy = (uint32_t)nheavy;
+    pa.self = (uint32_t)self;
+    std::memcpy(pa.heavy, heavy, sizeof(uint32_t) * kMaxHeavyCols * nheavy);
+  }
   for (uint32_t c = 0; c < in->ncols; c++) pa.in[c] = in->col[c];
   for (int d = 0; d < nparts; d++) counts_host[d] = st->counts[d] = 0;
   if (in->nrows == 0) {
@@ -2097,6 +2118,36 @@ MAPSQ_API mapsq_status mapsq_partition_plan_masked(mapsq_ctx *ctx, const mapsq_t
   *state = st;
   return MAPSQ_OK;
 }
+
+// The rows of `in` selected by `mask` (bit per row), in row order, into a new table (one-destination
+// K8 plan + scatter).  Caller releases *out.
+mapsq_status compact_rows(mapsq_ctx *ctx, const mapsq_table *in, const uint32_t *mask,
+                          mapsq_table *out, cudaStream_t s) {
+  clear_table(out);
+  uint64_t cnt = 0;
+  mapsq_partition_state *st = nullptr;
+  TRY(partition_plan_impl(ctx, in, in->var, 1, 1, mask, nullptr, 0, 0, &cnt, &st, s));
+  mapsq_status rc = alloc_table(ctx, out, cnt, in->ncols, s);
+  if (rc == MAPSQ_OK) {
+    out->flags = in->flags;
+    for (uint32_t c = 0; c < in->ncols; c++) {
+      out->var[c] = in->var[c];
+      out->lo[c] = in->lo[c];
+      out->hi[c] = in->hi[c];
+    }
+    if (cnt) {
+      const uint64_t row0 = 0;
+      rc = mapsq_partition_scatter(ctx, st, &row0, out->col, s);
+    }
+  }
+  mapsq_partition_state_free(ctx, st);
+  if (rc != MAPSQ_OK) {
+    dfree(ctx, out->owner, s);
+    clear_table(out);
+  }
+  return rc;
+}
+}  // namespace mapsq
 
 MAPSQ_API mapsq_status mapsq_partition_scatter(mapsq_ctx *ctx, mapsq_partition_state *st,
                                                const uint64_t *dest_row,
@@ -2210,6 +2261,10 @@ MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t valu
   }
   if (option == MAPSQ_OPT_SMALL_JOIN && (value == 0 || value == 1)) {
     ctx->small_joins = value != 0;
+    return MAPSQ_OK;
+  }
+  if (option == MAPSQ_OPT_SKEW && (value == 0 || value == 1)) {
+    ctx->skew = value != 0;
     return MAPSQ_OK;
   }
   return set_error(ctx, MAPSQ_E_INVALID, "unknown option or value");

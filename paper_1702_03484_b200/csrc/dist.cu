@@ -18,7 +18,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <array>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "internal.cuh"
@@ -308,16 +310,165 @@ mapsq_status ensure_arena(mapsq_ctx *ctx, DistState *d, int slot, const uint64_t
   return MAPSQ_OK;
 }
 
+// ---- skew: heavy keys split on one side, broadcast on the other.  Algorithm 1
+// joins each key's group on its own, so a key whose rows would overload its
+// hash destination can instead keep the rows of one side where they are (split across the ranks)
+// and send the other side's rows of that key to EVERY rank: each rank joins its share of the split
+// side with all of the broadcast side, and the union over ranks is still the key's full product.
+struct HeavySpec {
+  int n = 0;
+  uint32_t key[kMaxHeavy][kMaxHeavyCols] = {};
+  int bcast_side[kMaxHeavy] = {};  // 0: tp1's rows of the key are broadcast, 1: tp2's
+};
+
+// Detection from a strided sample of both sides' key tuples (<= 4096 rows per side per rank):
+// every rank proposes its 16 most frequent sampled keys of each side with their estimated row
+// counts (sample count x stride) on both sides; the all-gathered estimates are summed per key and
+// a key whose estimated rows reach max(1024, (N1 + N2) / (4 world)) is heavy (at most 8, largest
+// first).  Its broadcast side is the one with fewer estimated rows.  Every rank derives the same
+// list.  Keys wider than kMaxHeavyCols columns are not handled (no heavy keys).
+mapsq_status detect_heavy(mapsq_ctx *ctx, DistState *d, const mapsq_table *a, const mapsq_table *b,
+                          const std::vector<int32_t> &key, HeavySpec *hv, cudaStream_t s) {
+  hv->n = 0;
+  const int W = d->world;
+  if (W == 1 || key.size() > 3) return MAPSQ_OK;  // (the K8 kernels compare up to 3 key columns)
+  const uint32_t nk = (uint32_t)key.size();
+  using K = std::array<uint32_t, kMaxHeavyCols>;
+  std::map<K, uint64_t> est[2];
+  uint64_t nloc[2] = {a->nrows, b->nrows};
+  for (int side = 0; side < 2; side++) {
+    const mapsq_table *t = side ? b : a;
+    const uint64_t n = t->nrows;
+    if (n == 0) continue;
+    const uint64_t stride = std::max<uint64_t>(1, n / 4096), k = (n - 1) / stride + 1;
+    std::vector<uint32_t> buf(nk * k);
+    for (uint32_t c = 0; c < nk; c++) {
+      int col = -1;
+      for (uint32_t j = 0; j < t->ncols; j++)
+        if (t->var[j] == key[c]) col = (int)j;
+      CK(cudaMemcpy2DAsync(buf.data() + c * k, 4, t->col[col], 4 * stride, 4, k,
+                           cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (uint64_t r = 0; r < k; r++) {
+      K kk{};
+      for (uint32_t c = 0; c < nk; c++) kk[c] = buf[c * k + r];
+      est[side][kk] += stride;
+    }
+  }
+  // proposals: this rank's 16 most frequent sampled keys of each side (sampled at least twice)
+  struct Rec {
+    uint32_t key[kMaxHeavyCols];
+    uint32_t valid;
+    uint32_t pad;
+    uint64_t e[2];
+  };
+  constexpr int kProp = 32;
+  std::vector<Rec> mine(kProp);
+  std::memset(mine.data(), 0, sizeof(Rec) * kProp);
+  int np = 0;
+  for (int side = 0; side < 2; side++) {
+    std::vector<std::pair<uint64_t, K>> v;
+    for (auto &kv : est[side])
+      if (kv.second >= 2 * std::max<uint64_t>(1, nloc[side] / 4096)) v.push_back({kv.second, kv.first});
+    std::sort(v.begin(), v.end(), [](const auto &x, const auto &y) { return x.first > y.first; });
+    for (size_t i = 0; i < v.size() && i < (size_t)kProp / 2; i++) {
+      Rec &r = mine[np++];
+      std::memcpy(r.key, v[i].second.data(), sizeof r.key);
+      r.valid = 1;
+      for (int q = 0; q < 2; q++) {
+        auto it = est[q].find(v[i].second);
+        r.e[q] = it == est[q].end() ? 0 : it->second;
+      }
+    }
+  }
+  std::vector<Rec> all((size_t)kProp * W);
+  TRY(coll_allgather(ctx, d, mine.data(), all.data(), sizeof(Rec) * kProp, s));
+  std::vector<uint64_t> sizes(2 * (size_t)W);
+  TRY(coll_allgather(ctx, d, nloc, sizes.data(), sizeof nloc, s));
+  uint64_t N = 0;
+  for (uint64_t x : sizes) N += x;
+  // per key: the sum over ranks of each rank's estimate (a rank proposing a key reports its own
+  // sample counts of both sides; the same key proposed by several ranks is merged per rank)
+  std::map<K, std::array<uint64_t, 2>> tot;
+  for (int r = 0; r < W; r++) {
+    std::map<K, std::array<uint64_t, 2>> per;
+    for (int i = 0; i < kProp; i++) {
+      const Rec &q = all[(size_t)r * kProp + i];
+      if (!q.valid) continue;
+      K kk{};
+      std::memcpy(kk.data(), q.key, sizeof q.key);
+      per[kk] = {q.e[0], q.e[1]};
+    }
+    for (auto &kv : per) {
+      auto &t = tot[kv.first];
+      t[0] += kv.second[0];
+      t[1] += kv.second[1];
+    }
+  }
+  const uint64_t thr = std::max<uint64_t>(1024, N / (4ull * W));
+  std::vector<std::pair<uint64_t, K>> heavy;
+  for (auto &kv : tot)
+    if (kv.second[0] + kv.second[1] >= thr) heavy.push_back({kv.second[0] + kv.second[1], kv.first});
+  std::sort(heavy.begin(), heavy.end(), [](const auto &x, const auto &y) {
+    return x.first != y.first ? x.first > y.first : x.second < y.second;
+  });
+  for (size_t i = 0; i < heavy.size() && hv->n < kMaxHeavy; i++) {
+    const auto &t = tot[heavy[i].second];
+    std::memcpy(hv->key[hv->n], heavy[i].second.data(), sizeof(uint32_t) * kMaxHeavyCols);
+    hv->bcast_side[hv->n] = t[0] < t[1] ? 0 : 1;
+    hv->n++;
+  }
+  ctx->counters.skew_keys += hv->n;
+  return MAPSQ_OK;
+}
+
 // Hash-exchange `in` on key_vars into arena `slot`: *out is a view (owner NULL) of this rank's
 // received rows, grouped by source rank, with bounds valid over every rank's input.
 mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
                       const std::vector<int32_t> &key, int slot, const uint32_t *mask,
-                      mapsq_table *out, cudaStream_t s) {
+                      const HeavySpec &hv, mapsq_table *out, cudaStream_t s) {
   const int W = d->world, R = d->rank;
   const uint32_t nc = in->ncols;
+  // heavy keys: this side's rows of a key it splits stay here; of a key it broadcasts they are
+  // taken out of the hash exchange (keep mask) and copied to every rank (bcast table)
+  uint32_t stay[kMaxHeavy * kMaxHeavyCols] = {}, bcast[kMaxHeavy * kMaxHeavyCols] = {};
+  int nstay = 0, nbc = 0;
+  for (int h = 0; h < hv.n; h++) {
+    uint32_t *dst = hv.bcast_side[h] == slot ? bcast + kMaxHeavyCols * nbc++ : stay + kMaxHeavyCols * nstay++;
+    std::memcpy(dst, hv.key[h], sizeof(uint32_t) * kMaxHeavyCols);
+  }
+  Scratch sc(ctx, s);
+  mapsq_table bc;  // this rank's broadcast rows, compacted
+  std::memset(&bc, 0, sizeof bc);
+  struct TGuard {
+    mapsq_ctx *c;
+    mapsq_table *t;
+    cudaStream_t s;
+    ~TGuard() { mapsq_table_release(c, t, s); }
+  } tguard{ctx, &bc, s};
+  if (nbc) {
+    PartArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    pa.nkey = (uint32_t)key.size();
+    for (uint32_t q = 0; q < pa.nkey; q++)
+      for (uint32_t j = 0; j < in->ncols; j++)
+        if (in->var[j] == key[q]) pa.key[q] = in->col[j];
+    pa.n = in->nrows;
+    pa.mask = mask;
+    pa.nheavy = (uint32_t)nbc;
+    std::memcpy(pa.heavy, bcast, sizeof bcast);
+    uint32_t *keep = sc.get<uint32_t>(in->nrows / 32 + 2), *bm = sc.get<uint32_t>(in->nrows / 32 + 2);
+    if (!keep || !bm) return set_error(ctx, MAPSQ_E_NOMEM, "device allocation failed");
+    launch_heavy_mask(pa, keep, bm, s);
+    CK(cudaGetLastError());
+    mask = keep;
+    TRY(compact_rows(ctx, in, bm, &bc, s));
+  }
   uint64_t counts[kDistMaxRanks];
   mapsq_partition_state *st = nullptr;
-  TRY(mapsq_partition_plan_masked(ctx, in, key.data(), (int)key.size(), W, mask, counts, &st, s));
+  TRY(partition_plan_impl(ctx, in, key.data(), (int)key.size(), W, mask, stay, nstay, R, counts,
+                          &st, s));
   struct Guard {
     mapsq_ctx *c;
     mapsq_partition_state *p;
@@ -329,8 +480,18 @@ mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
   if (d->ipc_broken)
     return set_error(ctx, MAPSQ_E_CUDA, "CUDA IPC: the fused exchange is disabled on this communicator");
   const uint32_t nb = 2 * nc + 1;
-  std::vector<uint64_t> mat((size_t)W * W);
-  TRY(coll_allgather(ctx, d, counts, mat.data(), 8ull * W, s));
+  // count matrix rows: this rank's W hash-destination counts + its broadcast row count
+  std::vector<uint64_t> mine(counts, counts + W), all((size_t)W * (W + 1));
+  mine.push_back(bc.nrows);
+  TRY(coll_allgather(ctx, d, mine.data(), all.data(), 8ull * (W + 1), s));
+  std::vector<uint64_t> mat((size_t)W * W), hb(W);
+  uint64_t H = 0, hbefore = 0;  // broadcast rows of all ranks / of ranks before this one
+  for (int r = 0; r < W; r++) {
+    for (int q = 0; q < W; q++) mat[(size_t)r * W + q] = all[(size_t)r * (W + 1) + q];
+    hb[r] = all[(size_t)r * (W + 1) + W];
+    if (r < R) hbefore += hb[r];
+    H += hb[r];
+  }
   std::vector<uint32_t> bnd(nb);
   const bool has_b = (in->flags & MAPSQ_TABLE_BOUNDS) != 0;
   for (uint32_t c = 0; c < nc; c++) {
@@ -340,8 +501,15 @@ mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
   bnd[2 * nc] = (!has_b && in->nrows) ? 1u : 0u;
   TRY(coll_allreduce_max(ctx, d, bnd.data(), nb, s));
 
-  uint64_t dest_row[kDistMaxRanks], recv[kDistMaxRanks], need[kDistMaxRanks];
+  uint64_t dest_row[kDistMaxRanks], recv[kDistMaxRanks], need[kDistMaxRanks],
+      hashed[kDistMaxRanks];
   TRY(mapsq_exchange_layout(W, R, (int)nc, mat.data(), dest_row, recv, need));
+  // every rank receives, after its hash-exchanged rows, all ranks' broadcast rows (source order)
+  for (int q = 0; q < W; q++) {
+    hashed[q] = recv[q];
+    recv[q] += H;
+    need[q] = 4ull * nc * stride_rows(recv[q]);
+  }
   TRY(ensure_arena(ctx, d, slot, need, s));
   Arena &a = d->slot[slot];
   std::vector<uint32_t *> dest_cols((size_t)W * nc);
@@ -353,13 +521,20 @@ mapsq_status exchange(mapsq_ctx *ctx, DistState *d, const mapsq_table *in,
   // (4) no rank still reads the arena it is about to receive into; then the fused scatter
   TRY(barrier(ctx, d, s));
   TRY(mapsq_partition_scatter(ctx, st, dest_row, dest_cols.data(), s));
+  if (bc.nrows) {  // broadcast rows: one copy per destination and column (NVLink peer copies)
+    KTimer kt(ctx, s, "broadcast_copy", 8ull * nc * bc.nrows * W, (int)(W * nc));
+    for (int q = 0; q < W; q++)
+      for (uint32_t c = 0; c < nc; c++)
+        CK(cudaMemcpyAsync(dest_cols[(size_t)q * nc + c] + hashed[q] + hbefore, bc.col[c],
+                           4ull * bc.nrows, cudaMemcpyDeviceToDevice, s));
+  }
   TRY(barrier(ctx, d, s));  // every peer's stores into this rank's arena have landed
   for (int q = 0; q < W; q++)
     if (q != R) {
-      ctx->counters.exchange_rows += counts[q];
-      ctx->counters.exchange_bytes += 4ull * nc * counts[q];
-      ctx->counters.exchange_recv_rows += mat[(size_t)q * W + R];
-      ctx->counters.exchange_recv_bytes += 4ull * nc * mat[(size_t)q * W + R];
+      ctx->counters.exchange_rows += counts[q] + bc.nrows;
+      ctx->counters.exchange_bytes += 4ull * nc * (counts[q] + bc.nrows);
+      ctx->counters.exchange_recv_rows += mat[(size_t)q * W + R] + hb[q];
+      ctx->counters.exchange_recv_bytes += 4ull * nc * (mat[(size_t)q * W + R] + hb[q]);
     }
   ctx->counters.exchanges++;
 
@@ -527,14 +702,19 @@ mapsq_status join_dist_step(mapsq_ctx *ctx, const mapsq_table *a, const mapsq_ta
   uint32_t *ma = nullptr, *mb = nullptr;
   TRY(prefilter(ctx, d, a, b, key, sc, &ma, &mb, s));
   mapsq_table ea, eb;
-  if (part_key && *part_key == key) {
+  const bool a_placed = part_key && *part_key == key;
+  // skew handling needs both sides exchanged (an input already placed by hash keeps its rows)
+  HeavySpec hv;
+  if (!a_placed && ctx->skew) TRY(detect_heavy(ctx, d, a, b, key, &hv, s));
+  if (a_placed) {
     ea = *a;  // already partitioned on the key: stays (the local join filters it)
   } else {
-    TRY(exchange(ctx, d, a, key, 0, ma, &ea, s));
+    TRY(exchange(ctx, d, a, key, 0, ma, hv, &ea, s));
   }
-  TRY(exchange(ctx, d, b, key, 1, mb, &eb, s));
+  TRY(exchange(ctx, d, b, key, 1, mb, hv, &eb, s));
   TRY(join_tables(ctx, &ea, &eb, rs, s));
-  if (part_key) *part_key = key;
+  // a result with split heavy keys is not hash-partitioned on the key any more
+  if (part_key) *part_key = hv.n ? std::vector<int32_t>() : key;
   return MAPSQ_OK;
 }
 

@@ -53,6 +53,7 @@ struct mapsq_ctx {
   int wide_key_mode = MAPSQ_WIDE_KEY_HASH;
   int semijoin = MAPSQ_SEMIJOIN_AUTO;
   bool small_joins = true;  // MAPSQ_OPT_SMALL_JOIN: one-CTA path for joins of <= 4096 rows
+  bool skew = true;         // MAPSQ_OPT_SKEW: heavy keys split / broadcast in distributed joins
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
   std::map<std::string, mapsq::KAgg> kagg;
@@ -469,7 +470,23 @@ struct PartArgs {
   uint64_t n;
   uint32_t nparts;
   const uint32_t *mask;  // NULL, or bit r & 31 of mask[r >> 5]: row r is partitioned (else dropped)
+  // skew (dist.cu): rows whose key (nkey <= kMaxHeavyCols values) equals one of the nheavy keys
+  // heavy[h * kMaxHeavyCols ..] stay on this rank (dest = self) instead of their hash destination
+  uint32_t nheavy, self;
+  uint32_t heavy[8 * 4];
 };
+constexpr int kMaxHeavy = 8;
+constexpr int kMaxHeavyCols = 4;
+// keep[r] = in[r] && key(r) not heavy; bcast[r] = in[r] && key(r) heavy (a.heavy / a.nheavy;
+// in = a.mask, NULL = all rows).  Both ceil(n / 32) words.
+void launch_heavy_mask(const PartArgs &a, uint32_t *keep, uint32_t *bcast, cudaStream_t s);
+mapsq_status partition_plan_impl(mapsq_ctx *ctx, const mapsq_table *in, const int32_t *key_vars,
+                                 int nkey, int nparts, const uint32_t *row_mask,
+                                 const uint32_t *heavy, int nheavy, int self,
+                                 uint64_t *counts_host, mapsq_partition_state **state,
+                                 void *stream);
+mapsq_status compact_rows(mapsq_ctx *ctx, const mapsq_table *in, const uint32_t *mask,
+                          mapsq_table *out, cudaStream_t s);
 void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntiles,
                            cudaStream_t s);
 // dst_row[d]: first row of this rank's block in destination d's arena; dst_cols[d * ncols + c]:

@@ -30,12 +30,49 @@ template <int NKEY>
 __device__ __forceinline__ uint32_t dest_of(const PartArgs &a, uint64_t base, uint32_t i) {
   uint32_t h = 0x811c9dc5u;
   if (NKEY > 0) {
+    uint32_t v[NKEY > 0 ? NKEY : 1];
 #pragma unroll
-    for (int c = 0; c < NKEY; c++) h = (h ^ __ldg(a.key[c] + base + i)) * 0x01000193u;
+    for (int c = 0; c < NKEY; c++) {
+      v[c] = __ldg(a.key[c] + base + i);
+      h = (h ^ v[c]) * 0x01000193u;
+    }
+    // a heavy (skewed) key's rows of the split side stay where they are (dist.cu)
+    for (uint32_t q = 0; q < a.nheavy; q++) {
+      bool eq = true;
+#pragma unroll
+      for (int c = 0; c < NKEY; c++) eq &= v[c] == a.heavy[q * kMaxHeavyCols + c];
+      if (eq) return a.self;
+    }
   } else {
     for (uint32_t c = 0; c < a.nkey; c++) h = (h ^ __ldg(a.key[c] + base + i)) * 0x01000193u;
   }
   return __umulhi(fmix32(h), a.nparts);
+}
+
+// keep / broadcast masks of the heavy keys (one warp per 32 rows)
+__global__ void __launch_bounds__(256)
+heavy_mask_kernel(const PartArgs a, uint32_t *__restrict__ keep, uint32_t *__restrict__ bcast) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (a.n + 31) / 32;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; w < nw;
+       w += (uint64_t)gridDim.x * blockDim.x / 32) {
+    const uint64_t r = w * 32 + lane;
+    bool in = r < a.n && (!a.mask || (__ldg(a.mask + w) >> lane & 1u));
+    bool heavy = false;
+    if (in) {
+      for (uint32_t q = 0; q < a.nheavy && !heavy; q++) {
+        bool eq = true;
+        for (uint32_t c = 0; c < a.nkey; c++) eq &= __ldg(a.key[c] + r) == a.heavy[q * kMaxHeavyCols + c];
+        heavy = eq;
+      }
+    }
+    const uint32_t k = __ballot_sync(0xffffffffu, in && !heavy);
+    const uint32_t b = __ballot_sync(0xffffffffu, in && heavy);
+    if (lane == 0) {
+      keep[w] = k;
+      bcast[w] = b;
+    }
+  }
 }
 
 // Lanes of the warp holding the same destination: one ballot per destination bit (nbits =
@@ -179,6 +216,13 @@ partition_scatter_kernel(const PartArgs a, const uint64_t *__restrict__ tile_off
 }
 
 }  // namespace
+
+void launch_heavy_mask(const PartArgs &a, uint32_t *keep, uint32_t *bcast, cudaStream_t s) {
+  const uint64_t nw = (a.n + 31) / 32;
+  if (nw == 0) return;
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nw * 32 + 255) / 256, 148 * 8));
+  heavy_mask_kernel<<<g, 256, 0, s>>>(a, keep, bcast);
+}
 
 void launch_partition_hist(const PartArgs &a, uint32_t *tile_hist, uint64_t ntiles,
                            cudaStream_t s) {

@@ -37,11 +37,32 @@ def join_case_tables(case: int):
         A = np.stack([x1, rng.integers(0, 100, n1), z1], 1)
         B = np.stack([z2, x2, rng.integers(0, 100, n2)], 1)
         return [0, 1, 2], A.astype(np.uint32), [2, 0, 3], B.astype(np.uint32)
+    if case == 3:    # skew: two heavy single keys (7: mostly tp1, 11: mostly tp2) + a cold tail
+        n1, n2 = 40000, 30000
+        u1, u2 = rng.random(n1), rng.random(n2)
+        k1 = np.where(u1 < 0.4, 7, np.where(u1 < 0.43, 11, rng.integers(0, 5000, n1)))
+        k2 = np.where(u2 < 0.05, 7, np.where(u2 < 0.35, 11, rng.integers(0, 5000, n2)))
+        A = np.stack([k1, rng.integers(0, 1 << 32, n1, dtype=np.uint64)], 1)
+        B = np.stack([rng.integers(0, 1 << 32, n2, dtype=np.uint64), k2], 1)
+        return [0, 1], A.astype(np.uint32), [2, 0], B.astype(np.uint32)
+    if case == 4:    # skew on a composite key (x, z) = (3, 4), wide columns: HASH path locally
+        n1, n2 = 30000, 30000
+        hot1, hot2 = rng.random(n1) < 0.3, rng.random(n2) < 0.2
+        x1 = np.where(hot1, 3, rng.integers(0, 1 << 32, n1, dtype=np.uint64))
+        z1 = np.where(hot1, 4, rng.integers(0, 9, n1))
+        x2 = np.where(hot2, 3, rng.integers(0, 1 << 32, n2, dtype=np.uint64))
+        z2 = np.where(hot2, 4, rng.integers(0, 9, n2))
+        A = np.stack([x1, z1, np.arange(n1)], 1)
+        B = np.stack([z2, x2], 1)
+        return [0, 1, 2], A.astype(np.uint32), [1, 0], B.astype(np.uint32)
     # case 2: one side empty on some ranks (rows only in the first half)
     n1, n2 = 500, 6000
     A = np.stack([rng.integers(0, 50, n1), rng.integers(0, 9, n1)], 1)
     B = np.stack([rng.integers(0, 50, n2), rng.integers(0, 9, n2)], 1)
     return [0, 1], A.astype(np.uint32), [0, 2], B.astype(np.uint32)
+
+
+NCASES = 5
 
 
 def shard_rows(nrows: int, rank: int, world: int, case: int):
@@ -92,7 +113,7 @@ def main():
         put(f"qscan_{cfg}", ctx.query_dist(trip, config_query(cfg)))
     ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
     # random joins: rank r holds rows r::world of both inputs
-    for case in range(3):
+    for case in range(NCASES):
         va, A, vb, B = join_case_tables(case)
         ra, rb = shard_rows(len(A), args.rank, args.world, case), shard_rows(len(B), args.rank, args.world, 0)
         ta = mq.DeviceTable.from_torch(va, [dev(A[ra, c]) for c in range(len(va))])
@@ -101,9 +122,20 @@ def main():
             ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_ON if mode == "on" else mq.SEMIJOIN_AUTO)
             put(f"j{case}_{mode}", ctx.join_dist(ta, tb))
     ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
+    # the skew cases again with heavy-key handling off: same union, no split keys
+    ctx.set_option(mq.OPT_SKEW, 0)
+    for case in (3, 4):
+        va, A, vb, B = join_case_tables(case)
+        ra, rb = shard_rows(len(A), args.rank, args.world, case), shard_rows(len(B), args.rank, args.world, 0)
+        ta = mq.DeviceTable.from_torch(va, [dev(A[ra, c]) for c in range(len(va))])
+        tb = mq.DeviceTable.from_torch(vb, [dev(B[rb, c]) for c in range(len(vb))])
+        sk0 = ctx.stats()["skew_keys"]
+        put(f"j{case}_noskew", ctx.join_dist(ta, tb))
+        assert ctx.stats()["skew_keys"] == sk0
+    ctx.set_option(mq.OPT_SKEW, 1)
     st = ctx.stats()
     for k in ("exchanges", "exchange_rows", "exchange_bytes", "exchange_recv_rows",
-              "exchange_recv_bytes"):
+              "exchange_recv_bytes", "skew_keys"):
         res["stat_" + k] = np.array(st[k], np.int64)
     torch.cuda.synchronize()
     dist.barrier()

@@ -23,7 +23,7 @@ torch = pytest.importorskip("torch")
 
 import datagen  # noqa: E402
 import oracle  # noqa: E402
-from dist_worker import join_case_tables  # noqa: E402
+from dist_worker import NCASES, join_case_tables  # noqa: E402
 from fixtures import config_query  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -74,14 +74,18 @@ def test_dist_multiprocess_one_gpu(tmp_path, world, nu):
             vars_, rows = union(shards, name)
             assert vars_ == ref.vars, name
             assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), name
-    # random joins (skewed single key, composite wide key, everything on one rank)
-    for case in range(3):
+    # random joins (skewed single key, composite wide key, everything on one rank, two heavy
+    # single keys, a heavy composite key), with and without the pre-filter and the skew handling
+    for case in range(NCASES):
         va, A, vb, B = join_case_tables(case)
         ref = oracle.join(oracle.Table(va, A), oracle.Table(vb, B))
-        for mode in ("auto", "on"):
-            vars_, rows = union(shards, f"j{case}_{mode}")
+        names = [f"j{case}_auto", f"j{case}_on"] + ([f"j{case}_noskew"] if case in (3, 4) else [])
+        for name in names:
+            vars_, rows = union(shards, name)
             assert vars_ == ref.vars
-            assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), (case, mode)
+            assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), name
+    # the heavy keys of cases 3 and 4 were detected (split / broadcast) on every rank
+    assert all(int(sh["stat_skew_keys"]) >= 2 * 2 + 2 for sh in shards)
     # rows really crossed between the processes, and what one rank sent the others received
     sent = sum(int(sh["stat_exchange_rows"]) for sh in shards)
     recv = sum(int(sh["stat_exchange_recv_rows"]) for sh in shards)

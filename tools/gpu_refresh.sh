@@ -36,7 +36,7 @@ if [ "${NCU:-1}" = 1 ]; then
       --launch-count ${COUNT:-40} -o $OUT/ncu_full_$c -f $CMD > $OUT/ncu_f_$c.log 2>&1
     echo "ncu full $c exit $?"
     ncu -i $OUT/ncu_full_$c.ncu-rep --page raw --csv > $OUT/ncu_full_${c}_raw.csv 2>/dev/null
-    python tools/ncu_summary.py $OUT/ncu_full_${c}_raw.csv $OUT/ncu_traffic_$c.json > $OUT/ncu_full_$c.md 2>&1
+    python tools/ncu_summary.py $OUT/ncu_full_${c}_raw.csv $OUT/ncu_traffic_$c.json $([ $c = C4 ] && echo 0 || echo 2) > $OUT/ncu_full_$c.md 2>&1
     for k in sj_probe_stage radix_pass expand_kernel verify_emit find_groups; do
       ncu -i $OUT/ncu_full_$c.ncu-rep --page source --csv --kernel-name regex:$k --launch-count 1 \
         > $OUT/ncu_source_${c}_$k.csv 2>/dev/null

@@ -1,11 +1,16 @@
 """Summarise an ncu --set full report (raw page CSV) per kernel: time, DRAM bytes, throughput.
-Usage: ncu -i X.ncu-rep --page raw --csv > raw.csv; python tools/ncu_summary.py raw.csv [traffic.json]"""
+Usage: ncu -i X.ncu-rep --page raw --csv > raw.csv; python tools/ncu_summary.py raw.csv [traffic.json] [skip]
+skip: leading kernels excluded from the per-timer traffic (e.g. the index build's Map + digit pass,
+which run at load time before the first step)."""
 import csv
 import json
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
+import gzip
+opener = gzip.open if sys.argv[1].endswith(".gz") else open
+rows = list(csv.reader(opener(sys.argv[1], "rt")))
 h, units = rows[0], rows[1]
+SKIP = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 tscale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1}
 
@@ -18,7 +23,7 @@ def get(r, name):
 traffic = {}
 print("| kernel | grid | regs | time ms | DRAM read GB | DRAM write GB | DRAM GB/s | DRAM % peak | SM % | issued inst |")
 print("|---|---|---|---|---|---|---|---|---|---|")
-for r in rows[2:]:
+for ri, r in enumerate(rows[2:]):
     name = get(r, "Kernel Name")[0].split("(")[0].split("::")[-1]
     short = name.split("<")[0].replace("_kernel", "")
     t, tu = get(r, "gpu__time_duration.sum")
@@ -33,7 +38,8 @@ for r in rows[2:]:
     inst = get(r, "smsp__inst_executed.sum")[0]
     print(f"| {name} | {grid} | {regs} | {t*1e3:.3f} | {rd/1e9:.3f} | {wr/1e9:.3f} | "
           f"{(rd+wr)/t/1e9:.0f} | {dpct} | {smpct} | {inst} |")
-    traffic.setdefault(short, []).append(rd + wr)
+    if ri >= SKIP:
+        traffic.setdefault(short, []).append(rd + wr)
 # DRAM bytes per invocation of each library timer (bench.py's kernel names): a timer may cover
 # several kernels; its invocations are counted by its anchor kernel
 TIMERS = {  # timer: (member kernels, invocations from the launch counts)

@@ -371,7 +371,7 @@ float zipf_sort(K kern, int items, const char *name, uint64_t *w0, uint64_t *w1,
       cudaMemsetAsync(status, 0, ntiles * kRadix * 8);
       cudaMemsetAsync(ctr, 0, 4);
       kern<<<(unsigned)ntiles, 256, smem>>>(a, b, nullptr, nullptr, n, ib + 8 * p, bits,
-                                            hists + p * kRadix, status, ctr, nullptr, 0, 0);
+                                            hists + p * kRadix, status, ctr, nullptr, 0, 0, n, 0);
       cudaEventRecord(ev[p + 1]);
       std::swap(a, b);
     }
@@ -526,7 +526,7 @@ int main(int argc, char **argv) {
         cudaMemsetAsync(ctr, 0, 4);
         cudaEventRecord(a);
         cudaMemsetAsync(hnext, 0, kRadix * 4);
-        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 40, 8, histraw, status, ctr, use_next ? hnext : nullptr, 48, 0xff);
+        kern<<<(unsigned)ntiles, 256, smem>>>(kin, kout, nullptr, nullptr, n, 40, 8, histraw, status, ctr, use_next ? hnext : nullptr, 48, 0xff, n, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
