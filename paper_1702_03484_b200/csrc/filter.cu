@@ -56,32 +56,32 @@ struct Side {
 // loads in flight together); rows >= rows get key' 0 (callers mask them)
 // FINAL = false (hash modes, filter-only uses): the key_hash chain without its final mix — the
 // filter's bitmap index mixes again, and only the words need the exact key'.
-template <int MODE, bool FINAL = true>
+template <int MODE, bool FINAL = true, int N = kFItems>
 __device__ __forceinline__ void load_keys(const PackArgs &a, const Side &sd, uint64_t base,
-                                          uint32_t lane, KeyT<MODE> key[kFItems],
+                                          uint32_t lane, KeyT<MODE> key[N],
                                           uint32_t keep = 0xffffu) {
   constexpr bool hash = MODE >= 2;
 #pragma unroll
-  for (int it = 0; it < kFItems; it++) key[it] = hash ? kKeyHashSeed : 0;
+  for (int it = 0; it < N; it++) key[it] = hash ? kKeyHashSeed : 0;
   const uint32_t nk = mode_nkey<MODE>(a);
   for (uint32_t c = 0; c < nk; c++) {
     const uint32_t *p = sd.col[c];
     const uint32_t lo = a.lo[c], sh = a.shift[c];
-    uint32_t v[kFItems];
+    uint32_t v[N];
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) {
+    for (int it = 0; it < N; it++) {
       const uint64_t j = base + (uint64_t)it * 32 + lane;
       v[it] = (j < sd.rows && (keep >> it & 1u)) ? __ldcs(p + j) : lo;
     }
 #pragma unroll
-    for (int it = 0; it < kFItems; it++)
+    for (int it = 0; it < N; it++)
       key[it] = MODE == 0 ? (KeyT<MODE>)(v[it] - lo)
                      : (KeyT<MODE>)(hash ? key_hash_step(key[it], v[it])
                                          : (key[it] | (uint64_t)(v[it] - lo) << sh));
   }
   if (hash && FINAL) {
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) key[it] = (KeyT<MODE>)key_hash_final(key[it], a.kb);
+    for (int it = 0; it < N; it++) key[it] = (KeyT<MODE>)key_hash_final(key[it], a.kb);
   }
 }
 
@@ -143,16 +143,16 @@ __device__ __forceinline__ void red_or_bm32(uint32_t *p, uint32_t m, uint64_t po
 // (208 vs 75 G rows/s for distinct keys, tools/bitmap_bench.cu).
 // HINT = false: no L2 policy (the probe's SET bitmap: with the probed one also hot, two 64 MB
 // evict_last bitmaps overflow L2 — C4's column probe 2.28 -> 2.57 ms with both hinted).
-template <bool TEST = true, bool HINT = true>
-__device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[kFItems],
+template <bool TEST = true, bool HINT = true, int N = kFItems>
+__device__ __forceinline__ void set_bits(uint32_t *bm, const uint32_t bidx[N],
                                          uint32_t keep, uint32_t lane) {
   const uint64_t pol = HINT ? bm_policy() : 0;
-  uint32_t word[kFItems];
+  uint32_t word[N];
 #pragma unroll
-  for (int it = 0; it < kFItems; it++)  // (read-only path: a stale word costs one more atomic)
+  for (int it = 0; it < N; it++)  // (read-only path: a stale word costs one more atomic)
     word[it] = (TEST && (keep >> it & 1u)) ? (HINT ? ld_bm32(bm + (bidx[it] >> 5), pol) : __ldg(bm + (bidx[it] >> 5))) : 0u;
 #pragma unroll
-  for (int it = 0; it < kFItems; it++) {
+  for (int it = 0; it < N; it++) {
     const uint32_t b = bidx[it];
     const uint32_t k = keep >> it & 1u;
     const uint32_t bp = __shfl_up_sync(0xffffffffu, b, 1);
@@ -248,19 +248,19 @@ __device__ __forceinline__ void cblock(uint64_t h, uint32_t bbits, uint32_t &idx
 // set (idx, m) for the rows whose keep bit is set (fire-and-forget RED.OR: keys mostly distinct);
 // a lane whose left neighbour sets the same block bits skips.  TEST: read the word first and skip
 // bits already set (skewed keys: a hot key's word would otherwise serialise its atomics).
-template <bool TEST = false>
-__device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_t idx[kFItems],
-                                           const uint64_t m[kFItems], uint32_t keep,
+template <bool TEST = false, int N = kFItems>
+__device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_t idx[N],
+                                           const uint64_t m[N], uint32_t keep,
                                            uint32_t lane) {
   const uint64_t pol = bm_policy();
-  uint64_t cur[TEST ? kFItems : 1];
+  uint64_t cur[TEST ? N : 1];
   if (TEST) {
 #pragma unroll
-    for (int it = 0; it < kFItems; it++)
+    for (int it = 0; it < N; it++)
       cur[TEST ? it : 0] = (keep >> it & 1u) ? ld_bm(bm + idx[it], pol) : 0ull;
   }
 #pragma unroll
-  for (int it = 0; it < kFItems; it++) {
+  for (int it = 0; it < N; it++) {
     const uint32_t k = keep >> it & 1u;
     const uint32_t ip = __shfl_up_sync(0xffffffffu, idx[it], 1);
     const uint64_t mp = __shfl_up_sync(0xffffffffu, m[it], 1);
@@ -272,32 +272,37 @@ __device__ __forceinline__ void set_blocks(unsigned long long *bm, const uint32_
 }
 
 // Word segment of one side (packed words key' << ib | row id of that side's rows, ascending).
+template <int N = kFItems>
 __device__ __forceinline__ void load_words(const SjSeg &sd, uint64_t base, uint32_t lane,
-                                           uint64_t w[kFItems]) {
+                                           uint64_t w[N]) {
 #pragma unroll
-  for (int it = 0; it < kFItems; it++) {
+  for (int it = 0; it < N; it++) {
     const uint64_t j = base + (uint64_t)it * 32 + lane;
     w[it] = j < sd.rows ? __ldcs(sd.w + j) : 0ull;
   }
 }
 
-__global__ void __launch_bounds__(kFThreads)
+__global__ void __launch_bounds__(kFThreads, 4)
 wfilter_build_kernel(const SjSeg sd, uint32_t ib, uint64_t seed, uint32_t bbits,
                      unsigned long long *__restrict__ bm) {
+  constexpr int NB = kFItems / 2;  // batches of 8 rows per lane: four CTAs per SM
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < sd.rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    uint32_t idx[kFItems], keep = 0;
-    uint64_t w[kFItems], m[kFItems];
-    load_words(sd, base, lane, w);
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      wblock_key(w[it] >> ib, seed, bbits, idx[it], m[it]);
-      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+    for (int half = 0; half < 2; half++) {
+      const uint64_t base = ws * kFWarpRows + (uint64_t)half * NB * 32;
+      uint32_t idx[NB], keep = 0;
+      uint64_t w[NB], m[NB];
+      load_words<NB>(sd, base, lane, w);
+#pragma unroll
+      for (int it = 0; it < NB; it++) {
+        wblock_key(w[it] >> ib, seed, bbits, idx[it], m[it]);
+        keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+      }
+      set_blocks<false, NB>(bm, idx, m, keep, lane);
     }
-    set_blocks(bm, idx, m, keep, lane);
   }
 }
 
@@ -339,24 +344,29 @@ wfilter_sample_kernel(const SjSeg sd, uint32_t ib, uint64_t seed, uint32_t bbits
 // ---- hashed composite keys (PATH_HASH), first round on the key columns: the smaller side's
 // blocked Bloom bitmap from the key_hash chain of its shared columns (load_keys<MODE, false>)
 template <int MODE, bool TEST = false>
-__global__ void __launch_bounds__(kFThreads)
+__global__ void __launch_bounds__(kFThreads, TEST ? 3 : 4)
 cfilter_build_kernel(const PackArgs a, const Side sd, uint32_t bbits,
                      unsigned long long *__restrict__ bm) {
+  // batches of 8 rows per lane (two per 512-row slice): ~60 registers, four CTAs per SM
+  constexpr int NB = kFItems / 2;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < sd.rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    KeyT<MODE> key[kFItems];
-    load_keys<MODE, false>(a, sd, base, lane, key);
-    uint32_t idx[kFItems], keep = 0;
-    uint64_t m[kFItems];
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      cblock(key[it], bbits, idx[it], m[it]);
-      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+    for (int half = 0; half < 2; half++) {
+      const uint64_t base = ws * kFWarpRows + (uint64_t)half * NB * 32;
+      KeyT<MODE> key[NB];
+      load_keys<MODE, false, NB>(a, sd, base, lane, key);
+      uint32_t idx[NB], keep = 0;
+      uint64_t m[NB];
+#pragma unroll
+      for (int it = 0; it < NB; it++) {
+        cblock(key[it], bbits, idx[it], m[it]);
+        keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < sd.rows) << it;
+      }
+      set_blocks<TEST, NB>(bm, idx, m, keep, lane);
     }
-    set_blocks<TEST>(bm, idx, m, keep, lane);
   }
 }
 
@@ -429,8 +439,95 @@ __device__ __forceinline__ void probe_slot(uint64_t key, uint32_t bbits, uint32_
 }
 
 template <int KM, int BM, bool SET>
-__global__ void __launch_bounds__(kFThreads, KM == 0 ? 4 : 2)
+__global__ void __launch_bounds__(kFThreads, 3)
 sj_probe_stage_kernel(const PackArgs a, const Side sd, const SjSeg ws, const void *__restrict__ bm,
+                      uint32_t bbits, uint32_t hashed, uint64_t seed,
+                      uint32_t *__restrict__ bm_set, uint64_t *__restrict__ stage,
+                      uint32_t *__restrict__ cnt) {
+  // registers: the keys and the probed bitmap words only (slots and masks are recomputed from
+  // the key, a few ALU ops) — 32-bit for a single packed column against a plain bitmap.  64-bit
+  // keys are processed in batches of 8 rows per lane (two per 512-row slice) so three CTAs fit
+  // an SM (the same loads in flight per SM, more warps to hide the random-access latency).
+  using KT = typename std::conditional<KM == 0, uint32_t, uint64_t>::type;
+  using VT = typename std::conditional<BM == 0, uint32_t, uint64_t>::type;
+  constexpr int NB = kFItems / 2;
+  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  const uint64_t rows = KM == 4 ? ws.rows : sd.rows;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
+  const uint64_t pol = bm_policy();
+  constexpr int CM = KM == 4 ? 1 : KM;  // column mode for load_keys (unused for words)
+  for (uint64_t wsl = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); wsl * kFWarpRows < rows;
+       wsl += nwarps) {
+    uint32_t r = 0;  // the slice's survivors so far
+#pragma unroll
+    for (int half = 0; half < kFItems / NB; half++) {
+      const uint64_t base = wsl * kFWarpRows + (uint64_t)half * NB * 32;
+      // key' (the words themselves for KM 4; the key_hash chain for BM 1) of every item
+      KT key[NB];
+      if (KM == 4) {
+        uint64_t w[NB];
+        load_words<NB>(ws, base, lane, w);
+#pragma unroll
+        for (int it = 0; it < NB; it++) key[it] = (KT)w[it];
+      } else {
+        KeyT<CM> k[NB];
+        load_keys<CM, BM != 1, NB>(a, sd, base, lane, k);
+#pragma unroll
+        for (int it = 0; it < NB; it++) key[it] = (KT)k[it];
+      }
+      const uint32_t lim = base < rows ? (uint32_t)std::min<uint64_t>(rows - base, NB * 32) : 0u;
+      VT v[NB];
+#pragma unroll
+      for (int it = 0; it < NB; it++) {  // all probes of the batch in flight together
+        const bool in = (uint32_t)it * 32 + lane < lim;
+        uint32_t idx;
+        uint64_t m;
+        probe_slot<BM>(KM == 4 ? (uint64_t)key[it] >> a.ib : (uint64_t)key[it], bbits, hashed, seed,
+                       idx, m);
+        if (BM == 0)
+          v[it] = in ? (VT)ld_bm32(reinterpret_cast<const uint32_t *>(bm) + idx, pol) : (VT)0;
+        else
+          v[it] = in ? (VT)ld_bm(reinterpret_cast<const unsigned long long *>(bm) + idx, pol) : (VT)0;
+      }
+      uint32_t keep = 0;
+#pragma unroll
+      for (int it = 0; it < NB; it++) {
+        uint32_t idx;
+        uint64_t m;
+        // (an opaque copy: the slot is recomputed here instead of being kept live across the probes)
+        const uint64_t kq = opaque((uint64_t)key[it]);
+        probe_slot<BM>(KM == 4 ? kq >> a.ib : kq, bbits, hashed, seed, idx, m);
+        const bool k = ((uint64_t)v[it] & m) == m && (uint32_t)it * 32 + lane < lim;
+        keep |= (uint32_t)k << it;
+        const uint32_t bal = __ballot_sync(0xffffffffu, k);
+        if (k) {
+          uint64_t w;
+          if (KM == 4) {
+            w = key[it];
+          } else {
+            const uint64_t kp = (BM == 1) ? key_hash_final(key[it], a.kb) : (uint64_t)key[it];
+            w = (kp << a.ib) | (base + (uint64_t)it * 32 + lane + sd.id0);
+          }
+          __stcg(stage + wsl * kFWarpRows + r + __popc(bal & lt), w);
+        }
+        r += __popc(bal);
+      }
+      if (SET) {
+        uint32_t bidx[NB];
+#pragma unroll
+        for (int it = 0; it < NB; it++) bidx[it] = bit_index((uint64_t)key[it], bbits, hashed);
+        set_bits<true, false, NB>(bm_set, bidx, keep, lane);
+      }
+    }
+    if (lane == 0) cnt[sd.slice0 + wsl] = r;
+  }
+}
+
+// The single packed column against a plain bitmap (KM 0, BM 0): 32-bit keys, 16 rows per lane in
+// one batch, four CTAs per SM.
+template <int KM, int BM, bool SET>
+__global__ void __launch_bounds__(kFThreads, 4)
+sj_probe_stage16_kernel(const PackArgs a, const Side sd, const SjSeg ws, const void *__restrict__ bm,
                       uint32_t bbits, uint32_t hashed, uint64_t seed,
                       uint32_t *__restrict__ bm_set, uint64_t *__restrict__ stage,
                       uint32_t *__restrict__ cnt) {
@@ -558,32 +655,36 @@ sj_gather_kernel(const uint64_t *__restrict__ stage, const uint32_t *__restrict_
 // bit of key' (test before set), 2 = wblock of key' with `seed`.  Reads 8 B per survivor
 // instead of the side's key columns.
 template <int KIND>
-__global__ void __launch_bounds__(kFThreads)
+__global__ void __launch_bounds__(kFThreads, 4)
 sj_set_words_kernel(const uint64_t *__restrict__ w, const uint64_t *__restrict__ count,
                     uint32_t ib, uint32_t bbits, uint32_t hashed, uint64_t seed, void *bm) {
+  constexpr int NB = kFItems / 2;  // batches of 8 rows per lane: four CTAs per SM
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t rows = *count;
   const SjSeg sd{w, rows};
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
   for (uint64_t ws = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5);
        ws * kFWarpRows < rows; ws += nwarps) {
-    const uint64_t base = ws * kFWarpRows;
-    uint64_t wv[kFItems];
-    load_words(sd, base, lane, wv);
-    uint32_t idx[kFItems], keep = 0;
-    uint64_t m[kFItems];
 #pragma unroll
-    for (int it = 0; it < kFItems; it++) {
-      keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < rows) << it;
+    for (int half = 0; half < 2; half++) {
+      const uint64_t base = ws * kFWarpRows + (uint64_t)half * NB * 32;
+      uint64_t wv[NB];
+      load_words<NB>(sd, base, lane, wv);
+      uint32_t idx[NB], keep = 0;
+      uint64_t m[NB];
+#pragma unroll
+      for (int it = 0; it < NB; it++) {
+        keep |= (uint32_t)(base + (uint64_t)it * 32 + lane < rows) << it;
+        if (KIND == 0)
+          idx[it] = bit_index(wv[it] >> ib, bbits, hashed);
+        else
+          wblock_key(wv[it] >> ib, seed, bbits, idx[it], m[it]);
+      }
       if (KIND == 0)
-        idx[it] = bit_index(wv[it] >> ib, bbits, hashed);
+        set_bits<true, true, NB>(reinterpret_cast<uint32_t *>(bm), idx, keep, lane);
       else
-        wblock_key(wv[it] >> ib, seed, bbits, idx[it], m[it]);
+        set_blocks<false, NB>(reinterpret_cast<unsigned long long *>(bm), idx, m, keep, lane);
     }
-    if (KIND == 0)
-      set_bits(reinterpret_cast<uint32_t *>(bm), idx, keep, lane);
-    else
-      set_blocks(reinterpret_cast<unsigned long long *>(bm), idx, m, keep, lane);
   }
 }
 
@@ -683,8 +784,12 @@ void probe_launch(const PackArgs &a, const Side &sd, const SjSeg &ws, const void
                   uint64_t *stage, uint32_t *cnt, cudaStream_t s) {
   const uint64_t rows = KM == 4 ? ws.rows : sd.rows;
   if (rows == 0) return;
-  sj_probe_stage_kernel<KM, BM, SET><<<grid_for_rows(rows), kFThreads, 0, s>>>(
-      a, sd, ws, bm, bbits, hashed, seed, bm_set, stage, cnt);
+  if constexpr (KM == 0)
+    sj_probe_stage16_kernel<KM, BM, SET><<<grid_for_rows(rows), kFThreads, 0, s>>>(
+        a, sd, ws, bm, bbits, hashed, seed, bm_set, stage, cnt);
+  else
+    sj_probe_stage_kernel<KM, BM, SET><<<grid_for_rows(rows), kFThreads, 0, s>>>(
+        a, sd, ws, bm, bbits, hashed, seed, bm_set, stage, cnt);
 }
 
 }  // namespace
