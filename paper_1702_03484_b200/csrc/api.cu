@@ -1855,16 +1855,29 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
         for (size_t r = 0; r < np; r++)
           if (all ? true : (int)r == prange[j]) TRY(wait_range((int)r));
     }
-    int jn = 0;
     const JoinStep inner = step ? *step : JoinStep([ctx](const mapsq_table *a, const mapsq_table *t,
                                                          mapsq_table *out, cudaStream_t st) {
       return join_tables(ctx, a, t, out, st);
     });
+    // a join waits for the copies of exactly the ranges its inputs' columns live in (zero-copy
+    // views of the copied predicate ranges), whatever order the fold takes them in
+    auto wait_table = [&](const mapsq_table *t) -> mapsq_status {
+      for (uint32_t c = 0; c < t->ncols; c++) {
+        const uint32_t *q = t->col[c];
+        if (!q) continue;
+        for (size_t r = 0; r < np; r++) {
+          if (!cp.ev[r]) continue;
+          const uint64_t len = h->start[r + 1] - h->start[r];
+          for (const uint32_t *base : {D.s, D.o, D.p})
+            if (q >= base + at[r] && q < base + at[r] + len) TRY(wait_range((int)r));
+        }
+      }
+      return MAPSQ_OK;
+    };
     const JoinStep waited = [&](const mapsq_table *a, const mapsq_table *t, mapsq_table *out,
                                 cudaStream_t st) -> mapsq_status {
-      ++jn;  // join jn consumes pattern jn (and pattern 0 at the first join)
-      if (jn == 1) TRY(wait_range(prange[0]));
-      if (jn < npats) TRY(wait_range(prange[jn]));
+      TRY(wait_table(a));
+      TRY(wait_table(t));
       return inner(a, t, out, st);
     };
     TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D, &waited));

@@ -508,7 +508,7 @@ sj_probe_stage_kernel(const PackArgs a, const Side sd, const SjSeg ws, const voi
             const uint64_t kp = (BM == 1) ? key_hash_final(key[it], a.kb) : (uint64_t)key[it];
             w = (kp << a.ib) | (base + (uint64_t)it * 32 + lane + sd.id0);
           }
-          __stcg(stage + wsl * kFWarpRows + r + __popc(bal & lt), w);
+          __stcs(stage + wsl * kFWarpRows + r + __popc(bal & lt), w);
         }
         r += __popc(bal);
       }
@@ -589,7 +589,7 @@ sj_probe_stage16_kernel(const PackArgs a, const Side sd, const SjSeg ws, const v
           const uint64_t kp = (BM == 1) ? key_hash_final(key[it], a.kb) : (uint64_t)key[it];
           w = (kp << a.ib) | (base + (uint64_t)it * 32 + lane + sd.id0);
         }
-        __stcg(stage + base + r + __popc(bal & lt), w);
+        __stcs(stage + base + r + __popc(bal & lt), w);
       }
       r += __popc(bal);
     }

@@ -168,6 +168,22 @@ def test_query_host_indexed_matches_device_index_and_oracle(ctx, cfg):
     assert hidx.last_h2d_bytes == expect
 
 
+def test_query_host_indexed_late_large_range(ctx):
+    """C5's last pattern (takesCourse) owns the largest predicate range: its H2D copy is still
+    streaming while the first join runs, and the second join must wait for exactly that range
+    (the join waits on the ranges its input columns live in)."""
+    s, p, o, _ = datagen.lubm(40)
+    idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    hidx = ctx.index_to_host(idx)
+    for cfg in ("C5", "C3"):
+        pats = config_query(cfg)
+        want = ctx.query(idx, pats).to_numpy()
+        for _ in range(3):
+            vars_, rows = ctx.query_host(hidx, pats, copy=True)
+            assert np.array_equal(rows, want), cfg
+    hidx.release()
+
+
 def test_query_host_indexed_edge_cases(ctx):
     rng = np.random.default_rng(3)
     n = 50_000
