@@ -457,8 +457,18 @@ def run_gpu_dist(args, world, rank, local):
 
     import paper_1702_03484_b200 as mq
     from paper_1702_03484_b200 import dist as mqd
+    # MAPSQ_BENCH_HOSTCOLL=1 (testing only: exercises this code path with several ranks on ONE
+    # GPU): every rank uses cuda:0, torch.distributed runs on gloo and the library's control plane
+    # on host collectives (mapsq_dist_init_host) — the numbers of such a run are not measurements
+    hostcoll = os.environ.get("MAPSQ_BENCH_HOSTCOLL") == "1"
+    if hostcoll:
+        local = 0
     torch.cuda.set_device(local)
-    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if hostcoll:
+        tdist.init_process_group("gloo")
+    else:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cdev = "cpu" if hostcoll else "cuda"  # device of the bench's own collective tensors
     cfg = args.config
     kind, nu, qname, desc = CONFIGS[cfg]
     if args.univ:
@@ -466,7 +476,10 @@ def run_gpu_dist(args, world, rank, local):
     ctx = mq.Context(local)
     ctx.set_option(mq.OPT_SEMIJOIN, {"auto": mq.SEMIJOIN_AUTO, "on": mq.SEMIJOIN_ON,
                                      "off": mq.SEMIJOIN_OFF}[args.semijoin])
-    mqd.ensure_dist(ctx)
+    if hostcoll:
+        ctx.dist_init_host()
+    else:
+        mqd.ensure_dist(ctx)
     if kind == "zipf":
         # C4: each rank generates its contiguous row range of both sides (identical tables for any
         # N), step = mapsq_join_dist (both sides exchanged on the key, local join)
@@ -541,7 +554,7 @@ def run_gpu_dist(args, world, rank, local):
     # time is the max over ranks
     e2e = None
     # every rank takes the same branch: the fused-exchange fallback flag is agreed on first
-    fb = torch.tensor([1 if getattr(ctx, "ipc_unavailable", None) else 0], device="cuda")
+    fb = torch.tensor([1 if getattr(ctx, "ipc_unavailable", None) else 0], device=cdev)
     tdist.all_reduce(fb, op=tdist.ReduceOp.MAX)
     if not args.no_e2e and not (hidx is not None and int(fb.item())):
         if hidx is None:
@@ -567,21 +580,21 @@ def run_gpu_dist(args, world, rank, local):
             dt = (time.perf_counter() - t0) * 1e3
             if i:
                 e2e_ms.append(dt)
-        tm = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
+        tm = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=cdev)
         tdist.all_reduce(tm, op=tdist.ReduceOp.MAX)
-        io = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
+        io = torch.tensor([h2d, d2h], dtype=torch.float64, device=cdev)
         tdist.all_reduce(io, op=tdist.ReduceOp.SUM)
         e2e = (float(tm.item()), float(io[0].item()), float(io[1].item()))
-    t = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([sum(ms)], dtype=torch.float64, device=cdev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     agg = torch.tensor([st_plain["join_in_rows"] + st_plain["join_out_rows"], st_plain["launches"],
-                        sent], dtype=torch.float64, device="cuda")
+                        sent], dtype=torch.float64, device=cdev)
     tdist.all_reduce(agg, op=tdist.ReduceOp.SUM)
     # the fused scatter (partition + NVLink stores into the peers' arenas): bytes this rank sent
     # to peers over its scatter kernels' event-timed duration (profiled region), max over ranks
     sc = st_k["kernels"].get("partition_scatter", {"ms": 0.0, "launches": 0})
     xr = torch.tensor([st_k["exchange_bytes"] / max(sc["ms"], 1e-9) / 1e6 if sc["ms"] else 0.0,
-                       sc["ms"] / args.steps], dtype=torch.float64, device="cuda")
+                       sc["ms"] / args.steps], dtype=torch.float64, device=cdev)
     xmin = xr.clone()
     tdist.all_reduce(xr, op=tdist.ReduceOp.MAX)
     tdist.all_reduce(xmin, op=tdist.ReduceOp.MIN)

@@ -126,8 +126,9 @@ def join_dist(ctx, tp1, tp2, group=None, tp1_partitioned_on=None, partition_fn: 
     key = shared_vars(tp1.vars, tp2.vars)
     if not key:
         raise mq.MapsqError(2, "join inputs share no variable")
-    if fused is None:
-        fused = partition_fn is None and dist.get_backend(group) == "nccl"
+    if fused is None:  # the library path: NCCL, or a context joined with host collectives
+        fused = partition_fn is None and (dist.get_backend(group) == "nccl" or
+                                          getattr(ctx, "dist_world", None) is not None)
     if fused and not getattr(ctx, "ipc_unavailable", None):
         ensure_dist(ctx, group)
         rs = _fused_call(ctx, lambda: ctx.join_dist(tp1, tp2))
@@ -154,8 +155,9 @@ def query_dist(ctx, triples_shard, patterns, proj=None, group=None, fused: bool 
     on), then the left-deep fold with one hash exchange per join key change, then zero-copy
     projection.  Returns this rank's shard of the result."""
     import paper_1702_03484_b200 as mq
-    if fused is None:
-        fused = dist.get_backend(group) == "nccl"
+    if fused is None:  # the library path: NCCL, or a context joined with host collectives
+        fused = (dist.get_backend(group) == "nccl" or
+                 getattr(ctx, "dist_world", None) is not None)
     if fused and not getattr(ctx, "ipc_unavailable", None):
         ensure_dist(ctx, group)
         rs = _fused_call(ctx, lambda: ctx.query_dist(triples_shard, patterns, proj))

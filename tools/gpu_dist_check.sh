@@ -16,3 +16,12 @@ for k, v in d["kernels"].items():
     print("   %-18s %3d %.3f ms/step" % (k, v["launches"], v["avg_ms"] * v["launches"] / d["steps"]))
 PY
 done
+# the bench's N > 1 code path with 2 rank processes on this one GPU (gloo + host collectives;
+# a smoke test of the JSON line, not a measurement)
+if [ "${BENCH2:-1}" = 1 ]; then
+for c in "C3 --univ 50" "C5 --univ 100" "C4 --rows 10000000"; do
+  MAPSQ_BENCH_HOSTCOLL=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29544 \
+    bench.py --gpus 2 --steps 2 --warmup 1 --no-cpu-baseline --config $c > $OUT/bench2_$(echo $c | cut -d' ' -f1).json 2> $OUT/bench2_$(echo $c | cut -d' ' -f1).err
+  echo "bench world-2 (one GPU) $c rc=$?"; tail -c 600 $OUT/bench2_$(echo $c | cut -d' ' -f1).json; tail -2 $OUT/bench2_$(echo $c | cut -d' ' -f1).err
+done
+fi
