@@ -61,8 +61,10 @@ def build_mapsq(force: bool = False) -> str:
         objs = []
         for f in cu:
             o = os.path.join(objdir, os.path.basename(f) + ".o")
+            # MAPSQ_NVCC_DEFS: extra -D flags for ablation builds (tools/gpu_ablate_*.sh)
+            extra = os.environ.get("MAPSQ_NVCC_DEFS", "").split()
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
+                  "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr", *extra,
                   "-I", os.path.join(ROOT, "include"), "-c", f, "-o", o])
             objs.append(o)
         _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-cudart", "static", "-ldl"])

@@ -25,6 +25,7 @@ OPT_WIDE_KEY, WIDE_KEY_RESIDUAL, WIDE_KEY_KV, WIDE_KEY_HASH = 1, 0, 1, 2
 OPT_SEMIJOIN, SEMIJOIN_OFF, SEMIJOIN_AUTO, SEMIJOIN_ON = 2, 0, 1, 2
 OPT_SMALL_JOIN = 3
 OPT_SKEW = 4
+OPT_HOST_COMPRESS = 5
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NO_SHARED", 3: "E_NOMEM", 4: "E_CUDA",
           5: "E_NCCL", 6: "E_UNSUPPORTED"}
 DIST_ID_BYTES = 128

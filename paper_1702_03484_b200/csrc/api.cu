@@ -1697,7 +1697,10 @@ MAPSQ_API mapsq_status mapsq_query_host(mapsq_ctx *ctx, uint64_t n, const uint32
 // ------------------------------------------------------------------ host-resident index (e2e)
 struct mapsq_host_index {
   uint64_t n = 0;
-  uint32_t *s = nullptr, *p = nullptr, *o = nullptr;  // pinned, one allocation at s
+  uint32_t *s = nullptr, *p = nullptr, *o = nullptr;  // pinned, one allocation at s (plain)
+  // compressed mirror (hoststore.cu): one frame-of-reference segment per (range, column s/p/o)
+  uint32_t *blob = nullptr;                            // pinned
+  std::vector<uint64_t> seg_off[3], seg_words[3];      // per range, in 32-bit words
   std::vector<uint32_t> pred;
   std::vector<uint64_t> start;
   std::vector<uint32_t> slo, shi, olo, ohi;
@@ -1706,8 +1709,93 @@ struct mapsq_host_index {
 MAPSQ_API void mapsq_host_index_destroy(mapsq_host_index *h) {
   if (!h) return;
   if (h->s) cudaFreeHost(h->s);
+  if (h->blob) cudaFreeHost(h->blob);
   delete h;
 }
+
+namespace mapsq {
+// Compressed mirror: per predicate range and column, frame-of-reference blocks of 1024 values
+// (hoststore.cu) — stats kernel, host layout of the segments, pack kernel, one D2H per segment.
+static mapsq_status compress_index(mapsq_ctx *ctx, const mapsq_index *idx, mapsq_host_index *h,
+                                   cudaStream_t s) {
+  const size_t np = idx->pred.size();
+  const uint32_t *cols[3] = {idx->s, idx->p, idx->o};
+  // per segment: values, blocks, block offset in the concatenated stats arrays
+  std::vector<uint64_t> nv(3 * np), nb(3 * np), b0(3 * np + 1, 0);
+  for (size_t r = 0; r < np; r++)
+    for (int c = 0; c < 3; c++) {
+      const size_t g = 3 * r + c;
+      nv[g] = idx->start[r + 1] - idx->start[r];
+      nb[g] = for_blocks(nv[g]);
+      b0[g + 1] = b0[g] + nb[g];
+    }
+  const uint64_t NB = b0[3 * np];
+  Scratch sc(ctx, s);
+  uint32_t *dbase = sc.get<uint32_t>(NB + 1), *dbits = sc.get<uint32_t>(NB + 1);
+  uint32_t *dwoff = sc.get<uint32_t>(NB + 3 * np + 1);
+  NEED(dbase); NEED(dbits); NEED(dwoff);
+  for (size_t r = 0; r < np; r++)
+    for (int c = 0; c < 3; c++) {
+      const size_t g = 3 * r + c;
+      launch_for_stats(cols[c] + idx->start[r], nv[g], dbase + b0[g], dbits + b0[g], s);
+    }
+  CK(cudaGetLastError());
+  std::vector<uint32_t> hbase(NB), hbits(NB);
+  CK(cudaMemcpyAsync(hbase.data(), dbase, 4 * NB, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hbits.data(), dbits, 4 * NB, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // segment layout: base[nb] | bits[nb] | woff[nb + 1] | payload
+  std::vector<uint64_t> soff(3 * np + 1, 0), pay(3 * np);
+  std::vector<uint32_t> hwoff(NB + 3 * np);
+  for (size_t g = 0; g < 3 * np; g++) {
+    uint64_t w = 0;
+    for (uint64_t b = 0; b < nb[g]; b++) {
+      hwoff[b0[g] + g + b] = (uint32_t)w;
+      w += for_block_words(hbits[b0[g] + b]);
+    }
+    hwoff[b0[g] + g + nb[g]] = (uint32_t)w;
+    if (w >> 32) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "compressed segment over 16 GB");
+    pay[g] = w;
+    soff[g + 1] = soff[g] + 3 * nb[g] + 1 + w;
+  }
+  const uint64_t total = soff[3 * np];
+  void *blob = nullptr;
+  CK(cudaMallocHost(&blob, 4 * std::max<uint64_t>(total, 1)));
+  h->blob = static_cast<uint32_t *>(blob);
+  for (int c = 0; c < 3; c++) {
+    h->seg_off[c].resize(np);
+    h->seg_words[c].resize(np);
+  }
+  for (size_t r = 0; r < np; r++)
+    for (int c = 0; c < 3; c++) {
+      const size_t g = 3 * r + c;
+      uint32_t *seg = h->blob + soff[g];
+      std::memcpy(seg, hbase.data() + b0[g], 4 * nb[g]);
+      std::memcpy(seg + nb[g], hbits.data() + b0[g], 4 * nb[g]);
+      std::memcpy(seg + 2 * nb[g], hwoff.data() + b0[g] + g, 4 * (nb[g] + 1));
+      h->seg_off[c][r] = soff[g];
+      h->seg_words[c][r] = soff[g + 1] - soff[g];
+    }
+  // pack every segment's payload on the device, then copy it into the pinned blob
+  uint64_t maxpay = 0;
+  for (uint64_t w : pay) maxpay = std::max(maxpay, w);
+  uint32_t *dpay = sc.get<uint32_t>(maxpay + 1);
+  NEED(dpay);
+  CK(cudaMemcpyAsync(dwoff, hwoff.data(), 4 * (NB + 3 * np), cudaMemcpyHostToDevice, s));
+  for (size_t r = 0; r < np; r++)
+    for (int c = 0; c < 3; c++) {
+      const size_t g = 3 * r + c;
+      if (!pay[g]) continue;
+      launch_for_pack(cols[c] + idx->start[r], nv[g], dbase + b0[g], dbits + b0[g],
+                      dwoff + b0[g] + g, dpay, s);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h->blob + soff[g] + 3 * nb[g] + 1, dpay, 4 * pay[g],
+                         cudaMemcpyDeviceToHost, s));
+    }
+  CK(cudaStreamSynchronize(s));
+  return MAPSQ_OK;
+}
+}  // namespace mapsq
 
 MAPSQ_API mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *idx,
                                            mapsq_host_index **out, void *stream) {
@@ -1723,7 +1811,9 @@ MAPSQ_API mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *id
   h->shi = idx->shi;
   h->olo = idx->olo;
   h->ohi = idx->ohi;
-  if (idx->n) {
+  if (idx->n && ctx->host_compress) {
+    TRY(compress_index(ctx, idx, h.get(), S(stream)));
+  } else if (idx->n) {
     void *p = nullptr;
     CK(cudaMallocHost(&p, 12 * idx->n));
     h->s = static_cast<uint32_t *>(p);
@@ -1796,12 +1886,21 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
           if (e) cudaEventDestroy(e);
       }
     } cp{cs, std::vector<cudaEvent_t>(np + 1, nullptr)};
-    uint64_t rows = 0;
+    uint64_t rows = 0, cwords = 0;
     for (size_t r = 0; r < np; r++)
-      if (all || need[r]) rows += h->start[r + 1] - h->start[r];
+      if (all || need[r]) {
+        rows += h->start[r + 1] - h->start[r];
+        if (h->blob)
+          cwords += h->seg_words[0][r] + h->seg_words[2][r] +
+                    ((all || need[r] == 2) ? h->seg_words[1][r] : 0);
+      }
     const uint64_t stride = (rows + 3) & ~3ull;
     uint32_t *d = sc.get<uint32_t>(3 * stride + 12);
     NEED(d);
+    // compressed mirror: the touched segments land here and are expanded into D's columns
+    uint32_t *cstage = h->blob ? sc.get<uint32_t>(cwords + 4) : nullptr;
+    if (h->blob) NEED(cstage);
+    uint64_t cpos = 0;
     D.n = rows;
     D.s = d;
     D.p = d + stride;
@@ -1824,12 +1923,27 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
     CK(cudaStreamWaitEvent(cs, cp.ev[np], 0));
     auto copy_range = [&](size_t r) -> mapsq_status {
       const uint64_t b = h->start[r], c = h->start[r + 1] - b;
-      CK(cudaMemcpyAsync(D.s + at[r], h->s + b, 4 * c, cudaMemcpyHostToDevice, cs));
-      CK(cudaMemcpyAsync(D.o + at[r], h->o + b, 4 * c, cudaMemcpyHostToDevice, cs));
-      bytes += 8 * c;
-      if (all || need[r] == 2) {
-        CK(cudaMemcpyAsync(D.p + at[r], h->p + b, 4 * c, cudaMemcpyHostToDevice, cs));
-        bytes += 4 * c;
+      const bool with_p = all || need[r] == 2;
+      if (h->blob) {  // compressed segments: copy, then expand on the copy stream
+        for (int col : {0, 2, 1}) {
+          if (col == 1 && !with_p) continue;
+          uint32_t *dst = col == 0 ? D.s : (col == 1 ? D.p : D.o);
+          const uint64_t w = h->seg_words[col][r];
+          CK(cudaMemcpyAsync(cstage + cpos, h->blob + h->seg_off[col][r], 4 * w,
+                             cudaMemcpyHostToDevice, cs));
+          launch_for_unpack(cstage + cpos, c, dst + at[r], cs);
+          CK(cudaGetLastError());
+          cpos += w;
+          bytes += 4 * w;
+        }
+      } else {
+        CK(cudaMemcpyAsync(D.s + at[r], h->s + b, 4 * c, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(D.o + at[r], h->o + b, 4 * c, cudaMemcpyHostToDevice, cs));
+        bytes += 8 * c;
+        if (with_p) {
+          CK(cudaMemcpyAsync(D.p + at[r], h->p + b, 4 * c, cudaMemcpyHostToDevice, cs));
+          bytes += 4 * c;
+        }
       }
       CK(cudaEventCreateWithFlags(&cp.ev[r], cudaEventDisableTiming));
       CK(cudaEventRecord(cp.ev[r], cs));
@@ -2278,6 +2392,10 @@ MAPSQ_API mapsq_status mapsq_set_option(mapsq_ctx *ctx, int option, int64_t valu
   }
   if (option == MAPSQ_OPT_SKEW && (value == 0 || value == 1)) {
     ctx->skew = value != 0;
+    return MAPSQ_OK;
+  }
+  if (option == MAPSQ_OPT_HOST_COMPRESS && (value == 0 || value == 1)) {
+    ctx->host_compress = value != 0;
     return MAPSQ_OK;
   }
   return set_error(ctx, MAPSQ_E_INVALID, "unknown option or value");

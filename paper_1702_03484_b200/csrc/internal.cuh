@@ -54,6 +54,7 @@ struct mapsq_ctx {
   int semijoin = MAPSQ_SEMIJOIN_AUTO;
   bool small_joins = true;  // MAPSQ_OPT_SMALL_JOIN: one-CTA path for joins of <= 4096 rows
   bool skew = true;         // MAPSQ_OPT_SKEW: heavy keys split / broadcast in distributed joins
+  bool host_compress = true;  // MAPSQ_OPT_HOST_COMPRESS: mapsq_index_to_host compresses the mirror
   std::vector<mapsq::PendingTiming> pending;
   std::vector<cudaEvent_t> free_events;
   std::map<std::string, mapsq::KAgg> kagg;
@@ -451,6 +452,15 @@ void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t 
                            cudaStream_t s);
 void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t bbits,
                             const void *bm, unsigned long long *sample, cudaStream_t s);
+
+// Compressed host store (hoststore.cu): frame-of-reference blocks of 1024 values.
+uint64_t for_blocks(uint64_t n);
+uint64_t for_block_words(uint32_t bits);
+void launch_for_stats(const uint32_t *col, uint64_t n, uint32_t *base, uint32_t *bits,
+                      cudaStream_t s);
+void launch_for_pack(const uint32_t *col, uint64_t n, const uint32_t *base, const uint32_t *bits,
+                     const uint32_t *woff, uint32_t *payload, cudaStream_t s);
+void launch_for_unpack(const uint32_t *seg, uint64_t n, uint32_t *out, cudaStream_t s);
 
 // Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
 // (unordered, atomic slots < cap); per-run bounds [slo | olo | shi | ohi].

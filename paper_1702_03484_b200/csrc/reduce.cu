@@ -20,7 +20,10 @@ namespace mapsq {
 namespace {
 
 constexpr int kGThreads = 256;
-constexpr int kGItems = 32;
+#ifndef MAPSQ_G_ITEMS
+#define MAPSQ_G_ITEMS 32
+#endif
+constexpr int kGItems = MAPSQ_G_ITEMS;  // words per lane per warp slice
 constexpr uint64_t kGTile = kGThreads * kGItems;
 constexpr int kGWarps = kGThreads / 32;
 constexpr int kGSlice = 32 * kGItems;       // elements per warp slice
@@ -86,8 +89,11 @@ find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restr
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_nrec[kGWarps];
   __shared__ uint64_t s_base;
-  __shared__ uint32_t s_start[kGWarps][kGMaxRec], s_end[kGWarps][kGMaxRec];
-  __shared__ uint16_t s_split[kGWarps][kGMaxRec];  // offset inside the warp's slice
+  // per-warp record buffers (dynamic shared memory: kGWarps x kGMaxRec each)
+  extern __shared__ __align__(16) unsigned char g_smem[];
+  auto s_start = reinterpret_cast<uint32_t (*)[kGMaxRec]>(g_smem);
+  auto s_end = reinterpret_cast<uint32_t (*)[kGMaxRec]>(g_smem + sizeof(uint32_t) * kGWarps * kGMaxRec);
+  auto s_split = reinterpret_cast<uint16_t (*)[kGMaxRec]>(g_smem + 2 * sizeof(uint32_t) * kGWarps * kGMaxRec);
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
@@ -581,11 +587,14 @@ void launch_find_groups(const uint64_t *words, const uint64_t *keys, const uint3
   W.ib = ib;
   W.idx_mask = (ib >= 64) ? ~0ull : ((1ull << ib) - 1);
   const uint64_t ntiles = ceil_div(n, kGTile);
+  constexpr size_t smem = (2 * sizeof(uint32_t) + sizeof(uint16_t)) * kGWarps * kGMaxRec;
+  set_smem_limit((const void *)find_groups_kernel<false>, smem);
+  set_smem_limit((const void *)find_groups_kernel<true>, smem);
   if (words)
-    find_groups_kernel<false><<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
+    find_groups_kernel<false><<<(unsigned)ntiles, kGThreads, smem, s>>>(W, n, g, status, tile_counter,
                                                                    ngroups_dev);
   else
-    find_groups_kernel<true><<<(unsigned)ntiles, kGThreads, 0, s>>>(W, n, g, status, tile_counter,
+    find_groups_kernel<true><<<(unsigned)ntiles, kGThreads, smem, s>>>(W, n, g, status, tile_counter,
                                                                   ngroups_dev);
 }
 

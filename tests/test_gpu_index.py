@@ -149,15 +149,11 @@ def test_query_host_indexed_matches_device_index_and_oracle(ctx, cfg):
     and copies exactly the bytes its contract states."""
     s, p, o, _ = datagen.lubm(2)
     idx = ctx.index_build((dev(s), dev(p), dev(o)))
-    hidx = ctx.index_to_host(idx)
     pats = config_query(cfg)
     want = ctx.query(idx, pats).to_numpy()
-    vars_, rows = ctx.query_host(hidx, pats, copy=True)
-    assert np.array_equal(rows, want)
     ref = oracle.query(s, p, o, pats)
-    assert vars_ == ref.vars
-    assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows)
-    # bytes: 8 per row of every touched predicate (s, o), +4 where a pattern scans the range
+    # bytes of the plain mirror: 8 per row of every touched predicate (s, o), +4 where a pattern
+    # scans the range; the compressed mirror (default) copies fewer and expands them losslessly
     need = {}
     for pat in pats:
         (ks, _), (kp, pid), (ko, _) = pat
@@ -165,7 +161,19 @@ def test_query_host_indexed_matches_device_index_and_oracle(ctx, cfg):
             view = ks == V and ko == V and pat[0][1] != pat[2][1]
             need[pid] = max(need.get(pid, 0), 8 if view else 12)
     expect = sum(b * (idx.range(pid)[1] - idx.range(pid)[0]) for pid, b in need.items())
-    assert hidx.last_h2d_bytes == expect
+    for compress in (0, 1):
+        ctx.set_option(mq.OPT_HOST_COMPRESS, compress)
+        hidx = ctx.index_to_host(idx)
+        vars_, rows = ctx.query_host(hidx, pats, copy=True)
+        assert np.array_equal(rows, want), compress
+        assert vars_ == ref.vars
+        assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows)
+        if compress:
+            assert 0 < hidx.last_h2d_bytes < expect
+        else:
+            assert hidx.last_h2d_bytes == expect
+        hidx.release()
+    ctx.set_option(mq.OPT_HOST_COMPRESS, 1)
 
 
 def test_query_host_indexed_late_large_range(ctx):
@@ -184,6 +192,32 @@ def test_query_host_indexed_late_large_range(ctx):
     hidx.release()
 
 
+def test_compressed_host_mirror_codec_edges(ctx):
+    """The compressed mirror is lossless at every block width: full 32-bit ranges (bits = 32), a
+    constant column (bits = 0), ranges of 1 and 1025 rows, a block boundary inside a range."""
+    rng = np.random.default_rng(17)
+    parts = [
+        np.stack([rng.integers(0, 1 << 32, 5000, dtype=np.uint64), np.full(5000, 0),
+                  rng.integers(0, 1 << 32, 5000, dtype=np.uint64)], 1),            # 32-bit
+        np.stack([np.full(1025, 7), np.full(1025, 1), np.arange(1025) * 3 + 1], 1),  # bits 0 / 12
+        np.array([[5, 2, 9]]),                                                       # one row
+        np.stack([np.arange(3000) // 3, np.full(3000, 3), rng.integers(0, 77, 3000)], 1),
+    ]
+    T = np.unique(np.concatenate(parts).astype(np.uint32), axis=0)
+    s, p, o = (np.ascontiguousarray(T[:, j]) for j in range(3))
+    idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    ctx.set_option(mq.OPT_HOST_COMPRESS, 1)
+    hidx = ctx.index_to_host(idx)
+    for pid in range(4):
+        pats = [((V, 0), (C, pid), (V, 1))]
+        want = ctx.query(idx, pats).to_numpy()
+        _, rows = ctx.query_host(hidx, pats, copy=True)
+        assert np.array_equal(rows, want), pid
+    _, rows = ctx.query_host(hidx, [((V, 0), (V, 1), (V, 2))], copy=True)   # every range, p too
+    assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical_rows(T))
+    hidx.release()
+
+
 def test_query_host_indexed_edge_cases(ctx):
     rng = np.random.default_rng(3)
     n = 50_000
@@ -191,7 +225,10 @@ def test_query_host_indexed_edge_cases(ctx):
     T = np.unique(T.astype(np.uint32), axis=0)
     s, p, o = (np.ascontiguousarray(T[:, j]) for j in range(3))
     idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    ctx.set_option(mq.OPT_HOST_COMPRESS, 0)  # (the byte count below is the plain mirror's)
     hidx = ctx.index_to_host(idx)
+    ctx.set_option(mq.OPT_HOST_COMPRESS, 1)
+    hidx_c = ctx.index_to_host(idx)
     cases = [
         [((V, 0), (C, 3), (V, 1))],                                  # one view: result is a view
         [((V, 0), (V, 1), (V, 2))],                                  # variable predicate: all rows
@@ -200,10 +237,12 @@ def test_query_host_indexed_edge_cases(ctx):
         [((V, 0), (C, 2), (C, 17)), ((V, 0), (C, 5), (V, 1)), ((V, 1), (C, 5), (V, 2))],
     ]
     for pats in cases:
-        vars_, rows = ctx.query_host(hidx, pats, copy=True)
         ref = oracle.query(s, p, o, pats)
-        assert vars_ == ref.vars
-        assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), pats
+        for hx in (hidx, hidx_c):
+            vars_, rows = ctx.query_host(hx, pats, copy=True)
+            assert vars_ == ref.vars
+            assert np.array_equal(oracle.canonical_rows(rows), oracle.canonical(ref).rows), pats
     ctx.query_host(hidx, [((V, 0), (V, 1), (V, 2))])
     assert hidx.last_h2d_bytes == 12 * len(s)
     hidx.release()
+    hidx_c.release()
