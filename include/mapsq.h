@@ -262,7 +262,7 @@ mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
  * The paper's division of labour: the store answers partial matching on the host and the GPU
  * joins the partial matches.  mapsq_index_to_host mirrors an index into
  * pinned host memory (blocking, once per dataset): by default compressed (MAPSQ_OPT_HOST_COMPRESS:
- * frame-of-reference blocks of 1024 values per range and column, expanded on the GPU after the
+ * frame-of-reference or delta blocks of 128 values per range and column, expanded on the GPU after the
  * copy — lossless), else 12 B per triple + metadata.
  * mapsq_query_host_indexed answers a query from that mirror: it copies to the device ONLY the
  * predicate ranges the query's patterns touch (s and o of every constant-predicate range; p too
@@ -451,8 +451,9 @@ mapsq_status mapsq_table_bounds(mapsq_ctx *ctx, mapsq_table *t, void *stream);
 /* Distributed joins: heavy keys (estimated from a sample to exceed max(1024, N / (4 world)) rows)
  * keep one side's rows on their rank and broadcast the other side's rows to every rank. */
 #define MAPSQ_OPT_SKEW 4          /*   1 (default) / 0 */
-/* mapsq_index_to_host keeps every column of every predicate range as frame-of-reference blocks of
- * 1024 values (a block's minimum + offsets in the fewest bits that hold them); the host-indexed
+/* mapsq_index_to_host keeps every column of every predicate range as blocks of 128 values, each in
+ * the narrower of two codings (a block's minimum + offsets, or its first value + deltas, in the
+ * fewest bits that hold them); the host-indexed
  * query copies the touched blocks and expands them on the GPU (lossless).  0: plain 32-bit
  * columns (12 B per triple).  Read when the mirror is made. */
 #define MAPSQ_OPT_HOST_COMPRESS 5 /*   1 (default) / 0 */

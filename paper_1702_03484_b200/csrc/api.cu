@@ -1732,19 +1732,22 @@ static mapsq_status compress_index(mapsq_ctx *ctx, const mapsq_index *idx, mapsq
   const uint64_t NB = b0[3 * np];
   Scratch sc(ctx, s);
   uint32_t *dbase = sc.get<uint32_t>(NB + 1), *dbits = sc.get<uint32_t>(NB + 1);
+  uint32_t *ddmin = sc.get<uint32_t>(NB + 1);
   uint32_t *dwoff = sc.get<uint32_t>(NB + 3 * np + 1);
-  NEED(dbase); NEED(dbits); NEED(dwoff);
+  NEED(dbase); NEED(dbits); NEED(ddmin); NEED(dwoff);
   for (size_t r = 0; r < np; r++)
     for (int c = 0; c < 3; c++) {
       const size_t g = 3 * r + c;
-      launch_for_stats(cols[c] + idx->start[r], nv[g], dbase + b0[g], dbits + b0[g], s);
+      launch_for_stats(cols[c] + idx->start[r], nv[g], dbase + b0[g], dbits + b0[g],
+                       ddmin + b0[g], s);
     }
   CK(cudaGetLastError());
-  std::vector<uint32_t> hbase(NB), hbits(NB);
+  std::vector<uint32_t> hbase(NB), hbits(NB), hdmin(NB);
   CK(cudaMemcpyAsync(hbase.data(), dbase, 4 * NB, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hbits.data(), dbits, 4 * NB, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hdmin.data(), ddmin, 4 * NB, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  // segment layout: base[nb] | bits[nb] | woff[nb + 1] | payload
+  // segment layout: base[nb] | mode_bits[nb] | dmin[nb] | woff[nb + 1] | payload
   std::vector<uint64_t> soff(3 * np + 1, 0), pay(3 * np);
   std::vector<uint32_t> hwoff(NB + 3 * np);
   for (size_t g = 0; g < 3 * np; g++) {
@@ -1756,7 +1759,7 @@ static mapsq_status compress_index(mapsq_ctx *ctx, const mapsq_index *idx, mapsq
     hwoff[b0[g] + g + nb[g]] = (uint32_t)w;
     if (w >> 32) return set_error(ctx, MAPSQ_E_UNSUPPORTED, "compressed segment over 16 GB");
     pay[g] = w;
-    soff[g + 1] = soff[g] + 3 * nb[g] + 1 + w;
+    soff[g + 1] = soff[g] + 4 * nb[g] + 1 + w;
   }
   const uint64_t total = soff[3 * np];
   void *blob = nullptr;
@@ -1772,7 +1775,8 @@ static mapsq_status compress_index(mapsq_ctx *ctx, const mapsq_index *idx, mapsq
       uint32_t *seg = h->blob + soff[g];
       std::memcpy(seg, hbase.data() + b0[g], 4 * nb[g]);
       std::memcpy(seg + nb[g], hbits.data() + b0[g], 4 * nb[g]);
-      std::memcpy(seg + 2 * nb[g], hwoff.data() + b0[g] + g, 4 * (nb[g] + 1));
+      std::memcpy(seg + 2 * nb[g], hdmin.data() + b0[g], 4 * nb[g]);
+      std::memcpy(seg + 3 * nb[g], hwoff.data() + b0[g] + g, 4 * (nb[g] + 1));
       h->seg_off[c][r] = soff[g];
       h->seg_words[c][r] = soff[g + 1] - soff[g];
     }
@@ -1787,9 +1791,9 @@ static mapsq_status compress_index(mapsq_ctx *ctx, const mapsq_index *idx, mapsq
       const size_t g = 3 * r + c;
       if (!pay[g]) continue;
       launch_for_pack(cols[c] + idx->start[r], nv[g], dbase + b0[g], dbits + b0[g],
-                      dwoff + b0[g] + g, dpay, s);
+                      ddmin + b0[g], dwoff + b0[g] + g, dpay, s);
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(h->blob + soff[g] + 3 * nb[g] + 1, dpay, 4 * pay[g],
+      CK(cudaMemcpyAsync(h->blob + soff[g] + 4 * nb[g] + 1, dpay, 4 * pay[g],
                          cudaMemcpyDeviceToHost, s));
     }
   CK(cudaStreamSynchronize(s));

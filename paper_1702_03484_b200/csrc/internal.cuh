@@ -457,9 +457,10 @@ void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t
 uint64_t for_blocks(uint64_t n);
 uint64_t for_block_words(uint32_t bits);
 void launch_for_stats(const uint32_t *col, uint64_t n, uint32_t *base, uint32_t *bits,
-                      cudaStream_t s);
+                      uint32_t *dmin, cudaStream_t s);
 void launch_for_pack(const uint32_t *col, uint64_t n, const uint32_t *base, const uint32_t *bits,
-                     const uint32_t *woff, uint32_t *payload, cudaStream_t s);
+                     const uint32_t *dmin, const uint32_t *woff, uint32_t *payload,
+                     cudaStream_t s);
 void launch_for_unpack(const uint32_t *seg, uint64_t n, uint32_t *out, cudaStream_t s);
 
 // Predicate index (index.cu): permute s/p/o by the sorted words, record predicate run heads
