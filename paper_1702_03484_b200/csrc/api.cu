@@ -477,10 +477,13 @@ uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(
 // the smaller side's bitmap (survivors staged per 512-row slice in the stage buffer), scan its
 // slice counts and gather its survivors into their segment, set bm_L from those words, then the
 // same for the smaller side against bm_L; one blocking read of the two survivor counts.
+// carry[side] (n, src set by the caller): columns to carry through the column round (SjCarry);
+// on return carry[side].n is 0 unless they were carried (out[] then holds the side's survivors'
+// values, allocated from sc, and the words' row ids index them).
 mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *a,
                         const mapsq_table *b, Scratch &sc, cudaStream_t s, uint64_t *&cur,
                         uint64_t *&alt, uint32_t *hist, uint64_t *nA_out, uint64_t *offB_out,
-                        uint64_t *nB_out) {
+                        uint64_t *nB_out, SjCarry carry[2]) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
   PackArgs pa = pack_args(pl, a, b);
   const uint64_t bmw = std::max<uint64_t>(
@@ -516,7 +519,12 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   // scan one side's slice counts (slices [sl0, sl0 + nsl)) and gather its staged survivors to
   // out; fsc[side] receives their number
   std::vector<size_t> gpos;
-  auto scan_gather = [&](int side, uint64_t sl0, uint64_t nsl, uint64_t *out) -> mapsq_status {
+  SjCarry none;
+  none.n = 0;
+  const SjCarry use[2] = {carry[0], carry[1]};  // (n cleared below unless the column round carries)
+  carry[0].n = carry[1].n = 0;
+  auto scan_gather = [&](int side, uint64_t sl0, uint64_t nsl, uint64_t *out,
+                         const SjCarry &cr = SjCarry{}) -> mapsq_status {
     {
       KTimer kt(ctx, s, "filter_scan", 12ull * nsl, 3);
       launch_exclusive_scan_u32(cnt + sl0, off + sl0, nsl, ftmp, fsc + side, s);
@@ -525,7 +533,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     {
       KTimer kt(ctx, s, "filter_gather", 12ull * nsl);
       launch_sj_gather(stage + sl0 * kSjSlice, cnt + sl0, off + sl0, nsl, out,
-                       pl.passes ? hist : nullptr, pl.ib, dmask, s);
+                       pl.passes ? hist : nullptr, pl.ib, dmask, cr, pl.ib, side ? n1 : 0, s);
       CKL("filter_gather");
     }
     gpos.push_back(pending_pos());
@@ -533,7 +541,9 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   };
   // the round's one blocking read: both sides' survivors; the staged / gathered bytes go to the
   // probe and gather timers
-  auto read_counts = [&](size_t posL, size_t posS, size_t posSet, int sideL) -> mapsq_status {
+  // (ncL / ncS: columns carried by L / S — 4 B read + 4 B written per survivor in the gather)
+  auto read_counts = [&](size_t posL, size_t posS, size_t posSet, int sideL, uint32_t ncL = 0,
+                         uint32_t ncS = 0) -> mapsq_status {
     TRY(ensure_pinned(ctx, 2));
     CK(cudaMemcpyAsync(ctx->pinned, fsc, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -543,8 +553,8 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     add_bytes(posS, 8ull * survS);
     add_bytes(posSet, 8ull * survL);
     if (gpos.size() == 2) {
-      add_bytes(gpos[0], 16ull * survL);
-      add_bytes(gpos[1], 16ull * survS);
+      add_bytes(gpos[0], (16ull + 8ull * ncL) * survL);
+      add_bytes(gpos[1], (16ull + 8ull * ncS) * survS);
     }
     gpos.clear();
     if (debug_on())
@@ -581,6 +591,26 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     if (!skipped) {
       const uint64_t slA = sj_slices(n1), slB = sj_slices(n2);
       const uint64_t seedL = word_round_seed(0);
+      // carried columns (MAPSQ_SJ_CARRY: 0 off, 1 on, 2 = auto: exact bitmaps — this round is the
+      // last, its survivors are exactly the rows ReduceDuplicate reads — and the sampled probe
+      // kept at most half of the larger side; after a hashed round the word rounds still drop
+      // most survivors (C5 J2: 49.5 M -> 9.5 M), so carrying for all of them does not pay)
+      const uint64_t ssurv = ctx->pinned[0], srows = ctx->pinned[1];
+      const uint32_t cmode = env_u32("MAPSQ_SJ_CARRY", 2);
+      const bool do_carry = cmode == 1 || (cmode == 2 && !hashed && !colhash && srows > 0 &&
+                                           2 * ssurv <= srows);
+      SjCarry cr[2] = {none, none};
+      if (do_carry) {
+        for (int sd = 0; sd < 2; sd++) {
+          for (uint32_t c = 0; c < use[sd].n; c++) {
+            cr[sd].src[c] = use[sd].src[c];
+            cr[sd].out[c] = sc.get<uint32_t>(sd ? n2 : n1);
+            NEED(cr[sd].out[c]);
+          }
+          cr[sd].n = use[sd].n;
+          carry[sd] = cr[sd];
+        }
+      }
       // plain bitmaps: L's survivors set bm_L while probed (bit = key'); hashed composite keys:
       // bm_L (a wblock of the survivors' key') is set from L's gathered survivor words
       const bool set_in_probe = !colhash;
@@ -595,7 +625,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
         CKL("filter_probe");
       }
       posL = pending_pos();
-      TRY(scan_gather(sideL, sideL ? slA : 0, sideL ? slB : slA, outL));
+      TRY(scan_gather(sideL, sideL ? slA : 0, sideL ? slB : slA, outL, cr[sideL]));
       if (!set_in_probe) {
         KTimer kt(ctx, s, "filter_set", 0);
         launch_sj_set_words(outL, fsc + sideL, nL, 2, bmL, pl.ib, bbits, 0, seedL, s);
@@ -609,9 +639,9 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
         CKL("filter_probe");
       }
       posS = pending_pos();
-      TRY(scan_gather(sideS, sideS ? slA : 0, sideS ? slB : slA, outS));
+      TRY(scan_gather(sideS, sideS ? slA : 0, sideS ? slB : slA, outS, cr[sideS]));
       ctx->counters.filter_accesses += nL + nS;
-      TRY(read_counts(posL, posS, posSet, sideL));
+      TRY(read_counts(posL, posS, posSet, sideL, cr[sideL].n, cr[sideS].n));
       nA = ctx->pinned[0];
       nB = ctx->pinned[1];
       offB = n1;
@@ -834,9 +864,25 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     ctx->counters.last_kb = pl.kb;
     ctx->counters.last_passes = pl.passes;
   }
+  const bool residual = pl.path == MAPSQ_PATH_RESIDUAL || pl.path == MAPSQ_PATH_HASH;
+  uint64_t rowsA = n1, rowsB = n2;  // rows of the columns ReduceDuplicate gathers from
   if (filt) {
+    // the columns ReduceDuplicate reads by row id, offered to the filter to carry: every column
+    // (verification reads the shared ones too) or the non-key columns (expand decodes the key)
+    SjCarry carry[2];
+    uint32_t ccol[2][MAPSQ_MAX_COLS];
+    for (int sd = 0; sd < 2; sd++) {
+      const mapsq_table &t = sd ? b : a;
+      carry[sd].n = 0;
+      const uint32_t nr = sd ? pl.nrest2 : pl.nrest1;
+      for (uint32_t c = 0; c < (residual ? t.ncols : nr); c++) {
+        const uint32_t j = residual ? c : (sd ? pl.rest_col2[c] : pl.rest_col1[c]);
+        ccol[sd][carry[sd].n] = j;
+        carry[sd].src[carry[sd].n++] = t.col[j];
+      }
+    }
     uint64_t nA = 0, offB = 0, nB = 0;
-    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB));
+    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB, carry));
     nw = nA + nB;
     seg_n0 = nA;
     seg_gap = offB - nA;
@@ -844,6 +890,12 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     if (nA == 0 || nB == 0) {  // a side without survivors: no key on both sides
       fill_empty_join(pl, &a, &b, rs);
       return MAPSQ_OK;
+    }
+    // carried: the words' row ids now index the survivors' dense columns (side B's from n1 on)
+    for (int sd = 0; sd < 2; sd++) {
+      mapsq_table &t = sd ? b : a;
+      for (uint32_t c = 0; c < carry[sd].n; c++) t.col[ccol[sd][c]] = carry[sd].out[c];
+      if (carry[sd].n) (sd ? rowsB : rowsA) = sd ? nB : nA;
     }
   } else {
     const PackArgs pa = pack_args(pl, &a, &b);
@@ -879,7 +931,6 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   }
   // RESIDUAL and HASH: the nL * nR pairs of a key' group are candidates, verified on the shared
   // columns not (exactly) in key'
-  const bool residual = pl.path == MAPSQ_PATH_RESIDUAL || pl.path == MAPSQ_PATH_HASH;
   {
     KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
     launch_exclusive_scan_u64_dev(gc, go, scal, cap, tmp, scal + 1, s);
@@ -1007,7 +1058,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     ea.tile_g0 = sc.get<uint64_t>(expand_tiles(m) + 1);
     NEED(ea.tile_g0);
     const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * nw +
-                           4ull * (n1 * pl.nrest1 + n2 * pl.nrest2);
+                           4ull * (rowsA * pl.nrest1 + rowsB * pl.nrest2);
     KTimer kt(ctx, s, "expand", bytes, 2);
     launch_expand(ea, s);
     cudaError_t e = cudaGetLastError();

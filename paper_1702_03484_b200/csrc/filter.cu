@@ -25,12 +25,17 @@
 namespace mapsq {
 namespace {
 
+#ifndef MAPSQ_G_ROWS
+#define MAPSQ_G_ROWS 8
+#endif
 constexpr int kFThreads = 256;
 constexpr int kFWarps = kFThreads / 32;
 constexpr int kFItems = 16;                    // rows per lane per slice
 constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
 constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice
+constexpr int kGSlices = 8;                    // slices per warp iteration of the gather
+constexpr int kGRows = MAPSQ_G_ROWS;           // rows per lane in flight in the gather
 
 // MODE 0: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic); 1: generic
 // packed composite key; 2: PATH_HASH key over exactly 2 columns; 3: PATH_HASH over nkey columns.
@@ -606,10 +611,15 @@ sj_probe_stage16_kernel(const PackArgs a, const Side sd, const SjSeg ws, const v
 // Gather: slice s's staged survivors (cnt[s] words at stage[s * 512 ..]) go to out[off[s] ..]
 // (the exclusive scan of the counts over side A's slices then side B's: the output is
 // contiguous, side A first, row order kept); digit 0 of the words is counted into hist.
+// With CARRY the survivors' values of the carried columns are gathered too (by the staged word's
+// row id: ascending within a slice, so a warp's loads share lines) into out[c][position], and each
+// word's row id becomes its position + id0 (side B's offset by n1).
+template <bool CARRY>
 __global__ void __launch_bounds__(kFThreads)
 sj_gather_kernel(const uint64_t *__restrict__ stage, const uint32_t *__restrict__ cnt,
                  const uint64_t *__restrict__ off, uint64_t nslices, uint64_t *__restrict__ out,
-                 uint32_t *__restrict__ hist, uint32_t bit_lo, uint32_t dmask) {
+                 uint32_t *__restrict__ hist, uint32_t bit_lo, uint32_t dmask, const SjCarry cr,
+                 uint32_t ib, uint64_t id0) {
   __shared__ uint32_t s_h[kFCopies][kRadix];
   if (hist)
     for (uint32_t i = threadIdx.x; i < kFCopies * kRadix; i += kFThreads) (&s_h[0][0])[i] = 0;
@@ -617,25 +627,65 @@ sj_gather_kernel(const uint64_t *__restrict__ stage, const uint32_t *__restrict_
   const uint32_t lane = threadIdx.x & 31;
   uint32_t *h = s_h[(threadIdx.x >> 5) % kFCopies];
   const uint64_t nwarps = (uint64_t)gridDim.x * kFWarps;
-  for (uint64_t sl = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); sl < nslices;
-       sl += nwarps) {
-    const uint32_t c = __ldg(cnt + sl);
-    if (c == 0) continue;  // warp-uniform
-    const uint64_t pos = __ldg(off + sl);
-    const uint64_t *src = stage + sl * kFWarpRows;
-    for (uint32_t r0 = 0; r0 < c; r0 += 4 * 32) {  // 4 rows per lane in flight
-      uint64_t w[4];
+  const uint64_t imask = (1ull << ib) - 1;
+  // a warp moves the survivors of kGSlices consecutive slices per iteration as ONE flat list (a
+  // slice keeps ~36 of its 512 rows on C4: per-slice loops left the loads of a warp nearly
+  // serial); their output positions are contiguous: off[s0] + flat index
+  const uint64_t ngrp = (nslices + kGSlices - 1) / kGSlices;
+  for (uint64_t g = (uint64_t)blockIdx.x * kFWarps + (threadIdx.x >> 5); g < ngrp; g += nwarps) {
+    const uint64_t s0 = g * kGSlices;
+    uint32_t c = 0;
+    uint64_t p = 0;
+    if (lane < kGSlices && s0 + lane < nslices) {
+      c = __ldg(cnt + s0 + lane);
+      p = __ldg(off + s0 + lane);
+    }
+    uint32_t e = c;  // inclusive scan of the counts over lanes 0 .. kGSlices - 1
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint32_t r = r0 + q * 32 + lane;
-        w[q] = r < c ? __ldcs(src + r) : 0ull;
+    for (int o = 1; o < kGSlices; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, e, o);
+      if (lane >= (uint32_t)o) e += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, e, kGSlices - 1);
+    if (total == 0) continue;  // warp-uniform
+    const uint64_t pos = __shfl_sync(0xffffffffu, p, 0);
+    uint32_t ends[kGSlices];
+#pragma unroll
+    for (int i = 0; i < kGSlices; i++) ends[i] = __shfl_sync(0xffffffffu, e, i);
+    const uint32_t excl = e - c;
+    for (uint32_t f0 = 0; f0 < total; f0 += kGRows * 32) {  // kGRows rows per lane in flight
+      uint64_t w[kGRows];
+#pragma unroll
+      for (int q = 0; q < kGRows; q++) {
+        const uint32_t f = f0 + q * 32 + lane;
+        uint32_t j = 0;
+#pragma unroll
+        for (int i = 0; i < kGSlices - 1; i++) j += f >= ends[i];
+        const uint32_t st = __shfl_sync(0xffffffffu, excl, j);
+        w[q] = f < total ? __ldcs(stage + (s0 + j) * kFWarpRows + (f - st)) : 0ull;
       }
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint32_t r = r0 + q * 32 + lane;
-        if (r < c) {
-          __stcs(out + pos + r, w[q]);
-          if (hist) atomicAdd(h + ((uint32_t)(w[q] >> bit_lo) & dmask), 1u);
+      for (int q = 0; q < kGRows; q++) {
+        const uint32_t f = f0 + q * 32 + lane;
+        if (f < total) {
+          const uint64_t x = CARRY ? ((w[q] >> ib) << ib) | (pos + f + id0) : w[q];
+          __stcs(out + pos + f, x);
+          if (hist) atomicAdd(h + ((uint32_t)(x >> bit_lo) & dmask), 1u);
+        }
+      }
+      if (CARRY) {
+        for (uint32_t k = 0; k < cr.n; k++) {
+          uint32_t v[kGRows];
+#pragma unroll
+          for (int q = 0; q < kGRows; q++) {
+            const uint32_t f = f0 + q * 32 + lane;
+            v[q] = f < total ? __ldg(cr.src[k] + ((w[q] & imask) - id0)) : 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < kGRows; q++) {
+            const uint32_t f = f0 + q * 32 + lane;
+            if (f < total) __stcs(cr.out[k] + pos + f, v[q]);
+          }
         }
       }
     }
@@ -871,10 +921,16 @@ void launch_sj_set_words(const uint64_t *w, const uint64_t *count, uint64_t max_
 
 void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t *off,
                       uint64_t nslices, uint64_t *out, uint32_t *hist, uint32_t bit_lo,
-                      uint32_t dmask, cudaStream_t s) {
+                      uint32_t dmask, const SjCarry &cr, uint32_t ib, uint64_t id0,
+                      cudaStream_t s) {
   if (nslices == 0) return;
-  sj_gather_kernel<<<grid_for_rows(nslices * kFWarpRows), kFThreads, 0, s>>>(
-      stage, cnt, off, nslices, out, hist, bit_lo, dmask);
+  const int g = grid_for_rows(nslices * kFWarpRows);
+  if (cr.n)
+    sj_gather_kernel<true><<<g, kFThreads, 0, s>>>(stage, cnt, off, nslices, out, hist, bit_lo,
+                                                   dmask, cr, ib, id0);
+  else
+    sj_gather_kernel<false><<<g, kFThreads, 0, s>>>(stage, cnt, off, nslices, out, hist, bit_lo,
+                                                    dmask, cr, ib, id0);
 }
 
 void launch_sj_chain_build(const PackArgs &a, bool side_b, void *bm, uint32_t bbits, cudaStream_t s) {

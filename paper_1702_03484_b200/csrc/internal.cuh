@@ -413,6 +413,16 @@ uint64_t sj_slices(uint64_t rows);  // ceil(rows / 512)
 // key_hash chain).
 void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
                                  uint32_t hashed, unsigned long long *sample, cudaStream_t s);
+// Columns carried through the column round: the gather also moves the survivors'
+// values of these columns of the side (loaded by the staged words' row ids) into dense columns
+// (survivor i of the side at out[c][i]) and replaces each word's row id by the survivor's
+// position (+ n1 on side B): ReduceDuplicate then reads the dense survivor columns instead of
+// gathering from the side's full columns.  n = 0: nothing carried.
+struct SjCarry {
+  uint32_t n;
+  const uint32_t *src[MAPSQ_MAX_COLS];
+  uint32_t *out[MAPSQ_MAX_COLS];
+};
 // Probe one side's key columns (side B if side_b) against bm (bm_kind 0 plain / 1 cblock of the
 // chain / 2 wblock of key' with seed) and stage its survivors; bm_set (plain, single-column keys
 // only): survivors also set their bit there.
@@ -429,9 +439,12 @@ void launch_sj_set_words(const uint64_t *w, const uint64_t *count, uint64_t max_
                          void *bm, uint32_t ib, uint32_t bbits, uint32_t hashed, uint64_t seed,
                          cudaStream_t s);
 // out[off[s] ..] = the staged survivors of slice s (off = exclusive scan of cnt); hist += digit 0.
+// With carried columns (cr.n > 0) their survivors' values move too (read at the staged word's row
+// id - id0) and a word's row id becomes its position + id0.
 void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t *off,
                       uint64_t nslices, uint64_t *out, uint32_t *hist, uint32_t bit_lo,
-                      uint32_t dmask, cudaStream_t s);
+                      uint32_t dmask, const SjCarry &cr, uint32_t ib, uint64_t id0,
+                      cudaStream_t s);
 // Distributed pre-filter (dist.cu, f2): blocked Bloom bitmaps (cblock) of the key_hash chain of
 // the RAW key values — the same on every rank — built / probed on one side's key columns.
 // build: bm |= the side's keys.  probe: mask bit per row (row r -> bit r & 31 of mask[r >> 5]) =
@@ -453,7 +466,7 @@ void launch_sj_build_words(const SjSeg &S, uint32_t ib, uint64_t seed, uint32_t 
 void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t bbits,
                             const void *bm, unsigned long long *sample, cudaStream_t s);
 
-// Compressed host store (hoststore.cu): frame-of-reference blocks of 1024 values.
+// Compressed host store (hoststore.cu): frame-of-reference / delta blocks of 128 values.
 uint64_t for_blocks(uint64_t n);
 uint64_t for_block_words(uint32_t bits);
 void launch_for_stats(const uint32_t *col, uint64_t n, uint32_t *base, uint32_t *bits,

@@ -3,7 +3,8 @@
 Dropping rows whose key is absent from the other side must not change RS or its row order: every
 case is compared IN ORDER against the oracle's sort-merge tier (same (key, tp1 row, tp2 row)
 order as the unfiltered GPU join), with the filter forced on for all sizes, and the number of
-dropped rows is checked against a brute-force count (exact bitmaps) or bounded (hashed)."""
+dropped rows is checked against a brute-force count (exact bitmaps) or bounded (hashed).  Every
+case runs with the filter's carried columns forced on, off and on auto."""
 from __future__ import annotations
 
 import numpy as np
@@ -17,6 +18,15 @@ import datagen  # noqa: E402
 import oracle  # noqa: E402
 import paper_1702_03484_b200 as mq  # noqa: E402
 from fixtures import config_expected_counts, config_query  # noqa: E402
+
+
+@pytest.fixture(params=["0", "1", "2"], autouse=True)
+def carry(request, monkeypatch):
+    """MAPSQ_SJ_CARRY: the column round carries ReduceDuplicate's columns through the filter
+    (1), never (0), or when the sampled probe keeps at most half of the larger side (2, the
+    default) — RS and its order must not depend on it."""
+    monkeypatch.setenv("MAPSQ_SJ_CARRY", request.param)
+    return request.param
 
 
 @pytest.fixture(scope="module")
