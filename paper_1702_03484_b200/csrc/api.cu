@@ -421,9 +421,16 @@ void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const maps
   set_join_bounds(pl, a, b, rs);
 }
 
-PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b) {
+// pv: value-carrying words (pl.ib must then be kPvIb; at most one non-key column per side)
+PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b,
+                   bool pv = false) {
   PackArgs pa;
   std::memset(&pa, 0, sizeof pa);
+  if (pv) {
+    pa.pv = 1;
+    pa.pv1 = pl.nrest1 ? a->col[pl.rest_col1[0]] : nullptr;
+    pa.pv2 = pl.nrest2 ? b->col[pl.rest_col2[0]] : nullptr;
+  }
   const bool hash = pl.path == MAPSQ_PATH_HASH;
   for (uint32_t c = 0; c < pl.nshared; c++) {
     if (!hash && !(pl.packed_mask >> c & 1u)) continue;
@@ -480,12 +487,15 @@ uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(
 // carry[side] (n, src set by the caller): columns to carry through the column round (SjCarry);
 // on return carry[side].n is 0 unless they were carried (out[] then holds the side's survivors'
 // values, allocated from sc, and the words' row ids index them).
+// Value-carrying words (carry[side].pv): the column round's gathers write them from the staged
+// row-id words (both sides), every other Map writes them directly.
 mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *a,
                         const mapsq_table *b, Scratch &sc, cudaStream_t s, uint64_t *&cur,
                         uint64_t *&alt, uint32_t *hist, uint64_t *nA_out, uint64_t *offB_out,
                         uint64_t *nB_out, SjCarry carry[2]) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
-  PackArgs pa = pack_args(pl, a, b);
+  const bool pv = carry[0].pv;
+  PackArgs pa = pack_args(pl, a, b, pv);
   const uint64_t bmw = std::max<uint64_t>(
       1, (1ull << std::max(kSemijoinBits, env_u32("MAPSQ_SJ_COLBITS", kSemijoinBits))) / 32);
   const uint64_t nsl_max = sj_slices(n1) + sj_slices(n2) + 2;
@@ -519,8 +529,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   // scan one side's slice counts (slices [sl0, sl0 + nsl)) and gather its staged survivors to
   // out; fsc[side] receives their number
   std::vector<size_t> gpos;
-  SjCarry none;
-  none.n = 0;
+  const SjCarry none{};
   const SjCarry use[2] = {carry[0], carry[1]};  // (n cleared below unless the column round carries)
   carry[0].n = carry[1].n = 0;
   auto scan_gather = [&](int side, uint64_t sl0, uint64_t nsl, uint64_t *out,
@@ -600,7 +609,10 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
       const bool do_carry = cmode == 1 || (cmode == 2 && !hashed && !colhash && srows > 0 &&
                                            2 * ssurv <= srows);
       SjCarry cr[2] = {none, none};
-      if (do_carry) {
+      if (pv) {  // (no carried columns: the values ride in the words)
+        cr[0] = use[0];
+        cr[1] = use[1];
+      } else if (do_carry) {
         for (int sd = 0; sd < 2; sd++) {
           for (uint32_t c = 0; c < use[sd].n; c++) {
             cr[sd].src[c] = use[sd].src[c];
@@ -641,7 +653,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
       posS = pending_pos();
       TRY(scan_gather(sideS, sideS ? slA : 0, sideS ? slB : slA, outS, cr[sideS]));
       ctx->counters.filter_accesses += nL + nS;
-      TRY(read_counts(posL, posS, posSet, sideL, cr[sideL].n, cr[sideS].n));
+      TRY(read_counts(posL, posS, posSet, sideL, pv ? 0 : cr[sideL].n, pv ? 0 : cr[sideS].n));
       nA = ctx->pinned[0];
       nB = ctx->pinned[1];
       offB = n1;
@@ -732,7 +744,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     nB = n2;
     CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
     if (colpath) {
-      const PackArgs pm = pack_args(pl, a, b);
+      const PackArgs pm = pack_args(pl, a, b, pv);
       KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
       launch_pack_hist(pm, cur, nullptr, hist, s);
       CKL("pack_hist");
@@ -834,6 +846,15 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     TRY(small_join(ctx, pl, &a, &b, rs, s, &done));
     if (done) return MAPSQ_OK;
   }
+  // value-carrying words (kPvIb): P64 joins with at most one non-key column per side whose key
+  // fits 31 bits (MAPSQ_PV=0 in the environment: row-id words, for ablations).  The plan's ib
+  // becomes 33 for the words; n1 (the label boundary ReduceDuplicate compares with) 2^32.
+  const bool pv = pl.path == MAPSQ_PATH_P64 && pl.nrest1 <= 1 && pl.nrest2 <= 1 &&
+                  pl.kb + kPvIb <= 64 && n1 < (1ull << 32) && n2 < (1ull << 32) &&
+                  env_u32("MAPSQ_PV", 1) != 0;
+  if (pv) pl.ib = kPvIb;
+  ctx->counters.last_ib = pl.ib;
+  const uint64_t lab = pv ? (1ull << 32) : n1;  // words' label boundary
   Scratch sc(ctx, s);
   const bool kv = pl.path == MAPSQ_PATH_KV;
   // (+2 slices: the semi-join filter stages each side's survivors at slice-aligned offsets)
@@ -868,12 +889,19 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   uint64_t rowsA = n1, rowsB = n2;  // rows of the columns ReduceDuplicate gathers from
   if (filt) {
     // the columns ReduceDuplicate reads by row id, offered to the filter to carry: every column
-    // (verification reads the shared ones too) or the non-key columns (expand decodes the key)
+    // (verification reads the shared ones too) or the non-key columns (expand decodes the key);
+    // with value-carrying words the side's one non-key column goes into the words instead
     SjCarry carry[2];
     uint32_t ccol[2][MAPSQ_MAX_COLS];
     for (int sd = 0; sd < 2; sd++) {
       const mapsq_table &t = sd ? b : a;
       carry[sd].n = 0;
+      carry[sd].pv = pv;
+      if (pv) {
+        const uint32_t nr = sd ? pl.nrest2 : pl.nrest1;
+        if (nr) carry[sd].src[carry[sd].n++] = t.col[sd ? pl.rest_col2[0] : pl.rest_col1[0]];
+        continue;
+      }
       const uint32_t nr = sd ? pl.nrest2 : pl.nrest1;
       for (uint32_t c = 0; c < (residual ? t.ncols : nr); c++) {
         const uint32_t j = residual ? c : (sd ? pl.rest_col2[c] : pl.rest_col1[c]);
@@ -892,14 +920,14 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       return MAPSQ_OK;
     }
     // carried: the words' row ids now index the survivors' dense columns (side B's from n1 on)
-    for (int sd = 0; sd < 2; sd++) {
+    for (int sd = 0; sd < 2 && !pv; sd++) {
       mapsq_table &t = sd ? b : a;
       for (uint32_t c = 0; c < carry[sd].n; c++) t.col[ccol[sd][c]] = carry[sd].out[c];
       if (carry[sd].n) (sd ? rowsB : rowsA) = sd ? nB : nA;
     }
   } else {
-    const PackArgs pa = pack_args(pl, &a, &b);
-    KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + (kv ? 12ull : 8ull) * n);
+    const PackArgs pa = pack_args(pl, &a, &b, pv);
+    KTimer kt(ctx, s, "pack_hist", 4ull * (pl.nshared + (pv ? 1 : 0)) * n + (kv ? 12ull : 8ull) * n);
     launch_pack_hist(pa, cur, va, hist, s);
     CKL("pack_hist");
   }
@@ -925,7 +953,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   {
     KTimer kt(ctx, s, "find_groups", nw * 8ull);
     GroupOut g{gs, gp, ge, gc};
-    launch_find_groups(kv ? nullptr : words, kv ? words : nullptr, vals, nw, n1, pl.ib, g,
+    launch_find_groups(kv ? nullptr : words, kv ? words : nullptr, vals, nw, lab, pl.ib, g,
                        gstatus, reinterpret_cast<uint32_t *>(scal + 2), scal, s);
     CKL("find_groups");
   }
@@ -1036,7 +1064,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     ea.words = kv ? nullptr : words;
     ea.keys = kv ? words : nullptr;
     ea.vals = vals;
-    ea.n1 = n1;
+    ea.n1 = lab;
     ea.ib = pl.ib;
     ea.gstart = gs;
     ea.gsplit = gp;
@@ -1052,13 +1080,14 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     }
     ea.nrest1 = pl.nrest1;
     ea.nrest2 = pl.nrest2;
-    for (uint32_t c = 0; c < pl.nrest1; c++) ea.rest1[c] = a.col[pl.rest_col1[c]];
-    for (uint32_t c = 0; c < pl.nrest2; c++) ea.rest2[c] = b.col[pl.rest_col2[c]];
+    // (value-carrying words: no source columns, the values come from the words)
+    for (uint32_t c = 0; c < pl.nrest1; c++) ea.rest1[c] = pv ? nullptr : a.col[pl.rest_col1[c]];
+    for (uint32_t c = 0; c < pl.nrest2; c++) ea.rest2[c] = pv ? nullptr : b.col[pl.rest_col2[c]];
     for (uint32_t c = 0; c < pl.out_ncols; c++) ea.out[c] = rs->col[c];
     ea.tile_g0 = sc.get<uint64_t>(expand_tiles(m) + 1);
     NEED(ea.tile_g0);
     const uint64_t bytes = 4ull * m * pl.out_ncols + 8ull * nw +
-                           4ull * (rowsA * pl.nrest1 + rowsB * pl.nrest2);
+                           (pv ? 0ull : 4ull * (rowsA * pl.nrest1 + rowsB * pl.nrest2));
     KTimer kt(ctx, s, "expand", bytes, 2);
     launch_expand(ea, s);
     cudaError_t e = cudaGetLastError();

@@ -664,16 +664,25 @@ sj_gather_kernel(const uint64_t *__restrict__ stage, const uint32_t *__restrict_
         const uint32_t st = __shfl_sync(0xffffffffu, excl, j);
         w[q] = f < total ? __ldcs(stage + (s0 + j) * kFWarpRows + (f - st)) : 0ull;
       }
+      uint32_t pvv[kGRows];  // value-carrying words: the side's value of each survivor's row
+#pragma unroll
+      for (int q = 0; q < kGRows; q++) {
+        const uint32_t f = f0 + q * 32 + lane;
+        pvv[q] = (CARRY && cr.pv && cr.n && f < total)
+                     ? __ldg(cr.src[0] + ((w[q] & imask) - id0)) : 0u;
+      }
 #pragma unroll
       for (int q = 0; q < kGRows; q++) {
         const uint32_t f = f0 + q * 32 + lane;
         if (f < total) {
-          const uint64_t x = CARRY ? ((w[q] >> ib) << ib) | (pos + f + id0) : w[q];
+          const uint64_t x = !CARRY ? w[q]
+                             : cr.pv ? ((w[q] >> ib) << ib) | (id0 ? 1ull << 32 : 0ull) | pvv[q]
+                                     : ((w[q] >> ib) << ib) | (pos + f + id0);
           __stcs(out + pos + f, x);
           if (hist) atomicAdd(h + ((uint32_t)(x >> bit_lo) & dmask), 1u);
         }
       }
-      if (CARRY) {
+      if (CARRY && !cr.pv) {
         for (uint32_t k = 0; k < cr.n; k++) {
           uint32_t v[kGRows];
 #pragma unroll
@@ -925,7 +934,7 @@ void launch_sj_gather(const uint64_t *stage, const uint32_t *cnt, const uint64_t
                       cudaStream_t s) {
   if (nslices == 0) return;
   const int g = grid_for_rows(nslices * kFWarpRows);
-  if (cr.n)
+  if (cr.n || cr.pv)
     sj_gather_kernel<true><<<g, kFThreads, 0, s>>>(stage, cnt, off, nslices, out, hist, bit_lo,
                                                    dmask, cr, ib, id0);
   else

@@ -295,7 +295,15 @@ struct PackArgs {
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
   uint32_t kb;       // packed key bits
   uint32_t hash;     // 1 (PATH_HASH): key' = key_hash over the raw values of all nkey columns
+  // 1: value-carrying words (kPvIb): key' << 33 | label << 32 | the row's value of pv1 (Tp1) /
+  // pv2 (Tp2), the side's only non-key column (nullptr: 0)
+  uint32_t pv;
+  const uint32_t *pv1, *pv2;
 };
+// Value-carrying words (P64 joins with at most one non-key column per side and kb <= 31): the low
+// 33 bits hold (label, value) instead of the row id, so ReduceDuplicate reads the non-key values
+// from the sorted words themselves (no gathers).  The sort's stability keeps the rows' order.
+constexpr uint32_t kPvIb = 33;
 
 // PATH_HASH key': a 64-bit mix of the shared columns' raw values, top kb bits.  Equal keys get
 // equal key'; ReduceDuplicate verifies every pair's columns, so collisions cost time only.
@@ -422,6 +430,9 @@ struct SjCarry {
   uint32_t n;
   const uint32_t *src[MAPSQ_MAX_COLS];
   uint32_t *out[MAPSQ_MAX_COLS];
+  // pv = 1 (value-carrying words): the gather instead rewrites each word's low 33 bits to
+  // (label, src[0][row]) — label 1 on side B (id0 > 0), value 0 when n = 0; out[] is unused
+  uint32_t pv;
 };
 // Probe one side's key columns (side B if side_b) against bm (bm_kind 0 plain / 1 cblock of the
 // chain / 2 wblock of key' with seed) and stage its survivors; bm_set (plain, single-column keys

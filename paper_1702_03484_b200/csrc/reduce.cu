@@ -149,8 +149,9 @@ find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restr
       } else {
         if (lane == 0) wp = carry_w;
         same = ((w ^ wp) >> ib) == 0;
-        r = ((uint32_t)w & imask) >= n1;
-        rp = ((uint32_t)wp & imask) >= n1;
+        // (value-carrying words, ib = kPvIb: the label is bit 32)
+        r = ib > 32 ? (uint32_t)(w >> 32) & 1u : ((uint32_t)w & imask) >= n1;
+        rp = ib > 32 ? (uint32_t)(wp >> 32) & 1u : ((uint32_t)wp & imask) >= n1;
       }
       const bool head = in && (i == 0 || !same || (lane == 0 && sbeg == 0 && i == 0));
       const bool split = in && i > 0 && r && !rp && same;
@@ -395,10 +396,15 @@ expand_kernel(const ExpandArgs a) {
     } else {
       const uint32_t *src = s_src[col];
       const bool left = col < a.nkey + a.nrest1;
+      if (src == nullptr) {  // value-carrying words: the "row id" is the value itself
 #pragma unroll
-      for (int q = 0; q < R; q++) {
-        const bool v = (q % kERows) < nrow[q / kERows];
-        val[q] = v ? __ldg(src + (left ? lidx[q] : ridx[q])) : 0u;
+        for (int q = 0; q < R; q++) val[q] = left ? lidx[q] : ridx[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+          const bool v = (q % kERows) < nrow[q / kERows];
+          val[q] = v ? __ldg(src + (left ? lidx[q] : ridx[q])) : 0u;
+        }
       }
     }
 #pragma unroll

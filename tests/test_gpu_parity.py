@@ -218,6 +218,34 @@ def test_small_join_one_launch_equals_multikernel_path(ctx):
     ctx.set_option(mq.OPT_SMALL_JOIN, 1)
 
 
+@pytest.mark.parametrize("pv", ["1", "0"])
+def test_value_carrying_words(ctx, monkeypatch, pv):
+    # P64 joins with at most one non-key column per side sort words that carry (label, value)
+    # instead of the row id (kPvIb; MAPSQ_PV=0: row-id words).  Same rows, same order either way:
+    # 0 or 1 non-key columns on each side, full 32-bit values, a hot key, semi-join filter on / off
+    # (its column round writes the value words in the gather), ragged sizes over many tiles.
+    monkeypatch.setenv("MAPSQ_PV", pv)
+    rng = np.random.default_rng(606)
+    shapes = [([0, 1], [0, 2]), ([0], [0, 2]), ([0, 1], [0]), ([0], [0]), ([1, 0], [2, 0])]
+    for n1, n2, dom in [(5000, 7000, 3000), (70001, 40003, 1 << 20), (30000, 9000, 60)]:
+        for va, vb in shapes:
+            A = rng.integers(0, 1 << 32, (n1, len(va)), dtype=np.uint64).astype(np.uint32)
+            B = rng.integers(0, 1 << 32, (n2, len(vb)), dtype=np.uint64).astype(np.uint32)
+            A[:, va.index(0)] = rng.integers(0, dom, n1)
+            B[:, vb.index(0)] = rng.integers(0, dom, n2)
+            A[: n1 // 10, va.index(0)] = 3  # hot key
+            ref = oracle.join(oracle.Table(va, A), oracle.Table(vb, B))
+            for mode in (mq.SEMIJOIN_ON, mq.SEMIJOIN_OFF):
+                ctx.set_option(mq.OPT_SEMIJOIN, mode)
+                ctx.set_option(mq.OPT_SMALL_JOIN, 0)
+                got = ctx.join(dtable(va, A), dtable(vb, B))
+                assert_same(got, ref)  # in order
+                assert ctx.stats()["last_ib"] == (33 if pv == "1" else
+                                                  int(np.ceil(np.log2(n1 + n2))))
+    ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
+    ctx.set_option(mq.OPT_SMALL_JOIN, 1)
+
+
 def test_join_skewed_hot_key_large_groups(ctx):
     rng = np.random.default_rng(11)
     # one hot key: 6000 x 700 = 4.2e6 output rows, plus a cold tail
