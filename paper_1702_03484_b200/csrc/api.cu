@@ -471,6 +471,15 @@ uint32_t env_u32(const char *name, uint32_t dflt) {
   return (e && *e) ? (uint32_t)std::strtoul(e, nullptr, 10) : dflt;
 }
 
+// Tp2 streaming in (ctx->stream_b, mapsq_query_host_indexed): s waits until rows [0, rows) of it
+// are in place (the chunk holding row rows - 1; the copy stream lands chunks in order)
+mapsq_status wait_stream_b(mapsq_ctx *ctx, uint64_t rows, cudaStream_t s) {
+  const StreamIn *sb = ctx->stream_b;
+  if (!sb || sb->ev.empty() || rows == 0) return MAPSQ_OK;
+  const uint64_t k = std::min<uint64_t>((rows - 1) / sb->chunk_rows, sb->ev.size() - 1);
+  return cuda_check(ctx, cudaStreamWaitEvent(s, sb->ev[k], 0), "stream wait");
+}
+
 uint32_t word_round_bits(uint64_t small) {
   const uint32_t b = bits_for(8 * std::max<uint64_t>(small, 1));
   return std::max<uint32_t>(16, std::min<uint32_t>(kSemijoinBits, b));
@@ -590,11 +599,19 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     const uint64_t kbytes = 4ull * pa.nkey;
     CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
+    // Tp2 streaming in: as S it is waited for whole before the build; as L the build runs while
+    // it arrives, the sample reads its first chunk only and the probe runs chunk by chunk
+    const StreamIn *sb = ctx->stream_b;
+    if (s_is_b) TRY(wait_stream_b(ctx, n2, s));
+    const uint64_t l_rows = (sb && !s_is_b) ? sb->chunk_rows : ~0ull;
     {
-      KTimer kt(ctx, s, "filter_build", kbytes * (nS + nL / 16), 2);
-      launch_sj_build_sample_cols(pa, s_is_b, bmS, bbits, hashed, sample, s);
+      KTimer kt(ctx, s, "filter_build", kbytes * (nS + std::min(nL, l_rows) / 16), 2);
+      mapsq_status wst = MAPSQ_OK;
+      launch_sj_build_sample_cols(pa, s_is_b, bmS, bbits, hashed, sample, s, l_rows,
+                                  [&] { if (!s_is_b) wst = wait_stream_b(ctx, std::min(n2, l_rows), s); });
+      TRY(wst);
       CKL("filter_build");
-      ctx->counters.filter_accesses += nS + nL / 16;
+      ctx->counters.filter_accesses += nS + std::min(nL, l_rows) / 16;
     }
     TRY(sample_says_skip(&skipped));
     if (!skipped) {
@@ -632,10 +649,20 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
       CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
       {
         KTimer kt(ctx, s, "filter_probe", kbytes * nL);
-        launch_sj_probe_cols(pa, sideL == 1, colhash ? 1 : 0, bmS, bbits, hashed, 0,
-                             set_in_probe ? bmL : nullptr, stage, cnt, s);
+        if (sb && sideL == 1) {  // chunk by chunk as Tp2's copies land
+          for (uint64_t lo = 0; lo < n2; lo += sb->chunk_rows) {
+            const uint64_t hi = std::min(n2, lo + sb->chunk_rows);
+            TRY(wait_stream_b(ctx, hi, s));
+            launch_sj_probe_cols(pa, true, colhash ? 1 : 0, bmS, bbits, hashed, 0,
+                                 set_in_probe ? bmL : nullptr, stage, cnt, s, lo, hi);
+          }
+        } else {
+          launch_sj_probe_cols(pa, sideL == 1, colhash ? 1 : 0, bmS, bbits, hashed, 0,
+                               set_in_probe ? bmL : nullptr, stage, cnt, s);
+        }
         CKL("filter_probe");
       }
+      TRY(wait_stream_b(ctx, n2, s));  // (all of Tp2 from here on)
       posL = pending_pos();
       TRY(scan_gather(sideL, sideL ? slA : 0, sideL ? slB : slA, outL, cr[sideL]));
       if (!set_in_probe) {
@@ -664,6 +691,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     }
   } else {
     // composite packed keys: Map every row, then filter the words
+    TRY(wait_stream_b(ctx, n2, s));
     pa.passes = 0;  // (the histogram is counted by the last round's gathers)
     KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
     launch_pack_hist(pa, cur, nullptr, hist, s);
@@ -738,6 +766,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     if (nw * 10 > before * 9) break;  // < 10% dropped: further rounds would not pay
   }
   if (skipped) {  // unfiltered: every row's word, the first digit's histogram
+    TRY(wait_stream_b(ctx, n2, s));
     nw = n;
     nA = n1;
     offB = n1;
@@ -825,6 +854,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   TRY(check_table(ctx, tp2_in, "tp2"));
   mapsq_table a = *tp1_in, b = *tp2_in;
   TRY(bounds_of(ctx, &a, s));
+  if (!(b.flags & MAPSQ_TABLE_BOUNDS)) TRY(wait_stream_b(ctx, b.nrows, s));
   TRY(bounds_of(ctx, &b, s));
   mapsq_join_plan pl;
   TRY(plan_join(ctx, &a, &b, &pl, ctx->wide_key_mode));
@@ -842,6 +872,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     return MAPSQ_OK;
   }
   if (pl.path == MAPSQ_PATH_P64 && n <= kSmallMaxRows && ctx->small_joins) {
+    TRY(wait_stream_b(ctx, n2, s));
     bool done = false;
     TRY(small_join(ctx, pl, &a, &b, rs, s, &done));
     if (done) return MAPSQ_OK;
@@ -911,6 +942,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     }
     uint64_t nA = 0, offB = 0, nB = 0;
     TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB, carry));
+    TRY(wait_stream_b(ctx, n2, s));  // (filter_map waited; anything later reads all of Tp2)
     nw = nA + nB;
     seg_n0 = nA;
     seg_gap = offB - nA;
@@ -926,6 +958,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       if (carry[sd].n) (sd ? rowsB : rowsA) = sd ? nB : nA;
     }
   } else {
+    TRY(wait_stream_b(ctx, n2, s));
     const PackArgs pa = pack_args(pl, &a, &b, pv);
     KTimer kt(ctx, s, "pack_hist", 4ull * (pl.nshared + (pv ? 1 : 0)) * n + (kv ? 12ull : 8ull) * n);
     launch_pack_hist(pa, cur, va, hist, s);
@@ -1599,6 +1632,7 @@ MAPSQ_API void mapsq_destroy(mapsq_ctx *ctx) {
   if (ctx->arena_ev) cudaEventDestroy(ctx->arena_ev);
   dist_free(ctx);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->unpack_stream) cudaStreamDestroy(ctx->unpack_stream);
   delete ctx;
 }
 
@@ -1952,7 +1986,9 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
       if (it != h->pred.end() && *it == pats[j].id[1]) prange[j] = (int)(it - h->pred.begin());
     }
   if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-  cudaStream_t cs = ctx->copy_stream;
+  if (!ctx->unpack_stream)
+    CK(cudaStreamCreateWithFlags(&ctx->unpack_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->copy_stream, us = ctx->unpack_stream;
   mapsq_index D;  // device-side index over the copied ranges (columns owned by the scratch)
   mapsq_table rs;
   uint64_t bytes = 0;
@@ -1961,15 +1997,21 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
     // the H2D copies run on the copy stream in the order the query first uses the ranges; the
     // compute stream waits for a range only where it first reads it (scans: up front; views: at
     // the join that consumes them), so later ranges stream in while the first joins run
+    // (compressed chunks are expanded on a second stream, so that the copy engine never waits
+    // for an expansion kernel)
     struct Copies {
-      cudaStream_t cs;
+      cudaStream_t cs, us;
       std::vector<cudaEvent_t> ev;
       ~Copies() {
         cudaStreamSynchronize(cs);  // no copy may outlive the scratch it writes
+        cudaStreamSynchronize(us);
         for (cudaEvent_t e : ev)
           if (e) cudaEventDestroy(e);
       }
-    } cp{cs, std::vector<cudaEvent_t>(np + 1, nullptr)};
+    } cp{cs, us, std::vector<cudaEvent_t>(np + 1, nullptr)};
+    // rows per streamed chunk, a multiple of 512 (MAPSQ_STREAM_CHUNK: override, for tests)
+    const uint64_t kStreamChunk =
+        std::max<uint64_t>(512, (uint64_t)env_u32("MAPSQ_STREAM_CHUNK", 32u << 20) & ~511ull);
     uint64_t rows = 0, cwords = 0;
     for (size_t r = 0; r < np; r++)
       if (all || need[r]) {
@@ -2001,36 +2043,96 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
       D.olo.push_back(h->olo[r]);
       D.ohi.push_back(h->ohi[r]);
     }
+    // MAPSQ_DEBUG: the copy stream's range completion times and the joins' / readback's end,
+    // relative to the query's start (timing events; stderr)
+    std::vector<cudaEvent_t> dbg;
+    auto dbg_mark = [&](cudaStream_t st) {
+      if (!debug_on()) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      dbg.push_back(e);
+    };
+    dbg_mark(s);
     // the scratch may still be read by earlier work on s: the copies start after it
     CK(cudaEventCreateWithFlags(&cp.ev[np], cudaEventDisableTiming));
     CK(cudaEventRecord(cp.ev[np], s));
     CK(cudaStreamWaitEvent(cs, cp.ev[np], 0));
+    // A range is copied in chunks of kStreamChunk rows (one event each) so that a join whose
+    // Tp2 it is can start on the first chunks (JoinStep below, ctx->stream_b).
+    // MAPSQ_DEBUG_COPY_DELAY=<us>: before each chunk the copy stream poisons the chunk's rows and
+    // sleeps — a read that does not wait for its chunk then sees the poison (tests).
+    const uint32_t delay_us = env_u32("MAPSQ_DEBUG_COPY_DELAY", 0);
+    std::vector<StreamIn> streams(np);
     auto copy_range = [&](size_t r) -> mapsq_status {
       const uint64_t b = h->start[r], c = h->start[r + 1] - b;
       const bool with_p = all || need[r] == 2;
-      if (h->blob) {  // compressed segments: copy, then expand on the copy stream
+      StreamIn &si = streams[r];
+      si.rows = c;
+      si.chunk_rows = c > 2 * kStreamChunk ? kStreamChunk : std::max<uint64_t>(c, 1);
+      // compressed segments: every column's segment is staged whole in cstage (headers, then
+      // each chunk's payload words), and a chunk's blocks are expanded once they have landed
+      uint64_t cw[3] = {0, 0, 0};
+      const uint64_t nb = for_blocks(c);
+      if (h->blob)
         for (int col : {0, 2, 1}) {
           if (col == 1 && !with_p) continue;
-          uint32_t *dst = col == 0 ? D.s : (col == 1 ? D.p : D.o);
-          const uint64_t w = h->seg_words[col][r];
-          CK(cudaMemcpyAsync(cstage + cpos, h->blob + h->seg_off[col][r], 4 * w,
-                             cudaMemcpyHostToDevice, cs));
-          launch_for_unpack(cstage + cpos, c, dst + at[r], cs);
-          CK(cudaGetLastError());
-          cpos += w;
-          bytes += 4 * w;
+          cw[col] = cpos;
+          const uint32_t *seg = h->blob + h->seg_off[col][r];
+          CK(cudaMemcpyAsync(cstage + cpos, seg, 4 * (4 * nb + 1), cudaMemcpyHostToDevice, cs));
+          cpos += h->seg_words[col][r];
+          bytes += 4 * h->seg_words[col][r];
         }
-      } else {
-        CK(cudaMemcpyAsync(D.s + at[r], h->s + b, 4 * c, cudaMemcpyHostToDevice, cs));
-        CK(cudaMemcpyAsync(D.o + at[r], h->o + b, 4 * c, cudaMemcpyHostToDevice, cs));
-        bytes += 8 * c;
-        if (with_p) {
-          CK(cudaMemcpyAsync(D.p + at[r], h->p + b, 4 * c, cudaMemcpyHostToDevice, cs));
-          bytes += 4 * c;
+      for (uint64_t lo = 0; lo < c || (c == 0 && lo == 0); lo += si.chunk_rows) {
+        const uint64_t hi = std::min(c, lo + si.chunk_rows);
+        for (int col : {0, 2, 1}) {
+          if (col == 1 && !with_p) continue;
+          uint32_t *dst = (col == 0 ? D.s : (col == 1 ? D.p : D.o)) + at[r];
+          if (delay_us && hi > lo) CK(cudaMemsetAsync(dst + lo, 0xff, 4 * (hi - lo), cs));
         }
+        if (delay_us) launch_delay_us(delay_us, cs);
+        const uint64_t b0 = lo / 128, b1 = std::min(nb, (hi + 127) / 128);
+        for (int col : {0, 2, 1}) {
+          if (col == 1 && !with_p) continue;
+          uint32_t *dst = (col == 0 ? D.s : (col == 1 ? D.p : D.o)) + at[r];
+          if (hi <= lo) continue;
+          if (h->blob) {
+            const uint32_t *seg = h->blob + h->seg_off[col][r];
+            const uint32_t *woff = seg + 3 * nb;  // (host copy of the segment's word offsets)
+            const uint64_t p0 = 4 * nb + 1 + woff[b0], p1 = 4 * nb + 1 + woff[b1];
+            if (p1 > p0)
+              CK(cudaMemcpyAsync(cstage + cw[col] + p0, seg + p0, 4 * (p1 - p0),
+                                 cudaMemcpyHostToDevice, cs));
+          } else {
+            const uint32_t *src = (col == 0 ? h->s : (col == 1 ? h->p : h->o)) + b;
+            CK(cudaMemcpyAsync(dst + lo, src + lo, 4 * (hi - lo), cudaMemcpyHostToDevice, cs));
+            bytes += 4 * (hi - lo);
+          }
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, cs));
+        if (h->blob && hi > lo) {  // expand the chunk's blocks on the second stream
+          CK(cudaStreamWaitEvent(us, e, 0));
+          for (int col : {0, 2, 1}) {
+            if (col == 1 && !with_p) continue;
+            uint32_t *dst = (col == 0 ? D.s : (col == 1 ? D.p : D.o)) + at[r];
+            launch_for_unpack_blocks(cstage + cw[col], c, b0, b1, dst, us);
+            CK(cudaGetLastError());
+          }
+          cp.ev.push_back(e);  // (the copy event; the chunk's event is the expansion's)
+          CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          CK(cudaEventRecord(e, us));
+        }
+        si.ev.push_back(e);
+        if (c == 0) break;
       }
-      CK(cudaEventCreateWithFlags(&cp.ev[r], cudaEventDisableTiming));
-      CK(cudaEventRecord(cp.ev[r], cs));
+      // (destroyed with the copies: the last chunk's event stands for the whole range)
+      cp.ev[r] = si.ev.back();
+      cp.ev.insert(cp.ev.end(), si.ev.begin(), si.ev.end() - 1);
+      dbg_mark(h->blob ? us : cs);
+      if (debug_on()) std::fprintf(stderr, "[mapsq] e2e range %zu: %llu rows, %llu B so far\n", r,
+                                   (unsigned long long)c, (unsigned long long)bytes);
       return MAPSQ_OK;
     };
     std::vector<char> copied(np, 0);
@@ -2072,16 +2174,54 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
       }
       return MAPSQ_OK;
     };
+    // ... except a Tp2 that is one predicate range: the join waits for its chunks as it reads
+    // them (ctx->stream_b)
+    auto stream_of = [&](const mapsq_table *t) -> const StreamIn * {
+      int rr = -1;
+      for (uint32_t c = 0; c < t->ncols; c++) {
+        const uint32_t *q = t->col[c];
+        if (!q) continue;
+        int hit = -1;
+        for (size_t r = 0; r < np; r++) {
+          if (!cp.ev[r]) continue;
+          const uint64_t len = h->start[r + 1] - h->start[r];
+          for (const uint32_t *base : {D.s, D.o, D.p})
+            if (q == base + at[r] && t->nrows == len) hit = (int)r;
+        }
+        if (hit < 0 || (rr >= 0 && hit != rr)) return nullptr;
+        rr = hit;
+      }
+      return rr >= 0 && !step ? &streams[rr] : nullptr;  // (distributed joins: whole ranges)
+    };
     const JoinStep waited = [&](const mapsq_table *a, const mapsq_table *t, mapsq_table *out,
                                 cudaStream_t st) -> mapsq_status {
       TRY(wait_table(a));
-      TRY(wait_table(t));
-      return inner(a, t, out, st);
+      const StreamIn *sb = stream_of(t);
+      if (!sb) TRY(wait_table(t));
+      ctx->stream_b = sb;
+      const mapsq_status rc = inner(a, t, out, st);
+      ctx->stream_b = nullptr;
+      return rc;
     };
     TRY(query_impl(ctx, nullptr, pats, npats, proj, nproj, &rs, s, &D, &waited));
     for (size_t r = 0; r < np; r++) TRY(wait_range((int)r));  // (a one-pattern view result)
+    dbg_mark(s);
     // the result may be a zero-copy view of the copied ranges: read it back inside this scope
     TRY(result_to_host(ctx, &rs, s, host_rows, out_ncols, out_var, host_cols));
+    dbg_mark(s);
+    if (!dbg.empty()) {
+      cudaStreamSynchronize(s);
+      cudaStreamSynchronize(cs);
+      std::string line = "[mapsq] e2e ms from start: ranges";
+      for (size_t i = 1; i < dbg.size(); i++) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, dbg[0], dbg[i]);
+        line += (i + 2 == dbg.size() ? " | joins " : (i + 1 == dbg.size() ? " | readback " : " ")) +
+                std::to_string(ms);
+      }
+      std::fprintf(stderr, "%s\n", line.c_str());
+      for (cudaEvent_t e : dbg) cudaEventDestroy(e);
+    }
   }
   if (h2d_bytes) *h2d_bytes = bytes;
   return MAPSQ_OK;

@@ -856,22 +856,28 @@ void probe_launch(const PackArgs &a, const Side &sd, const SjSeg &ws, const void
 uint64_t sj_slices(uint64_t rows) { return ceil_div(rows, kFWarpRows); }
 
 void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
-                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s) {
-  const Side S = side_of(a, s_is_b), L = side_of(a, !s_is_b);
+                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s,
+                                 uint64_t l_rows, const std::function<void()> &before_sample) {
+  const Side S = side_of(a, s_is_b);
+  Side L = side_of(a, !s_is_b);
+  L.rows = std::min(L.rows, l_rows);
   const int gs = grid_for_rows(S.rows);
   const int mode = filter_mode(a);
   if (mode == 0) {
     filter_build_kernel<0><<<gs, kFThreads, 0, s>>>(a, S, (uint32_t *)bmS, bbits, hashed);
+    if (before_sample) before_sample();
     if (L.rows)
       filter_sample_kernel<0><<<sample_grid(L.rows), kFThreads, 0, s>>>(
           a, L, (const uint32_t *)bmS, bbits, hashed, kSampleStride, sample);
   } else if (mode == 2) {
     cfilter_build_kernel<2><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
+    if (before_sample) before_sample();
     if (L.rows)
       cfilter_sample_kernel<2><<<sample_grid(L.rows), kFThreads, 0, s>>>(
           a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
   } else {
     cfilter_build_kernel<3><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
+    if (before_sample) before_sample();
     if (L.rows)
       cfilter_sample_kernel<3><<<sample_grid(L.rows), kFThreads, 0, s>>>(
           a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
@@ -880,9 +886,17 @@ void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint
 
 void launch_sj_probe_cols(const PackArgs &a, bool side_b, int bm_kind, const void *bm,
                           uint32_t bbits, uint32_t hashed, uint64_t seed, uint32_t *bm_set,
-                          uint64_t *stage, uint32_t *cnt, cudaStream_t s) {
-  const Side sd = side_of(a, side_b);
+                          uint64_t *stage, uint32_t *cnt, cudaStream_t s, uint64_t row_lo,
+                          uint64_t row_hi) {
+  Side sd = side_of(a, side_b);
   const SjSeg none{nullptr, 0};
+  // rows [row_lo, row_hi) of the side: its slices from row_lo / 512 on
+  row_hi = std::min(row_hi, sd.rows);
+  if (row_lo >= row_hi) return;
+  for (uint32_t c = 0; c < a.nkey; c++) sd.col[c] += row_lo;
+  sd.rows = row_hi - row_lo;
+  sd.id0 += row_lo;
+  sd.slice0 += row_lo / kFWarpRows;
   // the side's slices: stage[slice * 512 ..] and cnt[slice], side B after side A's slices
   stage += sd.slice0 * kFWarpRows;
   const int mode = filter_mode(a);

@@ -109,13 +109,15 @@ for_pack_kernel(const uint32_t *__restrict__ col, uint64_t n, const uint32_t *__
 // expand a segment (device copy) into n values at out[0 ..); one warp per block.  Frame of
 // reference: lane-strided values (coalesced stores); deltas: each lane decodes kPer consecutive
 // values, prefix-sums them and adds the warp's exclusive scan of the lane totals.
+// (blocks [b0, b1) only: a range expanded chunk by chunk as its copies land)
 __global__ void __launch_bounds__(32 * kForWarps)
-for_unpack_kernel(const uint32_t *__restrict__ seg, uint64_t n, uint32_t *__restrict__ out) {
+for_unpack_kernel(const uint32_t *__restrict__ seg, uint64_t n, uint64_t b0, uint64_t b1,
+                  uint32_t *__restrict__ out) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nb = (n + kFor - 1) / kFor;
   const uint32_t *base = seg, *bits = seg + nb, *dmin = seg + 2 * nb, *woff = seg + 3 * nb;
   const uint32_t *payload = seg + 4 * nb + 1;
-  for (uint64_t b = (uint64_t)blockIdx.x * kForWarps + (threadIdx.x >> 5); b < nb;
+  for (uint64_t b = b0 + (uint64_t)blockIdx.x * kForWarps + (threadIdx.x >> 5); b < b1;
        b += (uint64_t)gridDim.x * kForWarps) {
     const uint32_t mb = __ldg(bits + b), nbits = mb & 63u, lo = __ldg(base + b);
     const uint32_t *p = payload + __ldg(woff + b);
@@ -184,7 +186,24 @@ void launch_for_pack(const uint32_t *col, uint64_t n, const uint32_t *base, cons
 }
 
 void launch_for_unpack(const uint32_t *seg, uint64_t n, uint32_t *out, cudaStream_t s) {
-  if (n) for_unpack_kernel<<<for_grid(n), 32 * kForWarps, 0, s>>>(seg, n, out);
+  if (n) for_unpack_kernel<<<for_grid(n), 32 * kForWarps, 0, s>>>(seg, n, 0, for_blocks(n), out);
 }
+
+void launch_for_unpack_blocks(const uint32_t *seg, uint64_t n, uint64_t b0, uint64_t b1,
+                              uint32_t *out, cudaStream_t s) {
+  if (b1 > b0)
+    for_unpack_kernel<<<for_grid((b1 - b0) * kFor), 32 * kForWarps, 0, s>>>(seg, n, b0, b1, out);
+}
+
+// (debugging aid, MAPSQ_DEBUG_COPY_DELAY: holds a stream for `us` microseconds)
+__global__ void delay_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+void launch_delay_us(uint32_t us, cudaStream_t s) { delay_kernel<<<1, 1, 0, s>>>(1000ull * us); }
 
 }  // namespace mapsq

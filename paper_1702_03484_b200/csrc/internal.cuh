@@ -41,6 +41,16 @@ struct DistState;
 
 }  // namespace mapsq
 
+namespace mapsq {
+// A join input whose rows arrive in chunks (mapsq_query_host_indexed: a predicate range copied
+// host -> device chunk by chunk): chunk k = rows [k * chunk_rows, min(rows, (k + 1) * chunk_rows))
+// is in place once ev[k] (recorded on the copy stream, in chunk order) has completed.
+struct StreamIn {
+  uint64_t rows = 0, chunk_rows = 0;
+  std::vector<cudaEvent_t> ev;
+};
+}  // namespace mapsq
+
 struct mapsq_ctx {
   int device = 0;
   int num_sms = 148;
@@ -72,6 +82,11 @@ struct mapsq_ctx {
   cudaEvent_t arena_ev = nullptr;
   mapsq::DistState *dist = nullptr;  // communicator + exchange arenas (dist.cu), or NULL
   cudaStream_t copy_stream = nullptr;  // H2D copies of mapsq_query_host_indexed (lazily created)
+  cudaStream_t unpack_stream = nullptr;  // expansion of the compressed copies (lazily created)
+  // set by mapsq_query_host_indexed around one join: its Tp2 input streams in (the join waits
+  // chunk by chunk where it can — the semi-join filter's probe of the larger side — and for all
+  // of it before anything else reads it)
+  const mapsq::StreamIn *stream_b = nullptr;
 };
 
 namespace mapsq {
@@ -420,7 +435,11 @@ uint64_t sj_slices(uint64_t rows);  // ceil(rows / 512)
 // Single packed column: plain bitmap (bit_index); PATH_HASH: blocked Bloom (cblock of the
 // key_hash chain).
 void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
-                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s);
+                                 uint32_t hashed, unsigned long long *sample, cudaStream_t s,
+                                 uint64_t l_rows = ~0ull,
+                                 const std::function<void()> &before_sample = nullptr);
+// (l_rows: sample only the larger side's first l_rows rows; before_sample runs between the two
+// launches — the streamed path waits there for those rows)
 // Columns carried through the column round: the gather also moves the survivors'
 // values of these columns of the side (loaded by the staged words' row ids) into dense columns
 // (survivor i of the side at out[c][i]) and replaces each word's row id by the survivor's
@@ -439,7 +458,8 @@ struct SjCarry {
 // only): survivors also set their bit there.
 void launch_sj_probe_cols(const PackArgs &a, bool side_b, int bm_kind, const void *bm,
                           uint32_t bbits, uint32_t hashed, uint64_t seed, uint32_t *bm_set,
-                          uint64_t *stage, uint32_t *cnt, cudaStream_t s);
+                          uint64_t *stage, uint32_t *cnt, cudaStream_t s, uint64_t row_lo = 0,
+                          uint64_t row_hi = ~0ull);  // rows [row_lo, row_hi) (row_lo % 512 == 0)
 // Word rounds: probe packed words (their slices start at slice0) against a wblock bitmap.
 void launch_sj_probe_words(const SjSeg &in, uint64_t slice0, uint32_t ib, const void *bm,
                            uint32_t bbits, uint64_t seed, uint64_t *stage, uint32_t *cnt,
@@ -482,6 +502,10 @@ uint64_t for_blocks(uint64_t n);
 uint64_t for_block_words(uint32_t bits);
 void launch_for_stats(const uint32_t *col, uint64_t n, uint32_t *base, uint32_t *bits,
                       uint32_t *dmin, cudaStream_t s);
+// expand blocks [b0, b1) of a segment of n values (launch_for_unpack: all of them)
+void launch_for_unpack_blocks(const uint32_t *seg, uint64_t n, uint64_t b0, uint64_t b1,
+                              uint32_t *out, cudaStream_t s);
+void launch_delay_us(uint32_t us, cudaStream_t s);
 void launch_for_pack(const uint32_t *col, uint64_t n, const uint32_t *base, const uint32_t *bits,
                      const uint32_t *dmin, const uint32_t *woff, uint32_t *payload,
                      cudaStream_t s);

@@ -192,6 +192,30 @@ def test_query_host_indexed_late_large_range(ctx):
     hidx.release()
 
 
+@pytest.mark.parametrize("compress", [1, 0])
+def test_query_host_indexed_streamed_chunks(ctx, monkeypatch, compress):
+    """The predicate ranges stream in chunk by chunk and a join whose Tp2 is one range starts on
+    the chunks that have landed (the filter's probe of the larger side waits per chunk).  With
+    MAPSQ_DEBUG_COPY_DELAY every chunk's rows hold a poison value while the copy stream sleeps
+    before copying it, so any read that does not wait for its chunk changes the result."""
+    monkeypatch.setenv("MAPSQ_STREAM_CHUNK", "65536")
+    monkeypatch.setenv("MAPSQ_DEBUG_COPY_DELAY", "300")
+    s, p, o, _ = datagen.lubm(60)
+    idx = ctx.index_build((dev(s), dev(p), dev(o)))
+    ctx.set_option(mq.OPT_HOST_COMPRESS, compress)
+    hidx = ctx.index_to_host(idx)
+    for mode in (mq.SEMIJOIN_ON, mq.SEMIJOIN_AUTO, mq.SEMIJOIN_OFF):
+        ctx.set_option(mq.OPT_SEMIJOIN, mode)
+        for cfg in ("C5", "C3", "C2", "C1"):
+            pats = config_query(cfg)
+            want = ctx.query(idx, pats).to_numpy()
+            vars_, rows = ctx.query_host(hidx, pats, copy=True)
+            assert np.array_equal(rows, want), (cfg, mode)
+    ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
+    ctx.set_option(mq.OPT_HOST_COMPRESS, 1)
+    hidx.release()
+
+
 def test_compressed_host_mirror_codec_edges(ctx):
     """The compressed mirror is lossless at every block width: full 32-bit ranges (bits = 32), a
     constant column (bits = 0), ranges of 1 and 1025 rows, a block boundary inside a range."""
