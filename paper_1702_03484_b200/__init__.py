@@ -217,12 +217,13 @@ class _CAI:
 class _Owner:
     """Holds a library-allocated table and releases it (stream ordered) when collected."""
 
-    def __init__(self, ctx: "Context", t: _Table):
-        self.ctx, self.t = ctx, t
+    def __init__(self, ctx: "Context", t: _Table, stream=None):
+        self.ctx, self.t, self.stream = ctx, t, stream
 
     def release(self):
         if self.t is not None and self.t.owner:
-            lib().mapsq_table_release(self.ctx.handle, ctypes.byref(self.t), _stream())
+            lib().mapsq_table_release(self.ctx.handle, ctypes.byref(self.t),
+                                      self.stream if self.stream is not None else _stream())
         self.t = None
 
     def __del__(self):
@@ -305,8 +306,8 @@ class DeviceTable:
         return DeviceTable(vars_, columns, n, t, owner=None)
 
 
-def _wrap(ctx: "Context", t: _Table, keep=None) -> DeviceTable:
-    owner = _Owner(ctx, t)
+def _wrap(ctx: "Context", t: _Table, keep=None, stream=None) -> DeviceTable:
+    owner = _Owner(ctx, t, stream)
     owner.keep = keep  # e.g. the Index whose memory a zero-copy view references
     n, w = int(t.nrows), int(t.ncols)
     ptrs = [t.col[c] for c in range(w)]
@@ -398,6 +399,32 @@ class HostIndex:
             pass
 
 
+class PreparedQuery:
+    """A query whose C arguments (patterns, projection, stream, store) are built once; each call
+    is one mapsq_query_indexed / mapsq_query call (latency-bound small queries, C1)."""
+
+    def __init__(self, ctx, triples, patterns, proj=None, stream=None):
+        self.ctx, self.triples = ctx, triples
+        self.k = len(patterns)
+        self.pats = (_Pattern * self.k)(*[pattern_struct(p) for p in patterns])
+        proj = list(proj or [])
+        self.nproj = len(proj)
+        self.pr = (ctypes.c_int32 * max(1, len(proj)))(*proj)
+        self.stream = _stream(stream)
+        if isinstance(triples, Index):
+            self.fn, self.src = lib().mapsq_query_indexed, triples.handle
+        else:
+            self._T = _triples(*triples)
+            self.fn, self.src = lib().mapsq_query, ctypes.byref(self._T)
+
+    def __call__(self) -> DeviceTable:
+        out = _Table()
+        self.ctx._check(self.fn(self.ctx.handle, self.src, self.pats, self.k, self.pr, self.nproj,
+                                ctypes.byref(out), self.stream))
+        keep = self.triples if isinstance(self.triples, Index) else None
+        return _wrap(self.ctx, out, keep=keep, stream=self.stream)
+
+
 class Context:
     """One libmapsq context on one device (default allocator: cudaMallocAsync pool)."""
 
@@ -463,6 +490,11 @@ class Context:
         return _wrap(self, out)
 
     # ---- query (row a7)
+    def prepare(self, triples, patterns, proj=None, stream=None) -> "PreparedQuery":
+        """``query`` with its arguments marshalled once (a prepared statement): calling the
+        result runs mapsq_query[_indexed] again on the same store, patterns and stream."""
+        return PreparedQuery(self, triples, patterns, proj, stream)
+
     def query(self, triples, patterns, proj=None, stream=None) -> DeviceTable:
         """``triples`` = (s, p, o) device tensors, or an Index."""
         k = len(patterns)

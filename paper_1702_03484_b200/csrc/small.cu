@@ -3,8 +3,8 @@
 //
 // The same method and the same result as the multi-kernel path, in one CTA: Map (Alg. 1 l.1-4,
 // PAPER.md:122-125) packs the words key' << ib | rowid (rowid >= n1 means RIGHT) into shared
-// memory; Sort (l.5) orders them — the words are distinct, so any correct sort gives the
-// unique (key', LEFT before RIGHT, rowid) order the radix path produces (a bitonic network here);
+// memory; Sort (l.5) orders them — a stable LSD radix sort over the key bits in shared
+// memory, so the order is the (key', LEFT before RIGHT, rowid) order the multi-kernel path produces;
 // ReduceDuplicate (l.6-11) finds each key's LEFT/RIGHT split, scans nL * nR and writes
 // every pair in (key', Tp1 row, Tp2 row) order.  A join this small is launch- and sync-bound on
 // the multi-kernel path (~10 launches and two blocking reads); here it is one launch and one read
@@ -22,70 +22,84 @@ small_join_kernel(const PackArgs pa, const ExpandArgs ea, uint64_t cap,
                   unsigned long long *__restrict__ m_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t n1 = (uint32_t)pa.n1, n = (uint32_t)(pa.n1 + pa.n2);
-  uint32_t np2 = 64;  // (at least one 64-word warp chunk)
-  while (np2 < n) np2 <<= 1;
   const uint32_t gcap = (n / 2 + 3) & ~1u;                            // groups (<= n / 2) + 1, even
-  uint64_t *w = reinterpret_cast<uint64_t *>(smem);                   // np2 words
-  uint32_t *g_start = reinterpret_cast<uint32_t *>(w + np2);
+  uint64_t *w0 = reinterpret_cast<uint64_t *>(smem);                  // n words
+  uint64_t *w1 = w0 + n;                                              // n words (sort buffer)
+  uint16_t *rank = reinterpret_cast<uint16_t *>(w1 + n);              // n (padded to 8 B)
+  uint32_t *g_start = reinterpret_cast<uint32_t *>(smem + 16ull * n + ((2ull * n + 7) & ~7ull));
   uint32_t *g_split = g_start + gcap;
   uint32_t *g_end = g_split + gcap;
   uint64_t *g_off = reinterpret_cast<uint64_t *>(g_end + gcap);       // (8 B aligned: 3 * gcap even)
+  __shared__ uint32_t s_cnt[kSmallThreads / 32][256];                 // per-warp digit counts
   __shared__ uint32_t s_wsum[kSmallThreads / 32];
   __shared__ uint32_t s_ng;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- Map
-  for (uint32_t i = tid; i < np2; i += kSmallThreads) {
-    if (i >= n) {
-      w[i] = ~0ull;  // padding sorts last
-      continue;
-    }
+  for (uint32_t i = tid; i < n; i += kSmallThreads) {
     const bool right = i >= n1;
     uint64_t key = 0;
     for (uint32_t c = 0; c < pa.nkey; c++) {
       const uint32_t v = right ? pa.key2[c][i - n1] : pa.key1[c][i];
       key |= (uint64_t)(v - pa.lo[c]) << pa.shift[c];
     }
-    w[i] = (key << pa.ib) | i;
+    w0[i] = (key << pa.ib) | i;
   }
   __syncthreads();
-  // ---- Sort: bitonic network over the np2 words (distinct, so the order is unique).  Stages with
-  // partner distance j >= 64 go through shared memory (one barrier each); the j <= 32 stages of a
-  // merge run inside a warp on a 64-word chunk held in registers (lane l: chunk words l, l + 32).
-  for (uint32_t k = 2; k <= np2; k <<= 1) {
-    for (uint32_t j = k >> 1; j >= 64; j >>= 1) {
-      for (uint32_t t = tid; t < np2 / 2; t += kSmallThreads) {
-        const uint32_t i = 2 * t - (t & (j - 1)), p = i + j;  // pairs (i, i + j), i & j == 0
-        const uint64_t a = w[i], b = w[p];
-        if ((a > b) == ((i & k) == 0)) {
-          w[i] = b;
-          w[p] = a;
-        }
-      }
-      __syncthreads();
-    }
-    for (uint32_t c0 = warp * 64; c0 < np2; c0 += kSmallThreads * 2) {
-      uint64_t e0 = w[c0 + lane], e1 = w[c0 + 32 + lane];
-      const uint32_t i0 = c0 + lane, i1 = i0 + 32;
-      for (uint32_t j = (k >> 1) < 32 ? (k >> 1) : 32; j > 0; j >>= 1) {
-        if (j == 32) {  // partners in the same lane
-          if ((e0 > e1) == ((i0 & k) == 0)) {
-            const uint64_t t = e0;
-            e0 = e1;
-            e1 = t;
-          }
-          continue;
-        }
-        const uint64_t q0 = __shfl_xor_sync(0xffffffffu, e0, j);
-        const uint64_t q1 = __shfl_xor_sync(0xffffffffu, e1, j);
-        const bool lo0 = (i0 & j) == 0, up0 = (i0 & k) == 0;
-        const bool lo1 = (i1 & j) == 0, up1 = (i1 & k) == 0;
-        e0 = (lo0 == up0) ? (e0 < q0 ? e0 : q0) : (e0 > q0 ? e0 : q0);
-        e1 = (lo1 == up1) ? (e1 < q1 ? e1 : q1) : (e1 > q1 ? e1 : q1);
-      }
-      w[c0 + lane] = e0;
-      w[c0 + 32 + lane] = e1;
+  // ---- Sort: stable LSD radix over the kb key bits, 8-bit digits, in shared memory (the words
+  // are distinct, so the sorted order is the unique (key', LEFT before RIGHT, rowid) order the
+  // multi-kernel path produces).  Warp q ranks the contiguous chunk [q E, (q + 1) E) of the words
+  // in rounds of 32 lanes (match.any peers; the highest peer bumps the warp's digit count), so
+  // ranks follow the input order within a digit; a block scan over (digit, warp) gives offsets.
+  const uint32_t E = (n + 31) / 32;
+  const uint32_t lt = lanemask_lt();
+  uint64_t *w = w0, *wt = w1;
+  for (uint32_t sh = pa.ib; sh < pa.ib + pa.kb; sh += 8) {
+    const uint32_t dm = (1u << min(8u, pa.ib + pa.kb - sh)) - 1u;
+    for (uint32_t i = tid; i < (kSmallThreads / 32) * 256; i += kSmallThreads) (&s_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t c0 = warp * E, c1 = min(n, c0 + E);
+    for (uint32_t b = c0; b < c1; b += 32) {
+      const uint32_t e = b + lane;
+      const bool in = e < c1;
+      const uint32_t d = in ? (uint32_t)(w[e] >> sh) & dm : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = in ? s_cnt[warp][d] : 0u;
+      __syncwarp();
+      if (in && lane == 31 - __clz(peers)) s_cnt[warp][d] = before + __popc(peers);
+      __syncwarp();
+      if (in) rank[e] = (uint16_t)(before + __popc(peers & lt));
     }
     __syncthreads();
+    if (tid < 256) {  // digit tid: exclusive offsets over (digit, warp)
+      uint32_t tot = 0;
+#pragma unroll 8
+      for (int q = 0; q < kSmallThreads / 32; q++) tot += s_cnt[q][tid];
+      uint32_t x = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      if (lane == 31) s_wsum[warp] = x;
+      asm volatile("bar.sync 1, 256;");
+      uint32_t run = x - tot;
+      for (uint32_t q = 0; q < warp; q++) run += s_wsum[q];
+#pragma unroll 8
+      for (int q = 0; q < kSmallThreads / 32; q++) {
+        const uint32_t c = s_cnt[q][tid];
+        s_cnt[q][tid] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < n; e += kSmallThreads) {
+      const uint64_t x = w[e];
+      wt[s_cnt[e / E][(uint32_t)(x >> sh) & dm] + rank[e]] = x;
+    }
+    __syncthreads();
+    uint64_t *t = w;
+    w = wt;
+    wt = t;
   }
   // ---- ReduceDuplicate 1: splits (a LEFT word followed by a RIGHT word of the same key), in key
   // order; block scan of the split flags gives each group's slot
@@ -191,10 +205,8 @@ small_join_kernel(const PackArgs pa, const ExpandArgs ea, uint64_t cap,
 }  // namespace
 
 size_t small_join_smem(uint64_t n) {
-  uint64_t np2 = 64;
-  while (np2 < n) np2 <<= 1;
   const uint64_t gcap = (n / 2 + 3) & ~1ull;
-  return np2 * 8 + 3 * gcap * 4 + gcap * 8;
+  return 16 * n + ((2 * n + 7) & ~7ull) + 3 * gcap * 4 + gcap * 8;
 }
 
 void launch_small_join(const PackArgs &pa, const ExpandArgs &ea, uint64_t cap,
