@@ -501,10 +501,19 @@ uint64_t word_round_seed(int round) { return 0x632BE59BD9B4E019ull * (uint64_t)(
 mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *a,
                         const mapsq_table *b, Scratch &sc, cudaStream_t s, uint64_t *&cur,
                         uint64_t *&alt, uint32_t *hist, uint64_t *nA_out, uint64_t *offB_out,
-                        uint64_t *nB_out, SjCarry carry[2]) {
+                        uint64_t *nB_out, SjCarry carry[2], uint32_t ib_row) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
-  const bool pv = carry[0].pv;
+  bool pv = carry[0].pv;
   PackArgs pa = pack_args(pl, a, b, pv);
+  // value-carrying words come only from the column round's gathers: a filter that Maps every
+  // row (composite packed keys, or a skipped filter) uses row-id words (measured: the Map that
+  // loads the values too ran 0.27-0.33 vs 0.17 ms on C5 J1, more than the expansion saves)
+  auto pv_off = [&] {
+    if (!pv) return;
+    pv = false;
+    pl.ib = ib_row;
+    pa = pack_args(pl, a, b, false);
+  };
   const uint64_t bmw = std::max<uint64_t>(
       1, (1ull << std::max(kSemijoinBits, env_u32("MAPSQ_SJ_COLBITS", kSemijoinBits))) / 32);
   const uint64_t nsl_max = sj_slices(n1) + sj_slices(n2) + 2;
@@ -587,6 +596,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   // packed composite keys are Mapped first and filtered as words
   const bool colhash = pa.hash;
   const bool colpath = (pa.nkey == 1 && pl.kb <= 32 && !pa.hash) || colhash;
+  if (!colpath) pv_off();
   if (colpath) {
     const bool s_is_b = n2 <= n1;  // S = the smaller side (ties: B)
     const uint64_t nS = s_is_b ? n2 : n1, nL = s_is_b ? n1 : n2;
@@ -614,6 +624,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
       ctx->counters.filter_accesses += nS + std::min(nL, l_rows) / 16;
     }
     TRY(sample_says_skip(&skipped));
+    if (skipped) pv_off();
     if (!skipped) {
       const uint64_t slA = sj_slices(n1), slB = sj_slices(n2);
       const uint64_t seedL = word_round_seed(0);
@@ -786,6 +797,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   *nA_out = nA;
   *offB_out = offB;
   *nB_out = nB;
+  carry[0].pv = carry[1].pv = pv;
   return MAPSQ_OK;
 }
 
@@ -880,12 +892,11 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   // value-carrying words (kPvIb): P64 joins with at most one non-key column per side whose key
   // fits 31 bits (MAPSQ_PV=0 in the environment: row-id words, for ablations).  The plan's ib
   // becomes 33 for the words; n1 (the label boundary ReduceDuplicate compares with) 2^32.
-  const bool pv = pl.path == MAPSQ_PATH_P64 && pl.nrest1 <= 1 && pl.nrest2 <= 1 &&
-                  pl.kb + kPvIb <= 64 && n1 < (1ull << 32) && n2 < (1ull << 32) &&
-                  env_u32("MAPSQ_PV", 1) != 0;
-  if (pv) pl.ib = kPvIb;
-  ctx->counters.last_ib = pl.ib;
-  const uint64_t lab = pv ? (1ull << 32) : n1;  // words' label boundary
+  // (candidates here; the semi-join filter's column round makes them, see filter_map)
+  bool pv = pl.path == MAPSQ_PATH_P64 && pl.nrest1 <= 1 && pl.nrest2 <= 1 &&
+            pl.kb + kPvIb <= 64 && n1 < (1ull << 32) && n2 < (1ull << 32) &&
+            env_u32("MAPSQ_PV", 1) != 0;
+  const uint32_t ib_row = pl.ib;
   Scratch sc(ctx, s);
   const bool kv = pl.path == MAPSQ_PATH_KV;
   // (+2 slices: the semi-join filter stages each side's survivors at slice-aligned offsets)
@@ -906,6 +917,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   const bool filt = !kv && pl.kb > 0 &&
                     (ctx->semijoin == MAPSQ_SEMIJOIN_ON ||
                      (ctx->semijoin == MAPSQ_SEMIJOIN_AUTO && n >= kSemijoinMinRows));
+  pv = pv && filt;
+  if (pv) pl.ib = kPvIb;
   if (filt && pl.path == MAPSQ_PATH_HASH && pl.kb < 64 - pl.ib &&
       env_u32("MAPSQ_HASH_WIDEN", 0)) {
     // (ablation knob) widen key' beyond 32 bits: after the filter only ~|L'|·|S'| / 2^32
@@ -941,7 +954,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
       }
     }
     uint64_t nA = 0, offB = 0, nB = 0;
-    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB, carry));
+    TRY(filter_map(ctx, pl, &a, &b, sc, s, cur, alt, hist, &nA, &offB, &nB, carry, ib_row));
+    pv = carry[0].pv;
     TRY(wait_stream_b(ctx, n2, s));  // (filter_map waited; anything later reads all of Tp2)
     nw = nA + nB;
     seg_n0 = nA;
@@ -964,6 +978,8 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     launch_pack_hist(pa, cur, va, hist, s);
     CKL("pack_hist");
   }
+  const uint64_t lab = pv ? (1ull << 32) : n1;  // the words' label boundary
+  ctx->counters.last_ib = pl.ib;
   // ---- Sort (row a4)
   int which = 0;
   TRY(radix_sort(ctx, cur, alt, va, vb, nw, kv ? 0 : pl.ib, pl.kb, hist, sc, s, &which, seg_n0,

@@ -310,14 +310,15 @@ struct PackArgs {
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
   uint32_t kb;       // packed key bits
   uint32_t hash;     // 1 (PATH_HASH): key' = key_hash over the raw values of all nkey columns
-  // 1: value-carrying words (kPvIb): key' << 33 | label << 32 | the row's value of pv1 (Tp1) /
-  // pv2 (Tp2), the side's only non-key column (nullptr: 0)
+  // 1: value-carrying words (kPvIb; made by the semi-join filter's gathers): key' << 33 |
+  // label << 32 | the row's value of pv1 (Tp1) / pv2 (Tp2), the side's only non-key column
   uint32_t pv;
   const uint32_t *pv1, *pv2;
 };
-// Value-carrying words (P64 joins with at most one non-key column per side and kb <= 31): the low
-// 33 bits hold (label, value) instead of the row id, so ReduceDuplicate reads the non-key values
-// from the sorted words themselves (no gathers).  The sort's stability keeps the rows' order.
+// Value-carrying words (filtered P64 joins with at most one non-key column per side and kb <= 31):
+// the low 33 bits hold (label, value) instead of the row id, so ReduceDuplicate reads the non-key
+// values from the sorted words themselves (no gathers).  The sort's stability keeps the rows'
+// order.  The semi-join filter's column round writes them in its gathers (SjCarry::pv).
 constexpr uint32_t kPvIb = 33;
 
 // PATH_HASH key': a 64-bit mix of the shared columns' raw values, top kb bits.  Equal keys get

@@ -13,6 +13,8 @@
 // digit offsets are resolved by decoupled look-back over per-(tile, digit) status words; each
 // pass's global digit counts come from the previous kernel (the Map kernel counts digit 0,
 // every pass counts the next digit).
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace mapsq {
@@ -65,25 +67,12 @@ pack_hist_kernel(const PackArgs a, uint64_t *__restrict__ words, uint32_t *__res
 #pragma unroll
       for (int it = 0; it < kHistItems; it++) key[it] = key_hash_final(key[it], a.kb);
     }
-    // value-carrying words: (label, value) replace the row id (all loads in flight together)
-    uint32_t pv[kHistItems];
-    if (a.pv) {
-#pragma unroll
-      for (int it = 0; it < kHistItems; it++) {
-        const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
-        const uint32_t *col = i < a.n1 ? a.pv1 : a.pv2;
-        pv[it] = (i < n && col) ? __ldcs(col + (i < a.n1 ? i : i - a.n1)) : 0u;
-      }
-    }
 #pragma unroll
     for (int it = 0; it < kHistItems; it++) {
       const uint64_t i = c0 + (uint64_t)it * kHistThreads + threadIdx.x;
       if (i >= n) continue;
       uint64_t kk = key[it];
-      if (!KV && a.pv) {
-        kk = (kk << a.ib) | (i < a.n1 ? 0ull : 1ull << 32) | pv[it];
-        __stcs(words + i, kk);
-      } else if (KV) {
+      if (KV) {
         __stcs(words + i, kk);
         __stcs(vals + i, (uint32_t)i);
       } else {

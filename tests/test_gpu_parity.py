@@ -220,8 +220,8 @@ def test_small_join_one_launch_equals_multikernel_path(ctx):
 
 @pytest.mark.parametrize("pv", ["1", "0"])
 def test_value_carrying_words(ctx, monkeypatch, pv):
-    # P64 joins with at most one non-key column per side sort words that carry (label, value)
-    # instead of the row id (kPvIb; MAPSQ_PV=0: row-id words).  Same rows, same order either way:
+    # Filtered P64 joins with at most one non-key column per side sort words that carry (label,
+    # value) instead of the row id (kPvIb; MAPSQ_PV=0: row-id words).  Same rows, same order:
     # 0 or 1 non-key columns on each side, full 32-bit values, a hot key, semi-join filter on / off
     # (its column round writes the value words in the gather), ragged sizes over many tiles.
     monkeypatch.setenv("MAPSQ_PV", pv)
@@ -240,8 +240,9 @@ def test_value_carrying_words(ctx, monkeypatch, pv):
                 ctx.set_option(mq.OPT_SMALL_JOIN, 0)
                 got = ctx.join(dtable(va, A), dtable(vb, B))
                 assert_same(got, ref)  # in order
-                assert ctx.stats()["last_ib"] == (33 if pv == "1" else
-                                                  int(np.ceil(np.log2(n1 + n2))))
+                # (value words come from the filter's column round)
+                assert ctx.stats()["last_ib"] == (33 if pv == "1" and mode == mq.SEMIJOIN_ON
+                                                  else int(np.ceil(np.log2(n1 + n2))))
     ctx.set_option(mq.OPT_SEMIJOIN, mq.SEMIJOIN_AUTO)
     ctx.set_option(mq.OPT_SMALL_JOIN, 1)
 
