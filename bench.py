@@ -424,7 +424,7 @@ def run_gpu(args):
         indexed = isinstance(s, mq.HostIndex)
         e2e_ms = []
         out_bytes = in_h2d = 0
-        for i in range(max(1, min(args.steps, 3)) + 1):
+        for i in range(max(1, min(args.steps, 5)) + 1):  # (median of up to 5 after a warm run)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             if indexed:
@@ -567,7 +567,7 @@ def run_gpu_dist(args, world, rank, local):
         if hidx is None:
             dev_bufs = [torch.empty(len(s), dtype=torch.int32, device="cuda") for _ in range(3)]
         e2e_ms, h2d, d2h = [], 12 * len(s), 0
-        for i in range(max(1, min(args.steps, 3)) + 1):
+        for i in range(max(1, min(args.steps, 5)) + 1):  # (median of up to 5 after a warm run)
             tdist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
