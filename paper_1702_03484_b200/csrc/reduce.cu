@@ -306,7 +306,9 @@ expand_kernel(const ExpandArgs a) {
   __syncthreads();
   const uint64_t idx_mask = (a.ib >= 64) ? ~0ull : ((1ull << a.ib) - 1);
   constexpr int R = kERows * kEChunks;
-  uint64_t lpos[R], rpos[R];
+  // (positions and in-group counters are 32-bit — n < 2^32 — and the group end is tracked as a
+  // count-down of the rows left in it: the walk is 32-bit arithmetic except at group changes)
+  uint32_t lpos[R], rpos[R];
   int nrow[kEChunks];
 #pragma unroll
   for (int c = 0; c < kEChunks; c++) {
@@ -314,8 +316,9 @@ expand_kernel(const ExpandArgs a) {
     nrow[c] = 0;
     if (r0 >= a.m) continue;
     // locate r0's group
-    uint64_t gl, gbeg, gend;
+    uint64_t gl, gend;
     uint32_t start, split, end;
+    uint64_t gbeg;
     if (staged) {
       uint32_t lo = 0, hi = (uint32_t)(g1 - g0);
       while (lo < hi) {
@@ -332,23 +335,24 @@ expand_kernel(const ExpandArgs a) {
       gend = (gl + 1 < a.ngroups) ? a.goff[gl + 1] : a.m;
       start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
     }
-    uint64_t nR = end - split;
+    uint32_t nR = end - split;
     const uint64_t local = r0 - gbeg;
-    uint64_t li, ri;
-    if ((local >> 32) == 0 && (nR >> 32) == 0) {
-      li = (uint32_t)local / (uint32_t)nR;
-      ri = (uint32_t)local - (uint32_t)li * (uint32_t)nR;
+    uint32_t li, ri;
+    if ((local >> 32) == 0) {
+      li = (uint32_t)local / nR;
+      ri = (uint32_t)local - li * nR;
     } else {
-      li = local / nR;
-      ri = local - li * nR;
+      li = (uint32_t)(local / nR);
+      ri = (uint32_t)(local - (uint64_t)li * nR);
     }
+    uint32_t left = (uint32_t)min(gend - r0, (uint64_t)0xffffffffu);  // rows left in the group
+    const uint32_t nv = (uint32_t)min(a.m - r0, (uint64_t)kERows);
 #pragma unroll
     for (int j = 0; j < kERows; j++) {
-      const uint64_t r = r0 + j;
-      if (r >= a.m) break;
-      if (r >= gend) {  // next group (groups are never empty)
+      if ((uint32_t)j >= nv) break;
+      if (left == 0) {  // next group (groups are never empty)
         gl++;
-        gbeg = gend;
+        const uint64_t gb = gend;
         if (staged) {
           gend = s_off[gl + 1];
           start = s_start[gl]; split = s_split[gl]; end = s_end[gl];
@@ -356,6 +360,7 @@ expand_kernel(const ExpandArgs a) {
           gend = (gl + 1 < a.ngroups) ? a.goff[gl + 1] : a.m;
           start = a.gstart[gl]; split = a.gsplit[gl]; end = a.gend[gl];
         }
+        left = (uint32_t)min(gend - gb, (uint64_t)0xffffffffu);
         nR = end - split;
         li = 0;
         ri = 0;
@@ -363,6 +368,7 @@ expand_kernel(const ExpandArgs a) {
       lpos[c * kERows + j] = start + li;
       rpos[c * kERows + j] = split + ri;
       nrow[c]++;
+      left--;
       if (++ri == nR) {
         ri = 0;
         li++;
