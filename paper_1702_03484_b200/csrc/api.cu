@@ -530,8 +530,9 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   uint64_t nA = n1, offB = n1, nB = n2, nw = n;  // the current segments (in cur)
   bool exact = false;    // the last round's bitmaps were exact (no false positives)
   bool skipped = false;  // the sampled probe said the filter would drop < 10%
-  // after building the smaller side's bitmap, a 1/16 sample of the larger side is probed; if
-  // >= 90% of it survives the filter cannot pay (C5 J1 drops 6%) and the join goes unfiltered
+  // after building the smaller side's bitmap, a sample of the larger side (every 16th 512-row
+  // slice, at most ~4 M rows) is probed; if >= 90% of it survives the filter cannot pay (C5 J1
+  // drops 6%) and the join goes unfiltered
   auto sample_says_skip = [&](bool *skip) -> mapsq_status {
     TRY(ensure_pinned(ctx, 2));
     CK(cudaMemcpyAsync(ctx->pinned, sample, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -615,13 +616,13 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     if (s_is_b) TRY(wait_stream_b(ctx, n2, s));
     const uint64_t l_rows = (sb && !s_is_b) ? sb->chunk_rows : ~0ull;
     {
-      KTimer kt(ctx, s, "filter_build", kbytes * (nS + std::min(nL, l_rows) / 16), 2);
+      KTimer kt(ctx, s, "filter_build", kbytes * (nS + sj_sample_rows(std::min(nL, l_rows))), 2);
       mapsq_status wst = MAPSQ_OK;
       launch_sj_build_sample_cols(pa, s_is_b, bmS, bbits, hashed, sample, s, l_rows,
                                   [&] { if (!s_is_b) wst = wait_stream_b(ctx, std::min(n2, l_rows), s); });
       TRY(wst);
       CKL("filter_build");
-      ctx->counters.filter_accesses += nS + std::min(nL, l_rows) / 16;
+      ctx->counters.filter_accesses += nS + sj_sample_rows(std::min(nL, l_rows));
     }
     TRY(sample_says_skip(&skipped));
     if (skipped) pv_off();
@@ -729,12 +730,12 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     CK(cudaMemsetAsync(bm, 0, 2 * bw * sizeof(uint32_t), s));
     if (round == 0) CK(cudaMemsetAsync(sample, 0, 2 * sizeof(uint64_t), s));
     {
-      KTimer kt(ctx, s, "filter_build", 8ull * (S.rows + (round == 0 ? L.rows / 16 : 0)),
+      KTimer kt(ctx, s, "filter_build", 8ull * (S.rows + (round == 0 ? sj_sample_rows(L.rows) : 0)),
                 round == 0 ? 2 : 1);
       launch_sj_build_words(S, pl.ib, seed, bbits, bmS, s);
       if (round == 0) launch_sj_sample_words(L, pl.ib, seed, bbits, bmS, sample, s);
       CKL("filter_build");
-      ctx->counters.filter_accesses += S.rows + (round == 0 ? L.rows / 16 : 0);
+      ctx->counters.filter_accesses += S.rows + (round == 0 ? sj_sample_rows(L.rows) : 0);
     }
     if (round == 0) {
       TRY(sample_says_skip(&skipped));

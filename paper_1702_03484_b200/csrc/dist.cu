@@ -654,7 +654,7 @@ mapsq_status prefilter(mapsq_ctx *ctx, DistState *d, const mapsq_table *a, const
   };
   TRY(or_reduce(peersS));
   {
-    KTimer kt(ctx, s, "dist_filter_sample", 4ull * pa.nkey * (nL / 16));
+    KTimer kt(ctx, s, "dist_filter_sample", 4ull * pa.nkey * sj_sample_rows(nL));
     launch_sj_chain_sample(pa, !s_is_b, bmS, bbits, sample, s);
     CK(cudaGetLastError());
   }
@@ -681,7 +681,7 @@ mapsq_status prefilter(mapsq_ctx *ctx, DistState *d, const mapsq_table *a, const
     launch_sj_chain_probe(pa, s_is_b, bmL, bbits, nullptr, mS, s);
     CK(cudaGetLastError());
   }
-  ctx->counters.filter_accesses += nS + nL / 16 + nL + nS;
+  ctx->counters.filter_accesses += nS + sj_sample_rows(nL) + nL + nS;
   *mask_a = ma;
   *mask_b = mb;
   return MAPSQ_OK;

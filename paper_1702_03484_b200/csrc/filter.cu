@@ -33,7 +33,8 @@ constexpr int kFWarps = kFThreads / 32;
 constexpr int kFItems = 16;                    // rows per lane per slice
 constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
-constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice
+constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice,
+constexpr uint64_t kSampleSlices = 8192;       // and at most ~8192 slices (4 M rows)
 constexpr int kGSlices = 8;                    // slices per warp iteration of the gather
 constexpr int kGRows = MAPSQ_G_ROWS;           // rows per lane in flight in the gather
 
@@ -822,8 +823,12 @@ Side side_of(const PackArgs &a, bool b) {
   return sd;
 }
 
+uint32_t sample_stride(uint64_t rows) {  // slices between sampled slices
+  return (uint32_t)std::max<uint64_t>(kSampleStride, ceil_div(ceil_div(rows, kFWarpRows), kSampleSlices));
+}
+
 int sample_grid(uint64_t rows) {  // one warp per sampled slice (up to 148 x 8 CTAs)
-  const uint64_t sampled = ceil_div(ceil_div(rows, kFWarpRows), kSampleStride);
+  const uint64_t sampled = ceil_div(ceil_div(rows, kFWarpRows), sample_stride(rows));
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(sampled, kFWarps), 148 * 8));
 }
 
@@ -854,6 +859,9 @@ void probe_launch(const PackArgs &a, const Side &sd, const SjSeg &ws, const void
 }  // namespace
 
 uint64_t sj_slices(uint64_t rows) { return ceil_div(rows, kFWarpRows); }
+uint64_t sj_sample_rows(uint64_t rows) {
+  return std::min(rows, ceil_div(ceil_div(rows, kFWarpRows), sample_stride(rows)) * kFWarpRows);
+}
 
 void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint32_t bbits,
                                  uint32_t hashed, unsigned long long *sample, cudaStream_t s,
@@ -868,19 +876,19 @@ void launch_sj_build_sample_cols(const PackArgs &a, bool s_is_b, void *bmS, uint
     if (before_sample) before_sample();
     if (L.rows)
       filter_sample_kernel<0><<<sample_grid(L.rows), kFThreads, 0, s>>>(
-          a, L, (const uint32_t *)bmS, bbits, hashed, kSampleStride, sample);
+          a, L, (const uint32_t *)bmS, bbits, hashed, sample_stride(L.rows), sample);
   } else if (mode == 2) {
     cfilter_build_kernel<2><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
     if (before_sample) before_sample();
     if (L.rows)
       cfilter_sample_kernel<2><<<sample_grid(L.rows), kFThreads, 0, s>>>(
-          a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
+          a, L, bbits, (const unsigned long long *)bmS, sample_stride(L.rows), sample);
   } else {
     cfilter_build_kernel<3><<<gs, kFThreads, 0, s>>>(a, S, bbits, (unsigned long long *)bmS);
     if (before_sample) before_sample();
     if (L.rows)
       cfilter_sample_kernel<3><<<sample_grid(L.rows), kFThreads, 0, s>>>(
-          a, L, bbits, (const unsigned long long *)bmS, kSampleStride, sample);
+          a, L, bbits, (const unsigned long long *)bmS, sample_stride(L.rows), sample);
   }
 }
 
@@ -989,9 +997,9 @@ void launch_sj_chain_sample(const PackArgs &a, bool side_b, const void *bm, uint
   if (sd.rows == 0) return;
   const auto *b = reinterpret_cast<const unsigned long long *>(bm);
   if (a.nkey == 2)
-    cfilter_sample_kernel<2><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, kSampleStride, sample);
+    cfilter_sample_kernel<2><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, sample_stride(sd.rows), sample);
   else
-    cfilter_sample_kernel<3><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, kSampleStride, sample);
+    cfilter_sample_kernel<3><<<sample_grid(sd.rows), kFThreads, 0, s>>>(a, sd, bbits, b, sample_stride(sd.rows), sample);
 }
 
 void launch_peer_or(unsigned long long *const *peers, int world, int rank, uint64_t words,
@@ -1014,7 +1022,7 @@ void launch_sj_sample_words(const SjSeg &L, uint32_t ib, uint64_t seed, uint32_t
                             const void *bm, unsigned long long *sample, cudaStream_t s) {
   if (L.rows == 0) return;
   wfilter_sample_kernel<<<sample_grid(L.rows), kFThreads, 0, s>>>(
-      L, ib, seed, bbits, reinterpret_cast<const unsigned long long *>(bm), kSampleStride, sample);
+      L, ib, seed, bbits, reinterpret_cast<const unsigned long long *>(bm), sample_stride(L.rows), sample);
 }
 
 }  // namespace mapsq

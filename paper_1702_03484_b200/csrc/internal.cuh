@@ -429,6 +429,8 @@ struct SjSeg {                                     // one side's packed words (a
   uint64_t rows;
 };
 uint64_t sj_slices(uint64_t rows);  // ceil(rows / 512)
+// rows the sampled probe reads of a side of `rows` rows (every 16th 512-row slice, at most ~4 M)
+uint64_t sj_sample_rows(uint64_t rows);
 // Stage layout: side A's slices first (slice s at stage[s * 512 ..], count cnt[s]), then side
 // B's from slice sj_slices(n1) on; stage needs (sj_slices(n1) + sj_slices(n2)) * 512 words.
 // Column round, phase 0: build bmS from the smaller side's key columns (side B if s_is_b) and
