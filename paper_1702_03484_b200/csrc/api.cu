@@ -421,16 +421,9 @@ void fill_empty_join(const mapsq_join_plan &pl, const mapsq_table *a, const maps
   set_join_bounds(pl, a, b, rs);
 }
 
-// pv: value-carrying words (pl.ib must then be kPvIb; at most one non-key column per side)
-PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b,
-                   bool pv = false) {
+PackArgs pack_args(const mapsq_join_plan &pl, const mapsq_table *a, const mapsq_table *b) {
   PackArgs pa;
   std::memset(&pa, 0, sizeof pa);
-  if (pv) {
-    pa.pv = 1;
-    pa.pv1 = pl.nrest1 ? a->col[pl.rest_col1[0]] : nullptr;
-    pa.pv2 = pl.nrest2 ? b->col[pl.rest_col2[0]] : nullptr;
-  }
   const bool hash = pl.path == MAPSQ_PATH_HASH;
   for (uint32_t c = 0; c < pl.nshared; c++) {
     if (!hash && !(pl.packed_mask >> c & 1u)) continue;
@@ -504,7 +497,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
                         uint64_t *nB_out, SjCarry carry[2], uint32_t ib_row) {
   const uint64_t n1 = pl.n1, n2 = pl.n2, n = n1 + n2;
   bool pv = carry[0].pv;
-  PackArgs pa = pack_args(pl, a, b, pv);
+  PackArgs pa = pack_args(pl, a, b);
   // value-carrying words come only from the column round's gathers: a filter that Maps every
   // row (composite packed keys, or a skipped filter) uses row-id words (measured: the Map that
   // loads the values too ran 0.27-0.33 vs 0.17 ms on C5 J1, more than the expansion saves)
@@ -512,7 +505,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     if (!pv) return;
     pv = false;
     pl.ib = ib_row;
-    pa = pack_args(pl, a, b, false);
+    pa = pack_args(pl, a, b);
   };
   const uint64_t bmw = std::max<uint64_t>(
       1, (1ull << std::max(kSemijoinBits, env_u32("MAPSQ_SJ_COLBITS", kSemijoinBits))) / 32);
@@ -785,7 +778,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
     nB = n2;
     CK(cudaMemsetAsync(hist, 0, kRadix * sizeof(uint32_t), s));
     if (colpath) {
-      const PackArgs pm = pack_args(pl, a, b, pv);
+      const PackArgs pm = pack_args(pl, a, b);
       KTimer kt(ctx, s, "pack_hist", 4ull * pl.nshared * n + 8ull * n);
       launch_pack_hist(pm, cur, nullptr, hist, s);
       CKL("pack_hist");
@@ -974,7 +967,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
     }
   } else {
     TRY(wait_stream_b(ctx, n2, s));
-    const PackArgs pa = pack_args(pl, &a, &b, pv);
+    const PackArgs pa = pack_args(pl, &a, &b);
     KTimer kt(ctx, s, "pack_hist", 4ull * (pl.nshared + (pv ? 1 : 0)) * n + (kv ? 12ull : 8ull) * n);
     launch_pack_hist(pa, cur, va, hist, s);
     CKL("pack_hist");

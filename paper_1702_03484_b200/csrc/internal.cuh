@@ -310,10 +310,6 @@ struct PackArgs {
   uint32_t kv;       // 1: write keys[] = key', vals[] = rowid; 0: words = key' << ib | rowid
   uint32_t kb;       // packed key bits
   uint32_t hash;     // 1 (PATH_HASH): key' = key_hash over the raw values of all nkey columns
-  // 1: value-carrying words (kPvIb; made by the semi-join filter's gathers): key' << 33 |
-  // label << 32 | the row's value of pv1 (Tp1) / pv2 (Tp2), the side's only non-key column
-  uint32_t pv;
-  const uint32_t *pv1, *pv2;
 };
 // Value-carrying words (filtered P64 joins with at most one non-key column per side and kb <= 31):
 // the low 33 bits hold (label, value) instead of the row id, so ReduceDuplicate reads the non-key
