@@ -271,8 +271,11 @@ mapsq_status mapsq_query_indexed(mapsq_ctx *ctx, const mapsq_index *idx,
  * context's pinned result arena exactly as mapsq_query_host does (same output contract, same
  * result rows as mapsq_query_indexed over the device index).  *h2d_bytes (optional) receives the
  * bytes copied host -> device.  The copies run on a context-owned copy stream in the order the
- * query first uses the ranges, and `stream` waits for each range only where it first reads it
- * (later ranges stream in while the first joins run).  Synchronous. */
+ * query first uses the ranges, in chunks of 32 M rows (compressed chunks are expanded on a second
+ * context-owned stream), and `stream` waits for each range only where it first reads it (later
+ * ranges stream in while the first joins run); a join whose Tp2 is one range waits chunk by chunk
+ * where it reads it in row order (the semi-join filter's probe of the larger side) and for the
+ * whole range before anything else reads it.  Synchronous. */
 typedef struct mapsq_host_index mapsq_host_index;
 mapsq_status mapsq_index_to_host(mapsq_ctx *ctx, const mapsq_index *idx, mapsq_host_index **out,
                                  void *stream);
