@@ -20,6 +20,12 @@
 namespace mapsq {
 namespace {
 
+#ifndef MAPSQ_RADIX_ITEMS
+#define MAPSQ_RADIX_ITEMS 24
+#endif
+#ifndef MAPSQ_RADIX_MINB
+#define MAPSQ_RADIX_MINB 3
+#endif
 constexpr int kWarps = kSortThreads / 32;
 constexpr int kLookWin = 8;
 constexpr int kHistThreads = 256;
@@ -423,11 +429,11 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     // shared-memory atomicOr with a warp-uniform shortcut (tools/radix_ablate.cu: a C4-shaped
     // 4e8-word Zipf sort 9.70 ms vs 10.72 with match.any / 10.57 with ballots at 8192-key tiles;
     // 6144-key tiles at 3 CTAs/SM then 8.89 ms, C5's join words -7%).
-    constexpr int kItems = 24;
+    constexpr int kItems = MAPSQ_RADIX_ITEMS;  // (ablation knobs: -DMAPSQ_RADIX_ITEMS / _MINB)
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = (gap && n0 < n) ? radix_pass_kernel<false, kItems, 4, 3, true, 3, true>
-                                : radix_pass_kernel<false, kItems, 4, 3, true, 3, false>;
+    auto kern = (gap && n0 < n) ? radix_pass_kernel<false, kItems, 4, MAPSQ_RADIX_MINB, true, 3, true>
+                                : radix_pass_kernel<false, kItems, 4, MAPSQ_RADIX_MINB, true, 3, false>;
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,
