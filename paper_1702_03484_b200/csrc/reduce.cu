@@ -266,9 +266,11 @@ __device__ __forceinline__ uint64_t group_of(const uint64_t *off, uint64_t lo, u
 // t0 + (c * kEThreads + t) * kERows, so a warp's chunks are contiguous): it locates its group in
 // shared memory, then computes the 8 (LEFT, RIGHT) positions, issues all word loads, then all
 // column gathers, then 16 B streaming stores — so the latencies of one thread's rows overlap.
-template <int kERows, int kEChunks>
+// FULL: every row of the tile exists (all tiles but the last; launched separately), so the
+// per-row bounds checks and partial-chunk paths compile away.
+template <int kERows, int kEChunks, bool FULL>
 __global__ void __launch_bounds__(kEThreads, 5)
-expand_kernel(const ExpandArgs a) {
+expand_kernel(const ExpandArgs a, uint64_t tile0, uint64_t ntiles) {
   static_assert(kERows * kEChunks == kERowsPerThread && kERows % 4 == 0, "tile shape");
   __shared__ const uint32_t *s_src[MAPSQ_MAX_COLS];
   __shared__ uint32_t *s_dst[MAPSQ_MAX_COLS];
@@ -283,12 +285,13 @@ expand_kernel(const ExpandArgs a) {
     s_src[tid] = c < a.nkey ? nullptr
                : (c < a.nkey + a.nrest1 ? a.rest1[c - a.nkey] : a.rest2[c - a.nkey - a.nrest1]);
   }
-  const uint64_t t0 = (uint64_t)blockIdx.x * kETile;
+  const uint64_t tile = tile0 + blockIdx.x;
+  const uint64_t t0 = tile * kETile;
   // the tile's group range from the precomputed first group of every tile (tile_groups_kernel):
   // the groups of rows [t0, t0 + kETile) lie in [first(t), first(t + 1)]
   if (tid == 0) {
-    s_g[0] = a.tile_g0[blockIdx.x];
-    s_g[1] = blockIdx.x + 1 < gridDim.x ? a.tile_g0[blockIdx.x + 1] : a.ngroups - 1;
+    s_g[0] = a.tile_g0[tile];
+    s_g[1] = tile + 1 < ntiles ? a.tile_g0[tile + 1] : a.ngroups - 1;
   }
   __syncthreads();
   const uint64_t g0 = s_g[0], g1 = s_g[1];
@@ -314,7 +317,7 @@ expand_kernel(const ExpandArgs a) {
   for (int c = 0; c < kEChunks; c++) {
     const uint64_t r0 = t0 + ((uint64_t)c * kEThreads + tid) * kERows;
     nrow[c] = 0;
-    if (r0 >= a.m) continue;
+    if (!FULL && r0 >= a.m) continue;
     // locate r0's group
     uint64_t gl, gend;
     uint32_t start, split, end;
@@ -346,10 +349,10 @@ expand_kernel(const ExpandArgs a) {
       ri = (uint32_t)(local - (uint64_t)li * nR);
     }
     uint32_t left = (uint32_t)min(gend - r0, (uint64_t)0xffffffffu);  // rows left in the group
-    const uint32_t nv = (uint32_t)min(a.m - r0, (uint64_t)kERows);
+    const uint32_t nv = FULL ? kERows : (uint32_t)min(a.m - r0, (uint64_t)kERows);
 #pragma unroll
     for (int j = 0; j < kERows; j++) {
-      if ((uint32_t)j >= nv) break;
+      if (!FULL && (uint32_t)j >= nv) break;
       if (left == 0) {  // next group (groups are never empty)
         gl++;
         const uint64_t gb = gend;
@@ -380,7 +383,7 @@ expand_kernel(const ExpandArgs a) {
   uint32_t lidx[R], ridx[R];
 #pragma unroll
   for (int q = 0; q < R; q++) {
-    const bool v = (q % kERows) < nrow[q / kERows];
+    const bool v = FULL || (q % kERows) < nrow[q / kERows];
     if (a.words) {
       const uint64_t lw = v ? __ldg(a.words + lpos[q]) : 0ull;
       const uint64_t rw = v ? __ldg(a.words + rpos[q]) : 0ull;
@@ -408,17 +411,17 @@ expand_kernel(const ExpandArgs a) {
       } else {
 #pragma unroll
         for (int q = 0; q < R; q++) {
-          const bool v = (q % kERows) < nrow[q / kERows];
+          const bool v = FULL || (q % kERows) < nrow[q / kERows];
           val[q] = v ? __ldg(src + (left ? lidx[q] : ridx[q])) : 0u;
         }
       }
     }
 #pragma unroll
     for (int c = 0; c < kEChunks; c++) {
-      if (nrow[c] == 0) continue;
+      if (!FULL && nrow[c] == 0) continue;
       const uint64_t r0 = t0 + ((uint64_t)c * kEThreads + tid) * kERows;
       uint32_t *dst = s_dst[col] + r0;
-      if (nrow[c] == kERows) {
+      if (FULL || nrow[c] == kERows) {
 #pragma unroll
         for (int v4 = 0; v4 < kERows; v4 += 4)
           st_cs_v4(dst + v4, make_uint4(val[c * kERows + v4], val[c * kERows + v4 + 1],
@@ -640,10 +643,14 @@ void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   // long runs of one group (C3's star: ~2e4 rows per group) favour 2 chunks of 4 rows per
   // thread; short groups (C5's first join: ~20 rows) one chunk of 8 rows (C3 2.50 vs 2.72 ms,
   // C5 J1 0.88 vs 0.81 ms)
-  if (a.m >= 256 * a.ngroups)
-    expand_kernel<4, 2><<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
-  else
-    expand_kernel<8, 1><<<(unsigned)nblocks, kEThreads, 0, s>>>(a);
+  const uint64_t nfull = a.m / kETile;  // tiles with every row (the last one may be partial)
+  if (a.m >= 256 * a.ngroups) {
+    if (nfull) expand_kernel<4, 2, true><<<(unsigned)nfull, kEThreads, 0, s>>>(a, 0, nblocks);
+    if (nblocks > nfull) expand_kernel<4, 2, false><<<1, kEThreads, 0, s>>>(a, nfull, nblocks);
+  } else {
+    if (nfull) expand_kernel<8, 1, true><<<(unsigned)nfull, kEThreads, 0, s>>>(a, 0, nblocks);
+    if (nblocks > nfull) expand_kernel<8, 1, false><<<1, kEThreads, 0, s>>>(a, nfull, nblocks);
+  }
 }
 
 }  // namespace mapsq
