@@ -133,6 +133,24 @@ def test_indexed_table1_and_projection(ctx):
     assert_same(one, oracle.scan(*T.T, P1))
 
 
+@pytest.mark.parametrize("cfg", ["C1", "C5"])
+def test_prepared_query_equals_query(ctx, cfg):
+    """Context.prepare marshals a query's C arguments once; every call is the same library call
+    (index store and plain triple table, with and without a projection)."""
+    s, p, o, _ = datagen.lubm(2)
+    trip = (dev(s), dev(p), dev(o))
+    idx = ctx.index_build(trip)
+    pats = config_query(cfg)
+    for src in (idx, trip):
+        for proj in (None, [0]):
+            want = ctx.query(src, pats, proj).to_numpy()
+            q = ctx.prepare(src, pats, proj)
+            for _ in range(3):
+                r = q()
+                assert np.array_equal(r.to_numpy(), want)
+                r.release()
+
+
 def test_index_empty_table(ctx):
     z = torch.empty(0, dtype=torch.int32, device="cuda")
     idx = ctx.index_build((z, z, z))
