@@ -547,7 +547,7 @@ mapsq_status filter_map(mapsq_ctx *ctx, mapsq_join_plan &pl, const mapsq_table *
   auto scan_gather = [&](int side, uint64_t sl0, uint64_t nsl, uint64_t *out,
                          const SjCarry &cr = SjCarry{}) -> mapsq_status {
     {
-      KTimer kt(ctx, s, "filter_scan", 12ull * nsl, 3);
+      KTimer kt(ctx, s, "filter_scan", 12ull * nsl);
       launch_exclusive_scan_u32(cnt + sl0, off + sl0, nsl, ftmp, fsc + side, s);
       CKL("filter_scan");
     }
@@ -1003,7 +1003,7 @@ mapsq_status join_impl(mapsq_ctx *ctx, const mapsq_table *tp1_in, const mapsq_ta
   // RESIDUAL and HASH: the nL * nR pairs of a key' group are candidates, verified on the shared
   // columns not (exactly) in key'
   {
-    KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
+    KTimer kt(ctx, s, "scan_counts", cap * 16ull);
     launch_exclusive_scan_u64_dev(gc, go, scal, cap, tmp, scal + 1, s);
     CKL("scan_counts");
   }
@@ -1216,7 +1216,7 @@ mapsq_status scan_impl(mapsq_ctx *ctx, const mapsq_triples *T, const mapsq_patte
     CKL("scan_count");
   }
   {
-    KTimer kt(ctx, s, "scan_tiles", 12ull * k * ntiles, 3);
+    KTimer kt(ctx, s, "scan_tiles", 12ull * k * ntiles);
     launch_exclusive_scan_u32(tcnt, toff, k * ntiles, tmp, toff + k * ntiles, s);
     CKL("scan_tiles");
   }
@@ -2347,7 +2347,7 @@ MAPSQ_API mapsq_status mapsq_reduce_groups(mapsq_ctx *ctx, const uint64_t *words
     CKL("find_groups");
   }
   {
-    KTimer kt(ctx, s, "scan_counts", cap * 16ull, 3);
+    KTimer kt(ctx, s, "scan_counts", cap * 16ull);
     launch_exclusive_scan_u64_dev(gc, group_off, scal, cap, tmp, scal + 1, s);
     CKL("scan_counts");
   }
@@ -2461,7 +2461,7 @@ mapsq_status partition_plan_impl(mapsq_ctx *ctx, const mapsq_table *in, const in
     launch_partition_hist(pa, th, st->ntiles, s);
   }
   {
-    KTimer kt(ctx, s, "scan_tiles", 12ull * st->ntiles * nparts, 3);
+    KTimer kt(ctx, s, "scan_tiles", 12ull * st->ntiles * nparts);
     launch_exclusive_scan_u32(th, st->tile_off, st->ntiles * nparts, tmp,
                               st->tile_off + st->ntiles * nparts, s);
   }

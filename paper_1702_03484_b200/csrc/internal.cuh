@@ -285,7 +285,7 @@ void launch_scan_write(const mapsq_triples &T, const ScanArgs &a, const uint32_t
                        uint64_t mask_words, const uint64_t *tile_off, uint64_t ntiles,
                        const ScanOut &out, uint32_t *bmin, uint32_t *bmax, cudaStream_t s);
 
-// exclusive scan of u32 / u64 counts into u64 offsets (3-phase reduce-then-scan);
+// exclusive scan of u32 / u64 counts into u64 offsets (one single-pass look-back kernel);
 // writes the total to *total_dev.  `tmp` needs scan_tmp_words(n) u64.
 uint64_t scan_tmp_words(uint64_t n);
 int launch_exclusive_scan_u32(const uint32_t *in, uint64_t *out, uint64_t n, uint64_t *tmp,

@@ -221,25 +221,6 @@ constexpr int kScanChunkThreads = 256;
 constexpr int kScanChunkItems = 16;
 constexpr uint64_t kChunk = kScanChunkThreads * kScanChunkItems;
 
-template <typename T>
-__device__ __forceinline__ uint64_t block_reduce_chunk(const T *in, uint64_t n, uint64_t base) {
-  __shared__ uint64_t s_red[kScanChunkThreads / 32];
-  uint64_t acc = 0;
-#pragma unroll
-  for (int it = 0; it < kScanChunkItems; it++) {
-    const uint64_t i = base + (uint64_t)it * kScanChunkThreads + threadIdx.x;
-    if (i < n) acc += (uint64_t)in[i];
-  }
-  for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  uint64_t t = 0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < kScanChunkThreads / 32; w++) t += s_red[w];
-  __syncthreads();
-  return t;  // valid in thread 0
-}
-
 // exclusive block scan of one value per thread; returns exclusive prefix, *total = block sum
 __device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t *total) {
   __shared__ uint64_t s_w[kScanChunkThreads / 32];
@@ -261,43 +242,62 @@ __device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t *total) {
   return wpre + x - v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kScanChunkThreads)
-scan_reduce_kernel(const T *__restrict__ in, const uint64_t *n_dev, uint64_t n_host,
-                   uint64_t *__restrict__ partial) {
-  const uint64_t n = n_dev ? *n_dev : n_host;
-  const uint64_t nchunks = ceil_div(n, kChunk);
-  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    uint64_t t = block_reduce_chunk(in, n, c * kChunk);
-    if (threadIdx.x == 0) partial[c] = t;
+// Single-pass exclusive scan: CTAs claim chunks in order (atomic counter) and resolve their
+// chunk's prefix by a decoupled look-back over per-chunk 64-bit status words (flags in the top two
+// bits, 62-bit sums), so one launch replaces reduce / partials / down.  The last chunk writes the
+// total.  status[0 .. nchunks) and the counter are zero on entry.
+__device__ __forceinline__ uint64_t warp_lookback64(uint64_t *status, uint64_t tile, uint64_t agg) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_u64(status, kFlagInc | agg);
+    return 0;
   }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | agg);
+  uint64_t excl = 0;
+  int64_t t0 = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = t0 - (int64_t)lane;
+    const uint64_t v = t >= 0 ? ld_relaxed_u64(status + t) : kFlagInc;  // virtual INC(0)
+    const uint64_t flag = v & ~kValMask;
+    const uint32_t inc = __ballot_sync(0xffffffffu, flag == kFlagInc);
+    const uint32_t zero = __ballot_sync(0xffffffffu, flag == 0);
+    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+    const uint32_t need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+    if (zero & need) {
+      __nanosleep(32);
+      continue;
+    }
+    uint64_t val = ((int)lane <= first_inc) ? (v & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    excl += val;
+    if (first_inc < 32) break;
+    t0 -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | (excl + agg));
+  return excl;
 }
 
-__global__ void __launch_bounds__(kScanChunkThreads)
-scan_partials_kernel(uint64_t *__restrict__ partial, const uint64_t *n_dev, uint64_t n_host,
-                     uint64_t *total_dev) {
-  const uint64_t n = n_dev ? *n_dev : n_host;
-  const uint64_t nchunks = ceil_div(n, kChunk);
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < nchunks; base += kScanChunkThreads) {
-    const uint64_t i = base + threadIdx.x;
-    const uint64_t v = i < nchunks ? partial[i] : 0;
-    uint64_t tot;
-    const uint64_t ex = block_exscan(v, &tot);
-    if (i < nchunks) partial[i] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0 && total_dev) *total_dev = carry;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kScanChunkThreads)
-scan_down_kernel(const T *__restrict__ in, uint64_t *__restrict__ out, const uint64_t *n_dev,
-                 uint64_t n_host, const uint64_t *__restrict__ partial) {
+scan_onepass_kernel(const T *__restrict__ in, uint64_t *__restrict__ out, const uint64_t *n_dev,
+                    uint64_t n_host, uint64_t *__restrict__ status, uint32_t *__restrict__ ctr,
+                    uint64_t *total_dev) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_excl;
   const uint64_t n = n_dev ? *n_dev : n_host;
   const uint64_t nchunks = ceil_div(n, kChunk);
-  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    // thread t scans items [base + t*ITEMS, +ITEMS) of the chunk (contiguous per thread)
+  const uint32_t warp = threadIdx.x >> 5;
+  while (true) {
+    __syncthreads();  // (s_tile / s_excl reuse)
+    if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const uint64_t c = s_tile;
+    if (c >= nchunks) {
+      if (c == 0 && threadIdx.x == 0 && total_dev) *total_dev = 0;  // (n == 0)
+      return;
+    }
+    // thread t scans items [base + t * ITEMS, + ITEMS) of the chunk (contiguous per thread)
     const uint64_t base = c * kChunk + (uint64_t)threadIdx.x * kScanChunkItems;
     uint64_t v[kScanChunkItems];
     uint64_t sum = 0;
@@ -308,7 +308,16 @@ scan_down_kernel(const T *__restrict__ in, uint64_t *__restrict__ out, const uin
       sum += v[it];
     }
     uint64_t tot;
-    uint64_t run = partial[c] + block_exscan(sum, &tot);
+    const uint64_t ex = block_exscan(sum, &tot);
+    if (warp == 0) {
+      const uint64_t excl = warp_lookback64(status, c, tot);
+      if (threadIdx.x == 0) {
+        s_excl = excl;
+        if (c + 1 == nchunks && total_dev) *total_dev = excl + tot;
+      }
+    }
+    __syncthreads();
+    uint64_t run = s_excl + ex;
 #pragma unroll
     for (int it = 0; it < kScanChunkItems; it++) {
       const uint64_t i = base + it;
@@ -371,33 +380,34 @@ static int scan_grid(uint64_t n) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(c, 148 * 8));
 }
 
+// (tmp: scan_tmp_words(n) words — the per-chunk status words, then the chunk counter)
 int launch_exclusive_scan_u32(const uint32_t *in, uint64_t *out, uint64_t n, uint64_t *tmp,
                               uint64_t *total_dev, cudaStream_t s) {
-  const int g = scan_grid(n);
-  scan_reduce_kernel<uint32_t><<<g, kScanChunkThreads, 0, s>>>(in, nullptr, n, tmp);
-  scan_partials_kernel<<<1, kScanChunkThreads, 0, s>>>(tmp, nullptr, n, total_dev);
-  scan_down_kernel<uint32_t><<<g, kScanChunkThreads, 0, s>>>(in, out, nullptr, n, tmp);
-  return 3;
+  const uint64_t nc = ceil_div(n, kChunk);
+  cudaMemsetAsync(tmp, 0, (nc + 1) * sizeof(uint64_t), s);
+  scan_onepass_kernel<uint32_t><<<scan_grid(n), kScanChunkThreads, 0, s>>>(
+      in, out, nullptr, n, tmp, reinterpret_cast<uint32_t *>(tmp + nc), total_dev);
+  return 1;
 }
 
 int launch_exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp,
                               uint64_t *total_dev, cudaStream_t s) {
-  const int g = scan_grid(n);
-  scan_reduce_kernel<uint64_t><<<g, kScanChunkThreads, 0, s>>>(in, nullptr, n, tmp);
-  scan_partials_kernel<<<1, kScanChunkThreads, 0, s>>>(tmp, nullptr, n, total_dev);
-  scan_down_kernel<uint64_t><<<g, kScanChunkThreads, 0, s>>>(in, out, nullptr, n, tmp);
-  return 3;
+  const uint64_t nc = ceil_div(n, kChunk);
+  cudaMemsetAsync(tmp, 0, (nc + 1) * sizeof(uint64_t), s);
+  scan_onepass_kernel<uint64_t><<<scan_grid(n), kScanChunkThreads, 0, s>>>(
+      in, out, nullptr, n, tmp, reinterpret_cast<uint32_t *>(tmp + nc), total_dev);
+  return 1;
 }
 
-// Variant whose element count lives on the device (grid sized for the capacity `cap`).
+// Variant whose element count lives on the device (grid and status sized for the capacity `cap`).
 int launch_exclusive_scan_u64_dev(const uint64_t *in, uint64_t *out, const uint64_t *n_dev,
                                   uint64_t cap, uint64_t *tmp, uint64_t *total_dev,
                                   cudaStream_t s) {
-  const int g = scan_grid(cap);
-  scan_reduce_kernel<uint64_t><<<g, kScanChunkThreads, 0, s>>>(in, n_dev, 0, tmp);
-  scan_partials_kernel<<<1, kScanChunkThreads, 0, s>>>(tmp, n_dev, 0, total_dev);
-  scan_down_kernel<uint64_t><<<g, kScanChunkThreads, 0, s>>>(in, out, n_dev, 0, tmp);
-  return 3;
+  const uint64_t nc = ceil_div(cap, kChunk);
+  cudaMemsetAsync(tmp, 0, (nc + 1) * sizeof(uint64_t), s);
+  scan_onepass_kernel<uint64_t><<<scan_grid(cap), kScanChunkThreads, 0, s>>>(
+      in, out, n_dev, 0, tmp, reinterpret_cast<uint32_t *>(tmp + nc), total_dev);
+  return 1;
 }
 
 void launch_minmax(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint32_t *bounds,
