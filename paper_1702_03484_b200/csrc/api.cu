@@ -2055,7 +2055,13 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
     }
     // MAPSQ_DEBUG: the copy stream's range completion times and the joins' / readback's end,
     // relative to the query's start (timing events; stderr)
-    std::vector<cudaEvent_t> dbg;
+    struct DbgEvents {  // (destroyed on every exit path)
+      std::vector<cudaEvent_t> v;
+      ~DbgEvents() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } dbgev;
+    std::vector<cudaEvent_t> &dbg = dbgev.v;
     auto dbg_mark = [&](cudaStream_t st) {
       if (!debug_on()) return;
       cudaEvent_t e;
@@ -2230,7 +2236,6 @@ mapsq_status query_host_indexed_impl(mapsq_ctx *ctx, const mapsq_host_index *h,
                 std::to_string(ms);
       }
       std::fprintf(stderr, "%s\n", line.c_str());
-      for (cudaEvent_t e : dbg) cudaEventDestroy(e);
     }
   }
   if (h2d_bytes) *h2d_bytes = bytes;
