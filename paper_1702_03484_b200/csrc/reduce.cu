@@ -225,6 +225,27 @@ find_groups_kernel(const WordView W, uint64_t n64, GroupOut g, uint64_t *__restr
   }
 }
 
+// Random 4 B column gathers (verification): MAPSQ_GATHER_HINT 1 = ld.global.nc.L2::64B (the
+// L2 fetches 64 B on a miss instead of 128: C5 J2's verification 2.81 -> 1.52 GB of DRAM reads,
+// 0.57 -> 0.54 ms — it is bound by the gathers' latency more than by their bytes), 2 = also no
+// L1 allocation, 0 = plain read-only loads (ablation knob)
+#ifndef MAPSQ_GATHER_HINT
+#define MAPSQ_GATHER_HINT 1
+#endif
+__device__ __forceinline__ uint32_t ld_rnd(const uint32_t *p) {
+#if MAPSQ_GATHER_HINT == 1
+  uint32_t v;
+  asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#elif MAPSQ_GATHER_HINT == 2
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // ------------------------------------------------------------------------------ expand (K6)
 constexpr int kEThreads = 256;
 constexpr int kERowsPerThread = 8;           // rows per thread = chunks x rows per chunk
@@ -535,8 +556,8 @@ verify_emit_kernel(const ResidualArgs a, const uint64_t *__restrict__ coff,
       uint32_t x[kVPer], y[kVPer];
 #pragma unroll
       for (int j = 0; j < kVPer; j++) {
-        x[j] = (match >> j & 1u) ? __ldg(a.res1[c] + lidx[j]) : 0u;
-        y[j] = (match >> j & 1u) ? __ldg(a.res2[c] + ridx[j]) : 0u;
+        x[j] = (match >> j & 1u) ? ld_rnd(a.res1[c] + lidx[j]) : 0u;
+        y[j] = (match >> j & 1u) ? ld_rnd(a.res2[c] + ridx[j]) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < kVPer; j++)
@@ -580,7 +601,7 @@ verify_emit_kernel(const ResidualArgs a, const uint64_t *__restrict__ coff,
     uint32_t v[kVPer];
 #pragma unroll
     for (int j = 0; j < kVPer; j++)
-      v[j] = (match >> j & 1u) ? __ldg(src + (right ? ridx[j] : lidx[j])) : 0u;
+      v[j] = (match >> j & 1u) ? ld_rnd(src + (right ? ridx[j] : lidx[j])) : 0u;
     uint32_t *dst = a.out[c] + pos0;
     uint32_t q = 0;
 #pragma unroll
