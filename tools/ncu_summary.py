@@ -21,6 +21,8 @@ def get(r, name):
 
 
 traffic = {}
+runs = {}  # kernel -> number of runs of consecutive launches (one library timer invocation may
+prev = None  # launch a kernel twice in a row, e.g. the expansion's full tiles + its last tile)
 print("| kernel | grid | regs | time ms | DRAM read GB | DRAM write GB | DRAM GB/s | DRAM % peak | SM % | issued inst |")
 print("|---|---|---|---|---|---|---|---|---|---|")
 for ri, r in enumerate(rows[2:]):
@@ -40,6 +42,9 @@ for ri, r in enumerate(rows[2:]):
           f"{(rd+wr)/t/1e9:.0f} | {dpct} | {smpct} | {inst} |")
     if ri >= SKIP:
         traffic.setdefault(short, []).append(rd + wr)
+        if short != prev:
+            runs[short] = runs.get(short, 0) + 1
+    prev = short
 # DRAM bytes per invocation of each library timer (bench.py's kernel names): a timer may cover
 # several kernels; its invocations are counted by its anchor kernel
 TIMERS = {  # timer: (member kernels, invocations from the launch counts)
@@ -47,18 +52,19 @@ TIMERS = {  # timer: (member kernels, invocations from the launch counts)
     "filter_build": (["filter_build", "filter_sample", "cfilter_build", "cfilter_sample",
                       "wfilter_build", "wfilter_sample"],
                      lambda c: c("filter_build") + c("cfilter_build") + c("wfilter_build")),
-    "filter_probe": (["sj_probe_stage"], lambda c: c("sj_probe_stage")),
+    "filter_probe": (["sj_probe_stage", "sj_probe_stage16"],
+                     lambda c: c("sj_probe_stage") + c("sj_probe_stage16")),
     "filter_gather": (["sj_gather"], lambda c: c("sj_gather")),
     "filter_set": (["sj_set_words"], lambda c: c("sj_set_words")),
     "pack_hist": (["pack_hist"], lambda c: c("pack_hist")),
     "find_groups": (["find_groups"], lambda c: c("find_groups")),
-    "expand": (["expand"], lambda c: c("expand")),
+    "expand": (["expand"], lambda c: c("expand", runs=True)),
     "verify_emit": (["verify_emit"], lambda c: c("verify_emit")),
     "scan_write": (["scan_write"], lambda c: c("scan_write")),
 }
 per_timer = {}
 for timer, (members, inv_of) in TIMERS.items():
-    inv = inv_of(lambda k: len(traffic.get(k, [])))
+    inv = inv_of(lambda k, runs_=runs, **kw: runs_.get(k, 0) if kw.get("runs") else len(traffic.get(k, [])))
     if inv:
         per_timer[timer] = sum(sum(traffic.get(m, [])) for m in members) / inv
 if len(sys.argv) > 2:
