@@ -14,6 +14,8 @@
 // consecutive output rows, finds its group by a binary search bracketed per CTA, and writes
 // (key columns decoded from the word, Tp1 non-shared, Tp2 non-shared) in (key, left rowid,
 // right rowid) order with 16 B streaming stores.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace mapsq {
@@ -665,7 +667,15 @@ void launch_expand(const ExpandArgs &a, cudaStream_t s) {
   // thread; short groups (C5's first join: ~20 rows) one chunk of 8 rows (C3 2.50 vs 2.72 ms,
   // C5 J1 0.88 vs 0.81 ms)
   const uint64_t nfull = a.m / kETile;  // tiles with every row (the last one may be partial)
-  if (a.m >= 256 * a.ngroups) {
+  static const uint32_t shape = [] {  // (ablation knob MAPSQ_EXPAND_SHAPE: 1 = 8x1, 2 = 4x2)
+    const char *e = std::getenv("MAPSQ_EXPAND_SHAPE");
+    return (e && *e) ? (uint32_t)std::strtoul(e, nullptr, 10) : 0u;
+  }();
+  // (no gathers — value-carrying words — also favour 4-row chunks: C4 0.80 -> 0.72 ms)
+  bool gathers = false;
+  for (uint32_t c = 0; c < a.nrest1; c++) gathers |= a.rest1[c] != nullptr;
+  for (uint32_t c = 0; c < a.nrest2; c++) gathers |= a.rest2[c] != nullptr;
+  if (shape == 2 || (shape == 0 && (a.m >= 256 * a.ngroups || !gathers))) {
     if (nfull) expand_kernel<4, 2, true><<<(unsigned)nfull, kEThreads, 0, s>>>(a, 0, nblocks);
     if (nblocks > nfull) expand_kernel<4, 2, false><<<1, kEThreads, 0, s>>>(a, nfull, nblocks);
   } else {
