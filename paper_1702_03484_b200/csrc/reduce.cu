@@ -463,15 +463,18 @@ expand_kernel(const ExpandArgs a, uint64_t tile0, uint64_t ntiles) {
 // them), so a key' group's (LEFT, RIGHT) pairs are CANDIDATES: a pair belongs to RS iff the rows
 // also agree on every residual shared column (reading R19).  "GPU's SIMD architectures contribute
 // to accelerate cartesian product in parallel": the verification is candidate-parallel
-// like the expansion — a CTA owns 2048 consecutive candidates (offsets = exclusive scan of
-// nL * nR), each thread 8 consecutive ones, so a hot key' group is spread over many CTAs.  Each
+// like the expansion — a CTA owns 1024 consecutive candidates (offsets = exclusive scan of
+// nL * nR), each thread 4 consecutive ones (C5 J2: 0.52 ms vs 0.57 with 8, 0.56 with 16), so a hot key' group is spread over many CTAs.  Each
 // thread compares its candidates' residual columns, the CTA counts the matches, and (WRITE)
 // tiles claimed in order resolve their output offset by decoupled look-back and write the matched
 // pairs in (key', Tp1 row, Tp2 row) order — one pass, the output gathered only for matches.
 // WRITE = false only counts the matches (for joins whose candidate count is too large to size
 // the output by).
 constexpr int kVThreads = 256;
-constexpr int kVPer = 8;
+#ifndef MAPSQ_V_PER
+#define MAPSQ_V_PER 4
+#endif
+constexpr int kVPer = MAPSQ_V_PER;  // (ablation knob -DMAPSQ_V_PER)
 constexpr uint64_t kVTile = (uint64_t)kVThreads * kVPer;
 
 template <bool WRITE>
