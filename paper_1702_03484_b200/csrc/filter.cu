@@ -35,7 +35,10 @@ constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
 constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice,
 constexpr uint64_t kSampleSlices = 8192;       // and at most ~8192 slices (4 M rows)
-constexpr int kGSlices = 8;                    // slices per warp iteration of the gather
+#ifndef MAPSQ_G_SLICES
+#define MAPSQ_G_SLICES 8
+#endif
+constexpr int kGSlices = MAPSQ_G_SLICES;       // slices per warp iteration of the gather
 constexpr int kGRows = MAPSQ_G_ROWS;           // rows per lane in flight in the gather
 
 // MODE 0: one packed key column and kb <= 32 (key' = v - lo in 32-bit arithmetic); 1: generic

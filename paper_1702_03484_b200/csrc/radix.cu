@@ -26,6 +26,9 @@ namespace {
 #ifndef MAPSQ_RADIX_MINB
 #define MAPSQ_RADIX_MINB 3
 #endif
+#ifndef MAPSQ_RADIX_WIN
+#define MAPSQ_RADIX_WIN 4  // look-back window of the P64 digit pass (predecessors read at once)
+#endif
 constexpr int kWarps = kSortThreads / 32;
 constexpr int kLookWin = 8;
 constexpr int kHistThreads = 256;
@@ -432,8 +435,9 @@ void launch_radix_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
     constexpr int kItems = MAPSQ_RADIX_ITEMS;  // (ablation knobs: -DMAPSQ_RADIX_ITEMS / _MINB)
     const uint64_t ntiles = ceil_div(n, (uint64_t)kSortThreads * kItems);
     const size_t smem = (size_t)kSortThreads * kItems * sizeof(uint64_t);
-    auto kern = (gap && n0 < n) ? radix_pass_kernel<false, kItems, 4, MAPSQ_RADIX_MINB, true, 3, true>
-                                : radix_pass_kernel<false, kItems, 4, MAPSQ_RADIX_MINB, true, 3, false>;
+    auto kern = (gap && n0 < n)
+                    ? radix_pass_kernel<false, kItems, MAPSQ_RADIX_WIN, MAPSQ_RADIX_MINB, true, 3, true>
+                    : radix_pass_kernel<false, kItems, MAPSQ_RADIX_WIN, MAPSQ_RADIX_MINB, true, 3, false>;
     set_smem_limit((const void *)kern, smem);
     kern<<<(unsigned)ntiles, kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, bits,
                                                       hist_pass, status, tile_counter, hist_next,
