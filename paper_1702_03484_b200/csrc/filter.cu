@@ -35,6 +35,9 @@ constexpr int kFWarpRows = 32 * kFItems;       // 512-row warp slice
 constexpr int kFCopies = 4;                    // private digit-histogram copies
 constexpr int kSampleStride = 16;              // the sampled probe reads every 16th slice,
 constexpr uint64_t kSampleSlices = 8192;       // and at most ~8192 slices (4 M rows)
+#ifndef MAPSQ_PROBE_MINB
+#define MAPSQ_PROBE_MINB 3  // CTAs per SM of the 64-bit-key probe (ablation knob)
+#endif
 #ifndef MAPSQ_G_SLICES
 #define MAPSQ_G_SLICES 8
 #endif
@@ -462,7 +465,7 @@ __device__ __forceinline__ void probe_slot(uint64_t key, uint32_t bbits, uint32_
 }
 
 template <int KM, int BM, bool SET>
-__global__ void __launch_bounds__(kFThreads, 3)
+__global__ void __launch_bounds__(kFThreads, MAPSQ_PROBE_MINB)
 sj_probe_stage_kernel(const PackArgs a, const Side sd, const SjSeg ws, const void *__restrict__ bm,
                       uint32_t bbits, uint32_t hashed, uint64_t seed,
                       uint32_t *__restrict__ bm_set, uint64_t *__restrict__ stage,
